@@ -1,0 +1,191 @@
+/*
+ * tlgpu.h — C ABI of the B200 two-level heat-solve library (libtlgpu.so).
+ *
+ * The reference (lpbfsim, pure Python) has no FFI; its seams are Python
+ * functions.  Each entry point below names the reference function whose work
+ * it replaces; the Python host layer (paper_2110_12932_b200/) keeps the
+ * reference signatures and calls these through ctypes.
+ *
+ * Conventions
+ *   - Plain C types only; all arrays are contiguous fp64 in the reference node
+ *     order  id = i + (nx+1)*(j + (ny+1)*k)  (lpbfsim/mesh.py:406-409).
+ *   - Host pointers are borrowed for the duration of the call.
+ *   - Every function returns TL_OK (0) or a negative TL_E* code; the message is
+ *     available from tl_last_error() (thread-local).  No C++ exception crosses
+ *     the ABI.  Solver non-convergence is NOT an error code: it is reported
+ *     per solve in tl_solve_info.status, and the Python layer raises the
+ *     reference's NonConvergence / SolverError from it.
+ *   - One CUDA stream per tl_run; handles are not thread-safe, distinct handles
+ *     may be used concurrently from different threads / devices.
+ */
+#ifndef TLGPU_H
+#define TLGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TLGPU_ABI_VERSION 1
+
+enum {
+    TL_OK = 0,
+    TL_E_INVALID = -1,   /* bad argument                         */
+    TL_E_CUDA = -2,      /* CUDA runtime failure                 */
+    TL_E_NODEVICE = -3,  /* no usable sm_100 device              */
+    TL_E_ALLOC = -4      /* device allocation failed             */
+};
+
+/* Dirichlet node sets the device kernels represent (structured, implicit). */
+enum {
+    TL_DIRICHLET_BOTTOM = 0,  /* z = lo face: global level, lpbfsim/twolevel.py:115-122     */
+    TL_DIRICHLET_GAMMA = 1    /* lateral + bottom faces: local level, twolevel.py:124-131,
+                                 mesh.py:498,507 (trace nodes)                              */
+};
+
+/* Per-solve outcome (mirrors what fem.solve_linear checks, fem.py:271-291). */
+enum {
+    TL_SOLVE_OK = 0,
+    TL_SOLVE_MAXITER = 1,     /* scipy cg info != 0                     */
+    TL_SOLVE_RESIDUAL = 2,    /* ||A x - b|| / ||b|| > 100 rtol         */
+    TL_SOLVE_NONFINITE = 3    /* FieldState finite check, fem.py:50-51  */
+};
+
+typedef struct {
+    int32_t iterations;   /* CG iterations (scipy callback count)        */
+    int32_t status;       /* TL_SOLVE_*                                   */
+    double bnorm;         /* ||b||_2 of the constrained system            */
+    double rnorm;         /* ||r||_2 of the recursive residual at exit    */
+    double true_resid;    /* ||A_c x - b||_2 / ||b||_2                    */
+} tl_solve_info;
+
+/* Structured grid: construction box, cell counts, accumulated translation. */
+typedef struct {
+    int32_t ncells[3];
+    double lo0[3];
+    double hi0[3];
+    double offset[3];      /* Mesh._offset (mesh.py:164,372)              */
+} tl_grid_desc;
+
+/* Volumetric conical Gaussian (sources.py:67-77): peak = 6 sqrt3 P eta / (2 pi r^2 d). */
+typedef struct {
+    double peak;
+    double radius;
+    double depth;
+    double center[3];
+    int32_t on;            /* 0: no source (laser off / after path end)   */
+} tl_gaussian;
+
+/* Whole two-level run: both grids, constant material, BCs, solver settings. */
+typedef struct {
+    tl_grid_desc global_grid;
+    tl_grid_desc local_grid;        /* initial placement                   */
+    double kappa;                   /* W/(m K), both levels (one-way coupling) */
+    double rho_c_global;            /* rho * c of the global material, J/(m^3 K) */
+    double rho_c_local;             /* rho * c of the local material         */
+    double T_buildplate;            /* global Dirichlet value              */
+    double beam_peak, beam_radius, beam_depth;
+    double rtol;                    /* SolverSettings.linear_tol           */
+    int32_t maxiter_factor;         /* maxiter = factor * n  (fem.py:285: 20) */
+    int32_t max_micro;              /* largest micro count per macro step  */
+    int32_t max_deposit;            /* largest deposit sample count per step */
+    int32_t device;                 /* CUDA device ordinal                 */
+} tl_run_desc;
+
+/* One macro step of the one-way multirate cycle (multirate.py:105-164), or one
+ * uniform step of run_space (n_micro == 1, multirate.py:203-216).  All values are
+ * precomputed on the host from the path and schedule only. */
+typedef struct {
+    double dt_global;               /* global step (fem.py:307, dt)        */
+    int32_t dep_offset;             /* first deposit sample of this step   */
+    int32_t dep_count;              /* deposit samples (SweptTrackDeposit) */
+    int32_t micro_offset;           /* first tl_micro_plan of this step    */
+    int32_t n_micro;                /* local solves that advance time      */
+    int32_t corrector;              /* 1: re-solve the last micro interval (multirate.py:149) */
+    int32_t relocate;               /* 1: local box moves after this step  */
+    int32_t record;                 /* 1: keep predictor + micro fields as snapshots */
+    double new_offset[3];           /* local offset after the move          */
+} tl_macro_plan;
+
+typedef struct {
+    double dt;                      /* local step length                    */
+    double w;                       /* trace blend weight (multirate.py:92-102) */
+    double center[3];               /* Gaussian centre at t1                */
+    int32_t source_on;
+} tl_micro_plan;
+
+typedef struct tl_run tl_run;
+
+/* ---- library ---------------------------------------------------------------- */
+int32_t tl_abi_version(void);
+const char* tl_last_error(void);
+/* SM count, L2 bytes, cooperative-launch support of a device. */
+int32_t tl_device_query(int32_t device, int32_t* sm_count, int64_t* l2_bytes, int32_t* coop);
+
+/* ---- single implicit step: replaces fem.step_backward_euler for a linear
+ *      problem (fem.py:307-355) = assemble_system (fem.py:129-194) +
+ *      constrained (fem.py:89-105) + solve_linear cg (fem.py:271-291).
+ *      dirichlet values: g = (1-w)*gA + w*gB on the Dirichlet set, or the
+ *      constant g_const when gA == NULL.  load (dense, optional) is the
+ *      extra_load / deposit term.  Host buffers in and out. */
+int32_t tl_step_host(const tl_grid_desc* grid, double kappa, double rho_c, double dt,
+                     int32_t dirichlet_kind, const double* gA, const double* gB, double w,
+                     double g_const, const double* T_old, const double* load,
+                     const tl_gaussian* src, double rtol, int32_t maxiter,
+                     double* x_out, tl_solve_info* info);
+
+/* ---- P1 interpolation of a global field at the nodes of a (translated) grid:
+ *      Mesh.interpolate (mesh.py:358-361) on Mesh.locate (mesh.py:308-339).
+ *      gamma_only != 0 evaluates only the gamma nodes (InterfaceGamma.trace_of,
+ *      mesh.py:471-474) and leaves the others untouched. */
+int32_t tl_interpolate_host(const tl_grid_desc* global_grid, const double* values,
+                            const tl_grid_desc* target, int32_t gamma_only, double* out);
+
+/* ---- P1 interpolation at arbitrary points (Mesh.interpolate). */
+int32_t tl_interpolate_points_host(const tl_grid_desc* global_grid, const double* values,
+                                   const double* points, int64_t npoints, double* out);
+
+/* ---- deposit scatter: SweptTrackDeposit.load (sources.py:164-172), deterministic. */
+int32_t tl_deposit_host(const tl_grid_desc* grid, const double* points, const double* power,
+                        int32_t count, double* load_out);
+
+/* ---- device-resident two-level run (run_spacetime / run_space hot loop). */
+int32_t tl_run_create(const tl_run_desc* desc, tl_run** out);
+int32_t tl_run_destroy(tl_run* run);
+/* initial_state (twolevel.py:145-156): global = T0 everywhere, local = P1(global),
+ * trace = P1(global) on gamma. */
+int32_t tl_run_initial(tl_run* run, double T0);
+/* Upload a global field and re-derive local field + trace (initial_state with a
+ * non-uniform T0). */
+int32_t tl_run_set_global(tl_run* run, const double* Tg_host, int64_t n);
+/* Run nsteps macro steps.  deposit arrays hold all samples referenced by the
+ * plans (points xyz interleaved).  Solve outcomes are appended to the run's
+ * info log (tl_run_take_info). */
+int32_t tl_run_macro_steps(tl_run* run, const tl_macro_plan* plans, int32_t nsteps,
+                           const tl_micro_plan* micro, int32_t nmicro,
+                           const double* dep_points, const double* dep_power, int32_t ndep);
+/* Snapshots kept by the last macro step with plan.record = 1:
+ * which 0 = predicted global field, 1 = local field after micro step `index`
+ * (index == n_micro: corrector result). */
+int32_t tl_run_get_snapshot(tl_run* run, int32_t which, int32_t index, double* host, int64_t n);
+/* Block until the run's stream is idle. */
+int32_t tl_run_sync(tl_run* run);
+/* which: 0 = global field, 1 = local field, 2 = trace (dense local array). */
+int32_t tl_run_get_field(tl_run* run, int32_t which, double* host, int64_t n);
+/* Copy out (and clear) the per-solve info log; *count receives the number written. */
+int32_t tl_run_take_info(tl_run* run, tl_solve_info* out, int32_t max, int32_t* count);
+/* Melt-pool summary of both fields: max T and count of nodes with T > T_liquidus
+ * (out: [gmax, lmax, gcount, lcount]).  Device reduction + 32-byte read. */
+int32_t tl_run_melt_summary(tl_run* run, double T_liquidus, double* out4);
+/* The run's CUDA stream (cudaStream_t) for event timing by the caller. */
+int32_t tl_run_stream(tl_run* run, void** stream);
+/* Number of kernels launched on the run's stream since creation. */
+int64_t tl_run_launch_count(tl_run* run);
+/* Write a scratch buffer larger than L2 on the run's stream (bench hygiene). */
+int32_t tl_run_flush_l2(tl_run* run);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TLGPU_H */

@@ -1,0 +1,151 @@
+"""ctypes binding of libtlgpu.so (C ABI declared in include/tlgpu.h).
+
+There is no CPU fallback: if the library is missing or fails to load, every
+entry point raises ``NativeLibraryMissing``.  Build it with
+``python -m paper_2110_12932_b200.build`` (or ``__graft_entry__.build()``).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+import numpy as np
+
+from .errors import NativeLibraryMissing, SolverError
+
+LIB_PATH = Path(__file__).resolve().parent / "libtlgpu.so"
+ABI_VERSION = 1
+
+TL_DIRICHLET_BOTTOM = 0
+TL_DIRICHLET_GAMMA = 1
+TL_SOLVE_OK, TL_SOLVE_MAXITER, TL_SOLVE_RESIDUAL, TL_SOLVE_NONFINITE = 0, 1, 2, 3
+
+_d3 = C.c_double * 3
+_i3 = C.c_int32 * 3
+
+
+class SolveInfo(C.Structure):
+    _fields_ = [("iterations", C.c_int32), ("status", C.c_int32), ("bnorm", C.c_double),
+                ("rnorm", C.c_double), ("true_resid", C.c_double)]
+
+
+class GridDesc(C.Structure):
+    _fields_ = [("ncells", _i3), ("lo0", _d3), ("hi0", _d3), ("offset", _d3)]
+
+    @classmethod
+    def make(cls, lo0, hi0, ncells, offset=(0.0, 0.0, 0.0)) -> "GridDesc":
+        return cls(_i3(*[int(v) for v in ncells]), _d3(*map(float, lo0)), _d3(*map(float, hi0)),
+                   _d3(*map(float, offset)))
+
+
+class Gaussian(C.Structure):
+    _fields_ = [("peak", C.c_double), ("radius", C.c_double), ("depth", C.c_double),
+                ("center", _d3), ("on", C.c_int32)]
+
+
+class RunDesc(C.Structure):
+    _fields_ = [("global_grid", GridDesc), ("local_grid", GridDesc), ("kappa", C.c_double),
+                ("rho_c_global", C.c_double), ("rho_c_local", C.c_double),
+                ("T_buildplate", C.c_double), ("beam_peak", C.c_double),
+                ("beam_radius", C.c_double), ("beam_depth", C.c_double), ("rtol", C.c_double),
+                ("maxiter_factor", C.c_int32), ("max_micro", C.c_int32),
+                ("max_deposit", C.c_int32), ("device", C.c_int32)]
+
+
+class MacroPlan(C.Structure):
+    _fields_ = [("dt_global", C.c_double), ("dep_offset", C.c_int32), ("dep_count", C.c_int32),
+                ("micro_offset", C.c_int32), ("n_micro", C.c_int32), ("corrector", C.c_int32),
+                ("relocate", C.c_int32), ("record", C.c_int32), ("new_offset", _d3)]
+
+
+class MicroPlan(C.Structure):
+    _fields_ = [("dt", C.c_double), ("w", C.c_double), ("center", _d3), ("source_on", C.c_int32)]
+
+
+# numpy views of the plan structs (same layout, built in bulk on the host)
+MACRO_DTYPE = np.dtype([("dt_global", "<f8"), ("dep_offset", "<i4"), ("dep_count", "<i4"),
+                        ("micro_offset", "<i4"), ("n_micro", "<i4"), ("corrector", "<i4"),
+                        ("relocate", "<i4"), ("record", "<i4"), ("new_offset", "<f8", (3,))],
+                       align=True)
+MICRO_DTYPE = np.dtype([("dt", "<f8"), ("w", "<f8"), ("center", "<f8", (3,)),
+                        ("source_on", "<i4")], align=True)
+assert MACRO_DTYPE.itemsize == C.sizeof(MacroPlan), (MACRO_DTYPE.itemsize, C.sizeof(MacroPlan))
+assert MICRO_DTYPE.itemsize == C.sizeof(MicroPlan), (MICRO_DTYPE.itemsize, C.sizeof(MicroPlan))
+
+_P = C.c_void_p
+_dp = C.POINTER(C.c_double)
+
+# (name, restype, argtypes) of every symbol include/tlgpu.h declares
+SIGNATURES = [
+    ("tl_abi_version", C.c_int32, []),
+    ("tl_last_error", C.c_char_p, []),
+    ("tl_device_query", C.c_int32, [C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int64),
+                                    C.POINTER(C.c_int32)]),
+    ("tl_step_host", C.c_int32, [C.POINTER(GridDesc), C.c_double, C.c_double, C.c_double, C.c_int32,
+                                 _dp, _dp, C.c_double, C.c_double, _dp, _dp, C.POINTER(Gaussian),
+                                 C.c_double, C.c_int32, _dp, C.POINTER(SolveInfo)]),
+    ("tl_interpolate_host", C.c_int32, [C.POINTER(GridDesc), _dp, C.POINTER(GridDesc), C.c_int32, _dp]),
+    ("tl_interpolate_points_host", C.c_int32, [C.POINTER(GridDesc), _dp, _dp, C.c_int64, _dp]),
+    ("tl_deposit_host", C.c_int32, [C.POINTER(GridDesc), _dp, _dp, C.c_int32, _dp]),
+    ("tl_run_create", C.c_int32, [C.POINTER(RunDesc), C.POINTER(_P)]),
+    ("tl_run_destroy", C.c_int32, [_P]),
+    ("tl_run_initial", C.c_int32, [_P, C.c_double]),
+    ("tl_run_set_global", C.c_int32, [_P, _dp, C.c_int64]),
+    ("tl_run_macro_steps", C.c_int32, [_P, _P, C.c_int32, _P, C.c_int32, _dp, _dp, C.c_int32]),
+    ("tl_run_get_snapshot", C.c_int32, [_P, C.c_int32, C.c_int32, _dp, C.c_int64]),
+    ("tl_run_sync", C.c_int32, [_P]),
+    ("tl_run_get_field", C.c_int32, [_P, C.c_int32, _dp, C.c_int64]),
+    ("tl_run_take_info", C.c_int32, [_P, C.POINTER(SolveInfo), C.c_int32, C.POINTER(C.c_int32)]),
+    ("tl_run_melt_summary", C.c_int32, [_P, C.c_double, _dp]),
+    ("tl_run_stream", C.c_int32, [_P, C.POINTER(_P)]),
+    ("tl_run_launch_count", C.c_int64, [_P]),
+    ("tl_run_flush_l2", C.c_int32, [_P]),
+]
+
+_lib = None
+
+
+def lib():
+    """Load libtlgpu.so once; raise NativeLibraryMissing if it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = Path(os.environ.get("TLGPU_LIB", LIB_PATH))
+    if not path.exists():
+        raise NativeLibraryMissing(
+            f"{path} not found: build it with `python -m paper_2110_12932_b200.build` "
+            "(there is no CPU fallback)")
+    try:
+        h = C.CDLL(str(path))
+    except OSError as exc:
+        raise NativeLibraryMissing(f"cannot load {path}: {exc}") from exc
+    for name, res, args in SIGNATURES:
+        fn = getattr(h, name)
+        fn.restype = res
+        fn.argtypes = args
+    if h.tl_abi_version() != ABI_VERSION:
+        raise NativeLibraryMissing(f"{path} has ABI {h.tl_abi_version()}, expected {ABI_VERSION}")
+    _lib = h
+    return h
+
+
+def check(rc: int, what: str = "tlgpu"):
+    if rc != 0:
+        msg = lib().tl_last_error().decode(errors="replace")
+        raise SolverError(f"{what} failed ({rc}): {msg}")
+
+
+def dptr(a: np.ndarray):
+    """Pointer to a C-contiguous float64 array (or None)."""
+    if a is None:
+        return None
+    assert a.dtype == np.float64 and a.flags["C_CONTIGUOUS"], "expected contiguous float64"
+    return a.ctypes.data_as(_dp)
+
+
+def device_query(device: int = 0):
+    sm, l2, coop = C.c_int32(), C.c_int64(), C.c_int32()
+    check(lib().tl_device_query(device, C.byref(sm), C.byref(l2), C.byref(coop)), "device query")
+    return {"sm_count": sm.value, "l2_bytes": l2.value, "cooperative": bool(coop.value)}

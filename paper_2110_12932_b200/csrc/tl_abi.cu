@@ -1,0 +1,587 @@
+// tl_abi.cu — C ABI (include/tlgpu.h) over the sm_100a kernels in tl_kernels.cuh.
+//
+// Host orchestration of one two-level run.  Per macro step of the one-way
+// multirate cycle (lpbfsim/multirate.py:105-164, one-way branch :144-155):
+//   k_deposit            swept-track deposit for [t, t + dt_macro]       (runner.py:75-79)
+//   k_pcg<false>         global backward-Euler step, bottom Dirichlet    (twolevel.py:242-271)
+//   k_interp (gamma)     trace_pred = P1(global) on the gamma nodes      (multirate.py:129)
+//   m x k_pcg<true>      micro local steps, blended trace, Gaussian      (multirate.py:133-142)
+//   [k_pcg<true>]        corrector re-solve of the last interval         (multirate.py:149-150)
+//   k_interp (all)       relocation: local = P1(global) at moved nodes  (scanpath.py:243-248)
+// All state stays on the device; the host only enqueues launches.
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/tlgpu.h"
+#include "tl_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define TL_CUDA(call)                                                                         \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            return fail(TL_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));       \
+    } while (0)
+
+int make_grid(const tl_grid_desc& d, int dkind, tl::Grid& g) {
+    for (int a = 0; a < 3; ++a) {
+        if (d.ncells[a] < 1) return fail(TL_E_INVALID, "grid needs at least one cell per axis");
+        if (!(d.hi0[a] > d.lo0[a])) return fail(TL_E_INVALID, "degenerate grid box");
+        g.nc[a] = d.ncells[a];
+        g.lo0[a] = d.lo0[a];
+        g.hi0[a] = d.hi0[a];
+        g.off[a] = d.offset[a];
+        g.step[a] = (d.hi0[a] - d.lo0[a]) / (double)d.ncells[a];  // linspace step = delta / div
+        g.h[a] = g.step[a];                                         // Box.lengths / ncells
+    }
+    g.NX = g.nc[0] + 1;
+    g.NY = g.nc[1] + 1;
+    g.NZ = g.nc[2] + 1;
+    long long n = (long long)g.NX * g.NY * g.NZ;
+    if (n >= (1ll << 31)) return fail(TL_E_INVALID, "grid exceeds 2^31 nodes");
+    g.n = (int)n;
+    g.divX.init((uint32_t)g.NX);
+    g.divY.init((uint32_t)g.NY);
+    g.dkind = dkind;
+    return TL_OK;
+}
+
+int coop_blocks(bool gauss, size_t smem, int sms, int& blocks) {
+    int per_sm = 0;
+    cudaError_t e;
+    if (gauss)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tl::k_pcg<true>, tl::kTPB, smem);
+    else
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tl::k_pcg<false>, tl::kTPB, smem);
+    if (e != cudaSuccess) return fail(TL_E_CUDA, std::string("occupancy: ") + cudaGetErrorString(e));
+    if (per_sm < 1) return fail(TL_E_CUDA, "k_pcg cannot be resident");
+    blocks = per_sm * sms;
+    return TL_OK;
+}
+
+size_t gauss_smem(const tl::Grid& g) { return sizeof(double) * 6 * (size_t)(g.nc[0] + g.nc[1] + g.nc[2]); }
+
+int launch_pcg(tl::PcgParams& P, bool gauss, int sms, cudaStream_t st, int64_t* launches) {
+    size_t smem = gauss ? gauss_smem(P.g) : 0;
+    if (gauss && smem > 200 * 1024) return fail(TL_E_INVALID, "local grid too long for Gaussian tables");
+    int blocks = 0;
+    int rc = coop_blocks(gauss, smem, sms, blocks);
+    if (rc) return rc;
+    void* args[] = {&P};
+    cudaError_t e;
+    if (gauss) {
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(tl::k_pcg<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        e = cudaLaunchCooperativeKernel((void*)tl::k_pcg<true>, blocks, tl::kTPB, args, smem, st);
+    } else {
+        e = cudaLaunchCooperativeKernel((void*)tl::k_pcg<false>, blocks, tl::kTPB, args, smem, st);
+    }
+    if (e != cudaSuccess) return fail(TL_E_CUDA, std::string("k_pcg launch: ") + cudaGetErrorString(e));
+    if (launches) ++*launches;
+    return TL_OK;
+}
+
+void set_coeffs(tl::PcgParams& P, double kappa, double rho_c, double dt) {
+    const double V = P.g.h[0] * P.g.h[1] * P.g.h[2];
+    for (int a = 0; a < 3; ++a) P.cbase[a] = kappa * V / (P.g.h[a] * P.g.h[a]) / 6.0;
+    P.mbase = (rho_c / dt) * V / 24.0;
+}
+
+int device_sms(int dev, int& sms) {
+    TL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    return TL_OK;
+}
+
+template <class T>
+int dalloc(T** p, size_t n) {
+    cudaError_t e = cudaMalloc((void**)p, sizeof(T) * (n ? n : 1));
+    if (e != cudaSuccess) return fail(TL_E_ALLOC, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    return TL_OK;
+}
+
+}  // namespace
+
+struct tl_run {
+    int device = 0, sms = 0;
+    cudaStream_t stream = nullptr;
+    tl_run_desc desc{};
+    tl::Grid G{}, L{};
+    double* Tg = nullptr; double* bg = nullptr; double* rg = nullptr; double* pg0 = nullptr; double* pg1 = nullptr; double* qg = nullptr;
+    double* loadg = nullptr;
+    double* Tl = nullptr; double* bl = nullptr; double* rl = nullptr; double* pl0 = nullptr; double* pl1 = nullptr; double* ql = nullptr;
+    double* tr_old = nullptr; double* tr_pred = nullptr; double* Tl_before = nullptr;
+    double* part = nullptr;
+    int* dep_prev = nullptr; int* dep_prev_n = nullptr;
+    double* dep_pts = nullptr; double* dep_pow = nullptr; int dep_cap = 0;
+    tl::SolveInfoDev* info = nullptr; int info_cap = 0; int info_n = 0;
+    double* melt = nullptr; double* melt_part = nullptr; double* melt_host = nullptr;
+    double* snap_g = nullptr; std::vector<double*> snap_l; int snap_n = 0;
+    double* flush = nullptr; size_t flush_n = 0;
+    int64_t launches = 0;
+};
+
+extern "C" {
+
+int32_t tl_abi_version(void) { return TLGPU_ABI_VERSION; }
+
+const char* tl_last_error(void) { return g_err.c_str(); }
+
+int32_t tl_device_query(int32_t device, int32_t* sm_count, int64_t* l2_bytes, int32_t* coop) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n <= device) return fail(TL_E_NODEVICE, "no CUDA device");
+    int v = 0;
+    TL_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device));
+    if (sm_count) *sm_count = v;
+    TL_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, device));
+    if (l2_bytes) *l2_bytes = v;
+    TL_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrCooperativeLaunch, device));
+    if (coop) *coop = v;
+    return TL_OK;
+}
+
+// ------------------------------------------------------------------------------------
+// Single step on host buffers (seam 3: fem.step_backward_euler for a linear problem).
+// ------------------------------------------------------------------------------------
+int32_t tl_step_host(const tl_grid_desc* grid, double kappa, double rho_c, double dt,
+                     int32_t dirichlet_kind, const double* gA, const double* gB, double w,
+                     double g_const, const double* T_old, const double* load,
+                     const tl_gaussian* src, double rtol, int32_t maxiter, double* x_out,
+                     tl_solve_info* info) {
+    if (!grid || !T_old || !x_out) return fail(TL_E_INVALID, "null argument");
+    if (dt <= 0) return fail(TL_E_INVALID, "time step must be positive");
+    if (dirichlet_kind != tl::kBottom && dirichlet_kind != tl::kGamma)
+        return fail(TL_E_INVALID, "unknown Dirichlet kind");
+    int dev = 0;
+    TL_CUDA(cudaGetDevice(&dev));
+    int sms = 0;
+    if (int rc = device_sms(dev, sms)) return rc;
+    tl::PcgParams P{};
+    if (int rc = make_grid(*grid, dirichlet_kind, P.g)) return rc;
+    const int n = P.g.n;
+    set_coeffs(P, kappa, rho_c, dt);
+    const size_t nb = sizeof(double) * n;
+    double *T, *b, *r, *p0, *p1, *q, *dA = nullptr, *dB = nullptr, *dload = nullptr, *part;
+    tl::SolveInfoDev* dinfo;
+    int rc = 0;
+    if ((rc = dalloc(&T, n)) || (rc = dalloc(&b, n)) || (rc = dalloc(&r, n)) || (rc = dalloc(&p0, n)) ||
+        (rc = dalloc(&p1, n)) || (rc = dalloc(&q, n)) || (rc = dalloc(&part, 4 * sms * 32)) ||
+        (rc = dalloc(&dinfo, 1)))
+        return rc;
+    TL_CUDA(cudaMemcpy(T, T_old, nb, cudaMemcpyHostToDevice));
+    if (gA) {
+        if ((rc = dalloc(&dA, n)) || (rc = dalloc(&dB, n))) return rc;
+        TL_CUDA(cudaMemcpy(dA, gA, nb, cudaMemcpyHostToDevice));
+        TL_CUDA(cudaMemcpy(dB, gB ? gB : gA, nb, cudaMemcpyHostToDevice));
+    }
+    if (load) {
+        if ((rc = dalloc(&dload, n))) return rc;
+        TL_CUDA(cudaMemcpy(dload, load, nb, cudaMemcpyHostToDevice));
+    }
+    P.T = T; P.gA = dA; P.gB = dB; P.w = gA ? w : 0.0; P.g_const = g_const; P.load = dload;
+    P.b = b; P.r = r; P.p0 = p0; P.p1 = p1; P.q = q; P.part = part;
+    P.rtol = rtol; P.maxiter = maxiter; P.info = dinfo;
+    bool gauss = src && src->on;
+    if (gauss) {
+        P.src.peak = src->peak; P.src.radius = src->radius; P.src.depth = src->depth;
+        for (int a = 0; a < 3; ++a) P.src.center[a] = src->center[a];
+        P.src.on = 1;
+    }
+    rc = launch_pcg(P, gauss, sms, 0, nullptr);
+    if (rc) return rc;
+    TL_CUDA(cudaDeviceSynchronize());
+    tl::SolveInfoDev hi{};
+    TL_CUDA(cudaMemcpy(&hi, dinfo, sizeof(hi), cudaMemcpyDeviceToHost));
+    TL_CUDA(cudaMemcpy(x_out, T, nb, cudaMemcpyDeviceToHost));
+    if (info) {
+        info->iterations = hi.iterations; info->status = hi.status; info->bnorm = hi.bnorm;
+        info->rnorm = hi.rnorm; info->true_resid = hi.true_resid;
+    }
+    cudaFree(T); cudaFree(b); cudaFree(r); cudaFree(p0); cudaFree(p1); cudaFree(q); cudaFree(part);
+    cudaFree(dinfo); if (dA) cudaFree(dA); if (dB) cudaFree(dB); if (dload) cudaFree(dload);
+    return TL_OK;
+}
+
+int32_t tl_interpolate_host(const tl_grid_desc* global_grid, const double* values,
+                            const tl_grid_desc* target, int32_t gamma_only, double* out) {
+    if (!global_grid || !values || !target || !out) return fail(TL_E_INVALID, "null argument");
+    tl::Grid G{}, L{};
+    if (int rc = make_grid(*global_grid, tl::kBottom, G)) return rc;
+    if (int rc = make_grid(*target, tl::kGamma, L)) return rc;
+    double *dv, *dout;
+    int rc = 0;
+    if ((rc = dalloc(&dv, G.n)) || (rc = dalloc(&dout, L.n))) return rc;
+    TL_CUDA(cudaMemcpy(dv, values, sizeof(double) * G.n, cudaMemcpyHostToDevice));
+    TL_CUDA(cudaMemcpy(dout, out, sizeof(double) * L.n, cudaMemcpyHostToDevice));
+    tl::k_interp<<<592, 256>>>(G, dv, L, gamma_only ? 1 : 0, gamma_only ? nullptr : dout,
+                               gamma_only ? dout : nullptr);
+    TL_CUDA(cudaGetLastError());
+    TL_CUDA(cudaMemcpy(out, dout, sizeof(double) * L.n, cudaMemcpyDeviceToHost));
+    cudaFree(dv); cudaFree(dout);
+    return TL_OK;
+}
+
+int32_t tl_interpolate_points_host(const tl_grid_desc* global_grid, const double* values,
+                                   const double* points, int64_t npoints, double* out) {
+    if (!global_grid || !values || !points || !out || npoints < 0) return fail(TL_E_INVALID, "bad argument");
+    tl::Grid G{};
+    if (int rc = make_grid(*global_grid, tl::kBottom, G)) return rc;
+    double *dv, *dp, *dout;
+    int rc = 0;
+    if ((rc = dalloc(&dv, G.n)) || (rc = dalloc(&dp, 3 * npoints)) || (rc = dalloc(&dout, npoints))) return rc;
+    TL_CUDA(cudaMemcpy(dv, values, sizeof(double) * G.n, cudaMemcpyHostToDevice));
+    TL_CUDA(cudaMemcpy(dp, points, sizeof(double) * 3 * npoints, cudaMemcpyHostToDevice));
+    if (npoints > 0) tl::k_interp_pts<<<296, 256>>>(G, dv, dp, npoints, dout);
+    TL_CUDA(cudaGetLastError());
+    TL_CUDA(cudaMemcpy(out, dout, sizeof(double) * npoints, cudaMemcpyDeviceToHost));
+    cudaFree(dv); cudaFree(dp); cudaFree(dout);
+    return TL_OK;
+}
+
+int32_t tl_deposit_host(const tl_grid_desc* grid, const double* points, const double* power,
+                        int32_t count, double* load_out) {
+    if (!grid || !load_out || count < 0) return fail(TL_E_INVALID, "bad argument");
+    if (count * 4 > tl::kDepMax) return fail(TL_E_INVALID, "too many deposit samples per call");
+    tl::Grid G{};
+    if (int rc = make_grid(*grid, tl::kBottom, G)) return rc;
+    double *dl, *dp, *dw;
+    int *prev, *prevn;
+    int rc = 0;
+    if ((rc = dalloc(&dl, G.n)) || (rc = dalloc(&dp, 3 * count)) || (rc = dalloc(&dw, count)) ||
+        (rc = dalloc(&prev, tl::kDepMax)) || (rc = dalloc(&prevn, 1)))
+        return rc;
+    TL_CUDA(cudaMemset(dl, 0, sizeof(double) * G.n));
+    TL_CUDA(cudaMemset(prevn, 0, sizeof(int)));
+    if (count) {
+        TL_CUDA(cudaMemcpy(dp, points, sizeof(double) * 3 * count, cudaMemcpyHostToDevice));
+        TL_CUDA(cudaMemcpy(dw, power, sizeof(double) * count, cudaMemcpyHostToDevice));
+    }
+    tl::k_deposit<<<1, 256>>>(G, dp, dw, count, dl, prev, prevn);
+    TL_CUDA(cudaGetLastError());
+    TL_CUDA(cudaMemcpy(load_out, dl, sizeof(double) * G.n, cudaMemcpyDeviceToHost));
+    cudaFree(dl); cudaFree(dp); cudaFree(dw); cudaFree(prev); cudaFree(prevn);
+    return TL_OK;
+}
+
+// ------------------------------------------------------------------------------------
+// Device-resident run.
+// ------------------------------------------------------------------------------------
+int32_t tl_run_create(const tl_run_desc* desc, tl_run** out) {
+    if (!desc || !out) return fail(TL_E_INVALID, "null argument");
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n <= desc->device) return fail(TL_E_NODEVICE, "no CUDA device");
+    TL_CUDA(cudaSetDevice(desc->device));
+    int coop = 0;
+    TL_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, desc->device));
+    if (!coop) return fail(TL_E_NODEVICE, "device lacks cooperative launch");
+    tl_run* R = new tl_run();
+    R->device = desc->device;
+    R->desc = *desc;
+    int rc = 0;
+    if ((rc = device_sms(R->device, R->sms)) || (rc = make_grid(desc->global_grid, tl::kBottom, R->G)) ||
+        (rc = make_grid(desc->local_grid, tl::kGamma, R->L))) {
+        delete R;
+        return rc;
+    }
+    if (gauss_smem(R->L) > 200 * 1024) { delete R; return fail(TL_E_INVALID, "local grid too long"); }
+    TL_CUDA(cudaStreamCreateWithFlags(&R->stream, cudaStreamNonBlocking));
+    const int ng = R->G.n, nl = R->L.n;
+    if ((rc = dalloc(&R->Tg, ng)) || (rc = dalloc(&R->bg, ng)) || (rc = dalloc(&R->rg, ng)) ||
+        (rc = dalloc(&R->pg0, ng)) || (rc = dalloc(&R->pg1, ng)) || (rc = dalloc(&R->qg, ng)) ||
+        (rc = dalloc(&R->loadg, ng)) || (rc = dalloc(&R->Tl, nl)) || (rc = dalloc(&R->bl, nl)) ||
+        (rc = dalloc(&R->rl, nl)) || (rc = dalloc(&R->pl0, nl)) || (rc = dalloc(&R->pl1, nl)) ||
+        (rc = dalloc(&R->ql, nl)) || (rc = dalloc(&R->tr_old, nl)) || (rc = dalloc(&R->tr_pred, nl)) ||
+        (rc = dalloc(&R->Tl_before, nl)) || (rc = dalloc(&R->part, 4 * R->sms * 32)) ||
+        (rc = dalloc(&R->dep_prev, tl::kDepMax)) || (rc = dalloc(&R->dep_prev_n, 1)) ||
+        (rc = dalloc(&R->melt, 4)) || (rc = dalloc(&R->melt_part, 2 * 1184))) {
+        tl_run_destroy(R);
+        return rc;
+    }
+    TL_CUDA(cudaMemsetAsync(R->loadg, 0, sizeof(double) * ng, R->stream));
+    TL_CUDA(cudaMemsetAsync(R->dep_prev_n, 0, sizeof(int), R->stream));
+    TL_CUDA(cudaMemsetAsync(R->tr_old, 0, sizeof(double) * nl, R->stream));
+    TL_CUDA(cudaMemsetAsync(R->tr_pred, 0, sizeof(double) * nl, R->stream));
+    TL_CUDA(cudaMallocHost((void**)&R->melt_host, 4 * sizeof(double)));
+    *out = R;
+    return TL_OK;
+}
+
+int32_t tl_run_destroy(tl_run* R) {
+    if (!R) return TL_OK;
+    cudaSetDevice(R->device);
+    if (R->stream) cudaStreamSynchronize(R->stream);
+    double* bufs[] = {R->Tg, R->bg, R->rg, R->pg0, R->pg1, R->qg, R->loadg, R->Tl, R->bl, R->rl, R->pl0,
+                      R->pl1, R->ql, R->tr_old, R->tr_pred, R->Tl_before, R->part, R->dep_pts,
+                      R->dep_pow, R->melt, R->melt_part, R->flush};
+    for (double* b : bufs)
+        if (b) cudaFree(b);
+    if (R->dep_prev) cudaFree(R->dep_prev);
+    if (R->dep_prev_n) cudaFree(R->dep_prev_n);
+    if (R->info) cudaFree(R->info);
+    if (R->snap_g) cudaFree(R->snap_g);
+    for (double* b : R->snap_l) cudaFree(b);
+    if (R->melt_host) cudaFreeHost(R->melt_host);
+    if (R->stream) cudaStreamDestroy(R->stream);
+    delete R;
+    return TL_OK;
+}
+
+static int run_interp_local(tl_run* R, int mode, double* out_all, double* out_gamma) {
+    tl::k_interp<<<4 * R->sms, 256, 0, R->stream>>>(R->G, R->Tg, R->L, mode, out_all, out_gamma);
+    ++R->launches;
+    TL_CUDA(cudaGetLastError());
+    return TL_OK;
+}
+
+int32_t tl_run_initial(tl_run* R, double T0) {
+    if (!R) return fail(TL_E_INVALID, "null run");
+    TL_CUDA(cudaSetDevice(R->device));
+    tl::k_fill<<<4 * R->sms, 256, 0, R->stream>>>(R->Tg, R->G.n, T0);
+    ++R->launches;
+    TL_CUDA(cudaGetLastError());
+    return run_interp_local(R, 0, R->Tl, R->tr_old);
+}
+
+int32_t tl_run_set_global(tl_run* R, const double* Tg_host, int64_t n) {
+    if (!R || !Tg_host || n != R->G.n) return fail(TL_E_INVALID, "global field size mismatch");
+    TL_CUDA(cudaSetDevice(R->device));
+    TL_CUDA(cudaMemcpyAsync(R->Tg, Tg_host, sizeof(double) * n, cudaMemcpyHostToDevice, R->stream));
+    return run_interp_local(R, 0, R->Tl, R->tr_old);
+}
+
+static int ensure_info(tl_run* R, int extra) {
+    if (R->info_n + extra <= R->info_cap) return TL_OK;
+    int cap = R->info_cap ? R->info_cap : 1024;
+    while (cap < R->info_n + extra) cap *= 2;
+    tl::SolveInfoDev* ni = nullptr;
+    if (int rc = dalloc(&ni, cap)) return rc;
+    if (R->info) {
+        TL_CUDA(cudaMemcpyAsync(ni, R->info, sizeof(tl::SolveInfoDev) * R->info_n, cudaMemcpyDeviceToDevice, R->stream));
+        TL_CUDA(cudaStreamSynchronize(R->stream));
+        cudaFree(R->info);
+    }
+    R->info = ni;
+    R->info_cap = cap;
+    return TL_OK;
+}
+
+static void base_params(tl_run* R, tl::PcgParams& P, bool local, double dt) {
+    P.g = local ? R->L : R->G;
+    set_coeffs(P, R->desc.kappa, local ? R->desc.rho_c_local : R->desc.rho_c_global, dt);
+    P.rtol = R->desc.rtol;
+    long long mi = (long long)R->desc.maxiter_factor * P.g.n;
+    P.maxiter = mi > 2000000000ll ? 2000000000 : (int)mi;
+    P.part = R->part;
+    if (local) {
+        P.b = R->bl; P.r = R->rl; P.p0 = R->pl0; P.p1 = R->pl1; P.q = R->ql;
+    } else {
+        P.b = R->bg; P.r = R->rg; P.p0 = R->pg0; P.p1 = R->pg1; P.q = R->qg;
+    }
+}
+
+static int ensure_snapshots(tl_run* R, int nl) {
+    if (!R->snap_g)
+        if (int rc = dalloc(&R->snap_g, R->G.n)) return rc;
+    while ((int)R->snap_l.size() < nl) {
+        double* b = nullptr;
+        if (int rc = dalloc(&b, R->L.n)) return rc;
+        R->snap_l.push_back(b);
+    }
+    return TL_OK;
+}
+
+static int local_solve(tl_run* R, double* T, const tl_micro_plan& mp) {
+    tl::PcgParams P{};
+    base_params(R, P, true, mp.dt);
+    P.T = T;
+    P.gA = R->tr_old;
+    P.gB = R->tr_pred;
+    P.w = mp.w;
+    P.load = nullptr;
+    bool gauss = mp.source_on != 0;
+    if (gauss) {
+        P.src.peak = R->desc.beam_peak; P.src.radius = R->desc.beam_radius; P.src.depth = R->desc.beam_depth;
+        for (int a = 0; a < 3; ++a) P.src.center[a] = mp.center[a];
+        P.src.on = 1;
+    }
+    P.info = R->info + R->info_n++;
+    return launch_pcg(P, gauss, R->sms, R->stream, &R->launches);
+}
+
+int32_t tl_run_macro_steps(tl_run* R, const tl_macro_plan* plans, int32_t nsteps,
+                           const tl_micro_plan* micro, int32_t nmicro, const double* dep_points,
+                           const double* dep_power, int32_t ndep) {
+    if (!R || (!plans && nsteps > 0)) return fail(TL_E_INVALID, "null argument");
+    TL_CUDA(cudaSetDevice(R->device));
+    int need = 0;
+    for (int s = 0; s < nsteps; ++s) {
+        const tl_macro_plan& mp = plans[s];
+        if (mp.n_micro < 1 || mp.micro_offset < 0 || mp.micro_offset + mp.n_micro + mp.corrector > nmicro)
+            return fail(TL_E_INVALID, "micro plan out of range");
+        if (mp.dep_count < 0 || mp.dep_offset < 0 || mp.dep_offset + mp.dep_count > ndep)
+            return fail(TL_E_INVALID, "deposit plan out of range");
+        if (mp.dep_count * 4 > tl::kDepMax) return fail(TL_E_INVALID, "too many deposit samples in one step");
+        need += 1 + mp.n_micro + mp.corrector;
+    }
+    if (int rc = ensure_info(R, need)) return rc;
+    if (ndep > R->dep_cap) {
+        if (R->dep_pts) cudaFree(R->dep_pts);
+        if (R->dep_pow) cudaFree(R->dep_pow);
+        int rc = 0;
+        if ((rc = dalloc(&R->dep_pts, 3 * (size_t)ndep)) || (rc = dalloc(&R->dep_pow, ndep))) return rc;
+        R->dep_cap = ndep;
+    }
+    if (ndep > 0) {
+        TL_CUDA(cudaMemcpyAsync(R->dep_pts, dep_points, sizeof(double) * 3 * ndep, cudaMemcpyHostToDevice, R->stream));
+        TL_CUDA(cudaMemcpyAsync(R->dep_pow, dep_power, sizeof(double) * ndep, cudaMemcpyHostToDevice, R->stream));
+    }
+    for (int s = 0; s < nsteps; ++s) {
+        const tl_macro_plan& mp = plans[s];
+        // -- global predictor (twolevel.solve_global): deposit + implicit step --
+        tl::k_deposit<<<1, 256, 0, R->stream>>>(R->G, R->dep_pts + 3 * (size_t)mp.dep_offset,
+                                                 R->dep_pow + mp.dep_offset, mp.dep_count, R->loadg,
+                                                 R->dep_prev, R->dep_prev_n);
+        ++R->launches;
+        TL_CUDA(cudaGetLastError());
+        tl::PcgParams P{};
+        base_params(R, P, false, mp.dt_global);
+        P.T = R->Tg;
+        P.gA = nullptr;
+        P.g_const = R->desc.T_buildplate;
+        P.load = R->loadg;
+        P.info = R->info + R->info_n++;
+        if (int rc = launch_pcg(P, false, R->sms, R->stream, &R->launches)) return rc;
+        if (mp.record) {
+            if (int rc = ensure_snapshots(R, mp.n_micro + mp.corrector)) return rc;
+            TL_CUDA(cudaMemcpyAsync(R->snap_g, R->Tg, sizeof(double) * R->G.n, cudaMemcpyDeviceToDevice, R->stream));
+            R->snap_n = mp.n_micro + mp.corrector;
+        }
+        // -- trace of the predicted global field on gamma --
+        if (int rc = run_interp_local(R, 1, nullptr, R->tr_pred)) return rc;
+        // -- micro steps --
+        for (int i = 0; i < mp.n_micro; ++i) {
+            const tl_micro_plan& up = micro[mp.micro_offset + i];
+            if (i == mp.n_micro - 1 && mp.corrector) {
+                tl::k_copy<<<4 * R->sms, 256, 0, R->stream>>>(R->Tl, R->Tl_before, R->L.n);
+                ++R->launches;
+            }
+            if (int rc = local_solve(R, R->Tl, up)) return rc;
+            if (mp.record)
+                TL_CUDA(cudaMemcpyAsync(R->snap_l[i], R->Tl, sizeof(double) * R->L.n, cudaMemcpyDeviceToDevice, R->stream));
+        }
+        if (mp.corrector) {
+            // corrector: re-solve the last micro interval from before_final with trace_pred
+            if (int rc = local_solve(R, R->Tl_before, micro[mp.micro_offset + mp.n_micro])) return rc;
+            std::swap(R->Tl, R->Tl_before);
+            if (mp.record)
+                TL_CUDA(cudaMemcpyAsync(R->snap_l[mp.n_micro], R->Tl, sizeof(double) * R->L.n, cudaMemcpyDeviceToDevice, R->stream));
+        }
+        // converged trace at the macro instant = trace_pred
+        std::swap(R->tr_old, R->tr_pred);
+        // -- relocation (scanpath.relocate_local) --
+        if (mp.relocate) {
+            for (int a = 0; a < 3; ++a) R->L.off[a] = mp.new_offset[a];
+            if (int rc = run_interp_local(R, 0, R->Tl, R->tr_old)) return rc;
+        }
+    }
+    TL_CUDA(cudaGetLastError());
+    return TL_OK;
+}
+
+int32_t tl_run_get_snapshot(tl_run* R, int32_t which, int32_t index, double* host, int64_t n) {
+    if (!R || !host) return fail(TL_E_INVALID, "null argument");
+    TL_CUDA(cudaSetDevice(R->device));
+    const double* src = nullptr;
+    if (which == 0 && R->snap_g && n == R->G.n) src = R->snap_g;
+    if (which == 1 && index >= 0 && index < R->snap_n && n == R->L.n) src = R->snap_l[index];
+    if (!src) return fail(TL_E_INVALID, "no such snapshot");
+    TL_CUDA(cudaMemcpyAsync(host, src, sizeof(double) * n, cudaMemcpyDeviceToHost, R->stream));
+    TL_CUDA(cudaStreamSynchronize(R->stream));
+    return TL_OK;
+}
+
+int32_t tl_run_sync(tl_run* R) {
+    if (!R) return fail(TL_E_INVALID, "null run");
+    TL_CUDA(cudaSetDevice(R->device));
+    TL_CUDA(cudaStreamSynchronize(R->stream));
+    return TL_OK;
+}
+
+int32_t tl_run_get_field(tl_run* R, int32_t which, double* host, int64_t n) {
+    if (!R || !host) return fail(TL_E_INVALID, "null argument");
+    TL_CUDA(cudaSetDevice(R->device));
+    const double* src = which == 0 ? R->Tg : (which == 1 ? R->Tl : R->tr_old);
+    const int64_t want = which == 0 ? R->G.n : R->L.n;
+    if (which < 0 || which > 2 || n != want) return fail(TL_E_INVALID, "field selector or size mismatch");
+    TL_CUDA(cudaMemcpyAsync(host, src, sizeof(double) * n, cudaMemcpyDeviceToHost, R->stream));
+    TL_CUDA(cudaStreamSynchronize(R->stream));
+    return TL_OK;
+}
+
+int32_t tl_run_take_info(tl_run* R, tl_solve_info* out, int32_t max, int32_t* count) {
+    if (!R || !count) return fail(TL_E_INVALID, "null argument");
+    TL_CUDA(cudaSetDevice(R->device));
+    TL_CUDA(cudaStreamSynchronize(R->stream));
+    const int n = R->info_n < max ? R->info_n : max;
+    std::vector<tl::SolveInfoDev> tmp(n > 0 ? n : 1);
+    if (n > 0) TL_CUDA(cudaMemcpy(tmp.data(), R->info, sizeof(tl::SolveInfoDev) * n, cudaMemcpyDeviceToHost));
+    for (int e = 0; e < n; ++e) {
+        out[e].iterations = tmp[e].iterations; out[e].status = tmp[e].status; out[e].bnorm = tmp[e].bnorm;
+        out[e].rnorm = tmp[e].rnorm; out[e].true_resid = tmp[e].true_resid;
+    }
+    if (n < R->info_n) {   // keep the remainder at the front
+        TL_CUDA(cudaMemcpy(R->info, R->info + n, sizeof(tl::SolveInfoDev) * (R->info_n - n), cudaMemcpyDeviceToDevice));
+    }
+    R->info_n -= n;
+    *count = n;
+    return TL_OK;
+}
+
+int32_t tl_run_melt_summary(tl_run* R, double T_liquidus, double* out4) {
+    if (!R || !out4) return fail(TL_E_INVALID, "null argument");
+    TL_CUDA(cudaSetDevice(R->device));
+    const int nb = 4 * R->sms;
+    tl::k_melt_partial<<<nb, 256, 0, R->stream>>>(R->Tg, R->G.n, T_liquidus, R->melt_part);
+    tl::k_melt_final<<<1, 32, 0, R->stream>>>(R->melt_part, nb, R->melt + 0, R->melt + 2);
+    tl::k_melt_partial<<<nb, 256, 0, R->stream>>>(R->Tl, R->L.n, T_liquidus, R->melt_part);
+    tl::k_melt_final<<<1, 32, 0, R->stream>>>(R->melt_part, nb, R->melt + 1, R->melt + 3);
+    R->launches += 4;
+    TL_CUDA(cudaGetLastError());
+    TL_CUDA(cudaMemcpyAsync(R->melt_host, R->melt, 4 * sizeof(double), cudaMemcpyDeviceToHost, R->stream));
+    TL_CUDA(cudaStreamSynchronize(R->stream));
+    for (int e = 0; e < 4; ++e) out4[e] = R->melt_host[e];
+    return TL_OK;
+}
+
+int32_t tl_run_stream(tl_run* R, void** stream) {
+    if (!R || !stream) return fail(TL_E_INVALID, "null argument");
+    *stream = (void*)R->stream;
+    return TL_OK;
+}
+
+int64_t tl_run_launch_count(tl_run* R) { return R ? R->launches : -1; }
+
+int32_t tl_run_flush_l2(tl_run* R) {
+    if (!R) return fail(TL_E_INVALID, "null run");
+    TL_CUDA(cudaSetDevice(R->device));
+    if (!R->flush) {
+        int l2 = 0;
+        TL_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, R->device));
+        R->flush_n = (size_t)l2 * 2 / sizeof(double);
+        if (int rc = dalloc(&R->flush, R->flush_n)) return rc;
+    }
+    tl::k_flush<<<4 * R->sms, 512, 0, R->stream>>>(R->flush, R->flush_n, 1.0);
+    TL_CUDA(cudaGetLastError());
+    return TL_OK;
+}
+
+}  // extern "C"

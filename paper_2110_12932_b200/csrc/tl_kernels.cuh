@@ -1,0 +1,571 @@
+// tl_kernels.cuh — device kernels of the two-level heat solve (sm_100a, fp64).
+//
+//   k_pcg        persistent cooperative kernel: RHS build (mass, Gaussian load,
+//                dense extra load, Dirichlet lift) + Jacobi-PCG mirroring scipy's
+//                cg + true-residual check + Dirichlet re-imposition.
+//                Replaces fem.assemble_system + constrained + solve_linear
+//                (lpbfsim/fem.py:129-194, 89-105, 271-298) for one solve.
+//   k_interp     Kuhn-P1 interpolation of the global field at local nodes
+//                (Mesh.interpolate / InterfaceGamma.trace_of, mesh.py:358-361,471-474;
+//                relocate_local re-interpolation, scanpath.py:243-248).
+//   k_interp_pts same at arbitrary points.
+//   k_deposit    SweptTrackDeposit.load scatter (sources.py:164-172), deterministic.
+//   k_melt       max T and melt-node count (T > T_liquidus) of one field.
+//   k_flush      writes a buffer larger than L2 (benchmark hygiene).
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include "tl_grid.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace tl {
+
+constexpr int kTPB = 512;                  // threads per block of k_pcg
+constexpr int kMaxTab = 4096;              // Gaussian table entries per axis (cells)
+
+// 4-point tet rule (mesh.py:116-128) and the six per-axis fractional offsets a
+// Kuhn-tet quadrature point can take inside its cell: {b, 2b, 3b, a, a+b, a+2b}.
+#define TL_QA ((5.0 + 3.0 * 2.23606797749978969640917366873127623544) / 20.0)
+#define TL_QB ((5.0 - 2.23606797749978969640917366873127623544) / 20.0)
+
+// For permutation index pi (itertools.permutations order) and quadrature point q,
+// the offset index (into the six values) along x, y, z.
+__constant__ int8_t c_qoff[6][4][3] = {
+    {{2, 1, 0}, {5, 1, 0}, {5, 4, 0}, {5, 4, 3}}, {{2, 0, 1}, {5, 0, 1}, {5, 0, 4}, {5, 3, 4}},
+    {{1, 2, 0}, {1, 5, 0}, {4, 5, 0}, {4, 5, 3}}, {{0, 2, 1}, {0, 5, 1}, {0, 5, 4}, {3, 5, 4}},
+    {{1, 0, 2}, {1, 0, 5}, {4, 0, 5}, {4, 3, 5}}, {{0, 1, 2}, {0, 1, 5}, {0, 4, 5}, {3, 4, 5}}};
+// Tets of a cell containing its corner with offset bits (bx | by<<1 | bz<<2): list of
+// (perm index, local vertex index j).  Offsets 0 and 7 lie on all six tets.
+__constant__ int8_t c_inc_n[8] = {6, 2, 2, 2, 2, 2, 2, 6};
+__constant__ int8_t c_inc[8][6][2] = {
+    {{0, 0}, {1, 0}, {2, 0}, {3, 0}, {4, 0}, {5, 0}}, {{0, 1}, {1, 1}},
+    {{2, 1}, {3, 1}}, {{0, 2}, {2, 2}}, {{4, 1}, {5, 1}}, {{1, 2}, {4, 2}},
+    {{3, 2}, {5, 2}}, {{0, 3}, {1, 3}, {2, 3}, {3, 3}, {4, 3}, {5, 3}}};
+
+struct Gauss {
+    double peak, radius, depth, center[3];
+    int on;
+};
+
+struct SolveInfoDev {
+    int iterations, status;
+    double bnorm, rnorm, true_resid;
+};
+
+struct PcgParams {
+    Grid g;
+    double cbase[3];     // kappa V / (6 h_a^2)
+    double mbase;        // (rho c / dt) V / 24
+    // inputs
+    double* T;           // T_old in, solution out (in place)
+    const double* gA;    // Dirichlet values (1-w) gA + w gB, or g_const if gA == nullptr
+    const double* gB;
+    double w, g_const;
+    const double* load;  // dense extra load or nullptr
+    Gauss src;
+    // workspace
+    double *b, *r, *p0, *p1, *q;
+    double* part;        // [4][gridDim]
+    double rtol;
+    int maxiter;
+    SolveInfoDev* info;
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Deterministic block sum of NV values; result valid in thread 0.
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&v)[NV], double* smem) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] = warp_sum(v[k]);
+    if (lane == 0)
+#pragma unroll
+        for (int k = 0; k < NV; ++k) smem[k * 32 + wid] = v[k];
+    __syncthreads();
+    if (wid == 0) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            double s = lane < nw ? smem[k * 32 + lane] : 0.0;
+            v[k] = warp_sum(s);
+        }
+    }
+    __syncthreads();
+}
+
+// Fixed-order sum of the per-block partials written before the last grid.sync.
+// Every block computes bitwise the same totals (commutative butterfly).
+template <int NV>
+__device__ __forceinline__ void grid_sum(const double* part, const int (&slot)[NV], int G,
+                                         double* smem_out) {
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            const double* p = part + slot[k] * G;
+            double s = 0.0;
+            for (int b = lane; b < G; b += 32) s += __ldcg(p + b);
+            s = warp_sum(s);
+            if (lane == 0) smem_out[k] = s;
+        }
+    }
+    __syncthreads();
+}
+
+// Dirichlet value at node p.
+__device__ __forceinline__ double dirichlet_value(const PcgParams& P, int p) {
+    if (P.gA == nullptr) return P.g_const;
+    return __dadd_rn(__dmul_rn(1.0 - P.w, P.gA[p]), __dmul_rn(P.w, P.gB[p]));
+}
+
+// Gaussian nodal load: sum over incident Kuhn tets of
+// (V/24) * (b * S_tet + (a - b) * Q_own), Q = peak * Ex * Ey * Ez from per-axis tables
+// tab[axis][cell * 6 + offset] (peak and V/24 folded into the z table).
+__device__ double gaussian_node(const Grid& g, const double* tx, const double* ty,
+                                const double* tz, int i, int j, int k) {
+    double F = 0.0;
+#pragma unroll
+    for (int bz = 0; bz < 2; ++bz) {
+        const int cz = k - bz;
+        if (cz < 0 || cz >= g.nc[2]) continue;
+#pragma unroll
+        for (int by = 0; by < 2; ++by) {
+            const int cy = j - by;
+            if (cy < 0 || cy >= g.nc[1]) continue;
+#pragma unroll
+            for (int bx = 0; bx < 2; ++bx) {
+                const int cx = i - bx;
+                if (cx < 0 || cx >= g.nc[0]) continue;
+                const double* ex = tx + cx * 6;
+                const double* ey = ty + cy * 6;
+                const double* ez = tz + cz * 6;
+                const int off = bx | (by << 1) | (bz << 2);
+                const int ninc = c_inc_n[off];
+                for (int t = 0; t < ninc; ++t) {
+                    const int pi = c_inc[off][t][0], jv = c_inc[off][t][1];
+                    double S = 0.0, Qj = 0.0;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const double Q = ex[c_qoff[pi][q][0]] * ey[c_qoff[pi][q][1]] * ez[c_qoff[pi][q][2]];
+                        S += Q;
+                        Qj = (q == jv) ? Q : Qj;
+                    }
+                    F += TL_QB * S + (TL_QA - TL_QB) * Qj;
+                }
+            }
+        }
+    }
+    return F;
+}
+
+__device__ inline void build_gauss_tables(const Grid& g, const Gauss& s, double* tx, double* ty,
+                                          double* tz) {
+    const double fr[6] = {TL_QB, 2.0 * TL_QB, 3.0 * TL_QB, TL_QA, TL_QA + TL_QB, TL_QA + 2.0 * TL_QB};
+    const double V24 = g.h[0] * g.h[1] * g.h[2] / 24.0;
+    const int tot = 6 * (g.nc[0] + g.nc[1] + g.nc[2]);
+    for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+        int a, rem = e;
+        if (rem < 6 * g.nc[0]) a = 0;
+        else if ((rem -= 6 * g.nc[0]) < 6 * g.nc[1]) a = 1;
+        else { rem -= 6 * g.nc[1]; a = 2; }
+        const int c = rem / 6, o = rem % 6;
+        const double x = node_coord(g, a, c) + fr[o] * g.h[a];
+        const double sc = (a == 2) ? s.depth : s.radius;
+        const double t = (x - s.center[a]) / sc;
+        double v = exp(-3.0 * (t * t));
+        double* dst = a == 0 ? tx : (a == 1 ? ty : tz);
+        if (a == 2) v *= s.peak * V24;
+        dst[rem] = v;
+    }
+}
+
+// Value of z = M r at node q (Jacobi), from its axis indices.
+__device__ __forceinline__ int class_of(const Grid& g, int i, int j, int k) {
+    return axis_class(i, g.nc[0]) + 3 * axis_class(j, g.nc[1]) + 9 * axis_class(k, g.nc[2]);
+}
+
+// y = (A_c v)_p for a free node p, v given by functor V(q, cls_q).
+template <class F>
+__device__ __forceinline__ double apply_free(const Grid& g, const ClassTable& T, int p, int i, int j,
+                                             int k, int cls, double vp, F V) {
+    double y = T.diag[cls] * vp;
+    double s = 0.0;
+    const int sy = g.NX, sz = g.NX * g.NY;
+    // x neighbours
+    {
+        const double c = T.c[0][cls];
+        double t = 0.0;
+        if (i > 0) { int qc = cls - axis_class(i, g.nc[0]) + axis_class(i - 1, g.nc[0]); t += T.nd[qc] * V(p - 1, qc); }
+        if (i < g.nc[0]) { int qc = cls - axis_class(i, g.nc[0]) + axis_class(i + 1, g.nc[0]); t += T.nd[qc] * V(p + 1, qc); }
+        s += c * t;
+    }
+    {
+        const double c = T.c[1][cls];
+        double t = 0.0;
+        if (j > 0) { int qc = cls + 3 * (axis_class(j - 1, g.nc[1]) - axis_class(j, g.nc[1])); t += T.nd[qc] * V(p - sy, qc); }
+        if (j < g.nc[1]) { int qc = cls + 3 * (axis_class(j + 1, g.nc[1]) - axis_class(j, g.nc[1])); t += T.nd[qc] * V(p + sy, qc); }
+        s += c * t;
+    }
+    {
+        const double c = T.c[2][cls];
+        double t = 0.0;
+        if (k > 0) { int qc = cls + 9 * (axis_class(k - 1, g.nc[2]) - axis_class(k, g.nc[2])); t += T.nd[qc] * V(p - sz, qc); }
+        if (k < g.nc[2]) { int qc = cls + 9 * (axis_class(k + 1, g.nc[2]) - axis_class(k, g.nc[2])); t += T.nd[qc] * V(p + sz, qc); }
+        s += c * t;
+    }
+    return y - s;
+}
+
+// ---------------------------------------------------------------------------------
+// Persistent cooperative PCG.  grid.sync() separates the phases:
+//   phase 0: b, r = b, x = 0, partial ||b||^2 and r.z             | sync
+//   loop:    test ||r|| < rtol ||b||  (scipy: top of each iteration)
+//            phase A: p = z (first) or beta p + z; q = A_c p; p.q | sync
+//            phase B: x += alpha p; r -= alpha q; r.z, r.r        | sync
+//   final:   ||A_c x - b||, non-finite check                      | sync
+//            x_D = g, info
+// ---------------------------------------------------------------------------------
+template <bool GAUSS>
+__global__ void __launch_bounds__(kTPB) k_pcg(PcgParams P) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ ClassTable T;
+    __shared__ double red[4 * 32];
+    __shared__ double tot[4];
+    extern __shared__ double gtab[];
+    const Grid& g = P.g;
+    build_class_table(T, threadIdx.x, P.mbase, P.cbase, g.dkind);
+    double *tx = gtab, *ty = gtab + 6 * g.nc[0], *tz = ty + 6 * g.nc[1];
+    if (GAUSS) build_gauss_tables(g, P.src, tx, ty, tz);
+    __syncthreads();
+
+    const int G = gridDim.x;
+    const int per = (g.n + G - 1) / G;
+    const int beg = blockIdx.x * per;
+    const int end = min(g.n, beg + per);
+
+    // ---- phase 0: constrained RHS (fem.py:169-191 + 89-105) ----
+    double acc[2] = {0.0, 0.0};
+    for (int p = beg + threadIdx.x; p < end; p += kTPB) {
+        int i, j, k;
+        decode(g, p, i, j, k);
+        const int cls = class_of(g, i, j, k);
+        double bv;
+        if (T.nd[cls] == 0.0) {
+            bv = dirichlet_value(P, p);
+        } else {
+            bv = T.mass[cls] * P.T[p];
+            if (P.load) bv += P.load[p];
+            if (GAUSS) bv += gaussian_node(g, tx, ty, tz, i, j, k);
+            // lift: b_p -= sum_{q in D} A_pq g_q,  A_pq = -c_pq
+            const int sy = g.NX, sz = g.NX * g.NY;
+            double lift = 0.0;
+            if (i > 0 && T.nd[cls - axis_class(i, g.nc[0]) + axis_class(i - 1, g.nc[0])] == 0.0) lift += T.c[0][cls] * dirichlet_value(P, p - 1);
+            if (i < g.nc[0] && T.nd[cls - axis_class(i, g.nc[0]) + axis_class(i + 1, g.nc[0])] == 0.0) lift += T.c[0][cls] * dirichlet_value(P, p + 1);
+            if (j > 0 && T.nd[cls + 3 * (axis_class(j - 1, g.nc[1]) - axis_class(j, g.nc[1]))] == 0.0) lift += T.c[1][cls] * dirichlet_value(P, p - sy);
+            if (j < g.nc[1] && T.nd[cls + 3 * (axis_class(j + 1, g.nc[1]) - axis_class(j, g.nc[1]))] == 0.0) lift += T.c[1][cls] * dirichlet_value(P, p + sy);
+            if (k > 0 && T.nd[cls + 9 * (axis_class(k - 1, g.nc[2]) - axis_class(k, g.nc[2]))] == 0.0) lift += T.c[2][cls] * dirichlet_value(P, p - sz);
+            if (k < g.nc[2] && T.nd[cls + 9 * (axis_class(k + 1, g.nc[2]) - axis_class(k, g.nc[2]))] == 0.0) lift += T.c[2][cls] * dirichlet_value(P, p + sz);
+            bv += lift;
+        }
+        P.b[p] = bv;
+        P.r[p] = bv;
+        P.T[p] = 0.0;
+        const double z = __dmul_rn(T.invd[cls], bv);
+        acc[0] += bv * bv;
+        acc[1] += bv * z;
+    }
+    block_sum<2>(acc, red);
+    if (threadIdx.x == 0) { P.part[0 * G + blockIdx.x] = acc[0]; P.part[1 * G + blockIdx.x] = acc[1]; }
+    grid.sync();
+    {
+        const int s[2] = {0, 1};
+        grid_sum<2>(P.part, s, G, tot);
+    }
+    const double bb = tot[0];
+    double rz = tot[1];
+    const double bnorm = sqrt(bb);
+    const double atol = P.rtol * bnorm;
+    double rnorm = bnorm;
+    int it = 0, status = 0;
+    double rho_prev = 1.0;
+    double* pold = P.p0;
+    double* pnew = P.p1;
+
+    if (bb == 0.0) {
+        status = 0;   // fem.py:275-276: zero solution
+    } else {
+        while (true) {
+            if (rnorm < atol) { status = 0; break; }
+            if (!isfinite(rnorm)) { status = 3; break; }
+            if (it >= P.maxiter) { status = 1; break; }
+            const double rho = rz;
+            const double beta = it > 0 ? rho / rho_prev : 0.0;
+            const bool first = it == 0;
+            // ---- phase A ----
+            double pq[1] = {0.0};
+            for (int p = beg + threadIdx.x; p < end; p += kTPB) {
+                int i, j, k;
+                decode(g, p, i, j, k);
+                const int cls = class_of(g, i, j, k);
+                auto pn = [&](int q, int qc) -> double {
+                    const double z = __dmul_rn(T.invd[qc], P.r[q]);
+                    return first ? z : __dadd_rn(__dmul_rn(beta, pold[q]), z);
+                };
+                const double pp = pn(p, cls);
+                double qv;
+                if (T.nd[cls] == 0.0) qv = pp;
+                else qv = apply_free(g, T, p, i, j, k, cls, pp, pn);
+                pnew[p] = pp;
+                P.q[p] = qv;
+                pq[0] += pp * qv;
+            }
+            block_sum<1>(pq, red);
+            if (threadIdx.x == 0) P.part[2 * G + blockIdx.x] = pq[0];
+            grid.sync();
+            {
+                const int s[1] = {2};
+                grid_sum<1>(P.part, s, G, tot);
+            }
+            const double alpha = rho / tot[0];
+            // ---- phase B ----
+            double a2[2] = {0.0, 0.0};
+            for (int p = beg + threadIdx.x; p < end; p += kTPB) {
+                int i, j, k;
+                decode(g, p, i, j, k);
+                const int cls = class_of(g, i, j, k);
+                const double pp = pnew[p];
+                const double x = __dadd_rn(P.T[p], __dmul_rn(alpha, pp));
+                const double rv = __dsub_rn(P.r[p], __dmul_rn(alpha, P.q[p]));
+                P.T[p] = x;
+                P.r[p] = rv;
+                const double z = __dmul_rn(T.invd[cls], rv);
+                a2[0] += rv * z;
+                a2[1] += rv * rv;
+            }
+            block_sum<2>(a2, red);
+            if (threadIdx.x == 0) { P.part[0 * G + blockIdx.x] = a2[0]; P.part[1 * G + blockIdx.x] = a2[1]; }
+            grid.sync();
+            {
+                const int s[2] = {0, 1};
+                grid_sum<2>(P.part, s, G, tot);
+            }
+            rz = tot[0];
+            rnorm = sqrt(tot[1]);
+            rho_prev = rho;
+            double* t = pold; pold = pnew; pnew = t;
+            ++it;
+        }
+    }
+
+    // ---- true residual ||A_c x - b|| / ||b|| (fem.py:286) and finite check ----
+    double res[2] = {0.0, 0.0};
+    for (int p = beg + threadIdx.x; p < end; p += kTPB) {
+        int i, j, k;
+        decode(g, p, i, j, k);
+        const int cls = class_of(g, i, j, k);
+        const double xp = P.T[p];
+        double ax;
+        if (T.nd[cls] == 0.0) ax = xp;
+        else ax = apply_free(g, T, p, i, j, k, cls, xp, [&](int q, int) { return P.T[q]; });
+        const double d = ax - P.b[p];
+        res[0] += d * d;
+        res[1] += isfinite(xp) ? 0.0 : 1.0;
+    }
+    block_sum<2>(res, red);
+    if (threadIdx.x == 0) { P.part[0 * G + blockIdx.x] = res[0]; P.part[3 * G + blockIdx.x] = res[1]; }
+    grid.sync();
+    {
+        const int s[2] = {0, 3};
+        grid_sum<2>(P.part, s, G, tot);
+    }
+    const double tres = bnorm > 0.0 ? sqrt(tot[0]) / bnorm : 0.0;
+    // ---- re-impose Dirichlet values (fem.py:289-290): x_D = g = b_D ----
+    for (int p = beg + threadIdx.x; p < end; p += kTPB) {
+        int i, j, k;
+        decode(g, p, i, j, k);
+        const int cls = class_of(g, i, j, k);
+        if (T.nd[cls] == 0.0) P.T[p] = P.b[p];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (status == 0 && tot[1] > 0.0) status = 3;
+        if (status == 0 && (!isfinite(tres) || tres > 1e2 * P.rtol)) status = 2;
+        P.info->iterations = (status == 1) ? P.maxiter : it;
+        P.info->status = status;
+        P.info->bnorm = bnorm;
+        P.info->rnorm = rnorm;
+        P.info->true_resid = tres;
+    }
+}
+
+// ---------------------------------------------------------------------------------
+// Kuhn-P1 location in the global grid (mesh.py:308-339): cell by floor((x-lo)/h)
+// clipped; tet by the descending order of the in-cell fractions.
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ double p1_eval(const Grid& G, const double* v, double x, double y, double z) {
+    const double pt[3] = {x, y, z};
+    int c[3];
+    double xi[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        int ci = (int)floor((pt[a] - G.lo0[a]) / G.h[a]);
+        ci = ci < 0 ? 0 : (ci > G.nc[a] - 1 ? G.nc[a] - 1 : ci);
+        c[a] = ci;
+        xi[a] = (pt[a] - node_coord(G, a, ci)) / G.h[a];
+    }
+    // sort axes by xi descending (stable on ties)
+    int o0 = 0, o1 = 1, o2 = 2;
+    if (xi[o1] > xi[o0]) { int t = o0; o0 = o1; o1 = t; }
+    if (xi[o2] > xi[o1]) { int t = o1; o1 = o2; o2 = t; }
+    if (xi[o1] > xi[o0]) { int t = o0; o0 = o1; o1 = t; }
+    const int st[3] = {1, G.NX, G.NX * G.NY};
+    const int n0 = c[0] + G.NX * (c[1] + G.NY * c[2]);
+    const int n1 = n0 + st[o0];
+    const int n2 = n1 + st[o1];
+    const int n3 = n2 + st[o2];
+    const double w0 = 1.0 - xi[o0], w1 = xi[o0] - xi[o1], w2 = xi[o1] - xi[o2], w3 = xi[o2];
+    return w0 * v[n0] + w1 * v[n1] + w2 * v[n2] + w3 * v[n3];
+}
+
+// mode 0: all target nodes -> out_all (and gamma nodes also -> out_gamma if non-null)
+// mode 1: gamma nodes only -> out_gamma
+__global__ void k_interp(Grid G, const double* __restrict__ v, Grid L, int mode, double* out_all,
+                         double* out_gamma) {
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < L.n; p += gridDim.x * blockDim.x) {
+        int i, j, k;
+        decode(L, p, i, j, k);
+        const bool gam = (k == 0) || i == 0 || i == L.nc[0] || j == 0 || j == L.nc[1];
+        if (mode == 1 && !gam) continue;
+        const double val = p1_eval(G, v, node_coord(L, 0, i), node_coord(L, 1, j), node_coord(L, 2, k));
+        if (mode == 0) out_all[p] = val;
+        if (gam && out_gamma) out_gamma[p] = val;
+    }
+}
+
+__global__ void k_interp_pts(Grid G, const double* __restrict__ v, const double* __restrict__ pts,
+                             int64_t np, double* out) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < np; e += (int64_t)gridDim.x * blockDim.x)
+        out[e] = p1_eval(G, v, pts[3 * e], pts[3 * e + 1], pts[3 * e + 2]);
+}
+
+// ---------------------------------------------------------------------------------
+// Deposit: one block.  Zero the nodes written last call, then scatter the new
+// samples with barycentric weights and merge repeated nodes in sample order
+// (np.add.at order), writing load[node] = sum.
+// ---------------------------------------------------------------------------------
+constexpr int kDepMax = 2048;   // contributions per call (samples * 4)
+
+__global__ void __launch_bounds__(256) k_deposit(Grid G, const double* __restrict__ pts,
+                                                 const double* __restrict__ pw, int count,
+                                                 double* load, int* prev_nodes, int* prev_count) {
+    __shared__ int s_node[kDepMax];
+    __shared__ double s_val[kDepMax];
+    const int np = *prev_count;
+    for (int e = threadIdx.x; e < np; e += blockDim.x) load[prev_nodes[e]] = 0.0;
+    __syncthreads();
+    const int nc = min(count * 4, kDepMax);
+    for (int s = threadIdx.x; s < count && s * 4 < kDepMax; s += blockDim.x) {
+        const double pt[3] = {pts[3 * s], pts[3 * s + 1], pts[3 * s + 2]};
+        int c[3];
+        double xi[3];
+        for (int a = 0; a < 3; ++a) {
+            int ci = (int)floor((pt[a] - G.lo0[a]) / G.h[a]);
+            ci = ci < 0 ? 0 : (ci > G.nc[a] - 1 ? G.nc[a] - 1 : ci);
+            c[a] = ci;
+            xi[a] = (pt[a] - node_coord(G, a, ci)) / G.h[a];
+        }
+        int o0 = 0, o1 = 1, o2 = 2;
+        if (xi[o1] > xi[o0]) { int t = o0; o0 = o1; o1 = t; }
+        if (xi[o2] > xi[o1]) { int t = o1; o1 = o2; o2 = t; }
+        if (xi[o1] > xi[o0]) { int t = o0; o0 = o1; o1 = t; }
+        const int st[3] = {1, G.NX, G.NX * G.NY};
+        const int n0 = c[0] + G.NX * (c[1] + G.NY * c[2]);
+        s_node[4 * s + 0] = n0;
+        s_node[4 * s + 1] = n0 + st[o0];
+        s_node[4 * s + 2] = n0 + st[o0] + st[o1];
+        s_node[4 * s + 3] = n0 + st[o0] + st[o1] + st[o2];
+        const double P = pw[s];
+        s_val[4 * s + 0] = P * (1.0 - xi[o0]);
+        s_val[4 * s + 1] = P * (xi[o0] - xi[o1]);
+        s_val[4 * s + 2] = P * (xi[o1] - xi[o2]);
+        s_val[4 * s + 3] = P * xi[o2];
+    }
+    __syncthreads();
+    // first occurrences write the in-order sum
+    __shared__ int s_cnt;
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    for (int e = threadIdx.x; e < nc; e += blockDim.x) {
+        const int nd = s_node[e];
+        bool first = true;
+        for (int f = 0; f < e; ++f)
+            if (s_node[f] == nd) { first = false; break; }
+        if (!first) continue;
+        double sum = 0.0;
+        for (int f = e; f < nc; ++f)
+            if (s_node[f] == nd) sum += s_val[f];
+        load[nd] = sum;
+        const int slot = atomicAdd(&s_cnt, 1);
+        prev_nodes[slot] = nd;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *prev_count = s_cnt;
+}
+
+// max and count(T > T_l) of a field: per-block partials, finished by block 0 of a
+// second launch (deterministic).
+__global__ void k_melt_partial(const double* __restrict__ v, int n, double Tl, double* part) {
+    __shared__ double smax[32], scnt[32];
+    double m = -1e300, c = 0.0;
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+        const double t = v[p];
+        m = fmax(m, t);
+        c += t > Tl ? 1.0 : 0.0;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+        c += __shfl_xor_sync(0xffffffffu, c, o);
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) { smax[wid] = m; scnt[wid] = c; }
+    __syncthreads();
+    if (wid == 0) {
+        const int nw = blockDim.x >> 5;
+        m = lane < nw ? smax[lane] : -1e300;
+        c = lane < nw ? scnt[lane] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) {
+            m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+            c += __shfl_xor_sync(0xffffffffu, c, o);
+        }
+        if (lane == 0) { part[2 * blockIdx.x] = m; part[2 * blockIdx.x + 1] = c; }
+    }
+}
+
+__global__ void k_melt_final(const double* part, int nb, double* out_max, double* out_cnt) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double m = -1e300, c = 0.0;
+        for (int b = 0; b < nb; ++b) { m = fmax(m, part[2 * b]); c += part[2 * b + 1]; }
+        *out_max = m;
+        *out_cnt = c;
+    }
+}
+
+__global__ void k_flush(double* buf, size_t n, double v) {
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x)
+        buf[e] = v;
+}
+
+__global__ void k_copy(const double* __restrict__ a, double* __restrict__ b, int n) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) b[e] = a[e];
+}
+
+__global__ void k_fill(double* a, int n, double v) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) a[e] = v;
+}
+
+}  // namespace tl

@@ -1,0 +1,160 @@
+"""Fields, solver settings and the implicit step on the device.
+
+``FieldState`` / ``uniform_field`` / ``SolverSettings`` / ``BoundarySpec`` keep
+the reference's names and checks (``lpbfsim/fem.py:36-76,108-126``).
+``step_backward_euler`` is seam 3 of the drop-in (``lpbfsim/fem.py:307-355``):
+for the linear problems the device represents (constant material, no latent
+heat, no radiation, Robin inactive) it performs the reference's single Picard
+pass — assemble + constrain + Jacobi-PCG + residual check + Dirichlet
+re-imposition — as one cooperative kernel.  Anything else raises
+``UnsupportedOnDevice`` rather than falling back to a CPU path.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from .config import SolverSettings
+from .control import ThermalBC, material_constants
+from .errors import SolverError, UnsupportedOnDevice
+from .grid import BOTTOM, TOP, StructuredGrid
+
+__all__ = ["FieldState", "uniform_field", "SolverSettings", "BoundarySpec", "GaussianSource",
+           "step_backward_euler", "device_rtol"]
+
+
+@dataclass(frozen=True)
+class FieldState:
+    """Nodal temperature field bound to a grid at one time (``fem.py:36-56``)."""
+
+    mesh: object
+    values: np.ndarray
+    time: float
+
+    def __post_init__(self):
+        v = np.asarray(self.values, dtype=float)
+        if v.shape != (self.mesh.n_nodes,):
+            raise SolverError(f"field has {v.shape} values for a mesh with {self.mesh.n_nodes} nodes")
+        if not np.all(np.isfinite(v)):
+            raise SolverError("field contains non-finite values")
+        v.setflags(write=False)
+        object.__setattr__(self, "values", v)
+
+    def with_values(self, values, time: float | None = None) -> "FieldState":
+        return FieldState(self.mesh, values, self.time if time is None else time)
+
+
+def uniform_field(mesh, value: float, time: float = 0.0) -> FieldState:
+    return FieldState(mesh, np.full(mesh.n_nodes, float(value)), time)
+
+
+@dataclass(frozen=True)
+class BoundarySpec:
+    """Boundary data for one solve (``fem.py:108-126``)."""
+
+    bc: ThermalBC
+    robin_tags: tuple = (TOP,)
+    radiation: bool = False
+    dirichlet_nodes: np.ndarray = field(default_factory=lambda: np.empty(0, dtype=np.int64))
+    dirichlet_values: np.ndarray | float = 0.0
+
+    def dirichlet_array(self) -> np.ndarray:
+        vals = np.broadcast_to(np.asarray(self.dirichlet_values, dtype=float),
+                               np.shape(self.dirichlet_nodes))
+        return np.asarray(vals, dtype=float)
+
+
+@dataclass(frozen=True)
+class GaussianSource:
+    """``gaussian_source_3d`` bound to a centre (``sources.py:67-77``).
+
+    The reference passes the source to ``assemble_system`` as an opaque
+    callable; the device evaluates this one analytically at the Kuhn-tet
+    quadrature points instead.  Calling it pointwise is still supported.
+    """
+
+    beam: object
+    center: tuple
+
+    def __call__(self, points):
+        p = np.atleast_2d(np.asarray(points, dtype=float))
+        c = np.asarray(self.center, dtype=float)
+        b = self.beam
+        ex = 3.0 * ((p[:, 0] - c[0]) / b.radius) ** 2
+        ey = 3.0 * ((p[:, 1] - c[1]) / b.radius) ** 2
+        ez = 3.0 * ((p[:, 2] - c[2]) / b.depth) ** 2
+        return b.gaussian_peak * np.exp(-(ex + ey + ez))
+
+    def device_args(self):
+        b = self.beam
+        return (b.gaussian_peak, b.radius, b.depth, tuple(float(v) for v in self.center))
+
+
+def device_rtol(settings: SolverSettings) -> float:
+    """CG tolerance the device uses for a SolverSettings.
+
+    ``cg`` uses ``linear_tol`` exactly as ``fem.py:285``.  The reference's
+    ``direct`` (sparse LU, ``fem.py:277-281``) has no device counterpart; it is
+    served by CG at 1e-14, which lands within ~1e-13 of the LU solution on these
+    mass-dominated systems.
+    """
+    return settings.linear_tol if settings.linear_solver == "cg" else min(settings.linear_tol, 1e-14)
+
+
+def check_linear_problem(mat, bounds: BoundarySpec | None, latent: bool):
+    if not getattr(mat, "is_constant", False):
+        raise UnsupportedOnDevice("temperature-dependent conductivity/capacity tables are not on "
+                                  "the device path (SURVEY.md §8 f, row 1)")
+    if latent and getattr(mat, "chi", 0.0) > 0.0:
+        raise UnsupportedOnDevice("latent heat (chi > 0) is not on the device path")
+    if bounds is not None:
+        bc = bounds.bc
+        if bounds.robin_tags and bc.h_conv > 0:
+            raise UnsupportedOnDevice("Robin convection (h_conv > 0) is not on the device path")
+        if bounds.robin_tags and bounds.radiation and bc.emissivity > 0:
+            raise UnsupportedOnDevice("radiation (emissivity > 0) is not on the device path")
+
+
+def _dirichlet_kind(mesh: StructuredGrid, nodes: np.ndarray) -> int:
+    nodes = np.asarray(nodes, dtype=np.int64)
+    if np.array_equal(nodes, mesh.nodes_on(BOTTOM)):
+        return N.TL_DIRICHLET_BOTTOM
+    if np.array_equal(nodes, np.nonzero(mesh.gamma_mask())[0]):
+        return N.TL_DIRICHLET_GAMMA
+    raise UnsupportedOnDevice("the device represents the bottom-face or interface Dirichlet sets only")
+
+
+def step_backward_euler(state: FieldState, dt: float, mat, source, bounds: BoundarySpec,
+                        settings: SolverSettings, latent: bool = False, latent_mask=None,
+                        extra_load=None, extra_mass_coeff=None, stats=None) -> FieldState:
+    """One implicit step (``fem.py:307-355``) for a linear problem, on the device."""
+    from .ops import raise_for, step
+    if dt <= 0:
+        raise SolverError("time step must be positive")
+    if latent_mask is not None or extra_mass_coeff is not None:
+        raise UnsupportedOnDevice("latent masks / overlap mass terms are not on the device path")
+    check_linear_problem(mat, bounds, latent)
+    if source is not None and not isinstance(source, GaussianSource):
+        raise UnsupportedOnDevice("the device evaluates GaussianSource objects, not opaque callables")
+    mesh = state.mesh
+    kind = _dirichlet_kind(mesh, bounds.dirichlet_nodes)
+    kappa, rho_c = material_constants(mat)
+    g = np.zeros(mesh.n_nodes)
+    g[np.asarray(bounds.dirichlet_nodes, dtype=np.int64)] = bounds.dirichlet_array()
+    timer = stats.timer("assembly") if stats is not None else None
+    if timer is not None:
+        timer.__enter__()
+    try:
+        x, info = step(mesh, kappa, rho_c, dt, kind, state.values, g=g, load=extra_load,
+                       gaussian=source.device_args() if source is not None else None,
+                       rtol=device_rtol(settings))
+    finally:
+        if timer is not None:
+            timer.__exit__(None, None, None)
+    raise_for(info)
+    if stats is not None:
+        stats.count("picard_iterations")
+    return state.with_values(x, state.time + dt)

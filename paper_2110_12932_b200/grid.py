@@ -1,0 +1,121 @@
+"""Lightweight structured-mesh stand-in for the reference ``Mesh``.
+
+The reference ``Mesh`` (``lpbfsim/mesh.py:154-385``) eagerly stores node
+coordinates and the Kuhn tet connectivity; at cfg4 scale those arrays are
+4.8 GB + 39 GB.  ``StructuredGrid`` keeps the attributes the two-level API
+reads (``box``, ``dim``, ``ncells``, ``spacing``, ``n_nodes``, ``h``,
+``coords``, ``translated``, ``interpolate``) and derives everything else from
+the lattice.  Node order is the reference's (x fastest,
+``lpbfsim/mesh.py:406-409``); coordinates are linspace of the construction box
+plus the accumulated offset (``lpbfsim/mesh.py:163-165,372``).
+"""
+
+from __future__ import annotations
+
+from functools import cached_property
+
+import numpy as np
+
+from .control import Box, LocalPlacement, structured_ncells
+from .errors import MeshError
+
+BOTTOM, TOP, LATERAL = 0, 1, 2
+
+
+class StructuredGrid:
+    """Uniform lattice of a box, Kuhn-subdivided implicitly (6 tets per cell)."""
+
+    def __init__(self, placement: LocalPlacement):
+        self._placement = placement
+        self.box = placement.box
+        self.dim = 3
+        self.ncells = placement.ncells
+        self.spacing = self.box.lengths / self.ncells
+
+    # -- reference Mesh attributes --------------------------------------------
+
+    @property
+    def placement(self) -> LocalPlacement:
+        return self._placement
+
+    @property
+    def shape(self) -> tuple:
+        n = self.ncells
+        return (int(n[2]) + 1, int(n[1]) + 1, int(n[0]) + 1)
+
+    @property
+    def n_nodes(self) -> int:
+        return int(np.prod(self.shape))
+
+    @property
+    def n_elems(self) -> int:
+        return 6 * int(np.prod(self.ncells))
+
+    @property
+    def h(self) -> float:
+        return float(self.spacing.max())
+
+    @property
+    def _offset(self) -> np.ndarray:
+        return self._placement.offset
+
+    def axis(self, a: int) -> np.ndarray:
+        return self._placement.axis_coords(a)
+
+    @cached_property
+    def coords(self) -> np.ndarray:
+        """(n_nodes, 3) node coordinates, materialised on first use."""
+        x, y, z = self.axis(0), self.axis(1), self.axis(2)
+        Z, Y, X = np.meshgrid(z, y, x, indexing="ij")
+        out = np.stack([X.ravel(), Y.ravel(), Z.ravel()], axis=1)
+        out.setflags(write=False)
+        return out
+
+    def nodes_on(self, *tags: int) -> np.ndarray:
+        """Sorted node ids of boundary facets with the given tags (``mesh.py:226-230``)."""
+        NZ, NY, NX = self.shape
+        m = np.zeros(self.shape, dtype=bool)
+        if BOTTOM in tags:
+            m[0] = True
+        if TOP in tags:
+            m[-1] = True
+        if LATERAL in tags:
+            m[:, 0, :] = m[:, -1, :] = True
+            m[:, :, 0] = m[:, :, -1] = True
+        return np.nonzero(m.ravel())[0]
+
+    def gamma_mask(self) -> np.ndarray:
+        """Flat bool mask of the interface (trace) nodes: lateral + bottom facets."""
+        m = np.zeros(self.shape, dtype=bool)
+        m[0] = True
+        m[:, 0, :] = m[:, -1, :] = True
+        m[:, :, 0] = m[:, :, -1] = True
+        return m.ravel()
+
+    def translated(self, offset, within: Box | None = None) -> "StructuredGrid":
+        return StructuredGrid(self._placement.translated(offset, within))
+
+    def interpolate(self, values: np.ndarray, points: np.ndarray) -> np.ndarray:
+        """P1 interpolant at points, evaluated on the device (``mesh.py:358-361``)."""
+        from .ops import interpolate_points
+        return interpolate_points(self, values, points)
+
+    def desc(self):
+        from ._native import GridDesc
+        p = self._placement
+        return GridDesc.make(p.box0.lo, p.box0.hi, p.ncells, p.offset)
+
+    def same_lattice(self, other: "StructuredGrid") -> bool:
+        return (np.array_equal(self.ncells, other.ncells)
+                and self._placement.box0 == other._placement.box0
+                and np.array_equal(self._offset, other._offset))
+
+    def __repr__(self):
+        return f"StructuredGrid(box={self.box}, ncells={self.ncells.tolist()})"
+
+
+def build_structured_grid(box: Box, h) -> StructuredGrid:
+    """``build_structured_mesh`` for 3D boxes (``lpbfsim/mesh.py:388-439``)."""
+    if box.dim != 3:
+        raise MeshError("the device path supports 3D boxes only")
+    return StructuredGrid(LocalPlacement(box, structured_ncells(box, h)))

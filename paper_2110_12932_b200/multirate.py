@@ -1,0 +1,294 @@
+"""Multirate / uniform two-level drivers — the device-resident hot loop.
+
+Drop-in for ``lpbfsim.multirate`` (``lpbfsim/multirate.py``):
+
+- ``run_spacetime(problem, schedule, local_mesh, T0, path, policy, stats, recorder)``
+  (``:167-191``) and ``run_space(problem, dt, n_steps, ...)`` (``:194-217``) keep
+  their signatures, recorder protocol (kinds ``initial``/``predictor``/``micro``/
+  ``macro`` at the same points) and ``RunStats`` counters, but run the whole
+  schedule as one device-resident ``tl_run``: fields never leave the GPU unless a
+  recorder asks for them.
+- ``macro_step`` (``:105-164``) and ``predictor_global`` / ``interpolate_trace``
+  keep the reference's step-level behaviour on top of the seam-2 solves.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import time
+
+import numpy as np
+
+from . import _native as N
+from .control import LocalPlacement, MacroSchedule
+from .errors import CouplingError, NonConvergence, SolverError
+from .fem import FieldState, device_rtol
+from .grid import StructuredGrid
+from .ops import raise_for
+from .schedule import Plan, plan_space, plan_spacetime
+from .twolevel import (
+    TwoLevelProblem, TwoLevelState, extract_interface, initial_state, solve_global, solve_local,
+    two_level_iterate,
+)
+
+__all__ = ["MacroSchedule", "DeviceRun", "run_spacetime", "run_space", "macro_step",
+           "predictor_global", "interpolate_trace"]
+
+
+class DeviceRun:
+    """Owns one ``tl_run``: both grids' fields and solver workspace on the GPU."""
+
+    def __init__(self, problem: TwoLevelProblem, local_mesh: StructuredGrid):
+        problem.check_device_supported()
+        self.problem = problem
+        self.local_mesh = local_mesh
+        kappa, rcg, rcl = problem.constants()
+        beam = problem.beam
+        desc = N.RunDesc()
+        desc.global_grid = problem.global_mesh.desc()
+        desc.local_grid = local_mesh.desc()
+        desc.kappa = kappa
+        desc.rho_c_global = rcg
+        desc.rho_c_local = rcl
+        desc.T_buildplate = problem.bc.T_buildplate
+        if beam is not None:
+            desc.beam_peak, desc.beam_radius, desc.beam_depth = beam.gaussian_peak, beam.radius, beam.depth
+        desc.rtol = device_rtol(problem.solver)
+        desc.maxiter_factor = 20                 # fem.py:285
+        desc.max_micro = 64
+        desc.max_deposit = 512
+        desc.device = problem.device
+        self._h = C.c_void_p()
+        N.check(N.lib().tl_run_create(C.byref(desc), C.byref(self._h)), "tl_run_create")
+        self.n_global = problem.global_mesh.n_nodes
+        self.n_local = local_mesh.n_nodes
+        self.solve_log: list = []
+
+    # -- lifecycle -----------------------------------------------------------------
+
+    def close(self):
+        if self._h:
+            N.lib().tl_run_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+        return False
+
+    # -- state -----------------------------------------------------------------------
+
+    def initial(self, T0: FieldState):
+        v = np.asarray(T0.values)
+        if v.size and np.all(v == v.flat[0]):
+            N.check(N.lib().tl_run_initial(self._h, float(v.flat[0])), "tl_run_initial")
+        else:
+            a = np.ascontiguousarray(v, dtype=np.float64)
+            N.check(N.lib().tl_run_set_global(self._h, N.dptr(a), a.size), "tl_run_set_global")
+
+    def field(self, which: int) -> np.ndarray:
+        n = self.n_global if which == 0 else self.n_local
+        out = np.empty(n)
+        N.check(N.lib().tl_run_get_field(self._h, which, N.dptr(out), n), "tl_run_get_field")
+        return out
+
+    def snapshot(self, which: int, index: int = 0) -> np.ndarray:
+        n = self.n_global if which == 0 else self.n_local
+        out = np.empty(n)
+        N.check(N.lib().tl_run_get_snapshot(self._h, which, index, N.dptr(out), n), "snapshot")
+        return out
+
+    def run(self, plan: Plan):
+        macro = np.ascontiguousarray(plan.macro)
+        micro = np.ascontiguousarray(plan.micro)
+        pts = np.ascontiguousarray(plan.dep_points.reshape(-1), dtype=np.float64)
+        pw = np.ascontiguousarray(plan.dep_power, dtype=np.float64)
+        N.check(N.lib().tl_run_macro_steps(
+            self._h, macro.ctypes.data_as(C.c_void_p), len(macro), micro.ctypes.data_as(C.c_void_p),
+            len(micro), N.dptr(pts), N.dptr(pw), len(pw)), "tl_run_macro_steps")
+
+    def sync(self):
+        N.check(N.lib().tl_run_sync(self._h), "tl_run_sync")
+
+    def take_info(self) -> list:
+        out = []
+        buf = (N.SolveInfo * 4096)()
+        cnt = C.c_int32()
+        while True:
+            N.check(N.lib().tl_run_take_info(self._h, buf, 4096, C.byref(cnt)), "take_info")
+            out.extend({"iterations": buf[e].iterations, "status": buf[e].status,
+                        "bnorm": buf[e].bnorm, "rnorm": buf[e].rnorm,
+                        "true_resid": buf[e].true_resid} for e in range(cnt.value))
+            if cnt.value < 4096:
+                break
+        self.solve_log.extend(out)
+        return out
+
+    def check_solves(self, infos):
+        for inf in infos:
+            raise_for(inf)
+
+    def melt_summary(self, T_liquidus: float):
+        out = np.empty(4)
+        N.check(N.lib().tl_run_melt_summary(self._h, float(T_liquidus), N.dptr(out)), "melt")
+        return {"global_max": out[0], "local_max": out[1], "global_melt_nodes": int(out[2]),
+                "local_melt_nodes": int(out[3])}
+
+    def stream(self) -> int:
+        s = C.c_void_p()
+        N.check(N.lib().tl_run_stream(self._h, C.byref(s)), "stream")
+        return s.value or 0
+
+    def launch_count(self) -> int:
+        return int(N.lib().tl_run_launch_count(self._h))
+
+    def flush_l2(self):
+        N.check(N.lib().tl_run_flush_l2(self._h), "flush")
+
+
+def _merge_counters(stats, counters: dict):
+    if stats is None:
+        return
+    for k, v in counters.items():
+        stats.count(k, v)
+
+
+def _drive(problem, run: DeviceRun, plan_fn, local_mesh, T0, stats, recorder, t_initial,
+           batch: int | None):
+    """Shared driver: plan on the host, execute on the device, deliver records."""
+    gmesh = problem.global_mesh
+    run.initial(T0)
+    if recorder is not None:
+        lv = run.field(1)
+        recorder("initial", t_initial, FieldState(local_mesh, lv, T0.time), T0, 0)
+    t0 = time.perf_counter()
+    k = 0
+    placement, tg, tl = local_mesh.placement, T0.time, T0.time
+    last_plan = None
+    while True:
+        plan = plan_fn(placement, tg, tl, k, 1 if recorder is not None else batch,
+                       recorder is not None)
+        if plan.n_steps == 0:
+            break
+        run.run(plan)
+        infos = run.take_info()
+        run.check_solves(infos)
+        _merge_counters(stats, plan.counters)
+        if recorder is not None:
+            _deliver(run, problem, plan, infos, recorder)
+        placement, tg, tl = plan.final_placement, plan.final_t_global, plan.final_t_local
+        k += plan.n_steps
+        last_plan = plan
+        if batch is None and recorder is None:
+            break
+    if stats is not None:
+        stats.seconds["device_run"] = stats.seconds.get("device_run", 0.0) + time.perf_counter() - t0
+    final_local = StructuredGrid(placement)
+    gv, lv = run.field(0), run.field(1)
+    gamma = extract_interface(final_local, gmesh)
+    trace = run.field(2)[gamma.trace_nodes]
+    return TwoLevelState(FieldState(gmesh, gv, tg), FieldState(final_local, lv, tl), gamma, trace), last_plan
+
+
+def _deliver(run: DeviceRun, problem, plan: Plan, infos, recorder):
+    """Replay the recorder calls of one macro step from the device snapshots."""
+    gmesh = problem.global_mesh
+    mp = plan.macro[0]
+    local_mesh = StructuredGrid(plan.placements[0])
+    spacetime = plan.mode == "spacetime"
+    gpred = run.snapshot(0)
+    t_next = plan.t_next[0]
+    if spacetime:
+        recorder("predictor", t_next, None, FieldState(gmesh, gpred, plan.t_global[0]), 0)
+        for i, ti in enumerate(plan.micro_times[0]):
+            recorder("micro", ti, FieldState(local_mesh, run.snapshot(1, i), ti), None, 0)
+    n = int(mp["n_micro"]) - 1 + int(mp["corrector"])
+    lfinal = run.snapshot(1, n)
+    recorder("macro", t_next, FieldState(local_mesh, lfinal, t_next),
+             FieldState(gmesh, gpred, plan.t_global[0] if spacetime else t_next), 1)
+
+
+def run_spacetime(problem: TwoLevelProblem, schedule: MacroSchedule, local_mesh: StructuredGrid,
+                  T0: FieldState, path=None, policy=None, stats=None, recorder=None,
+                  batch: int | None = None) -> TwoLevelState:
+    """Multirate driver over the whole schedule (``multirate.py:167-191``) on the device."""
+    extract_interface(local_mesh, problem.global_mesh)
+    with DeviceRun(problem, local_mesh) as run:
+        def plan_fn(placement, tg, tl, k, nsteps, record):
+            return plan_spacetime(problem, schedule, placement, path, policy, tg, tl, k0=k,
+                                  nsteps=nsteps, record=record)
+        state, _ = _drive(problem, run, plan_fn, local_mesh, T0, stats, recorder,
+                          schedule.t_start, batch)
+    return state
+
+
+def run_space(problem: TwoLevelProblem, dt: float, n_steps: int, local_mesh: StructuredGrid,
+              T0: FieldState, path=None, policy=None, stats=None, recorder=None,
+              batch: int | None = None) -> TwoLevelState:
+    """Uniform-step driver (``multirate.py:194-217``) on the device."""
+    extract_interface(local_mesh, problem.global_mesh)
+    with DeviceRun(problem, local_mesh) as run:
+        def plan_fn(placement, tg, tl, k, nsteps, record):
+            return plan_space(problem, dt, n_steps, placement, path, policy, T0.time, tg, k0=k,
+                              nsteps=nsteps, record=record)
+        state, _ = _drive(problem, run, plan_fn, local_mesh, T0, stats, recorder, T0.time, batch)
+    return state
+
+
+# -- step-level API (reference behaviour on the seam-2 solves) ----------------------------
+
+def predictor_global(problem, state, dt, stats=None) -> FieldState:
+    """``multirate.py:78-89``."""
+    if stats is not None:
+        stats.count("predictor_solves")
+    return solve_global(problem, state, dt, state.local_field, stats=stats, predictor=True)
+
+
+def interpolate_trace(i: int, m: int, trace_old, trace_pred):
+    """``multirate.py:92-102``."""
+    if not 0 <= i <= m:
+        raise CouplingError(f"micro index {i} outside 0..{m}")
+    w = i / m
+    return (1.0 - w) * trace_old + w * trace_pred
+
+
+def macro_step(problem, state: TwoLevelState, schedule: MacroSchedule, k: int, stats=None,
+               recorder=None) -> TwoLevelState:
+    """One predictor / micro / corrector cycle (``multirate.py:105-164``), one-way branch."""
+    if not (problem.one_way and problem.interval_source):
+        raise SolverError("the device path implements the one-way, interval-source branch only")
+    m = schedule.micro_per_macro
+    delta = schedule.dt_micro
+    t_next = schedule.t_macro(k + 1)
+    predicted = predictor_global(problem, state, schedule.dt_macro, stats=stats)
+    if recorder is not None:
+        recorder("predictor", t_next, None, predicted, 0)
+    trace_old = state.trace
+    trace_pred = state.gamma.trace_of(predicted.values, problem.global_mesh)
+    local = state.local_field
+    before_final = state.local_field
+    for i in range(m):
+        t_i = schedule.t_micro(k, i + 1)
+        trace_i = interpolate_trace(i + 1, m, trace_old, trace_pred)
+        if i == m - 1:
+            before_final = local
+        local = solve_local(problem, local, t_i - local.time, state.gamma, trace_i, stats=stats)
+        local = FieldState(local.mesh, local.values, t_i)
+        if recorder is not None:
+            recorder("micro", t_i, local, None, 0)
+    corrected = solve_local(problem, before_final, delta, state.gamma, trace_pred, stats=stats)
+    corrected = FieldState(corrected.mesh, corrected.values, t_next)
+    if stats is not None:
+        stats.count("coupling_iterations")
+    new_state = TwoLevelState(predicted, corrected, state.gamma, trace_pred)
+    if recorder is not None:
+        recorder("macro", t_next, new_state.local_field, new_state.global_field, 1)
+    return new_state

@@ -1,0 +1,247 @@
+"""Two-level coupling: problem, state, interface, and the step-level solves.
+
+Mirrors ``lpbfsim/twolevel.py`` for the branch the device represents: equal
+conductivities on both levels (so ``one_way`` holds and the interface
+functional ``transmission_load`` is identically zero, ``twolevel.py:101-113,
+175``) with the interval-based swept-track global source.  The opaque source
+closures of the reference problem (``runner.py:49-81``) are replaced by the
+beam and scan path themselves, so the device can evaluate the sources.
+
+Seam 2 (``solve_global`` / ``solve_local``, ``twolevel.py:242-288``) runs one
+device solve per call on host buffers.  The device-resident fast path is
+``multirate.run_spacetime`` / ``run_space``.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .config import CouplingSettings, SolverSettings
+from .control import LaserBeam, ScanPath, ThermalBC, check_immersed, material_constants
+from .errors import CouplingError, UnsupportedOnDevice
+from .fem import BoundarySpec, FieldState, GaussianSource, check_linear_problem, step_backward_euler
+from .grid import BOTTOM, TOP, StructuredGrid
+
+__all__ = ["TwoLevelProblem", "TwoLevelState", "InterfaceGamma", "initial_state", "solve_global",
+           "solve_local", "transmission_load", "extract_interface", "two_level_iterate"]
+
+
+@dataclass(frozen=True)
+class InterfaceGamma:
+    """Interface node set of a local lattice (``mesh.py:442-474``).
+
+    ``trace_nodes`` are the lateral + bottom boundary nodes (sorted ids, as
+    ``np.unique`` returns them, ``mesh.py:507``).
+    """
+
+    local: StructuredGrid
+    trace_nodes: np.ndarray
+
+    def trace_of(self, global_field_values, global_mesh) -> np.ndarray:
+        from .ops import interpolate_to_grid
+        full = interpolate_to_grid(global_mesh, global_field_values, self.local, gamma_only=True)
+        return full[self.trace_nodes]
+
+
+def extract_interface(local: StructuredGrid, global_mesh: StructuredGrid) -> InterfaceGamma:
+    """``extract_interface`` node part (``mesh.py:477-523``) with its immersion checks."""
+    check_immersed(local.box, global_mesh.box, global_mesh.h)
+    return InterfaceGamma(local, np.nonzero(local.gamma_mask())[0])
+
+
+@dataclass(frozen=True)
+class TwoLevelState:
+    global_field: FieldState
+    local_field: FieldState
+    gamma: InterfaceGamma
+    trace: np.ndarray
+
+    def __post_init__(self):
+        tol = 1e-9 * max(abs(self.global_field.time), 1.0)
+        if abs(self.global_field.time - self.local_field.time) > tol:
+            raise CouplingError("global and local fields must share a time stamp")
+
+    @property
+    def time(self) -> float:
+        return self.global_field.time
+
+
+@dataclass
+class TwoLevelProblem:
+    """Everything fixed across a two-level run (``twolevel.py:78-142``), device flavour."""
+
+    global_mesh: StructuredGrid
+    mat_global: object
+    mat_local: object
+    bc: ThermalBC
+    solver: SolverSettings = field(default_factory=SolverSettings)
+    coupling: CouplingSettings = field(default_factory=CouplingSettings)
+    mode: str = "alternate"
+    beam: LaserBeam | None = None
+    path: ScanPath | None = None
+    source_global: str = "distributed"
+    resolve_corrector: bool = True
+    device: int = 0
+
+    def __post_init__(self):
+        if self.mode not in ("alternate", "full"):
+            raise CouplingError(f"unknown global formulation {self.mode!r}")
+
+    # -- reference attributes ----------------------------------------------------
+
+    @property
+    def one_way(self) -> bool:
+        a, b = self.mat_global, self.mat_local
+        if a is b:
+            return True
+        same_k = (a.conductivity_table.shape == b.conductivity_table.shape
+                  and np.array_equal(a.conductivity_table, b.conductivity_table))
+        if not same_k:
+            return False
+        if self.mode == "alternate":
+            return True
+        same_c = (a.heat_capacity_table.shape == b.heat_capacity_table.shape
+                  and np.array_equal(a.heat_capacity_table, b.heat_capacity_table))
+        return same_c and a.rho == b.rho and a.chi == b.chi and b.chi == 0.0
+
+    @property
+    def interval_source(self) -> bool:
+        return self.source_global == "distributed"
+
+    def global_source(self, t0: float, t1: float, predictor: bool = False):
+        """The swept-track deposit of [t0, t1] as (points, power) or None (``runner.py:75-79``)."""
+        from .schedule import swept_samples
+        if self.path is None or self.beam is None:
+            return None
+        pieces = self.path.swept_pieces(t0, t1)
+        if not pieces:
+            return None
+        return swept_samples(self.beam, pieces, t1 - t0)
+
+    def local_source(self, t: float):
+        """GaussianSource at the laser position of t, None outside the path (``runner.py:49-61``)."""
+        if self.path is None or self.beam is None:
+            return None
+        tol = 1e-12 * max(self.path.t_end, 1.0)
+        if t > self.path.t_end + tol or t < self.path.t_start - tol:
+            return None
+        return GaussianSource(self.beam, tuple(self.path.position(t)))
+
+    def global_bounds(self) -> BoundarySpec:
+        return BoundarySpec(bc=self.bc, robin_tags=(TOP,), radiation=False,
+                            dirichlet_nodes=self.global_mesh.nodes_on(BOTTOM),
+                            dirichlet_values=self.bc.T_buildplate)
+
+    def local_bounds(self, gamma: InterfaceGamma, trace) -> BoundarySpec:
+        return BoundarySpec(bc=self.bc, robin_tags=(TOP,), radiation=True,
+                            dirichlet_nodes=gamma.trace_nodes, dirichlet_values=trace)
+
+    # -- device support ---------------------------------------------------------
+
+    def check_device_supported(self):
+        check_linear_problem(self.mat_global, None, False)
+        check_linear_problem(self.mat_local, None, True)
+        if self.bc.h_conv > 0:
+            raise UnsupportedOnDevice("Robin convection (h_conv > 0) is not on the device path")
+        if self.bc.emissivity > 0:
+            raise UnsupportedOnDevice("radiation (emissivity > 0) is not on the device path")
+        if not self.one_way:
+            raise UnsupportedOnDevice("two-way coupling (kappa_global != kappa_local) is SURVEY §8 f "
+                                      "row 2, not on the device path")
+        if not self.interval_source:
+            raise UnsupportedOnDevice("only the distributed (swept-track) global source is on the "
+                                      "device path")
+        if self.global_mesh.dim != 3:
+            raise UnsupportedOnDevice("the device path is 3D only")
+
+    def constants(self):
+        kg, rcg = material_constants(self.mat_global)
+        kl, rcl = material_constants(self.mat_local)
+        return kg, rcg, rcl
+
+
+def initial_state(problem: TwoLevelProblem, local_mesh: StructuredGrid,
+                  global_field: FieldState) -> TwoLevelState:
+    """``initial_state`` (``twolevel.py:145-156``): local = P1(global), trace = P1 on gamma."""
+    from .ops import interpolate_to_grid
+    gamma = extract_interface(local_mesh, problem.global_mesh)
+    lv = interpolate_to_grid(problem.global_mesh, global_field.values, local_mesh)
+    local = FieldState(local_mesh, lv, global_field.time)
+    return TwoLevelState(global_field, local, gamma, lv[gamma.trace_nodes].copy())
+
+
+def transmission_load(local_field, gamma, global_mesh, mat_global, mat_local) -> np.ndarray:
+    """Interface functional (``twolevel.py:159-183``): exactly zero for equal conductivities."""
+    if not np.array_equal(mat_global.conductivity_table, mat_local.conductivity_table):
+        raise UnsupportedOnDevice("non-zero transmission load (two-way coupling) is not on the "
+                                  "device path")
+    return np.zeros(global_mesh.n_nodes)
+
+
+def solve_global(problem: TwoLevelProblem, state: TwoLevelState, dt: float,
+                 local_for_coupling: FieldState, stats=None, predictor: bool = False) -> FieldState:
+    """One global backward-Euler step on the device (``twolevel.py:242-271``)."""
+    from .ops import deposit_load
+    t0, t1 = state.global_field.time, state.global_field.time + dt
+    load = transmission_load(local_for_coupling, state.gamma, problem.global_mesh,
+                             problem.mat_global, problem.mat_local)
+    dep = problem.global_source(t0, t1, predictor=predictor)
+    if dep is not None:
+        load = load + deposit_load(problem.global_mesh, dep[0], dep[1])
+    timer = stats.timer("global_solve") if stats is not None else _Null()
+    with timer:
+        out = step_backward_euler(state.global_field, dt, problem.mat_global, None,
+                                  problem.global_bounds(), problem.solver, latent=False,
+                                  extra_load=load, stats=stats)
+    if stats is not None:
+        stats.count("global_solves")
+    return out
+
+
+def solve_local(problem: TwoLevelProblem, local_from: FieldState, dt: float, gamma: InterfaceGamma,
+                trace, stats=None) -> FieldState:
+    """One local step with the trace as Dirichlet data (``twolevel.py:274-288``)."""
+    t1 = local_from.time + dt
+    source = problem.local_source(t1)
+    timer = stats.timer("local_solve") if stats is not None else _Null()
+    with timer:
+        out = step_backward_euler(local_from, dt, problem.mat_local, source,
+                                  problem.local_bounds(gamma, trace), problem.solver, latent=True,
+                                  stats=stats)
+    if stats is not None:
+        stats.count("local_solves")
+    return out
+
+
+def two_level_iterate(problem: TwoLevelProblem, state: TwoLevelState, dt: float,
+                      local_from=None, local_dt=None, transmission_seed=None, trace_start=None,
+                      stats=None):
+    """One-way pass of ``two_level_iterate`` (``twolevel.py:299-358``)."""
+    if not problem.one_way:
+        raise UnsupportedOnDevice("the relaxed two-way fixed point is not on the device path")
+    if local_from is None:
+        local_from = state.local_field
+    if local_dt is None:
+        local_dt = dt
+    t1 = state.global_field.time + dt
+    if abs(local_from.time + local_dt - t1) > 1e-9 * max(abs(t1), 1e-30):
+        raise CouplingError("fine and coarse steps must land on the same time")
+    seed = state.local_field if transmission_seed is None else transmission_seed
+    new_global = solve_global(problem, state, dt, seed, stats=stats)
+    trace = state.gamma.trace_of(new_global.values, problem.global_mesh)
+    new_local = solve_local(problem, local_from, local_dt, state.gamma, trace, stats=stats)
+    if stats is not None:
+        stats.count("coupling_iterations")
+    out = TwoLevelState(new_global, FieldState(new_local.mesh, new_local.values, t1),
+                        state.gamma, trace)
+    return out, 1
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False

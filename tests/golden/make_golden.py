@@ -1,0 +1,327 @@
+"""Generate golden vectors by running the UNMODIFIED reference (lpbfsim).
+
+Run in the build container only (needs /root/reference; the GPU box never
+reads it):
+
+    OPENBLAS_NUM_THREADS=1 python tests/golden/make_golden.py [--quick]
+
+Outputs (committed, small): tests/golden/*.npz and *.json.  Every array here
+comes from calling the reference's own functions:
+
+- op_*.npz       assemble_system(...).constrained() applied to a random
+                 vector, the constrained RHS, and solve_linear (cg, 1e-12)
+                 — fem.py:129-194,89-105,271-291
+- interp.npz     Mesh.interpolate at random points       — mesh.py:358-361
+- deposit.npz    SweptTrackDeposit.load                  — sources.py:164-172
+- gaussian.json  gaussian_source_3d known answers         — sources.py:67-77
+- run_*.npz      run_spacetime / run_space with a field-capturing recorder
+                 and a CG-iteration counter wrapped around fem._cg
+                 — multirate.py:167-217
+- schedule_*.json local-box origins per macro step from the reference's
+                 LocalDomainPolicy / Mesh.translated / DomainEscape clamp,
+                 path.position and swept_pieces         — scanpath.py:68-248
+Versions: numpy and scipy versions are stored in every file.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+import time
+from pathlib import Path
+
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+REF = Path("/root/reference/pkg/src")
+sys.path.insert(0, str(REF))
+
+import numpy as np  # noqa: E402
+import scipy  # noqa: E402
+import scipy.sparse.linalg as spla  # noqa: E402
+
+import lpbfsim  # noqa: E402
+from lpbfsim import fem, mesh as lmesh, multirate, runner, scanpath, sources, twolevel  # noqa: E402
+from lpbfsim.config import load_config  # noqa: E402
+from lpbfsim.stats import RunStats  # noqa: E402
+
+OUT = Path(__file__).resolve().parent
+CFG = OUT.parent.parent / "configs"
+VERS = {"numpy": np.__version__, "scipy": scipy.__version__, "lpbfsim": lpbfsim.__version__}
+
+CG_ITERS: list = []
+
+
+def _counting_cg(A, b, rtol, M, maxiter):
+    n = [0]
+
+    def cb(_x):
+        n[0] += 1
+
+    out = spla.cg(A, b, rtol=rtol, M=M, maxiter=maxiter, callback=cb)
+    CG_ITERS.append(n[0])
+    return out
+
+
+fem._cg = _counting_cg
+
+
+def stride_sample(v, s):
+    return np.asarray(v)[::s].copy()
+
+
+# -- A: operator / RHS / single-step pins ----------------------------------------
+
+def op_case(name, lo, hi, h, kind, seed=0):
+    rng = np.random.default_rng(seed)
+    box = lmesh.Box(lo, hi)
+    m = lmesh.build_structured_mesh(box, h)
+    mat = lpbfsim.materials.load_material(CFG / "const.mat")
+    bc = sources.ThermalBC(0.0, 0.0, 293.0, 293.0)
+    beam = sources.LaserBeam(200.0, 0.35, 5e-5, 5e-5, 0.8)
+    T_old = rng.uniform(293.0, 2293.0, m.n_nodes)
+    dt = 2.5e-6
+    if kind == "local":
+        # local level: gamma Dirichlet with trace values, Gaussian at an off-node centre
+        lbox = box
+        glo = np.asarray(lo) - np.array([3e-4, 3e-4, 3e-4])
+        ghi = np.asarray(hi) + np.array([3e-4, 3e-4, 0.0])
+        gm = lmesh.build_structured_mesh(lmesh.Box(tuple(glo), tuple(ghi)), 5e-5)
+        gam = lmesh.extract_interface(m, gm)
+        dnodes = gam.trace_nodes
+        dvals = rng.uniform(293.0, 1500.0, dnodes.size)
+        center = np.asarray(lo) + 0.37 * (np.asarray(hi) - np.asarray(lo))
+        center[2] = hi[2]
+        src = lambda pts: sources.gaussian_source_3d(beam, center, pts)  # noqa: E731
+        extra = None
+    else:
+        dnodes = m.nodes_on(lmesh.BOTTOM)
+        dvals = 293.0
+        center = None
+        src = None
+        a = np.asarray(lo) + np.array([0.2, 0.5, 1.0]) * (np.asarray(hi) - np.asarray(lo))
+        b = a + np.array([0.8 * dt, 0.0, 0.0]) * 40
+        dep = sources.SweptTrackDeposit(beam, [(a, b)], dt * 40)
+        extra = dep.load(m)
+    bounds = fem.BoundarySpec(bc=bc, robin_tags=(lmesh.TOP,), radiation=(kind == "local"),
+                              dirichlet_nodes=np.asarray(dnodes, dtype=np.int64),
+                              dirichlet_values=dvals)
+    state = fem.FieldState(m, T_old, 0.0)
+    sysm = fem.assemble_system(m, mat, state, state, dt, src, bounds, latent=(kind == "local"),
+                               extra_load=extra)
+    A, b = sysm.constrained()
+    x = rng.uniform(-1.0, 1.0, m.n_nodes)
+    CG_ITERS.clear()
+    sol = fem.solve_linear(sysm, fem.SolverSettings(linear_tol=1e-12, linear_solver="cg"))
+    its = CG_ITERS[-1]
+    direct = fem.solve_linear(sysm, fem.SolverSettings(linear_tol=1e-12, linear_solver="direct"))
+    np.savez_compressed(
+        OUT / f"op_{name}.npz", lo=np.asarray(lo), hi=np.asarray(hi), h=np.asarray(h, dtype=float),
+        ncells=m.ncells, kind=kind, T_old=T_old, dt=dt, dnodes=np.asarray(dnodes),
+        dvals=np.broadcast_to(np.asarray(dvals, dtype=float), np.shape(dnodes)).copy(),
+        center=np.asarray(center if center is not None else [np.nan] * 3),
+        extra=extra if extra is not None else np.zeros(0), x=x, Ax=A @ x, b=b,
+        diag=A.diagonal(), sol=sol, direct=direct, cg_iters=its, versions=json.dumps(VERS))
+    print(f"op_{name}: n={m.n_nodes} its={its}")
+
+
+# -- B/C: interpolation and deposit ------------------------------------------------
+
+def interp_case():
+    rng = np.random.default_rng(1)
+    m = lmesh.build_structured_mesh(lmesh.Box((0, 0, 0), (2e-3, 1e-3, 5e-4)), 5e-5)
+    vals = rng.uniform(293.0, 2293.0, m.n_nodes)
+    pts = rng.uniform([0, 0, 0], [2e-3, 1e-3, 5e-4], size=(5000, 3))
+    # include node-coincident and face points (lattice ties)
+    pts = np.vstack([pts, m.coords[rng.choice(m.n_nodes, 500, replace=False)],
+                     np.array([[1e-3, 5e-4, 2.5e-4], [2e-3, 1e-3, 5e-4], [0, 0, 0]])])
+    out = m.interpolate(vals, pts)
+    np.savez_compressed(OUT / "interp.npz", lo=[0, 0, 0], hi=[2e-3, 1e-3, 5e-4], h=5e-5,
+                        vals=vals, pts=pts, out=out, versions=json.dumps(VERS))
+
+
+def deposit_case():
+    cfg = load_config(CFG / "cfg2.cfg")
+    gm = lmesh.build_structured_mesh(lmesh.Box((0, 0, 0), (1.5e-3, 1e-3, 5e-4)), 2.5e-5)
+    beam = sources.LaserBeam(200.0, 0.35, 5e-5, 5e-5, 0.8)
+    path = scanpath.build_alternating_path(3, 1e-3, 1e-4, 0.8, (2.5e-4, 3e-4, 5e-4))
+    rows = []
+    # intervals including a track turn (two pieces) and one past the path end
+    for t0, t1 in [(0.0, 2e-5), (1.24e-3, 1.26e-3), (1.2499e-3, 1.2701e-3), (3.74e-3, 3.76e-3)]:
+        pieces = path.swept_pieces(t0, t1)
+        dep = sources.SweptTrackDeposit(beam, pieces, t1 - t0)
+        load = dep.load(gm)
+        nz = np.nonzero(load)[0]
+        pts, pw = dep.sample_points()
+        rows.append(dict(t0=t0, t1=t1, npieces=len(pieces), idx=nz.tolist(),
+                         val=load[nz].tolist(), total=float(load.sum()),
+                         pts=pts.tolist(), pw=pw.tolist()))
+    (OUT / "deposit.json").write_text(json.dumps(dict(
+        lo=[0, 0, 0], hi=[1.5e-3, 1e-3, 5e-4], h=2.5e-5, beam=[200.0, 0.35, 5e-5, 5e-5, 0.8],
+        path=dict(n=3, L=1e-3, hatch=1e-4, v=0.8, origin=[2.5e-4, 3e-4, 5e-4]),
+        cases=rows, versions=VERS)))
+    _ = cfg
+
+
+def gaussian_case():
+    beam = sources.LaserBeam(179.2, 0.38, 8.5e-5, 5e-5, 0.8)
+    c = np.array([1e-4, 2e-4, 3e-4])
+    rng = np.random.default_rng(2)
+    pts = c + rng.normal(0, 6e-5, size=(64, 3))
+    vals = sources.gaussian_source_3d(beam, c, pts)
+    peak = sources.gaussian_source_3d(beam, c, c[None, :])[0]
+    (OUT / "gaussian.json").write_text(json.dumps(dict(
+        beam=[179.2, 0.38, 8.5e-5, 5e-5, 0.8], center=c.tolist(), pts=pts.tolist(),
+        vals=vals.tolist(), peak=float(peak), versions=VERS)))
+
+
+# -- D: schedule pins ---------------------------------------------------------------
+
+def schedule_case(name, max_steps=None):
+    """Local-box origin after every relocation, from the reference's own functions.
+
+    The loop restates run_spacetime's relocation cadence (multirate.py:184-190) and
+    the shift/clamp of relocate_local (scanpath.py:219-241); the geometry calls are
+    the reference's (LocalDomainPolicy.target_origin, Mesh.translated with its
+    DomainEscape test, ScanPath.position/direction/swept_pieces).
+    """
+    cfg = load_config(CFG / f"{name}.cfg")
+    gbox = cfg.global_box
+    t0 = cfg.path.t_start
+    origin = cfg.policy.target_origin(cfg.path.position(t0), cfg.path.direction(t0))
+    size = np.asarray(cfg.policy.box_size)
+    glo, ghi = np.asarray(gbox.lo), np.asarray(gbox.hi)
+    margin = np.minimum(cfg.h_local, (ghi - glo - size) / 2)
+    origin = np.clip(origin, glo + margin, ghi - size - margin)
+    origin[-1] = ghi[-1] - size[-1]
+    lbox = lmesh.Box(tuple(origin), tuple(origin + size))
+    q = lbox.lengths / cfg.h_local
+    ncells = np.where(np.abs(q - np.round(q)) <= 1e-9 * q, np.round(q), np.ceil(q)).astype(np.int64)
+    stub = lmesh.Mesh(lbox, ncells, np.zeros((1, 3)), np.zeros((1, 4), dtype=np.int64))
+    spacetime = cfg.mode == "two-level-spacetime"
+    if spacetime:
+        sched = multirate.MacroSchedule(cfg.dt_macro, cfg.micro_steps, 0.0, cfg.t_end)
+        n = sched.n_macro
+    else:
+        dt = cfg.dt_macro / cfg.micro_steps
+        n = int(round(cfg.t_end / dt))
+    steps = n if max_steps is None else min(n, max_steps)
+    boxes, npieces, centers = [list(stub.box.lo)], [], []
+    tg = 0.0
+    for k in range(steps):
+        if spacetime:
+            t_next = sched.t_macro(k + 1)
+            pieces = cfg.path.swept_pieces(tg, tg + cfg.dt_macro)
+            tg = tg + cfg.dt_macro
+            ti = sched.t_micro(k, 1)
+        else:
+            t_next = (k + 1) * dt
+            pieces = cfg.path.swept_pieces(tg, tg + (t_next - tg))
+            ti = tg + (t_next - tg)
+            tg = t_next
+        npieces.append(len(pieces))
+        centers.append(cfg.path.position(min(ti, cfg.path.t_end)).tolist())
+        if k < n - 1:
+            t = min(t_next, cfg.path.t_end)
+            laser, direction = cfg.path.position(t), cfg.path.direction(t)
+            snap = np.asarray(cfg.policy.snap if cfg.policy.snap is not None else stub.spacing)
+            target = cfg.policy.target_origin(laser, direction)
+            shift = np.round((target - np.asarray(stub.box.lo)) / snap) * snap
+            shift[-1] = 0.0
+            if np.any(shift != 0.0):
+                try:
+                    stub = stub.translated(shift, within=gbox)
+                except lmesh.DomainEscape:
+                    lo, hi = np.asarray(stub.box.lo), np.asarray(stub.box.hi)
+                    room_lo = np.ceil((glo - lo) / snap + 1.0 - 1e-9) * snap
+                    room_hi = np.floor((ghi - hi) / snap - 1.0 + 1e-9) * snap
+                    shift = np.clip(shift, room_lo, room_hi)
+                    shift[-1] = 0.0
+                    if np.any(shift != 0.0):
+                        stub = stub.translated(shift, within=gbox)
+        boxes.append(list(stub.box.lo))
+    (OUT / f"schedule_{name}.json").write_text(json.dumps(dict(
+        steps=steps, boxes=boxes, npieces=npieces, centers=centers,
+        offset_final=stub._offset.tolist(), versions=VERS)))
+    print(f"schedule_{name}: {steps} steps")
+
+
+# -- E/F/G: full reference runs -----------------------------------------------------
+
+def run_case(name, max_steps, full_at, stride):
+    cfg = load_config(CFG / f"{name}.cfg")
+    if max_steps is not None:
+        cfg.t_end = max_steps * cfg.dt_macro
+        # the path keeps its own t_end; only the schedule is truncated
+    problem, lm = runner.build_problem(cfg)
+    stats = RunStats()
+    T0 = fem.uniform_field(problem.global_mesh, cfg.T_initial, time=0.0)
+    rec = {"t": [], "kind": [], "box": [], "gmax": [], "lmax": [], "gsum": [], "lsum": [],
+           "gsub": [], "lsub": [], "gmelt": [], "lmelt": [], "gmargin": [], "lmargin": []}
+    full = {}
+    TL = cfg.material.T_liquidus
+
+    def recorder(kind, t, local, glob, iters):
+        if kind not in ("initial", "macro"):
+            return
+        g, loc = glob.values, local.values
+        k = len(rec["t"])
+        rec["t"].append(t)
+        rec["kind"].append(kind)
+        rec["box"].append(list(local.mesh.box.lo))
+        rec["gmax"].append(float(g.max()))
+        rec["lmax"].append(float(loc.max()))
+        rec["gsum"].append(float(g.sum()))
+        rec["lsum"].append(float(loc.sum()))
+        rec["gsub"].append(stride_sample(g, stride))
+        rec["lsub"].append(stride_sample(loc, stride))
+        rec["gmelt"].append(np.packbits(g > TL))
+        rec["lmelt"].append(np.packbits(loc > TL))
+        rec["gmargin"].append(float(np.min(np.abs(g - TL))))
+        rec["lmargin"].append(float(np.min(np.abs(loc - TL))))
+        if k in full_at:
+            full[f"g{k}"] = g.copy()
+            full[f"l{k}"] = loc.copy()
+
+    CG_ITERS.clear()
+    t0 = time.perf_counter()
+    if cfg.mode == "two-level-spacetime":
+        sched = multirate.MacroSchedule(cfg.dt_macro, cfg.micro_steps, 0.0, cfg.t_end)
+        multirate.run_spacetime(problem, sched, lm, T0, path=cfg.path, policy=cfg.policy,
+                                stats=stats, recorder=recorder)
+    else:
+        dt = cfg.dt_macro / cfg.micro_steps
+        n = int(round(cfg.t_end / dt))
+        multirate.run_space(problem, dt, n, lm, T0, path=cfg.path, policy=cfg.policy,
+                            stats=stats, recorder=recorder)
+    wall = time.perf_counter() - t0
+    np.savez_compressed(
+        OUT / f"run_{name}.npz", t=np.array(rec["t"]), box=np.array(rec["box"]),
+        gmax=np.array(rec["gmax"]), lmax=np.array(rec["lmax"]), gsum=np.array(rec["gsum"]),
+        lsum=np.array(rec["lsum"]), gsub=np.array(rec["gsub"]), lsub=np.array(rec["lsub"]),
+        gmelt=np.array(rec["gmelt"]), lmelt=np.array(rec["lmelt"]),
+        gmargin=np.array(rec["gmargin"]), lmargin=np.array(rec["lmargin"]),
+        stride=stride, cg_iters=np.array(CG_ITERS), full_at=np.array(sorted(full_at)),
+        counters=json.dumps(stats.counters), wall=wall, versions=json.dumps(VERS), **full)
+    print(f"run_{name}: steps={len(rec['t']) - 1} wall={wall:.1f}s counters={stats.counters}")
+
+
+def main():
+    quick = "--quick" in sys.argv
+    op_case("aniso_local", (1e-4, 2e-4, 3e-4), (2.75e-4, 2.85e-4, 3.44e-4), (2.5e-5, 1.7e-5, 1.1e-5), "local")
+    op_case("aniso_global", (0.0, 0.0, 0.0), (1.75e-4, 1.7e-4, 1.1e-4), (2.5e-5, 1.7e-5, 1.1e-5), "global")
+    op_case("cfg1_local", (8e-4, 3e-4, 3e-4), (1.2e-3, 7e-4, 5e-4), 1e-5, "local")
+    op_case("cfg1_global", (0.0, 0.0, 0.0), (2e-3, 1e-3, 5e-4), 5e-5, "global")
+    interp_case()
+    deposit_case()
+    gaussian_case()
+    for name in ("cfg1_m4", "cfg1_uniform", "cfg2", "cfg3", "cfg4"):
+        schedule_case(name, max_steps=None if name.startswith("cfg1") or name == "cfg2" else 3000)
+    if quick:
+        return
+    run_case("cfg1_m4", None, {1, 2, 10, 40, 80}, 17)
+    run_case("cfg1_uniform", None, {1, 80}, 17)
+    run_case("cfg2", 2, {1, 2}, 97)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,139 @@
+"""Pin the CPU oracle to golden vectors produced by the unmodified reference.
+
+tests/golden/make_golden.py ran lpbfsim 0.1.0 (numpy 2.3.5, scipy 1.18.1) and
+stored its outputs; here the oracle must reproduce them: operator/RHS/solve at
+rounding level with identical CG iteration counts, interpolation and deposit,
+and whole two-level runs (cfg1 multirate m=4 and uniform, all 80 macro steps;
+cfg2 first 2 macro steps).
+"""
+
+import json
+
+import numpy as np
+import pytest
+
+import paper_2110_12932_b200 as P
+from oracle import assembly, kuhn
+from oracle.pcg import solve_constrained
+from oracle.twolevel import OracleRun
+
+from .conftest import CONFIGS, GOLDEN
+
+OP_CASES = ["aniso_local", "aniso_global", "cfg1_local", "cfg1_global"]
+
+
+def _op(name):
+    z = np.load(GOLDEN / f"op_{name}.npz")
+    G = kuhn.KuhnGrid(z["lo"], z["hi"], z["ncells"])
+    D = np.zeros(G.n_nodes, bool)
+    D[z["dnodes"]] = True
+    g = np.zeros(G.n_nodes)
+    g[z["dnodes"]] = z["dvals"]
+    local = str(z["kind"]) == "local"
+    beam = P.LaserBeam(200.0, 0.35, 5e-5, 5e-5, 0.8)
+    return z, G, D, g, local, beam
+
+
+@pytest.mark.parametrize("name", OP_CASES)
+def test_stencil_operator_rhs_solve(name):
+    z, G, D, g, local, beam = _op(name)
+    op = kuhn.StencilOperator(G, 9.8, 8440 * 410.0, float(z["dt"]), D.reshape(G.shape))
+    Ax = op.apply(z["x"])
+    assert np.abs(Ax - z["Ax"]).max() <= 1e-14 * np.abs(z["Ax"]).max()
+    assert np.abs(op.diag_c.ravel() - z["diag"]).max() <= 1e-14 * np.abs(z["diag"]).max()
+    load = kuhn.gaussian_load(G, beam, z["center"]) if local else z["extra"]
+    b = op.rhs(z["T_old"], load, g)
+    assert np.abs(b - z["b"]).max() <= 1e-14 * np.abs(z["b"]).max()
+    x, its, res = solve_constrained(op, b, g, 1e-12)
+    assert its == int(z["cg_iters"])
+    assert np.abs(x - z["sol"]).max() <= 1e-13 * np.abs(z["sol"]).max()
+    # CG vs the reference's own direct solve: the oracle's noise floor
+    assert np.abs(x - z["direct"]).max() <= 1e-9 * np.abs(z["direct"]).max()
+
+
+@pytest.mark.parametrize("name", OP_CASES)
+def test_literal_assembly_is_bitwise(name):
+    z, G, D, g, local, beam = _op(name)
+    src = (beam, z["center"]) if local else None
+    x, its = assembly.step(G, 9.8, 8440 * 410.0, float(z["dt"]), D, z["T_old"], src,
+                           None if local else z["extra"], g, 1e-12)
+    assert its == int(z["cg_iters"])
+    # bitwise with single-threaded BLAS (OPENBLAS_NUM_THREADS=1); threaded einsum reorders sums
+    assert np.abs(x - z["sol"]).max() <= 2e-15 * np.abs(z["sol"]).max()
+
+
+def test_interpolation():
+    z = np.load(GOLDEN / "interp.npz")
+    box = P.Box(tuple(z["lo"]), tuple(z["hi"]))
+    G = kuhn.KuhnGrid(box.lo, box.hi, P.control.structured_ncells(box, float(z["h"])))
+    out = kuhn.interpolate(G, z["vals"], z["pts"])
+    assert np.abs(out - z["out"]).max() <= 1e-14 * np.abs(z["out"]).max()
+
+
+def test_deposit_and_samples():
+    d = json.loads((GOLDEN / "deposit.json").read_text())
+    box = P.Box(tuple(d["lo"]), tuple(d["hi"]))
+    G = kuhn.KuhnGrid(box.lo, box.hi, P.control.structured_ncells(box, d["h"]))
+    beam = P.LaserBeam(*d["beam"])
+    p = d["path"]
+    path = P.build_alternating_path(p["n"], p["L"], p["hatch"], p["v"], p["origin"])
+    assert [c["npieces"] for c in d["cases"]] == [1, 2, 2, 1]
+    for c in d["cases"]:
+        pieces = path.swept_pieces(c["t0"], c["t1"])
+        pts, pw = kuhn.swept_samples(beam, pieces, c["t1"] - c["t0"])
+        np.testing.assert_array_equal(pts, np.array(c["pts"]).reshape(-1, 3))
+        np.testing.assert_array_equal(pw, np.array(c["pw"]))
+        load = kuhn.deposit_load(G, pts, pw)
+        nz = np.nonzero(load)[0]
+        np.testing.assert_array_equal(nz, c["idx"])
+        assert np.abs(load[nz] - c["val"]).max() <= 1e-13 * np.abs(c["val"]).max()
+        assert load.sum() == pytest.approx(c["total"], rel=1e-13)
+
+
+def test_gaussian_known_answers():
+    d = json.loads((GOLDEN / "gaussian.json").read_text())
+    beam = P.LaserBeam(*d["beam"])
+    assert beam.gaussian_peak == d["peak"]
+    assert beam.gaussian_peak == pytest.approx(3.12e14, rel=5e-3)      # tests/test_sources.py:53
+    vals = P.GaussianSource(beam, tuple(d["center"]))(np.array(d["pts"]))
+    np.testing.assert_allclose(vals, d["vals"], rtol=1e-14)
+
+
+def _check_run(name, n_steps, full_tol=1e-12):
+    z = np.load(GOLDEN / f"run_{name}.npz")
+    cfg = P.load_config(CONFIGS / f"{name}.cfg")
+    run = OracleRun(cfg)
+    rec = []
+    run_fn = run.run_spacetime if cfg.mode == "two-level-spacetime" else run.run_space
+    run_fn(n_steps=n_steps, recorder=lambda kind, t, Tl, Tg, pl: rec.append((t, Tl, Tg, pl.box.lo)))
+    assert len(rec) == len(z["t"])
+    its = [i for _, i in run.iterations]
+    assert its == z["cg_iters"].tolist()
+    TL = cfg.material.T_liquidus
+    s = int(z["stride"])
+    for k, (t, Tl, Tg, lo) in enumerate(rec):
+        assert t == z["t"][k]
+        np.testing.assert_array_equal(lo, z["box"][k])
+        for sub, ref in ((Tg[::s], z["gsub"][k]), (Tl[::s], z["lsub"][k])):
+            assert np.abs(sub - ref).max() <= full_tol * np.abs(ref).max()
+        np.testing.assert_array_equal(np.packbits(Tg > TL), z["gmelt"][k])
+        np.testing.assert_array_equal(np.packbits(Tl > TL), z["lmelt"][k])
+        if k in z["full_at"]:
+            g, l = z[f"g{k}"], z[f"l{k}"]
+            assert np.abs(Tg - g).max() <= full_tol * np.abs(g).max()
+            assert np.abs(Tl - l).max() <= full_tol * np.abs(l).max()
+    return run
+
+
+def test_run_cfg1_multirate_all_steps():
+    run = _check_run("cfg1_m4", None)
+    assert run.counters["relocations"] == 79
+
+
+def test_run_cfg1_uniform_all_steps():
+    _check_run("cfg1_uniform", None)
+
+
+@pytest.mark.slow
+def test_run_cfg2_first_steps():
+    _check_run("cfg2", 2)
