@@ -1,0 +1,345 @@
+#!/usr/bin/env python
+"""Benchmark: DOF-timesteps/s of the two-level multirate heat solve (BASELINE.json metric).
+
+Workload (N=1): BASELINE config 2 — 5-track alternating scan, global 121x121x41
+(600,281 nodes, h = 25 um), local 101x101x51 (520,251 nodes, h = 5 um), multirate
+m = 10, fp64, Jacobi-PCG rtol 1e-12.  One "step" = one macro step of
+``run_spacetime``: 1 global solve + 10 micro local solves + the corrector
+re-solve + trace + relocation, i.e. N_g + m N_l = 5,802,791 DOF-timesteps
+(the corrector re-solve is performed but not counted).
+
+N > 1 (torchrun): every rank runs its own independent scenario replica on its GPU
+(scenario sharding, no data-path collective, weak scaling); timing is the max
+over ranks of the device time.  ``--impl reference`` times the reference's CPU
+algorithm (the literal P1-assembly + scipy-CG port in oracle/assembly.py, pinned
+bit-for-bit to the reference) on rank 0.
+
+Prints one JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+METRIC = "DOF-timesteps/sec (global+local solves, fp64)"
+UNIT = "DOF-timesteps/s"
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def measured_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        return False
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_sample(cfg_path: Path, what: str = "global+local"):
+    """Reference CPU algorithm (oracle/assembly.py, bitwise-pinned port) on a bounded sample."""
+    import paper_2110_12932_b200 as P
+    from oracle import kuhn
+    from oracle.twolevel import OracleRun
+    cfg = P.load_config(cfg_path)
+    run = OracleRun(cfg, backend="assembly")
+    Tg = np.full(run.G.n_nodes, cfg.T_initial)
+    L = kuhn.KuhnGrid.from_placement(run.placement0)
+    Tl = kuhn.interpolate(run.G, Tg, L.coords())
+    sched = P.MacroSchedule(cfg.dt_macro, cfg.micro_steps, 0.0, cfg.t_end)
+    t0 = time.perf_counter()
+    dof = 0
+    if "global" in what:
+        Tg2 = run.solve_global(Tg, 0.0, cfg.dt_macro)
+        dof += run.G.n_nodes
+    else:
+        Tg2 = Tg
+    trace = run.trace_of(L, Tg2)
+    w = 1.0 / sched.micro_per_macro
+    run.solve_local(L, Tl, 0.0, sched.t_micro(0, 1), (1.0 - w) * run.trace_of(L, Tg) + w * trace)
+    dof += L.n_nodes
+    dt = time.perf_counter() - t0
+    return dof, dt, run.iterations
+
+
+def reference_arm(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    cfg_path = ROOT / "configs" / f"{args.config}.cfg"
+    times, dofs = [], []
+    for s in range(args.warmup + args.steps):
+        dof, dt, _ = cpu_sample(cfg_path, what="local")
+        if s >= args.warmup:
+            times.append(dt)
+            dofs.append(dof)
+    total = sum(times)
+    value = sum(dofs) / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (BASELINE config 2 geometry; uniform 293 K initial field, first micro step)",
+        "config": {"workload": f"{args.config}: one local micro solve per step", "config_file": f"configs/{args.config}.cfg"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
+                         "sample": "one cfg2 local micro solve (520,251 nodes) per step via the literal "
+                                   "P1-assembly + scipy-CG port (oracle/assembly.py, bitwise equal to lpbfsim)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--skip", type=int, default=0, help="macro steps to run before warm-up")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        return reference_arm(args)
+
+    import torch
+    import paper_2110_12932_b200 as P
+    from paper_2110_12932_b200.schedule import plan_spacetime
+
+    rank, world, local_rank = env_rank()
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    cfg_path = ROOT / "configs" / f"{args.config}.cfg"
+    cfg = P.load_config(cfg_path)
+    problem, lmesh = P.build_problem(cfg, device=local_rank)
+    sched = P.MacroSchedule(cfg.dt_macro, cfg.micro_steps, 0.0, cfg.t_end)
+    m = sched.micro_per_macro
+    Ng, Nl = problem.global_mesh.n_nodes, lmesh.n_nodes
+    dof_step = Ng + m * Nl
+    nsteps = args.skip + args.warmup + args.steps
+    if nsteps > sched.n_macro:
+        raise SystemExit(f"{args.config} has only {sched.n_macro} macro steps")
+
+    # per-step plans (host, outside the timed region)
+    plans = []
+    placement, tg, tl = lmesh.placement, 0.0, 0.0
+    for k in range(nsteps):
+        pl = plan_spacetime(problem, sched, placement, cfg.path, cfg.policy, tg, tl, k0=k, nsteps=1)
+        plans.append(pl)
+        placement, tg, tl = pl.final_placement, pl.final_t_global, pl.final_t_local
+
+    run = P.DeviceRun(problem, lmesh)
+    run.initial(P.uniform_field(problem.global_mesh, cfg.T_initial))
+    stream = torch.cuda.ExternalStream(run.stream(), device=torch.device("cuda", local_rank))
+    for k in range(args.skip + args.warmup):
+        run.run(plans[k])
+    run.sync()
+    run.check_solves(run.take_info())
+
+    # ---- timed region: K macro steps, per-step CUDA events on the run's stream ----
+    timed = plans[args.skip + args.warmup:]
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in timed]
+    run.set_timing(True)
+    run.take_timing()
+    launches0 = run.launch_count()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clocks:
+        wall0 = time.perf_counter()
+        for (e0, e1), pl in zip(ev, timed):
+            if not args.no_flush:
+                run.flush_l2()
+            e0.record(stream)
+            run.run(pl)
+            e1.record(stream)
+        run.sync()
+        wall = time.perf_counter() - wall0
+    torch.cuda.synchronize()
+    launches = run.launch_count() - launches0
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    dev_ms = float(sum(step_ms))
+    infos = run.take_info()
+    run.check_solves(infos)
+    kt = run.take_timing()
+    run.set_timing(False)
+    if dist is not None:
+        t = torch.tensor([dev_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_ms = float(t.item())
+
+    value = dof_step * len(timed) * world / (dev_ms / 1e3)
+
+    # ---- roofline of the dominant kernel (k_pcg on the local grid) ----
+    peak, peak_src = measured_peak()
+    loc = [(ms, inf["iterations"]) for (ms, lv), inf in zip(kt, infos) if lv == 1]
+    glo = [(ms, inf["iterations"]) for (ms, lv), inf in zip(kt, infos) if lv == 0]
+
+    def kstats(rows, n):
+        if not rows:
+            return None
+        bytes_ = sum(n * (64 * k + 32) for _, k in rows)
+        ms = sum(t for t, _ in rows)
+        return {"launches": len(rows), "avg_ms": ms / len(rows), "avg_iterations": float(np.mean([k for _, k in rows])),
+                "alg_bytes_per_launch": bytes_ / len(rows), "achieved_gbs": bytes_ / (ms / 1e3) / 1e9,
+                "share_of_step": ms / dev_ms if world == 1 else None}
+
+    kloc, kglo = kstats(loc, Nl), kstats(glo, Ng)
+    traffic = None
+    tfile = ROOT / "profiles" / "traffic.json"
+    if tfile.exists():
+        traffic = json.loads(tfile.read_text()).get(f"{args.config}_local_pcg_dram_bytes_per_launch")
+    roofline = {"bound": "hbm", "achieved": kloc["achieved_gbs"], "peak": peak, "unit": "GB/s",
+                "frac": kloc["achieved_gbs"] / peak, "traffic": traffic, "kernel": "k_pcg<true> (local solve)",
+                "peak_source": peak_src,
+                "note": "algorithmic bytes N(64k+32) per solve (SURVEY §8d); cfg2 vectors are L2-resident"}
+
+    # ---- e2e through the public API: pinned plan upload + field read-back every step ----
+    e2e = None
+    if rank == 0 or True:
+        pin_local = torch.empty(Nl, dtype=torch.float64, pin_memory=True).numpy()
+        e2e_plans = []
+        for pl in timed:
+            pinned = {}
+            for key in ("macro", "micro"):
+                arr = getattr(pl, key)
+                buf = torch.empty(arr.nbytes, dtype=torch.uint8, pin_memory=True).numpy().view(arr.dtype)
+                buf[:] = arr
+                pinned[key] = buf
+            for key in ("dep_points", "dep_power"):
+                arr = np.ascontiguousarray(getattr(pl, key), dtype=np.float64).reshape(-1)
+                buf = torch.empty(max(arr.size, 1), dtype=torch.float64, pin_memory=True).numpy()[:arr.size]
+                buf[:] = arr
+                pinned[key] = buf
+            e2e_plans.append(pinned)
+        # restart from the state after the timed region would differ; rewind a fresh run
+        run2 = P.DeviceRun(problem, lmesh)
+        run2.initial(P.uniform_field(problem.global_mesh, cfg.T_initial))
+        for k in range(args.skip + args.warmup):
+            run2.run(plans[k])
+        run2.sync()
+        h2d = d2h = 0
+        t0 = time.perf_counter()
+        for pl, pin in zip(timed, e2e_plans):
+            pl2 = type(pl)(macro=pin["macro"], micro=pin["micro"],
+                           dep_points=pin["dep_points"].reshape(-1, 3), dep_power=pin["dep_power"])
+            run2.run(pl2)
+            run2.field(1, out=pin_local)
+            h2d += pin["macro"].nbytes + pin["micro"].nbytes + pin["dep_points"].nbytes + pin["dep_power"].nbytes
+            d2h += pin_local.nbytes
+        e2e_s = time.perf_counter() - t0
+        run2.check_solves(run2.take_info())
+        run2.close()
+        e2e = {"value": dof_step * len(timed) * world / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": h2d // len(timed), "d2h_bytes_per_step": d2h // len(timed),
+               "note": "host wall clock through DeviceRun.run per macro step: plan arrays from pinned "
+                       "memory H2D, local field (the melt-pool grid) D2H to pinned memory every step"}
+    run.close()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        dof, dt, its = cpu_sample(cfg_path)
+        cpu = {"value": dof / dt, "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": f"one global + one local implicit step of {args.config} ({dof} DOF-timesteps, "
+                         f"{dt:.1f} s) via the literal P1-assembly + scipy-CG port (oracle/assembly.py, "
+                         "bitwise equal to lpbfsim); OPENBLAS_NUM_THREADS=1"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": len(timed),
+        "warmup": args.warmup, "ms_per_step": dev_ms / len(timed), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (BASELINE config 2 scan path and geometry; no dataset involved)",
+        "config": {"workload": f"{args.config}: two-level multirate macro step (1 global + {m} local "
+                               f"solves + corrector), global {Ng} + local {Nl} nodes",
+                   "config_file": f"configs/{args.config}.cfg", "dof_timesteps_per_step": dof_step,
+                   "macro_steps": f"{args.skip + args.warmup}..{nsteps - 1}",
+                   "l2": "flushed between timed steps" if not args.no_flush else "not flushed",
+                   "parallelism": f"scenario replicas x{world}" if world > 1 else "single GPU"},
+        "roofline": roofline, "kernels": {"local_pcg": kloc, "global_pcg": kglo},
+        "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+        "clocks": clocks.summary(), "wall_s_timed_region": wall,
+        "iterations": {"local": kloc["avg_iterations"] if kloc else None,
+                       "global": kglo["avg_iterations"] if kglo else None},
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -182,6 +182,12 @@ int32_t tl_run_melt_summary(tl_run* run, double T_liquidus, double* out4);
 int32_t tl_run_stream(tl_run* run, void** stream);
 /* Number of kernels launched on the run's stream since creation. */
 int64_t tl_run_launch_count(tl_run* run);
+/* Per-launch CUDA-event timing of the solve kernel (k_pcg) on the run's stream.
+ * When on, every solve launch is bracketed by an event pair; take_timing returns
+ * (after a sync) the durations in ms and the level (0 global, 1 local) of the
+ * launches since the last call, in launch order (same order as tl_run_take_info). */
+int32_t tl_run_set_timing(tl_run* run, int32_t on);
+int32_t tl_run_take_timing(tl_run* run, float* ms, int32_t* level, int32_t max, int32_t* count);
 /* Write a scratch buffer larger than L2 on the run's stream (bench hygiene). */
 int32_t tl_run_flush_l2(tl_run* run);
 

@@ -128,7 +128,31 @@ struct tl_run {
     double* snap_g = nullptr; std::vector<double*> snap_l; int snap_n = 0;
     double* flush = nullptr; size_t flush_n = 0;
     int64_t launches = 0;
+    bool timing = false;
+    std::vector<cudaEvent_t> ev;     // pairs
+    std::vector<int> ev_level;
+    int ev_n = 0;                    // pairs in use
 };
+
+static int timed_begin(tl_run* R, int level) {
+    if (!R->timing) return TL_OK;
+    while ((int)R->ev.size() < 2 * (R->ev_n + 1)) {
+        cudaEvent_t e;
+        TL_CUDA(cudaEventCreate(&e));
+        R->ev.push_back(e);
+    }
+    if ((int)R->ev_level.size() < R->ev_n + 1) R->ev_level.resize(R->ev_n + 1);
+    R->ev_level[R->ev_n] = level;
+    TL_CUDA(cudaEventRecord(R->ev[2 * R->ev_n], R->stream));
+    return TL_OK;
+}
+
+static int timed_end(tl_run* R) {
+    if (!R->timing) return TL_OK;
+    TL_CUDA(cudaEventRecord(R->ev[2 * R->ev_n + 1], R->stream));
+    ++R->ev_n;
+    return TL_OK;
+}
 
 extern "C" {
 
@@ -328,6 +352,7 @@ int32_t tl_run_destroy(tl_run* R) {
     if (R->dep_prev_n) cudaFree(R->dep_prev_n);
     if (R->info) cudaFree(R->info);
     if (R->snap_g) cudaFree(R->snap_g);
+    for (cudaEvent_t e : R->ev) cudaEventDestroy(e);
     for (double* b : R->snap_l) cudaFree(b);
     if (R->melt_host) cudaFreeHost(R->melt_host);
     if (R->stream) cudaStreamDestroy(R->stream);
@@ -414,7 +439,9 @@ static int local_solve(tl_run* R, double* T, const tl_micro_plan& mp) {
         P.src.on = 1;
     }
     P.info = R->info + R->info_n++;
-    return launch_pcg(P, gauss, R->sms, R->stream, &R->launches);
+    if (int rc = timed_begin(R, 1)) return rc;
+    if (int rc = launch_pcg(P, gauss, R->sms, R->stream, &R->launches)) return rc;
+    return timed_end(R);
 }
 
 int32_t tl_run_macro_steps(tl_run* R, const tl_macro_plan* plans, int32_t nsteps,
@@ -459,7 +486,9 @@ int32_t tl_run_macro_steps(tl_run* R, const tl_macro_plan* plans, int32_t nsteps
         P.g_const = R->desc.T_buildplate;
         P.load = R->loadg;
         P.info = R->info + R->info_n++;
+        if (int rc = timed_begin(R, 0)) return rc;
         if (int rc = launch_pcg(P, false, R->sms, R->stream, &R->launches)) return rc;
+        if (int rc = timed_end(R)) return rc;
         if (mp.record) {
             if (int rc = ensure_snapshots(R, mp.n_micro + mp.corrector)) return rc;
             TL_CUDA(cudaMemcpyAsync(R->snap_g, R->Tg, sizeof(double) * R->G.n, cudaMemcpyDeviceToDevice, R->stream));
@@ -569,6 +598,34 @@ int32_t tl_run_stream(tl_run* R, void** stream) {
 }
 
 int64_t tl_run_launch_count(tl_run* R) { return R ? R->launches : -1; }
+
+int32_t tl_run_set_timing(tl_run* R, int32_t on) {
+    if (!R) return fail(TL_E_INVALID, "null run");
+    R->timing = on != 0;
+    return TL_OK;
+}
+
+int32_t tl_run_take_timing(tl_run* R, float* ms, int32_t* level, int32_t max, int32_t* count) {
+    if (!R || !count) return fail(TL_E_INVALID, "null argument");
+    TL_CUDA(cudaSetDevice(R->device));
+    TL_CUDA(cudaStreamSynchronize(R->stream));
+    const int n = R->ev_n < max ? R->ev_n : max;
+    for (int e = 0; e < n; ++e) {
+        float t = 0.f;
+        TL_CUDA(cudaEventElapsedTime(&t, R->ev[2 * e], R->ev[2 * e + 1]));
+        ms[e] = t;
+        level[e] = R->ev_level[e];
+    }
+    // drop the pairs we returned (keep the rest in order)
+    for (int e = n; e < R->ev_n; ++e) {
+        std::swap(R->ev[2 * (e - n)], R->ev[2 * e]);
+        std::swap(R->ev[2 * (e - n) + 1], R->ev[2 * e + 1]);
+        R->ev_level[e - n] = R->ev_level[e];
+    }
+    R->ev_n -= n;
+    *count = n;
+    return TL_OK;
+}
 
 int32_t tl_run_flush_l2(tl_run* R) {
     if (!R) return fail(TL_E_INVALID, "null run");

@@ -94,9 +94,9 @@ class DeviceRun:
             a = np.ascontiguousarray(v, dtype=np.float64)
             N.check(N.lib().tl_run_set_global(self._h, N.dptr(a), a.size), "tl_run_set_global")
 
-    def field(self, which: int) -> np.ndarray:
+    def field(self, which: int, out: np.ndarray | None = None) -> np.ndarray:
         n = self.n_global if which == 0 else self.n_local
-        out = np.empty(n)
+        out = np.empty(n) if out is None else out
         N.check(N.lib().tl_run_get_field(self._h, which, N.dptr(out), n), "tl_run_get_field")
         return out
 
@@ -149,6 +149,22 @@ class DeviceRun:
 
     def launch_count(self) -> int:
         return int(N.lib().tl_run_launch_count(self._h))
+
+    def set_timing(self, on: bool = True):
+        N.check(N.lib().tl_run_set_timing(self._h, int(on)), "set_timing")
+
+    def take_timing(self):
+        """[(ms, level)] of the solve launches since the last call (level 0 global, 1 local)."""
+        out = []
+        ms = (C.c_float * 4096)()
+        lv = (C.c_int32 * 4096)()
+        cnt = C.c_int32()
+        while True:
+            N.check(N.lib().tl_run_take_timing(self._h, ms, lv, 4096, C.byref(cnt)), "take_timing")
+            out.extend((float(ms[e]), int(lv[e])) for e in range(cnt.value))
+            if cnt.value < 4096:
+                break
+        return out
 
     def flush_l2(self):
         N.check(N.lib().tl_run_flush_l2(self._h), "flush")

@@ -1,0 +1,233 @@
+"""Device parity: the CUDA path through the C ABI against the oracle and the golden vectors.
+
+Tolerance (north_star): relative L-inf <= 1e-9 per step with CG tolerance 1e-12,
+melt masks (T > T_liquidus) bit-exact, CG iteration counts within +-1 of the
+reference's.  Single steps are held to 1e-12 (the device mirrors scipy's CG
+operation for operation; only summation order differs).
+"""
+
+import json
+
+import numpy as np
+import pytest
+
+import paper_2110_12932_b200 as P
+from paper_2110_12932_b200 import _native as N
+from paper_2110_12932_b200 import ops
+from paper_2110_12932_b200.errors import NonConvergence
+from paper_2110_12932_b200.grid import StructuredGrid
+from paper_2110_12932_b200.control import LocalPlacement
+from oracle import kuhn
+from oracle.twolevel import OracleRun
+
+from .conftest import CONFIGS, GOLDEN
+
+pytestmark = pytest.mark.gpu
+REL = 1e-9
+
+
+def rel(a, b):
+    return float(np.abs(np.asarray(a) - np.asarray(b)).max() / np.abs(np.asarray(b)).max())
+
+
+def _grid(lo, hi, n, off=(0.0, 0.0, 0.0)):
+    box = P.Box(tuple(lo), tuple(hi))
+    return StructuredGrid(LocalPlacement(box, np.asarray(n), np.asarray(off, dtype=float),
+                                         box.translated(off)))
+
+
+@pytest.mark.parametrize("name", ["aniso_local", "aniso_global", "cfg1_local", "cfg1_global"])
+def test_single_step_vs_reference_golden(name):
+    z = np.load(GOLDEN / f"op_{name}.npz")
+    grid = _grid(z["lo"], z["hi"], z["ncells"])
+    local = str(z["kind"]) == "local"
+    g = np.zeros(grid.n_nodes)
+    g[z["dnodes"]] = z["dvals"]
+    beam = P.LaserBeam(200.0, 0.35, 5e-5, 5e-5, 0.8)
+    x, info = ops.step(grid, 9.8, 8440 * 410.0, float(z["dt"]),
+                       N.TL_DIRICHLET_GAMMA if local else N.TL_DIRICHLET_BOTTOM, z["T_old"],
+                       g=g, load=None if local else z["extra"],
+                       gaussian=(beam.gaussian_peak, beam.radius, beam.depth, z["center"]) if local else None,
+                       rtol=1e-12)
+    assert info.status == 0
+    assert abs(info.iterations - int(z["cg_iters"])) <= 1
+    assert rel(x, z["sol"]) <= 1e-12
+    assert info.true_resid <= 100 * 1e-12
+
+
+def test_step_backward_euler_seam():
+    """Seam 3: fem.step_backward_euler with reference-shaped arguments."""
+    z = np.load(GOLDEN / "op_cfg1_local.npz")
+    grid = _grid(z["lo"], z["hi"], z["ncells"])
+    mat = P.load_material(CONFIGS / "const.mat")
+    beam = P.LaserBeam(200.0, 0.35, 5e-5, 5e-5, 0.8)
+    bounds = P.BoundarySpec(bc=P.ThermalBC(0.0, 0.0, 293.0, 293.0), radiation=True,
+                            dirichlet_nodes=z["dnodes"], dirichlet_values=z["dvals"])
+    st = P.FieldState(grid, z["T_old"], 0.0)
+    out = P.step_backward_euler(st, float(z["dt"]), mat, P.GaussianSource(beam, tuple(z["center"])),
+                                bounds, P.SolverSettings(linear_tol=1e-12, linear_solver="cg"),
+                                latent=True)
+    assert out.time == float(z["dt"])
+    assert rel(out.values, z["sol"]) <= 1e-12
+
+
+def test_nonconvergence_maps_to_reference_exception():
+    z = np.load(GOLDEN / "op_cfg1_global.npz")
+    grid = _grid(z["lo"], z["hi"], z["ncells"])
+    x, info = ops.step(grid, 9.8, 8440 * 410.0, float(z["dt"]), N.TL_DIRICHLET_BOTTOM, z["T_old"],
+                       g_const=293.0, load=z["extra"], rtol=1e-12, maxiter=2)
+    assert info.status == N.TL_SOLVE_MAXITER and info.iterations == 2
+    with pytest.raises(NonConvergence) as exc:
+        ops.raise_for(info)
+    assert exc.value.iterations == 2
+
+
+def test_interpolation_points_vs_golden():
+    z = np.load(GOLDEN / "interp.npz")
+    box = P.Box(tuple(z["lo"]), tuple(z["hi"]))
+    grid = P.build_structured_grid(box, float(z["h"]))
+    out = grid.interpolate(z["vals"], z["pts"])
+    assert rel(out, z["out"]) <= 1e-14
+
+
+def test_interpolation_to_translated_lattice_vs_oracle():
+    rng = np.random.default_rng(3)
+    G = P.build_structured_grid(P.Box((0, 0, 0), (2e-3, 1e-3, 5e-4)), 5e-5)
+    vals = rng.uniform(293, 2293, G.n_nodes)
+    L = StructuredGrid(LocalPlacement(P.Box((3.3e-4, 2.1e-4, 1e-4), (7.3e-4, 6.1e-4, 3e-4)),
+                                      np.array([40, 40, 20]))).translated((1.7e-5, -3e-5, 0.0))
+    full = ops.interpolate_to_grid(G, vals, L)
+    ref = kuhn.interpolate(kuhn.KuhnGrid(G.box.lo, G.box.hi, G.ncells), vals, L.coords)
+    assert rel(full, ref) <= 1e-14
+    gam = ops.interpolate_to_grid(G, vals, L, gamma_only=True)
+    m = L.gamma_mask()
+    assert rel(gam[m], ref[m]) <= 1e-14 and np.all(gam[~m] == 0.0)
+
+
+def test_deposit_vs_golden():
+    d = json.loads((GOLDEN / "deposit.json").read_text())
+    grid = P.build_structured_grid(P.Box(tuple(d["lo"]), tuple(d["hi"])), d["h"])
+    for c in d["cases"]:
+        load = ops.deposit_load(grid, np.array(c["pts"]).reshape(-1, 3), np.array(c["pw"]))
+        nz = np.nonzero(load)[0]
+        np.testing.assert_array_equal(nz, c["idx"])
+        assert rel(load[nz], c["val"]) <= 1e-13
+
+
+def _golden_run(name, n_steps=None):
+    z = np.load(GOLDEN / f"run_{name}.npz")
+    cfg = P.load_config(CONFIGS / f"{name}.cfg")
+    rec = []
+
+    def recorder(kind, t, local, glob, iters):
+        if kind in ("initial", "macro"):
+            rec.append((t, local.values.copy(), glob.values.copy(), local.mesh.box.lo))
+
+    state, stats = P.two_level_run(cfg, recorder=recorder, n_steps=n_steps)
+    return z, cfg, rec, stats
+
+
+@pytest.mark.parametrize("name", ["cfg1_m4", "cfg1_uniform"])
+def test_full_run_cfg1_vs_reference(name):
+    z, cfg, rec, stats = _golden_run(name)
+    counters = json.loads(str(z["counters"]))
+    assert stats.counters == counters
+    TL = cfg.material.T_liquidus
+    s = int(z["stride"])
+    worst = 0.0
+    for k, (t, Tl, Tg, lo) in enumerate(rec):
+        assert t == z["t"][k]
+        np.testing.assert_array_equal(lo, z["box"][k])
+        worst = max(worst, rel(Tg[::s], z["gsub"][k]), rel(Tl[::s], z["lsub"][k]))
+        np.testing.assert_array_equal(np.packbits(Tg > TL), z["gmelt"][k])
+        np.testing.assert_array_equal(np.packbits(Tl > TL), z["lmelt"][k])
+        if k in z["full_at"]:
+            assert rel(Tg, z[f"g{k}"]) <= REL
+            assert rel(Tl, z[f"l{k}"]) <= REL
+    assert worst <= REL
+
+
+def test_device_iterations_match_reference_cfg1():
+    z = np.load(GOLDEN / "run_cfg1_m4.npz")
+    cfg = P.load_config(CONFIGS / "cfg1_m4.cfg")
+    problem, lm = P.build_problem(cfg)
+    sched = P.MacroSchedule(cfg.dt_macro, cfg.micro_steps, 0.0, cfg.t_end)
+    with P.DeviceRun(problem, lm) as run:
+        from paper_2110_12932_b200.schedule import plan_spacetime
+        run.initial(P.uniform_field(problem.global_mesh, 293.0))
+        run.run(plan_spacetime(problem, sched, lm.placement, cfg.path, cfg.policy, 0.0, 0.0))
+        its = [i["iterations"] for i in run.take_info()]
+    ref = z["cg_iters"]
+    assert len(its) == len(ref)
+    assert max(abs(a - b) for a, b in zip(its, ref)) <= 1
+
+
+def test_cfg2_first_steps_vs_reference():
+    z, cfg, rec, stats = _golden_run("cfg2", n_steps=2)
+    TL = cfg.material.T_liquidus
+    s = int(z["stride"])
+    for k, (t, Tl, Tg, lo) in enumerate(rec):
+        assert rel(Tg[::s], z["gsub"][k]) <= REL and rel(Tl[::s], z["lsub"][k]) <= REL
+        np.testing.assert_array_equal(np.packbits(Tg > TL), z["gmelt"][k])
+        np.testing.assert_array_equal(np.packbits(Tl > TL), z["lmelt"][k])
+        if k in z["full_at"]:
+            assert rel(Tg, z[f"g{k}"]) <= REL and rel(Tl, z[f"l{k}"]) <= REL
+
+
+def test_cfg2_twelve_steps_vs_oracle():
+    """Full-size cfg2 grids, 12 macro steps (track start, relocations) against the oracle."""
+    cfg = P.load_config(CONFIGS / "cfg2.cfg")
+    orc = OracleRun(cfg)
+    ref = []
+    orc.run_spacetime(n_steps=12, recorder=lambda kind, t, Tl, Tg, pl: ref.append((Tl, Tg)))
+    rec = []
+    P.two_level_run(cfg, n_steps=12,
+                    recorder=lambda kind, t, l, g, it: rec.append((l.values, g.values))
+                    if kind in ("initial", "macro") else None)
+    TL = cfg.material.T_liquidus
+    for (Tl, Tg), (Rl, Rg) in zip(rec, ref):
+        assert rel(Tg, Rg) <= REL and rel(Tl, Rl) <= REL
+        assert np.array_equal(Tg > TL, Rg > TL) and np.array_equal(Tl > TL, Rl > TL)
+
+
+def test_recorder_protocol_kinds_and_times():
+    cfg = P.load_config(CONFIGS / "cfg1_m4.cfg")
+    kinds = []
+    P.two_level_run(cfg, n_steps=2, recorder=lambda kind, t, l, g, it: kinds.append(
+        (kind, t, l is None, g is None, it)))
+    sched = P.MacroSchedule(cfg.dt_macro, 4, 0.0, 2 * cfg.dt_macro)
+    expect = [("initial", 0.0, False, False, 0)]
+    for k in range(2):
+        expect.append(("predictor", sched.t_macro(k + 1), True, False, 0))
+        expect += [("micro", sched.t_micro(k, i + 1), False, True, 0) for i in range(4)]
+        expect.append(("macro", sched.t_macro(k + 1), False, False, 1))
+    assert kinds == expect
+
+
+def test_run_without_recorder_matches_recorded_run():
+    cfg = P.load_config(CONFIGS / "cfg1_m4.cfg")
+    a, _ = P.two_level_run(cfg, n_steps=6)
+    b, _ = P.two_level_run(cfg, n_steps=6, recorder=lambda *args: None)
+    np.testing.assert_array_equal(a.global_field.values, b.global_field.values)
+    np.testing.assert_array_equal(a.local_field.values, b.local_field.values)
+    assert a.local_field.mesh.box == b.local_field.mesh.box
+
+
+def test_deterministic_run_to_run():
+    cfg = P.load_config(CONFIGS / "cfg1_m4.cfg")
+    a, _ = P.two_level_run(cfg, n_steps=5)
+    b, _ = P.two_level_run(cfg, n_steps=5)
+    np.testing.assert_array_equal(a.global_field.values, b.global_field.values)
+    np.testing.assert_array_equal(a.local_field.values, b.local_field.values)
+
+
+def test_source_off_after_path_end():
+    """Past t_end the Gaussian and the deposit vanish (runner.py:54-55, scanpath.py:103-106)."""
+    text = (CONFIGS / "cfg1_m4.cfg").read_text().replace("t_end 2 ms", "t_end 2.1 ms")
+    cfg = P.config_from_text(text, CONFIGS)
+    orc = OracleRun(cfg)
+    ref = []
+    orc.run_spacetime(recorder=lambda kind, t, Tl, Tg, pl: ref.append((Tl, Tg)))
+    state, _ = P.two_level_run(cfg)
+    assert rel(state.global_field.values, ref[-1][1]) <= REL
+    assert rel(state.local_field.values, ref[-1][0]) <= REL

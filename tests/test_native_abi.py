@@ -1,0 +1,59 @@
+"""libtlgpu.so builds for sm_100a, loads, and exports every symbol include/tlgpu.h declares.
+
+CPU-only: no compute call is made (there is no GPU in the build container).
+"""
+
+import ctypes
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from paper_2110_12932_b200 import _native as N
+from paper_2110_12932_b200.build import OUT, build
+
+from .conftest import ROOT
+
+
+def header_functions():
+    text = (ROOT / "include" / "tlgpu.h").read_text()
+    return sorted(set(re.findall(r"^\s*(?:int32_t|int64_t|const char\*)\s+(tl_\w+)\s*\(", text, re.M)))
+
+
+@pytest.fixture(scope="module")
+def lib_path():
+    return build()
+
+
+def test_library_exports_header_symbols(lib_path):
+    lib = ctypes.CDLL(str(lib_path))
+    declared = header_functions()
+    assert len(declared) >= 18
+    for name in declared:
+        assert hasattr(lib, name), name
+    # the ctypes binding covers exactly the header
+    assert sorted(n for n, _, _ in N.SIGNATURES) == declared
+
+
+def test_binding_loads_and_reports_abi(lib_path):
+    lib = N.lib()
+    assert lib.tl_abi_version() == N.ABI_VERSION
+
+
+def test_plan_struct_layouts_match_header():
+    assert N.MACRO_DTYPE.itemsize == ctypes.sizeof(N.MacroPlan) == 64
+    assert N.MICRO_DTYPE.itemsize == ctypes.sizeof(N.MicroPlan) == 48
+
+
+def test_sass_is_sm100a(lib_path):
+    out = subprocess.run(["cuobjdump", "--list-elf", str(lib_path)], capture_output=True, text=True)
+    assert "sm_100a" in out.stdout
+
+
+def test_no_cpu_fallback_when_library_missing(monkeypatch, tmp_path):
+    monkeypatch.setattr(N, "_lib", None)
+    monkeypatch.setenv("TLGPU_LIB", str(tmp_path / "missing.so"))
+    with pytest.raises(N.NativeLibraryMissing):
+        N.lib()
+    monkeypatch.setattr(N, "_lib", None)
