@@ -28,7 +28,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from ._native import MACRO_DTYPE, MICRO_DTYPE
-from .control import LocalPlacement, MacroSchedule
+from .control import LocalPlacement, MacroSchedule, check_immersed
 
 
 def swept_samples(beam, pieces, dt: float):
@@ -138,6 +138,9 @@ class _Builder:
                                    self.problem.global_mesh.box)
         if moved is None:
             return placement, False
+        # relocate_local re-extracts the interface (scanpath.py:244): strict immersion
+        gm = self.problem.global_mesh
+        check_immersed(moved.box, gm.box, gm.h)
         self.count("relocations")
         return moved, True
 

@@ -222,8 +222,10 @@ def test_deterministic_run_to_run():
 
 
 def test_source_off_after_path_end():
-    """Past t_end the Gaussian and the deposit vanish (runner.py:54-55, scanpath.py:103-106)."""
-    text = (CONFIGS / "cfg1_m4.cfg").read_text().replace("t_end 2 ms", "t_end 2.1 ms")
+    """Past the path's end the Gaussian and the deposit vanish (runner.py:54-55,
+    scanpath.py:103-106); the laser stops at x = 1.6 mm at t = 1.75 ms of a 2 ms run."""
+    text = (CONFIGS / "cfg1_m4.cfg").read_text().replace("segment 0.2 0.5 0.5 1.8 0.5 0.5 mm",
+                                                         "segment 0.2 0.5 0.5 1.6 0.5 0.5 mm")
     cfg = P.config_from_text(text, CONFIGS)
     orc = OracleRun(cfg)
     ref = []
@@ -231,3 +233,12 @@ def test_source_off_after_path_end():
     state, _ = P.two_level_run(cfg)
     assert rel(state.global_field.values, ref[-1][1]) <= REL
     assert rel(state.local_field.values, ref[-1][0]) <= REL
+
+
+def test_box_reaching_the_wall_raises_like_the_reference():
+    """A relocation that lands the box on the global wall passes Mesh.translated's
+    test but fails extract_interface's strict immersion (mesh.py:489-496) -> MeshError."""
+    text = (CONFIGS / "cfg1_m4.cfg").read_text().replace("t_end 2 ms", "t_end 2.1 ms")
+    cfg = P.config_from_text(text, CONFIGS)
+    with pytest.raises(P.MeshError):
+        P.two_level_run(cfg)
