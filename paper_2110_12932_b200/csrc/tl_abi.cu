@@ -9,13 +9,15 @@
 //   [k_pcg<true>]        corrector re-solve of the last interval         (multirate.py:149-150)
 //   k_interp (all)       relocation: local = P1(global) at moved nodes  (scanpath.py:243-248)
 // All state stays on the device; the host only enqueues launches.
+#include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
 
 #include "../../include/tlgpu.h"
-#include "tl_kernels.cuh"
+#include "tl_resident.cuh"
 
 namespace {
 
@@ -91,6 +93,112 @@ int launch_pcg(tl::PcgParams& P, bool gauss, int sms, cudaStream_t st, int64_t* 
     return TL_OK;
 }
 
+// ---- SMEM-resident brick PCG: decomposition + launch ------------------------------
+struct BrickPlan {
+    bool ok = false;
+    int ng[3] = {1, 1, 1};
+    int maxnodes = 0;
+    size_t smem = 0;
+    int npt = 0;
+};
+
+static void split_axis(int N, int parts, int* off) {
+    for (int e = 0; e <= parts; ++e) off[e] = (int)((long long)N * e / parts);
+}
+
+static BrickPlan plan_bricks(const tl::Grid& g, bool gauss, int sms, size_t smem_cap) {
+    BrickPlan best;
+    const int N[3] = {g.NX, g.NY, g.NZ};
+    const long long n = (long long)g.n;
+    // small grids: fewer, larger bricks (cheaper barriers); large: one brick per SM
+    int target = (int)std::min<long long>(sms, std::max<long long>(1, (n + 2047) / 2048));
+    const size_t gtab = gauss ? sizeof(double) * 6 * (size_t)(g.nc[0] + g.nc[1] + g.nc[2]) : 0;
+    double best_cost = 1e300;
+    for (int gx = 1; gx <= std::min(N[0], tl::kResMaxSplit); ++gx)
+        for (int gy = 1; gy <= std::min(N[1], tl::kResMaxSplit); ++gy)
+            for (int gz = 1; gz <= std::min(N[2], tl::kResMaxSplit); ++gz) {
+                const int G = gx * gy * gz;
+                if (G > target || G > tl::kResMaxBlocks) continue;
+                const int lx = (N[0] + gx - 1) / gx, ly = (N[1] + gy - 1) / gy, lz = (N[2] + gz - 1) / gz;
+                const int own = lx * ly * lz;
+                const size_t H = (size_t)(lx + 2) * (ly + 2) * (lz + 2);
+                const size_t smem = gtab + H * 25 + 64;
+                if (own > 12 * tl::kResTPB || smem > smem_cap || H >= 16384) continue;
+                // cost: max work per CTA, then halo, then fewer CTAs
+                const double cost = (double)own * 1.0 + 0.25 * (double)(H - own) + 0.01 * G;
+                if (cost < best_cost) {
+                    best_cost = cost;
+                    best.ok = true;
+                    best.ng[0] = gx; best.ng[1] = gy; best.ng[2] = gz;
+                    best.maxnodes = own;
+                    best.smem = smem;
+                }
+            }
+    if (best.ok) {
+        int npt = (best.maxnodes + tl::kResTPB - 1) / tl::kResTPB;
+        best.npt = npt <= 2 ? 2 : npt <= 4 ? 4 : npt <= 6 ? 6 : npt <= 8 ? 8 : npt <= 10 ? 10 : 12;
+    }
+    return best;
+}
+
+template <bool GAUSS, int NPT>
+static cudaError_t launch_res_t(tl::ResParams& RP, int G, size_t smem, cudaStream_t st) {
+    auto fn = tl::k_pcg_resident<GAUSS, NPT>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    void* args[] = {&RP};
+    return cudaLaunchCooperativeKernel((void*)fn, G, tl::kResTPB, args, smem, st);
+}
+
+template <bool GAUSS>
+static cudaError_t launch_res_g(tl::ResParams& RP, int npt, int G, size_t smem, cudaStream_t st) {
+    switch (npt) {
+        case 2: return launch_res_t<GAUSS, 2>(RP, G, smem, st);
+        case 4: return launch_res_t<GAUSS, 4>(RP, G, smem, st);
+        case 6: return launch_res_t<GAUSS, 6>(RP, G, smem, st);
+        case 8: return launch_res_t<GAUSS, 8>(RP, G, smem, st);
+        case 10: return launch_res_t<GAUSS, 10>(RP, G, smem, st);
+        default: return launch_res_t<GAUSS, 12>(RP, G, smem, st);
+    }
+}
+
+static int g_force_streaming = -1;
+
+static bool force_streaming() {
+    if (g_force_streaming < 0) {
+        const char* e = getenv("TLGPU_STREAMING");
+        g_force_streaming = (e && e[0] == '1') ? 1 : 0;
+    }
+    return g_force_streaming == 1;
+}
+
+// Resident kernel when the grid fits on-chip, streaming k_pcg otherwise.
+static int launch_solve(tl::PcgParams& P, bool gauss, int sms, double* xg, cudaStream_t st,
+                        int64_t* launches, int* kind_out = nullptr) {
+    if (xg && !force_streaming()) {
+        BrickPlan bp = plan_bricks(P.g, gauss, sms, 200 * 1024);
+        if (bp.ok) {
+            tl::ResParams RP{};
+            RP.P = P;
+            RP.xg = xg;
+            const int N[3] = {P.g.NX, P.g.NY, P.g.NZ};
+            for (int a = 0; a < 3; ++a) {
+                RP.ng[a] = bp.ng[a];
+                split_axis(N[a], bp.ng[a], RP.off[a]);
+            }
+            const int G = bp.ng[0] * bp.ng[1] * bp.ng[2];
+            cudaError_t e = gauss ? launch_res_g<true>(RP, bp.npt, G, bp.smem, st)
+                                  : launch_res_g<false>(RP, bp.npt, G, bp.smem, st);
+            if (e != cudaSuccess) return fail(TL_E_CUDA, std::string("k_pcg_resident launch: ") + cudaGetErrorString(e));
+            if (launches) ++*launches;
+            if (kind_out) *kind_out = 1;
+            return TL_OK;
+        }
+    }
+    if (kind_out) *kind_out = 0;
+    return launch_pcg(P, gauss, sms, st, launches);
+}
+
 void set_coeffs(tl::PcgParams& P, double kappa, double rho_c, double dt) {
     const double V = P.g.h[0] * P.g.h[1] * P.g.h[2];
     for (int a = 0; a < 3; ++a) P.cbase[a] = kappa * V / (P.g.h[a] * P.g.h[a]) / 6.0;
@@ -126,6 +234,7 @@ struct tl_run {
     tl::SolveInfoDev* info = nullptr; int info_cap = 0; int info_n = 0;
     double* melt = nullptr; double* melt_part = nullptr; double* melt_host = nullptr;
     double* snap_g = nullptr; std::vector<double*> snap_l; int snap_n = 0;
+    double* xg = nullptr;            // exchange array of the resident kernel
     double* flush = nullptr; size_t flush_n = 0;
     int64_t launches = 0;
     bool timing = false;
@@ -220,7 +329,9 @@ int32_t tl_step_host(const tl_grid_desc* grid, double kappa, double rho_c, doubl
         for (int a = 0; a < 3; ++a) P.src.center[a] = src->center[a];
         P.src.on = 1;
     }
-    rc = launch_pcg(P, gauss, sms, 0, nullptr);
+    double* xg = nullptr;
+    if ((rc = dalloc(&xg, n))) return rc;
+    rc = launch_solve(P, gauss, sms, xg, 0, nullptr);
     if (rc) return rc;
     TL_CUDA(cudaDeviceSynchronize());
     tl::SolveInfoDev hi{};
@@ -231,7 +342,7 @@ int32_t tl_step_host(const tl_grid_desc* grid, double kappa, double rho_c, doubl
         info->rnorm = hi.rnorm; info->true_resid = hi.true_resid;
     }
     cudaFree(T); cudaFree(b); cudaFree(r); cudaFree(p0); cudaFree(p1); cudaFree(q); cudaFree(part);
-    cudaFree(dinfo); if (dA) cudaFree(dA); if (dB) cudaFree(dB); if (dload) cudaFree(dload);
+    cudaFree(dinfo); cudaFree(xg); if (dA) cudaFree(dA); if (dB) cudaFree(dB); if (dload) cudaFree(dload);
     return TL_OK;
 }
 
@@ -326,7 +437,8 @@ int32_t tl_run_create(const tl_run_desc* desc, tl_run** out) {
         (rc = dalloc(&R->ql, nl)) || (rc = dalloc(&R->tr_old, nl)) || (rc = dalloc(&R->tr_pred, nl)) ||
         (rc = dalloc(&R->Tl_before, nl)) || (rc = dalloc(&R->part, 4 * R->sms * 32)) ||
         (rc = dalloc(&R->dep_prev, tl::kDepMax)) || (rc = dalloc(&R->dep_prev_n, 1)) ||
-        (rc = dalloc(&R->melt, 4)) || (rc = dalloc(&R->melt_part, 2 * 1184))) {
+        (rc = dalloc(&R->melt, 4)) || (rc = dalloc(&R->melt_part, 2 * 1184)) ||
+        (rc = dalloc(&R->xg, std::max(ng, nl)))) {
         tl_run_destroy(R);
         return rc;
     }
@@ -345,7 +457,7 @@ int32_t tl_run_destroy(tl_run* R) {
     if (R->stream) cudaStreamSynchronize(R->stream);
     double* bufs[] = {R->Tg, R->bg, R->rg, R->pg0, R->pg1, R->qg, R->loadg, R->Tl, R->bl, R->rl, R->pl0,
                       R->pl1, R->ql, R->tr_old, R->tr_pred, R->Tl_before, R->part, R->dep_pts,
-                      R->dep_pow, R->melt, R->melt_part, R->flush};
+                      R->dep_pow, R->melt, R->melt_part, R->flush, R->xg};
     for (double* b : bufs)
         if (b) cudaFree(b);
     if (R->dep_prev) cudaFree(R->dep_prev);
@@ -440,7 +552,7 @@ static int local_solve(tl_run* R, double* T, const tl_micro_plan& mp) {
     }
     P.info = R->info + R->info_n++;
     if (int rc = timed_begin(R, 1)) return rc;
-    if (int rc = launch_pcg(P, gauss, R->sms, R->stream, &R->launches)) return rc;
+    if (int rc = launch_solve(P, gauss, R->sms, R->xg, R->stream, &R->launches)) return rc;
     return timed_end(R);
 }
 
@@ -487,7 +599,7 @@ int32_t tl_run_macro_steps(tl_run* R, const tl_macro_plan* plans, int32_t nsteps
         P.load = R->loadg;
         P.info = R->info + R->info_n++;
         if (int rc = timed_begin(R, 0)) return rc;
-        if (int rc = launch_pcg(P, false, R->sms, R->stream, &R->launches)) return rc;
+        if (int rc = launch_solve(P, false, R->sms, R->xg, R->stream, &R->launches)) return rc;
         if (int rc = timed_end(R)) return rc;
         if (mp.record) {
             if (int rc = ensure_snapshots(R, mp.n_micro + mp.corrector)) return rc;

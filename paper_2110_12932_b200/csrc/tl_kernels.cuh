@@ -118,6 +118,33 @@ __device__ __forceinline__ void grid_sum(const double* part, const int (&slot)[N
     __syncthreads();
 }
 
+constexpr int kResMaxBlocks = 512;
+
+// Fixed-order, load-parallel sum of G <= kResMaxBlocks partials (all blocks agree bitwise).
+template <int NV>
+__device__ __forceinline__ void grid_sum_fast(const double* part, const int (&slot)[NV], int G,
+                                              double* smem_out) {
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            const double* p = part + slot[k] * G;
+            double v[kResMaxBlocks / 32];
+#pragma unroll
+            for (int t = 0; t < kResMaxBlocks / 32; ++t) {
+                const int b = lane + 32 * t;
+                v[t] = b < G ? __ldcg(p + b) : 0.0;
+            }
+            double s = 0.0;
+#pragma unroll
+            for (int t = 0; t < kResMaxBlocks / 32; ++t) s += v[t];
+            s = warp_sum(s);
+            if (lane == 0) smem_out[k] = s;
+        }
+    }
+    __syncthreads();
+}
+
 // Dirichlet value at node p.
 __device__ __forceinline__ double dirichlet_value(const PcgParams& P, int p) {
     if (P.gA == nullptr) return P.g_const;
@@ -285,7 +312,7 @@ __global__ void __launch_bounds__(kTPB) k_pcg(PcgParams P) {
     grid.sync();
     {
         const int s[2] = {0, 1};
-        grid_sum<2>(P.part, s, G, tot);
+        grid_sum_fast<2>(P.part, s, G, tot);
     }
     const double bb = tot[0];
     double rz = tot[1];
@@ -330,7 +357,7 @@ __global__ void __launch_bounds__(kTPB) k_pcg(PcgParams P) {
             grid.sync();
             {
                 const int s[1] = {2};
-                grid_sum<1>(P.part, s, G, tot);
+                grid_sum_fast<1>(P.part, s, G, tot);
             }
             const double alpha = rho / tot[0];
             // ---- phase B ----
@@ -353,7 +380,7 @@ __global__ void __launch_bounds__(kTPB) k_pcg(PcgParams P) {
             grid.sync();
             {
                 const int s[2] = {0, 1};
-                grid_sum<2>(P.part, s, G, tot);
+                grid_sum_fast<2>(P.part, s, G, tot);
             }
             rz = tot[0];
             rnorm = sqrt(tot[1]);
@@ -382,7 +409,7 @@ __global__ void __launch_bounds__(kTPB) k_pcg(PcgParams P) {
     grid.sync();
     {
         const int s[2] = {0, 3};
-        grid_sum<2>(P.part, s, G, tot);
+        grid_sum_fast<2>(P.part, s, G, tot);
     }
     const double tres = bnorm > 0.0 ? sqrt(tot[0]) / bnorm : 0.0;
     // ---- re-impose Dirichlet values (fem.py:289-290): x_D = g = b_D ----

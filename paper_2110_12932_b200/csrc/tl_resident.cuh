@@ -1,0 +1,308 @@
+// tl_resident.cuh — SMEM-resident brick PCG for grids that fit on-chip (sm_100a, fp64).
+//
+// Same algorithm, operator and stopping rule as k_pcg (scipy cg mirrored, see
+// tl_kernels.cuh), different data placement.  The grid is cut into one brick per
+// SM.  Each CTA keeps its brick's p (with a one-node halo), r (with halo) and x in
+// shared memory and q in registers for the whole solve; per iteration only the
+// brick-surface values of r cross CTAs (written to a global exchange array before a
+// grid barrier, read back into the neighbours' halos after it).  The halo p values
+// are advanced by the same recurrence p = beta p + M^-1 r as their owners, so they
+// stay bitwise identical without a second exchange.  Two grid barriers per
+// iteration carry the two CG reductions (p.q, then r.z and r.r).
+#pragma once
+
+#include "tl_kernels.cuh"
+
+namespace tl {
+
+constexpr int kResTPB = 512;
+constexpr int kResMaxSplit = 64;
+constexpr uint8_t kNoNode = 27;
+
+struct ResParams {
+    PcgParams P;                  // grid, coefficients, inputs, workspace (b, part, info)
+    double* xg;                   // global exchange array (brick-surface values), n doubles
+    int ng[3];                    // bricks per axis
+    int off[3][kResMaxSplit + 1]; // brick boundaries per axis (node indices)
+};
+
+// own-node descriptor bits: [0,14) smem index, [14,20) free-neighbour mask
+// (x-, x+, y-, y+, z-, z+), [20,25) class, bit 25 brick-surface node.
+__device__ __forceinline__ int od_s(int d) { return d & 0x3fff; }
+__device__ __forceinline__ int od_mask(int d) { return (d >> 14) & 0x3f; }
+__device__ __forceinline__ int od_cls(int d) { return (d >> 20) & 0x1f; }
+__device__ __forceinline__ bool od_surf(int d) { return (d >> 25) & 1; }
+
+template <bool GAUSS, int NPT>
+__global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident(ResParams RP) {
+    cg::grid_group grid = cg::this_grid();
+    const PcgParams& P = RP.P;
+    const Grid& g = P.g;
+    __shared__ ClassTable T;
+    __shared__ double red[4 * 32];
+    __shared__ double tot[4];
+    extern __shared__ __align__(16) unsigned char smem[];
+
+    // ---- brick of this CTA ----
+    const int G = gridDim.x;
+    const int b = blockIdx.x;
+    const int bxi = b % RP.ng[0], byi = (b / RP.ng[0]) % RP.ng[1], bzi = b / (RP.ng[0] * RP.ng[1]);
+    const int x0 = RP.off[0][bxi], y0 = RP.off[1][byi], z0 = RP.off[2][bzi];
+    const int lx = RP.off[0][bxi + 1] - x0, ly = RP.off[1][byi + 1] - y0, lz = RP.off[2][bzi + 1] - z0;
+    const int LX = lx + 2, LY = ly + 2, LZ = lz + 2;
+    const int H = LX * LY * LZ;
+    const int SY = LX, SZ = LX * LY;
+
+    int gtab_n = GAUSS ? 6 * (g.nc[0] + g.nc[1] + g.nc[2]) : 0;
+    double* tx = reinterpret_cast<double*>(smem);
+    double* ty = tx + 6 * g.nc[0];
+    double* tz = ty + 6 * g.nc[1];
+    double* PS = reinterpret_cast<double*>(smem) + gtab_n;
+    double* RS = PS + H;
+    double* XS = RS + H;
+    uint8_t* CL = reinterpret_cast<uint8_t*>(XS + H);
+
+    build_class_table(T, threadIdx.x, P.mbase, P.cbase, g.dkind);
+    if (GAUSS) build_gauss_tables(g, P.src, tx, ty, tz);
+    for (int s = threadIdx.x; s < H; s += kResTPB) {
+        const int u = s % LX, v = (s / LX) % LY, w = s / SZ;
+        const int i = x0 + u - 1, j = y0 + v - 1, k = z0 + w - 1;
+        const bool in = i >= 0 && i <= g.nc[0] && j >= 0 && j <= g.nc[1] && k >= 0 && k <= g.nc[2];
+        CL[s] = in ? (uint8_t)class_of(g, i, j, k) : kNoNode;
+        PS[s] = 0.0;
+        RS[s] = 0.0;
+        XS[s] = 0.0;
+    }
+    __syncthreads();
+
+    // ---- own nodes: descriptors in registers ----
+    const int nown = lx * ly * lz;
+    int od[NPT], gid[NPT];
+#pragma unroll
+    for (int m = 0; m < NPT; ++m) {
+        const int nl = threadIdx.x + m * kResTPB;
+        od[m] = -1;
+        gid[m] = 0;
+        if (nl < nown) {
+            const int u = nl % lx + 1, v = (nl / lx) % ly + 1, w = nl / (lx * ly) + 1;
+            const int s = u + SY * v + SZ * w;
+            const int cls = CL[s];
+            int mask = 0;
+            const int nb[6] = {s - 1, s + 1, s - SY, s + SY, s - SZ, s + SZ};
+#pragma unroll
+            for (int e = 0; e < 6; ++e) {
+                const int c = CL[nb[e]];
+                if (c != kNoNode && T.nd[c] != 0.0) mask |= 1 << e;
+            }
+            const bool surf = u == 1 || u == lx || v == 1 || v == ly || w == 1 || w == lz;
+            od[m] = s | (mask << 14) | (cls << 20) | ((int)surf << 25);
+            gid[m] = (x0 + u - 1) + g.NX * ((y0 + v - 1) + g.NY * (z0 + w - 1));
+        }
+    }
+
+    // ---- phase 0: constrained RHS, r = b, x = 0 ----
+    double acc[2] = {0.0, 0.0};
+#pragma unroll
+    for (int m = 0; m < NPT; ++m) {
+        if (od[m] < 0) continue;
+        const int p = gid[m];
+        const int cls = od_cls(od[m]);
+        double bv;
+        if (T.nd[cls] == 0.0) {
+            bv = dirichlet_value(P, p);
+        } else {
+            int i, j, k;
+            decode(g, p, i, j, k);
+            bv = T.mass[cls] * P.T[p];
+            if (P.load) bv += P.load[p];
+            if (GAUSS) bv += gaussian_node(g, tx, ty, tz, i, j, k);
+            const int sy = g.NX, sz = g.NX * g.NY;
+            double lift = 0.0;
+            if (i > 0 && T.nd[cls - axis_class(i, g.nc[0]) + axis_class(i - 1, g.nc[0])] == 0.0) lift += T.c[0][cls] * dirichlet_value(P, p - 1);
+            if (i < g.nc[0] && T.nd[cls - axis_class(i, g.nc[0]) + axis_class(i + 1, g.nc[0])] == 0.0) lift += T.c[0][cls] * dirichlet_value(P, p + 1);
+            if (j > 0 && T.nd[cls + 3 * (axis_class(j - 1, g.nc[1]) - axis_class(j, g.nc[1]))] == 0.0) lift += T.c[1][cls] * dirichlet_value(P, p - sy);
+            if (j < g.nc[1] && T.nd[cls + 3 * (axis_class(j + 1, g.nc[1]) - axis_class(j, g.nc[1]))] == 0.0) lift += T.c[1][cls] * dirichlet_value(P, p + sy);
+            if (k > 0 && T.nd[cls + 9 * (axis_class(k - 1, g.nc[2]) - axis_class(k, g.nc[2]))] == 0.0) lift += T.c[2][cls] * dirichlet_value(P, p - sz);
+            if (k < g.nc[2] && T.nd[cls + 9 * (axis_class(k + 1, g.nc[2]) - axis_class(k, g.nc[2]))] == 0.0) lift += T.c[2][cls] * dirichlet_value(P, p + sz);
+            bv += lift;
+        }
+        P.b[p] = bv;
+        RS[od_s(od[m])] = bv;
+        if (od_surf(od[m])) RP.xg[p] = bv;
+        const double z = __dmul_rn(T.invd[cls], bv);
+        acc[0] += bv * bv;
+        acc[1] += bv * z;
+    }
+    block_sum<2>(acc, red);
+    if (threadIdx.x == 0) { P.part[0 * G + b] = acc[0]; P.part[1 * G + b] = acc[1]; }
+    grid.sync();
+    {
+        const int s2[2] = {0, 1};
+        grid_sum_fast<2>(P.part, s2, G, tot);
+    }
+    const double bb = tot[0];
+    double rz = tot[1];
+    const double bnorm = sqrt(bb);
+    const double atol = P.rtol * bnorm;
+    double rnorm = bnorm;
+    int it = 0, status = 0;
+    double rho_prev = 1.0;
+
+    // halo face cells: x faces (ly*lz each), y faces (lx*lz), z faces (lx*ly)
+    const int fx = ly * lz, fy = lx * lz, fz = lx * ly;
+    const int nface = 2 * (fx + fy + fz);
+    auto face_cell = [&](int e, int& s, int& gidh) -> bool {
+        int u, v, w;
+        if (e < 2 * fx) {
+            const int side = e / fx, r = e % fx;
+            u = side ? LX - 1 : 0; v = r % ly + 1; w = r / ly + 1;
+        } else if ((e -= 2 * fx) < 2 * fy) {
+            const int side = e / fy, r = e % fy;
+            v = side ? LY - 1 : 0; u = r % lx + 1; w = r / lx + 1;
+        } else {
+            e -= 2 * fy;
+            const int side = e / fz, r = e % fz;
+            w = side ? LZ - 1 : 0; u = r % lx + 1; v = r / lx + 1;
+        }
+        s = u + SY * v + SZ * w;
+        if (CL[s] == kNoNode) return false;
+        gidh = (x0 + u - 1) + g.NX * ((y0 + v - 1) + g.NY * (z0 + w - 1));
+        return true;
+    };
+
+    double q[NPT];
+    if (bb != 0.0) {
+        while (true) {
+            if (rnorm < atol) { status = 0; break; }
+            if (!isfinite(rnorm)) { status = 3; break; }
+            if (it >= P.maxiter) { status = 1; break; }
+            const double rho = rz;
+            const double beta = it > 0 ? rho / rho_prev : 0.0;
+            const bool first = it == 0;
+            // ---- phase A: halo r in, p = z (+ beta p) on own + halo, q = A_c p ----
+            for (int e = threadIdx.x; e < nface; e += kResTPB) {
+                int s, gh;
+                if (!face_cell(e, s, gh)) continue;
+                const double rv = __ldcg(RP.xg + gh);
+                RS[s] = rv;
+                const double z = __dmul_rn(T.invd[CL[s]], rv);
+                PS[s] = first ? z : __dadd_rn(__dmul_rn(beta, PS[s]), z);
+            }
+#pragma unroll
+            for (int m = 0; m < NPT; ++m) {
+                if (od[m] < 0) continue;
+                const int s = od_s(od[m]);
+                const double z = __dmul_rn(T.invd[od_cls(od[m])], RS[s]);
+                PS[s] = first ? z : __dadd_rn(__dmul_rn(beta, PS[s]), z);
+            }
+            __syncthreads();
+            double pq[1] = {0.0};
+#pragma unroll
+            for (int m = 0; m < NPT; ++m) {
+                if (od[m] < 0) continue;
+                const int d = od[m], s = od_s(d), cls = od_cls(d), mk = od_mask(d);
+                const double pp = PS[s];
+                double qv;
+                if (T.nd[cls] == 0.0) {
+                    qv = pp;
+                } else {
+                    const double tx_ = ((mk & 1) ? PS[s - 1] : 0.0) + ((mk & 2) ? PS[s + 1] : 0.0);
+                    const double ty_ = ((mk & 4) ? PS[s - SY] : 0.0) + ((mk & 8) ? PS[s + SY] : 0.0);
+                    const double tz_ = ((mk & 16) ? PS[s - SZ] : 0.0) + ((mk & 32) ? PS[s + SZ] : 0.0);
+                    qv = T.diag[cls] * pp - ((T.c[0][cls] * tx_ + T.c[1][cls] * ty_) + T.c[2][cls] * tz_);
+                }
+                q[m] = qv;
+                pq[0] += pp * qv;
+            }
+            block_sum<1>(pq, red);
+            if (threadIdx.x == 0) P.part[2 * G + b] = pq[0];
+            grid.sync();
+            {
+                const int s1[1] = {2};
+                grid_sum_fast<1>(P.part, s1, G, tot);
+            }
+            const double alpha = rho / tot[0];
+            // ---- phase B: x += alpha p, r -= alpha q, r.z, r.r; publish surface r ----
+            double a2[2] = {0.0, 0.0};
+#pragma unroll
+            for (int m = 0; m < NPT; ++m) {
+                if (od[m] < 0) continue;
+                const int d = od[m], s = od_s(d);
+                XS[s] = __dadd_rn(XS[s], __dmul_rn(alpha, PS[s]));
+                const double rv = __dsub_rn(RS[s], __dmul_rn(alpha, q[m]));
+                RS[s] = rv;
+                if (od_surf(d)) RP.xg[gid[m]] = rv;
+                const double z = __dmul_rn(T.invd[od_cls(d)], rv);
+                a2[0] += rv * z;
+                a2[1] += rv * rv;
+            }
+            block_sum<2>(a2, red);
+            if (threadIdx.x == 0) { P.part[0 * G + b] = a2[0]; P.part[1 * G + b] = a2[1]; }
+            grid.sync();
+            {
+                const int s2[2] = {0, 1};
+                grid_sum_fast<2>(P.part, s2, G, tot);
+            }
+            rz = tot[0];
+            rnorm = sqrt(tot[1]);
+            rho_prev = rho;
+            ++it;
+        }
+    }
+
+    // ---- true residual ||A_c x - b||: publish surface x, gather halo x into PS ----
+#pragma unroll
+    for (int m = 0; m < NPT; ++m) {
+        if (od[m] < 0) continue;
+        const int s = od_s(od[m]);
+        PS[s] = XS[s];
+        if (od_surf(od[m])) RP.xg[gid[m]] = XS[s];
+    }
+    grid.sync();
+    for (int e = threadIdx.x; e < nface; e += kResTPB) {
+        int s, gh;
+        if (face_cell(e, s, gh)) PS[s] = __ldcg(RP.xg + gh);
+    }
+    __syncthreads();
+    double res[2] = {0.0, 0.0};
+#pragma unroll
+    for (int m = 0; m < NPT; ++m) {
+        if (od[m] < 0) continue;
+        const int d = od[m], s = od_s(d), cls = od_cls(d), mk = od_mask(d);
+        const double xp = PS[s];
+        double ax;
+        if (T.nd[cls] == 0.0) {
+            ax = xp;
+        } else {
+            const double tx_ = ((mk & 1) ? PS[s - 1] : 0.0) + ((mk & 2) ? PS[s + 1] : 0.0);
+            const double ty_ = ((mk & 4) ? PS[s - SY] : 0.0) + ((mk & 8) ? PS[s + SY] : 0.0);
+            const double tz_ = ((mk & 16) ? PS[s - SZ] : 0.0) + ((mk & 32) ? PS[s + SZ] : 0.0);
+            ax = T.diag[cls] * xp - ((T.c[0][cls] * tx_ + T.c[1][cls] * ty_) + T.c[2][cls] * tz_);
+        }
+        const double bv = P.b[gid[m]];
+        const double dd = ax - bv;
+        res[0] += dd * dd;
+        res[1] += isfinite(xp) ? 0.0 : 1.0;
+        // x_D = g = b_D (fem.py:289-290)
+        P.T[gid[m]] = (T.nd[cls] == 0.0) ? bv : xp;
+    }
+    block_sum<2>(res, red);
+    if (threadIdx.x == 0) { P.part[0 * G + b] = res[0]; P.part[3 * G + b] = res[1]; }
+    grid.sync();
+    {
+        const int s2[2] = {0, 3};
+        grid_sum_fast<2>(P.part, s2, G, tot);
+    }
+    if (b == 0 && threadIdx.x == 0) {
+        const double tres = bnorm > 0.0 ? sqrt(tot[0]) / bnorm : 0.0;
+        if (status == 0 && tot[1] > 0.0) status = 3;
+        if (status == 0 && (!isfinite(tres) || tres > 1e2 * P.rtol)) status = 2;
+        P.info->iterations = (status == 1) ? P.maxiter : it;
+        P.info->status = status;
+        P.info->bnorm = bnorm;
+        P.info->rnorm = rnorm;
+        P.info->true_resid = tres;
+    }
+}
+
+}  // namespace tl
