@@ -188,6 +188,11 @@ int64_t tl_run_launch_count(tl_run* run);
  * launches since the last call, in launch order (same order as tl_run_take_info). */
 int32_t tl_run_set_timing(tl_run* run, int32_t on);
 int32_t tl_run_take_timing(tl_run* run, float* ms, int32_t* level, int32_t max, int32_t* count);
+/* Diagnostics: with TLGPU_PROF=1 in the environment the resident solve kernel records
+ * %globaltimer stamps of CTA 0 at its phase boundaries (start, after the RHS, after
+ * each of the two barriers of the first 64 iterations, end); this returns the stamps
+ * of the most recent resident solve. */
+int32_t tl_debug_profile(uint64_t* out, int32_t max, int32_t* count);
 /* Write a scratch buffer larger than L2 on the run's stream (bench hygiene). */
 int32_t tl_run_flush_l2(tl_run* run);
 

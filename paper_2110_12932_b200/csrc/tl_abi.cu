@@ -59,6 +59,9 @@ int make_grid(const tl_grid_desc& d, int dkind, tl::Grid& g) {
 }
 
 int coop_blocks(bool gauss, size_t smem, int sms, int& blocks) {
+    static thread_local int cached[2] = {0, 0};
+    static thread_local size_t cached_smem[2] = {0, 0};
+    if (cached[gauss] > 0 && cached_smem[gauss] == smem) { blocks = cached[gauss] * sms; return TL_OK; }
     int per_sm = 0;
     cudaError_t e;
     if (gauss)
@@ -67,6 +70,8 @@ int coop_blocks(bool gauss, size_t smem, int sms, int& blocks) {
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tl::k_pcg<false>, tl::kTPB, smem);
     if (e != cudaSuccess) return fail(TL_E_CUDA, std::string("occupancy: ") + cudaGetErrorString(e));
     if (per_sm < 1) return fail(TL_E_CUDA, "k_pcg cannot be resident");
+    cached[gauss] = per_sm;
+    cached_smem[gauss] = smem;
     blocks = per_sm * sms;
     return TL_OK;
 }
@@ -106,24 +111,27 @@ static void split_axis(int N, int parts, int* off) {
     for (int e = 0; e <= parts; ++e) off[e] = (int)((long long)N * e / parts);
 }
 
-static BrickPlan plan_bricks(const tl::Grid& g, bool gauss, int sms, size_t smem_cap) {
+static BrickPlan plan_bricks_uncached(const tl::Grid& g, bool gauss, int sms, size_t smem_cap) {
     BrickPlan best;
     const int N[3] = {g.NX, g.NY, g.NZ};
     const long long n = (long long)g.n;
     // small grids: fewer, larger bricks (cheaper barriers); large: one brick per SM
     int target = (int)std::min<long long>(sms, std::max<long long>(1, (n + 2047) / 2048));
-    const size_t gtab = gauss ? sizeof(double) * 6 * (size_t)(g.nc[0] + g.nc[1] + g.nc[2]) : 0;
+    const int gtab = gauss ? 6 * (g.nc[0] + g.nc[1] + g.nc[2]) : 0;
     double best_cost = 1e300;
     for (int gx = 1; gx <= std::min(N[0], tl::kResMaxSplit); ++gx)
-        for (int gy = 1; gy <= std::min(N[1], tl::kResMaxSplit); ++gy)
-            for (int gz = 1; gz <= std::min(N[2], tl::kResMaxSplit); ++gz) {
+        for (int gy = 1; gy <= std::min(N[1], tl::kResMaxSplit) && gx * gy <= target; ++gy)
+            for (int gz = 1; gz <= std::min(N[2], tl::kResMaxSplit) && gx * gy * gz <= target; ++gz) {
                 const int G = gx * gy * gz;
-                if (G > target || G > tl::kResMaxBlocks) continue;
+                if (G > tl::kResMaxBlocks) continue;
                 const int lx = (N[0] + gx - 1) / gx, ly = (N[1] + gy - 1) / gy, lz = (N[2] + gz - 1) / gz;
                 const int own = lx * ly * lz;
-                const size_t H = (size_t)(lx + 2) * (ly + 2) * (lz + 2);
-                const size_t smem = gtab + H * 25 + 64;
-                if (own > 12 * tl::kResTPB || smem > smem_cap || H >= 16384) continue;
+                const int H = (lx + 2) * (ly + 2) * (lz + 2);
+                const int nface = 2 * (ly * lz + lx * lz + lx * ly);
+                const size_t smem = tl::res_smem_bytes(lx, ly, lz, gtab);
+                if (own > 12 * tl::kResTPB || smem > smem_cap || H >= 16384 ||
+                    nface > tl::kResKF * tl::kResTPB)
+                    continue;
                 // cost: max work per CTA, then halo, then fewer CTAs
                 const double cost = (double)own * 1.0 + 0.25 * (double)(H - own) + 0.01 * G;
                 if (cost < best_cost) {
@@ -139,6 +147,30 @@ static BrickPlan plan_bricks(const tl::Grid& g, bool gauss, int sms, size_t smem
         best.npt = npt <= 2 ? 2 : npt <= 4 ? 4 : npt <= 6 ? 6 : npt <= 8 ? 8 : npt <= 10 ? 10 : 12;
     }
     return best;
+}
+
+// decomposition cache keyed by grid shape (the search is a few hundred microseconds)
+static BrickPlan plan_bricks(const tl::Grid& g, bool gauss, int sms, size_t smem_cap) {
+    struct Entry { int nc[3]; bool gauss; int sms; BrickPlan plan; };
+    static thread_local std::vector<Entry> cache;
+    for (const Entry& e : cache)
+        if (e.nc[0] == g.nc[0] && e.nc[1] == g.nc[1] && e.nc[2] == g.nc[2] && e.gauss == gauss && e.sms == sms)
+            return e.plan;
+    BrickPlan bp = plan_bricks_uncached(g, gauss, sms, smem_cap);
+    cache.push_back({{g.nc[0], g.nc[1], g.nc[2]}, gauss, sms, bp});
+    return bp;
+}
+
+static unsigned long long* g_prof = nullptr;     // TLGPU_PROF=1: phase timestamps of block 0
+
+static unsigned long long* prof_buffer() {
+    static int want = -1;
+    if (want < 0) {
+        const char* e = getenv("TLGPU_PROF");
+        want = (e && e[0] == '1') ? 1 : 0;
+        if (want) cudaMalloc((void**)&g_prof, 128 * sizeof(unsigned long long));
+    }
+    return g_prof;
 }
 
 template <bool GAUSS, int NPT>
@@ -181,6 +213,7 @@ static int launch_solve(tl::PcgParams& P, bool gauss, int sms, double* xg, cudaS
             tl::ResParams RP{};
             RP.P = P;
             RP.xg = xg;
+            RP.prof = prof_buffer();
             const int N[3] = {P.g.NX, P.g.NY, P.g.NZ};
             for (int a = 0; a < 3; ++a) {
                 RP.ng[a] = bp.ng[a];
@@ -710,6 +743,19 @@ int32_t tl_run_stream(tl_run* R, void** stream) {
 }
 
 int64_t tl_run_launch_count(tl_run* R) { return R ? R->launches : -1; }
+
+int32_t tl_debug_profile(uint64_t* out, int32_t max, int32_t* count) {
+    if (!out || !count) return fail(TL_E_INVALID, "null argument");
+    *count = 0;
+    if (!g_prof) return TL_OK;
+    unsigned long long h[128];
+    TL_CUDA(cudaDeviceSynchronize());
+    TL_CUDA(cudaMemcpy(h, g_prof, sizeof(h), cudaMemcpyDeviceToHost));
+    const int n = (int)std::min<unsigned long long>(h[127], (unsigned long long)std::min(max, 127));
+    for (int e = 0; e < n; ++e) out[e] = h[e];
+    *count = n;
+    return TL_OK;
+}
 
 int32_t tl_run_set_timing(tl_run* R, int32_t on) {
     if (!R) return fail(TL_E_INVALID, "null run");

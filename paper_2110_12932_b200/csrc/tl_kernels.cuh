@@ -191,6 +191,30 @@ __device__ double gaussian_node(const Grid& g, const double* tx, const double* t
     return F;
 }
 
+}  // namespace tl
+#include "tl_gauss_gen.cuh"
+namespace tl {
+
+// Same load, branch-free: the 2 x 6 table values per axis in registers (zero for
+// cells outside the grid) and the 96 terms of tl_gauss_gen.cuh.
+__device__ __forceinline__ double gaussian_node_fast(const Grid& g, const double* tx, const double* ty,
+                                                     const double* tz, int i, int j, int k) {
+    double X[2][6], Y[2][6], Z[2][6];
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+        const bool vx = (i - b) >= 0 && (i - b) < g.nc[0];
+        const bool vy = (j - b) >= 0 && (j - b) < g.nc[1];
+        const bool vz = (k - b) >= 0 && (k - b) < g.nc[2];
+#pragma unroll
+        for (int o = 0; o < 6; ++o) {
+            X[b][o] = vx ? tx[(i - b) * 6 + o] : 0.0;
+            Y[b][o] = vy ? ty[(j - b) * 6 + o] : 0.0;
+            Z[b][o] = vz ? tz[(k - b) * 6 + o] : 0.0;
+        }
+    }
+    return gauss_terms(X, Y, Z);
+}
+
 __device__ inline void build_gauss_tables(const Grid& g, const Gauss& s, double* tx, double* ty,
                                           double* tz) {
     const double fr[6] = {TL_QB, 2.0 * TL_QB, 3.0 * TL_QB, TL_QA, TL_QA + TL_QB, TL_QA + 2.0 * TL_QB};
@@ -288,7 +312,7 @@ __global__ void __launch_bounds__(kTPB) k_pcg(PcgParams P) {
         } else {
             bv = T.mass[cls] * P.T[p];
             if (P.load) bv += P.load[p];
-            if (GAUSS) bv += gaussian_node(g, tx, ty, tz, i, j, k);
+            if (GAUSS) bv += gaussian_node_fast(g, tx, ty, tz, i, j, k);
             // lift: b_p -= sum_{q in D} A_pq g_q,  A_pq = -c_pq
             const int sy = g.NX, sz = g.NX * g.NY;
             double lift = 0.0;

@@ -9,6 +9,9 @@
 // are advanced by the same recurrence p = beta p + M^-1 r as their owners, so they
 // stay bitwise identical without a second exchange.  Two grid barriers per
 // iteration carry the two CG reductions (p.q, then r.z and r.r).
+//
+// Shared memory (per CTA, H = halo'd brick nodes, n = own nodes, F = halo face cells):
+//   [Gaussian tables][PS: H doubles][RS: H][XS: n][GID: n ints][FS: F ints][FG: F ints][CL: H bytes]
 #pragma once
 
 #include "tl_kernels.cuh"
@@ -17,14 +20,23 @@ namespace tl {
 
 constexpr int kResTPB = 512;
 constexpr int kResMaxSplit = 64;
+constexpr int kResKF = 8;              // halo face cells per thread (F <= kResKF * kResTPB)
 constexpr uint8_t kNoNode = 27;
 
 struct ResParams {
     PcgParams P;                  // grid, coefficients, inputs, workspace (b, part, info)
     double* xg;                   // global exchange array (brick-surface values), n doubles
+    unsigned long long* prof;     // optional phase timestamps (block 0), or nullptr
     int ng[3];                    // bricks per axis
     int off[3][kResMaxSplit + 1]; // brick boundaries per axis (node indices)
 };
+
+__host__ __device__ inline size_t res_smem_bytes(int lx, int ly, int lz, int gtab) {
+    const size_t H = (size_t)(lx + 2) * (ly + 2) * (lz + 2);
+    const size_t n = (size_t)lx * ly * lz;
+    const size_t F = 2 * ((size_t)ly * lz + (size_t)lx * lz + (size_t)lx * ly);
+    return 8 * (size_t)gtab + 16 * H + 8 * n + 4 * n + 8 * F + H + 16;
+}
 
 // own-node descriptor bits: [0,14) smem index, [14,20) free-neighbour mask
 // (x-, x+, y-, y+, z-, z+), [20,25) class, bit 25 brick-surface node.
@@ -32,6 +44,21 @@ __device__ __forceinline__ int od_s(int d) { return d & 0x3fff; }
 __device__ __forceinline__ int od_mask(int d) { return (d >> 14) & 0x3f; }
 __device__ __forceinline__ int od_cls(int d) { return (d >> 20) & 0x1f; }
 __device__ __forceinline__ bool od_surf(int d) { return (d >> 25) & 1; }
+
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// (A_c v)_s for a free own node from the halo'd smem array V.
+__device__ __forceinline__ double stencil_smem(const ClassTable& T, const double* V, int s, int cls,
+                                               int mk, int SY, int SZ) {
+    const double tx_ = ((mk & 1) ? V[s - 1] : 0.0) + ((mk & 2) ? V[s + 1] : 0.0);
+    const double ty_ = ((mk & 4) ? V[s - SY] : 0.0) + ((mk & 8) ? V[s + SY] : 0.0);
+    const double tz_ = ((mk & 16) ? V[s - SZ] : 0.0) + ((mk & 32) ? V[s + SZ] : 0.0);
+    return T.diag[cls] * V[s] - ((T.c[0][cls] * tx_ + T.c[1][cls] * ty_) + T.c[2][cls] * tz_);
+}
 
 template <bool GAUSS, int NPT>
 __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident(ResParams RP) {
@@ -42,6 +69,9 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident(ResParams RP) {
     __shared__ double red[4 * 32];
     __shared__ double tot[4];
     extern __shared__ __align__(16) unsigned char smem[];
+    const bool prof = RP.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
+    int np = 0;
+    if (prof) RP.prof[np++] = global_ns();
 
     // ---- brick of this CTA ----
     const int G = gridDim.x;
@@ -52,15 +82,21 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident(ResParams RP) {
     const int LX = lx + 2, LY = ly + 2, LZ = lz + 2;
     const int H = LX * LY * LZ;
     const int SY = LX, SZ = LX * LY;
+    const int nown = lx * ly * lz;
+    const int fx = ly * lz, fy = lx * lz, fz = lx * ly;
+    const int nface = 2 * (fx + fy + fz);
 
-    int gtab_n = GAUSS ? 6 * (g.nc[0] + g.nc[1] + g.nc[2]) : 0;
+    const int gtab_n = GAUSS ? 6 * (g.nc[0] + g.nc[1] + g.nc[2]) : 0;
     double* tx = reinterpret_cast<double*>(smem);
     double* ty = tx + 6 * g.nc[0];
     double* tz = ty + 6 * g.nc[1];
-    double* PS = reinterpret_cast<double*>(smem) + gtab_n;
+    double* PS = tx + gtab_n;
     double* RS = PS + H;
     double* XS = RS + H;
-    uint8_t* CL = reinterpret_cast<uint8_t*>(XS + H);
+    int* GID = reinterpret_cast<int*>(XS + nown);
+    int* FS = GID + nown;
+    int* FG = FS + nface;
+    uint8_t* CL = reinterpret_cast<uint8_t*>(FG + nface);
 
     build_class_table(T, threadIdx.x, P.mbase, P.cbase, g.dkind);
     if (GAUSS) build_gauss_tables(g, P.src, tx, ty, tz);
@@ -71,18 +107,34 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident(ResParams RP) {
         CL[s] = in ? (uint8_t)class_of(g, i, j, k) : kNoNode;
         PS[s] = 0.0;
         RS[s] = 0.0;
-        XS[s] = 0.0;
     }
     __syncthreads();
+    // halo face cells (the 7-point stencil needs no edge or corner cells)
+    for (int e0 = threadIdx.x; e0 < nface; e0 += kResTPB) {
+        int e = e0, u, v, w;
+        if (e < 2 * fx) {
+            const int side = e / fx, r = e % fx;
+            u = side ? LX - 1 : 0; v = r % ly + 1; w = r / ly + 1;
+        } else if ((e -= 2 * fx) < 2 * fy) {
+            const int side = e / fy, r = e % fy;
+            v = side ? LY - 1 : 0; u = r % lx + 1; w = r / lx + 1;
+        } else {
+            e -= 2 * fy;
+            const int side = e / fz, r = e % fz;
+            w = side ? LZ - 1 : 0; u = r % lx + 1; v = r / lx + 1;
+        }
+        const int s = u + SY * v + SZ * w;
+        const bool in = CL[s] != kNoNode;
+        FS[e0] = in ? s : -1;
+        FG[e0] = in ? (x0 + u - 1) + g.NX * ((y0 + v - 1) + g.NY * (z0 + w - 1)) : 0;
+    }
 
-    // ---- own nodes: descriptors in registers ----
-    const int nown = lx * ly * lz;
-    int od[NPT], gid[NPT];
+    // ---- own nodes: descriptors in registers, global ids in smem ----
+    int od[NPT];
 #pragma unroll
     for (int m = 0; m < NPT; ++m) {
         const int nl = threadIdx.x + m * kResTPB;
         od[m] = -1;
-        gid[m] = 0;
         if (nl < nown) {
             const int u = nl % lx + 1, v = (nl / lx) % ly + 1, w = nl / (lx * ly) + 1;
             const int s = u + SY * v + SZ * w;
@@ -96,7 +148,8 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident(ResParams RP) {
             }
             const bool surf = u == 1 || u == lx || v == 1 || v == ly || w == 1 || w == lz;
             od[m] = s | (mask << 14) | (cls << 20) | ((int)surf << 25);
-            gid[m] = (x0 + u - 1) + g.NX * ((y0 + v - 1) + g.NY * (z0 + w - 1));
+            GID[nl] = (x0 + u - 1) + g.NX * ((y0 + v - 1) + g.NY * (z0 + w - 1));
+            XS[nl] = 0.0;
         }
     }
 
@@ -105,7 +158,7 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident(ResParams RP) {
 #pragma unroll
     for (int m = 0; m < NPT; ++m) {
         if (od[m] < 0) continue;
-        const int p = gid[m];
+        const int p = GID[threadIdx.x + m * kResTPB];
         const int cls = od_cls(od[m]);
         double bv;
         if (T.nd[cls] == 0.0) {
@@ -115,7 +168,7 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident(ResParams RP) {
             decode(g, p, i, j, k);
             bv = T.mass[cls] * P.T[p];
             if (P.load) bv += P.load[p];
-            if (GAUSS) bv += gaussian_node(g, tx, ty, tz, i, j, k);
+            if (GAUSS) bv += gaussian_node_fast(g, tx, ty, tz, i, j, k);
             const int sy = g.NX, sz = g.NX * g.NY;
             double lift = 0.0;
             if (i > 0 && T.nd[cls - axis_class(i, g.nc[0]) + axis_class(i - 1, g.nc[0])] == 0.0) lift += T.c[0][cls] * dirichlet_value(P, p - 1);
@@ -140,6 +193,7 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident(ResParams RP) {
         const int s2[2] = {0, 1};
         grid_sum_fast<2>(P.part, s2, G, tot);
     }
+    if (prof) RP.prof[np++] = global_ns();
     const double bb = tot[0];
     double rz = tot[1];
     const double bnorm = sqrt(bb);
@@ -147,28 +201,6 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident(ResParams RP) {
     double rnorm = bnorm;
     int it = 0, status = 0;
     double rho_prev = 1.0;
-
-    // halo face cells: x faces (ly*lz each), y faces (lx*lz), z faces (lx*ly)
-    const int fx = ly * lz, fy = lx * lz, fz = lx * ly;
-    const int nface = 2 * (fx + fy + fz);
-    auto face_cell = [&](int e, int& s, int& gidh) -> bool {
-        int u, v, w;
-        if (e < 2 * fx) {
-            const int side = e / fx, r = e % fx;
-            u = side ? LX - 1 : 0; v = r % ly + 1; w = r / ly + 1;
-        } else if ((e -= 2 * fx) < 2 * fy) {
-            const int side = e / fy, r = e % fy;
-            v = side ? LY - 1 : 0; u = r % lx + 1; w = r / lx + 1;
-        } else {
-            e -= 2 * fy;
-            const int side = e / fz, r = e % fz;
-            w = side ? LZ - 1 : 0; u = r % lx + 1; v = r / lx + 1;
-        }
-        s = u + SY * v + SZ * w;
-        if (CL[s] == kNoNode) return false;
-        gidh = (x0 + u - 1) + g.NX * ((y0 + v - 1) + g.NY * (z0 + w - 1));
-        return true;
-    };
 
     double q[NPT];
     if (bb != 0.0) {
@@ -180,13 +212,11 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident(ResParams RP) {
             const double beta = it > 0 ? rho / rho_prev : 0.0;
             const bool first = it == 0;
             // ---- phase A: halo r in, p = z (+ beta p) on own + halo, q = A_c p ----
-            for (int e = threadIdx.x; e < nface; e += kResTPB) {
-                int s, gh;
-                if (!face_cell(e, s, gh)) continue;
-                const double rv = __ldcg(RP.xg + gh);
-                RS[s] = rv;
-                const double z = __dmul_rn(T.invd[CL[s]], rv);
-                PS[s] = first ? z : __dadd_rn(__dmul_rn(beta, PS[s]), z);
+            double fv[kResKF];
+#pragma unroll
+            for (int t = 0; t < kResKF; ++t) {      // issue every halo load first
+                const int e = threadIdx.x + t * kResTPB;
+                fv[t] = (e < nface && FS[e] >= 0) ? __ldcg(RP.xg + FG[e]) : 0.0;
             }
 #pragma unroll
             for (int m = 0; m < NPT; ++m) {
@@ -195,22 +225,24 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident(ResParams RP) {
                 const double z = __dmul_rn(T.invd[od_cls(od[m])], RS[s]);
                 PS[s] = first ? z : __dadd_rn(__dmul_rn(beta, PS[s]), z);
             }
+#pragma unroll
+            for (int t = 0; t < kResKF; ++t) {
+                const int e = threadIdx.x + t * kResTPB;
+                if (e >= nface) break;
+                const int s = FS[e];
+                if (s < 0) continue;
+                RS[s] = fv[t];
+                const double z = __dmul_rn(T.invd[CL[s]], fv[t]);
+                PS[s] = first ? z : __dadd_rn(__dmul_rn(beta, PS[s]), z);
+            }
             __syncthreads();
             double pq[1] = {0.0};
 #pragma unroll
             for (int m = 0; m < NPT; ++m) {
                 if (od[m] < 0) continue;
-                const int d = od[m], s = od_s(d), cls = od_cls(d), mk = od_mask(d);
+                const int d = od[m], s = od_s(d), cls = od_cls(d);
                 const double pp = PS[s];
-                double qv;
-                if (T.nd[cls] == 0.0) {
-                    qv = pp;
-                } else {
-                    const double tx_ = ((mk & 1) ? PS[s - 1] : 0.0) + ((mk & 2) ? PS[s + 1] : 0.0);
-                    const double ty_ = ((mk & 4) ? PS[s - SY] : 0.0) + ((mk & 8) ? PS[s + SY] : 0.0);
-                    const double tz_ = ((mk & 16) ? PS[s - SZ] : 0.0) + ((mk & 32) ? PS[s + SZ] : 0.0);
-                    qv = T.diag[cls] * pp - ((T.c[0][cls] * tx_ + T.c[1][cls] * ty_) + T.c[2][cls] * tz_);
-                }
+                const double qv = (T.nd[cls] == 0.0) ? pp : stencil_smem(T, PS, s, cls, od_mask(d), SY, SZ);
                 q[m] = qv;
                 pq[0] += pp * qv;
             }
@@ -221,17 +253,18 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident(ResParams RP) {
                 const int s1[1] = {2};
                 grid_sum_fast<1>(P.part, s1, G, tot);
             }
+            if (prof && it < 64) RP.prof[np++] = global_ns();
             const double alpha = rho / tot[0];
             // ---- phase B: x += alpha p, r -= alpha q, r.z, r.r; publish surface r ----
             double a2[2] = {0.0, 0.0};
 #pragma unroll
             for (int m = 0; m < NPT; ++m) {
                 if (od[m] < 0) continue;
-                const int d = od[m], s = od_s(d);
-                XS[s] = __dadd_rn(XS[s], __dmul_rn(alpha, PS[s]));
+                const int d = od[m], s = od_s(d), nl = threadIdx.x + m * kResTPB;
+                XS[nl] = __dadd_rn(XS[nl], __dmul_rn(alpha, PS[s]));
                 const double rv = __dsub_rn(RS[s], __dmul_rn(alpha, q[m]));
                 RS[s] = rv;
-                if (od_surf(d)) RP.xg[gid[m]] = rv;
+                if (od_surf(d)) RP.xg[GID[nl]] = rv;
                 const double z = __dmul_rn(T.invd[od_cls(d)], rv);
                 a2[0] += rv * z;
                 a2[1] += rv * rv;
@@ -243,6 +276,7 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident(ResParams RP) {
                 const int s2[2] = {0, 1};
                 grid_sum_fast<2>(P.part, s2, G, tot);
             }
+            if (prof && it < 64) RP.prof[np++] = global_ns();
             rz = tot[0];
             rnorm = sqrt(tot[1]);
             rho_prev = rho;
@@ -254,37 +288,30 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident(ResParams RP) {
 #pragma unroll
     for (int m = 0; m < NPT; ++m) {
         if (od[m] < 0) continue;
-        const int s = od_s(od[m]);
-        PS[s] = XS[s];
-        if (od_surf(od[m])) RP.xg[gid[m]] = XS[s];
+        const int nl = threadIdx.x + m * kResTPB;
+        PS[od_s(od[m])] = XS[nl];
+        if (od_surf(od[m])) RP.xg[GID[nl]] = XS[nl];
     }
     grid.sync();
-    for (int e = threadIdx.x; e < nface; e += kResTPB) {
-        int s, gh;
-        if (face_cell(e, s, gh)) PS[s] = __ldcg(RP.xg + gh);
+#pragma unroll
+    for (int t = 0; t < kResKF; ++t) {
+        const int e = threadIdx.x + t * kResTPB;
+        if (e < nface && FS[e] >= 0) PS[FS[e]] = __ldcg(RP.xg + FG[e]);
     }
     __syncthreads();
     double res[2] = {0.0, 0.0};
 #pragma unroll
     for (int m = 0; m < NPT; ++m) {
         if (od[m] < 0) continue;
-        const int d = od[m], s = od_s(d), cls = od_cls(d), mk = od_mask(d);
+        const int d = od[m], s = od_s(d), cls = od_cls(d);
+        const int p = GID[threadIdx.x + m * kResTPB];
         const double xp = PS[s];
-        double ax;
-        if (T.nd[cls] == 0.0) {
-            ax = xp;
-        } else {
-            const double tx_ = ((mk & 1) ? PS[s - 1] : 0.0) + ((mk & 2) ? PS[s + 1] : 0.0);
-            const double ty_ = ((mk & 4) ? PS[s - SY] : 0.0) + ((mk & 8) ? PS[s + SY] : 0.0);
-            const double tz_ = ((mk & 16) ? PS[s - SZ] : 0.0) + ((mk & 32) ? PS[s + SZ] : 0.0);
-            ax = T.diag[cls] * xp - ((T.c[0][cls] * tx_ + T.c[1][cls] * ty_) + T.c[2][cls] * tz_);
-        }
-        const double bv = P.b[gid[m]];
+        const double ax = (T.nd[cls] == 0.0) ? xp : stencil_smem(T, PS, s, cls, od_mask(d), SY, SZ);
+        const double bv = P.b[p];
         const double dd = ax - bv;
         res[0] += dd * dd;
         res[1] += isfinite(xp) ? 0.0 : 1.0;
-        // x_D = g = b_D (fem.py:289-290)
-        P.T[gid[m]] = (T.nd[cls] == 0.0) ? bv : xp;
+        P.T[p] = (T.nd[cls] == 0.0) ? bv : xp;      // x_D = g = b_D (fem.py:289-290)
     }
     block_sum<2>(res, red);
     if (threadIdx.x == 0) { P.part[0 * G + b] = res[0]; P.part[3 * G + b] = res[1]; }
@@ -302,6 +329,7 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident(ResParams RP) {
         P.info->bnorm = bnorm;
         P.info->rnorm = rnorm;
         P.info->true_resid = tres;
+        if (prof) { RP.prof[np++] = global_ns(); RP.prof[127] = np; }
     }
 }
 
