@@ -76,7 +76,7 @@ int coop_blocks(bool gauss, size_t smem, int sms, int& blocks) {
     return TL_OK;
 }
 
-size_t gauss_smem(const tl::Grid& g) { return sizeof(double) * 6 * (size_t)(g.nc[0] + g.nc[1] + g.nc[2]); }
+size_t gauss_smem(const tl::Grid& g) { return sizeof(double) * (size_t)tl::gauss_smem_len(g); }
 
 int launch_pcg(tl::PcgParams& P, bool gauss, int sms, cudaStream_t st, int64_t* launches) {
     size_t smem = gauss ? gauss_smem(P.g) : 0;
@@ -117,7 +117,7 @@ static BrickPlan plan_bricks_uncached(const tl::Grid& g, bool gauss, int sms, si
     const long long n = (long long)g.n;
     // small grids: fewer, larger bricks (cheaper barriers); large: one brick per SM
     int target = (int)std::min<long long>(sms, std::max<long long>(1, (n + 2047) / 2048));
-    const int gtab = gauss ? 6 * (g.nc[0] + g.nc[1] + g.nc[2]) : 0;
+    const int gtab = gauss ? tl::gauss_smem_len(g) : 0;
     double best_cost = 1e300;
     for (int gx = 1; gx <= std::min(N[0], tl::kResMaxSplit); ++gx)
         for (int gy = 1; gy <= std::min(N[1], tl::kResMaxSplit) && gx * gy <= target; ++gy)
@@ -212,7 +212,8 @@ static int launch_solve(tl::PcgParams& P, bool gauss, int sms, double* xg, cudaS
         if (bp.ok) {
             tl::ResParams RP{};
             RP.P = P;
-            RP.xg = xg;
+            RP.xg = xg;              // exchange buffer holds 2 n doubles: r, then x
+            RP.xx = xg + P.g.n;
             RP.prof = prof_buffer();
             const int N[3] = {P.g.NX, P.g.NY, P.g.NZ};
             for (int a = 0; a < 3; ++a) {
@@ -363,7 +364,7 @@ int32_t tl_step_host(const tl_grid_desc* grid, double kappa, double rho_c, doubl
         P.src.on = 1;
     }
     double* xg = nullptr;
-    if ((rc = dalloc(&xg, n))) return rc;
+    if ((rc = dalloc(&xg, 2 * (size_t)n))) return rc;
     rc = launch_solve(P, gauss, sms, xg, 0, nullptr);
     if (rc) return rc;
     TL_CUDA(cudaDeviceSynchronize());
@@ -471,7 +472,7 @@ int32_t tl_run_create(const tl_run_desc* desc, tl_run** out) {
         (rc = dalloc(&R->Tl_before, nl)) || (rc = dalloc(&R->part, 4 * R->sms * 32)) ||
         (rc = dalloc(&R->dep_prev, tl::kDepMax)) || (rc = dalloc(&R->dep_prev_n, 1)) ||
         (rc = dalloc(&R->melt, 4)) || (rc = dalloc(&R->melt_part, 2 * 1184)) ||
-        (rc = dalloc(&R->xg, std::max(ng, nl)))) {
+        (rc = dalloc(&R->xg, 2 * (size_t)std::max(ng, nl)))) {
         tl_run_destroy(R);
         return rc;
     }
@@ -751,7 +752,8 @@ int32_t tl_debug_profile(uint64_t* out, int32_t max, int32_t* count) {
     unsigned long long h[128];
     TL_CUDA(cudaDeviceSynchronize());
     TL_CUDA(cudaMemcpy(h, g_prof, sizeof(h), cudaMemcpyDeviceToHost));
-    const int n = (int)std::min<unsigned long long>(h[127], (unsigned long long)std::min(max, 127));
+    // slots [0, h[127]) phase stamps, 120..122 setup stamps, 127 = stamp count
+    const int n = std::min(max, 128);
     for (int e = 0; e < n; ++e) out[e] = h[e];
     *count = n;
     return TL_OK;

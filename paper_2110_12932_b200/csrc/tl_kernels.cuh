@@ -215,6 +215,39 @@ __device__ __forceinline__ double gaussian_node_fast(const Grid& g, const double
     return gauss_terms(X, Y, Z);
 }
 
+// Per-node-index upper bound of the Gaussian table factors: m[idx] = max over the
+// (up to) two cells idx-1, idx and the six offsets.  F_p <= 24 mx[i] my[j] mz[k]
+// (the 24 incident tets each weigh their four points by a + 3b = 1).
+__host__ __device__ inline int gauss_smem_len(const Grid& g) {
+    return 6 * (g.nc[0] + g.nc[1] + g.nc[2]) + (g.nc[0] + 1) + (g.nc[1] + 1) + (g.nc[2] + 1);
+}
+
+__device__ inline void build_gauss_bounds(const Grid& g, const double* tx, const double* ty,
+                                          const double* tz, double* mx, double* my, double* mz) {
+    const int tot = g.NX + g.NY + g.NZ;
+    for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+        int a = 0, idx = e;
+        if (idx >= g.NX) { idx -= g.NX; a = 1; if (idx >= g.NY) { idx -= g.NY; a = 2; } }
+        const double* t = a == 0 ? tx : (a == 1 ? ty : tz);
+        double m = 0.0;
+        for (int c = idx - 1; c <= idx; ++c)
+            if (c >= 0 && c < g.nc[a])
+                for (int o = 0; o < 6; ++o) m = fmax(m, t[c * 6 + o]);
+        (a == 0 ? mx : (a == 1 ? my : mz))[idx] = m;
+    }
+}
+
+// b0 + F_p, skipping the 96-term evaluation when F_p cannot change b0: for
+// 0 <= F < 2^-55 b0 the rounded sum is b0 exactly, so the result is bitwise the
+// same as adding the evaluated load (the Gaussian is negligible far from the beam).
+__device__ __forceinline__ double add_gaussian(double b0, const Grid& g, const double* tx,
+                                               const double* ty, const double* tz, const double* mx,
+                                               const double* my, const double* mz, int i, int j, int k) {
+    const double bound = 24.0 * mx[i] * my[j] * mz[k];
+    if (b0 > 0.0 && bound < b0 * 0x1p-55) return b0;
+    return b0 + gaussian_node_fast(g, tx, ty, tz, i, j, k);
+}
+
 __device__ inline void build_gauss_tables(const Grid& g, const Gauss& s, double* tx, double* ty,
                                           double* tz) {
     const double fr[6] = {TL_QB, 2.0 * TL_QB, 3.0 * TL_QB, TL_QA, TL_QA + TL_QB, TL_QA + 2.0 * TL_QB};
@@ -292,8 +325,13 @@ __global__ void __launch_bounds__(kTPB) k_pcg(PcgParams P) {
     const Grid& g = P.g;
     build_class_table(T, threadIdx.x, P.mbase, P.cbase, g.dkind);
     double *tx = gtab, *ty = gtab + 6 * g.nc[0], *tz = ty + 6 * g.nc[1];
+    double *bx_ = tz + 6 * g.nc[2], *by_ = bx_ + g.NX, *bz_ = by_ + g.NY;
     if (GAUSS) build_gauss_tables(g, P.src, tx, ty, tz);
     __syncthreads();
+    if (GAUSS) {
+        build_gauss_bounds(g, tx, ty, tz, bx_, by_, bz_);
+        __syncthreads();
+    }
 
     const int G = gridDim.x;
     const int per = (g.n + G - 1) / G;
@@ -312,7 +350,7 @@ __global__ void __launch_bounds__(kTPB) k_pcg(PcgParams P) {
         } else {
             bv = T.mass[cls] * P.T[p];
             if (P.load) bv += P.load[p];
-            if (GAUSS) bv += gaussian_node_fast(g, tx, ty, tz, i, j, k);
+            if (GAUSS) bv = add_gaussian(bv, g, tx, ty, tz, bx_, by_, bz_, i, j, k);
             // lift: b_p -= sum_{q in D} A_pq g_q,  A_pq = -c_pq
             const int sy = g.NX, sz = g.NX * g.NY;
             double lift = 0.0;

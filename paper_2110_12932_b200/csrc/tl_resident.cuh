@@ -25,7 +25,8 @@ constexpr uint8_t kNoNode = 27;
 
 struct ResParams {
     PcgParams P;                  // grid, coefficients, inputs, workspace (b, part, info)
-    double* xg;                   // global exchange array (brick-surface values), n doubles
+    double* xg;                   // global exchange array (brick-surface r), n doubles
+    double* xx;                   // global exchange array (brick-surface x), n doubles
     unsigned long long* prof;     // optional phase timestamps (block 0), or nullptr
     int ng[3];                    // bricks per axis
     int off[3][kResMaxSplit + 1]; // brick boundaries per axis (node indices)
@@ -86,10 +87,13 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident(ResParams RP) {
     const int fx = ly * lz, fy = lx * lz, fz = lx * ly;
     const int nface = 2 * (fx + fy + fz);
 
-    const int gtab_n = GAUSS ? 6 * (g.nc[0] + g.nc[1] + g.nc[2]) : 0;
+    const int gtab_n = GAUSS ? gauss_smem_len(g) : 0;
     double* tx = reinterpret_cast<double*>(smem);
     double* ty = tx + 6 * g.nc[0];
     double* tz = ty + 6 * g.nc[1];
+    double* bx_ = tz + 6 * g.nc[2];
+    double* by_ = bx_ + g.NX;
+    double* bz_ = by_ + g.NY;
     double* PS = tx + gtab_n;
     double* RS = PS + H;
     double* XS = RS + H;
@@ -109,6 +113,8 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident(ResParams RP) {
         RS[s] = 0.0;
     }
     __syncthreads();
+    if (GAUSS) build_gauss_bounds(g, tx, ty, tz, bx_, by_, bz_);
+    if (prof) RP.prof[120] = global_ns();
     // halo face cells (the 7-point stencil needs no edge or corner cells)
     for (int e0 = threadIdx.x; e0 < nface; e0 += kResTPB) {
         int e = e0, u, v, w;
@@ -154,6 +160,8 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident(ResParams RP) {
     }
 
     // ---- phase 0: constrained RHS, r = b, x = 0 ----
+    if (GAUSS) __syncthreads();          // Gaussian bounds visible
+    if (prof) RP.prof[121] = global_ns();
     double acc[2] = {0.0, 0.0};
 #pragma unroll
     for (int m = 0; m < NPT; ++m) {
@@ -168,7 +176,7 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident(ResParams RP) {
             decode(g, p, i, j, k);
             bv = T.mass[cls] * P.T[p];
             if (P.load) bv += P.load[p];
-            if (GAUSS) bv += gaussian_node_fast(g, tx, ty, tz, i, j, k);
+            if (GAUSS) bv = add_gaussian(bv, g, tx, ty, tz, bx_, by_, bz_, i, j, k);
             const int sy = g.NX, sz = g.NX * g.NY;
             double lift = 0.0;
             if (i > 0 && T.nd[cls - axis_class(i, g.nc[0]) + axis_class(i - 1, g.nc[0])] == 0.0) lift += T.c[0][cls] * dirichlet_value(P, p - 1);
@@ -186,6 +194,7 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident(ResParams RP) {
         acc[0] += bv * bv;
         acc[1] += bv * z;
     }
+    if (prof) RP.prof[122] = global_ns();
     block_sum<2>(acc, red);
     if (threadIdx.x == 0) { P.part[0 * G + b] = acc[0]; P.part[1 * G + b] = acc[1]; }
     grid.sync();
@@ -261,10 +270,15 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident(ResParams RP) {
             for (int m = 0; m < NPT; ++m) {
                 if (od[m] < 0) continue;
                 const int d = od[m], s = od_s(d), nl = threadIdx.x + m * kResTPB;
-                XS[nl] = __dadd_rn(XS[nl], __dmul_rn(alpha, PS[s]));
+                const double xv = __dadd_rn(XS[nl], __dmul_rn(alpha, PS[s]));
+                XS[nl] = xv;
                 const double rv = __dsub_rn(RS[s], __dmul_rn(alpha, q[m]));
                 RS[s] = rv;
-                if (od_surf(d)) RP.xg[GID[nl]] = rv;
+                if (od_surf(d)) {
+                    // r for the next iteration's halo; x speculatively, for the final residual
+                    RP.xg[GID[nl]] = rv;
+                    RP.xx[GID[nl]] = xv;
+                }
                 const double z = __dmul_rn(T.invd[od_cls(d)], rv);
                 a2[0] += rv * z;
                 a2[1] += rv * rv;
@@ -284,19 +298,18 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident(ResParams RP) {
         }
     }
 
-    // ---- true residual ||A_c x - b||: publish surface x, gather halo x into PS ----
+    // ---- true residual ||A_c x - b||: surface x was published by the last phase B
+    //      (before the barrier that ended the loop); gather the halo x into PS ----
+    __syncthreads();
 #pragma unroll
     for (int m = 0; m < NPT; ++m) {
         if (od[m] < 0) continue;
-        const int nl = threadIdx.x + m * kResTPB;
-        PS[od_s(od[m])] = XS[nl];
-        if (od_surf(od[m])) RP.xg[GID[nl]] = XS[nl];
+        PS[od_s(od[m])] = XS[threadIdx.x + m * kResTPB];
     }
-    grid.sync();
 #pragma unroll
     for (int t = 0; t < kResKF; ++t) {
         const int e = threadIdx.x + t * kResTPB;
-        if (e < nface && FS[e] >= 0) PS[FS[e]] = __ldcg(RP.xg + FG[e]);
+        if (e < nface && FS[e] >= 0) PS[FS[e]] = it > 0 ? __ldcg(RP.xx + FG[e]) : 0.0;
     }
     __syncthreads();
     double res[2] = {0.0, 0.0};

@@ -23,15 +23,20 @@ def stamps():
     buf = (C.c_uint64 * 128)()
     cnt = C.c_int32()
     N.check(N.lib().tl_debug_profile(buf, 128, C.byref(cnt)))
-    return np.array(buf[:cnt.value], dtype=np.float64)
+    raw = np.array(buf[:cnt.value], dtype=np.float64)
+    n = int(buf[127])
+    return raw[:n], raw[120:123]
 
 
-def report(tag, t):
+def report(tag, tt):
+    t, setup_marks = tt
     if len(t) < 4:
         print(tag, "no stamps")
         return
     d = np.diff(t) / 1e3
     setup = d[0]
+    s = (setup_marks - t[0]) / 1e3
+    print(f"  setup marks (us from start): tables+classes {s[0]:.1f}, faces+own {s[1]:.1f}, rhs {s[2]:.1f}")
     iters = d[1:-1]
     a, b = iters[0::2], iters[1::2]
     print(f"{tag}: total {(t[-1] - t[0]) / 1e3:.1f} us | setup+rhs {setup:.1f} | iters {len(b)}: "
