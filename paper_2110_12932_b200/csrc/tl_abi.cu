@@ -230,6 +230,20 @@ static int launch_solve(tl::PcgParams& P, bool gauss, int sms, double* xg, cudaS
         }
     }
     if (kind_out) *kind_out = 0;
+    if (gauss && xg && P.load == nullptr) {
+        // streaming path: Gaussian load into the second half of the exchange buffer by a
+        // plain kernel, then the lean (non-Gaussian) cooperative solve adds it
+        double* gl = xg + P.g.n;
+        const size_t smem = gauss_smem(P.g);
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(tl::k_gauss_load, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        tl::k_gauss_load<<<2 * sms, 256, smem, st>>>(P.g, P.src, P.mbase, P.T, gl);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return fail(TL_E_CUDA, std::string("k_gauss_load: ") + cudaGetErrorString(e));
+        if (launches) ++*launches;
+        P.load = gl;
+        return launch_pcg(P, false, sms, st, launches);
+    }
     return launch_pcg(P, gauss, sms, st, launches);
 }
 

@@ -396,22 +396,38 @@ __global__ void __launch_bounds__(kTPB) k_pcg(PcgParams P) {
             const double rho = rz;
             const double beta = it > 0 ? rho / rho_prev : 0.0;
             const bool first = it == 0;
-            // ---- phase A ----
+            // ---- phase A: p = z (+ beta p), q = A_c p only for p.q (q is recomputed in B,
+            //      so each iteration moves 64 B/node: r, p read + p written here, x, r, p
+            //      read + x, r written in B).  Nodes two or more away from every face
+            //      take the constant-coefficient path (their neighbours are interior too). ----
             double pq[1] = {0.0};
+            const double ivc = T.invd[13], dgc = T.diag[13];
+            const double c0 = T.c[0][13], c1 = T.c[1][13], c2 = T.c[2][13];
+            const int sy = g.NX, sz = g.NX * g.NY;
             for (int p = beg + threadIdx.x; p < end; p += kTPB) {
                 int i, j, k;
                 decode(g, p, i, j, k);
-                const int cls = class_of(g, i, j, k);
-                auto pn = [&](int q, int qc) -> double {
-                    const double z = __dmul_rn(T.invd[qc], P.r[q]);
-                    return first ? z : __dadd_rn(__dmul_rn(beta, pold[q]), z);
-                };
-                const double pp = pn(p, cls);
-                double qv;
-                if (T.nd[cls] == 0.0) qv = pp;
-                else qv = apply_free(g, T, p, i, j, k, cls, pp, pn);
+                double pp, qv;
+                if (i >= 2 && i <= g.nc[0] - 2 && j >= 2 && j <= g.nc[1] - 2 && k >= 2 && k <= g.nc[2] - 2) {
+                    auto pc = [&](int q) -> double {
+                        const double z = __dmul_rn(ivc, P.r[q]);
+                        return first ? z : __dadd_rn(__dmul_rn(beta, pold[q]), z);
+                    };
+                    pp = pc(p);
+                    const double tx_ = pc(p - 1) + pc(p + 1);
+                    const double ty_ = pc(p - sy) + pc(p + sy);
+                    const double tz_ = pc(p - sz) + pc(p + sz);
+                    qv = dgc * pp - ((c0 * tx_ + c1 * ty_) + c2 * tz_);
+                } else {
+                    const int cls = class_of(g, i, j, k);
+                    auto pn = [&](int q, int qc) -> double {
+                        const double z = __dmul_rn(T.invd[qc], P.r[q]);
+                        return first ? z : __dadd_rn(__dmul_rn(beta, pold[q]), z);
+                    };
+                    pp = pn(p, cls);
+                    qv = (T.nd[cls] == 0.0) ? pp : apply_free(g, T, p, i, j, k, cls, pp, pn);
+                }
                 pnew[p] = pp;
-                P.q[p] = qv;
                 pq[0] += pp * qv;
             }
             block_sum<1>(pq, red);
@@ -429,8 +445,18 @@ __global__ void __launch_bounds__(kTPB) k_pcg(PcgParams P) {
                 decode(g, p, i, j, k);
                 const int cls = class_of(g, i, j, k);
                 const double pp = pnew[p];
+                double qv;
+                if (i >= 1 && i <= g.nc[0] - 1 && j >= 1 && j <= g.nc[1] - 1 && k >= 2 && k <= g.nc[2] - 1 &&
+                    (g.dkind != kGamma || (i >= 2 && i <= g.nc[0] - 2 && j >= 2 && j <= g.nc[1] - 2))) {
+                    // interior class, all six neighbours free: constant coefficients
+                    qv = dgc * pp - ((c0 * (pnew[p - 1] + pnew[p + 1]) + c1 * (pnew[p - sy] + pnew[p + sy])) +
+                                     c2 * (pnew[p - sz] + pnew[p + sz]));
+                } else {
+                    qv = (T.nd[cls] == 0.0) ? pp
+                                            : apply_free(g, T, p, i, j, k, cls, pp, [&](int q, int) { return pnew[q]; });
+                }
                 const double x = __dadd_rn(P.T[p], __dmul_rn(alpha, pp));
-                const double rv = __dsub_rn(P.r[p], __dmul_rn(alpha, P.q[p]));
+                const double rv = __dsub_rn(P.r[p], __dmul_rn(alpha, qv));
                 P.T[p] = x;
                 P.r[p] = rv;
                 const double z = __dmul_rn(T.invd[cls], rv);
@@ -489,6 +515,37 @@ __global__ void __launch_bounds__(kTPB) k_pcg(PcgParams P) {
         P.info->bnorm = bnorm;
         P.info->rnorm = rnorm;
         P.info->true_resid = tres;
+    }
+}
+
+// ---------------------------------------------------------------------------------
+// Gaussian nodal load as a dense array, for the streaming solve (keeps the Gaussian's
+// registers out of the iteration loop).  Applies the same exact cutoff as add_gaussian
+// against b0 = (rho c/dt) V n_p/24 * T_old: load = F, or 0 where F cannot change b0.
+// ---------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_gauss_load(Grid g, Gauss src, double mbase, const double* T,
+                                                    double* load) {
+    extern __shared__ double gtab[];
+    __shared__ double massc[27];
+    double *tx = gtab, *ty = tx + 6 * g.nc[0], *tz = ty + 6 * g.nc[1];
+    double *bx_ = tz + 6 * g.nc[2], *by_ = bx_ + g.NX, *bz_ = by_ + g.NY;
+    build_gauss_tables(g, src, tx, ty, tz);
+    if (threadIdx.x < 27) {
+        int n_p, n_e[3], cnt[3], h0[3], h1[3];
+        class_counts(threadIdx.x, n_p, n_e, cnt, h0, h1);
+        massc[threadIdx.x] = class_is_dirichlet(threadIdx.x, g.dkind) ? -1.0 : mbase * (double)n_p;
+    }
+    __syncthreads();
+    build_gauss_bounds(g, tx, ty, tz, bx_, by_, bz_);
+    __syncthreads();
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < g.n; p += gridDim.x * blockDim.x) {
+        int i, j, k;
+        decode(g, p, i, j, k);
+        const double m = massc[class_of(g, i, j, k)];
+        if (m < 0.0) { load[p] = 0.0; continue; }
+        const double b0 = m * T[p];
+        const double bound = 24.0 * bx_[i] * by_[j] * bz_[k];
+        load[p] = (b0 > 0.0 && bound < b0 * 0x1p-55) ? 0.0 : gaussian_node_fast(g, tx, ty, tz, i, j, k);
     }
 }
 
