@@ -306,6 +306,112 @@ __device__ __forceinline__ double apply_free(const Grid& g, const ClassTable& T,
     return y - s;
 }
 
+// ---- streaming CG phases (vectors in global memory) --------------------------------
+// Two nodes per loop trip with __restrict__ operands so both nodes' 14 stencil loads
+// are in flight together (memory-level parallelism for the HBM-bound grids).
+
+// phase A for one node: pp = z (+ beta p_old), qv = (A_c p)_p
+__device__ __forceinline__ void stream_a_node(const Grid& g, const ClassTable& T, int p,
+                                              const double* __restrict__ r, const double* __restrict__ pold,
+                                              bool first, double beta, double& pp, double& qv) {
+    int i, j, k;
+    decode(g, p, i, j, k);
+    const int sy = g.NX, sz = g.NX * g.NY;
+    if (i >= 2 && i <= g.nc[0] - 2 && j >= 2 && j <= g.nc[1] - 2 && k >= 2 && k <= g.nc[2] - 2) {
+        // node and neighbours interior: constant coefficients (class 13)
+        const double ivc = T.invd[13];
+        auto pc = [&](int q) -> double {
+            const double z = __dmul_rn(ivc, r[q]);
+            return first ? z : __dadd_rn(__dmul_rn(beta, pold[q]), z);
+        };
+        pp = pc(p);
+        const double tx_ = pc(p - 1) + pc(p + 1);
+        const double ty_ = pc(p - sy) + pc(p + sy);
+        const double tz_ = pc(p - sz) + pc(p + sz);
+        qv = T.diag[13] * pp - ((T.c[0][13] * tx_ + T.c[1][13] * ty_) + T.c[2][13] * tz_);
+    } else {
+        const int cls = class_of(g, i, j, k);
+        auto pn = [&](int q, int qc) -> double {
+            const double z = __dmul_rn(T.invd[qc], r[q]);
+            return first ? z : __dadd_rn(__dmul_rn(beta, pold[q]), z);
+        };
+        pp = pn(p, cls);
+        qv = (T.nd[cls] == 0.0) ? pp : apply_free(g, T, p, i, j, k, cls, pp, pn);
+    }
+}
+
+__device__ __forceinline__ double stream_phase_a(const Grid& g, const ClassTable& T, int beg, int stride,
+                                                 const double* __restrict__ r, const double* __restrict__ pold,
+                                                 double* __restrict__ pnew, bool first, double beta) {
+    double pq = 0.0;
+    int p = beg;
+    for (; p + stride < g.n; p += 2 * stride) {
+        double pa, qa, pb, qb;
+        stream_a_node(g, T, p, r, pold, first, beta, pa, qa);
+        stream_a_node(g, T, p + stride, r, pold, first, beta, pb, qb);
+        pnew[p] = pa;
+        pnew[p + stride] = pb;
+        pq += pa * qa;
+        pq += pb * qb;
+    }
+    if (p < g.n) {
+        double pa, qa;
+        stream_a_node(g, T, p, r, pold, first, beta, pa, qa);
+        pnew[p] = pa;
+        pq += pa * qa;
+    }
+    return pq;
+}
+
+// phase B for one node: q recomputed from the stored p; returns (x_new, r_new, invd)
+__device__ __forceinline__ void stream_b_node(const Grid& g, const ClassTable& T, int p,
+                                              const double* __restrict__ pnew, double& pp, double& qv,
+                                              double& iv) {
+    int i, j, k;
+    decode(g, p, i, j, k);
+    const int cls = class_of(g, i, j, k);
+    const int sy = g.NX, sz = g.NX * g.NY;
+    pp = pnew[p];
+    iv = T.invd[cls];
+    if (i >= 1 && i <= g.nc[0] - 1 && j >= 1 && j <= g.nc[1] - 1 && k >= 2 && k <= g.nc[2] - 1 &&
+        (g.dkind != kGamma || (i >= 2 && i <= g.nc[0] - 2 && j >= 2 && j <= g.nc[1] - 2))) {
+        // interior class with six free neighbours
+        qv = T.diag[13] * pp - ((T.c[0][13] * (pnew[p - 1] + pnew[p + 1]) +
+                                 T.c[1][13] * (pnew[p - sy] + pnew[p + sy])) +
+                                T.c[2][13] * (pnew[p - sz] + pnew[p + sz]));
+    } else {
+        qv = (T.nd[cls] == 0.0) ? pp : apply_free(g, T, p, i, j, k, cls, pp, [&](int q, int) { return pnew[q]; });
+    }
+}
+
+__device__ __forceinline__ void stream_phase_b(const Grid& g, const ClassTable& T, int beg, int stride,
+                                               double* __restrict__ x, double* __restrict__ r,
+                                               const double* __restrict__ pnew, double alpha, double& rz,
+                                               double& rr) {
+    auto finish = [&](int p, double pp, double qv, double iv) {
+        const double xv = __dadd_rn(x[p], __dmul_rn(alpha, pp));
+        const double rv = __dsub_rn(r[p], __dmul_rn(alpha, qv));
+        x[p] = xv;
+        r[p] = rv;
+        const double z = __dmul_rn(iv, rv);
+        rz += rv * z;
+        rr += rv * rv;
+    };
+    int p = beg;
+    for (; p + stride < g.n; p += 2 * stride) {
+        double pa, qa, ia, pb, qb, ib;
+        stream_b_node(g, T, p, pnew, pa, qa, ia);
+        stream_b_node(g, T, p + stride, pnew, pb, qb, ib);
+        finish(p, pa, qa, ia);
+        finish(p + stride, pb, qb, ib);
+    }
+    if (p < g.n) {
+        double pa, qa, ia;
+        stream_b_node(g, T, p, pnew, pa, qa, ia);
+        finish(p, pa, qa, ia);
+    }
+}
+
 // ---------------------------------------------------------------------------------
 // Persistent cooperative PCG.  grid.sync() separates the phases:
 //   phase 0: b, r = b, x = 0, partial ||b||^2 and r.z             | sync
@@ -316,7 +422,7 @@ __device__ __forceinline__ double apply_free(const Grid& g, const ClassTable& T,
 //            x_D = g, info
 // ---------------------------------------------------------------------------------
 template <bool GAUSS>
-__global__ void __launch_bounds__(kTPB) k_pcg(PcgParams P) {
+__global__ void __launch_bounds__(kTPB, 2) k_pcg(PcgParams P) {
     cg::grid_group grid = cg::this_grid();
     __shared__ ClassTable T;
     __shared__ double red[4 * 32];
@@ -334,13 +440,15 @@ __global__ void __launch_bounds__(kTPB) k_pcg(PcgParams P) {
     }
 
     const int G = gridDim.x;
-    const int per = (g.n + G - 1) / G;
-    const int beg = blockIdx.x * per;
-    const int end = min(g.n, beg + per);
+    // nodes interleaved across CTAs (grid stride): faces and edges, which take the
+    // class-table path, are spread evenly instead of landing on a few CTAs
+    const int beg = blockIdx.x * kTPB + threadIdx.x;
+    const int stride = G * kTPB;
+    const int end = g.n;
 
     // ---- phase 0: constrained RHS (fem.py:169-191 + 89-105) ----
     double acc[2] = {0.0, 0.0};
-    for (int p = beg + threadIdx.x; p < end; p += kTPB) {
+    for (int p = beg; p < end; p += stride) {
         int i, j, k;
         decode(g, p, i, j, k);
         const int cls = class_of(g, i, j, k);
@@ -400,36 +508,7 @@ __global__ void __launch_bounds__(kTPB) k_pcg(PcgParams P) {
             //      so each iteration moves 64 B/node: r, p read + p written here, x, r, p
             //      read + x, r written in B).  Nodes two or more away from every face
             //      take the constant-coefficient path (their neighbours are interior too). ----
-            double pq[1] = {0.0};
-            const double ivc = T.invd[13], dgc = T.diag[13];
-            const double c0 = T.c[0][13], c1 = T.c[1][13], c2 = T.c[2][13];
-            const int sy = g.NX, sz = g.NX * g.NY;
-            for (int p = beg + threadIdx.x; p < end; p += kTPB) {
-                int i, j, k;
-                decode(g, p, i, j, k);
-                double pp, qv;
-                if (i >= 2 && i <= g.nc[0] - 2 && j >= 2 && j <= g.nc[1] - 2 && k >= 2 && k <= g.nc[2] - 2) {
-                    auto pc = [&](int q) -> double {
-                        const double z = __dmul_rn(ivc, P.r[q]);
-                        return first ? z : __dadd_rn(__dmul_rn(beta, pold[q]), z);
-                    };
-                    pp = pc(p);
-                    const double tx_ = pc(p - 1) + pc(p + 1);
-                    const double ty_ = pc(p - sy) + pc(p + sy);
-                    const double tz_ = pc(p - sz) + pc(p + sz);
-                    qv = dgc * pp - ((c0 * tx_ + c1 * ty_) + c2 * tz_);
-                } else {
-                    const int cls = class_of(g, i, j, k);
-                    auto pn = [&](int q, int qc) -> double {
-                        const double z = __dmul_rn(T.invd[qc], P.r[q]);
-                        return first ? z : __dadd_rn(__dmul_rn(beta, pold[q]), z);
-                    };
-                    pp = pn(p, cls);
-                    qv = (T.nd[cls] == 0.0) ? pp : apply_free(g, T, p, i, j, k, cls, pp, pn);
-                }
-                pnew[p] = pp;
-                pq[0] += pp * qv;
-            }
+            double pq[1] = {stream_phase_a(g, T, beg, stride, P.r, pold, pnew, first, beta)};
             block_sum<1>(pq, red);
             if (threadIdx.x == 0) P.part[2 * G + blockIdx.x] = pq[0];
             grid.sync();
@@ -440,29 +519,7 @@ __global__ void __launch_bounds__(kTPB) k_pcg(PcgParams P) {
             const double alpha = rho / tot[0];
             // ---- phase B ----
             double a2[2] = {0.0, 0.0};
-            for (int p = beg + threadIdx.x; p < end; p += kTPB) {
-                int i, j, k;
-                decode(g, p, i, j, k);
-                const int cls = class_of(g, i, j, k);
-                const double pp = pnew[p];
-                double qv;
-                if (i >= 1 && i <= g.nc[0] - 1 && j >= 1 && j <= g.nc[1] - 1 && k >= 2 && k <= g.nc[2] - 1 &&
-                    (g.dkind != kGamma || (i >= 2 && i <= g.nc[0] - 2 && j >= 2 && j <= g.nc[1] - 2))) {
-                    // interior class, all six neighbours free: constant coefficients
-                    qv = dgc * pp - ((c0 * (pnew[p - 1] + pnew[p + 1]) + c1 * (pnew[p - sy] + pnew[p + sy])) +
-                                     c2 * (pnew[p - sz] + pnew[p + sz]));
-                } else {
-                    qv = (T.nd[cls] == 0.0) ? pp
-                                            : apply_free(g, T, p, i, j, k, cls, pp, [&](int q, int) { return pnew[q]; });
-                }
-                const double x = __dadd_rn(P.T[p], __dmul_rn(alpha, pp));
-                const double rv = __dsub_rn(P.r[p], __dmul_rn(alpha, qv));
-                P.T[p] = x;
-                P.r[p] = rv;
-                const double z = __dmul_rn(T.invd[cls], rv);
-                a2[0] += rv * z;
-                a2[1] += rv * rv;
-            }
+            stream_phase_b(g, T, beg, stride, P.T, P.r, pnew, alpha, a2[0], a2[1]);
             block_sum<2>(a2, red);
             if (threadIdx.x == 0) { P.part[0 * G + blockIdx.x] = a2[0]; P.part[1 * G + blockIdx.x] = a2[1]; }
             grid.sync();
@@ -480,7 +537,7 @@ __global__ void __launch_bounds__(kTPB) k_pcg(PcgParams P) {
 
     // ---- true residual ||A_c x - b|| / ||b|| (fem.py:286) and finite check ----
     double res[2] = {0.0, 0.0};
-    for (int p = beg + threadIdx.x; p < end; p += kTPB) {
+    for (int p = beg; p < end; p += stride) {
         int i, j, k;
         decode(g, p, i, j, k);
         const int cls = class_of(g, i, j, k);
@@ -501,7 +558,7 @@ __global__ void __launch_bounds__(kTPB) k_pcg(PcgParams P) {
     }
     const double tres = bnorm > 0.0 ? sqrt(tot[0]) / bnorm : 0.0;
     // ---- re-impose Dirichlet values (fem.py:289-290): x_D = g = b_D ----
-    for (int p = beg + threadIdx.x; p < end; p += kTPB) {
+    for (int p = beg; p < end; p += stride) {
         int i, j, k;
         decode(g, p, i, j, k);
         const int cls = class_of(g, i, j, k);
