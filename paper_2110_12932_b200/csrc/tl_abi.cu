@@ -144,7 +144,7 @@ static BrickPlan plan_bricks_uncached(const tl::Grid& g, bool gauss, int sms, si
             }
     if (best.ok) {
         int npt = (best.maxnodes + tl::kResTPB - 1) / tl::kResTPB;
-        best.npt = npt <= 2 ? 2 : npt <= 4 ? 4 : npt <= 6 ? 6 : npt <= 8 ? 8 : npt <= 10 ? 10 : 12;
+        best.npt = npt <= 4 ? 4 : npt <= 8 ? 8 : 12;
     }
     return best;
 }
@@ -173,25 +173,43 @@ static unsigned long long* prof_buffer() {
     return g_prof;
 }
 
-template <bool GAUSS, int NPT>
+// TLGPU_EXACT_CG=1 selects the two-barrier kernel that mirrors scipy's cg operation for
+// operation; the default is the one-barrier variant (same recurrences, identity scalars).
+static bool exact_cg() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("TLGPU_EXACT_CG");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
+}
+
+template <bool GAUSS, int NPT, bool ONEBAR>
 static cudaError_t launch_res_t(tl::ResParams& RP, int G, size_t smem, cudaStream_t st) {
-    auto fn = tl::k_pcg_resident<GAUSS, NPT>;
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
+    auto fn = tl::k_pcg_resident<GAUSS, NPT, ONEBAR>;
+    static thread_local size_t set_smem = 0;      // attribute set once per instantiation
+    if (set_smem < smem) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        if (e != cudaSuccess) return e;
+        set_smem = 220 * 1024;
+    }
     void* args[] = {&RP};
     return cudaLaunchCooperativeKernel((void*)fn, G, tl::kResTPB, args, smem, st);
 }
 
+template <bool GAUSS, bool ONEBAR>
+static cudaError_t launch_res_n(tl::ResParams& RP, int npt, int G, size_t smem, cudaStream_t st) {
+    switch (npt) {
+        case 4: return launch_res_t<GAUSS, 4, ONEBAR>(RP, G, smem, st);
+        case 8: return launch_res_t<GAUSS, 8, ONEBAR>(RP, G, smem, st);
+        default: return launch_res_t<GAUSS, 12, ONEBAR>(RP, G, smem, st);
+    }
+}
+
 template <bool GAUSS>
 static cudaError_t launch_res_g(tl::ResParams& RP, int npt, int G, size_t smem, cudaStream_t st) {
-    switch (npt) {
-        case 2: return launch_res_t<GAUSS, 2>(RP, G, smem, st);
-        case 4: return launch_res_t<GAUSS, 4>(RP, G, smem, st);
-        case 6: return launch_res_t<GAUSS, 6>(RP, G, smem, st);
-        case 8: return launch_res_t<GAUSS, 8>(RP, G, smem, st);
-        case 10: return launch_res_t<GAUSS, 10>(RP, G, smem, st);
-        default: return launch_res_t<GAUSS, 12>(RP, G, smem, st);
-    }
+    return exact_cg() ? launch_res_n<GAUSS, false>(RP, npt, G, smem, st)
+                      : launch_res_n<GAUSS, true>(RP, npt, G, smem, st);
 }
 
 static int g_force_streaming = -1;
@@ -212,8 +230,9 @@ static int launch_solve(tl::PcgParams& P, bool gauss, int sms, double* xg, cudaS
         if (bp.ok) {
             tl::ResParams RP{};
             RP.P = P;
-            RP.xg = xg;              // exchange buffer holds 2 n doubles: r, then x
+            RP.xg = xg;              // exchange buffer holds 4 n doubles: r, x, q (x2)
             RP.xx = xg + P.g.n;
+            RP.xq = xg + 2 * (size_t)P.g.n;   // 2 n: ping-pong
             RP.prof = prof_buffer();
             const int N[3] = {P.g.NX, P.g.NY, P.g.NZ};
             for (int a = 0; a < 3; ++a) {
@@ -378,7 +397,7 @@ int32_t tl_step_host(const tl_grid_desc* grid, double kappa, double rho_c, doubl
         P.src.on = 1;
     }
     double* xg = nullptr;
-    if ((rc = dalloc(&xg, 2 * (size_t)n))) return rc;
+    if ((rc = dalloc(&xg, 4 * (size_t)n))) return rc;
     rc = launch_solve(P, gauss, sms, xg, 0, nullptr);
     if (rc) return rc;
     TL_CUDA(cudaDeviceSynchronize());
@@ -486,7 +505,7 @@ int32_t tl_run_create(const tl_run_desc* desc, tl_run** out) {
         (rc = dalloc(&R->Tl_before, nl)) || (rc = dalloc(&R->part, 4 * R->sms * 32)) ||
         (rc = dalloc(&R->dep_prev, tl::kDepMax)) || (rc = dalloc(&R->dep_prev_n, 1)) ||
         (rc = dalloc(&R->melt, 4)) || (rc = dalloc(&R->melt_part, 2 * 1184)) ||
-        (rc = dalloc(&R->xg, 2 * (size_t)std::max(ng, nl)))) {
+        (rc = dalloc(&R->xg, 4 * (size_t)std::max(ng, nl)))) {
         tl_run_destroy(R);
         return rc;
     }

@@ -340,12 +340,27 @@ __device__ __forceinline__ void stream_a_node(const Grid& g, const ClassTable& T
     }
 }
 
+// L2 prefetch of the lines a sweep will first touch kPfTrips grid-stride trips ahead
+// (the +z plane of the stencil vectors and the unit-stride vectors): raises the DRAM
+// requests in flight without holding registers.
+constexpr int kPfTrips = 4;
+
+__device__ __forceinline__ void prefetch_l2(const double* a) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+}
+
 __device__ __forceinline__ double stream_phase_a(const Grid& g, const ClassTable& T, int beg, int stride,
                                                  const double* __restrict__ r, const double* __restrict__ pold,
                                                  double* __restrict__ pnew, bool first, double beta) {
     double pq = 0.0;
     int p = beg;
+    const int sz = g.NX * g.NY;
     for (; p + stride < g.n; p += 2 * stride) {
+        const int pf = p + kPfTrips * stride + sz;
+        if (pf < g.n) {
+            prefetch_l2(r + pf);
+            if (!first) prefetch_l2(pold + pf);
+        }
         double pa, qa, pb, qb;
         stream_a_node(g, T, p, r, pold, first, beta, pa, qa);
         stream_a_node(g, T, p + stride, r, pold, first, beta, pb, qb);
@@ -398,7 +413,14 @@ __device__ __forceinline__ void stream_phase_b(const Grid& g, const ClassTable& 
         rr += rv * rv;
     };
     int p = beg;
+    const int sz = g.NX * g.NY;
     for (; p + stride < g.n; p += 2 * stride) {
+        const int pf = p + kPfTrips * stride;
+        if (pf + sz < g.n) prefetch_l2(pnew + pf + sz);
+        if (pf < g.n) {
+            prefetch_l2(x + pf);
+            prefetch_l2(r + pf);
+        }
         double pa, qa, ia, pb, qb, ib;
         stream_b_node(g, T, p, pnew, pa, qa, ia);
         stream_b_node(g, T, p + stride, pnew, pb, qb, ib);
