@@ -173,43 +173,26 @@ static unsigned long long* prof_buffer() {
     return g_prof;
 }
 
-// TLGPU_EXACT_CG=1 selects the two-barrier kernel that mirrors scipy's cg operation for
-// operation; the default is the one-barrier variant (same recurrences, identity scalars).
-static bool exact_cg() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("TLGPU_EXACT_CG");
-        v = (e && e[0] == '1') ? 1 : 0;
-    }
-    return v == 1;
-}
-
-template <bool GAUSS, int NPT, bool ONEBAR>
+template <bool GAUSS, int NPT>
 static cudaError_t launch_res_t(tl::ResParams& RP, int G, size_t smem, cudaStream_t st) {
-    auto fn = tl::k_pcg_resident<GAUSS, NPT, ONEBAR>;
-    static thread_local size_t set_smem = 0;      // attribute set once per instantiation
-    if (set_smem < smem) {
+    auto fn = tl::k_pcg_resident<GAUSS, NPT>;
+    static thread_local bool attr_set = false;      // attribute set once per instantiation
+    if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
         if (e != cudaSuccess) return e;
-        set_smem = 220 * 1024;
+        attr_set = true;
     }
     void* args[] = {&RP};
     return cudaLaunchCooperativeKernel((void*)fn, G, tl::kResTPB, args, smem, st);
 }
 
-template <bool GAUSS, bool ONEBAR>
-static cudaError_t launch_res_n(tl::ResParams& RP, int npt, int G, size_t smem, cudaStream_t st) {
-    switch (npt) {
-        case 4: return launch_res_t<GAUSS, 4, ONEBAR>(RP, G, smem, st);
-        case 8: return launch_res_t<GAUSS, 8, ONEBAR>(RP, G, smem, st);
-        default: return launch_res_t<GAUSS, 12, ONEBAR>(RP, G, smem, st);
-    }
-}
-
 template <bool GAUSS>
 static cudaError_t launch_res_g(tl::ResParams& RP, int npt, int G, size_t smem, cudaStream_t st) {
-    return exact_cg() ? launch_res_n<GAUSS, false>(RP, npt, G, smem, st)
-                      : launch_res_n<GAUSS, true>(RP, npt, G, smem, st);
+    switch (npt) {
+        case 4: return launch_res_t<GAUSS, 4>(RP, G, smem, st);
+        case 8: return launch_res_t<GAUSS, 8>(RP, G, smem, st);
+        default: return launch_res_t<GAUSS, 12>(RP, G, smem, st);
+    }
 }
 
 static int g_force_streaming = -1;
@@ -232,7 +215,6 @@ static int launch_solve(tl::PcgParams& P, bool gauss, int sms, double* xg, cudaS
             RP.P = P;
             RP.xg = xg;              // exchange buffer holds 4 n doubles: r, x, q (x2)
             RP.xx = xg + P.g.n;
-            RP.xq = xg + 2 * (size_t)P.g.n;   // 2 n: ping-pong
             RP.prof = prof_buffer();
             const int N[3] = {P.g.NX, P.g.NY, P.g.NZ};
             for (int a = 0; a < 3; ++a) {

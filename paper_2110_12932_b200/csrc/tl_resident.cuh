@@ -27,7 +27,6 @@ struct ResParams {
     PcgParams P;                  // grid, coefficients, inputs, workspace (b, part, info)
     double* xg;                   // global exchange array (brick-surface r), n doubles
     double* xx;                   // global exchange array (brick-surface x), n doubles
-    double* xq;                   // one-barrier mode: brick-surface q, 2 n doubles (ping-pong)
     unsigned long long* prof;     // optional phase timestamps (block 0), or nullptr
     int ng[3];                    // bricks per axis
     int off[3][kResMaxSplit + 1]; // brick boundaries per axis (node indices)
@@ -62,14 +61,8 @@ __device__ __forceinline__ double stencil_smem(const ClassTable& T, const double
     return T.diag[cls] * V[s] - ((T.c[0][cls] * tx_ + T.c[1][cls] * ty_) + T.c[2][cls] * tz_);
 }
 
-// ONEBAR = false: scipy's cg operation for operation, two grid barriers per iteration
-//   (p.q; then r.z and r.r).
-// ONEBAR = true: the same x, r, p, q recurrences, but rho' = r'.z' and |r'|^2 from the
-//   exact identities rho' = rho - 2 alpha q.z + alpha^2 q.Mq and
-//   |r'|^2 = |r|^2 - 2 alpha q.r + alpha^2 q.q, so the five dots of one iteration travel
-//   in a single reduction and only q crosses CTAs: one grid barrier per iteration.
-//   Scalars differ from scipy's only by rounding (parity section).
-template <bool GAUSS, int NPT, bool ONEBAR>
+// scipy's cg operation for operation: two grid barriers per iteration (p.q; then r.z, r.r).
+template <bool GAUSS, int NPT>
 __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident(ResParams RP) {
     cg::grid_group grid = cg::this_grid();
     const PcgParams& P = RP.P;
@@ -220,103 +213,7 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident(ResParams RP) {
     double rho_prev = 1.0;
 
     double q[NPT];
-    if (ONEBAR && bb != 0.0) {
-        // halo r0 (published with b in phase 0) into RS
-#pragma unroll
-        for (int t = 0; t < kResKF; ++t) {
-            const int e = threadIdx.x + t * kResTPB;
-            if (e < nface && FS[e] >= 0) RS[FS[e]] = __ldcg(RP.xg + FG[e]);
-        }
-        double rr = bb;
-        double rho = rz;
-        while (true) {
-            if (it > 0) {
-                // tot = [p.q, q.z, q.Mq, q.r, q.q] of iteration it-1: finish it (scipy's
-                // second half): alpha, x += alpha p, r -= alpha q on own + halo nodes
-                const double alpha = rho / tot[0];
-                const double rho_new = (rho - (2.0 * alpha) * tot[1]) + (alpha * alpha) * tot[2];
-                rr = (rr - (2.0 * alpha) * tot[3]) + (alpha * alpha) * tot[4];
-                const double* qin = RP.xq + (size_t)((it - 1) & 1) * g.n;
-                double fq[kResKF];
-#pragma unroll
-                for (int t = 0; t < kResKF; ++t) {
-                    const int e = threadIdx.x + t * kResTPB;
-                    fq[t] = (e < nface && FS[e] >= 0) ? __ldcg(qin + FG[e]) : 0.0;
-                }
-#pragma unroll
-                for (int m = 0; m < NPT; ++m) {
-                    if (od[m] < 0) continue;
-                    const int d = od[m], s = od_s(d), nl = threadIdx.x + m * kResTPB;
-                    const double xv = __dadd_rn(XS[nl], __dmul_rn(alpha, PS[s]));
-                    XS[nl] = xv;
-                    RS[s] = __dsub_rn(RS[s], __dmul_rn(alpha, q[m]));
-                    if (od_surf(d)) RP.xx[GID[nl]] = xv;
-                }
-#pragma unroll
-                for (int t = 0; t < kResKF; ++t) {
-                    const int e = threadIdx.x + t * kResTPB;
-                    if (e < nface && FS[e] >= 0) RS[FS[e]] = __dsub_rn(RS[FS[e]], __dmul_rn(alpha, fq[t]));
-                }
-                rho_prev = rho;
-                rho = rho_new;
-            }
-            rnorm = sqrt(fmax(rr, 0.0));
-            if (rnorm < atol) { status = 0; break; }
-            if (!isfinite(rnorm)) { status = 3; break; }
-            if (it >= P.maxiter) { status = 1; break; }
-            const double beta = it > 0 ? rho / rho_prev : 0.0;
-            const bool first = it == 0;
-            // p = z (+ beta p) on own + halo nodes (each thread touches the nodes whose r it set)
-#pragma unroll
-            for (int m = 0; m < NPT; ++m) {
-                if (od[m] < 0) continue;
-                const int s = od_s(od[m]);
-                const double z = __dmul_rn(T.invd[od_cls(od[m])], RS[s]);
-                PS[s] = first ? z : __dadd_rn(__dmul_rn(beta, PS[s]), z);
-            }
-#pragma unroll
-            for (int t = 0; t < kResKF; ++t) {
-                const int e = threadIdx.x + t * kResTPB;
-                if (e >= nface) break;
-                const int s = FS[e];
-                if (s < 0) continue;
-                const double z = __dmul_rn(T.invd[CL[s]], RS[s]);
-                PS[s] = first ? z : __dadd_rn(__dmul_rn(beta, PS[s]), z);
-            }
-            __syncthreads();
-            // q = A_c p; the five dots; publish surface q
-            double d5[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-            double* qout = RP.xq + (size_t)(it & 1) * g.n;
-#pragma unroll
-            for (int m = 0; m < NPT; ++m) {
-                if (od[m] < 0) continue;
-                const int d = od[m], s = od_s(d), cls = od_cls(d);
-                const double pp = PS[s];
-                const double qv = (T.nd[cls] == 0.0) ? pp : stencil_smem(T, PS, s, cls, od_mask(d), SY, SZ);
-                q[m] = qv;
-                const double iv = T.invd[cls];
-                const double rv = RS[s];
-                d5[0] += pp * qv;
-                d5[1] += qv * __dmul_rn(iv, rv);
-                d5[2] += qv * __dmul_rn(iv, qv);
-                d5[3] += qv * rv;
-                d5[4] += qv * qv;
-                if (od_surf(d)) qout[GID[threadIdx.x + m * kResTPB]] = qv;
-            }
-            block_sum<5>(d5, red);
-            if (threadIdx.x == 0)
-#pragma unroll
-                for (int e = 0; e < 5; ++e) P.part[e * G + b] = d5[e];
-            grid.sync();
-            {
-                const int s5[5] = {0, 1, 2, 3, 4};
-                grid_sum_fast<5>(P.part, s5, G, tot);
-            }
-            if (prof && it < 64) RP.prof[np++] = global_ns();
-            ++it;
-        }
-        grid.sync();      // surface x of the final update visible to the neighbours
-    } else if (bb != 0.0) {
+    if (bb != 0.0) {
         while (true) {
             if (rnorm < atol) { status = 0; break; }
             if (!isfinite(rnorm)) { status = 3; break; }
