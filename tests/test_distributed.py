@@ -1,0 +1,81 @@
+"""Host-side multi-rank logic on CPU (gloo, world_size 2): scenario sharding (config 5)
+and the max-over-ranks timing reduction bench.py uses."""
+
+import os
+import socket
+
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2110_12932_b200 import dist as D
+from paper_2110_12932_b200 import scenarios as S
+
+
+def test_cfg5_draw_matches_survey_probe():
+    """SURVEY Probe P10: seed 0 gives m counts {5: 24, 10: 23, 20: 17}, 418-980 macro
+    steps per scenario, 37,853 in total, 2.31e11 DOF-timesteps."""
+    sc = S.draw(0, 64)
+    counts = {m: sum(s.micro == m for s in sc) for m in (5, 10, 20)}
+    assert counts == {5: 24, 10: 23, 20: 17}
+    assert min(s.n_macro for s in sc) == 418 and max(s.n_macro for s in sc) == 980
+    assert sum(s.n_macro for s in sc) == 37853
+    assert sum(s.dof_timesteps for s in sc) == pytest.approx(2.31e11, rel=5e-3)
+
+
+def test_scenario_config_loads():
+    s = S.draw()[7]
+    cfg = s.config()
+    assert cfg.micro_steps == s.micro and cfg.beam.power == s.power
+    assert abs(cfg.path.segments[0].start[1] - (1.5e-3 - 2 * s.hatch)) < 1e-15
+    assert abs(cfg.t_end / 2e-5 - s.n_macro) < 1e-9
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_shard_is_a_balanced_partition(world):
+    sc = S.draw()
+    parts = [S.shard(sc, r, world) for r in range(world)]
+    idx = sorted(s.index for p in parts for s in p)
+    assert idx == list(range(64))
+    loads = [sum(s.dof_timesteps for s in p) for p in parts]
+    assert max(loads) - min(loads) <= max(s.dof_timesteps for s in sc)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        r, w, lr = D.world_from_env()
+        mine = S.shard(S.draw(), r, w)
+        gathered = [None] * w
+        dist.all_gather_object(gathered, [s.index for s in mine])
+        tmax = D.max_over_ranks(10.0 * (r + 1))
+        total = D.sum_over_ranks(sum(s.dof_timesteps for s in mine))
+        q.put((r, gathered, tmax, total))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_two_ranks_shard_and_reduce():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r, gathered, tmax, total in out:
+        assert sorted(i for g in gathered for i in g) == list(range(64))
+        assert tmax == 20.0
+        assert total == sum(s.dof_timesteps for s in S.draw())
