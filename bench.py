@@ -263,7 +263,8 @@ def main():
     if tfile.exists():
         traffic = json.loads(tfile.read_text()).get(f"{args.config}_local_pcg_dram_bytes_per_launch")
     roofline = {"bound": "hbm", "achieved": kloc["achieved_gbs"], "peak": peak, "unit": "GB/s",
-                "frac": kloc["achieved_gbs"] / peak, "traffic": traffic, "kernel": "k_pcg<true> (local solve)",
+                "frac": kloc["achieved_gbs"] / peak, "traffic": traffic,
+                "kernel": "local-grid PCG solve (k_pcg_resident when the grid fits on chip, else k_pcg)",
                 "peak_source": peak_src,
                 "note": "algorithmic bytes N(64k+32) per solve (SURVEY §8d); cfg2 vectors are L2-resident"}
 
