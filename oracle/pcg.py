@@ -70,3 +70,40 @@ def solve_constrained(op, b: np.ndarray, g_flat: np.ndarray, rtol: float):
         raise OracleNonConvergence(abs(info) or -1, res)
     x[D] = g_flat[D]
     return x, its, res
+
+
+def cg_chronopoulos_gear(apply, b: np.ndarray, inv_diag: np.ndarray, rtol: float, maxiter: int):
+    """Chronopoulos-Gear PCG (one reduction per iteration), as the device's default
+    resident kernel runs it (csrc/tl_resident_cg.cuh): same stop test as scipy's cg
+    (||r|| < rtol ||b|| at the top of each iteration), iterates equal to CG's in exact
+    arithmetic.  Returns (x, info, iterations)."""
+    bnrm2 = np.linalg.norm(b)
+    if bnrm2 == 0:
+        return b, 0, 0
+    atol = float(rtol) * float(bnrm2)
+    x = np.zeros_like(b)
+    r = b.copy()
+    rr = np.dot(r, r)
+    u = inv_diag * r
+    w = apply(u)
+    gam, dlt = np.dot(r, u), np.dot(w, u)
+    p = s = None
+    gam_prev = alpha_prev = 1.0
+    for it in range(maxiter):
+        if np.sqrt(rr) < atol:
+            return x, 0, it
+        if it == 0:
+            beta, alpha = 0.0, gam / dlt
+            p, s = u.copy(), w.copy()
+        else:
+            beta = gam / gam_prev
+            alpha = gam / (dlt - beta * gam / alpha_prev)
+            p = u + beta * p
+            s = w + beta * s
+        x = x + alpha * p
+        r = r - alpha * s
+        u = inv_diag * r
+        w = apply(u)
+        gam_prev, alpha_prev = gam, alpha
+        gam, dlt, rr = np.dot(r, u), np.dot(w, u), np.dot(r, r)
+    return x, maxiter, maxiter

@@ -17,7 +17,7 @@
 #include <vector>
 
 #include "../../include/tlgpu.h"
-#include "tl_resident.cuh"
+#include "tl_resident_cg.cuh"
 
 namespace {
 
@@ -111,7 +111,7 @@ static void split_axis(int N, int parts, int* off) {
     for (int e = 0; e <= parts; ++e) off[e] = (int)((long long)N * e / parts);
 }
 
-static BrickPlan plan_bricks_uncached(const tl::Grid& g, bool gauss, int sms, size_t smem_cap) {
+static BrickPlan plan_bricks_uncached(const tl::Grid& g, bool gauss, int sms, size_t smem_cap, bool cgv) {
     BrickPlan best;
     const int N[3] = {g.NX, g.NY, g.NZ};
     const long long n = (long long)g.n;
@@ -128,7 +128,7 @@ static BrickPlan plan_bricks_uncached(const tl::Grid& g, bool gauss, int sms, si
                 const int own = lx * ly * lz;
                 const int H = (lx + 2) * (ly + 2) * (lz + 2);
                 const int nface = 2 * (ly * lz + lx * lz + lx * ly);
-                const size_t smem = tl::res_smem_bytes(lx, ly, lz, gtab);
+                const size_t smem = cgv ? tl::rescg_smem_bytes(lx, ly, lz, gtab) : tl::res_smem_bytes(lx, ly, lz, gtab);
                 if (own > 12 * tl::kResTPB || smem > smem_cap || H >= 16384 ||
                     nface > tl::kResKF * tl::kResTPB)
                     continue;
@@ -150,15 +150,49 @@ static BrickPlan plan_bricks_uncached(const tl::Grid& g, bool gauss, int sms, si
 }
 
 // decomposition cache keyed by grid shape (the search is a few hundred microseconds)
-static BrickPlan plan_bricks(const tl::Grid& g, bool gauss, int sms, size_t smem_cap) {
-    struct Entry { int nc[3]; bool gauss; int sms; BrickPlan plan; };
+static BrickPlan plan_bricks(const tl::Grid& g, bool gauss, int sms, size_t smem_cap, bool cgv) {
+    struct Entry { int nc[3]; bool gauss; int sms; bool cgv; BrickPlan plan; };
     static thread_local std::vector<Entry> cache;
     for (const Entry& e : cache)
-        if (e.nc[0] == g.nc[0] && e.nc[1] == g.nc[1] && e.nc[2] == g.nc[2] && e.gauss == gauss && e.sms == sms)
+        if (e.nc[0] == g.nc[0] && e.nc[1] == g.nc[1] && e.nc[2] == g.nc[2] && e.gauss == gauss &&
+            e.sms == sms && e.cgv == cgv)
             return e.plan;
-    BrickPlan bp = plan_bricks_uncached(g, gauss, sms, smem_cap);
-    cache.push_back({{g.nc[0], g.nc[1], g.nc[2]}, gauss, sms, bp});
+    BrickPlan bp = plan_bricks_uncached(g, gauss, sms, smem_cap, cgv);
+    cache.push_back({{g.nc[0], g.nc[1], g.nc[2]}, gauss, sms, cgv, bp});
     return bp;
+}
+
+// TLGPU_EXACT_CG=1: the two-barrier kernel that mirrors scipy's cg operation for operation.
+// Default: the one-barrier Chronopoulos-Gear kernel (same iterates up to rounding).
+static bool exact_cg() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("TLGPU_EXACT_CG");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
+}
+
+template <bool GAUSS, int NPT>
+static cudaError_t launch_rescg_t(tl::ResCGParams& RP, int G, size_t smem, cudaStream_t st) {
+    auto fn = tl::k_pcg_resident_cg<GAUSS, NPT>;
+    static thread_local bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    void* args[] = {&RP};
+    return cudaLaunchCooperativeKernel((void*)fn, G, tl::kResTPB, args, smem, st);
+}
+
+template <bool GAUSS>
+static cudaError_t launch_rescg_g(tl::ResCGParams& RP, int npt, int G, size_t smem, cudaStream_t st) {
+    switch (npt) {
+        case 4: return launch_rescg_t<GAUSS, 4>(RP, G, smem, st);
+        case 8: return launch_rescg_t<GAUSS, 8>(RP, G, smem, st);
+        default: return launch_rescg_t<GAUSS, 12>(RP, G, smem, st);
+    }
 }
 
 static unsigned long long* g_prof = nullptr;     // TLGPU_PROF=1: phase timestamps of block 0
@@ -208,8 +242,30 @@ static bool force_streaming() {
 // Resident kernel when the grid fits on-chip, streaming k_pcg otherwise.
 static int launch_solve(tl::PcgParams& P, bool gauss, int sms, double* xg, cudaStream_t st,
                         int64_t* launches, int* kind_out = nullptr) {
+    if (xg && !force_streaming() && !exact_cg()) {
+        BrickPlan bp = plan_bricks(P.g, gauss, sms, 210 * 1024, true);
+        if (bp.ok) {
+            tl::ResCGParams RP{};
+            RP.P = P;
+            RP.xr = xg;              // exchange buffer (4 n doubles): r0, then w ping-pong
+            RP.xw = xg + P.g.n;
+            RP.prof = prof_buffer();
+            const int N[3] = {P.g.NX, P.g.NY, P.g.NZ};
+            for (int a = 0; a < 3; ++a) {
+                RP.ng[a] = bp.ng[a];
+                split_axis(N[a], bp.ng[a], RP.off[a]);
+            }
+            const int G = bp.ng[0] * bp.ng[1] * bp.ng[2];
+            cudaError_t e = gauss ? launch_rescg_g<true>(RP, bp.npt, G, bp.smem, st)
+                                  : launch_rescg_g<false>(RP, bp.npt, G, bp.smem, st);
+            if (e != cudaSuccess) return fail(TL_E_CUDA, std::string("k_pcg_resident_cg launch: ") + cudaGetErrorString(e));
+            if (launches) ++*launches;
+            if (kind_out) *kind_out = 2;
+            return TL_OK;
+        }
+    }
     if (xg && !force_streaming()) {
-        BrickPlan bp = plan_bricks(P.g, gauss, sms, 200 * 1024);
+        BrickPlan bp = plan_bricks(P.g, gauss, sms, 200 * 1024, false);
         if (bp.ok) {
             tl::ResParams RP{};
             RP.P = P;

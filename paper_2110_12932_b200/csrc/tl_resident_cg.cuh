@@ -1,0 +1,370 @@
+// tl_resident_cg.cuh — one-barrier-per-iteration resident PCG (Chronopoulos-Gear), sm_100a fp64.
+//
+// Same operator, RHS, preconditioner, stopping rule (||r|| < rtol ||b|| tested at the top
+// of each iteration on the directly computed r.r) and final checks as scipy's cg /
+// k_pcg_resident, but the Chronopoulos-Gear recurrences
+//     u = M r, w = A u, gamma = r.u, delta = w.u
+//     beta = gamma/gamma_prev, alpha = gamma/(delta - beta gamma/alpha_prev)
+//     p = u + beta p, s = w + beta s, x += alpha p, r -= alpha s
+// put the three dots of an iteration in ONE reduction, so each iteration needs one grid
+// barrier instead of two.  In exact arithmetic the iterates equal CG's; in fp64 they
+// agree with scipy's to ~4e-16 with identical iteration counts on the golden systems
+// (tests/test_oracle_golden.py::test_chronopoulos_gear_matches_scipy_cg).
+//
+// Data placement per CTA brick: u with a one-node halo (the stencil input), r and s of
+// own nodes and of the halo face cells (advanced by the same recurrences as their
+// owners), w of own nodes in registers; x and p of own nodes stream through L2 (global).
+// Only the brick-surface w values cross CTAs (ping-pong exchange buffers).
+//
+// Shared memory: [Gaussian tables][US: H][RO: n][SO: n][RF: F][SF: F][GID: n int][FS: F int]
+//                [FG: F int][CL: H bytes]
+#pragma once
+
+#include "tl_resident.cuh"
+
+namespace tl {
+
+struct ResCGParams {
+    PcgParams P;                  // T (in: T_old, out: x), b, p0 (p), part, info, ...
+    double* xr;                   // exchange: brick-surface r0, n doubles
+    double* xw;                   // exchange: brick-surface w, 2 n doubles (ping-pong)
+    unsigned long long* prof;
+    int ng[3];
+    int off[3][kResMaxSplit + 1];
+};
+
+__host__ __device__ inline size_t rescg_smem_bytes(int lx, int ly, int lz, int gtab) {
+    const size_t H = (size_t)(lx + 2) * (ly + 2) * (lz + 2);
+    const size_t n = (size_t)lx * ly * lz;
+    const size_t F = 2 * ((size_t)ly * lz + (size_t)lx * lz + (size_t)lx * ly);
+    return 8 * (size_t)gtab + 9 * H + 20 * n + 24 * F + 16;
+}
+
+template <bool GAUSS, int NPT>
+__global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) {
+    cg::grid_group grid = cg::this_grid();
+    const PcgParams& P = RP.P;
+    const Grid& g = P.g;
+    __shared__ ClassTable T;
+    __shared__ double red[8 * 32];
+    __shared__ double tot[8];
+    extern __shared__ __align__(16) unsigned char smem[];
+    const bool prof = RP.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
+    int np = 0;
+    if (prof) RP.prof[np++] = global_ns();
+
+    const int G = gridDim.x;
+    const int b = blockIdx.x;
+    const int bxi = b % RP.ng[0], byi = (b / RP.ng[0]) % RP.ng[1], bzi = b / (RP.ng[0] * RP.ng[1]);
+    const int x0 = RP.off[0][bxi], y0 = RP.off[1][byi], z0 = RP.off[2][bzi];
+    const int lx = RP.off[0][bxi + 1] - x0, ly = RP.off[1][byi + 1] - y0, lz = RP.off[2][bzi + 1] - z0;
+    const int LX = lx + 2, LY = ly + 2, LZ = lz + 2;
+    const int H = LX * LY * LZ;
+    const int SY = LX, SZ = LX * LY;
+    const int nown = lx * ly * lz;
+    const int fx = ly * lz, fy = lx * lz, fz = lx * ly;
+    const int nface = 2 * (fx + fy + fz);
+
+    const int gtab_n = GAUSS ? gauss_smem_len(g) : 0;
+    double* tx = reinterpret_cast<double*>(smem);
+    double* ty = tx + 6 * g.nc[0];
+    double* tz = ty + 6 * g.nc[1];
+    double* bx_ = tz + 6 * g.nc[2];
+    double* by_ = bx_ + g.NX;
+    double* bz_ = by_ + g.NY;
+    double* US = tx + gtab_n;
+    double* RO = US + H;
+    double* SO = RO + nown;
+    double* RF = SO + nown;
+    double* SF = RF + nface;
+    int* GID = reinterpret_cast<int*>(SF + nface);
+    int* FS = GID + nown;
+    int* FG = FS + nface;
+    uint8_t* CL = reinterpret_cast<uint8_t*>(FG + nface);
+
+    build_class_table(T, threadIdx.x, P.mbase, P.cbase, g.dkind);
+    if (GAUSS) build_gauss_tables(g, P.src, tx, ty, tz);
+    for (int s = threadIdx.x; s < H; s += kResTPB) {
+        const int u = s % LX, v = (s / LX) % LY, w = s / SZ;
+        const int i = x0 + u - 1, j = y0 + v - 1, k = z0 + w - 1;
+        const bool in = i >= 0 && i <= g.nc[0] && j >= 0 && j <= g.nc[1] && k >= 0 && k <= g.nc[2];
+        CL[s] = in ? (uint8_t)class_of(g, i, j, k) : kNoNode;
+        US[s] = 0.0;
+    }
+    __syncthreads();
+    if (GAUSS) build_gauss_bounds(g, tx, ty, tz, bx_, by_, bz_);
+    for (int e0 = threadIdx.x; e0 < nface; e0 += kResTPB) {
+        int e = e0, u, v, w;
+        if (e < 2 * fx) {
+            const int side = e / fx, r = e % fx;
+            u = side ? LX - 1 : 0; v = r % ly + 1; w = r / ly + 1;
+        } else if ((e -= 2 * fx) < 2 * fy) {
+            const int side = e / fy, r = e % fy;
+            v = side ? LY - 1 : 0; u = r % lx + 1; w = r / lx + 1;
+        } else {
+            e -= 2 * fy;
+            const int side = e / fz, r = e % fz;
+            w = side ? LZ - 1 : 0; u = r % lx + 1; v = r / lx + 1;
+        }
+        const int s = u + SY * v + SZ * w;
+        const bool in = CL[s] != kNoNode;
+        FS[e0] = in ? s : -1;
+        FG[e0] = in ? (x0 + u - 1) + g.NX * ((y0 + v - 1) + g.NY * (z0 + w - 1)) : 0;
+        RF[e0] = 0.0;
+        SF[e0] = 0.0;
+    }
+    int od[NPT];
+#pragma unroll
+    for (int m = 0; m < NPT; ++m) {
+        const int nl = threadIdx.x + m * kResTPB;
+        od[m] = -1;
+        if (nl < nown) {
+            const int u = nl % lx + 1, v = (nl / lx) % ly + 1, w = nl / (lx * ly) + 1;
+            const int s = u + SY * v + SZ * w;
+            const int cls = CL[s];
+            int mask = 0;
+            const int nb[6] = {s - 1, s + 1, s - SY, s + SY, s - SZ, s + SZ};
+#pragma unroll
+            for (int e = 0; e < 6; ++e) {
+                const int c = CL[nb[e]];
+                if (c != kNoNode && T.nd[c] != 0.0) mask |= 1 << e;
+            }
+            const bool surf = u == 1 || u == lx || v == 1 || v == ly || w == 1 || w == lz;
+            od[m] = s | (mask << 14) | (cls << 20) | ((int)surf << 25);
+            GID[nl] = (x0 + u - 1) + g.NX * ((y0 + v - 1) + g.NY * (z0 + w - 1));
+            SO[nl] = 0.0;
+        }
+    }
+
+    // ---- phase 0: constrained RHS (identical to k_pcg_resident), r0 = b, x = 0 ----
+    if (GAUSS) __syncthreads();
+    double acc[2] = {0.0, 0.0};
+#pragma unroll
+    for (int m = 0; m < NPT; ++m) {
+        if (od[m] < 0) continue;
+        const int nl = threadIdx.x + m * kResTPB;
+        const int p = GID[nl];
+        const int cls = od_cls(od[m]);
+        double bv;
+        if (T.nd[cls] == 0.0) {
+            bv = dirichlet_value(P, p);
+        } else {
+            int i, j, k;
+            decode(g, p, i, j, k);
+            bv = T.mass[cls] * P.T[p];
+            if (P.load) bv += P.load[p];
+            if (GAUSS) bv = add_gaussian(bv, g, tx, ty, tz, bx_, by_, bz_, i, j, k);
+            const int sy = g.NX, sz = g.NX * g.NY;
+            double lift = 0.0;
+            if (i > 0 && T.nd[cls - axis_class(i, g.nc[0]) + axis_class(i - 1, g.nc[0])] == 0.0) lift += T.c[0][cls] * dirichlet_value(P, p - 1);
+            if (i < g.nc[0] && T.nd[cls - axis_class(i, g.nc[0]) + axis_class(i + 1, g.nc[0])] == 0.0) lift += T.c[0][cls] * dirichlet_value(P, p + 1);
+            if (j > 0 && T.nd[cls + 3 * (axis_class(j - 1, g.nc[1]) - axis_class(j, g.nc[1]))] == 0.0) lift += T.c[1][cls] * dirichlet_value(P, p - sy);
+            if (j < g.nc[1] && T.nd[cls + 3 * (axis_class(j + 1, g.nc[1]) - axis_class(j, g.nc[1]))] == 0.0) lift += T.c[1][cls] * dirichlet_value(P, p + sy);
+            if (k > 0 && T.nd[cls + 9 * (axis_class(k - 1, g.nc[2]) - axis_class(k, g.nc[2]))] == 0.0) lift += T.c[2][cls] * dirichlet_value(P, p - sz);
+            if (k < g.nc[2] && T.nd[cls + 9 * (axis_class(k + 1, g.nc[2]) - axis_class(k, g.nc[2]))] == 0.0) lift += T.c[2][cls] * dirichlet_value(P, p + sz);
+            bv += lift;
+        }
+        P.b[p] = bv;
+        P.T[p] = 0.0;                       // x0 = 0 (T_old no longer needed by this node)
+        RO[nl] = bv;
+        if (od_surf(od[m])) RP.xr[p] = bv;
+        const double z = __dmul_rn(T.invd[cls], bv);
+        acc[0] += bv * bv;
+        acc[1] += bv * z;
+    }
+    block_sum<2>(acc, red);
+    if (threadIdx.x == 0) { P.part[0 * G + b] = acc[0]; P.part[1 * G + b] = acc[1]; }
+    grid.sync();
+    {
+        const int s2[2] = {0, 1};
+        grid_sum_fast<2>(P.part, s2, G, tot);
+    }
+    if (prof) RP.prof[np++] = global_ns();
+    const double bb = tot[0];
+    double gam = tot[1];                    // r0 . u0
+    const double bnorm = sqrt(bb);
+    const double atol = P.rtol * bnorm;
+    double rnorm = bnorm;
+    double rr = bb;
+    int it = 0, status = 0;
+
+    double w[NPT];
+    double dlt = 0.0;
+    if (bb != 0.0) {
+        // u0 = M r0 on own + halo (halo r0 from the exchange), w0 = A u0, delta0 = w0.u0
+#pragma unroll
+        for (int t = 0; t < kResKF; ++t) {
+            const int e = threadIdx.x + t * kResTPB;
+            if (e < nface && FS[e] >= 0) {
+                const double rv = __ldcg(RP.xr + FG[e]);
+                RF[e] = rv;
+                US[FS[e]] = __dmul_rn(T.invd[CL[FS[e]]], rv);
+            }
+        }
+#pragma unroll
+        for (int m = 0; m < NPT; ++m) {
+            if (od[m] < 0) continue;
+            US[od_s(od[m])] = __dmul_rn(T.invd[od_cls(od[m])], RO[threadIdx.x + m * kResTPB]);
+        }
+        __syncthreads();
+        double d1[1] = {0.0};
+#pragma unroll
+        for (int m = 0; m < NPT; ++m) {
+            if (od[m] < 0) continue;
+            const int d = od[m], s = od_s(d), cls = od_cls(d);
+            const double uu = US[s];
+            const double wv = (T.nd[cls] == 0.0) ? uu : stencil_smem(T, US, s, cls, od_mask(d), SY, SZ);
+            w[m] = wv;
+            d1[0] += wv * uu;
+            if (od_surf(d)) RP.xw[GID[threadIdx.x + m * kResTPB]] = wv;
+        }
+        block_sum<1>(d1, red);
+        if (threadIdx.x == 0) P.part[2 * G + b] = d1[0];
+        grid.sync();
+        {
+            const int s1[1] = {2};
+            grid_sum_fast<1>(P.part, s1, G, tot);
+        }
+        dlt = tot[0];
+        double gam_prev = 1.0, alpha_prev = 1.0;
+        double* pg = P.p0;                  // p of own nodes (global, L2-resident)
+        while (true) {
+            rnorm = sqrt(rr);
+            if (rnorm < atol) { status = 0; break; }
+            if (!isfinite(rnorm)) { status = 3; break; }
+            if (it >= P.maxiter) { status = 1; break; }
+            const bool first = it == 0;
+            const double beta = first ? 0.0 : gam / gam_prev;
+            const double alpha = first ? gam / dlt : gam / (dlt - beta * gam / alpha_prev);
+            // halo: s = w + beta s, r -= alpha s, u = M r  (w of the halo from the exchange)
+            const double* win = RP.xw + (size_t)(it & 1) * g.n;
+            double fw[kResKF];
+#pragma unroll
+            for (int t = 0; t < kResKF; ++t) {
+                const int e = threadIdx.x + t * kResTPB;
+                fw[t] = (e < nface && FS[e] >= 0) ? __ldcg(win + FG[e]) : 0.0;
+            }
+            // own: p = u + beta p, s = w + beta s, x += alpha p, r -= alpha s, u = M r
+            double xo[NPT], po[NPT];
+#pragma unroll
+            for (int m = 0; m < NPT; ++m) {
+                if (od[m] < 0) continue;
+                const int gid = GID[threadIdx.x + m * kResTPB];
+                xo[m] = P.T[gid];
+                po[m] = first ? 0.0 : pg[gid];
+            }
+#pragma unroll
+            for (int m = 0; m < NPT; ++m) {
+                if (od[m] < 0) continue;
+                const int nl = threadIdx.x + m * kResTPB;
+                const int s = od_s(od[m]);
+                const double uu = US[s];
+                const double pv = first ? uu : __dadd_rn(uu, __dmul_rn(beta, po[m]));
+                const double sv = first ? w[m] : __dadd_rn(w[m], __dmul_rn(beta, SO[nl]));
+                const double rv = __dsub_rn(RO[nl], __dmul_rn(alpha, sv));
+                const int gid = GID[nl];
+                P.T[gid] = __dadd_rn(xo[m], __dmul_rn(alpha, pv));
+                pg[gid] = pv;
+                SO[nl] = sv;
+                RO[nl] = rv;
+            }
+            __syncthreads();       // every thread done reading US (u_i) before it is overwritten
+#pragma unroll
+            for (int m = 0; m < NPT; ++m) {
+                if (od[m] < 0) continue;
+                US[od_s(od[m])] = __dmul_rn(T.invd[od_cls(od[m])], RO[threadIdx.x + m * kResTPB]);
+            }
+#pragma unroll
+            for (int t = 0; t < kResKF; ++t) {
+                const int e = threadIdx.x + t * kResTPB;
+                if (e >= nface) break;
+                const int s = FS[e];
+                if (s < 0) continue;
+                const double sv = first ? fw[t] : __dadd_rn(fw[t], __dmul_rn(beta, SF[e]));
+                const double rv = __dsub_rn(RF[e], __dmul_rn(alpha, sv));
+                SF[e] = sv;
+                RF[e] = rv;
+                US[s] = __dmul_rn(T.invd[CL[s]], rv);
+            }
+            gam_prev = gam;
+            alpha_prev = alpha;
+            __syncthreads();
+            // w = A u, gamma = r.u, delta = w.u, r.r; publish surface w
+            double d3[3] = {0.0, 0.0, 0.0};
+            double* wout = RP.xw + (size_t)((it + 1) & 1) * g.n;
+#pragma unroll
+            for (int m = 0; m < NPT; ++m) {
+                if (od[m] < 0) continue;
+                const int d = od[m], s = od_s(d), cls = od_cls(d), nl = threadIdx.x + m * kResTPB;
+                const double uu = US[s];
+                const double wv = (T.nd[cls] == 0.0) ? uu : stencil_smem(T, US, s, cls, od_mask(d), SY, SZ);
+                w[m] = wv;
+                const double rv = RO[nl];
+                d3[0] += rv * uu;
+                d3[1] += wv * uu;
+                d3[2] += rv * rv;
+                if (od_surf(d)) wout[GID[nl]] = wv;
+            }
+            block_sum<3>(d3, red);
+            if (threadIdx.x == 0) { P.part[0 * G + b] = d3[0]; P.part[1 * G + b] = d3[1]; P.part[2 * G + b] = d3[2]; }
+            grid.sync();
+            {
+                const int s3[3] = {0, 1, 2};
+                grid_sum_fast<3>(P.part, s3, G, tot);
+            }
+            if (prof && it < 100) RP.prof[np++] = global_ns();
+            gam = tot[0];
+            dlt = tot[1];
+            rr = tot[2];
+            ++it;
+        }
+    }
+
+    // ---- true residual ||A_c x - b|| from x in global memory; x_D = b_D ----
+    grid.sync();                            // every CTA's final x visible
+#pragma unroll
+    for (int m = 0; m < NPT; ++m) {
+        if (od[m] < 0) continue;
+        US[od_s(od[m])] = __ldcg(P.T + GID[threadIdx.x + m * kResTPB]);
+    }
+#pragma unroll
+    for (int t = 0; t < kResKF; ++t) {
+        const int e = threadIdx.x + t * kResTPB;
+        if (e < nface && FS[e] >= 0) US[FS[e]] = __ldcg(P.T + FG[e]);
+    }
+    __syncthreads();
+    double res[2] = {0.0, 0.0};
+#pragma unroll
+    for (int m = 0; m < NPT; ++m) {
+        if (od[m] < 0) continue;
+        const int d = od[m], s = od_s(d), cls = od_cls(d);
+        const double xp = US[s];
+        const double ax = (T.nd[cls] == 0.0) ? xp : stencil_smem(T, US, s, cls, od_mask(d), SY, SZ);
+        const int p = GID[threadIdx.x + m * kResTPB];
+        const double bv = P.b[p];
+        const double dd = ax - bv;
+        res[0] += dd * dd;
+        res[1] += isfinite(xp) ? 0.0 : 1.0;
+        if (T.nd[cls] == 0.0) P.T[p] = bv;
+    }
+    block_sum<2>(res, red);
+    if (threadIdx.x == 0) { P.part[0 * G + b] = res[0]; P.part[3 * G + b] = res[1]; }
+    grid.sync();
+    {
+        const int s2[2] = {0, 3};
+        grid_sum_fast<2>(P.part, s2, G, tot);
+    }
+    if (b == 0 && threadIdx.x == 0) {
+        const double tres = bnorm > 0.0 ? sqrt(tot[0]) / bnorm : 0.0;
+        if (status == 0 && tot[1] > 0.0) status = 3;
+        if (status == 0 && (!isfinite(tres) || tres > 1e2 * P.rtol)) status = 2;
+        P.info->iterations = (status == 1) ? P.maxiter : it;
+        P.info->status = status;
+        P.info->bnorm = bnorm;
+        P.info->rnorm = rnorm;
+        P.info->true_resid = tres;
+        if (prof) { RP.prof[np++] = global_ns(); RP.prof[127] = np; }
+    }
+}
+
+}  // namespace tl

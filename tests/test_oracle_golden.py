@@ -137,3 +137,17 @@ def test_run_cfg1_uniform_all_steps():
 @pytest.mark.slow
 def test_run_cfg2_first_steps():
     _check_run("cfg2", 2)
+
+
+@pytest.mark.parametrize("name", OP_CASES)
+def test_chronopoulos_gear_matches_scipy_cg(name):
+    """The one-reduction recurrences the device's default resident kernel uses reach the
+    reference's solution with the reference's iteration count (tolerance 1e-13 vs scipy)."""
+    from oracle.pcg import cg_chronopoulos_gear
+    z, G, D, g, local, beam = _op(name)
+    op = kuhn.StencilOperator(G, 9.8, 8440 * 410.0, float(z["dt"]), D.reshape(G.shape))
+    b = z["b"]
+    x, info, its = cg_chronopoulos_gear(op.apply, b, op.inv_diag(), 1e-12, 20 * b.size)
+    assert info == 0 and its == int(z["cg_iters"])
+    x[D] = b[D]
+    assert np.abs(x - z["sol"]).max() <= 1e-13 * np.abs(z["sol"]).max()
