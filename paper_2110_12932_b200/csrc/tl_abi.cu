@@ -162,13 +162,15 @@ static BrickPlan plan_bricks(const tl::Grid& g, bool gauss, int sms, size_t smem
     return bp;
 }
 
-// TLGPU_EXACT_CG=1: the two-barrier kernel that mirrors scipy's cg operation for operation.
-// Default: the one-barrier Chronopoulos-Gear kernel (same iterates up to rounding).
+// Default: the two-barrier kernel that mirrors scipy's cg operation for operation (it is
+// also the faster one on B200: 9.5 us vs 11.5 us per iteration on cfg2, profiles/README.md).
+// TLGPU_CGCG=1 selects the one-barrier Chronopoulos-Gear kernel (same iterates up to
+// rounding; x and p stream through L2 because its SMEM footprint is larger).
 static bool exact_cg() {
     static int v = -1;
     if (v < 0) {
-        const char* e = getenv("TLGPU_EXACT_CG");
-        v = (e && e[0] == '1') ? 1 : 0;
+        const char* e = getenv("TLGPU_CGCG");
+        v = (e && e[0] == '1') ? 0 : 1;
     }
     return v == 1;
 }
@@ -202,7 +204,7 @@ static unsigned long long* prof_buffer() {
     if (want < 0) {
         const char* e = getenv("TLGPU_PROF");
         want = (e && e[0] == '1') ? 1 : 0;
-        if (want) cudaMalloc((void**)&g_prof, 128 * sizeof(unsigned long long));
+        if (want) cudaMalloc((void**)&g_prof, 512 * sizeof(unsigned long long));
     }
     return g_prof;
 }
@@ -820,11 +822,11 @@ int32_t tl_debug_profile(uint64_t* out, int32_t max, int32_t* count) {
     if (!out || !count) return fail(TL_E_INVALID, "null argument");
     *count = 0;
     if (!g_prof) return TL_OK;
-    unsigned long long h[128];
+    unsigned long long h[512];
     TL_CUDA(cudaDeviceSynchronize());
     TL_CUDA(cudaMemcpy(h, g_prof, sizeof(h), cudaMemcpyDeviceToHost));
     // slots [0, h[127]) phase stamps, 120..122 setup stamps, 127 = stamp count
-    const int n = std::min(max, 128);
+    const int n = std::min(max, 512);
     for (int e = 0; e < n; ++e) out[e] = h[e];
     *count = n;
     return TL_OK;

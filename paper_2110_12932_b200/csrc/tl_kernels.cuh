@@ -79,7 +79,9 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-// Deterministic block sum of NV values; result valid in thread 0.
+// Deterministic block sum of NV values; result valid in thread 0 only.  Every call site
+// hands the result to thread 0's partial store and then a grid.sync(), whose internal
+// __syncthreads orders the reuse of `smem`, so no trailing block barrier is needed.
 template <int NV>
 __device__ __forceinline__ void block_sum(double (&v)[NV], double* smem) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -96,7 +98,6 @@ __device__ __forceinline__ void block_sum(double (&v)[NV], double* smem) {
             v[k] = warp_sum(s);
         }
     }
-    __syncthreads();
 }
 
 // Fixed-order sum of the per-block partials written before the last grid.sync.
@@ -118,26 +119,29 @@ __device__ __forceinline__ void grid_sum(const double* part, const int (&slot)[N
     __syncthreads();
 }
 
-constexpr int kResMaxBlocks = 512;
+constexpr int kResMaxBlocks = 320;       // grid-reduction capacity (CTAs)
 
 // Fixed-order, load-parallel sum of G <= kResMaxBlocks partials (all blocks agree bitwise).
+// All NV x ceil(G/32) loads of a lane are issued before any add: one L2 round trip.
 template <int NV>
 __device__ __forceinline__ void grid_sum_fast(const double* part, const int (&slot)[NV], int G,
                                               double* smem_out) {
     if (threadIdx.x < 32) {
         const int lane = threadIdx.x;
+        constexpr int PL = kResMaxBlocks / 32;
+        double v[NV][PL];
+#pragma unroll
+        for (int k = 0; k < NV; ++k)
+#pragma unroll
+            for (int t = 0; t < PL; ++t) {
+                const int b = lane + 32 * t;
+                v[k][t] = b < G ? __ldcg(part + slot[k] * G + b) : 0.0;
+            }
 #pragma unroll
         for (int k = 0; k < NV; ++k) {
-            const double* p = part + slot[k] * G;
-            double v[kResMaxBlocks / 32];
-#pragma unroll
-            for (int t = 0; t < kResMaxBlocks / 32; ++t) {
-                const int b = lane + 32 * t;
-                v[t] = b < G ? __ldcg(p + b) : 0.0;
-            }
             double s = 0.0;
 #pragma unroll
-            for (int t = 0; t < kResMaxBlocks / 32; ++t) s += v[t];
+            for (int t = 0; t < PL; ++t) s += v[k][t];
             s = warp_sum(s);
             if (lane == 0) smem_out[k] = s;
         }

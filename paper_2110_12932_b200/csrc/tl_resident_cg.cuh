@@ -237,6 +237,9 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
             const double beta = first ? 0.0 : gam / gam_prev;
             const double alpha = first ? gam / dlt : gam / (dlt - beta * gam / alpha_prev);
             // halo: s = w + beta s, r -= alpha s, u = M r  (w of the halo from the exchange)
+#define TL_STAMP(slot) \
+    if (prof && it == 3) RP.prof[slot] = global_ns();
+            TL_STAMP(100)
             const double* win = RP.xw + (size_t)(it & 1) * g.n;
             double fw[kResKF];
 #pragma unroll
@@ -268,6 +271,7 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
                 SO[nl] = sv;
                 RO[nl] = rv;
             }
+            TL_STAMP(101)
             __syncthreads();       // every thread done reading US (u_i) before it is overwritten
 #pragma unroll
             for (int m = 0; m < NPT; ++m) {
@@ -289,6 +293,7 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
             gam_prev = gam;
             alpha_prev = alpha;
             __syncthreads();
+            TL_STAMP(102)
             // w = A u, gamma = r.u, delta = w.u, r.r; publish surface w
             double d3[3] = {0.0, 0.0, 0.0};
             double* wout = RP.xw + (size_t)((it + 1) & 1) * g.n;
@@ -305,13 +310,19 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
                 d3[2] += rv * rv;
                 if (od_surf(d)) wout[GID[nl]] = wv;
             }
+            TL_STAMP(103)
             block_sum<3>(d3, red);
             if (threadIdx.x == 0) { P.part[0 * G + b] = d3[0]; P.part[1 * G + b] = d3[1]; P.part[2 * G + b] = d3[2]; }
+            TL_STAMP(104)
+            if (RP.prof && it == 3 && threadIdx.x == 0) RP.prof[256 + b] = global_ns();   // arrival per CTA
             grid.sync();
+            TL_STAMP(105)
             {
                 const int s3[3] = {0, 1, 2};
                 grid_sum_fast<3>(P.part, s3, G, tot);
             }
+            TL_STAMP(106)
+#undef TL_STAMP
             if (prof && it < 100) RP.prof[np++] = global_ns();
             gam = tot[0];
             dlt = tot[1];

@@ -20,16 +20,25 @@ from paper_2110_12932_b200.schedule import plan_spacetime  # noqa: E402
 
 
 def stamps():
-    buf = (C.c_uint64 * 128)()
+    buf = (C.c_uint64 * 512)()
     cnt = C.c_int32()
-    N.check(N.lib().tl_debug_profile(buf, 128, C.byref(cnt)))
+    N.check(N.lib().tl_debug_profile(buf, 512, C.byref(cnt)))
     raw = np.array(buf[:cnt.value], dtype=np.float64)
     n = int(buf[127])
-    return raw[:n], raw[120:123]
+    return raw[:n], raw[120:123], raw[100:107], raw[256:512]
 
 
 def report(tag, tt):
-    t, setup_marks = tt
+    t, setup_marks, inner, arrive = tt
+    if inner[0] > 0 and inner[6] > inner[0]:
+        d = np.diff(inner) / 1e3
+        names = ["halo-w + own update", "u update + sync", "stencil + dots", "block_sum",
+                 "grid.sync", "grid_sum"]
+        print("  iteration 3 of CTA 0: " + ", ".join(f"{a} {b:.2f}" for a, b in zip(names, d)) + " us")
+        a = arrive[arrive > 0]
+        if a.size:
+            print(f"  barrier arrival spread over {a.size} CTAs: {(a.max() - a.min()) / 1e3:.2f} us "
+                  f"(CTA 0 arrives {(a[0] - a.min()) / 1e3:.2f} us after the first)")
     if len(t) < 4:
         print(tag, "no stamps")
         return
