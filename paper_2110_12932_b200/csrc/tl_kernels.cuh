@@ -98,6 +98,7 @@ __device__ __forceinline__ void block_sum(double (&v)[NV], double* smem) {
             v[k] = warp_sum(s);
         }
     }
+    __syncthreads();
 }
 
 // Fixed-order sum of the per-block partials written before the last grid.sync.
@@ -121,14 +122,14 @@ __device__ __forceinline__ void grid_sum(const double* part, const int (&slot)[N
 
 constexpr int kResMaxBlocks = 320;       // grid-reduction capacity (CTAs)
 
-// Fixed-order, load-parallel sum of G <= kResMaxBlocks partials (all blocks agree bitwise).
+// Fixed-order, load-parallel sum of G <= MAXG partials (all blocks agree bitwise).
 // All NV x ceil(G/32) loads of a lane are issued before any add: one L2 round trip.
-template <int NV>
+template <int NV, int MAXG = 160>
 __device__ __forceinline__ void grid_sum_fast(const double* part, const int (&slot)[NV], int G,
                                               double* smem_out) {
     if (threadIdx.x < 32) {
         const int lane = threadIdx.x;
-        constexpr int PL = kResMaxBlocks / 32;
+        constexpr int PL = MAXG / 32;
         double v[NV][PL];
 #pragma unroll
         for (int k = 0; k < NV; ++k)
@@ -508,7 +509,7 @@ __global__ void __launch_bounds__(kTPB, 2) k_pcg(PcgParams P) {
     grid.sync();
     {
         const int s[2] = {0, 1};
-        grid_sum_fast<2>(P.part, s, G, tot);
+        grid_sum_fast<2, kResMaxBlocks>(P.part, s, G, tot);
     }
     const double bb = tot[0];
     double rz = tot[1];
@@ -540,7 +541,7 @@ __global__ void __launch_bounds__(kTPB, 2) k_pcg(PcgParams P) {
             grid.sync();
             {
                 const int s[1] = {2};
-                grid_sum_fast<1>(P.part, s, G, tot);
+                grid_sum_fast<1, kResMaxBlocks>(P.part, s, G, tot);
             }
             const double alpha = rho / tot[0];
             // ---- phase B ----
@@ -551,7 +552,7 @@ __global__ void __launch_bounds__(kTPB, 2) k_pcg(PcgParams P) {
             grid.sync();
             {
                 const int s[2] = {0, 1};
-                grid_sum_fast<2>(P.part, s, G, tot);
+                grid_sum_fast<2, kResMaxBlocks>(P.part, s, G, tot);
             }
             rz = tot[0];
             rnorm = sqrt(tot[1]);
@@ -580,7 +581,7 @@ __global__ void __launch_bounds__(kTPB, 2) k_pcg(PcgParams P) {
     grid.sync();
     {
         const int s[2] = {0, 3};
-        grid_sum_fast<2>(P.part, s, G, tot);
+        grid_sum_fast<2, kResMaxBlocks>(P.part, s, G, tot);
     }
     const double tres = bnorm > 0.0 ? sqrt(tot[0]) / bnorm : 0.0;
     // ---- re-impose Dirichlet values (fem.py:289-290): x_D = g = b_D ----
