@@ -222,6 +222,9 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident(ResParams RP) {
             const double beta = it > 0 ? rho / rho_prev : 0.0;
             const bool first = it == 0;
             // ---- phase A: halo r in, p = z (+ beta p) on own + halo, q = A_c p ----
+#define TL_STX(slot) \
+    if (prof && it == 3) RP.prof[slot] = global_ns();
+            TL_STX(140)
             double fv[kResKF];
 #pragma unroll
             for (int t = 0; t < kResKF; ++t) {      // issue every halo load first
@@ -245,7 +248,9 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident(ResParams RP) {
                 const double z = __dmul_rn(T.invd[CL[s]], fv[t]);
                 PS[s] = first ? z : __dadd_rn(__dmul_rn(beta, PS[s]), z);
             }
+            TL_STX(141)
             __syncthreads();
+            TL_STX(142)
             double pq[1] = {0.0};
 #pragma unroll
             for (int m = 0; m < NPT; ++m) {
@@ -256,13 +261,18 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident(ResParams RP) {
                 q[m] = qv;
                 pq[0] += pp * qv;
             }
+            TL_STX(143)
             block_sum<1>(pq, red);
             if (threadIdx.x == 0) P.part[2 * G + b] = pq[0];
+            TL_STX(144)
+            if (RP.prof && it == 3 && threadIdx.x == 0) RP.prof[256 + b] = global_ns();
             grid.sync();
+            TL_STX(145)
             {
                 const int s1[1] = {2};
                 grid_sum_fast<1>(P.part, s1, G, tot);
             }
+            TL_STX(146)
             if (prof && it < 64) RP.prof[np++] = global_ns();
             const double alpha = rho / tot[0];
             // ---- phase B: x += alpha p, r -= alpha q, r.z, r.r; publish surface r ----
@@ -284,13 +294,18 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident(ResParams RP) {
                 a2[0] += rv * z;
                 a2[1] += rv * rv;
             }
+            TL_STX(147)
             block_sum<2>(a2, red);
             if (threadIdx.x == 0) { P.part[0 * G + b] = a2[0]; P.part[1 * G + b] = a2[1]; }
+            TL_STX(148)
             grid.sync();
+            TL_STX(149)
             {
                 const int s2[2] = {0, 1};
                 grid_sum_fast<2>(P.part, s2, G, tot);
             }
+            TL_STX(150)
+#undef TL_STX
             if (prof && it < 64) RP.prof[np++] = global_ns();
             rz = tot[0];
             rnorm = sqrt(tot[1]);

@@ -13,11 +13,11 @@
 //
 // Data placement per CTA brick: u with a one-node halo (the stencil input), r and s of
 // own nodes and of the halo face cells (advanced by the same recurrences as their
-// owners), w of own nodes in registers; x and p of own nodes stream through L2 (global).
+// owners), w of own nodes in registers, x and p of own nodes in shared memory.
 // Only the brick-surface w values cross CTAs (ping-pong exchange buffers).
 //
-// Shared memory: [Gaussian tables][US: H][RO: n][SO: n][RF: F][SF: F][GID: n int][FS: F int]
-//                [FG: F int][CL: H bytes]
+// Shared memory: [US: H][RO: n][SO: n][XO: n][PO: n (+ Gaussian tables overlay during phase 0)]
+//                [RF: F][SF: F][GID: n int][FS: F int][FG: F int][CL: H bytes]
 #pragma once
 
 #include "tl_resident.cuh"
@@ -37,7 +37,8 @@ __host__ __device__ inline size_t rescg_smem_bytes(int lx, int ly, int lz, int g
     const size_t H = (size_t)(lx + 2) * (ly + 2) * (lz + 2);
     const size_t n = (size_t)lx * ly * lz;
     const size_t F = 2 * ((size_t)ly * lz + (size_t)lx * lz + (size_t)lx * ly);
-    return 8 * (size_t)gtab + 9 * H + 20 * n + 24 * F + 16;
+    const size_t extra = (size_t)gtab > n ? (size_t)gtab - n : 0;   // tables overlay PO
+    return 8 * extra + 9 * H + 36 * n + 24 * F + 16;
 }
 
 template <bool GAUSS, int NPT>
@@ -65,17 +66,22 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
     const int fx = ly * lz, fy = lx * lz, fz = lx * ly;
     const int nface = 2 * (fx + fy + fz);
 
+    // the Gaussian tables live only during phase 0, so they overlay PO (p is first written
+    // in iteration 0), extended past it when the tables are longer than the brick
     const int gtab_n = GAUSS ? gauss_smem_len(g) : 0;
-    double* tx = reinterpret_cast<double*>(smem);
+    const int extra = gtab_n > nown ? gtab_n - nown : 0;
+    double* US = reinterpret_cast<double*>(smem);
+    double* RO = US + H;
+    double* SO = RO + nown;
+    double* XO = SO + nown;
+    double* PO = XO + nown;
+    double* tx = PO;
     double* ty = tx + 6 * g.nc[0];
     double* tz = ty + 6 * g.nc[1];
     double* bx_ = tz + 6 * g.nc[2];
     double* by_ = bx_ + g.NX;
     double* bz_ = by_ + g.NY;
-    double* US = tx + gtab_n;
-    double* RO = US + H;
-    double* SO = RO + nown;
-    double* RF = SO + nown;
+    double* RF = PO + nown + extra;
     double* SF = RF + nface;
     int* GID = reinterpret_cast<int*>(SF + nface);
     int* FS = GID + nown;
@@ -133,6 +139,7 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
             od[m] = s | (mask << 14) | (cls << 20) | ((int)surf << 25);
             GID[nl] = (x0 + u - 1) + g.NX * ((y0 + v - 1) + g.NY * (z0 + w - 1));
             SO[nl] = 0.0;
+            XO[nl] = 0.0;
         }
     }
 
@@ -165,7 +172,6 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
             bv += lift;
         }
         P.b[p] = bv;
-        P.T[p] = 0.0;                       // x0 = 0 (T_old no longer needed by this node)
         RO[nl] = bv;
         if (od_surf(od[m])) RP.xr[p] = bv;
         const double z = __dmul_rn(T.invd[cls], bv);
@@ -227,7 +233,6 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
         }
         dlt = tot[0];
         double gam_prev = 1.0, alpha_prev = 1.0;
-        double* pg = P.p0;                  // p of own nodes (global, L2-resident)
         while (true) {
             rnorm = sqrt(rr);
             if (rnorm < atol) { status = 0; break; }
@@ -248,26 +253,17 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
                 fw[t] = (e < nface && FS[e] >= 0) ? __ldcg(win + FG[e]) : 0.0;
             }
             // own: p = u + beta p, s = w + beta s, x += alpha p, r -= alpha s, u = M r
-            double xo[NPT], po[NPT];
-#pragma unroll
-            for (int m = 0; m < NPT; ++m) {
-                if (od[m] < 0) continue;
-                const int gid = GID[threadIdx.x + m * kResTPB];
-                xo[m] = P.T[gid];
-                po[m] = first ? 0.0 : pg[gid];
-            }
 #pragma unroll
             for (int m = 0; m < NPT; ++m) {
                 if (od[m] < 0) continue;
                 const int nl = threadIdx.x + m * kResTPB;
                 const int s = od_s(od[m]);
                 const double uu = US[s];
-                const double pv = first ? uu : __dadd_rn(uu, __dmul_rn(beta, po[m]));
+                const double pv = first ? uu : __dadd_rn(uu, __dmul_rn(beta, PO[nl]));
                 const double sv = first ? w[m] : __dadd_rn(w[m], __dmul_rn(beta, SO[nl]));
                 const double rv = __dsub_rn(RO[nl], __dmul_rn(alpha, sv));
-                const int gid = GID[nl];
-                P.T[gid] = __dadd_rn(xo[m], __dmul_rn(alpha, pv));
-                pg[gid] = pv;
+                XO[nl] = __dadd_rn(XO[nl], __dmul_rn(alpha, pv));
+                PO[nl] = pv;
                 SO[nl] = sv;
                 RO[nl] = rv;
             }
@@ -331,17 +327,20 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
         }
     }
 
-    // ---- true residual ||A_c x - b|| from x in global memory; x_D = b_D ----
-    grid.sync();                            // every CTA's final x visible
+    // ---- true residual ||A_c x - b||: publish surface x, gather the halo; x_D = b_D ----
+    __syncthreads();                        // all reads of US by the last stencil done
 #pragma unroll
     for (int m = 0; m < NPT; ++m) {
         if (od[m] < 0) continue;
-        US[od_s(od[m])] = __ldcg(P.T + GID[threadIdx.x + m * kResTPB]);
+        const int nl = threadIdx.x + m * kResTPB;
+        US[od_s(od[m])] = XO[nl];
+        if (od_surf(od[m])) RP.xr[GID[nl]] = XO[nl];
     }
+    grid.sync();                            // every CTA's surface x visible
 #pragma unroll
     for (int t = 0; t < kResKF; ++t) {
         const int e = threadIdx.x + t * kResTPB;
-        if (e < nface && FS[e] >= 0) US[FS[e]] = __ldcg(P.T + FG[e]);
+        if (e < nface && FS[e] >= 0) US[FS[e]] = __ldcg(RP.xr + FG[e]);
     }
     __syncthreads();
     double res[2] = {0.0, 0.0};
@@ -356,7 +355,7 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
         const double dd = ax - bv;
         res[0] += dd * dd;
         res[1] += isfinite(xp) ? 0.0 : 1.0;
-        if (T.nd[cls] == 0.0) P.T[p] = bv;
+        P.T[p] = (T.nd[cls] == 0.0) ? bv : xp;      // x_D = g = b_D (fem.py:289-290)
     }
     block_sum<2>(res, red);
     if (threadIdx.x == 0) { P.part[0 * G + b] = res[0]; P.part[3 * G + b] = res[1]; }

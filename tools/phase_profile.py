@@ -25,11 +25,24 @@ def stamps():
     N.check(N.lib().tl_debug_profile(buf, 512, C.byref(cnt)))
     raw = np.array(buf[:cnt.value], dtype=np.float64)
     n = int(buf[127])
-    return raw[:n], raw[120:123], raw[100:107], raw[256:512]
+    return raw[:n], raw[120:123], raw[100:107], raw[256:512], raw[140:151]
 
 
 def report(tag, tt):
-    t, setup_marks, inner, arrive = tt
+    t, setup_marks, inner, arrive, ex = tt
+    if ex[0] > 0 and ex[10] > ex[0]:
+        d = np.diff(ex) / 1e3
+        names = ["A: halo r + p update", "A: syncthreads", "A: stencil", "A: block_sum", "A: grid.sync",
+                 "A: grid_sum", "B: updates", "B: block_sum", "B: grid.sync", "B: grid_sum"]
+        print("  iteration 3 of CTA 0: " + ", ".join(f"{a} {b:.2f}" for a, b in zip(names, d)) + " us")
+        a = arrive.copy()
+        nz = np.nonzero(a > 0)[0]
+        if nz.size:
+            rel = (a[nz] - a[nz].min()) / 1e3
+            order = np.argsort(-rel)
+            print(f"  phase-A barrier arrival spread over {nz.size} CTAs: {rel.max():.2f} us; latest CTAs "
+                  + ", ".join(f"{nz[i]}(+{rel[i]:.2f})" for i in order[:8])
+                  + f"; median +{np.median(rel):.2f}")
     if inner[0] > 0 and inner[6] > inner[0]:
         d = np.diff(inner) / 1e3
         names = ["halo-w + own update", "u update + sync", "stencil + dots", "block_sum",
