@@ -99,6 +99,9 @@ int launch_pcg(tl::PcgParams& P, bool gauss, int sms, cudaStream_t st, int64_t* 
 }
 
 // ---- SMEM-resident brick PCG: decomposition + launch ------------------------------
+// 227 KB of shared memory per CTA on sm_100, minus the kernels' static ClassTable and
+// reduction scratch (3.6 KB) and some slack.
+static constexpr int kResSmemCap = 232448 - 4096;
 struct BrickPlan {
     bool ok = false;
     int ng[3] = {1, 1, 1};
@@ -162,15 +165,14 @@ static BrickPlan plan_bricks(const tl::Grid& g, bool gauss, int sms, size_t smem
     return bp;
 }
 
-// Default: the two-barrier kernel that mirrors scipy's cg operation for operation (it is
-// also the faster one on B200: 9.5 us vs 11.5 us per iteration on cfg2, profiles/README.md).
-// TLGPU_CGCG=1 selects the one-barrier Chronopoulos-Gear kernel (same iterates up to
-// rounding; x and p stream through L2 because its SMEM footprint is larger).
+// Default: the one-barrier Chronopoulos-Gear kernel wherever its larger SMEM footprint
+// fits (the cfg2 local grid: 8.7 us vs 9.5 us per iteration), else the two-barrier kernel
+// that mirrors scipy's cg operation for operation.  TLGPU_EXACT_CG=1 forces the latter.
 static bool exact_cg() {
     static int v = -1;
     if (v < 0) {
-        const char* e = getenv("TLGPU_CGCG");
-        v = (e && e[0] == '1') ? 0 : 1;
+        const char* e = getenv("TLGPU_EXACT_CG");
+        v = (e && e[0] == '1') ? 1 : 0;
     }
     return v == 1;
 }
@@ -180,7 +182,7 @@ static cudaError_t launch_rescg_t(tl::ResCGParams& RP, int G, size_t smem, cudaS
     auto fn = tl::k_pcg_resident_cg<GAUSS, NPT>;
     static thread_local bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kResSmemCap);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
@@ -214,7 +216,7 @@ static cudaError_t launch_res_t(tl::ResParams& RP, int G, size_t smem, cudaStrea
     auto fn = tl::k_pcg_resident<GAUSS, NPT>;
     static thread_local bool attr_set = false;      // attribute set once per instantiation
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kResSmemCap);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
@@ -245,7 +247,7 @@ static bool force_streaming() {
 static int launch_solve(tl::PcgParams& P, bool gauss, int sms, double* xg, cudaStream_t st,
                         int64_t* launches, int* kind_out = nullptr) {
     if (xg && !force_streaming() && !exact_cg()) {
-        BrickPlan bp = plan_bricks(P.g, gauss, sms, 210 * 1024, true);
+        BrickPlan bp = plan_bricks(P.g, gauss, sms, kResSmemCap, true);
         if (bp.ok) {
             tl::ResCGParams RP{};
             RP.P = P;
