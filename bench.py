@@ -245,16 +245,23 @@ def main():
 
     # ---- roofline of the dominant kernel (k_pcg on the local grid) ----
     peak, peak_src = measured_peak()
-    loc = [(ms, inf["iterations"]) for (ms, lv), inf in zip(kt, infos) if lv == 1]
-    glo = [(ms, inf["iterations"]) for (ms, lv), inf in zip(kt, infos) if lv == 0]
+    # pair each timed launch with the solve records it produced (a persistent local
+    # launch runs all micro solves + corrector of a macro step)
+    loc, glo, pos = [], [], 0
+    for ms, lv, ns in kt:
+        its = [inf["iterations"] for inf in infos[pos:pos + ns]]
+        pos += ns
+        (loc if lv == 1 else glo).append((ms, its))
 
     def kstats(rows, n):
         if not rows:
             return None
-        bytes_ = sum(n * (64 * k + 32) for _, k in rows)
+        solves = sum(len(its) for _, its in rows)
+        bytes_ = sum(n * (64 * k + 32) for _, its in rows for k in its)
         ms = sum(t for t, _ in rows)
-        return {"launches": len(rows), "avg_ms": ms / len(rows), "avg_iterations": float(np.mean([k for _, k in rows])),
-                "alg_bytes_per_launch": bytes_ / len(rows), "achieved_gbs": bytes_ / (ms / 1e3) / 1e9,
+        return {"launches": len(rows), "solves": solves, "avg_ms_per_solve": ms / solves,
+                "avg_iterations": float(np.mean([k for _, its in rows for k in its])),
+                "alg_bytes_per_solve": bytes_ / solves, "achieved_gbs": bytes_ / (ms / 1e3) / 1e9,
                 "share_of_step": ms / dev_ms if world == 1 else None}
 
     kloc, kglo = kstats(loc, Nl), kstats(glo, Ng)

@@ -185,9 +185,12 @@ int64_t tl_run_launch_count(tl_run* run);
 /* Per-launch CUDA-event timing of the solve kernel (k_pcg) on the run's stream.
  * When on, every solve launch is bracketed by an event pair; take_timing returns
  * (after a sync) the durations in ms and the level (0 global, 1 local) of the
- * launches since the last call, in launch order (same order as tl_run_take_info). */
+ * launches since the last call, in launch order, with the number of solves each launch
+ * ran (a persistent launch runs all micro solves of a macro step; the solve records of
+ * tl_run_take_info are in the same order). */
 int32_t tl_run_set_timing(tl_run* run, int32_t on);
-int32_t tl_run_take_timing(tl_run* run, float* ms, int32_t* level, int32_t max, int32_t* count);
+int32_t tl_run_take_timing(tl_run* run, float* ms, int32_t* level, int32_t* nsolve, int32_t max,
+                           int32_t* count);
 /* Diagnostics: with TLGPU_PROF=1 in the environment the resident solve kernel records
  * %globaltimer stamps of CTA 0 at its phase boundaries (start, after the RHS, after
  * each of the two barriers of the first 64 iterations, end); this returns the stamps

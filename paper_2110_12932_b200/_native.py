@@ -102,8 +102,8 @@ SIGNATURES = [
     ("tl_run_stream", C.c_int32, [_P, C.POINTER(_P)]),
     ("tl_run_launch_count", C.c_int64, [_P]),
     ("tl_run_set_timing", C.c_int32, [_P, C.c_int32]),
-    ("tl_run_take_timing", C.c_int32, [_P, C.POINTER(C.c_float), C.POINTER(C.c_int32), C.c_int32,
-                                       C.POINTER(C.c_int32)]),
+    ("tl_run_take_timing", C.c_int32, [_P, C.POINTER(C.c_float), C.POINTER(C.c_int32),
+                                       C.POINTER(C.c_int32), C.c_int32, C.POINTER(C.c_int32)]),
     ("tl_run_flush_l2", C.c_int32, [_P]),
     ("tl_debug_profile", C.c_int32, [C.POINTER(C.c_uint64), C.c_int32, C.POINTER(C.c_int32)]),
 ]

@@ -244,21 +244,46 @@ static bool force_streaming() {
 }
 
 // Resident kernel when the grid fits on-chip, streaming k_pcg otherwise.
+// Exchange buffer layout (4 n doubles): [r0 / final x][w ping-pong: 2 n][saved T_old: n].
+static void fill_rescg(tl::ResCGParams& RP, const tl::PcgParams& P, double* xg, const BrickPlan& bp) {
+    RP.P = P;
+    RP.xr = xg;
+    RP.xw = xg + P.g.n;
+    RP.saved = xg + 3 * (size_t)P.g.n;
+    RP.prof = prof_buffer();
+    const int N[3] = {P.g.NX, P.g.NY, P.g.NZ};
+    for (int a = 0; a < 3; ++a) {
+        RP.ng[a] = bp.ng[a];
+        split_axis(N[a], bp.ng[a], RP.off[a]);
+    }
+}
+
+static bool cg_fits(const tl::Grid& g, bool gauss, int sms, BrickPlan& bp) {
+    if (force_streaming() || exact_cg()) return false;
+    bp = plan_bricks(g, gauss, sms, kResSmemCap, true);
+    return bp.ok;
+}
+
 static int launch_solve(tl::PcgParams& P, bool gauss, int sms, double* xg, cudaStream_t st,
-                        int64_t* launches, int* kind_out = nullptr) {
-    if (xg && !force_streaming() && !exact_cg()) {
-        BrickPlan bp = plan_bricks(P.g, gauss, sms, kResSmemCap, true);
-        if (bp.ok) {
+                        int64_t* launches, tl::SolveSpec* dspec = nullptr, int* kind_out = nullptr) {
+    BrickPlan bp;
+    if (xg && dspec && cg_fits(P.g, gauss, sms, bp)) {
+        {
+            tl::SolveSpec hs{};
+            hs.mbase = P.mbase;
+            hs.w = P.w;
+            hs.src = P.src;
+            hs.src.on = gauss ? 1 : 0;
+            hs.tin = 0;
+            hs.save_before = 0;
+            hs.tout = 1;
+            hs.info = P.info;
+            hs.snap = nullptr;
+            TL_CUDA(cudaMemcpyAsync(dspec, &hs, sizeof(hs), cudaMemcpyHostToDevice, st));
             tl::ResCGParams RP{};
-            RP.P = P;
-            RP.xr = xg;              // exchange buffer (4 n doubles): r0, then w ping-pong
-            RP.xw = xg + P.g.n;
-            RP.prof = prof_buffer();
-            const int N[3] = {P.g.NX, P.g.NY, P.g.NZ};
-            for (int a = 0; a < 3; ++a) {
-                RP.ng[a] = bp.ng[a];
-                split_axis(N[a], bp.ng[a], RP.off[a]);
-            }
+            fill_rescg(RP, P, xg, bp);
+            RP.specs = dspec;
+            RP.nspec = 1;
             const int G = bp.ng[0] * bp.ng[1] * bp.ng[2];
             cudaError_t e = gauss ? launch_rescg_g<true>(RP, bp.npt, G, bp.smem, st)
                                   : launch_rescg_g<false>(RP, bp.npt, G, bp.smem, st);
@@ -343,7 +368,10 @@ struct tl_run {
     tl::SolveInfoDev* info = nullptr; int info_cap = 0; int info_n = 0;
     double* melt = nullptr; double* melt_part = nullptr; double* melt_host = nullptr;
     double* snap_g = nullptr; std::vector<double*> snap_l; int snap_n = 0;
-    double* xg = nullptr;            // exchange array of the resident kernel
+    double* xg = nullptr;            // exchange array of the resident kernels (4 n)
+    tl::SolveSpec* d_specs = nullptr; int specs_cap = 0;
+    std::vector<tl::SolveSpec> h_specs;
+    std::vector<int> ev_nsolve;
     double* flush = nullptr; size_t flush_n = 0;
     int64_t launches = 0;
     bool timing = false;
@@ -352,7 +380,7 @@ struct tl_run {
     int ev_n = 0;                    // pairs in use
 };
 
-static int timed_begin(tl_run* R, int level) {
+static int timed_begin(tl_run* R, int level, int nsolve = 1) {
     if (!R->timing) return TL_OK;
     while ((int)R->ev.size() < 2 * (R->ev_n + 1)) {
         cudaEvent_t e;
@@ -361,6 +389,8 @@ static int timed_begin(tl_run* R, int level) {
     }
     if ((int)R->ev_level.size() < R->ev_n + 1) R->ev_level.resize(R->ev_n + 1);
     R->ev_level[R->ev_n] = level;
+    if ((int)R->ev_nsolve.size() < R->ev_n + 1) R->ev_nsolve.resize(R->ev_n + 1);
+    R->ev_nsolve[R->ev_n] = nsolve;
     TL_CUDA(cudaEventRecord(R->ev[2 * R->ev_n], R->stream));
     return TL_OK;
 }
@@ -439,8 +469,9 @@ int32_t tl_step_host(const tl_grid_desc* grid, double kappa, double rho_c, doubl
         P.src.on = 1;
     }
     double* xg = nullptr;
-    if ((rc = dalloc(&xg, 4 * (size_t)n))) return rc;
-    rc = launch_solve(P, gauss, sms, xg, 0, nullptr);
+    tl::SolveSpec* dspec = nullptr;
+    if ((rc = dalloc(&xg, 4 * (size_t)n)) || (rc = dalloc(&dspec, 1))) return rc;
+    rc = launch_solve(P, gauss, sms, xg, 0, nullptr, dspec);
     if (rc) return rc;
     TL_CUDA(cudaDeviceSynchronize());
     tl::SolveInfoDev hi{};
@@ -451,7 +482,7 @@ int32_t tl_step_host(const tl_grid_desc* grid, double kappa, double rho_c, doubl
         info->rnorm = hi.rnorm; info->true_resid = hi.true_resid;
     }
     cudaFree(T); cudaFree(b); cudaFree(r); cudaFree(p0); cudaFree(p1); cudaFree(q); cudaFree(part);
-    cudaFree(dinfo); cudaFree(xg); if (dA) cudaFree(dA); if (dB) cudaFree(dB); if (dload) cudaFree(dload);
+    cudaFree(dinfo); cudaFree(xg); cudaFree(dspec); if (dA) cudaFree(dA); if (dB) cudaFree(dB); if (dload) cudaFree(dload);
     return TL_OK;
 }
 
@@ -509,7 +540,7 @@ int32_t tl_deposit_host(const tl_grid_desc* grid, const double* points, const do
         TL_CUDA(cudaMemcpy(dp, points, sizeof(double) * 3 * count, cudaMemcpyHostToDevice));
         TL_CUDA(cudaMemcpy(dw, power, sizeof(double) * count, cudaMemcpyHostToDevice));
     }
-    tl::k_deposit<<<1, 256>>>(G, dp, dw, count, dl, prev, prevn);
+    tl::k_deposit<<<1, 1024>>>(G, dp, dw, count, dl, prev, prevn);
     TL_CUDA(cudaGetLastError());
     TL_CUDA(cudaMemcpy(load_out, dl, sizeof(double) * G.n, cudaMemcpyDeviceToHost));
     cudaFree(dl); cudaFree(dp); cudaFree(dw); cudaFree(prev); cudaFree(prevn);
@@ -547,10 +578,11 @@ int32_t tl_run_create(const tl_run_desc* desc, tl_run** out) {
         (rc = dalloc(&R->Tl_before, nl)) || (rc = dalloc(&R->part, 4 * R->sms * 32)) ||
         (rc = dalloc(&R->dep_prev, tl::kDepMax)) || (rc = dalloc(&R->dep_prev_n, 1)) ||
         (rc = dalloc(&R->melt, 4)) || (rc = dalloc(&R->melt_part, 2 * 1184)) ||
-        (rc = dalloc(&R->xg, 4 * (size_t)std::max(ng, nl)))) {
+        (rc = dalloc(&R->xg, 4 * (size_t)std::max(ng, nl))) || (rc = dalloc(&R->d_specs, 64))) {
         tl_run_destroy(R);
         return rc;
     }
+    R->specs_cap = 64;
     TL_CUDA(cudaMemsetAsync(R->loadg, 0, sizeof(double) * ng, R->stream));
     TL_CUDA(cudaMemsetAsync(R->dep_prev_n, 0, sizeof(int), R->stream));
     TL_CUDA(cudaMemsetAsync(R->tr_old, 0, sizeof(double) * nl, R->stream));
@@ -572,6 +604,7 @@ int32_t tl_run_destroy(tl_run* R) {
     if (R->dep_prev) cudaFree(R->dep_prev);
     if (R->dep_prev_n) cudaFree(R->dep_prev_n);
     if (R->info) cudaFree(R->info);
+    if (R->d_specs) cudaFree(R->d_specs);
     if (R->snap_g) cudaFree(R->snap_g);
     for (cudaEvent_t e : R->ev) cudaEventDestroy(e);
     for (double* b : R->snap_l) cudaFree(b);
@@ -661,7 +694,60 @@ static int local_solve(tl_run* R, double* T, const tl_micro_plan& mp) {
     }
     P.info = R->info + R->info_n++;
     if (int rc = timed_begin(R, 1)) return rc;
-    if (int rc = launch_solve(P, gauss, R->sms, R->xg, R->stream, &R->launches)) return rc;
+    if (int rc = launch_solve(P, gauss, R->sms, R->xg, R->stream, &R->launches, R->d_specs)) return rc;
+    return timed_end(R);
+}
+
+// All micro solves of one macro step (+ the corrector) as one k_pcg_resident_cg launch.
+static int local_multi(tl_run* R, const tl_macro_plan& mp, const tl_micro_plan* micro,
+                       const BrickPlan& bp) {
+    const int ns = mp.n_micro + (mp.corrector ? 1 : 0);
+    if (R->specs_cap < ns + 1) {
+        if (R->d_specs) cudaFree(R->d_specs);
+        R->d_specs = nullptr;
+        if (int rc = dalloc(&R->d_specs, ns + 1)) return rc;
+        R->specs_cap = ns + 1;
+    }
+    R->h_specs.assign(ns, tl::SolveSpec{});
+    const double V = R->L.h[0] * R->L.h[1] * R->L.h[2];
+    for (int e = 0; e < ns; ++e) {
+        const tl_micro_plan& up = micro[mp.micro_offset + e];
+        const bool corr = mp.corrector && e == mp.n_micro;
+        tl::SolveSpec& sp = R->h_specs[e];
+        sp.mbase = (R->desc.rho_c_local / up.dt) * V / 24.0;      // set_coeffs
+        sp.w = up.w;
+        sp.src.peak = R->desc.beam_peak;
+        sp.src.radius = R->desc.beam_radius;
+        sp.src.depth = R->desc.beam_depth;
+        for (int a = 0; a < 3; ++a) sp.src.center[a] = up.center[a];
+        sp.src.on = up.source_on ? 1 : 0;
+        sp.tin = corr ? 2 : (e == 0 ? 0 : 1);
+        sp.save_before = (mp.corrector && e == mp.n_micro - 1) ? 1 : 0;
+        sp.tout = (e == ns - 1) ? 1 : 0;
+        sp.info = R->info + R->info_n++;
+        sp.snap = nullptr;
+        if (mp.record) {
+            if (int rc = ensure_snapshots(R, ns)) return rc;
+            sp.snap = R->snap_l[e];
+        }
+    }
+    TL_CUDA(cudaMemcpyAsync(R->d_specs + 1, R->h_specs.data(), sizeof(tl::SolveSpec) * ns,
+                            cudaMemcpyHostToDevice, R->stream));
+    tl::PcgParams P{};
+    base_params(R, P, true, micro[mp.micro_offset].dt);
+    P.T = R->Tl;
+    P.gA = R->tr_old;
+    P.gB = R->tr_pred;
+    P.load = nullptr;
+    tl::ResCGParams RP{};
+    fill_rescg(RP, P, R->xg, bp);
+    RP.specs = R->d_specs + 1;
+    RP.nspec = ns;
+    const int G = bp.ng[0] * bp.ng[1] * bp.ng[2];
+    if (int rc = timed_begin(R, 1, ns)) return rc;
+    cudaError_t e = launch_rescg_g<true>(RP, bp.npt, G, bp.smem, R->stream);
+    if (e != cudaSuccess) return fail(TL_E_CUDA, std::string("k_pcg_resident_cg (multi) launch: ") + cudaGetErrorString(e));
+    ++R->launches;
     return timed_end(R);
 }
 
@@ -670,6 +756,8 @@ int32_t tl_run_macro_steps(tl_run* R, const tl_macro_plan* plans, int32_t nsteps
                            const double* dep_power, int32_t ndep) {
     if (!R || (!plans && nsteps > 0)) return fail(TL_E_INVALID, "null argument");
     TL_CUDA(cudaSetDevice(R->device));
+    BrickPlan lbp;
+    const bool multi = cg_fits(R->L, true, R->sms, lbp) && getenv("TLGPU_PER_SOLVE") == nullptr;
     int need = 0;
     for (int s = 0; s < nsteps; ++s) {
         const tl_macro_plan& mp = plans[s];
@@ -695,7 +783,7 @@ int32_t tl_run_macro_steps(tl_run* R, const tl_macro_plan* plans, int32_t nsteps
     for (int s = 0; s < nsteps; ++s) {
         const tl_macro_plan& mp = plans[s];
         // -- global predictor (twolevel.solve_global): deposit + implicit step --
-        tl::k_deposit<<<1, 256, 0, R->stream>>>(R->G, R->dep_pts + 3 * (size_t)mp.dep_offset,
+        tl::k_deposit<<<1, 1024, 0, R->stream>>>(R->G, R->dep_pts + 3 * (size_t)mp.dep_offset,
                                                  R->dep_pow + mp.dep_offset, mp.dep_count, R->loadg,
                                                  R->dep_prev, R->dep_prev_n);
         ++R->launches;
@@ -708,7 +796,7 @@ int32_t tl_run_macro_steps(tl_run* R, const tl_macro_plan* plans, int32_t nsteps
         P.load = R->loadg;
         P.info = R->info + R->info_n++;
         if (int rc = timed_begin(R, 0)) return rc;
-        if (int rc = launch_solve(P, false, R->sms, R->xg, R->stream, &R->launches)) return rc;
+        if (int rc = launch_solve(P, false, R->sms, R->xg, R->stream, &R->launches, R->d_specs)) return rc;
         if (int rc = timed_end(R)) return rc;
         if (mp.record) {
             if (int rc = ensure_snapshots(R, mp.n_micro + mp.corrector)) return rc;
@@ -717,7 +805,10 @@ int32_t tl_run_macro_steps(tl_run* R, const tl_macro_plan* plans, int32_t nsteps
         }
         // -- trace of the predicted global field on gamma --
         if (int rc = run_interp_local(R, 1, nullptr, R->tr_pred)) return rc;
-        // -- micro steps --
+        // -- micro steps (+ corrector): one persistent launch when the local grid fits --
+        if (multi) {
+            if (int rc = local_multi(R, mp, micro, lbp)) return rc;
+        } else
         for (int i = 0; i < mp.n_micro; ++i) {
             const tl_micro_plan& up = micro[mp.micro_offset + i];
             if (i == mp.n_micro - 1 && mp.corrector) {
@@ -728,7 +819,7 @@ int32_t tl_run_macro_steps(tl_run* R, const tl_macro_plan* plans, int32_t nsteps
             if (mp.record)
                 TL_CUDA(cudaMemcpyAsync(R->snap_l[i], R->Tl, sizeof(double) * R->L.n, cudaMemcpyDeviceToDevice, R->stream));
         }
-        if (mp.corrector) {
+        if (mp.corrector && !multi) {
             // corrector: re-solve the last micro interval from before_final with trace_pred
             if (int rc = local_solve(R, R->Tl_before, micro[mp.micro_offset + mp.n_micro])) return rc;
             std::swap(R->Tl, R->Tl_before);
@@ -840,7 +931,8 @@ int32_t tl_run_set_timing(tl_run* R, int32_t on) {
     return TL_OK;
 }
 
-int32_t tl_run_take_timing(tl_run* R, float* ms, int32_t* level, int32_t max, int32_t* count) {
+int32_t tl_run_take_timing(tl_run* R, float* ms, int32_t* level, int32_t* nsolve, int32_t max,
+                           int32_t* count) {
     if (!R || !count) return fail(TL_E_INVALID, "null argument");
     TL_CUDA(cudaSetDevice(R->device));
     TL_CUDA(cudaStreamSynchronize(R->stream));
@@ -850,12 +942,14 @@ int32_t tl_run_take_timing(tl_run* R, float* ms, int32_t* level, int32_t max, in
         TL_CUDA(cudaEventElapsedTime(&t, R->ev[2 * e], R->ev[2 * e + 1]));
         ms[e] = t;
         level[e] = R->ev_level[e];
+        if (nsolve) nsolve[e] = R->ev_nsolve[e];
     }
     // drop the pairs we returned (keep the rest in order)
     for (int e = n; e < R->ev_n; ++e) {
         std::swap(R->ev[2 * (e - n)], R->ev[2 * e]);
         std::swap(R->ev[2 * (e - n) + 1], R->ev[2 * e + 1]);
         R->ev_level[e - n] = R->ev_level[e];
+        R->ev_nsolve[e - n] = R->ev_nsolve[e];
     }
     R->ev_n -= n;
     *count = n;

@@ -1,5 +1,9 @@
 // tl_resident_cg.cuh — one-barrier-per-iteration resident PCG (Chronopoulos-Gear), sm_100a fp64.
 //
+// One launch runs a list of solves back to back (SolveSpec): the micro steps and the
+// corrector of a macro step share the CTA setup (node classes, halo lists) and keep the
+// evolving local field x in shared memory from one solve to the next.
+//
 // Same operator, RHS, preconditioner, stopping rule (||r|| < rtol ||b|| tested at the top
 // of each iteration on the directly computed r.r) and final checks as scipy's cg /
 // k_pcg_resident, but the Chronopoulos-Gear recurrences
@@ -24,10 +28,25 @@
 
 namespace tl {
 
+// One solve of a multi-solve launch (all micro steps + corrector of a macro step).
+struct SolveSpec {
+    double mbase;                 // (rho c / dt) V / 24 of this step
+    double w;                     // trace blend weight of the Dirichlet data (1-w) gA + w gB
+    Gauss src;                    // Gaussian at this step's t1 (src.on == 0: none)
+    int tin;                      // T_old: 0 = P.T (global), 1 = previous solve's x, 2 = saved copy
+    int save_before;              // 1: save T_old of this solve (before_final, multirate.py:136-137)
+    int tout;                     // 1: write the result to P.T
+    SolveInfoDev* info;           // this solve's outcome record
+    double* snap;                 // optional copy of the result (recorder snapshots), or nullptr
+};
+
 struct ResCGParams {
-    PcgParams P;                  // T (in: T_old, out: x), b, p0 (p), part, info, ...
-    double* xr;                   // exchange: brick-surface r0, n doubles
+    PcgParams P;                  // grid, cbase, gA/gB, g_const, load, b, part, rtol, maxiter
+    double* xr;                   // exchange: brick-surface r0 / final x, n doubles
     double* xw;                   // exchange: brick-surface w, 2 n doubles (ping-pong)
+    double* saved;                // n doubles: T_old saved for the corrector
+    const SolveSpec* specs;       // nspec solves run back to back in one launch
+    int nspec;
     unsigned long long* prof;
     int ng[3];
     int off[3][kResMaxSplit + 1];
@@ -88,8 +107,7 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
     int* FG = FS + nface;
     uint8_t* CL = reinterpret_cast<uint8_t*>(FG + nface);
 
-    build_class_table(T, threadIdx.x, P.mbase, P.cbase, g.dkind);
-    if (GAUSS) build_gauss_tables(g, P.src, tx, ty, tz);
+    build_class_table(T, threadIdx.x, RP.specs[0].mbase, P.cbase, g.dkind);
     for (int s = threadIdx.x; s < H; s += kResTPB) {
         const int u = s % LX, v = (s / LX) % LY, w = s / SZ;
         const int i = x0 + u - 1, j = y0 + v - 1, k = z0 + w - 1;
@@ -98,7 +116,6 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
         US[s] = 0.0;
     }
     __syncthreads();
-    if (GAUSS) build_gauss_bounds(g, tx, ty, tz, bx_, by_, bz_);
     for (int e0 = threadIdx.x; e0 < nface; e0 += kResTPB) {
         int e = e0, u, v, w;
         if (e < 2 * fx) {
@@ -143,8 +160,25 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
         }
     }
 
+  __shared__ SolveSpec S;                   // this solve's parameters (shared: no registers)
+  for (int si = 0; si < RP.nspec; ++si) {
+    __syncthreads();                        // previous solve done with T, PO, US, S
+    if (threadIdx.x == 0) S = RP.specs[si];
+    __syncthreads();
+    const bool gauss = GAUSS && S.src.on;
+    build_class_table(T, threadIdx.x, S.mbase, P.cbase, g.dkind);
+    if (gauss) build_gauss_tables(g, S.src, tx, ty, tz);
+    __syncthreads();
+    if (gauss) {
+        build_gauss_bounds(g, tx, ty, tz, bx_, by_, bz_);
+        __syncthreads();
+    }
+    auto dvalue = [&](int q) -> double {    // Dirichlet value of this solve
+        if (P.gA == nullptr) return P.g_const;
+        return __dadd_rn(__dmul_rn(1.0 - S.w, P.gA[q]), __dmul_rn(S.w, P.gB[q]));
+    };
+
     // ---- phase 0: constrained RHS (identical to k_pcg_resident), r0 = b, x = 0 ----
-    if (GAUSS) __syncthreads();
     double acc[2] = {0.0, 0.0};
 #pragma unroll
     for (int m = 0; m < NPT; ++m) {
@@ -152,23 +186,26 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
         const int nl = threadIdx.x + m * kResTPB;
         const int p = GID[nl];
         const int cls = od_cls(od[m]);
+        const double told = S.tin == 0 ? P.T[p] : (S.tin == 1 ? XO[nl] : RP.saved[p]);
+        if (S.save_before) RP.saved[p] = told;
+        XO[nl] = 0.0;                       // x0 = 0
         double bv;
         if (T.nd[cls] == 0.0) {
-            bv = dirichlet_value(P, p);
+            bv = dvalue(p);
         } else {
             int i, j, k;
             decode(g, p, i, j, k);
-            bv = T.mass[cls] * P.T[p];
+            bv = T.mass[cls] * told;
             if (P.load) bv += P.load[p];
-            if (GAUSS) bv = add_gaussian(bv, g, tx, ty, tz, bx_, by_, bz_, i, j, k);
+            if (gauss) bv = add_gaussian(bv, g, tx, ty, tz, bx_, by_, bz_, i, j, k);
             const int sy = g.NX, sz = g.NX * g.NY;
             double lift = 0.0;
-            if (i > 0 && T.nd[cls - axis_class(i, g.nc[0]) + axis_class(i - 1, g.nc[0])] == 0.0) lift += T.c[0][cls] * dirichlet_value(P, p - 1);
-            if (i < g.nc[0] && T.nd[cls - axis_class(i, g.nc[0]) + axis_class(i + 1, g.nc[0])] == 0.0) lift += T.c[0][cls] * dirichlet_value(P, p + 1);
-            if (j > 0 && T.nd[cls + 3 * (axis_class(j - 1, g.nc[1]) - axis_class(j, g.nc[1]))] == 0.0) lift += T.c[1][cls] * dirichlet_value(P, p - sy);
-            if (j < g.nc[1] && T.nd[cls + 3 * (axis_class(j + 1, g.nc[1]) - axis_class(j, g.nc[1]))] == 0.0) lift += T.c[1][cls] * dirichlet_value(P, p + sy);
-            if (k > 0 && T.nd[cls + 9 * (axis_class(k - 1, g.nc[2]) - axis_class(k, g.nc[2]))] == 0.0) lift += T.c[2][cls] * dirichlet_value(P, p - sz);
-            if (k < g.nc[2] && T.nd[cls + 9 * (axis_class(k + 1, g.nc[2]) - axis_class(k, g.nc[2]))] == 0.0) lift += T.c[2][cls] * dirichlet_value(P, p + sz);
+            if (i > 0 && T.nd[cls - axis_class(i, g.nc[0]) + axis_class(i - 1, g.nc[0])] == 0.0) lift += T.c[0][cls] * dvalue(p - 1);
+            if (i < g.nc[0] && T.nd[cls - axis_class(i, g.nc[0]) + axis_class(i + 1, g.nc[0])] == 0.0) lift += T.c[0][cls] * dvalue(p + 1);
+            if (j > 0 && T.nd[cls + 3 * (axis_class(j - 1, g.nc[1]) - axis_class(j, g.nc[1]))] == 0.0) lift += T.c[1][cls] * dvalue(p - sy);
+            if (j < g.nc[1] && T.nd[cls + 3 * (axis_class(j + 1, g.nc[1]) - axis_class(j, g.nc[1]))] == 0.0) lift += T.c[1][cls] * dvalue(p + sy);
+            if (k > 0 && T.nd[cls + 9 * (axis_class(k - 1, g.nc[2]) - axis_class(k, g.nc[2]))] == 0.0) lift += T.c[2][cls] * dvalue(p - sz);
+            if (k < g.nc[2] && T.nd[cls + 9 * (axis_class(k + 1, g.nc[2]) - axis_class(k, g.nc[2]))] == 0.0) lift += T.c[2][cls] * dvalue(p + sz);
             bv += lift;
         }
         P.b[p] = bv;
@@ -185,7 +222,7 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
         const int s2[2] = {0, 1};
         grid_sum_fast<2>(P.part, s2, G, tot);
     }
-    if (prof) RP.prof[np++] = global_ns();
+    if (prof && si == 0) RP.prof[np++] = global_ns();
     const double bb = tot[0];
     double gam = tot[1];                    // r0 . u0
     const double bnorm = sqrt(bb);
@@ -243,7 +280,7 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
             const double alpha = first ? gam / dlt : gam / (dlt - beta * gam / alpha_prev);
             // halo: s = w + beta s, r -= alpha s, u = M r  (w of the halo from the exchange)
 #define TL_STAMP(slot) \
-    if (prof && it == 3) RP.prof[slot] = global_ns();
+    if (prof && si == 0 && it == 3) RP.prof[slot] = global_ns();
             TL_STAMP(100)
             const double* win = RP.xw + (size_t)(it & 1) * g.n;
             double fw[kResKF];
@@ -310,7 +347,7 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
             block_sum<3>(d3, red);
             if (threadIdx.x == 0) { P.part[0 * G + b] = d3[0]; P.part[1 * G + b] = d3[1]; P.part[2 * G + b] = d3[2]; }
             TL_STAMP(104)
-            if (RP.prof && it == 3 && threadIdx.x == 0) RP.prof[256 + b] = global_ns();   // arrival per CTA
+            if (RP.prof && si == 0 && it == 3 && threadIdx.x == 0) RP.prof[256 + b] = global_ns();   // arrival per CTA
             grid.sync();
             TL_STAMP(105)
             {
@@ -319,7 +356,7 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
             }
             TL_STAMP(106)
 #undef TL_STAMP
-            if (prof && it < 100) RP.prof[np++] = global_ns();
+            if (prof && si == 0 && it < 100) RP.prof[np++] = global_ns();
             gam = tot[0];
             dlt = tot[1];
             rr = tot[2];
@@ -355,7 +392,10 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
         const double dd = ax - bv;
         res[0] += dd * dd;
         res[1] += isfinite(xp) ? 0.0 : 1.0;
-        P.T[p] = (T.nd[cls] == 0.0) ? bv : xp;      // x_D = g = b_D (fem.py:289-290)
+        const double xv = (T.nd[cls] == 0.0) ? bv : xp;   // x_D = g = b_D (fem.py:289-290)
+        XO[threadIdx.x + m * kResTPB] = xv;
+        if (S.tout) P.T[p] = xv;
+        if (S.snap) S.snap[p] = xv;
     }
     block_sum<2>(res, red);
     if (threadIdx.x == 0) { P.part[0 * G + b] = res[0]; P.part[3 * G + b] = res[1]; }
@@ -368,13 +408,14 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
         const double tres = bnorm > 0.0 ? sqrt(tot[0]) / bnorm : 0.0;
         if (status == 0 && tot[1] > 0.0) status = 3;
         if (status == 0 && (!isfinite(tres) || tres > 1e2 * P.rtol)) status = 2;
-        P.info->iterations = (status == 1) ? P.maxiter : it;
-        P.info->status = status;
-        P.info->bnorm = bnorm;
-        P.info->rnorm = rnorm;
-        P.info->true_resid = tres;
-        if (prof) { RP.prof[np++] = global_ns(); RP.prof[127] = np; }
+        S.info->iterations = (status == 1) ? P.maxiter : it;
+        S.info->status = status;
+        S.info->bnorm = bnorm;
+        S.info->rnorm = rnorm;
+        S.info->true_resid = tres;
+        if (prof && si == 0) { RP.prof[np++] = global_ns(); RP.prof[127] = np; }
     }
+  }
 }
 
 }  // namespace tl

@@ -154,14 +154,16 @@ class DeviceRun:
         N.check(N.lib().tl_run_set_timing(self._h, int(on)), "set_timing")
 
     def take_timing(self):
-        """[(ms, level)] of the solve launches since the last call (level 0 global, 1 local)."""
+        """[(ms, level, nsolve)] of the solve launches since the last call (level 0 global,
+        1 local; nsolve = solves run by that launch, in the order of take_info's records)."""
         out = []
         ms = (C.c_float * 4096)()
         lv = (C.c_int32 * 4096)()
+        ns = (C.c_int32 * 4096)()
         cnt = C.c_int32()
         while True:
-            N.check(N.lib().tl_run_take_timing(self._h, ms, lv, 4096, C.byref(cnt)), "take_timing")
-            out.extend((float(ms[e]), int(lv[e])) for e in range(cnt.value))
+            N.check(N.lib().tl_run_take_timing(self._h, ms, lv, ns, 4096, C.byref(cnt)), "take_timing")
+            out.extend((float(ms[e]), int(lv[e]), int(ns[e])) for e in range(cnt.value))
             if cnt.value < 4096:
                 break
         return out
