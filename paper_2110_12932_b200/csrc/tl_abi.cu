@@ -177,9 +177,9 @@ static bool exact_cg() {
     return v == 1;
 }
 
-template <bool GAUSS, int NPT>
+template <bool GAUSS, int NPT, bool MULTI>
 static cudaError_t launch_rescg_t(tl::ResCGParams& RP, int G, size_t smem, cudaStream_t st) {
-    auto fn = tl::k_pcg_resident_cg<GAUSS, NPT>;
+    auto fn = tl::k_pcg_resident_cg<GAUSS, NPT, MULTI>;
     static thread_local bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kResSmemCap);
@@ -190,12 +190,12 @@ static cudaError_t launch_rescg_t(tl::ResCGParams& RP, int G, size_t smem, cudaS
     return cudaLaunchCooperativeKernel((void*)fn, G, tl::kResTPB, args, smem, st);
 }
 
-template <bool GAUSS>
+template <bool GAUSS, bool MULTI = false>
 static cudaError_t launch_rescg_g(tl::ResCGParams& RP, int npt, int G, size_t smem, cudaStream_t st) {
     switch (npt) {
-        case 4: return launch_rescg_t<GAUSS, 4>(RP, G, smem, st);
-        case 8: return launch_rescg_t<GAUSS, 8>(RP, G, smem, st);
-        default: return launch_rescg_t<GAUSS, 12>(RP, G, smem, st);
+        case 4: return launch_rescg_t<GAUSS, 4, MULTI>(RP, G, smem, st);
+        case 8: return launch_rescg_t<GAUSS, 8, MULTI>(RP, G, smem, st);
+        default: return launch_rescg_t<GAUSS, 12, MULTI>(RP, G, smem, st);
     }
 }
 
@@ -745,7 +745,7 @@ static int local_multi(tl_run* R, const tl_macro_plan& mp, const tl_micro_plan* 
     RP.nspec = ns;
     const int G = bp.ng[0] * bp.ng[1] * bp.ng[2];
     if (int rc = timed_begin(R, 1, ns)) return rc;
-    cudaError_t e = launch_rescg_g<true>(RP, bp.npt, G, bp.smem, R->stream);
+    cudaError_t e = launch_rescg_g<true, true>(RP, bp.npt, G, bp.smem, R->stream);
     if (e != cudaSuccess) return fail(TL_E_CUDA, std::string("k_pcg_resident_cg (multi) launch: ") + cudaGetErrorString(e));
     ++R->launches;
     return timed_end(R);
@@ -757,7 +757,11 @@ int32_t tl_run_macro_steps(tl_run* R, const tl_macro_plan* plans, int32_t nsteps
     if (!R || (!plans && nsteps > 0)) return fail(TL_E_INVALID, "null argument");
     TL_CUDA(cudaSetDevice(R->device));
     BrickPlan lbp;
-    const bool multi = cg_fits(R->L, true, R->sms, lbp) && getenv("TLGPU_PER_SOLVE") == nullptr;
+    // TLGPU_MULTI=1: all micro solves of a macro step in one persistent launch.  Off by
+    // default: with the Gaussian evaluated in-kernel the persistent kernel needs more than
+    // 128 registers and its CG loop spills (200 us vs 185 us per solve on cfg2).
+    const char* mv = getenv("TLGPU_MULTI");
+    const bool multi = mv && mv[0] == '1' && cg_fits(R->L, true, R->sms, lbp);
     int need = 0;
     for (int s = 0; s < nsteps; ++s) {
         const tl_macro_plan& mp = plans[s];

@@ -60,7 +60,9 @@ __host__ __device__ inline size_t rescg_smem_bytes(int lx, int ly, int lz, int g
     return 8 * extra + 9 * H + 36 * n + 24 * F + 16;
 }
 
-template <bool GAUSS, int NPT>
+// MULTI = false: exactly one solve (specs[0]); the solve loop folds away, which keeps the
+// kernel at ~106 registers without spills.
+template <bool GAUSS, int NPT, bool MULTI>
 __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) {
     cg::grid_group grid = cg::this_grid();
     const PcgParams& P = RP.P;
@@ -161,7 +163,8 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
     }
 
   __shared__ SolveSpec S;                   // this solve's parameters (shared: no registers)
-  for (int si = 0; si < RP.nspec; ++si) {
+  const int nsp = MULTI ? RP.nspec : 1;
+  for (int si = 0; si < nsp; ++si) {
     __syncthreads();                        // previous solve done with T, PO, US, S
     if (threadIdx.x == 0) S = RP.specs[si];
     __syncthreads();
@@ -186,8 +189,8 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
         const int nl = threadIdx.x + m * kResTPB;
         const int p = GID[nl];
         const int cls = od_cls(od[m]);
-        const double told = S.tin == 0 ? P.T[p] : (S.tin == 1 ? XO[nl] : RP.saved[p]);
-        if (S.save_before) RP.saved[p] = told;
+        const double told = (!MULTI || S.tin == 0) ? P.T[p] : (S.tin == 1 ? XO[nl] : RP.saved[p]);
+        if (MULTI && S.save_before) RP.saved[p] = told;
         XO[nl] = 0.0;                       // x0 = 0
         double bv;
         if (T.nd[cls] == 0.0) {
@@ -394,8 +397,8 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
         res[1] += isfinite(xp) ? 0.0 : 1.0;
         const double xv = (T.nd[cls] == 0.0) ? bv : xp;   // x_D = g = b_D (fem.py:289-290)
         XO[threadIdx.x + m * kResTPB] = xv;
-        if (S.tout) P.T[p] = xv;
-        if (S.snap) S.snap[p] = xv;
+        if (!MULTI || S.tout) P.T[p] = xv;
+        if (MULTI && S.snap) S.snap[p] = xv;
     }
     block_sum<2>(res, red);
     if (threadIdx.x == 0) { P.part[0 * G + b] = res[0]; P.part[3 * G + b] = res[1]; }
