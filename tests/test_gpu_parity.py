@@ -242,3 +242,68 @@ def test_box_reaching_the_wall_raises_like_the_reference():
     cfg = P.config_from_text(text, CONFIGS)
     with pytest.raises(P.MeshError):
         P.two_level_run(cfg)
+
+
+def _oracle_step(grid, kind, T_old, dt, g, load=None, gauss=None):
+    from oracle.pcg import solve_constrained
+    G = kuhn.KuhnGrid(grid.placement.box0.lo, grid.placement.box0.hi, grid.ncells, grid.placement.offset)
+    D = (G.bottom_mask() if kind == N.TL_DIRICHLET_BOTTOM else G.gamma_mask())
+    op = kuhn.StencilOperator(G, 9.8, 8440 * 410.0, dt, D)
+    if gauss is not None:
+        load = kuhn.gaussian_load(G, gauss[0], gauss[1])
+    b = op.rhs(T_old, load, g)
+    x, its, _ = solve_constrained(op, b, g, 1e-12)
+    return x, its
+
+
+def test_streaming_global_step_cfg3_size_vs_oracle():
+    """HBM-bound size (6.9M nodes, the streaming kernel): one global step vs the oracle."""
+    cfg = P.load_config(CONFIGS / "cfg3.cfg")
+    problem, lm = P.build_problem(cfg)
+    grid = problem.global_mesh
+    rng = np.random.default_rng(0)
+    T = rng.uniform(293.0, 2293.0, grid.n_nodes)
+    g = np.full(grid.n_nodes, 293.0)
+    pts, pw = problem.global_source(0.0, cfg.dt_macro)
+    load = ops.deposit_load(grid, pts, pw)
+    x, info = ops.step(grid, 9.8, 8440 * 410.0, cfg.dt_macro, N.TL_DIRICHLET_BOTTOM, T, g_const=293.0,
+                       load=load, rtol=1e-12)
+    ref, its = _oracle_step(grid, N.TL_DIRICHLET_BOTTOM, T, cfg.dt_macro, g, load=load)
+    assert info.status == 0 and abs(info.iterations - its) <= 1
+    assert rel(x, ref) <= 1e-12
+
+
+def test_streaming_local_step_cfg3_size_vs_oracle():
+    """cfg3 local grid (1.73M nodes, streaming kernel + Gaussian load kernel) vs the oracle."""
+    cfg = P.load_config(CONFIGS / "cfg3.cfg")
+    problem, lm = P.build_problem(cfg)
+    rng = np.random.default_rng(1)
+    T = rng.uniform(293.0, 2293.0, lm.n_nodes)
+    g = np.where(lm.gamma_mask(), rng.uniform(293.0, 900.0, lm.n_nodes), 0.0)
+    src = problem.local_source(2e-6)
+    dt = cfg.dt_macro / cfg.micro_steps
+    x, info = ops.step(lm, 9.8, 8440 * 410.0, dt, N.TL_DIRICHLET_GAMMA, T, g=g,
+                       gaussian=src.device_args(), rtol=1e-12)
+    ref, its = _oracle_step(lm, N.TL_DIRICHLET_GAMMA, T, dt, g, gauss=(cfg.beam, src.center))
+    assert info.status == 0 and abs(info.iterations - its) <= 1
+    assert rel(x, ref) <= 1e-12
+
+
+def test_linearity_full_size_cfg4_global_step():
+    """cfg4's 201M-node global grid is beyond any CPU oracle; a size-independent property
+    instead: the implicit step is affine in (T_old, load), so
+    step(T1 + T2, L1 + L2) - step(T2, L2) == step(T1, L1) - step(0, 0) to CG tolerance."""
+    cfg = P.load_config(CONFIGS / "cfg4.cfg")
+    problem, _ = P.build_problem(cfg)
+    grid = problem.global_mesh
+    n = grid.n_nodes
+    rng = np.random.default_rng(2)
+    k = 9.8, 8440 * 410.0
+    T1 = rng.uniform(0.0, 100.0, n)
+    T2 = np.full(n, 293.0)
+    s = lambda T: ops.step(grid, *k, cfg.dt_macro, N.TL_DIRICHLET_BOTTOM, T, g_const=0.0, rtol=1e-12)  # noqa: E731
+    a, ia = s(T1 + T2)
+    b, ib = s(T2)
+    c, ic = s(T1)
+    assert ia.status == ib.status == ic.status == 0
+    assert np.abs((a - b) - c).max() <= 1e-9 * np.abs(a).max()
