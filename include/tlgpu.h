@@ -199,6 +199,46 @@ int32_t tl_debug_profile(uint64_t* out, int32_t max, int32_t* count);
 /* Write a scratch buffer larger than L2 on the run's stream (bench hygiene). */
 int32_t tl_run_flush_l2(tl_run* run);
 
+/* ---- multi-GPU: z-slab decomposition of the global solve ----------------
+ * Replaces, per rank, the share of the global backward-Euler step
+ * (twolevel.solve_global, lpbfsim/twolevel.py:242-271 -> fem.step_backward_euler,
+ * fem.py:307-355 -> scipy cg, fem.py:271-298) that falls on the rank's node planes.
+ * The reference has no decomposition; these entry points are the phases of one CG
+ * iteration between the collectives the host issues (paper_2110_12932_b200/slab.py):
+ *   rhs -> [sum bb, rz] -> halo r -> loop { direction -> [sum pq] -> update -> [sum rz, rr]
+ *   -> halo r } -> halo x -> residual -> [sum] -> finish.
+ * Rank owns node planes [k0, k1) and stores planes [h0, h1) = [max(k0-1,0), min(k1+1,nz+1)):
+ * every array below is device memory of (h1-h0)*(nx+1)*(ny+1) doubles, plane h0 first.
+ * sums receives this rank's partial sums: slot 0/1 after rhs (b.b, r.z) and update
+ * (r.z, r.r), slot 2 after direction (p.q), slots 0/3 after residual (||Ax-b||^2,
+ * non-finite count).  work must hold tl_slab_work_len() doubles, zeroed once before first
+ * use (the kernels leave it zeroed).  Only TL_DIRICHLET_BOTTOM is supported. */
+typedef struct {
+    tl_grid_desc grid;        /* the whole global grid                           */
+    int32_t dirichlet_kind;   /* TL_DIRICHLET_BOTTOM                             */
+    int32_t k0, k1;           /* owned node planes                               */
+    double kappa, rho_c, dt;
+    double g_const;           /* Dirichlet value (build-plate temperature)       */
+    double* x;                /* T_old in (own planes), solution out, in place   */
+    double *b, *r, *p0, *p1;  /* CG workspace                                    */
+    const double* load;       /* deposit load or NULL                            */
+    double* work;
+    double* sums;             /* 4 doubles                                       */
+    void* stream;             /* cudaStream_t, NULL = legacy default stream      */
+} tl_slab;
+
+int64_t tl_slab_work_len(void);
+/* RHS (mass T_old + load [+ Gaussian] + Dirichlet lift), r = b, x = 0 on own planes. */
+int32_t tl_slab_rhs(const tl_slab* s, const tl_gaussian* src);
+/* p = z (first) or beta p + z on stored planes; p.q over own planes. */
+int32_t tl_slab_direction(const tl_slab* s, int32_t first, double beta, int32_t parity);
+/* x += alpha p, r -= alpha A p on own planes; r.z, r.r. */
+int32_t tl_slab_update(const tl_slab* s, double alpha, int32_t parity);
+/* ||A x - b||^2 and the non-finite count over own planes (x halo must be current). */
+int32_t tl_slab_residual(const tl_slab* s);
+/* Re-impose the Dirichlet values x_D = b_D (fem.py:289-290). */
+int32_t tl_slab_finish(const tl_slab* s);
+
 #ifdef __cplusplus
 }
 #endif

@@ -64,6 +64,14 @@ class MicroPlan(C.Structure):
     _fields_ = [("dt", C.c_double), ("w", C.c_double), ("center", _d3), ("source_on", C.c_int32)]
 
 
+class Slab(C.Structure):
+    _fields_ = [("grid", GridDesc), ("dirichlet_kind", C.c_int32), ("k0", C.c_int32), ("k1", C.c_int32),
+                ("kappa", C.c_double), ("rho_c", C.c_double), ("dt", C.c_double), ("g_const", C.c_double),
+                ("x", C.c_void_p), ("b", C.c_void_p), ("r", C.c_void_p), ("p0", C.c_void_p),
+                ("p1", C.c_void_p), ("load", C.c_void_p), ("work", C.c_void_p), ("sums", C.c_void_p),
+                ("stream", C.c_void_p)]
+
+
 # numpy views of the plan structs (same layout, built in bulk on the host)
 MACRO_DTYPE = np.dtype([("dt_global", "<f8"), ("dep_offset", "<i4"), ("dep_count", "<i4"),
                         ("micro_offset", "<i4"), ("n_micro", "<i4"), ("corrector", "<i4"),
@@ -106,6 +114,12 @@ SIGNATURES = [
                                        C.POINTER(C.c_int32), C.c_int32, C.POINTER(C.c_int32)]),
     ("tl_run_flush_l2", C.c_int32, [_P]),
     ("tl_debug_profile", C.c_int32, [C.POINTER(C.c_uint64), C.c_int32, C.POINTER(C.c_int32)]),
+    ("tl_slab_work_len", C.c_int64, []),
+    ("tl_slab_rhs", C.c_int32, [C.POINTER(Slab), C.POINTER(Gaussian)]),
+    ("tl_slab_direction", C.c_int32, [C.POINTER(Slab), C.c_int32, C.c_double, C.c_int32]),
+    ("tl_slab_update", C.c_int32, [C.POINTER(Slab), C.c_double, C.c_int32]),
+    ("tl_slab_residual", C.c_int32, [C.POINTER(Slab)]),
+    ("tl_slab_finish", C.c_int32, [C.POINTER(Slab)]),
 ]
 
 _lib = None

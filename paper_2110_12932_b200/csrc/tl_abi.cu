@@ -18,6 +18,7 @@
 
 #include "../../include/tlgpu.h"
 #include "tl_resident_cg.cuh"
+#include "tl_slab.cuh"
 
 namespace {
 
@@ -970,6 +971,105 @@ int32_t tl_run_flush_l2(tl_run* R) {
         if (int rc = dalloc(&R->flush, R->flush_n)) return rc;
     }
     tl::k_flush<<<4 * R->sms, 512, 0, R->stream>>>(R->flush, R->flush_n, 1.0);
+    TL_CUDA(cudaGetLastError());
+    return TL_OK;
+}
+
+// ---- z-slab global solve (multi-GPU) ----------------------------------------------
+
+static int slab_params(const tl_slab* s, tl::SlabParams& S, int& blocks, cudaStream_t& st) {
+    if (!s || !s->x || !s->b || !s->r || !s->p0 || !s->p1 || !s->work || !s->sums)
+        return fail(TL_E_INVALID, "null slab argument");
+    if (s->dirichlet_kind != tl::kBottom) return fail(TL_E_INVALID, "slabs support TL_DIRICHLET_BOTTOM only");
+    if (s->dt <= 0) return fail(TL_E_INVALID, "time step must be positive");
+    if (int rc = make_grid(s->grid, s->dirichlet_kind, S.g)) return rc;
+    const int NZ = S.g.NZ, nxy = S.g.NX * S.g.NY;
+    if (s->k0 < 0 || s->k1 > NZ || s->k0 >= s->k1) return fail(TL_E_INVALID, "bad slab plane range");
+    const int h0 = s->k0 > 0 ? s->k0 - 1 : 0;
+    const int h1 = s->k1 < NZ ? s->k1 + 1 : NZ;
+    S.own_lo = s->k0 * nxy; S.own_hi = s->k1 * nxy;
+    S.st_lo = h0 * nxy; S.st_hi = h1 * nxy;
+    const ptrdiff_t base = (ptrdiff_t)S.st_lo;
+    S.x = s->x - base; S.b = s->b - base; S.r = s->r - base; S.p0 = s->p0 - base; S.p1 = s->p1 - base;
+    S.load = s->load ? s->load - base : nullptr;
+    const double V = S.g.h[0] * S.g.h[1] * S.g.h[2];
+    for (int a = 0; a < 3; ++a) S.cbase[a] = s->kappa * V / (S.g.h[a] * S.g.h[a]) / 6.0;
+    S.mbase = (s->rho_c / s->dt) * V / 24.0;
+    S.g_const = s->g_const;
+    S.part = s->work;
+    S.count = reinterpret_cast<unsigned*>(s->work + 4 * tl::kResMaxBlocks);
+    S.sums = s->sums;
+    int dev = 0;
+    TL_CUDA(cudaGetDevice(&dev));
+    static int sms_cache[64] = {0};
+    if (dev < 0 || dev >= 64) return fail(TL_E_INVALID, "device index");
+    if (!sms_cache[dev])
+        if (int rc = device_sms(dev, sms_cache[dev])) return rc;
+    blocks = 2 * sms_cache[dev];
+    if (blocks > tl::kResMaxBlocks) blocks = tl::kResMaxBlocks;
+    st = (cudaStream_t)s->stream;
+    return TL_OK;
+}
+
+int64_t tl_slab_work_len(void) { return 4 * (int64_t)tl::kResMaxBlocks + 1; }
+
+int32_t tl_slab_rhs(const tl_slab* s, const tl_gaussian* src) {
+    tl::SlabParams S{};
+    int blocks = 0;
+    cudaStream_t st;
+    if (int rc = slab_params(s, S, blocks, st)) return rc;
+    if (src && src->on) {
+        S.src.peak = src->peak; S.src.radius = src->radius; S.src.depth = src->depth;
+        for (int a = 0; a < 3; ++a) S.src.center[a] = src->center[a];
+        S.src.on = 1;
+        const size_t smem = gauss_smem(S.g);
+        if (smem > 200 * 1024) return fail(TL_E_INVALID, "grid too long for Gaussian tables");
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(tl::k_slab_rhs<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        tl::k_slab_rhs<true><<<blocks, tl::kSlabTPB, smem, st>>>(S);
+    } else {
+        tl::k_slab_rhs<false><<<blocks, tl::kSlabTPB, 0, st>>>(S);
+    }
+    TL_CUDA(cudaGetLastError());
+    return TL_OK;
+}
+
+int32_t tl_slab_direction(const tl_slab* s, int32_t first, double beta, int32_t parity) {
+    tl::SlabParams S{};
+    int blocks = 0;
+    cudaStream_t st;
+    if (int rc = slab_params(s, S, blocks, st)) return rc;
+    tl::k_slab_direction<<<blocks, tl::kSlabTPB, 0, st>>>(S, first ? 1 : 0, beta, parity & 1);
+    TL_CUDA(cudaGetLastError());
+    return TL_OK;
+}
+
+int32_t tl_slab_update(const tl_slab* s, double alpha, int32_t parity) {
+    tl::SlabParams S{};
+    int blocks = 0;
+    cudaStream_t st;
+    if (int rc = slab_params(s, S, blocks, st)) return rc;
+    tl::k_slab_update<<<blocks, tl::kSlabTPB, 0, st>>>(S, alpha, parity & 1);
+    TL_CUDA(cudaGetLastError());
+    return TL_OK;
+}
+
+int32_t tl_slab_residual(const tl_slab* s) {
+    tl::SlabParams S{};
+    int blocks = 0;
+    cudaStream_t st;
+    if (int rc = slab_params(s, S, blocks, st)) return rc;
+    tl::k_slab_residual<<<blocks, tl::kSlabTPB, 0, st>>>(S);
+    TL_CUDA(cudaGetLastError());
+    return TL_OK;
+}
+
+int32_t tl_slab_finish(const tl_slab* s) {
+    tl::SlabParams S{};
+    int blocks = 0;
+    cudaStream_t st;
+    if (int rc = slab_params(s, S, blocks, st)) return rc;
+    tl::k_slab_finish<<<blocks, tl::kSlabTPB, 0, st>>>(S);
     TL_CUDA(cudaGetLastError());
     return TL_OK;
 }

@@ -353,15 +353,17 @@ __device__ __forceinline__ void prefetch_l2(const double* a) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
 }
 
+// Nodes beg, beg+stride, ... < end; lim bounds the stored index range (prefetch only).
 __device__ __forceinline__ double stream_phase_a(const Grid& g, const ClassTable& T, int beg, int stride,
-                                                 const double* __restrict__ r, const double* __restrict__ pold,
-                                                 double* __restrict__ pnew, bool first, double beta) {
+                                                 int end, int lim, const double* __restrict__ r,
+                                                 const double* __restrict__ pold, double* __restrict__ pnew,
+                                                 bool first, double beta) {
     double pq = 0.0;
     int p = beg;
     const int sz = g.NX * g.NY;
-    for (; p + stride < g.n; p += 2 * stride) {
+    for (; p + stride < end; p += 2 * stride) {
         const int pf = p + kPfTrips * stride + sz;
-        if (pf < g.n) {
+        if (pf < lim) {
             prefetch_l2(r + pf);
             if (!first) prefetch_l2(pold + pf);
         }
@@ -373,7 +375,7 @@ __device__ __forceinline__ double stream_phase_a(const Grid& g, const ClassTable
         pq += pa * qa;
         pq += pb * qb;
     }
-    if (p < g.n) {
+    if (p < end) {
         double pa, qa;
         stream_a_node(g, T, p, r, pold, first, beta, pa, qa);
         pnew[p] = pa;
@@ -404,7 +406,7 @@ __device__ __forceinline__ void stream_b_node(const Grid& g, const ClassTable& T
 }
 
 __device__ __forceinline__ void stream_phase_b(const Grid& g, const ClassTable& T, int beg, int stride,
-                                               double* __restrict__ x, double* __restrict__ r,
+                                               int end, int lim, double* __restrict__ x, double* __restrict__ r,
                                                const double* __restrict__ pnew, double alpha, double& rz,
                                                double& rr) {
     auto finish = [&](int p, double pp, double qv, double iv) {
@@ -418,10 +420,10 @@ __device__ __forceinline__ void stream_phase_b(const Grid& g, const ClassTable& 
     };
     int p = beg;
     const int sz = g.NX * g.NY;
-    for (; p + stride < g.n; p += 2 * stride) {
+    for (; p + stride < end; p += 2 * stride) {
         const int pf = p + kPfTrips * stride;
-        if (pf + sz < g.n) prefetch_l2(pnew + pf + sz);
-        if (pf < g.n) {
+        if (pf + sz < lim) prefetch_l2(pnew + pf + sz);
+        if (pf < end) {
             prefetch_l2(x + pf);
             prefetch_l2(r + pf);
         }
@@ -431,7 +433,7 @@ __device__ __forceinline__ void stream_phase_b(const Grid& g, const ClassTable& 
         finish(p, pa, qa, ia);
         finish(p + stride, pb, qb, ib);
     }
-    if (p < g.n) {
+    if (p < end) {
         double pa, qa, ia;
         stream_b_node(g, T, p, pnew, pa, qa, ia);
         finish(p, pa, qa, ia);
@@ -534,7 +536,7 @@ __global__ void __launch_bounds__(kTPB, 2) k_pcg(PcgParams P) {
             //      so each iteration moves 64 B/node: r, p read + p written here, x, r, p
             //      read + x, r written in B).  Nodes two or more away from every face
             //      take the constant-coefficient path (their neighbours are interior too). ----
-            double pq[1] = {stream_phase_a(g, T, beg, stride, P.r, pold, pnew, first, beta)};
+            double pq[1] = {stream_phase_a(g, T, beg, stride, g.n, g.n, P.r, pold, pnew, first, beta)};
             block_sum<1>(pq, red);
             if (threadIdx.x == 0) P.part[2 * G + blockIdx.x] = pq[0];
             grid.sync();
@@ -545,7 +547,7 @@ __global__ void __launch_bounds__(kTPB, 2) k_pcg(PcgParams P) {
             const double alpha = rho / tot[0];
             // ---- phase B ----
             double a2[2] = {0.0, 0.0};
-            stream_phase_b(g, T, beg, stride, P.T, P.r, pnew, alpha, a2[0], a2[1]);
+            stream_phase_b(g, T, beg, stride, g.n, g.n, P.T, P.r, pnew, alpha, a2[0], a2[1]);
             block_sum<2>(a2, red);
             if (threadIdx.x == 0) { P.part[0 * G + blockIdx.x] = a2[0]; P.part[1 * G + blockIdx.x] = a2[1]; }
             grid.sync();

@@ -79,3 +79,69 @@ def test_gloo_two_ranks_shard_and_reduce():
         assert sorted(i for g in gathered for i in g) == list(range(64))
         assert tmax == 20.0
         assert total == sum(s.dof_timesteps for s in S.draw())
+
+
+# ---- z-slab decomposition of the global solve: host logic (partition, halos, sums) ----
+
+from paper_2110_12932_b200 import slab as SL  # noqa: E402
+
+
+@pytest.mark.parametrize("planes,world", [(41, 1), (41, 2), (41, 3), (201, 8), (8, 8)])
+def test_plane_partition_covers_and_balances(planes, world):
+    parts = SL.plane_partition(planes, world)
+    assert parts[0][0] == 0 and parts[-1][1] == planes
+    assert all(a[1] == b[0] for a, b in zip(parts, parts[1:]))
+    sizes = [k1 - k0 for k0, k1 in parts]
+    assert max(sizes) - min(sizes) <= 1 and min(sizes) >= 1
+    for r, (k0, k1) in enumerate(parts):
+        h0, h1 = SL.stored_planes(k0, k1, planes)
+        assert h0 == (k0 - 1 if r > 0 else 0) and h1 == (k1 + 1 if r < world - 1 else planes)
+
+
+def test_plane_partition_rejects_more_ranks_than_planes():
+    with pytest.raises(ValueError):
+        SL.plane_partition(4, 5)
+
+
+def _halo_worker(rank, world, port, q):
+    import numpy as np
+    import torch
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        nz, nxy = 11, 6
+        k0, k1 = SL.plane_partition(nz, world)[rank]
+        h0, h1 = SL.stored_planes(k0, k1, nz)
+        buf = torch.full(((h1 - h0) * nxy,), -1.0, dtype=torch.float64)
+        for k in range(k0, k1):   # own plane k holds 100 k + column index
+            buf[(k - h0) * nxy:(k - h0 + 1) * nxy] = 100.0 * k + torch.arange(nxy, dtype=torch.float64)
+        SL.HaloExchange(rank, world, k0, k1, h0, nxy).exchange(buf)
+        planes = buf.view(h1 - h0, nxy).numpy()
+        ok = all(np.array_equal(planes[k - h0], 100.0 * k + np.arange(nxy)) for k in range(h0, h1))
+        # rank-ordered sums: rank r contributes (r + 1) * [1e16, 1, -1e16, 0.5]
+        sums = torch.tensor([1e16, 1.0, -1e16, 0.5], dtype=torch.float64) * (rank + 1)
+        tot = SL.rank_sum(sums, world)
+        q.put((rank, ok, tot.tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_halo_exchange_and_rank_ordered_sums(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_halo_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok for _, ok, _ in out)
+    tots = [tot for _, _, tot in out]
+    assert all(t == tots[0] for t in tots)          # bitwise the same on every rank
+    expect = [0.0] * 4
+    for r in range(world):                            # the rank order is the summation order
+        expect = [e + v * (r + 1) for e, v in zip(expect, [1e16, 1.0, -1e16, 0.5])]
+    assert tots[0] == expect

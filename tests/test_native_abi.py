@@ -57,3 +57,27 @@ def test_no_cpu_fallback_when_library_missing(monkeypatch, tmp_path):
     with pytest.raises(N.NativeLibraryMissing):
         N.lib()
     monkeypatch.setattr(N, "_lib", None)
+
+
+def test_struct_layouts_match_c_compiler(tmp_path):
+    """sizeof / offsetof of every ABI struct as gcc lays them out == the ctypes mirror."""
+    structs = {"tl_solve_info": N.SolveInfo, "tl_grid_desc": N.GridDesc, "tl_gaussian": N.Gaussian,
+               "tl_run_desc": N.RunDesc, "tl_macro_plan": N.MacroPlan, "tl_micro_plan": N.MicroPlan,
+               "tl_slab": N.Slab}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{ROOT / "include" / "tlgpu.h"}"',
+             "int main(void) {"]
+    for cname, py in structs.items():
+        lines.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')
+        for fname, _ in py._fields_:
+            lines.append(f'printf("{cname} {fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines += ["return 0;", "}"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-o", str(exe), str(src)], check=True)
+    got = dict(l.rsplit(" ", 1) for l in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                         check=True).stdout.splitlines())
+    for cname, py in structs.items():
+        assert int(got[f"{cname} size"]) == ctypes.sizeof(py), cname
+        for fname, _ in py._fields_:
+            assert int(got[f"{cname} {fname}"]) == getattr(py, fname).offset, (cname, fname)
