@@ -198,6 +198,15 @@ int32_t tl_run_take_timing(tl_run* run, float* ms, int32_t* level, int32_t* nsol
 int32_t tl_debug_profile(uint64_t* out, int32_t max, int32_t* count);
 /* Write a scratch buffer larger than L2 on the run's stream (bench hygiene). */
 int32_t tl_run_flush_l2(tl_run* run);
+/* Multi-GPU: when on, tl_run_macro_steps skips the deposit and the global solve
+ * (the z-slab solve below does them across ranks) and runs only the local part of each
+ * macro step (trace, micro solves, corrector, relocation) against the global field
+ * placed with tl_run_put_global_planes (multirate.py:129-162 on the rank that holds
+ * the local problem). */
+int32_t tl_run_set_external_global(tl_run* run, int32_t on);
+/* Copy device planes [k0, k1) of the global field (plane k0 first) into the run
+ * (device-to-device on the run's stream; src must be ready when the call is made). */
+int32_t tl_run_put_global_planes(tl_run* run, const double* src, int32_t k0, int32_t k1);
 
 /* ---- multi-GPU: z-slab decomposition of the global solve ----------------
  * Replaces, per rank, the share of the global backward-Euler step
@@ -238,6 +247,11 @@ int32_t tl_slab_update(const tl_slab* s, double alpha, int32_t parity);
 int32_t tl_slab_residual(const tl_slab* s);
 /* Re-impose the Dirichlet values x_D = b_D (fem.py:289-290). */
 int32_t tl_slab_finish(const tl_slab* s);
+/* Swept-track deposit (SweptTrackDeposit.load, sources.py:164-172) into s->load on the
+ * rank's own nodes: the previous call's nodes are zeroed, the new samples scattered with
+ * Kuhn-P1 weights and merged in np.add.at order.  points (3 count) and power (count)
+ * are DEVICE arrays; count <= 512. */
+int32_t tl_slab_deposit(const tl_slab* s, const double* points, const double* power, int32_t count);
 
 #ifdef __cplusplus
 }

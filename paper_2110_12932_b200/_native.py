@@ -114,7 +114,10 @@ SIGNATURES = [
                                        C.POINTER(C.c_int32), C.c_int32, C.POINTER(C.c_int32)]),
     ("tl_run_flush_l2", C.c_int32, [_P]),
     ("tl_debug_profile", C.c_int32, [C.POINTER(C.c_uint64), C.c_int32, C.POINTER(C.c_int32)]),
+    ("tl_run_set_external_global", C.c_int32, [_P, C.c_int32]),
+    ("tl_run_put_global_planes", C.c_int32, [_P, C.c_void_p, C.c_int32, C.c_int32]),
     ("tl_slab_work_len", C.c_int64, []),
+    ("tl_slab_deposit", C.c_int32, [C.POINTER(Slab), C.c_void_p, C.c_void_p, C.c_int32]),
     ("tl_slab_rhs", C.c_int32, [C.POINTER(Slab), C.POINTER(Gaussian)]),
     ("tl_slab_direction", C.c_int32, [C.POINTER(Slab), C.c_int32, C.c_double, C.c_int32]),
     ("tl_slab_update", C.c_int32, [C.POINTER(Slab), C.c_double, C.c_int32]),

@@ -375,6 +375,7 @@ struct tl_run {
     std::vector<int> ev_nsolve;
     double* flush = nullptr; size_t flush_n = 0;
     int64_t launches = 0;
+    bool external_global = false;   // global field supplied by the slab solve (multi-GPU)
     bool timing = false;
     std::vector<cudaEvent_t> ev;     // pairs
     std::vector<int> ev_level;
@@ -541,7 +542,7 @@ int32_t tl_deposit_host(const tl_grid_desc* grid, const double* points, const do
         TL_CUDA(cudaMemcpy(dp, points, sizeof(double) * 3 * count, cudaMemcpyHostToDevice));
         TL_CUDA(cudaMemcpy(dw, power, sizeof(double) * count, cudaMemcpyHostToDevice));
     }
-    tl::k_deposit<<<1, 1024>>>(G, dp, dw, count, dl, prev, prevn);
+    tl::k_deposit<<<1, 1024>>>(G, dp, dw, count, dl, prev, prevn, 0, G.n);
     TL_CUDA(cudaGetLastError());
     TL_CUDA(cudaMemcpy(load_out, dl, sizeof(double) * G.n, cudaMemcpyDeviceToHost));
     cudaFree(dl); cudaFree(dp); cudaFree(dw); cudaFree(prev); cudaFree(prevn);
@@ -771,7 +772,7 @@ int32_t tl_run_macro_steps(tl_run* R, const tl_macro_plan* plans, int32_t nsteps
         if (mp.dep_count < 0 || mp.dep_offset < 0 || mp.dep_offset + mp.dep_count > ndep)
             return fail(TL_E_INVALID, "deposit plan out of range");
         if (mp.dep_count * 4 > tl::kDepMax) return fail(TL_E_INVALID, "too many deposit samples in one step");
-        need += 1 + mp.n_micro + mp.corrector;
+        need += (R->external_global ? 0 : 1) + mp.n_micro + mp.corrector;
     }
     if (int rc = ensure_info(R, need)) return rc;
     if (ndep > R->dep_cap) {
@@ -788,9 +789,10 @@ int32_t tl_run_macro_steps(tl_run* R, const tl_macro_plan* plans, int32_t nsteps
     for (int s = 0; s < nsteps; ++s) {
         const tl_macro_plan& mp = plans[s];
         // -- global predictor (twolevel.solve_global): deposit + implicit step --
+        if (!R->external_global) {
         tl::k_deposit<<<1, 1024, 0, R->stream>>>(R->G, R->dep_pts + 3 * (size_t)mp.dep_offset,
                                                  R->dep_pow + mp.dep_offset, mp.dep_count, R->loadg,
-                                                 R->dep_prev, R->dep_prev_n);
+                                                 R->dep_prev, R->dep_prev_n, 0, R->G.n);
         ++R->launches;
         TL_CUDA(cudaGetLastError());
         tl::PcgParams P{};
@@ -803,6 +805,7 @@ int32_t tl_run_macro_steps(tl_run* R, const tl_macro_plan* plans, int32_t nsteps
         if (int rc = timed_begin(R, 0)) return rc;
         if (int rc = launch_solve(P, false, R->sms, R->xg, R->stream, &R->launches, R->d_specs)) return rc;
         if (int rc = timed_end(R)) return rc;
+        }
         if (mp.record) {
             if (int rc = ensure_snapshots(R, mp.n_micro + mp.corrector)) return rc;
             TL_CUDA(cudaMemcpyAsync(R->snap_g, R->Tg, sizeof(double) * R->G.n, cudaMemcpyDeviceToDevice, R->stream));
@@ -975,6 +978,22 @@ int32_t tl_run_flush_l2(tl_run* R) {
     return TL_OK;
 }
 
+int32_t tl_run_set_external_global(tl_run* R, int32_t on) {
+    if (!R) return fail(TL_E_INVALID, "null run");
+    R->external_global = on != 0;
+    return TL_OK;
+}
+
+int32_t tl_run_put_global_planes(tl_run* R, const double* src, int32_t k0, int32_t k1) {
+    if (!R || !src) return fail(TL_E_INVALID, "null argument");
+    if (k0 < 0 || k1 > R->G.NZ || k0 >= k1) return fail(TL_E_INVALID, "bad plane range");
+    TL_CUDA(cudaSetDevice(R->device));
+    const size_t nxy = (size_t)R->G.NX * R->G.NY;
+    TL_CUDA(cudaMemcpyAsync(R->Tg + (size_t)k0 * nxy, src, sizeof(double) * nxy * (k1 - k0),
+                            cudaMemcpyDeviceToDevice, R->stream));
+    return TL_OK;
+}
+
 // ---- z-slab global solve (multi-GPU) ----------------------------------------------
 
 static int slab_params(const tl_slab* s, tl::SlabParams& S, int& blocks, cudaStream_t& st) {
@@ -1011,7 +1030,25 @@ static int slab_params(const tl_slab* s, tl::SlabParams& S, int& blocks, cudaStr
     return TL_OK;
 }
 
-int64_t tl_slab_work_len(void) { return 4 * (int64_t)tl::kResMaxBlocks + 1; }
+// work layout: [4 kResMaxBlocks partials][counter][deposit count][deposit nodes kDepMax ints]
+constexpr int64_t kSlabDepOff = 4 * (int64_t)tl::kResMaxBlocks + 1;
+int64_t tl_slab_work_len(void) { return kSlabDepOff + 1 + tl::kDepMax / 2; }
+
+int32_t tl_slab_deposit(const tl_slab* s, const double* points, const double* power, int32_t count) {
+    tl::SlabParams S{};
+    int blocks = 0;
+    cudaStream_t st;
+    if (int rc = slab_params(s, S, blocks, st)) return rc;
+    if (!s->load) return fail(TL_E_INVALID, "slab has no load array");
+    if (count < 0 || count * 4 > tl::kDepMax) return fail(TL_E_INVALID, "too many deposit samples");
+    if (count > 0 && (!points || !power)) return fail(TL_E_INVALID, "null deposit samples");
+    int* prev_n = reinterpret_cast<int*>(s->work + kSlabDepOff);
+    int* prev = reinterpret_cast<int*>(s->work + kSlabDepOff + 1);
+    tl::k_deposit<<<1, 1024, 0, st>>>(S.g, points, power, count, const_cast<double*>(S.load), prev, prev_n,
+                                      S.own_lo, S.own_hi);
+    TL_CUDA(cudaGetLastError());
+    return TL_OK;
+}
 
 int32_t tl_slab_rhs(const tl_slab* s, const tl_gaussian* src) {
     tl::SlabParams S{};

@@ -691,9 +691,12 @@ __global__ void k_interp_pts(Grid G, const double* __restrict__ v, const double*
 // ---------------------------------------------------------------------------------
 constexpr int kDepMax = 2048;   // contributions per call (samples * 4)
 
+// Only nodes in [lo, hi) are written (a slab's own nodes; 0..n for the whole grid);
+// load may be base-shifted so that load[id] addresses global node id.
 __global__ void __launch_bounds__(1024) k_deposit(Grid G, const double* __restrict__ pts,
                                                  const double* __restrict__ pw, int count,
-                                                 double* load, int* prev_nodes, int* prev_count) {
+                                                 double* load, int* prev_nodes, int* prev_count,
+                                                 int lo, int hi) {
     __shared__ int s_node[kDepMax];
     __shared__ double s_val[kDepMax];
     const int np = *prev_count;
@@ -736,7 +739,7 @@ __global__ void __launch_bounds__(1024) k_deposit(Grid G, const double* __restri
         bool first = true;
         for (int f = 0; f < e; ++f)
             if (s_node[f] == nd) { first = false; break; }
-        if (!first) continue;
+        if (!first || nd < lo || nd >= hi) continue;
         double sum = 0.0;
         for (int f = e; f < nc; ++f)
             if (s_node[f] == nd) sum += s_val[f];

@@ -109,3 +109,28 @@ def two_level_run(cfg, spacetime: bool | None = None, dt_macro: float | None = N
         state = run_space(problem, dt, n, lmesh, T0, path=c["path"] if moving else None,
                           policy=c["policy"], stats=stats, recorder=recorder)
     return state, stats
+
+
+def two_level_run_slabs(cfg, stats: RunStats | None = None, n_steps: int | None = None,
+                        device=None, group=None, resolve_corrector: bool = True):
+    """Multirate two-level run with the global grid z-slab-decomposed over the ranks of
+    the current process group (one process per GPU); see ``multirate_dist``.
+
+    Returns (state, stats) on the top rank and (None, stats) on the others."""
+    from .multirate_dist import run_spacetime_slabs
+    c = convert_config(cfg)
+    if c["mode"] == "two-level-space":
+        from .errors import UnsupportedOnDevice
+        raise UnsupportedOnDevice("slab decomposition implements the multirate (spacetime) mode")
+    if device is None:
+        import torch
+        device = torch.cuda.current_device()
+    problem, lmesh = build_problem(cfg, device=int(device), resolve_corrector=resolve_corrector)
+    stats = RunStats() if stats is None else stats
+    T0 = uniform_field(problem.global_mesh, c["T_initial"], time=0.0)
+    t_end = c["t_end"] if n_steps is None else n_steps * c["dt_macro"]
+    sched = MacroSchedule(c["dt_macro"], c["micro_steps"], 0.0, t_end)
+    moving = c["policy"] is not None
+    state = run_spacetime_slabs(problem, sched, lmesh, T0, path=c["path"] if moving else None,
+                                policy=c["policy"], stats=stats, group=group, device=f"cuda:{int(device)}")
+    return state, stats

@@ -267,22 +267,55 @@ class SlabGlobalSolver:
             status = 2
         return SlabInfo(self.maxiter if status == 1 else it, status, bnorm, rnorm, tres)
 
-    def gather_field(self) -> np.ndarray | None:
-        """Whole-grid field on rank 0 (None elsewhere): host copy for checks and output."""
+    def deposit(self, points, power) -> None:
+        """Swept-track deposit of one macro interval into ``load`` (own nodes only)."""
+        import torch
+        pts = torch.as_tensor(np.ascontiguousarray(points, dtype=np.float64).reshape(-1)).to(self.device)
+        pw = torch.as_tensor(np.ascontiguousarray(power, dtype=np.float64)).to(self.device)
+        s = self._desc(1.0, 0.0, True)
+        N.check(N.lib().tl_slab_deposit(C.byref(s), pts.data_ptr() if pw.numel() else None,
+                                        pw.data_ptr() if pw.numel() else None, int(pw.numel())),
+                "slab deposit")
+        self.launches += 1
+
+    def gather_planes(self, k_lo: int, root: int):
+        """Planes [k_lo, nz) of the solution on ``root`` as one device tensor (None elsewhere).
+
+        Used to hand the global sub-block under the local box to the rank that runs the
+        local problem (trace and relocation need only that block)."""
         import torch
         d = _dist()
-        if self.world == 1 or d is None:
-            return self.x[self.own_local].detach().cpu().numpy().copy()
-        dev = self.device if self.halo.nccl else torch.device("cpu")
-        own = self.x[self.own_local].detach().to(dev).contiguous()
         parts = plane_partition(self.nz, self.world)
-        if self.rank == 0:
-            out = [own]
-            for r in range(1, self.world):
-                k0, k1 = parts[r]
-                t = torch.empty((k1 - k0) * self.nxy, dtype=torch.float64, device=dev)
-                d.recv(t, r, group=self.group)
-                out.append(t)
-            return torch.cat(out).cpu().numpy()
-        d.send(own, 0, group=self.group)
+
+        def mine(r):
+            k0, k1 = parts[r]
+            return max(k0, k_lo), k1
+
+        if self.world == 1 or d is None:
+            a, b = mine(0)
+            return self.x[(a - self.h0) * self.nxy:(b - self.h0) * self.nxy]
+        dev = self.device if self.halo.nccl else torch.device("cpu")
+        if self.rank == root:
+            out = torch.empty((self.nz - k_lo) * self.nxy, dtype=torch.float64, device=self.device)
+            for r in range(self.world):
+                a, b = mine(r)
+                if a >= b:
+                    continue
+                dst = out[(a - k_lo) * self.nxy:(b - k_lo) * self.nxy]
+                if r == self.rank:
+                    dst.copy_(self.x[(a - self.h0) * self.nxy:(b - self.h0) * self.nxy])
+                else:
+                    t = torch.empty(dst.numel(), dtype=torch.float64, device=dev)
+                    d.recv(t, r, group=self.group)
+                    dst.copy_(t)
+            return out
+        a, b = mine(self.rank)
+        if a < b:
+            d.send(self.x[(a - self.h0) * self.nxy:(b - self.h0) * self.nxy].detach().to(dev).contiguous(),
+                   root, group=self.group)
         return None
+
+    def gather_field(self, root: int = 0) -> np.ndarray | None:
+        """Whole-grid field on ``root`` (None elsewhere): host copy for checks and output."""
+        t = self.gather_planes(0, root)
+        return None if t is None else t.detach().cpu().numpy().copy()
