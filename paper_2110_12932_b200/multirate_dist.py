@@ -58,6 +58,8 @@ class SlabRun:
             self.local = DeviceRun(problem, local_mesh)
             N.check(N.lib().tl_run_set_external_global(self.local._h, 1), "external global")
         self.global_infos: list = []
+        self.phase_ms: list = []       # (global ms, local ms) per step when timing is on
+        self.timing = False
 
     def close(self):
         if self.local is not None:
@@ -78,10 +80,15 @@ class SlabRun:
         mp = plan.macro[0]
         a, n = int(mp["dep_offset"]), int(mp["dep_count"])
         S = self.solver
+        if self.timing:
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            ev[0].record()
         S.deposit(plan.dep_points[a:a + n], plan.dep_power[a:a + n])
         info = S.step(float(mp["dt_global"]), self.problem.bc.T_buildplate, with_load=True)
         raise_for(info)
         self.global_infos.append(info)
+        if self.timing:
+            ev[1].record()
         k_lo = min(_first_plane_under(self.problem.global_mesh, StructuredGrid(p))
                    for p in (plan.placements[0], plan.placement_after[0]))
         block = S.gather_planes(k_lo, self.root)
@@ -92,6 +99,10 @@ class SlabRun:
             self.local.run(plan)
             infos = self.local.take_info()
             self.local.check_solves(infos)
+        if self.timing:
+            ev[2].record()
+            ev[2].synchronize()
+            self.phase_ms.append((ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2])))
 
 
 def run_spacetime_slabs(problem, schedule, local_mesh: StructuredGrid, T0: FieldState, path=None,

@@ -190,7 +190,7 @@ class SlabGlobalSolver:
     def set_own(self, tensor, values) -> None:
         """Copy this rank's share of a full-grid (host or device) array into ``tensor``."""
         import torch
-        v = torch.as_tensor(np.asarray(values)[self.own_ids] if isinstance(values, np.ndarray)
+        v = torch.as_tensor(np.array(values[self.own_ids]) if isinstance(values, np.ndarray)
                             else values[self.own_ids])
         tensor[self.own_local].copy_(v)
 
