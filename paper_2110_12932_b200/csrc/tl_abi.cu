@@ -207,7 +207,7 @@ static unsigned long long* prof_buffer() {
     if (want < 0) {
         const char* e = getenv("TLGPU_PROF");
         want = (e && e[0] == '1') ? 1 : 0;
-        if (want) cudaMalloc((void**)&g_prof, 512 * sizeof(unsigned long long));
+        if (want) cudaMalloc((void**)&g_prof, 1024 * sizeof(unsigned long long));
     }
     return g_prof;
 }
@@ -374,6 +374,8 @@ struct tl_run {
     std::vector<tl::SolveSpec> h_specs;
     std::vector<int> ev_nsolve;
     double* flush = nullptr; size_t flush_n = 0;
+    double* gload = nullptr; tl::Gauss* d_srcs = nullptr; int gload_cap = 0;   // multi-solve Gaussian loads
+    std::vector<tl::Gauss> h_srcs;
     int64_t launches = 0;
     bool external_global = false;   // global field supplied by the slab solve (multi-GPU)
     bool timing = false;
@@ -600,13 +602,14 @@ int32_t tl_run_destroy(tl_run* R) {
     if (R->stream) cudaStreamSynchronize(R->stream);
     double* bufs[] = {R->Tg, R->bg, R->rg, R->pg0, R->pg1, R->qg, R->loadg, R->Tl, R->bl, R->rl, R->pl0,
                       R->pl1, R->ql, R->tr_old, R->tr_pred, R->Tl_before, R->part, R->dep_pts,
-                      R->dep_pow, R->melt, R->melt_part, R->flush, R->xg};
+                      R->dep_pow, R->melt, R->melt_part, R->flush, R->xg, R->gload};
     for (double* b : bufs)
         if (b) cudaFree(b);
     if (R->dep_prev) cudaFree(R->dep_prev);
     if (R->dep_prev_n) cudaFree(R->dep_prev_n);
     if (R->info) cudaFree(R->info);
     if (R->d_specs) cudaFree(R->d_specs);
+    if (R->d_srcs) cudaFree(R->d_srcs);
     if (R->snap_g) cudaFree(R->snap_g);
     for (cudaEvent_t e : R->ev) cudaEventDestroy(e);
     for (double* b : R->snap_l) cudaFree(b);
@@ -711,6 +714,17 @@ static int local_multi(tl_run* R, const tl_macro_plan& mp, const tl_micro_plan* 
         R->specs_cap = ns + 1;
     }
     R->h_specs.assign(ns, tl::SolveSpec{});
+    R->h_srcs.assign(ns, tl::Gauss{});
+    if (R->gload_cap < ns) {
+        if (R->gload) cudaFree(R->gload);
+        if (R->d_srcs) cudaFree(R->d_srcs);
+        R->gload = nullptr;
+        R->d_srcs = nullptr;
+        if (int rc = dalloc(&R->gload, (size_t)ns * R->L.n)) return rc;
+        if (int rc = dalloc(&R->d_srcs, ns)) return rc;
+        R->gload_cap = ns;
+    }
+    bool any_src = false;
     const double V = R->L.h[0] * R->L.h[1] * R->L.h[2];
     for (int e = 0; e < ns; ++e) {
         const tl_micro_plan& up = micro[mp.micro_offset + e];
@@ -723,6 +737,11 @@ static int local_multi(tl_run* R, const tl_macro_plan& mp, const tl_micro_plan* 
         sp.src.depth = R->desc.beam_depth;
         for (int a = 0; a < 3; ++a) sp.src.center[a] = up.center[a];
         sp.src.on = up.source_on ? 1 : 0;
+        // the Gaussian is precomputed for all solves by k_gauss_loads (no in-kernel tables)
+        R->h_srcs[e] = sp.src;
+        sp.load = sp.src.on ? R->gload + (size_t)e * R->L.n : nullptr;
+        any_src = any_src || sp.src.on;
+        sp.src.on = 0;
         sp.tin = corr ? 2 : (e == 0 ? 0 : 1);
         sp.save_before = (mp.corrector && e == mp.n_micro - 1) ? 1 : 0;
         sp.tout = (e == ns - 1) ? 1 : 0;
@@ -735,6 +754,21 @@ static int local_multi(tl_run* R, const tl_macro_plan& mp, const tl_micro_plan* 
     }
     TL_CUDA(cudaMemcpyAsync(R->d_specs + 1, R->h_specs.data(), sizeof(tl::SolveSpec) * ns,
                             cudaMemcpyHostToDevice, R->stream));
+    if (any_src) {
+        TL_CUDA(cudaMemcpyAsync(R->d_srcs, R->h_srcs.data(), sizeof(tl::Gauss) * ns, cudaMemcpyHostToDevice,
+                                R->stream));
+        const size_t smem = gauss_smem(R->L);
+        static bool attr = false;
+        if (!attr && smem > 48 * 1024) {
+            cudaFuncSetAttribute(tl::k_gauss_loads, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            attr = true;
+        }
+        const dim3 grid((unsigned)std::max(1, (2 * R->sms + ns - 1) / ns), (unsigned)ns);
+        tl::k_gauss_loads<<<grid, 256, smem, R->stream>>>(R->L, R->d_specs + 1, R->d_srcs,
+                                                          0.5 * R->desc.T_buildplate, R->gload);
+        TL_CUDA(cudaGetLastError());
+        ++R->launches;
+    }
     tl::PcgParams P{};
     base_params(R, P, true, micro[mp.micro_offset].dt);
     P.T = R->Tl;
@@ -747,7 +781,7 @@ static int local_multi(tl_run* R, const tl_macro_plan& mp, const tl_micro_plan* 
     RP.nspec = ns;
     const int G = bp.ng[0] * bp.ng[1] * bp.ng[2];
     if (int rc = timed_begin(R, 1, ns)) return rc;
-    cudaError_t e = launch_rescg_g<true, true>(RP, bp.npt, G, bp.smem, R->stream);
+    cudaError_t e = launch_rescg_g<false, true>(RP, bp.npt, G, bp.smem, R->stream);
     if (e != cudaSuccess) return fail(TL_E_CUDA, std::string("k_pcg_resident_cg (multi) launch: ") + cudaGetErrorString(e));
     ++R->launches;
     return timed_end(R);
@@ -763,7 +797,7 @@ int32_t tl_run_macro_steps(tl_run* R, const tl_macro_plan* plans, int32_t nsteps
     // default: with the Gaussian evaluated in-kernel the persistent kernel needs more than
     // 128 registers and its CG loop spills (200 us vs 185 us per solve on cfg2).
     const char* mv = getenv("TLGPU_MULTI");
-    const bool multi = mv && mv[0] == '1' && cg_fits(R->L, true, R->sms, lbp);
+    const bool multi = mv && mv[0] == '1' && cg_fits(R->L, false, R->sms, lbp);
     int need = 0;
     for (int s = 0; s < nsteps; ++s) {
         const tl_macro_plan& mp = plans[s];
@@ -923,11 +957,11 @@ int32_t tl_debug_profile(uint64_t* out, int32_t max, int32_t* count) {
     if (!out || !count) return fail(TL_E_INVALID, "null argument");
     *count = 0;
     if (!g_prof) return TL_OK;
-    unsigned long long h[512];
+    unsigned long long h[1024];
     TL_CUDA(cudaDeviceSynchronize());
     TL_CUDA(cudaMemcpy(h, g_prof, sizeof(h), cudaMemcpyDeviceToHost));
     // slots [0, h[127]) phase stamps, 120..122 setup stamps, 127 = stamp count
-    const int n = std::min(max, 512);
+    const int n = std::min(max, 1024);
     for (int e = 0; e < n; ++e) out[e] = h[e];
     *count = n;
     return TL_OK;

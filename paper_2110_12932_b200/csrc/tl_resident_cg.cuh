@@ -38,6 +38,7 @@ struct SolveSpec {
     int tout;                     // 1: write the result to P.T
     SolveInfoDev* info;           // this solve's outcome record
     double* snap;                 // optional copy of the result (recorder snapshots), or nullptr
+    const double* load;           // this solve's dense load (precomputed Gaussian), or nullptr = P.load
 };
 
 struct ResCGParams {
@@ -74,6 +75,7 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
     const bool prof = RP.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
     int np = 0;
     if (prof) RP.prof[np++] = global_ns();
+    if (RP.prof && threadIdx.x == 0 && blockIdx.x < 256) RP.prof[768 + blockIdx.x] = global_ns();   // CTA start
 
     const int G = gridDim.x;
     const int b = blockIdx.x;
@@ -118,6 +120,7 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
         US[s] = 0.0;
     }
     __syncthreads();
+    if (prof) RP.prof[120] = global_ns();
     for (int e0 = threadIdx.x; e0 < nface; e0 += kResTPB) {
         int e = e0, u, v, w;
         if (e < 2 * fx) {
@@ -164,7 +167,9 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
 
   __shared__ SolveSpec S;                   // this solve's parameters (shared: no registers)
   const int nsp = MULTI ? RP.nspec : 1;
+  constexpr int kPS = MULTI ? 1 : 0;        // solve whose phases TLGPU_PROF stamps
   for (int si = 0; si < nsp; ++si) {
+    if (MULTI && prof && si == kPS) { np = 0; RP.prof[np++] = global_ns(); }
     __syncthreads();                        // previous solve done with T, PO, US, S
     if (threadIdx.x == 0) S = RP.specs[si];
     __syncthreads();
@@ -176,6 +181,7 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
         build_gauss_bounds(g, tx, ty, tz, bx_, by_, bz_);
         __syncthreads();
     }
+    if (prof && si == kPS) RP.prof[121] = global_ns();
     auto dvalue = [&](int q) -> double {    // Dirichlet value of this solve
         if (P.gA == nullptr) return P.g_const;
         return __dadd_rn(__dmul_rn(1.0 - S.w, P.gA[q]), __dmul_rn(S.w, P.gB[q]));
@@ -199,7 +205,8 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
             int i, j, k;
             decode(g, p, i, j, k);
             bv = T.mass[cls] * told;
-            if (P.load) bv += P.load[p];
+            const double* ld = S.load ? S.load : P.load;
+            if (ld) bv += ld[p];
             if (gauss) bv = add_gaussian(bv, g, tx, ty, tz, bx_, by_, bz_, i, j, k);
             const int sy = g.NX, sz = g.NX * g.NY;
             double lift = 0.0;
@@ -218,14 +225,16 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
         acc[0] += bv * bv;
         acc[1] += bv * z;
     }
+    if (prof && si == kPS) RP.prof[122] = global_ns();
     block_sum<2>(acc, red);
     if (threadIdx.x == 0) { P.part[0 * G + b] = acc[0]; P.part[1 * G + b] = acc[1]; }
+    if (RP.prof && si == kPS && threadIdx.x == 0 && b < 256) RP.prof[512 + b] = global_ns();   // RHS done
     grid.sync();
     {
         const int s2[2] = {0, 1};
         grid_sum_fast<2>(P.part, s2, G, tot);
     }
-    if (prof && si == 0) RP.prof[np++] = global_ns();
+    if (prof && si == kPS) RP.prof[np++] = global_ns();
     const double bb = tot[0];
     double gam = tot[1];                    // r0 . u0
     const double bnorm = sqrt(bb);
@@ -283,7 +292,7 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
             const double alpha = first ? gam / dlt : gam / (dlt - beta * gam / alpha_prev);
             // halo: s = w + beta s, r -= alpha s, u = M r  (w of the halo from the exchange)
 #define TL_STAMP(slot) \
-    if (prof && si == 0 && it == 3) RP.prof[slot] = global_ns();
+    if (prof && si == kPS && it == 3) RP.prof[slot] = global_ns();
             TL_STAMP(100)
             const double* win = RP.xw + (size_t)(it & 1) * g.n;
             double fw[kResKF];
@@ -350,7 +359,7 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
             block_sum<3>(d3, red);
             if (threadIdx.x == 0) { P.part[0 * G + b] = d3[0]; P.part[1 * G + b] = d3[1]; P.part[2 * G + b] = d3[2]; }
             TL_STAMP(104)
-            if (RP.prof && si == 0 && it == 3 && threadIdx.x == 0) RP.prof[256 + b] = global_ns();   // arrival per CTA
+            if (RP.prof && si == kPS && it == 3 && threadIdx.x == 0) RP.prof[256 + b] = global_ns();   // arrival per CTA
             grid.sync();
             TL_STAMP(105)
             {
@@ -359,7 +368,7 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
             }
             TL_STAMP(106)
 #undef TL_STAMP
-            if (prof && si == 0 && it < 100) RP.prof[np++] = global_ns();
+            if (prof && si == kPS && it < 100) RP.prof[np++] = global_ns();
             gam = tot[0];
             dlt = tot[1];
             rr = tot[2];
@@ -416,9 +425,46 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
         S.info->bnorm = bnorm;
         S.info->rnorm = rnorm;
         S.info->true_resid = tres;
-        if (prof && si == 0) { RP.prof[np++] = global_ns(); RP.prof[127] = np; }
+        if (prof && si == kPS) { RP.prof[np++] = global_ns(); RP.prof[127] = np; }
     }
   }
+}
+
+// ---------------------------------------------------------------------------------
+// Gaussian loads of all solves of a multi-solve launch, one dense array per solve
+// (loads + e n), computed by one launch before the solve so the persistent kernel
+// carries no Gaussian code (registers) and no beam-dependent work imbalance.  Values
+// are those add_gaussian evaluates in-kernel; the exact cutoff is taken against the
+// floor T_lo instead of the solve's own T_old: for T_old >= T_lo the RHS is bitwise the
+// same (a skipped term has F <= bound < 2^-55 m T_lo <= 2^-55 b0, which cannot change
+// the rounded b0 + F), and no T_old is needed, so all solves fit in one launch.
+// grid = (blocks per solve, solves).
+// ---------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_gauss_loads(Grid g, const SolveSpec* specs, const Gauss* srcs,
+                                                     double T_lo, double* loads) {
+    extern __shared__ double gtab[];
+    __shared__ double massc[27];
+    const int e = blockIdx.y;
+    double* out = loads + (size_t)e * g.n;
+    double *tx = gtab, *ty = tx + 6 * g.nc[0], *tz = ty + 6 * g.nc[1];
+    double *bx_ = tz + 6 * g.nc[2], *by_ = bx_ + g.NX, *bz_ = by_ + g.NY;
+    build_gauss_tables(g, srcs[e], tx, ty, tz);
+    if (threadIdx.x < 27) {
+        int n_p, n_e[3], cnt[3], h0[3], h1[3];
+        class_counts(threadIdx.x, n_p, n_e, cnt, h0, h1);
+        massc[threadIdx.x] = class_is_dirichlet(threadIdx.x, g.dkind) ? -1.0 : specs[e].mbase * (double)n_p;
+    }
+    __syncthreads();
+    build_gauss_bounds(g, tx, ty, tz, bx_, by_, bz_);
+    __syncthreads();
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < g.n; p += gridDim.x * blockDim.x) {
+        int i, j, k;
+        decode(g, p, i, j, k);
+        const double m = massc[class_of(g, i, j, k)];
+        if (m < 0.0) { out[p] = 0.0; continue; }
+        const double bound = 24.0 * bx_[i] * by_[j] * bz_[k];
+        out[p] = (bound < m * T_lo * 0x1p-55) ? 0.0 : gaussian_node_fast(g, tx, ty, tz, i, j, k);
+    }
 }
 
 }  // namespace tl

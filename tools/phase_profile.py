@@ -20,16 +20,23 @@ from paper_2110_12932_b200.schedule import plan_spacetime  # noqa: E402
 
 
 def stamps():
-    buf = (C.c_uint64 * 512)()
+    buf = (C.c_uint64 * 1024)()
     cnt = C.c_int32()
-    N.check(N.lib().tl_debug_profile(buf, 512, C.byref(cnt)))
+    N.check(N.lib().tl_debug_profile(buf, 1024, C.byref(cnt)))
     raw = np.array(buf[:cnt.value], dtype=np.float64)
     n = int(buf[127])
-    return raw[:n], raw[120:123], raw[100:107], raw[256:512], raw[140:151]
+    return raw[:n], raw[120:123], raw[100:107], raw[256:512], raw[140:151], raw[512:768], raw[768:1024]
 
 
 def report(tag, tt):
-    t, setup_marks, inner, arrive, ex = tt
+    t, setup_marks, inner, arrive, ex, rhs_done, cta_start = tt
+    ok = (cta_start > 0) & (rhs_done > 0)
+    if ok.any() and len(t) > 0:
+        st, rd = cta_start[ok], rhs_done[ok]
+        t0 = t[0]
+        print(f"  CTA start spread {(st.max() - st.min()) / 1e3:.2f} us; RHS-done (before barrier) from kernel "
+              f"start: min {(rd.min() - t0) / 1e3:.2f} median {(np.median(rd) - t0) / 1e3:.2f} "
+              f"max {(rd.max() - t0) / 1e3:.2f} us (slowest CTAs {list(np.nonzero(ok)[0][np.argsort(-rd)[:6]])})")
     if ex[0] > 0 and ex[10] > ex[0]:
         d = np.diff(ex) / 1e3
         names = ["A: halo r + p update", "A: syncthreads", "A: stencil", "A: block_sum", "A: grid.sync",
