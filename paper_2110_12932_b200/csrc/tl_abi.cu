@@ -18,6 +18,7 @@
 
 #include "../../include/tlgpu.h"
 #include "tl_resident_cg.cuh"
+#include "tl_stream.cuh"
 #include "tl_slab.cuh"
 
 namespace {
@@ -96,6 +97,57 @@ int launch_pcg(tl::PcgParams& P, bool gauss, int sms, cudaStream_t st, int64_t* 
     }
     if (e != cudaSuccess) return fail(TL_E_CUDA, std::string("k_pcg launch: ") + cudaGetErrorString(e));
     if (launches) ++*launches;
+    return TL_OK;
+}
+
+// ---- streaming PCG in four launches (tl_stream.cuh) ----------------------------------
+// Default for grids that do not fit on chip; TLGPU_SPLIT=0 restores the single cooperative
+// k_pcg.  TLGPU_SMINB picks the CG loop kernel's CTAs per SM and unroll: 2, 3, 4 (one
+// node per trip) or 22, 32 (two); default 32 (40 registers, 1536 threads per SM, measured
+// best on the cfg3 / cfg4 grids: profiles/README.md).
+static int split_minb() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("TLGPU_SPLIT");
+        const char* m = getenv("TLGPU_SMINB");
+        v = (e && e[0] == '0') ? 0 : (m ? atoi(m) : 32);
+        if (v != 0 && v != 2 && v != 3 && v != 4 && v != 22 && v != 32) v = 32;
+    }
+    return v;
+}
+
+template <int MINB, int UNR = 1>
+static cudaError_t launch_s_cg(tl::PcgParams& P, int Gr, int sms, cudaStream_t st) {
+    static thread_local int per_sm = 0;
+    if (per_sm == 0) {
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tl::k_s_cg<MINB, UNR>, tl::kSTPB, 0);
+        if (e != cudaSuccess) return e;
+        if (per_sm < 1) return cudaErrorCooperativeLaunchTooLarge;
+    }
+    const int G = per_sm * sms;
+    void* args[] = {&P, &Gr};
+    return cudaLaunchCooperativeKernel((void*)tl::k_s_cg<MINB, UNR>, G, tl::kSTPB, args, 0, st);
+}
+
+static int launch_stream(tl::PcgParams& P, int sms, cudaStream_t st, int64_t* launches) {
+    const int minb = split_minb();
+    if (minb == 0) return launch_pcg(P, false, sms, st, launches);
+    const int Gr = 4 * sms;
+    tl::k_s_rhs<<<Gr, tl::kSTPB, 0, st>>>(P);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess)
+        e = minb == 2 ? launch_s_cg<2>(P, Gr, sms, st)
+          : minb == 4 ? launch_s_cg<4>(P, Gr, sms, st)
+          : minb == 22 ? launch_s_cg<2, 2>(P, Gr, sms, st)
+          : minb == 32 ? launch_s_cg<3, 2>(P, Gr, sms, st)
+                       : launch_s_cg<3>(P, Gr, sms, st);
+    if (e == cudaSuccess) {
+        tl::k_s_resid<<<Gr, tl::kSTPB, 0, st>>>(P);
+        tl::k_s_final<<<Gr, tl::kSTPB, 0, st>>>(P, Gr);
+        e = cudaGetLastError();
+    }
+    if (e != cudaSuccess) return fail(TL_E_CUDA, std::string("streaming solve launch: ") + cudaGetErrorString(e));
+    if (launches) *launches += 4;
     return TL_OK;
 }
 
@@ -329,8 +381,9 @@ static int launch_solve(tl::PcgParams& P, bool gauss, int sms, double* xg, cudaS
         if (e != cudaSuccess) return fail(TL_E_CUDA, std::string("k_gauss_load: ") + cudaGetErrorString(e));
         if (launches) ++*launches;
         P.load = gl;
-        return launch_pcg(P, false, sms, st, launches);
+        return launch_stream(P, sms, st, launches);
     }
+    if (!gauss) return launch_stream(P, sms, st, launches);
     return launch_pcg(P, gauss, sms, st, launches);
 }
 

@@ -155,6 +155,22 @@ __device__ __forceinline__ double dirichlet_value(const PcgParams& P, int p) {
     return __dadd_rn(__dmul_rn(1.0 - P.w, P.gA[p]), __dmul_rn(P.w, P.gB[p]));
 }
 
+// Dirichlet lift of a free row (SparseSystem.constrained, fem.py:96-101):
+// -sum_{q in D} A_pq g_q with A_pq = -c_pq.
+__device__ __forceinline__ double dirichlet_lift(const PcgParams& P, const ClassTable& T, int p, int i, int j,
+                                                 int k, int cls) {
+    const Grid& g = P.g;
+    const int sy = g.NX, sz = g.NX * g.NY;
+    double lift = 0.0;
+    if (i > 0 && T.nd[cls - axis_class(i, g.nc[0]) + axis_class(i - 1, g.nc[0])] == 0.0) lift += T.c[0][cls] * dirichlet_value(P, p - 1);
+    if (i < g.nc[0] && T.nd[cls - axis_class(i, g.nc[0]) + axis_class(i + 1, g.nc[0])] == 0.0) lift += T.c[0][cls] * dirichlet_value(P, p + 1);
+    if (j > 0 && T.nd[cls + 3 * (axis_class(j - 1, g.nc[1]) - axis_class(j, g.nc[1]))] == 0.0) lift += T.c[1][cls] * dirichlet_value(P, p - sy);
+    if (j < g.nc[1] && T.nd[cls + 3 * (axis_class(j + 1, g.nc[1]) - axis_class(j, g.nc[1]))] == 0.0) lift += T.c[1][cls] * dirichlet_value(P, p + sy);
+    if (k > 0 && T.nd[cls + 9 * (axis_class(k - 1, g.nc[2]) - axis_class(k, g.nc[2]))] == 0.0) lift += T.c[2][cls] * dirichlet_value(P, p - sz);
+    if (k < g.nc[2] && T.nd[cls + 9 * (axis_class(k + 1, g.nc[2]) - axis_class(k, g.nc[2]))] == 0.0) lift += T.c[2][cls] * dirichlet_value(P, p + sz);
+    return lift;
+}
+
 // Gaussian nodal load: sum over incident Kuhn tets of
 // (V/24) * (b * S_tet + (a - b) * Q_own), Q = peak * Ex * Ey * Ez from per-axis tables
 // tab[axis][cell * 6 + offset] (peak and V/24 folded into the z table).
@@ -487,16 +503,7 @@ __global__ void __launch_bounds__(kTPB, 2) k_pcg(PcgParams P) {
             bv = T.mass[cls] * P.T[p];
             if (P.load) bv += P.load[p];
             if (GAUSS) bv = add_gaussian(bv, g, tx, ty, tz, bx_, by_, bz_, i, j, k);
-            // lift: b_p -= sum_{q in D} A_pq g_q,  A_pq = -c_pq
-            const int sy = g.NX, sz = g.NX * g.NY;
-            double lift = 0.0;
-            if (i > 0 && T.nd[cls - axis_class(i, g.nc[0]) + axis_class(i - 1, g.nc[0])] == 0.0) lift += T.c[0][cls] * dirichlet_value(P, p - 1);
-            if (i < g.nc[0] && T.nd[cls - axis_class(i, g.nc[0]) + axis_class(i + 1, g.nc[0])] == 0.0) lift += T.c[0][cls] * dirichlet_value(P, p + 1);
-            if (j > 0 && T.nd[cls + 3 * (axis_class(j - 1, g.nc[1]) - axis_class(j, g.nc[1]))] == 0.0) lift += T.c[1][cls] * dirichlet_value(P, p - sy);
-            if (j < g.nc[1] && T.nd[cls + 3 * (axis_class(j + 1, g.nc[1]) - axis_class(j, g.nc[1]))] == 0.0) lift += T.c[1][cls] * dirichlet_value(P, p + sy);
-            if (k > 0 && T.nd[cls + 9 * (axis_class(k - 1, g.nc[2]) - axis_class(k, g.nc[2]))] == 0.0) lift += T.c[2][cls] * dirichlet_value(P, p - sz);
-            if (k < g.nc[2] && T.nd[cls + 9 * (axis_class(k + 1, g.nc[2]) - axis_class(k, g.nc[2]))] == 0.0) lift += T.c[2][cls] * dirichlet_value(P, p + sz);
-            bv += lift;
+            bv += dirichlet_lift(P, T, p, i, j, k, cls);
         }
         P.b[p] = bv;
         P.r[p] = bv;
