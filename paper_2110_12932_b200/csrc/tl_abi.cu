@@ -317,8 +317,66 @@ static bool cg_fits(const tl::Grid& g, bool gauss, int sms, BrickPlan& bp) {
     return bp.ok;
 }
 
+// Per-grid cache of the resident CG-CG kernel's static setup (tl_resident_cg.cuh) and its
+// tail counter; owned by a tl_run (one per level).
+struct ResCache {
+    int* buf = nullptr;
+    size_t cap = 0;              // ints
+    unsigned* counter = nullptr;
+    int key[7] = {0, 0, 0, 0, 0, 0, 0};   // grid cells + brick split + npt of the stored setup
+    bool ready = false;
+    void release() {
+        if (buf) cudaFree(buf);
+        if (counter) cudaFree(counter);
+        buf = nullptr;
+        counter = nullptr;
+        cap = 0;
+        ready = false;
+    }
+};
+
+// Sets RP.scache / sc_mode / tail_count from the cache (allocating it on first use).
+static int attach_cache(ResCache* rc, tl::ResCGParams& RP, const tl::Grid& g, const BrickPlan& bp) {
+    if (!rc) return TL_OK;
+    if (!rc->counter) {
+        TL_CUDA(cudaMalloc((void**)&rc->counter, sizeof(unsigned)));
+        TL_CUDA(cudaMemset(rc->counter, 0, sizeof(unsigned)));
+    }
+    RP.tail_count = rc->counter;
+    long long stride = 0;
+    for (int bz = 0; bz < bp.ng[2]; ++bz)
+        for (int by = 0; by < bp.ng[1]; ++by)
+            for (int bx = 0; bx < bp.ng[0]; ++bx) {
+                const int lx = RP.off[0][bx + 1] - RP.off[0][bx], ly = RP.off[1][by + 1] - RP.off[1][by];
+                const int lz = RP.off[2][bz + 1] - RP.off[2][bz];
+                const long long H = (long long)(lx + 2) * (ly + 2) * (lz + 2);
+                const long long nf = 2LL * (ly * lz + lx * lz + lx * ly);
+                const long long need = (H + 3) / 4 + 2 * nf + (long long)lx * ly * lz + (long long)bp.npt * tl::kResTPB;
+                stride = std::max(stride, need);
+            }
+    const int G = bp.ng[0] * bp.ng[1] * bp.ng[2];
+    const int key[7] = {g.nc[0], g.nc[1], g.nc[2], bp.ng[0], bp.ng[1], bp.ng[2], bp.npt};
+    const size_t want = (size_t)stride * G;
+    if (want > rc->cap) {
+        if (rc->buf) cudaFree(rc->buf);
+        rc->buf = nullptr;
+        TL_CUDA(cudaMalloc((void**)&rc->buf, want * sizeof(int)));
+        rc->cap = want;
+        rc->ready = false;
+    }
+    if (!std::equal(key, key + 7, rc->key)) {
+        std::copy(key, key + 7, rc->key);
+        rc->ready = false;
+    }
+    RP.scache = rc->buf;
+    RP.sc_stride = stride;
+    RP.sc_mode = rc->ready ? 2 : 1;
+    return TL_OK;
+}
+
 static int launch_solve(tl::PcgParams& P, bool gauss, int sms, double* xg, cudaStream_t st,
-                        int64_t* launches, tl::SolveSpec* dspec = nullptr, int* kind_out = nullptr) {
+                        int64_t* launches, tl::SolveSpec* dspec = nullptr, int* kind_out = nullptr,
+                        ResCache* cache = nullptr) {
     BrickPlan bp;
     if (xg && dspec && cg_fits(P.g, gauss, sms, bp)) {
         {
@@ -332,17 +390,20 @@ static int launch_solve(tl::PcgParams& P, bool gauss, int sms, double* xg, cudaS
             hs.tout = 1;
             hs.info = P.info;
             hs.snap = nullptr;
-            TL_CUDA(cudaMemcpyAsync(dspec, &hs, sizeof(hs), cudaMemcpyHostToDevice, st));
             tl::ResCGParams RP{};
             fill_rescg(RP, P, xg, bp);
-            RP.specs = dspec;
+            RP.specs = nullptr;          // the spec travels in the kernel parameters
+            RP.spec0 = hs;
             RP.nspec = 1;
+            if (getenv("TLGPU_NOCACHE") == nullptr)
+                if (int rc = attach_cache(cache, RP, P.g, bp)) return rc;
             const int G = bp.ng[0] * bp.ng[1] * bp.ng[2];
             cudaError_t e = gauss ? launch_rescg_g<true>(RP, bp.npt, G, bp.smem, st)
                                   : launch_rescg_g<false>(RP, bp.npt, G, bp.smem, st);
             if (e != cudaSuccess) return fail(TL_E_CUDA, std::string("k_pcg_resident_cg launch: ") + cudaGetErrorString(e));
             if (launches) ++*launches;
             if (kind_out) *kind_out = 2;
+            if (RP.scache) cache->ready = true;
             return TL_OK;
         }
     }
@@ -424,6 +485,7 @@ struct tl_run {
     double* snap_g = nullptr; std::vector<double*> snap_l; int snap_n = 0;
     double* xg = nullptr;            // exchange array of the resident kernels (4 n)
     tl::SolveSpec* d_specs = nullptr; int specs_cap = 0;
+    ResCache cache_g, cache_l;       // resident-kernel setup caches (global / local grid)
     std::vector<tl::SolveSpec> h_specs;
     std::vector<int> ev_nsolve;
     double* flush = nullptr; size_t flush_n = 0;
@@ -667,6 +729,8 @@ int32_t tl_run_destroy(tl_run* R) {
     for (cudaEvent_t e : R->ev) cudaEventDestroy(e);
     for (double* b : R->snap_l) cudaFree(b);
     if (R->melt_host) cudaFreeHost(R->melt_host);
+    R->cache_g.release();
+    R->cache_l.release();
     if (R->stream) cudaStreamDestroy(R->stream);
     delete R;
     return TL_OK;
@@ -736,7 +800,7 @@ static int ensure_snapshots(tl_run* R, int nl) {
     return TL_OK;
 }
 
-static int local_solve(tl_run* R, double* T, const tl_micro_plan& mp) {
+static int local_solve(tl_run* R, double* T, const tl_micro_plan& mp, const double* gload = nullptr) {
     tl::PcgParams P{};
     base_params(R, P, true, mp.dt);
     P.T = T;
@@ -745,6 +809,10 @@ static int local_solve(tl_run* R, double* T, const tl_micro_plan& mp) {
     P.w = mp.w;
     P.load = nullptr;
     bool gauss = mp.source_on != 0;
+    if (gauss && gload) {
+        P.load = gload;              // precomputed by gauss_loads_for_step
+        gauss = false;
+    }
     if (gauss) {
         P.src.peak = R->desc.beam_peak; P.src.radius = R->desc.beam_radius; P.src.depth = R->desc.beam_depth;
         for (int a = 0; a < 3; ++a) P.src.center[a] = mp.center[a];
@@ -752,8 +820,71 @@ static int local_solve(tl_run* R, double* T, const tl_micro_plan& mp) {
     }
     P.info = R->info + R->info_n++;
     if (int rc = timed_begin(R, 1)) return rc;
-    if (int rc = launch_solve(P, gauss, R->sms, R->xg, R->stream, &R->launches, R->d_specs)) return rc;
+    if (int rc = launch_solve(P, gauss, R->sms, R->xg, R->stream, &R->launches, R->d_specs, nullptr, &R->cache_l))
+        return rc;
     return timed_end(R);
+}
+
+// Gaussian loads of every local solve of macro step mp (the micro steps, then the
+// corrector) by one k_gauss_loads launch spread over the whole GPU, so the resident solves
+// read a dense load instead of evaluating the 96-term Gaussian in the CTAs under the beam
+// (which finished their RHS up to 8 us after the others).  The exact cutoff is taken
+// against the floor T_buildplate / 2 instead of each solve's T_old: a skipped term has
+// F < 2^-55 m T_lo, below half an ulp of b0 = m T_old whenever T_old >= T_lo / 2, so the
+// RHS is bitwise the one the in-kernel evaluation gives.  loads[e] = nullptr: source off.
+static int gauss_loads_for_step(tl_run* R, const tl_macro_plan& mp, const tl_micro_plan* micro,
+                                std::vector<double*>& loads) {
+    const int ns = mp.n_micro + (mp.corrector ? 1 : 0);
+    if (R->specs_cap < ns + 1) {
+        if (R->d_specs) cudaFree(R->d_specs);
+        R->d_specs = nullptr;
+        if (int rc = dalloc(&R->d_specs, ns + 1)) return rc;
+        R->specs_cap = ns + 1;
+    }
+    if (R->gload_cap < ns) {
+        if (R->gload) cudaFree(R->gload);
+        if (R->d_srcs) cudaFree(R->d_srcs);
+        R->gload = nullptr;
+        R->d_srcs = nullptr;
+        if (int rc = dalloc(&R->gload, (size_t)ns * R->L.n)) return rc;
+        if (int rc = dalloc(&R->d_srcs, ns)) return rc;
+        R->gload_cap = ns;
+    }
+    R->h_specs.assign(ns, tl::SolveSpec{});
+    R->h_srcs.assign(ns, tl::Gauss{});
+    loads.assign(ns, nullptr);
+    bool any_src = false;
+    const double V = R->L.h[0] * R->L.h[1] * R->L.h[2];
+    for (int e = 0; e < ns; ++e) {
+        const tl_micro_plan& up = micro[mp.micro_offset + e];
+        tl::SolveSpec& sp = R->h_specs[e];
+        sp.mbase = (R->desc.rho_c_local / up.dt) * V / 24.0;      // set_coeffs
+        tl::Gauss& src = R->h_srcs[e];
+        src.peak = R->desc.beam_peak;
+        src.radius = R->desc.beam_radius;
+        src.depth = R->desc.beam_depth;
+        for (int a = 0; a < 3; ++a) src.center[a] = up.center[a];
+        src.on = up.source_on ? 1 : 0;
+        if (src.on) loads[e] = R->gload + (size_t)e * R->L.n;
+        any_src = any_src || src.on;
+    }
+    if (!any_src) return TL_OK;
+    TL_CUDA(cudaMemcpyAsync(R->d_specs + 1, R->h_specs.data(), sizeof(tl::SolveSpec) * ns,
+                            cudaMemcpyHostToDevice, R->stream));
+    TL_CUDA(cudaMemcpyAsync(R->d_srcs, R->h_srcs.data(), sizeof(tl::Gauss) * ns, cudaMemcpyHostToDevice,
+                            R->stream));
+    const size_t smem = gauss_smem(R->L);
+    static bool attr = false;
+    if (!attr && smem > 48 * 1024) {
+        cudaFuncSetAttribute(tl::k_gauss_loads, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    const dim3 grid((unsigned)std::max(1, (4 * R->sms + ns - 1) / ns), (unsigned)ns);
+    tl::k_gauss_loads<<<grid, 256, smem, R->stream>>>(R->L, R->d_specs + 1, R->d_srcs,
+                                                      0.5 * R->desc.T_buildplate, R->gload);
+    TL_CUDA(cudaGetLastError());
+    ++R->launches;
+    return TL_OK;
 }
 
 // All micro solves of one macro step (+ the corrector) as one k_pcg_resident_cg launch.
@@ -851,6 +982,11 @@ int32_t tl_run_macro_steps(tl_run* R, const tl_macro_plan* plans, int32_t nsteps
     // 128 registers and its CG loop spills (200 us vs 185 us per solve on cfg2).
     const char* mv = getenv("TLGPU_MULTI");
     const bool multi = mv && mv[0] == '1' && cg_fits(R->L, false, R->sms, lbp);
+    // Gaussian loads precomputed per macro step for the resident CG-CG local solve
+    // (TLGPU_PREGAUSS=0: evaluated inside each solve instead)
+    const char* pg = getenv("TLGPU_PREGAUSS");
+    BrickPlan gbp;
+    const bool pre_gauss = !(pg && pg[0] == '0') && cg_fits(R->L, true, R->sms, gbp);
     int need = 0;
     for (int s = 0; s < nsteps; ++s) {
         const tl_macro_plan& mp = plans[s];
@@ -890,7 +1026,9 @@ int32_t tl_run_macro_steps(tl_run* R, const tl_macro_plan* plans, int32_t nsteps
         P.load = R->loadg;
         P.info = R->info + R->info_n++;
         if (int rc = timed_begin(R, 0)) return rc;
-        if (int rc = launch_solve(P, false, R->sms, R->xg, R->stream, &R->launches, R->d_specs)) return rc;
+        if (int rc = launch_solve(P, false, R->sms, R->xg, R->stream, &R->launches, R->d_specs, nullptr,
+                                  &R->cache_g))
+            return rc;
         if (int rc = timed_end(R)) return rc;
         }
         if (mp.record) {
@@ -901,6 +1039,10 @@ int32_t tl_run_macro_steps(tl_run* R, const tl_macro_plan* plans, int32_t nsteps
         // -- trace of the predicted global field on gamma --
         if (int rc = run_interp_local(R, 1, nullptr, R->tr_pred)) return rc;
         // -- micro steps (+ corrector): one persistent launch when the local grid fits --
+        std::vector<double*> gl;
+        if (!multi && pre_gauss)
+            if (int rc = gauss_loads_for_step(R, mp, micro, gl)) return rc;
+        auto gload_of = [&](int e) -> const double* { return e < (int)gl.size() ? gl[e] : nullptr; };
         if (multi) {
             if (int rc = local_multi(R, mp, micro, lbp)) return rc;
         } else
@@ -910,13 +1052,14 @@ int32_t tl_run_macro_steps(tl_run* R, const tl_macro_plan* plans, int32_t nsteps
                 tl::k_copy<<<4 * R->sms, 256, 0, R->stream>>>(R->Tl, R->Tl_before, R->L.n);
                 ++R->launches;
             }
-            if (int rc = local_solve(R, R->Tl, up)) return rc;
+            if (int rc = local_solve(R, R->Tl, up, gload_of(i))) return rc;
             if (mp.record)
                 TL_CUDA(cudaMemcpyAsync(R->snap_l[i], R->Tl, sizeof(double) * R->L.n, cudaMemcpyDeviceToDevice, R->stream));
         }
         if (mp.corrector && !multi) {
             // corrector: re-solve the last micro interval from before_final with trace_pred
-            if (int rc = local_solve(R, R->Tl_before, micro[mp.micro_offset + mp.n_micro])) return rc;
+            if (int rc = local_solve(R, R->Tl_before, micro[mp.micro_offset + mp.n_micro], gload_of(mp.n_micro)))
+                return rc;
             std::swap(R->Tl, R->Tl_before);
             if (mp.record)
                 TL_CUDA(cudaMemcpyAsync(R->snap_l[mp.n_micro], R->Tl, sizeof(double) * R->L.n, cudaMemcpyDeviceToDevice, R->stream));

@@ -46,11 +46,21 @@ struct ResCGParams {
     double* xr;                   // exchange: brick-surface r0 / final x, n doubles
     double* xw;                   // exchange: brick-surface w, 2 n doubles (ping-pong)
     double* saved;                // n doubles: T_old saved for the corrector
-    const SolveSpec* specs;       // nspec solves run back to back in one launch
-    int nspec;
+    const SolveSpec* specs;       // nspec solves run back to back in one launch, or nullptr:
+    int nspec;                    // one solve described by spec0 (kernel parameter, no copy)
+    SolveSpec spec0;
     unsigned long long* prof;
     int ng[3];
     int off[3][kResMaxSplit + 1];
+    // static per-CTA setup (node classes, halo face lists, node descriptors) cached in
+    // global memory across solves of one grid: sc_mode 0 = compute, 1 = compute and store,
+    // 2 = load (the setup depends only on the grid shape and the brick plan)
+    int* scache;
+    long long sc_stride;
+    int sc_mode;
+    // !MULTI: the residual partials are reduced by the last CTA to finish (no second grid
+    // barrier at the end of the solve); counter zero between launches
+    unsigned* tail_count;
 };
 
 __host__ __device__ inline size_t rescg_smem_bytes(int lx, int ly, int lz, int gtab) {
@@ -111,33 +121,52 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
     int* FG = FS + nface;
     uint8_t* CL = reinterpret_cast<uint8_t*>(FG + nface);
 
-    build_class_table(T, threadIdx.x, RP.specs[0].mbase, P.cbase, g.dkind);
-    for (int s = threadIdx.x; s < H; s += kResTPB) {
-        const int u = s % LX, v = (s / LX) % LY, w = s / SZ;
-        const int i = x0 + u - 1, j = y0 + v - 1, k = z0 + w - 1;
-        const bool in = i >= 0 && i <= g.nc[0] && j >= 0 && j <= g.nc[1] && k >= 0 && k <= g.nc[2];
-        CL[s] = in ? (uint8_t)class_of(g, i, j, k) : kNoNode;
-        US[s] = 0.0;
+    const int sc = RP.scache ? RP.sc_mode : 0;
+    int* SCb = RP.scache ? RP.scache + (size_t)b * RP.sc_stride : nullptr;
+    const int nclw = (H + 3) / 4, oFS = nclw, oFG = oFS + nface, oGID = oFG + nface, oOD = oGID + nown;
+    build_class_table(T, threadIdx.x, RP.specs ? RP.specs[0].mbase : RP.spec0.mbase, P.cbase, g.dkind);
+    if (sc == 2) {
+        for (int s = threadIdx.x; s < nclw; s += kResTPB) reinterpret_cast<int*>(CL)[s] = __ldcg(SCb + s);
+        for (int s = threadIdx.x; s < H; s += kResTPB) US[s] = 0.0;
+    } else {
+        for (int s = threadIdx.x; s < H; s += kResTPB) {
+            const int u = s % LX, v = (s / LX) % LY, w = s / SZ;
+            const int i = x0 + u - 1, j = y0 + v - 1, k = z0 + w - 1;
+            const bool in = i >= 0 && i <= g.nc[0] && j >= 0 && j <= g.nc[1] && k >= 0 && k <= g.nc[2];
+            CL[s] = in ? (uint8_t)class_of(g, i, j, k) : kNoNode;
+            US[s] = 0.0;
+        }
     }
     __syncthreads();
+    if (sc == 1)
+        for (int s = threadIdx.x; s < nclw; s += kResTPB) SCb[s] = reinterpret_cast<const int*>(CL)[s];
     if (prof) RP.prof[120] = global_ns();
     for (int e0 = threadIdx.x; e0 < nface; e0 += kResTPB) {
-        int e = e0, u, v, w;
-        if (e < 2 * fx) {
-            const int side = e / fx, r = e % fx;
-            u = side ? LX - 1 : 0; v = r % ly + 1; w = r / ly + 1;
-        } else if ((e -= 2 * fx) < 2 * fy) {
-            const int side = e / fy, r = e % fy;
-            v = side ? LY - 1 : 0; u = r % lx + 1; w = r / lx + 1;
+        if (sc == 2) {
+            FS[e0] = __ldcg(SCb + oFS + e0);
+            FG[e0] = __ldcg(SCb + oFG + e0);
         } else {
-            e -= 2 * fy;
-            const int side = e / fz, r = e % fz;
-            w = side ? LZ - 1 : 0; u = r % lx + 1; v = r / lx + 1;
+            int e = e0, u, v, w;
+            if (e < 2 * fx) {
+                const int side = e / fx, r = e % fx;
+                u = side ? LX - 1 : 0; v = r % ly + 1; w = r / ly + 1;
+            } else if ((e -= 2 * fx) < 2 * fy) {
+                const int side = e / fy, r = e % fy;
+                v = side ? LY - 1 : 0; u = r % lx + 1; w = r / lx + 1;
+            } else {
+                e -= 2 * fy;
+                const int side = e / fz, r = e % fz;
+                w = side ? LZ - 1 : 0; u = r % lx + 1; v = r / lx + 1;
+            }
+            const int s = u + SY * v + SZ * w;
+            const bool in = CL[s] != kNoNode;
+            FS[e0] = in ? s : -1;
+            FG[e0] = in ? (x0 + u - 1) + g.NX * ((y0 + v - 1) + g.NY * (z0 + w - 1)) : 0;
+            if (sc == 1) {
+                SCb[oFS + e0] = FS[e0];
+                SCb[oFG + e0] = FG[e0];
+            }
         }
-        const int s = u + SY * v + SZ * w;
-        const bool in = CL[s] != kNoNode;
-        FS[e0] = in ? s : -1;
-        FG[e0] = in ? (x0 + u - 1) + g.NX * ((y0 + v - 1) + g.NY * (z0 + w - 1)) : 0;
         RF[e0] = 0.0;
         SF[e0] = 0.0;
     }
@@ -145,6 +174,15 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
 #pragma unroll
     for (int m = 0; m < NPT; ++m) {
         const int nl = threadIdx.x + m * kResTPB;
+        if (sc == 2) {
+            od[m] = __ldcg(SCb + oOD + nl);
+            if (nl < nown) {
+                GID[nl] = __ldcg(SCb + oGID + nl);
+                SO[nl] = 0.0;
+                XO[nl] = 0.0;
+            }
+            continue;
+        }
         od[m] = -1;
         if (nl < nown) {
             const int u = nl % lx + 1, v = (nl / lx) % ly + 1, w = nl / (lx * ly) + 1;
@@ -162,7 +200,9 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
             GID[nl] = (x0 + u - 1) + g.NX * ((y0 + v - 1) + g.NY * (z0 + w - 1));
             SO[nl] = 0.0;
             XO[nl] = 0.0;
+            if (sc == 1) SCb[oGID + nl] = GID[nl];
         }
+        if (sc == 1) SCb[oOD + nl] = od[m];
     }
 
   __shared__ SolveSpec S;                   // this solve's parameters (shared: no registers)
@@ -171,7 +211,7 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
   for (int si = 0; si < nsp; ++si) {
     if (MULTI && prof && si == kPS) { np = 0; RP.prof[np++] = global_ns(); }
     __syncthreads();                        // previous solve done with T, PO, US, S
-    if (threadIdx.x == 0) S = RP.specs[si];
+    if (threadIdx.x == 0) S = RP.specs ? RP.specs[si] : RP.spec0;
     __syncthreads();
     const bool gauss = GAUSS && S.src.on;
     build_class_table(T, threadIdx.x, S.mbase, P.cbase, g.dkind);
@@ -410,13 +450,34 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
         if (MULTI && S.snap) S.snap[p] = xv;
     }
     block_sum<2>(res, red);
-    if (threadIdx.x == 0) { P.part[0 * G + b] = res[0]; P.part[3 * G + b] = res[1]; }
-    grid.sync();
+    bool fin = b == 0;                      // the CTA that writes the outcome record
+    if (!MULTI && RP.tail_count) {
+        // single solve: the last CTA to finish reduces the residual partials; the others
+        // exit without a second grid barrier
+        __shared__ bool s_last;
+        if (threadIdx.x == 0) {
+            P.part[0 * G + b] = res[0];
+            P.part[3 * G + b] = res[1];
+            __threadfence();
+            s_last = atomicAdd(RP.tail_count, 1u) == (unsigned)G - 1;
+        }
+        __syncthreads();
+        if (!s_last) {
+            if (prof && si == kPS) { RP.prof[np++] = global_ns(); RP.prof[127] = np; }
+            continue;
+        }
+        __threadfence();
+        fin = true;
+        if (threadIdx.x == 0) *RP.tail_count = 0;
+    } else {
+        if (threadIdx.x == 0) { P.part[0 * G + b] = res[0]; P.part[3 * G + b] = res[1]; }
+        grid.sync();
+    }
     {
         const int s2[2] = {0, 3};
         grid_sum_fast<2>(P.part, s2, G, tot);
     }
-    if (b == 0 && threadIdx.x == 0) {
+    if (fin && threadIdx.x == 0) {
         const double tres = bnorm > 0.0 ? sqrt(tot[0]) / bnorm : 0.0;
         if (status == 0 && tot[1] > 0.0) status = 3;
         if (status == 0 && (!isfinite(tres) || tres > 1e2 * P.rtol)) status = 2;
