@@ -339,10 +339,13 @@ struct ResCache {
 static int attach_cache(ResCache* rc, tl::ResCGParams& RP, const tl::Grid& g, const BrickPlan& bp) {
     if (!rc) return TL_OK;
     if (!rc->counter) {
-        TL_CUDA(cudaMalloc((void**)&rc->counter, sizeof(unsigned)));
-        TL_CUDA(cudaMemset(rc->counter, 0, sizeof(unsigned)));
+        TL_CUDA(cudaMalloc((void**)&rc->counter, 2 * sizeof(unsigned)));   // tail, barrier
+        TL_CUDA(cudaMemset(rc->counter, 0, 2 * sizeof(unsigned)));
     }
     RP.tail_count = rc->counter;
+    const char* cb = getenv("TLGPU_CGSYNC");          // 1: cg grid.sync in the CG loop
+    const int Gb = bp.ng[0] * bp.ng[1] * bp.ng[2];
+    RP.bar_count = ((cb && cb[0] == '1') || Gb > 160) ? nullptr : rc->counter + 1;   // grid_allreduce: G <= 160
     long long stride = 0;
     for (int bz = 0; bz < bp.ng[2]; ++bz)
         for (int by = 0; by < bp.ng[1]; ++by)

@@ -61,6 +61,8 @@ struct ResCGParams {
     // !MULTI: the residual partials are reduced by the last CTA to finish (no second grid
     // barrier at the end of the solve); counter zero between launches
     unsigned* tail_count;
+    // launch-persistent arrival counter of grid_allreduce (nullptr: cg grid.sync)
+    unsigned* bar_count;
 };
 
 __host__ __device__ inline size_t rescg_smem_bytes(int lx, int ly, int lz, int gtab) {
@@ -69,6 +71,55 @@ __host__ __device__ inline size_t rescg_smem_bytes(int lx, int ly, int lz, int g
     const size_t F = 2 * ((size_t)ly * lz + (size_t)lx * lz + (size_t)lx * ly);
     const size_t extra = (size_t)gtab > n ? (size_t)gtab - n : 0;   // tables overlay PO
     return 8 * extra + 9 * H + 36 * n + 24 * F + 16;
+}
+
+// Block reduction + grid barrier + grid reduction in one pass (replaces block_sum,
+// grid.sync and grid_sum_fast, saving their extra __syncthreads): warp 0 of each CTA
+// publishes the CTA partials, arrives with a release increment of a launch-persistent
+// counter, polls it with acquire loads until all G CTAs of this epoch arrived, then sums
+// the G partials in the same fixed order in every CTA (deterministic, bitwise equal).
+template <int NV>
+__device__ __forceinline__ void grid_allreduce(double (&v)[NV], double* red, double* part, int G,
+                                               unsigned* cnt, unsigned target, double* tot) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] = warp_sum(v[k]);
+    if (lane == 0)
+#pragma unroll
+        for (int k = 0; k < NV; ++k) red[k * 32 + wid] = v[k];
+    __syncthreads();
+    if (wid == 0) {
+        double sv[NV];
+#pragma unroll
+        for (int k = 0; k < NV; ++k) sv[k] = warp_sum(lane < nw ? red[k * 32 + lane] : 0.0);
+        if (lane == 0) {
+#pragma unroll
+            for (int k = 0; k < NV; ++k) part[k * G + blockIdx.x] = sv[k];
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
+        }
+        unsigned c;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(c) : "l"(cnt) : "memory");
+        } while ((int)(c - target) < 0);
+        constexpr int PL = 5;                  // G <= 160
+        double pv[NV][PL];
+#pragma unroll
+        for (int k = 0; k < NV; ++k)
+#pragma unroll
+            for (int t = 0; t < PL; ++t) {
+                const int bb = lane + 32 * t;
+                pv[k][t] = bb < G ? __ldcg(part + k * G + bb) : 0.0;
+            }
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            double acc = 0.0;
+#pragma unroll
+            for (int t = 0; t < PL; ++t) acc += pv[k][t];
+            acc = warp_sum(acc);
+            if (lane == 0) tot[k] = acc;
+        }
+    }
+    __syncthreads();
 }
 
 // MULTI = false: exactly one solve (specs[0]); the solve loop folds away, which keeps the
@@ -89,6 +140,9 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
 
     const int G = gridDim.x;
     const int b = blockIdx.x;
+    // grid_allreduce epochs count from the counter value before this launch's first
+    // grid.sync (no CTA can arrive at a grid_allreduce before every CTA passed that sync)
+    unsigned bar_target = RP.bar_count ? __ldcg(RP.bar_count) : 0u;
     const int bxi = b % RP.ng[0], byi = (b / RP.ng[0]) % RP.ng[1], bzi = b / (RP.ng[0] * RP.ng[1]);
     const int x0 = RP.off[0][bxi], y0 = RP.off[1][byi], z0 = RP.off[2][bzi];
     const int lx = RP.off[0][bxi + 1] - x0, ly = RP.off[1][byi + 1] - y0, lz = RP.off[2][bzi + 1] - z0;
@@ -355,14 +409,11 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
                 PO[nl] = pv;
                 SO[nl] = sv;
                 RO[nl] = rv;
+                // a thread reads and writes only its own nodes' u here (the neighbours' u
+                // were last read by the previous stencil, before the grid barrier)
+                US[s] = __dmul_rn(T.invd[od_cls(od[m])], rv);
             }
             TL_STAMP(101)
-            __syncthreads();       // every thread done reading US (u_i) before it is overwritten
-#pragma unroll
-            for (int m = 0; m < NPT; ++m) {
-                if (od[m] < 0) continue;
-                US[od_s(od[m])] = __dmul_rn(T.invd[od_cls(od[m])], RO[threadIdx.x + m * kResTPB]);
-            }
 #pragma unroll
             for (int t = 0; t < kResKF; ++t) {
                 const int e = threadIdx.x + t * kResTPB;
@@ -396,6 +447,14 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
                 if (od_surf(d)) wout[GID[nl]] = wv;
             }
             TL_STAMP(103)
+            if (RP.bar_count) {
+                TL_STAMP(104)
+                if (RP.prof && si == kPS && it == 3 && threadIdx.x == 0) RP.prof[256 + b] = global_ns();
+                bar_target += (unsigned)G;
+                grid_allreduce<3>(d3, red, P.part, G, RP.bar_count, bar_target, tot);
+                TL_STAMP(105)
+                TL_STAMP(106)
+            } else {
             block_sum<3>(d3, red);
             if (threadIdx.x == 0) { P.part[0 * G + b] = d3[0]; P.part[1 * G + b] = d3[1]; P.part[2 * G + b] = d3[2]; }
             TL_STAMP(104)
@@ -407,6 +466,7 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
                 grid_sum_fast<3>(P.part, s3, G, tot);
             }
             TL_STAMP(106)
+            }
 #undef TL_STAMP
             if (prof && si == kPS && it < 100) RP.prof[np++] = global_ns();
             gam = tot[0];
