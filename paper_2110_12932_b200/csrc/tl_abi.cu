@@ -966,11 +966,14 @@ static int local_multi(tl_run* R, const tl_macro_plan& mp, const tl_micro_plan* 
     fill_rescg(RP, P, R->xg, bp);
     RP.specs = R->d_specs + 1;
     RP.nspec = ns;
+    if (getenv("TLGPU_NOCACHE") == nullptr)
+        if (int rc = attach_cache(&R->cache_l, RP, R->L, bp)) return rc;
     const int G = bp.ng[0] * bp.ng[1] * bp.ng[2];
     if (int rc = timed_begin(R, 1, ns)) return rc;
     cudaError_t e = launch_rescg_g<false, true>(RP, bp.npt, G, bp.smem, R->stream);
     if (e != cudaSuccess) return fail(TL_E_CUDA, std::string("k_pcg_resident_cg (multi) launch: ") + cudaGetErrorString(e));
     ++R->launches;
+    if (RP.scache) R->cache_l.ready = true;
     return timed_end(R);
 }
 
@@ -980,11 +983,12 @@ int32_t tl_run_macro_steps(tl_run* R, const tl_macro_plan* plans, int32_t nsteps
     if (!R || (!plans && nsteps > 0)) return fail(TL_E_INVALID, "null argument");
     TL_CUDA(cudaSetDevice(R->device));
     BrickPlan lbp;
-    // TLGPU_MULTI=1: all micro solves of a macro step in one persistent launch.  Off by
-    // default: with the Gaussian evaluated in-kernel the persistent kernel needs more than
-    // 128 registers and its CG loop spills (200 us vs 185 us per solve on cfg2).
+    // All micro solves + the corrector of a macro step in one persistent launch when the
+    // local grid fits the resident CG-CG kernel (Gaussian loads precomputed by one
+    // k_gauss_loads launch, setup shared by the solves, one launch instead of 11: cfg2
+    // 2.16 vs 2.21 ms per step).  TLGPU_MULTI=0: one launch per solve.
     const char* mv = getenv("TLGPU_MULTI");
-    const bool multi = mv && mv[0] == '1' && cg_fits(R->L, false, R->sms, lbp);
+    const bool multi = !(mv && mv[0] == '0') && cg_fits(R->L, false, R->sms, lbp);
     // Gaussian loads precomputed per macro step for the resident CG-CG local solve
     // (TLGPU_PREGAUSS=0: evaluated inside each solve instead)
     const char* pg = getenv("TLGPU_PREGAUSS");
