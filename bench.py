@@ -370,7 +370,9 @@ def main():
         traffic = json.loads(tfile.read_text()).get(f"{args.config}_local_pcg_dram_bytes_per_launch")
     roofline = {"bound": "hbm", "achieved": kloc["achieved_gbs"], "peak": peak, "unit": "GB/s",
                 "frac": kloc["achieved_gbs"] / peak, "traffic": traffic,
-                "kernel": "local-grid PCG solve (k_pcg_resident when the grid fits on chip, else k_pcg)",
+                "kernel": ("local-grid PCG solve: k_pcg_resident_cg (SMEM-resident bricks, all micro solves + "
+                           "corrector of a macro step in one launch) where the grid fits on chip, else the "
+                           "streaming k_s_rhs / k_s_cg / k_s_resid / k_s_final"),
                 "peak_source": peak_src,
                 "note": "algorithmic bytes N(64k+32) per solve (SURVEY §8d); cfg2 vectors are L2-resident"}
 
