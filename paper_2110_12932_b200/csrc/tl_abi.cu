@@ -1253,7 +1253,7 @@ static int slab_params(const tl_slab* s, tl::SlabParams& S, int& blocks, cudaStr
     S.mbase = (s->rho_c / s->dt) * V / 24.0;
     S.g_const = s->g_const;
     S.part = s->work;
-    S.count = reinterpret_cast<unsigned*>(s->work + 4 * tl::kResMaxBlocks);
+    S.count = reinterpret_cast<unsigned*>(s->work + 4 * tl::kSlabMaxBlocks);
     S.sums = s->sums;
     int dev = 0;
     TL_CUDA(cudaGetDevice(&dev));
@@ -1261,14 +1261,14 @@ static int slab_params(const tl_slab* s, tl::SlabParams& S, int& blocks, cudaStr
     if (dev < 0 || dev >= 64) return fail(TL_E_INVALID, "device index");
     if (!sms_cache[dev])
         if (int rc = device_sms(dev, sms_cache[dev])) return rc;
-    blocks = 2 * sms_cache[dev];
-    if (blocks > tl::kResMaxBlocks) blocks = tl::kResMaxBlocks;
+    blocks = 3 * sms_cache[dev];          // k_slab_direction / k_slab_update: 3 CTAs per SM
+    if (blocks > tl::kSlabMaxBlocks) blocks = tl::kSlabMaxBlocks;
     st = (cudaStream_t)s->stream;
     return TL_OK;
 }
 
-// work layout: [4 kResMaxBlocks partials][counter][deposit count][deposit nodes kDepMax ints]
-constexpr int64_t kSlabDepOff = 4 * (int64_t)tl::kResMaxBlocks + 1;
+// work layout: [4 kSlabMaxBlocks partials][counter][deposit count][deposit nodes kDepMax ints]
+constexpr int64_t kSlabDepOff = 4 * (int64_t)tl::kSlabMaxBlocks + 1;
 int64_t tl_slab_work_len(void) { return kSlabDepOff + 1 + tl::kDepMax / 2; }
 
 int32_t tl_slab_deposit(const tl_slab* s, const double* points, const double* power, int32_t count) {

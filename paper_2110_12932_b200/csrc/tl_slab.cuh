@@ -6,8 +6,9 @@
 // (id = i + NX (j + NY k), lpbfsim/mesh.py:406-409), so a halo is one contiguous
 // NX*NY run that NCCL send/recv moves without packing.
 //
-// The solve is the streaming k_pcg split at its grid barriers into launches the host
-// orchestrates between the collectives:
+// The solve is the streaming CG of tl_stream.cuh (same sweeps: forward-edge p.Ap in the
+// direction sweep, q recomputed in the update sweep) split at its reductions into launches
+// the host orchestrates between the collectives:
 //   k_slab_rhs        phase 0 over own nodes: b, r = b, x = 0; sums bb, r.z
 //   k_slab_direction  p = z (+ beta p) on own AND halo planes (the halo p follows the
 //                     same recurrence as its owner, so only r crosses ranks), q = A p
@@ -21,11 +22,12 @@
 // Kernel arrays are base-shifted by the host: a[id] addresses global node id.
 #pragma once
 
-#include "tl_kernels.cuh"
+#include "tl_stream.cuh"
 
 namespace tl {
 
 constexpr int kSlabTPB = 512;
+constexpr int kSlabMaxBlocks = 640;        // partial slots per reduction value
 
 struct SlabParams {
     Grid g;                        // the whole global grid
@@ -117,7 +119,7 @@ __global__ void __launch_bounds__(kSlabTPB) k_slab_rhs(SlabParams S) {
 }
 
 // parity 0: p_old = p0, p_new = p1; parity 1: swapped (k_pcg's ping-pong order)
-__global__ void __launch_bounds__(kSlabTPB, 2) k_slab_direction(SlabParams S, int first, double beta,
+__global__ void __launch_bounds__(kSlabTPB, 3) k_slab_direction(SlabParams S, int first, double beta,
                                                                int parity) {
     __shared__ ClassTable T;
     __shared__ double red[4 * 32];
@@ -137,13 +139,24 @@ __global__ void __launch_bounds__(kSlabTPB, 2) k_slab_direction(SlabParams S, in
         const double z = __dmul_rn(T.invd[class_of(g, i, j, k)], S.r[p]);
         pnew[p] = first ? z : __dadd_rn(__dmul_rn(beta, pold[p]), z);
     }
-    double pq[1] = {stream_phase_a(g, T, S.own_lo + tid, stride, S.own_hi, S.st_hi, S.r, pold, pnew,
-                                   first != 0, beta)};
+    // own nodes: p and p.Ap over the node and its forward edges (the +z edges of the top
+    // own plane reach the halo plane, whose p this rank recomputes from r and p_old)
+    double pq[1] = {0.0};
+    {
+        int p = S.own_lo + tid;
+        for (; p + stride < S.own_hi; p += 2 * stride) {
+            const double a = s_sweep_a_node(g, T, p, S.r, pold, pnew, first != 0, beta);
+            const double c = s_sweep_a_node(g, T, p + stride, S.r, pold, pnew, first != 0, beta);
+            pq[0] += a;
+            pq[0] += c;
+        }
+        for (; p < S.own_hi; p += stride) pq[0] += s_sweep_a_node(g, T, p, S.r, pold, pnew, first != 0, beta);
+    }
     const int s[1] = {2};
     slab_reduce<1>(S, s, pq, red);
 }
 
-__global__ void __launch_bounds__(kSlabTPB, 2) k_slab_update(SlabParams S, double alpha, int parity) {
+__global__ void __launch_bounds__(kSlabTPB, 3) k_slab_update(SlabParams S, double alpha, int parity) {
     __shared__ ClassTable T;
     __shared__ double red[4 * 32];
     const Grid& g = S.g;
@@ -151,8 +164,15 @@ __global__ void __launch_bounds__(kSlabTPB, 2) k_slab_update(SlabParams S, doubl
     __syncthreads();
     const double* pnew = parity ? S.p0 : S.p1;
     double a2[2] = {0.0, 0.0};
-    stream_phase_b(g, T, S.own_lo + blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x, S.own_hi,
-                   S.st_hi, S.x, S.r, pnew, alpha, a2[0], a2[1]);
+    {
+        const int stride = gridDim.x * blockDim.x;
+        int p = S.own_lo + blockIdx.x * blockDim.x + threadIdx.x;
+        for (; p + stride < S.own_hi; p += 2 * stride) {
+            s_sweep_b_node(g, T, p, S.x, S.r, pnew, alpha, a2[0], a2[1]);
+            s_sweep_b_node(g, T, p + stride, S.x, S.r, pnew, alpha, a2[0], a2[1]);
+        }
+        for (; p < S.own_hi; p += stride) s_sweep_b_node(g, T, p, S.x, S.r, pnew, alpha, a2[0], a2[1]);
+    }
     const int s[2] = {0, 1};
     slab_reduce<2>(S, s, a2, red);
 }
