@@ -803,7 +803,7 @@ static int ensure_snapshots(tl_run* R, int nl) {
     return TL_OK;
 }
 
-static int local_solve(tl_run* R, double* T, const tl_micro_plan& mp, const double* gload = nullptr) {
+static int local_solve(tl_run* R, double* T, const tl_micro_plan& mp) {
     tl::PcgParams P{};
     base_params(R, P, true, mp.dt);
     P.T = T;
@@ -812,10 +812,6 @@ static int local_solve(tl_run* R, double* T, const tl_micro_plan& mp, const doub
     P.w = mp.w;
     P.load = nullptr;
     bool gauss = mp.source_on != 0;
-    if (gauss && gload) {
-        P.load = gload;              // precomputed by gauss_loads_for_step
-        gauss = false;
-    }
     if (gauss) {
         P.src.peak = R->desc.beam_peak; P.src.radius = R->desc.beam_radius; P.src.depth = R->desc.beam_depth;
         for (int a = 0; a < 3; ++a) P.src.center[a] = mp.center[a];
@@ -826,68 +822,6 @@ static int local_solve(tl_run* R, double* T, const tl_micro_plan& mp, const doub
     if (int rc = launch_solve(P, gauss, R->sms, R->xg, R->stream, &R->launches, R->d_specs, nullptr, &R->cache_l))
         return rc;
     return timed_end(R);
-}
-
-// Gaussian loads of every local solve of macro step mp (the micro steps, then the
-// corrector) by one k_gauss_loads launch spread over the whole GPU, so the resident solves
-// read a dense load instead of evaluating the 96-term Gaussian in the CTAs under the beam
-// (which finished their RHS up to 8 us after the others).  The exact cutoff is taken
-// against the floor T_buildplate / 2 instead of each solve's T_old: a skipped term has
-// F < 2^-55 m T_lo, below half an ulp of b0 = m T_old whenever T_old >= T_lo / 2, so the
-// RHS is bitwise the one the in-kernel evaluation gives.  loads[e] = nullptr: source off.
-static int gauss_loads_for_step(tl_run* R, const tl_macro_plan& mp, const tl_micro_plan* micro,
-                                std::vector<double*>& loads) {
-    const int ns = mp.n_micro + (mp.corrector ? 1 : 0);
-    if (R->specs_cap < ns + 1) {
-        if (R->d_specs) cudaFree(R->d_specs);
-        R->d_specs = nullptr;
-        if (int rc = dalloc(&R->d_specs, ns + 1)) return rc;
-        R->specs_cap = ns + 1;
-    }
-    if (R->gload_cap < ns) {
-        if (R->gload) cudaFree(R->gload);
-        if (R->d_srcs) cudaFree(R->d_srcs);
-        R->gload = nullptr;
-        R->d_srcs = nullptr;
-        if (int rc = dalloc(&R->gload, (size_t)ns * R->L.n)) return rc;
-        if (int rc = dalloc(&R->d_srcs, ns)) return rc;
-        R->gload_cap = ns;
-    }
-    R->h_specs.assign(ns, tl::SolveSpec{});
-    R->h_srcs.assign(ns, tl::Gauss{});
-    loads.assign(ns, nullptr);
-    bool any_src = false;
-    const double V = R->L.h[0] * R->L.h[1] * R->L.h[2];
-    for (int e = 0; e < ns; ++e) {
-        const tl_micro_plan& up = micro[mp.micro_offset + e];
-        tl::SolveSpec& sp = R->h_specs[e];
-        sp.mbase = (R->desc.rho_c_local / up.dt) * V / 24.0;      // set_coeffs
-        tl::Gauss& src = R->h_srcs[e];
-        src.peak = R->desc.beam_peak;
-        src.radius = R->desc.beam_radius;
-        src.depth = R->desc.beam_depth;
-        for (int a = 0; a < 3; ++a) src.center[a] = up.center[a];
-        src.on = up.source_on ? 1 : 0;
-        if (src.on) loads[e] = R->gload + (size_t)e * R->L.n;
-        any_src = any_src || src.on;
-    }
-    if (!any_src) return TL_OK;
-    TL_CUDA(cudaMemcpyAsync(R->d_specs + 1, R->h_specs.data(), sizeof(tl::SolveSpec) * ns,
-                            cudaMemcpyHostToDevice, R->stream));
-    TL_CUDA(cudaMemcpyAsync(R->d_srcs, R->h_srcs.data(), sizeof(tl::Gauss) * ns, cudaMemcpyHostToDevice,
-                            R->stream));
-    const size_t smem = gauss_smem(R->L);
-    static bool attr = false;
-    if (!attr && smem > 48 * 1024) {
-        cudaFuncSetAttribute(tl::k_gauss_loads, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
-    const dim3 grid((unsigned)std::max(1, (4 * R->sms + ns - 1) / ns), (unsigned)ns);
-    tl::k_gauss_loads<<<grid, 256, smem, R->stream>>>(R->L, R->d_specs + 1, R->d_srcs,
-                                                      0.5 * R->desc.T_buildplate, R->gload);
-    TL_CUDA(cudaGetLastError());
-    ++R->launches;
-    return TL_OK;
 }
 
 // All micro solves of one macro step (+ the corrector) as one k_pcg_resident_cg launch.
@@ -950,7 +884,8 @@ static int local_multi(tl_run* R, const tl_macro_plan& mp, const tl_micro_plan* 
             cudaFuncSetAttribute(tl::k_gauss_loads, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             attr = true;
         }
-        const dim3 grid((unsigned)std::max(1, (2 * R->sms + ns - 1) / ns), (unsigned)ns);
+        // the box of each solve is ~15 % of the local grid: spread it over the whole GPU
+        const dim3 grid((unsigned)std::max(1, (8 * R->sms + ns - 1) / ns), (unsigned)ns);
         tl::k_gauss_loads<<<grid, 256, smem, R->stream>>>(R->L, R->d_specs + 1, R->d_srcs,
                                                           0.5 * R->desc.T_buildplate, R->gload);
         TL_CUDA(cudaGetLastError());
@@ -989,11 +924,7 @@ int32_t tl_run_macro_steps(tl_run* R, const tl_macro_plan* plans, int32_t nsteps
     // 2.16 vs 2.21 ms per step).  TLGPU_MULTI=0: one launch per solve.
     const char* mv = getenv("TLGPU_MULTI");
     const bool multi = !(mv && mv[0] == '0') && cg_fits(R->L, false, R->sms, lbp);
-    // Gaussian loads precomputed per macro step for the resident CG-CG local solve
-    // (TLGPU_PREGAUSS=0: evaluated inside each solve instead)
-    const char* pg = getenv("TLGPU_PREGAUSS");
-    BrickPlan gbp;
-    const bool pre_gauss = !(pg && pg[0] == '0') && cg_fits(R->L, true, R->sms, gbp);
+
     int need = 0;
     for (int s = 0; s < nsteps; ++s) {
         const tl_macro_plan& mp = plans[s];
@@ -1046,10 +977,6 @@ int32_t tl_run_macro_steps(tl_run* R, const tl_macro_plan* plans, int32_t nsteps
         // -- trace of the predicted global field on gamma --
         if (int rc = run_interp_local(R, 1, nullptr, R->tr_pred)) return rc;
         // -- micro steps (+ corrector): one persistent launch when the local grid fits --
-        std::vector<double*> gl;
-        if (!multi && pre_gauss)
-            if (int rc = gauss_loads_for_step(R, mp, micro, gl)) return rc;
-        auto gload_of = [&](int e) -> const double* { return e < (int)gl.size() ? gl[e] : nullptr; };
         if (multi) {
             if (int rc = local_multi(R, mp, micro, lbp)) return rc;
         } else
@@ -1059,14 +986,13 @@ int32_t tl_run_macro_steps(tl_run* R, const tl_macro_plan* plans, int32_t nsteps
                 tl::k_copy<<<4 * R->sms, 256, 0, R->stream>>>(R->Tl, R->Tl_before, R->L.n);
                 ++R->launches;
             }
-            if (int rc = local_solve(R, R->Tl, up, gload_of(i))) return rc;
+            if (int rc = local_solve(R, R->Tl, up)) return rc;
             if (mp.record)
                 TL_CUDA(cudaMemcpyAsync(R->snap_l[i], R->Tl, sizeof(double) * R->L.n, cudaMemcpyDeviceToDevice, R->stream));
         }
         if (mp.corrector && !multi) {
             // corrector: re-solve the last micro interval from before_final with trace_pred
-            if (int rc = local_solve(R, R->Tl_before, micro[mp.micro_offset + mp.n_micro], gload_of(mp.n_micro)))
-                return rc;
+            if (int rc = local_solve(R, R->Tl_before, micro[mp.micro_offset + mp.n_micro])) return rc;
             std::swap(R->Tl, R->Tl_before);
             if (mp.record)
                 TL_CUDA(cudaMemcpyAsync(R->snap_l[mp.n_micro], R->Tl, sizeof(double) * R->L.n, cudaMemcpyDeviceToDevice, R->stream));

@@ -38,7 +38,9 @@ struct SolveSpec {
     int tout;                     // 1: write the result to P.T
     SolveInfoDev* info;           // this solve's outcome record
     double* snap;                 // optional copy of the result (recorder snapshots), or nullptr
-    const double* load;           // this solve's dense load (precomputed Gaussian), or nullptr = P.load
+    const double* load;           // this solve's precomputed Gaussian load over box (or nullptr)
+    int box[6];                   // [i0, i1) x [j0, j1) x [k0, k1): nodes whose Gaussian term can
+                                  // change the RHS; load is dense over it (x fastest)
 };
 
 struct ResCGParams {
@@ -299,8 +301,10 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
             int i, j, k;
             decode(g, p, i, j, k);
             bv = T.mass[cls] * told;
-            const double* ld = S.load ? S.load : P.load;
-            if (ld) bv += ld[p];
+            if (P.load) bv += P.load[p];
+            if (S.load && i >= S.box[0] && i < S.box[1] && j >= S.box[2] && j < S.box[3] && k >= S.box[4] &&
+                k < S.box[5])
+                bv += S.load[(i - S.box[0]) + (S.box[1] - S.box[0]) * ((j - S.box[2]) + (S.box[3] - S.box[2]) * (k - S.box[4]))];
             if (gauss) bv = add_gaussian(bv, g, tx, ty, tz, bx_, by_, bz_, i, j, k);
             const int sy = g.NX, sz = g.NX * g.NY;
             double lift = 0.0;
@@ -552,19 +556,28 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
 }
 
 // ---------------------------------------------------------------------------------
-// Gaussian loads of all solves of a multi-solve launch, one dense array per solve
-// (loads + e n), computed by one launch before the solve so the persistent kernel
-// carries no Gaussian code (registers) and no beam-dependent work imbalance.  Values
-// are those add_gaussian evaluates in-kernel; the exact cutoff is taken against the
-// floor T_lo instead of the solve's own T_old: for T_old >= T_lo the RHS is bitwise the
-// same (a skipped term has F <= bound < 2^-55 m T_lo <= 2^-55 b0, which cannot change
-// the rounded b0 + F), and no T_old is needed, so all solves fit in one launch.
+// Gaussian loads of all solves of a multi-solve launch, computed by one launch before the
+// solve so the persistent kernel carries no Gaussian code (registers) and no
+// beam-dependent work imbalance.  Values are those add_gaussian evaluates in-kernel; the
+// exact cutoff is taken against the floor T_lo instead of the solve's own T_old: for
+// T_old >= T_lo / 2 the RHS is bitwise the same (a skipped term has F <= bound <
+// 2^-55 m T_lo <= 2^-54 b0, below half an ulp of b0, so b0 + F rounds to b0), and no T_old
+// is needed, so all solves fit in one launch.
+//
+// Only the box of nodes where the term can survive the cutoff is evaluated and stored:
+// along each axis, the indices a with 24 mx[a] max(my) max(mz) >= 2^-55 mbase n_min T_lo
+// (n_min: the smallest lumped-mass count of a free class; every node outside has
+// bound < 2^-55 m T_lo and gets exactly 0).  Every block derives the same box from the
+// same tables; block 0 of a solve records it in specs[e].box for the solve kernel.
 // grid = (blocks per solve, solves).
 // ---------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_gauss_loads(Grid g, const SolveSpec* specs, const Gauss* srcs,
+__global__ void __launch_bounds__(256) k_gauss_loads(Grid g, SolveSpec* specs, const Gauss* srcs,
                                                      double T_lo, double* loads) {
     extern __shared__ double gtab[];
     __shared__ double massc[27];
+    __shared__ double s_thr;
+    __shared__ double s_max[3];
+    __shared__ int s_lo[3], s_hi[3];
     const int e = blockIdx.y;
     double* out = loads + (size_t)e * g.n;
     double *tx = gtab, *ty = tx + 6 * g.nc[0], *tz = ty + 6 * g.nc[1];
@@ -575,16 +588,56 @@ __global__ void __launch_bounds__(256) k_gauss_loads(Grid g, const SolveSpec* sp
         class_counts(threadIdx.x, n_p, n_e, cnt, h0, h1);
         massc[threadIdx.x] = class_is_dirichlet(threadIdx.x, g.dkind) ? -1.0 : specs[e].mbase * (double)n_p;
     }
+    if (threadIdx.x < 3) {
+        s_lo[threadIdx.x] = 1 << 30;
+        s_hi[threadIdx.x] = -1;
+    }
     __syncthreads();
     build_gauss_bounds(g, tx, ty, tz, bx_, by_, bz_);
+    if (threadIdx.x == 0) {
+        double mmin = 1e300;
+        for (int c = 0; c < 27; ++c)
+            if (massc[c] > 0.0) mmin = fmin(mmin, massc[c]);
+        s_thr = mmin * T_lo * 0x1p-55;
+    }
     __syncthreads();
-    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < g.n; p += gridDim.x * blockDim.x) {
-        int i, j, k;
-        decode(g, p, i, j, k);
+    if (threadIdx.x < 3) {
+        const int a = threadIdx.x, n = a == 0 ? g.NX : (a == 1 ? g.NY : g.NZ);
+        const double* m = a == 0 ? bx_ : (a == 1 ? by_ : bz_);
+        double mx = 0.0;
+        for (int i = 0; i < n; ++i) mx = fmax(mx, m[i]);
+        s_max[a] = mx;
+    }
+    __syncthreads();
+    {
+        const int tot = g.NX + g.NY + g.NZ;
+        for (int t = threadIdx.x; t < tot; t += blockDim.x) {
+            int a = 0, idx = t;
+            if (idx >= g.NX) { idx -= g.NX; a = 1; if (idx >= g.NY) { idx -= g.NY; a = 2; } }
+            const double* m = a == 0 ? bx_ : (a == 1 ? by_ : bz_);
+            const double other = a == 0 ? s_max[1] * s_max[2] : (a == 1 ? s_max[0] * s_max[2] : s_max[0] * s_max[1]);
+            if (24.0 * m[idx] * other >= s_thr) {
+                atomicMin(&s_lo[a], idx);
+                atomicMax(&s_hi[a], idx + 1);
+            }
+        }
+    }
+    __syncthreads();
+    int box[6];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        box[2 * a] = s_hi[a] > s_lo[a] ? s_lo[a] : 0;
+        box[2 * a + 1] = s_hi[a] > s_lo[a] ? s_hi[a] : 0;
+    }
+    if (blockIdx.x == 0 && threadIdx.x < 6) specs[e].box[threadIdx.x] = box[threadIdx.x];
+    const int bw = box[1] - box[0], bh = box[3] - box[2], bd = box[5] - box[4];
+    const int nb = bw * bh * bd;
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nb; q += gridDim.x * blockDim.x) {
+        const int i = box[0] + q % bw, j = box[2] + (q / bw) % bh, k = box[4] + q / (bw * bh);
         const double m = massc[class_of(g, i, j, k)];
-        if (m < 0.0) { out[p] = 0.0; continue; }
+        if (m < 0.0) { out[q] = 0.0; continue; }
         const double bound = 24.0 * bx_[i] * by_[j] * bz_[k];
-        out[p] = (bound < m * T_lo * 0x1p-55) ? 0.0 : gaussian_node_fast(g, tx, ty, tz, i, j, k);
+        out[q] = (bound < m * T_lo * 0x1p-55) ? 0.0 : gaussian_node_fast(g, tx, ty, tz, i, j, k);
     }
 }
 
