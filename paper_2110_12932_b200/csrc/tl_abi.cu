@@ -161,6 +161,7 @@ struct BrickPlan {
     int maxnodes = 0;
     size_t smem = 0;
     int npt = 0;
+    bool xglob = false;          // CG-CG with x in global memory (see rescg_smem_bytes)
 };
 
 static void split_axis(int N, int parts, int* off) {
@@ -175,6 +176,8 @@ static BrickPlan plan_bricks_uncached(const tl::Grid& g, bool gauss, int sms, si
     int target = (int)std::min<long long>(sms, std::max<long long>(1, (n + 2047) / 2048));
     const int gtab = gauss ? tl::gauss_smem_len(g) : 0;
     double best_cost = 1e300;
+    // CG-CG: x in SMEM if any decomposition fits, else x in global memory
+    for (int xg = 0; xg < ((cgv && gtab == 0) ? 2 : 1) && !best.ok; ++xg)
     for (int gx = 1; gx <= std::min(N[0], tl::kResMaxSplit); ++gx)
         for (int gy = 1; gy <= std::min(N[1], tl::kResMaxSplit) && gx * gy <= target; ++gy)
             for (int gz = 1; gz <= std::min(N[2], tl::kResMaxSplit) && gx * gy * gz <= target; ++gz) {
@@ -184,7 +187,8 @@ static BrickPlan plan_bricks_uncached(const tl::Grid& g, bool gauss, int sms, si
                 const int own = lx * ly * lz;
                 const int H = (lx + 2) * (ly + 2) * (lz + 2);
                 const int nface = 2 * (ly * lz + lx * lz + lx * ly);
-                const size_t smem = cgv ? tl::rescg_smem_bytes(lx, ly, lz, gtab) : tl::res_smem_bytes(lx, ly, lz, gtab);
+                const size_t smem = cgv ? tl::rescg_smem_bytes(lx, ly, lz, gtab, xg == 1)
+                                        : tl::res_smem_bytes(lx, ly, lz, gtab);
                 if (own > 12 * tl::kResTPB || smem > smem_cap || H >= 16384 ||
                     nface > tl::kResKF * tl::kResTPB)
                     continue;
@@ -196,6 +200,7 @@ static BrickPlan plan_bricks_uncached(const tl::Grid& g, bool gauss, int sms, si
                     best.ng[0] = gx; best.ng[1] = gy; best.ng[2] = gz;
                     best.maxnodes = own;
                     best.smem = smem;
+                    best.xglob = xg == 1;
                 }
             }
     if (best.ok) {
@@ -230,9 +235,9 @@ static bool exact_cg() {
     return v == 1;
 }
 
-template <bool GAUSS, int NPT, bool MULTI>
+template <bool GAUSS, int NPT, bool MULTI, bool XG = false>
 static cudaError_t launch_rescg_t(tl::ResCGParams& RP, int G, size_t smem, cudaStream_t st) {
-    auto fn = tl::k_pcg_resident_cg<GAUSS, NPT, MULTI>;
+    auto fn = tl::k_pcg_resident_cg<GAUSS, NPT, MULTI, XG>;
     static thread_local bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kResSmemCap);
@@ -245,6 +250,11 @@ static cudaError_t launch_rescg_t(tl::ResCGParams& RP, int G, size_t smem, cudaS
 
 template <bool GAUSS, bool MULTI = false>
 static cudaError_t launch_rescg_g(tl::ResCGParams& RP, int npt, int G, size_t smem, cudaStream_t st) {
+    if (RP.xglob) {                  // x in global memory: large bricks, no Gaussian tables
+        if (GAUSS || npt < 8) return cudaErrorInvalidConfiguration;
+        return npt == 8 ? launch_rescg_t<false, 8, MULTI, true>(RP, G, smem, st)
+                        : launch_rescg_t<false, 12, MULTI, true>(RP, G, smem, st);
+    }
     switch (npt) {
         case 4: return launch_rescg_t<GAUSS, 4, MULTI>(RP, G, smem, st);
         case 8: return launch_rescg_t<GAUSS, 8, MULTI>(RP, G, smem, st);
@@ -322,12 +332,17 @@ static bool cg_fits(const tl::Grid& g, bool gauss, int sms, BrickPlan& bp) {
 struct ResCache {
     int* buf = nullptr;
     size_t cap = 0;              // ints
+    double* xbuf = nullptr;      // own-node x of an xglob plan
+    size_t xcap = 0;
     unsigned* counter = nullptr;
     int key[7] = {0, 0, 0, 0, 0, 0, 0};   // grid cells + brick split + npt of the stored setup
     bool ready = false;
     void release() {
         if (buf) cudaFree(buf);
         if (counter) cudaFree(counter);
+        if (xbuf) cudaFree(xbuf);
+        xbuf = nullptr;
+        xcap = 0;
         buf = nullptr;
         counter = nullptr;
         cap = 0;
@@ -374,6 +389,17 @@ static int attach_cache(ResCache* rc, tl::ResCGParams& RP, const tl::Grid& g, co
     RP.scache = rc->buf;
     RP.sc_stride = stride;
     RP.sc_mode = rc->ready ? 2 : 1;
+    if (bp.xglob) {
+        const size_t xn = (size_t)bp.maxnodes * G;
+        if (xn > rc->xcap) {
+            if (rc->xbuf) cudaFree(rc->xbuf);
+            rc->xbuf = nullptr;
+            TL_CUDA(cudaMalloc((void**)&rc->xbuf, xn * sizeof(double)));
+            rc->xcap = xn;
+        }
+        RP.xglob = rc->xbuf;
+        RP.xg_stride = bp.maxnodes;
+    }
     return TL_OK;
 }
 
@@ -381,7 +407,7 @@ static int launch_solve(tl::PcgParams& P, bool gauss, int sms, double* xg, cudaS
                         int64_t* launches, tl::SolveSpec* dspec = nullptr, int* kind_out = nullptr,
                         ResCache* cache = nullptr) {
     BrickPlan bp;
-    if (xg && dspec && cg_fits(P.g, gauss, sms, bp)) {
+    if (xg && dspec && cg_fits(P.g, gauss, sms, bp) && (!bp.xglob || (cache && !getenv("TLGPU_NOCACHE")))) {
         {
             tl::SolveSpec hs{};
             hs.mbase = P.mbase;
@@ -923,7 +949,8 @@ int32_t tl_run_macro_steps(tl_run* R, const tl_macro_plan* plans, int32_t nsteps
     // k_gauss_loads launch, setup shared by the solves, one launch instead of 11: cfg2
     // 2.16 vs 2.21 ms per step).  TLGPU_MULTI=0: one launch per solve.
     const char* mv = getenv("TLGPU_MULTI");
-    const bool multi = !(mv && mv[0] == '0') && cg_fits(R->L, false, R->sms, lbp);
+    const bool multi = !(mv && mv[0] == '0') && cg_fits(R->L, false, R->sms, lbp) &&
+                       !(lbp.xglob && getenv("TLGPU_NOCACHE"));
 
     int need = 0;
     for (int s = 0; s < nsteps; ++s) {

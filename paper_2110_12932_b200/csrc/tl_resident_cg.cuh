@@ -20,7 +20,7 @@
 // owners), w of own nodes in registers, x and p of own nodes in shared memory.
 // Only the brick-surface w values cross CTAs (ping-pong exchange buffers).
 //
-// Shared memory: [US: H][RO: n][SO: n][XO: n][PO: n (+ Gaussian tables overlay during phase 0)]
+// Shared memory: [US: H][RO: n][SO: n][XO: n, unless xglob][PO: n (+ Gaussian tables overlay during phase 0)]
 //                [RF: F][SF: F][GID: n int][FS: F int][FG: F int][CL: H bytes]
 #pragma once
 
@@ -65,14 +65,19 @@ struct ResCGParams {
     unsigned* tail_count;
     // launch-persistent arrival counter of grid_allreduce (nullptr: cg grid.sync)
     unsigned* bar_count;
+    // own-node x in global memory (CTA b at xglob + b * xg_stride), or nullptr: in SMEM
+    double* xglob;
+    long long xg_stride;
 };
 
-__host__ __device__ inline size_t rescg_smem_bytes(int lx, int ly, int lz, int gtab) {
+// xglob: x of the own nodes kept in global memory (L2) instead of SMEM, for bricks that
+// would not fit otherwise (the cfg2 global grid); x is touched once per iteration.
+__host__ __device__ inline size_t rescg_smem_bytes(int lx, int ly, int lz, int gtab, bool xglob = false) {
     const size_t H = (size_t)(lx + 2) * (ly + 2) * (lz + 2);
     const size_t n = (size_t)lx * ly * lz;
     const size_t F = 2 * ((size_t)ly * lz + (size_t)lx * lz + (size_t)lx * ly);
     const size_t extra = (size_t)gtab > n ? (size_t)gtab - n : 0;   // tables overlay PO
-    return 8 * extra + 9 * H + 36 * n + 24 * F + 16;
+    return 8 * extra + 9 * H + (xglob ? 28 : 36) * n + 24 * F + 16;
 }
 
 // Block reduction + grid barrier + grid reduction in one pass (replaces block_sum,
@@ -126,7 +131,7 @@ __device__ __forceinline__ void grid_allreduce(double (&v)[NV], double* red, dou
 
 // MULTI = false: exactly one solve (specs[0]); the solve loop folds away, which keeps the
 // kernel at ~106 registers without spills.
-template <bool GAUSS, int NPT, bool MULTI>
+template <bool GAUSS, int NPT, bool MULTI, bool XG = false>
 __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) {
     cg::grid_group grid = cg::this_grid();
     const PcgParams& P = RP.P;
@@ -162,8 +167,10 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
     double* US = reinterpret_cast<double*>(smem);
     double* RO = US + H;
     double* SO = RO + nown;
-    double* XO = SO + nown;
-    double* PO = XO + nown;
+    // XG (x in global memory) is a template flag so that the SMEM variant keeps x
+    // accesses as shared-memory instructions
+    double* XO = XG ? RP.xglob + (size_t)b * RP.xg_stride : SO + nown;
+    double* PO = XG ? SO + nown : XO + nown;
     double* tx = PO;
     double* ty = tx + 6 * g.nc[0];
     double* tz = ty + 6 * g.nc[1];
