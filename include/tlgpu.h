@@ -173,6 +173,15 @@ int32_t tl_run_get_snapshot(tl_run* run, int32_t which, int32_t index, double* h
 int32_t tl_run_sync(tl_run* run);
 /* which: 0 = global field, 1 = local field, 2 = trace (dense local array). */
 int32_t tl_run_get_field(tl_run* run, int32_t which, double* host, int64_t n);
+/* Asynchronous read-back for pipelined callers (a recorder or a viewer consuming every
+ * macro step while the next one computes).  Enqueues, in the run's stream order, a
+ * device copy of the field into staging slot `slot` (0..3), then its transfer to `host`
+ * on a separate copy stream, and returns at once; the run may go on with further macro
+ * steps.  `host` should be pinned (page-locked) and must stay valid until
+ * tl_run_field_wait(run, slot) returns. */
+int32_t tl_run_field_async(tl_run* run, int32_t which, double* host, int64_t n, int32_t slot);
+/* Block until the read-back enqueued on `slot` has landed in host memory. */
+int32_t tl_run_field_wait(tl_run* run, int32_t slot);
 /* Copy out (and clear) the per-solve info log; *count receives the number written. */
 int32_t tl_run_take_info(tl_run* run, tl_solve_info* out, int32_t max, int32_t* count);
 /* Melt-pool summary of both fields: max T and count of nodes with T > T_liquidus

@@ -515,6 +515,12 @@ struct tl_run {
     double* xg = nullptr;            // exchange array of the resident kernels (4 n)
     tl::SolveSpec* d_specs = nullptr; int specs_cap = 0;
     ResCache cache_g, cache_l;       // resident-kernel setup caches (global / local grid)
+    // asynchronous field read-back (tl_run_field_async): staging copies + copy stream
+    cudaStream_t copy_stream = nullptr;
+    double* stage[4] = {nullptr, nullptr, nullptr, nullptr};
+    size_t stage_n[4] = {0, 0, 0, 0};
+    cudaEvent_t stage_ready[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t stage_done[4] = {nullptr, nullptr, nullptr, nullptr};
     std::vector<tl::SolveSpec> h_specs;
     std::vector<int> ev_nsolve;
     double* flush = nullptr; size_t flush_n = 0;
@@ -760,6 +766,15 @@ int32_t tl_run_destroy(tl_run* R) {
     if (R->melt_host) cudaFreeHost(R->melt_host);
     R->cache_g.release();
     R->cache_l.release();
+    for (int k = 0; k < 4; ++k) {
+        if (R->stage[k]) cudaFree(R->stage[k]);
+        if (R->stage_ready[k]) cudaEventDestroy(R->stage_ready[k]);
+        if (R->stage_done[k]) cudaEventDestroy(R->stage_done[k]);
+    }
+    if (R->copy_stream) {
+        cudaStreamSynchronize(R->copy_stream);
+        cudaStreamDestroy(R->copy_stream);
+    }
     if (R->stream) cudaStreamDestroy(R->stream);
     delete R;
     return TL_OK;
@@ -1063,6 +1078,45 @@ int32_t tl_run_get_field(tl_run* R, int32_t which, double* host, int64_t n) {
     if (which < 0 || which > 2 || n != want) return fail(TL_E_INVALID, "field selector or size mismatch");
     TL_CUDA(cudaMemcpyAsync(host, src, sizeof(double) * n, cudaMemcpyDeviceToHost, R->stream));
     TL_CUDA(cudaStreamSynchronize(R->stream));
+    return TL_OK;
+}
+
+int32_t tl_run_field_async(tl_run* R, int32_t which, double* host, int64_t n, int32_t slot) {
+    if (!R || !host) return fail(TL_E_INVALID, "null argument");
+    if (slot < 0 || slot > 3) return fail(TL_E_INVALID, "read-back slot must be 0..3");
+    TL_CUDA(cudaSetDevice(R->device));
+    const double* src = which == 0 ? R->Tg : (which == 1 ? R->Tl : R->tr_old);
+    const int64_t want = which == 0 ? R->G.n : R->L.n;
+    if (which < 0 || which > 2 || n != want) return fail(TL_E_INVALID, "field selector or size mismatch");
+    if (!R->copy_stream) TL_CUDA(cudaStreamCreateWithFlags(&R->copy_stream, cudaStreamNonBlocking));
+    if (!R->stage_ready[slot]) {
+        TL_CUDA(cudaEventCreateWithFlags(&R->stage_ready[slot], cudaEventDisableTiming));
+        TL_CUDA(cudaEventCreateWithFlags(&R->stage_done[slot], cudaEventDisableTiming));
+    }
+    if (R->stage_n[slot] < (size_t)n) {
+        // the previous transfer out of this slot must have finished before it is freed
+        TL_CUDA(cudaEventSynchronize(R->stage_done[slot]));
+        if (R->stage[slot]) cudaFree(R->stage[slot]);
+        R->stage[slot] = nullptr;
+        if (int rc = dalloc(&R->stage[slot], (size_t)n)) return rc;
+        R->stage_n[slot] = (size_t)n;
+    }
+    // the staging slot may still be read by the slot's previous transfer
+    TL_CUDA(cudaStreamWaitEvent(R->stream, R->stage_done[slot], 0));
+    TL_CUDA(cudaMemcpyAsync(R->stage[slot], src, sizeof(double) * n, cudaMemcpyDeviceToDevice, R->stream));
+    TL_CUDA(cudaEventRecord(R->stage_ready[slot], R->stream));
+    TL_CUDA(cudaStreamWaitEvent(R->copy_stream, R->stage_ready[slot], 0));
+    TL_CUDA(cudaMemcpyAsync(host, R->stage[slot], sizeof(double) * n, cudaMemcpyDeviceToHost, R->copy_stream));
+    TL_CUDA(cudaEventRecord(R->stage_done[slot], R->copy_stream));
+    return TL_OK;
+}
+
+int32_t tl_run_field_wait(tl_run* R, int32_t slot) {
+    if (!R) return fail(TL_E_INVALID, "null argument");
+    if (slot < 0 || slot > 3) return fail(TL_E_INVALID, "read-back slot must be 0..3");
+    if (!R->stage_done[slot]) return TL_OK;
+    TL_CUDA(cudaSetDevice(R->device));
+    TL_CUDA(cudaEventSynchronize(R->stage_done[slot]));
     return TL_OK;
 }
 

@@ -100,6 +100,17 @@ class DeviceRun:
         N.check(N.lib().tl_run_get_field(self._h, which, N.dptr(out), n), "tl_run_get_field")
         return out
 
+    def field_async(self, which: int, out: np.ndarray, slot: int = 0) -> None:
+        """Enqueue the read-back of a field into `out` (pinned memory for full overlap)
+        and return at once; the run may continue.  Complete with field_wait(slot)."""
+        n = self.n_global if which == 0 else self.n_local
+        if out.shape != (n,) or out.dtype != np.float64 or not out.flags.c_contiguous:
+            raise ValueError(f"out must be a contiguous float64 array of {n} values")
+        N.check(N.lib().tl_run_field_async(self._h, which, N.dptr(out), n, slot), "tl_run_field_async")
+
+    def field_wait(self, slot: int = 0) -> None:
+        N.check(N.lib().tl_run_field_wait(self._h, slot), "tl_run_field_wait")
+
     def snapshot(self, which: int, index: int = 0) -> np.ndarray:
         n = self.n_global if which == 0 else self.n_local
         out = np.empty(n)

@@ -162,6 +162,41 @@ def test_device_iterations_match_reference_cfg1():
     assert max(abs(a - b) for a, b in zip(its, ref)) <= 1
 
 
+def test_async_field_readback_matches_sync():
+    """tl_run_field_async / _wait (pipelined read-back while later macro steps run) return
+    bitwise the fields tl_run_get_field returns after each step."""
+    from paper_2110_12932_b200.schedule import plan_spacetime
+    cfg = P.load_config(CONFIGS / "cfg1_m4.cfg")
+    problem, lm = P.build_problem(cfg)
+    sched = P.MacroSchedule(cfg.dt_macro, cfg.micro_steps, 0.0, cfg.t_end)
+    plans, placement, tg, tl = [], lm.placement, 0.0, 0.0
+    for k in range(6):
+        pl = plan_spacetime(problem, sched, placement, cfg.path, cfg.policy, tg, tl, k0=k, nsteps=1)
+        plans.append(pl)
+        placement, tg, tl = pl.final_placement, pl.final_t_global, pl.final_t_local
+    sync_fields = []
+    with P.DeviceRun(problem, lm) as run:
+        run.initial(P.uniform_field(problem.global_mesh, 293.0))
+        for pl in plans:
+            run.run(pl)
+            sync_fields.append((run.field(0), run.field(1)))
+    bufs = [(np.empty(problem.global_mesh.n_nodes), np.empty(lm.n_nodes)) for _ in range(len(plans))]
+    with P.DeviceRun(problem, lm) as run:
+        run.initial(P.uniform_field(problem.global_mesh, 293.0))
+        for s, pl in enumerate(plans):
+            run.run(pl)
+            run.field_async(0, bufs[s][0], slot=(2 * s) % 4)
+            run.field_async(1, bufs[s][1], slot=(2 * s + 1) % 4)
+            if s >= 1:
+                run.field_wait((2 * s - 2) % 4)
+                run.field_wait((2 * s - 1) % 4)
+        run.field_wait((2 * len(plans) - 2) % 4)
+        run.field_wait((2 * len(plans) - 1) % 4)
+    for (g, l), (ga, la) in zip(sync_fields, bufs):
+        np.testing.assert_array_equal(g, ga)
+        np.testing.assert_array_equal(l, la)
+
+
 def test_cfg2_first_steps_vs_reference():
     z, cfg, rec, stats = _golden_run("cfg2", n_steps=2)
     TL = cfg.material.T_liquidus
