@@ -20,7 +20,7 @@ from paper_2110_12932_b200.control import LocalPlacement
 from oracle import kuhn
 from oracle.twolevel import OracleRun
 
-from .conftest import CONFIGS, GOLDEN
+from .conftest import CONFIGS, GOLDEN, ROOT
 
 pytestmark = pytest.mark.gpu
 REL = 1e-9
@@ -342,3 +342,39 @@ def test_linearity_full_size_cfg4_global_step():
     c, ic = s(T1)
     assert ia.status == ib.status == ic.status == 0
     assert np.abs((a - b) - c).max() <= 1e-9 * np.abs(a).max()
+
+
+_MODE_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import paper_2110_12932_b200 as P
+cfg = P.load_config({cfg!r})
+cfg.t_end = {nsteps} * cfg.dt_macro
+state, stats = P.two_level_run(cfg)
+np.savez({out!r}, g=state.global_field.values, l=state.local_field.values,
+         c=np.array([stats.counters[k] for k in ("global_solves", "local_solves", "relocations")]))
+"""
+
+
+@pytest.mark.parametrize("env", [{"TLGPU_MULTI": "0"}, {"TLGPU_NOCACHE": "1", "TLGPU_CGSYNC": "1"},
+                                 {"TLGPU_EXACT_CG": "1"}])
+def test_alternative_solver_modes_match_default(env, tmp_path):
+    """The non-default device paths (one launch per local solve; no setup cache and
+    cg::grid.sync barriers; scipy-exact two-barrier kernel) give the default run's fields
+    to CG rounding with the same counters (env switches are read once per process, so
+    each mode runs in a subprocess)."""
+    import os
+    import subprocess
+    import sys
+    cfg = CONFIGS / "cfg1_m4.cfg"
+    runs = {}
+    for tag, extra in (("default", {}), ("mode", env)):
+        out = tmp_path / f"{tag}.npz"
+        code = _MODE_SCRIPT.format(root=str(ROOT), cfg=str(cfg), nsteps=6, out=str(out))
+        res = subprocess.run([sys.executable, "-c", code], env={**os.environ, **extra},
+                             capture_output=True, text=True, timeout=600)
+        assert res.returncode == 0, res.stderr[-2000:]
+        runs[tag] = np.load(out)
+    a, b = runs["default"], runs["mode"]
+    assert rel(b["g"], a["g"]) <= 1e-12 and rel(b["l"], a["l"]) <= 1e-12
+    np.testing.assert_array_equal(a["c"], b["c"])

@@ -151,3 +151,24 @@ def test_chronopoulos_gear_matches_scipy_cg(name):
     assert info == 0 and its == int(z["cg_iters"])
     x[D] = b[D]
     assert np.abs(x - z["sol"]).max() <= 1e-13 * np.abs(z["sol"]).max()
+
+
+@pytest.mark.parametrize("name", OP_CASES)
+def test_forward_edge_pAp_identity(name):
+    """The streaming sweep A (tl_stream.cuh) forms the CG denominator p.A_c p from each
+    node and its three forward edges: sum_p d_p p_p^2 - 2 sum_{edges, both ends free}
+    c_e p_lo p_hi (A_c is symmetric after the symmetric Dirichlet elimination, identity
+    rows give p_p^2).  Check the identity against p.(A_c p) on the golden operators."""
+    z, G, D, g, local, beam = _op(name)
+    op = kuhn.StencilOperator(G, 9.8, 8440 * 410.0, float(z["dt"]), D.reshape(G.shape))
+    rng = np.random.default_rng(7)
+    p = rng.standard_normal(G.n_nodes)
+    ref = float(p @ op.apply(p))
+    Pg = p.reshape(G.shape)
+    free = ~op.D
+    fwd = float(np.sum(op.diag_c * Pg * Pg))
+    for a in range(3):
+        lo, hi = kuhn._edge_slices(a)
+        both = free[lo] & free[hi]
+        fwd -= 2.0 * float(np.sum(np.where(both, op.c[a] * Pg[lo] * Pg[hi], 0.0)))
+    assert abs(fwd - ref) <= 1e-13 * abs(ref)
