@@ -19,6 +19,7 @@
 #include "../../include/tlgpu.h"
 #include "tl_resident_cg.cuh"
 #include "tl_stream.cuh"
+#include "tl_tiled.cuh"
 #include "tl_slab.cuh"
 
 namespace {
@@ -129,13 +130,104 @@ static cudaError_t launch_s_cg(tl::PcgParams& P, int Gr, int sms, cudaStream_t s
     return cudaLaunchCooperativeKernel((void*)tl::k_s_cg<MINB, UNR>, G, tl::kSTPB, args, 0, st);
 }
 
+// ---- z-marching CG loop on bulk copies (tl_tiled.cuh) --------------------------------
+// Default CG loop of the streaming solve; TLGPU_TILED=0 falls back to k_s_cg.  Tile plan:
+// grids of at least TLGPU_TILED_MIN nodes (default 20M: measured faster than k_s_cg on
+// the 201M-node cfg4 grid, slower on the 6-7M-node cfg3 / cfg4-local grids whose ~40 us
+// sweeps do not amortise the per-sweep pipeline fill and item reduction).  H full x-rows
+// per item so that five sweep-B stages fit in 220 KB and a consumer thread has at most 4
+// nodes per plane, z chunks of about a tenth of a CTA's share (at least TLGPU_TZ planes),
+// as many ring stages as fit in 220 KB (at least 4).  TLGPU_TH overrides H.
+constexpr int kTNCW = 16;                      // consumer warps of k_t_cg
+static bool tiled_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("TLGPU_TILED");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
+static bool tiled_plan(const tl::Grid& g, int sms, tl::TPlan& tp, size_t& smem) {
+    static long long nmin = -1;
+    if (nmin < 0) {
+        const char* e = getenv("TLGPU_TILED_MIN");
+        nmin = e ? atoll(e) : 20000000LL;
+    }
+    if ((long long)g.n < nmin) return false;
+    const int NX = g.NX;
+    // rows per item: a sweep-B stage ((H + 2) + 2 H rows) small enough for 5 ring stages in
+    // 220 KB, and at most 4 nodes per consumer thread per plane
+    int H = std::max(1, (220 * 1024 / 8 / 5 - 2 * NX - 8) / (3 * NX));
+    H = std::max(1, std::min(H, 4 * kTNCW * 32 / NX));
+    if (const char* e = getenv("TLGPU_TH")) H = std::max(1, atoi(e));
+    H = std::min(H, g.NY);
+    if (H * NX > 4 * kTNCW * 32) return false;
+    tp.H = H;
+    tp.NB = (g.NY + H - 1) / H;
+    auto even = [](int v) { return (v + 1) & ~1; };
+    tp.RA = even((H + 1) * NX + 2);
+    tp.RB = even((H + 2) * NX + 2);
+    tp.RX = even(H * NX + 2);
+    tp.stage = (std::max(2 * tp.RA, tp.RB + 2 * tp.RX) + 15) & ~15;
+    const size_t cap = 220 * 1024;
+    tp.NS = (int)std::min<size_t>(tl::kTMaxStages, cap / ((size_t)tp.stage * 8));
+    if (tp.NS < 4) return false;
+    // z chunk: about a tenth of a CTA's share of the sweep per item (dynamic balance),
+    // at least TLGPU_TZ planes (default 3)
+    int zmin = 3;
+    if (const char* e = getenv("TLGPU_TZ")) zmin = std::max(1, atoi(e));
+    const double share = (double)g.n / sms;
+    int Z = (int)(share / (10.0 * H * NX));
+    Z = std::max(zmin, std::min(Z, g.NZ));
+    int C = (g.NZ + Z - 1) / Z;
+    C = std::min(C, std::max(1, 7000 / tp.NB));
+    tp.C = C;
+    tp.I = tp.NB * C;
+    if (tp.I > 7000) return false;
+    tp.nsd.init(tp.NS);
+    tp.nbd.init(tp.NB);
+    tp.cd.init(tp.C);
+    smem = (size_t)tp.NS * tp.stage * 8;
+    return true;
+}
+
+static cudaError_t launch_t_cg(tl::PcgParams& P, int Gr, int sms, cudaStream_t st, bool& launched) {
+    launched = false;
+    tl::TPlan tp{};
+    size_t smem = 0;
+    if (!tiled_enabled() || !tiled_plan(P.g, sms, tp, smem)) return cudaSuccess;
+    const int ncw = kTNCW;
+    const bool two = tp.H * P.g.NX <= 2 * kTNCW * 32;
+    auto kern = two ? tl::k_t_cg<kTNCW, 2> : tl::k_t_cg<kTNCW, 4>;
+    static thread_local size_t smem_set[2] = {0, 0};
+    cudaError_t e = cudaSuccess;
+    if (smem > smem_set[two]) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        smem_set[two] = smem;
+    }
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (ncw + 1) * 32, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaSuccess;
+    e = cudaMemsetAsync(P.part + tl::kTCounter, 0, 4 * sizeof(unsigned), st);
+    if (e != cudaSuccess) return e;
+    void* args[] = {&P, &Gr, &tp};
+    e = cudaLaunchCooperativeKernel((void*)kern, sms, (ncw + 1) * 32, args, smem, st);
+    launched = e == cudaSuccess;
+    return e;
+}
+
 static int launch_stream(tl::PcgParams& P, int sms, cudaStream_t st, int64_t* launches) {
     const int minb = split_minb();
     if (minb == 0) return launch_pcg(P, false, sms, st, launches);
     const int Gr = 4 * sms;
     tl::k_s_rhs<<<Gr, tl::kSTPB, 0, st>>>(P);
     cudaError_t e = cudaGetLastError();
-    if (e == cudaSuccess)
+    bool tiled = false;
+    if (e == cudaSuccess) e = launch_t_cg(P, Gr, sms, st, tiled);
+    if (e == cudaSuccess && !tiled)
         e = minb == 2 ? launch_s_cg<2>(P, Gr, sms, st)
           : minb == 4 ? launch_s_cg<4>(P, Gr, sms, st)
           : minb == 22 ? launch_s_cg<2, 2>(P, Gr, sms, st)
@@ -490,7 +582,8 @@ int device_sms(int dev, int& sms) {
 
 template <class T>
 int dalloc(T** p, size_t n) {
-    cudaError_t e = cudaMalloc((void**)p, sizeof(T) * (n ? n : 1));
+    // +2 elements: the bulk copies of k_t_cg round node ranges out to 16-byte boundaries
+    cudaError_t e = cudaMalloc((void**)p, sizeof(T) * (n + 2));
     if (e != cudaSuccess) return fail(TL_E_ALLOC, std::string("cudaMalloc: ") + cudaGetErrorString(e));
     return TL_OK;
 }

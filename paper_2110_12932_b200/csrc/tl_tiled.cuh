@@ -1,0 +1,523 @@
+// tl_tiled.cuh — z-marching CG loop fed by the bulk-copy engine (sm_100a, fp64).
+//
+// Same iterations as k_s_cg (tl_stream.cuh; scipy's cg as used by lpbfsim/fem.py:271-298)
+// and the same per-node arithmetic (s_sweep_a_node / s_sweep_b_node read through a
+// shared-memory view instead of global memory), so a node's p, x, r are bitwise the ones
+// k_s_cg computes for the same alpha and beta.
+//
+// Why: the flat grid-stride sweeps of k_s_cg fetch each node's y and z neighbours from L2
+// (3x the DRAM bytes of the operand in sweep A, 5x in sweep B), and the L2 slice
+// throughput (~6.3 kB/clk chip-wide, B300_MICROARCH.md) caps them below the HBM peak.
+// Here every operand plane crosses L2 once per item:
+//
+//   item      = (row block jb: H full x-rows, z chunk kc: planes [k0, k1))
+//   stage     = one z-plane of an item: the item's rows (plus one halo row on each side
+//               for the stencil operand) of each vector, ONE contiguous range per vector
+//               (full x-rows are contiguous in the reference node order), moved by
+//               cp.async.bulk into a ring of NS shared-memory stages
+//   producer  = one lane of the last warp: takes items from a per-sweep atomic counter
+//               (dynamic balance), waits for a free stage (empty mbarrier), arms the full
+//               mbarrier with the byte count and issues the bulk copies
+//   consumers = NCW warps: wait for plane k (and k+1, and keep k-1), compute the plane,
+//               release the stage; no CTA-wide barrier in the march
+//
+// Sweep A (p = z + beta p_old and p.Ap over forward edges) needs r and p_old at planes
+// k, k+1 and rows j0..j1 (one forward halo row); sweep B (q = A p, x += alpha p,
+// r -= alpha q) needs p at planes k-1, k, k+1 with one halo row each side, and x, r at
+// plane k.  Dot products are reduced per item in a fixed order and the item partials
+// summed in item order by every CTA after the grid barrier: the result does not depend
+// on which CTA ran which item (deterministic despite the dynamic schedule).
+#pragma once
+
+#include "tl_stream.cuh"
+
+namespace tl {
+
+constexpr int kTMaxStages = 16;
+constexpr int kTPartItems = 4096;          // offset of the item partials in PcgParams::part
+constexpr int kTCounter = 2048;            // offset (in doubles) of the 4 sweep counters
+
+struct TPlan {
+    int H;          // rows per item
+    int NB;         // row blocks
+    int C;          // z chunks
+    int I;          // items = NB * C
+    int NS;         // ring stages
+    int stage;      // doubles per stage
+    int RA;         // sweep A: r at [0, RA), p_old at [RA, 2 RA)
+    int RB, RX;     // sweep B: p at [0, RB), x at [RB, RB + RX), r at [RB + RX, RB + 2 RX)
+    FastDiv nsd, nbd, cd;   // division by NS, NB, C
+};
+
+// Ring slot of position u; parity of its phase in *ph.
+__device__ __forceinline__ int t_slot(const TPlan& tp, uint32_t u, unsigned& ph) {
+    const uint32_t q = tp.nsd.div(u);
+    ph = q & 1u;
+    return (int)(u - q * (uint32_t)tp.NS);
+}
+__device__ __forceinline__ int t_slot(const TPlan& tp, uint32_t u) {
+    unsigned ph;
+    return t_slot(tp, u, ph);
+}
+
+// ---- mbarrier / bulk-copy primitives (PTX ISA 8.0+, sm_90+) -------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+    unsigned done;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_u32(b)), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+// Global -> shared bulk copy completing on mbarrier b (16-byte aligned, bytes % 16 == 0).
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* b) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(b))
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// Item geometry.
+struct TItem {
+    int j0, j1, k0, k1;
+};
+__device__ __forceinline__ TItem t_item(const Grid& g, const TPlan& tp, int item) {
+    const int kc = (int)tp.nbd.div((uint32_t)item), jb = item - kc * tp.NB;
+    TItem it;
+    it.j0 = jb * tp.H;
+    it.j1 = min(g.NY, it.j0 + tp.H);
+    it.k0 = (int)tp.cd.div((uint32_t)(kc * g.NZ));
+    it.k1 = (int)tp.cd.div((uint32_t)((kc + 1) * g.NZ));
+    return it;
+}
+// Aligned (even) start of the node range [a, b) and its byte count rounded up to 16.
+__device__ __forceinline__ int t_abeg(int a) { return a & ~1; }
+__device__ __forceinline__ unsigned t_bytes(int a, int b) { return (unsigned)((((b + 1) & ~1) - (a & ~1)) * 8); }
+
+// ---- producer ---------------------------------------------------------------------------
+// Sweep A stage of plane k: r, p_old rows [j0, min(j1 + 1, NY)); sweep B stage of plane k:
+// p rows [max(j0 - 1, 0), min(j1 + 1, NY)), plus x, r rows [j0, j1) on centre planes.
+template <bool SWEEP_B>
+__device__ void t_produce(const Grid& g, const TPlan& tp, double* sm, uint64_t* full, uint64_t* empty,
+                          int* s_item, unsigned* ctr, uint32_t& t, bool first, const double* r,
+                          const double* pold, const double* pc, const double* x) {
+    const int NXY = g.NX * g.NY;
+    unsigned next = atomicAdd(ctr, 1u);
+    while (true) {
+        const int item = (int)next;
+        if (item >= tp.I) {
+            unsigned ph;
+            const int s = t_slot(tp, t, ph);
+            mbar_wait(&empty[s], ph ^ 1);
+            s_item[s] = -1;
+            mbar_arrive(&full[s]);
+            ++t;
+            return;
+        }
+        next = atomicAdd(ctr, 1u);       // the next item's id arrives while this one streams
+        const TItem it = t_item(g, tp, item);
+        const int ks = SWEEP_B ? max(it.k0 - 1, 0) : it.k0;
+        const int ke = min(it.k1, g.NZ - 1);
+        for (int k = ks; k <= ke; ++k) {
+            unsigned ph;
+            const int s = t_slot(tp, t, ph);
+            mbar_wait(&empty[s], ph ^ 1);
+            if (k == ks) s_item[s] = item;
+            double* st = sm + (size_t)s * tp.stage;
+            if (!SWEEP_B) {
+                const int a = k * NXY + it.j0 * g.NX, b = k * NXY + min(it.j1 + 1, g.NY) * g.NX;
+                const unsigned nb = t_bytes(a, b);
+                mbar_arrive_tx(&full[s], first ? nb : 2 * nb);
+                bulk_g2s(st, r + t_abeg(a), nb, &full[s]);
+                if (!first) bulk_g2s(st + tp.RA, pold + t_abeg(a), nb, &full[s]);
+            } else {
+                const int a = k * NXY + max(it.j0 - 1, 0) * g.NX, b = k * NXY + min(it.j1 + 1, g.NY) * g.NX;
+                const unsigned nb = t_bytes(a, b);
+                const bool centre = k >= it.k0 && k < it.k1;
+                const int c = k * NXY + it.j0 * g.NX, d = k * NXY + it.j1 * g.NX;
+                const unsigned nc = centre ? t_bytes(c, d) : 0u;
+                mbar_arrive_tx(&full[s], nb + 2 * nc);
+                bulk_g2s(st, pc + t_abeg(a), nb, &full[s]);
+                if (centre) {
+                    bulk_g2s(st + tp.RB, x + t_abeg(c), nc, &full[s]);
+                    bulk_g2s(st + tp.RB + tp.RX, r + t_abeg(c), nc, &full[s]);
+                }
+            }
+            ++t;
+        }
+    }
+}
+
+// Ring cursor: position t, its slot and phase parity, advanced without divisions.
+struct TRing {
+    uint32_t t;
+    int s;
+    unsigned ph;
+    __device__ __forceinline__ void set(const TPlan& tp, uint32_t u) {
+        t = u;
+        s = t_slot(tp, u, ph);
+    }
+    __device__ __forceinline__ void adv(const TPlan& tp) {
+        ++t;
+        if (++s == tp.NS) { s = 0; ph ^= 1u; }
+    }
+    __device__ __forceinline__ TRing next(const TPlan& tp) const {
+        TRing r = *this;
+        r.adv(tp);
+        return r;
+    }
+};
+// Consumer-side release of a stage (one arrival per warp) and wait for a full stage.
+__device__ __forceinline__ void t_release(uint64_t* empty, const TRing& r) {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[r.s]);
+}
+__device__ __forceinline__ void t_wait_full(uint64_t* full, const TRing& r) { mbar_wait(&full[r.s], r.ph); }
+
+// Per-item fixed-order reduction of NV values over the NCW consumer warps; warp 0 lane 0
+// writes part[v * I + item].
+template <int NV, int NCW>
+__device__ __forceinline__ void t_item_sum(double (&v)[NV], double (*ired)[32], double* part, int I, int item) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] = warp_sum(v[k]);
+    if (lane == 0)
+#pragma unroll
+        for (int k = 0; k < NV; ++k) ired[k][w] = v[k];
+    asm volatile("bar.sync 1, %0;" ::"r"(NCW * 32) : "memory");
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            double s = 0.0;
+#pragma unroll
+            for (int u = 0; u < NCW; ++u) s += ired[k][u];
+            part[k * I + item] = s;
+        }
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(NCW * 32) : "memory");
+}
+
+// The ring lives in dynamic shared memory; helpers index it through this symbol so that
+// every access compiles to LDS.
+extern __shared__ __align__(128) double t_sm[];
+
+// Sweep A value of p at node q (plane offset o: t_sm[o + q] = r[q], t_sm[o + RA + q] = p_old[q]).
+__device__ __forceinline__ double t_pv(int o, int RA, int q, double iv, bool first, double beta) {
+    const double z = __dmul_rn(iv, t_sm[o + q]);
+    return first ? z : __dadd_rn(__dmul_rn(beta, t_sm[o + RA + q]), z);
+}
+
+// Per-item node table of a consumer thread: node m of every plane of the item sits at
+// offset off[m] inside the plane, with its x/y class part cxy[m] = cx + 3 cy, the class
+// steps to its x+ / y+ neighbours and flag bits (below).  Every node then runs the same
+// branch-free code: no warp of the CTA is slowed by boundary nodes (the empty barrier of
+// a stage waits for the slowest warp).
+enum : unsigned { kFOk = 1, kFXm = 2, kFXp = 4, kFYm = 8, kFYp = 16, kFCol = 32 };
+template <int NPT, int NT>
+struct TNodes {
+    int off[NPT], cxy[NPT], dxp[NPT], dyp[NPT];
+    unsigned fl[NPT];
+    __device__ __forceinline__ void init(const Grid& g, const TItem& it) {
+        const int nn = (it.j1 - it.j0) * g.NX;
+        // free (non-Dirichlet) node of x/y classes (a, b) on a plane with cz >= 1
+        auto freec = [&](int a, int b) { return !class_is_dirichlet(a + 3 * b + 9, g.dkind); };
+#pragma unroll
+        for (int m = 0; m < NPT; ++m) {
+            const int e = threadIdx.x + m * NT;
+            const int jj = (int)g.divX.div((uint32_t)e);
+            const int i = e - jj * g.NX, j = it.j0 + jj;
+            off[m] = i + g.NX * j;
+            const int cx = axis_class(i, g.nc[0]), cy = axis_class(j, g.nc[1]);
+            cxy[m] = cx + 3 * cy;
+            const int cxn = i < g.nc[0] ? axis_class(i + 1, g.nc[0]) : cx;
+            const int cyn = j < g.nc[1] ? axis_class(j + 1, g.nc[1]) : cy;
+            dxp[m] = cxn - cx;
+            dyp[m] = 3 * (cyn - cy);
+            unsigned f = e < nn ? kFOk : 0u;
+            if (i > 0 && freec(axis_class(i - 1, g.nc[0]), cy)) f |= kFXm;
+            if (i < g.nc[0] && freec(cxn, cy)) f |= kFXp;
+            if (j > 0 && freec(cx, axis_class(j - 1, g.nc[1]))) f |= kFYm;
+            if (j < g.nc[1] && freec(cx, cyn)) f |= kFYp;
+            if (freec(cx, cy)) f |= kFCol;
+            fl[m] = f;
+        }
+    }
+};
+
+// ---- consumers: sweep A ------------------------------------------------------------------
+// p = z (+ beta p_old) and its p.Ap contribution over the node and its free forward
+// neighbours (s_sweep_a_node, one expression for every class).
+template <int NCW, int NPT>
+__device__ void t_consume_a(const Grid& g, const TPlan& tp, const ClassTable& T, uint64_t* full, uint64_t* empty,
+                            const int* s_item, uint32_t& t, bool first, double beta, double* __restrict__ pnew,
+                            double* part, double (*ired)[32]) {
+    const int NXY = g.NX * g.NY, sy = g.NX, RA = tp.RA;
+    constexpr int NT = NCW * 32;
+    TRing cur;
+    cur.set(tp, t);
+    while (true) {
+        t_wait_full(full, cur);
+        const int item = s_item[cur.s];
+        if (item < 0) { t_release(empty, cur); cur.adv(tp); t = cur.t; return; }
+        const TItem it = t_item(g, tp, item);
+        TNodes<NPT, NT> nd;
+        nd.init(g, it);
+        double acc[1] = {0.0};
+        for (int k = it.k0; k < it.k1; ++k) {
+            const bool nxt = k + 1 < g.NZ;
+            const TRing nx = cur.next(tp);
+            if (nxt) t_wait_full(full, nx);
+            const int kb = k * NXY;
+            const int s0 = cur.s * tp.stage - t_abeg(kb + it.j0 * g.NX);
+            const int o1 = nxt ? nx.s * tp.stage - t_abeg(kb + NXY + it.j0 * g.NX) : 0;
+            const int cz = axis_class(k, g.nc[2]);
+            const int dzp = nxt ? 9 * (axis_class(k + 1, g.nc[2]) - cz) : 0;
+#pragma unroll
+            for (int m = 0; m < NPT; ++m) {
+                const unsigned f = nd.fl[m];
+                if (!(f & kFOk)) continue;
+                const int p = kb + nd.off[m];
+                const int cl = nd.cxy[m] + 9 * cz;
+                const double pp = t_pv(s0, RA, p, T.invd[cl], first, beta);
+                pnew[p] = pp;
+                double a;
+                if (T.nd[cl] == 0.0) {
+                    a = pp * pp;                         // identity row
+                } else {
+                    const double px = (f & kFXp) ? t_pv(s0, RA, p + 1, T.invd[cl + nd.dxp[m]], first, beta) : 0.0;
+                    const double py = (f & kFYp) ? t_pv(s0, RA, p + sy, T.invd[cl + nd.dyp[m]], first, beta) : 0.0;
+                    const double pz = (nxt && (f & kFCol)) ? t_pv(o1, RA, p + NXY, T.invd[cl + dzp], first, beta) : 0.0;
+                    a = pp * (T.diag[cl] * pp - 2.0 * ((T.c[0][cl] * px + T.c[1][cl] * py) + T.c[2][cl] * pz));
+                }
+                acc[0] += a;
+            }
+            t_release(empty, cur);
+            cur.adv(tp);
+        }
+        if (it.k1 < g.NZ) { t_release(empty, cur); cur.adv(tp); }    // the forward plane k1
+        t_item_sum<1, NCW>(acc, ired, part, tp.I, item);
+        t = cur.t;
+    }
+}
+
+// ---- consumers: sweep B ------------------------------------------------------------------
+// q = A_c p (apply_free, one expression for every class), x += alpha p, r -= alpha q.
+// Holds stages k and k+1; the p values of plane k-1 at the thread's own nodes (its z
+// neighbour below) are the centre values of the previous plane, kept in registers.
+template <int NCW, int NPT>
+__device__ void t_consume_b(const Grid& g, const TPlan& tp, const ClassTable& T, uint64_t* full, uint64_t* empty,
+                            const int* s_item, uint32_t& t, double alpha, double* __restrict__ x,
+                            double* __restrict__ r, double* part, double (*ired)[32]) {
+    const int NXY = g.NX * g.NY, sy = g.NX, RX = tp.RX;
+    constexpr int NT = NCW * 32;
+    TRing cur;
+    cur.set(tp, t);
+    while (true) {
+        t_wait_full(full, cur);
+        const int item = s_item[cur.s];
+        if (item < 0) { t_release(empty, cur); cur.adv(tp); t = cur.t; return; }
+        const TItem it = t_item(g, tp, item);
+        TNodes<NPT, NT> nd;
+        nd.init(g, it);
+        const int jlo = max(it.j0 - 1, 0);
+        double prev[NPT];
+        if (it.k0 > 0) {          // halo plane k0 - 1: only the own-node values are needed
+            const int kb = (it.k0 - 1) * NXY;
+            const int om = cur.s * tp.stage - t_abeg(kb + jlo * g.NX);
+#pragma unroll
+            for (int m = 0; m < NPT; ++m) prev[m] = (nd.fl[m] & kFOk) ? t_sm[om + kb + nd.off[m]] : 0.0;
+            t_release(empty, cur);
+            cur.adv(tp);
+        } else {
+#pragma unroll
+            for (int m = 0; m < NPT; ++m) prev[m] = 0.0;
+        }
+        double acc[2] = {0.0, 0.0};
+        for (int k = it.k0; k < it.k1; ++k) {
+            const bool nxt = k + 1 < g.NZ;
+            const TRing nx = cur.next(tp);
+            t_wait_full(full, cur);
+            if (nxt) t_wait_full(full, nx);
+            const int kb = k * NXY;
+            const int oc = cur.s * tp.stage - t_abeg(kb + jlo * g.NX);
+            const int op = nxt ? nx.s * tp.stage - t_abeg(kb + NXY + jlo * g.NX) : 0;
+            const int ox = cur.s * tp.stage + tp.RB - t_abeg(kb + it.j0 * g.NX);
+            const int cz9 = 9 * axis_class(k, g.nc[2]);
+            const bool zm_ok = k >= 2, zp_ok = nxt;
+#pragma unroll
+            for (int m = 0; m < NPT; ++m) {
+                const unsigned f = nd.fl[m];
+                if (!(f & kFOk)) continue;
+                const int p = kb + nd.off[m];
+                const int cl = nd.cxy[m] + cz9;
+                const double pp = t_sm[oc + p];
+                double qv;
+                if (T.nd[cl] == 0.0) {
+                    qv = pp;                              // identity row
+                } else {
+                    const double xm = (f & kFXm) ? t_sm[oc + p - 1] : 0.0;
+                    const double xp = (f & kFXp) ? t_sm[oc + p + 1] : 0.0;
+                    const double ym = (f & kFYm) ? t_sm[oc + p - sy] : 0.0;
+                    const double yp = (f & kFYp) ? t_sm[oc + p + sy] : 0.0;
+                    const double zm = (zm_ok && (f & kFCol)) ? prev[m] : 0.0;
+                    const double zp = (zp_ok && (f & kFCol)) ? t_sm[op + p + NXY] : 0.0;
+                    qv = T.diag[cl] * pp - ((T.c[0][cl] * (xm + xp) + T.c[1][cl] * (ym + yp)) + T.c[2][cl] * (zm + zp));
+                }
+                const double iv = T.invd[cl];
+                const double xv = __dadd_rn(t_sm[ox + p], __dmul_rn(alpha, pp));
+                const double rv = __dsub_rn(t_sm[ox + RX + p], __dmul_rn(alpha, qv));
+                x[p] = xv;
+                r[p] = rv;
+                acc[0] += rv * __dmul_rn(iv, rv);
+                acc[1] += rv * rv;
+                prev[m] = pp;
+            }
+            t_release(empty, cur);
+            cur.adv(tp);
+        }
+        if (it.k1 < g.NZ) { t_release(empty, cur); cur.adv(tp); }   // the forward halo plane k1
+        t_item_sum<2, NCW>(acc, ired, part, tp.I, item);
+        t = cur.t;
+    }
+}
+
+// Fixed-order sum of I item partials per value by the whole CTA (every CTA bitwise equal):
+// thread t adds items t, t + B, ... in order (loads batched), then the deterministic
+// block_sum.
+template <int NV>
+__device__ __forceinline__ void t_grid_sum(const double* part, int I, double* red, double* out) {
+    const int B = blockDim.x;
+    double s[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+        double acc = 0.0;
+        int b = threadIdx.x;
+        for (; b + 3 * B < I; b += 4 * B) {
+            const double v0 = __ldcg(part + k * I + b), v1 = __ldcg(part + k * I + b + B);
+            const double v2 = __ldcg(part + k * I + b + 2 * B), v3 = __ldcg(part + k * I + b + 3 * B);
+            acc += v0; acc += v1; acc += v2; acc += v3;
+        }
+        for (; b < I; b += B) acc += __ldcg(part + k * I + b);
+        s[k] = acc;
+    }
+    block_sum<NV>(s, red);
+    if (threadIdx.x == 0)
+#pragma unroll
+        for (int k = 0; k < NV; ++k) out[k] = s[k];
+    __syncthreads();
+}
+
+// ---- k_t_cg: the CG iterations (cooperative, one CTA per SM, NCW + 1 warps). ----------
+// Reads k_s_rhs's Grhs partials; writes the same SolveInfoDev fields as k_s_cg.
+template <int NCW, int NPT>
+__global__ void __launch_bounds__((NCW + 1) * 32, 1) k_t_cg(PcgParams P, int Grhs, TPlan tp) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ ClassTable T;
+    __shared__ double red[2 * 32];
+    __shared__ double tot[2];
+    __shared__ double ired[2][32];
+    __shared__ __align__(8) uint64_t full[kTMaxStages], empty[kTMaxStages];
+    __shared__ int s_item[kTMaxStages];
+    const Grid& g = P.g;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < tp.NS; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NCW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    build_class_table(T, threadIdx.x, P.mbase, P.cbase, g.dkind);
+    {
+        const int s[2] = {0, 1};
+        grid_sum_wide<2>(P.part, s, Grhs, red, tot);   // also syncs T and the barriers
+    }
+    const bool producer = (threadIdx.x >> 5) == NCW;
+    const bool plane0 = producer && (threadIdx.x & 31) == 0;
+    unsigned* ctr = reinterpret_cast<unsigned*>(P.part + kTCounter);
+    double* part = P.part + kTPartItems;
+    const double bb = tot[0];
+    double rz = tot[1];
+    const double bnorm = sqrt(bb);
+    const double atol = P.rtol * bnorm;
+    double rnorm = bnorm;
+    int it = 0, status = 0;
+    double rho_prev = 1.0;
+    double* pold = P.p0;
+    double* pnew = P.p1;
+    uint32_t t = 0;          // ring position (identical sequence on producer and consumers)
+    unsigned seq = 0;        // sweep sequence number (counter slot seq & 3)
+    if (bb != 0.0) {
+        while (true) {
+            if (rnorm < atol) { status = 0; break; }
+            if (!isfinite(rnorm)) { status = 3; break; }
+            if (it >= P.maxiter) { status = 1; break; }
+            const double rho = rz;
+            const double beta = it > 0 ? rho / rho_prev : 0.0;
+            const bool first = it == 0;
+            // ---- sweep A ----
+            if (blockIdx.x == 0 && threadIdx.x == 0) ctr[(seq + 2) & 3] = 0u;
+            if (producer) {
+                if (plane0) t_produce<false>(g, tp, t_sm, full, empty, s_item, ctr + (seq & 3), t, first, P.r, pold,
+                                             nullptr, nullptr);
+            } else {
+                t_consume_a<NCW, NPT>(g, tp, T, full, empty, s_item, t, first, beta, pnew, part, ired);
+                fence_proxy_async_global();
+            }
+            ++seq;
+            grid.sync();
+            t = __shfl_sync(0xffffffffu, t, 0);     // producer warp: lane 0 holds the position
+            fence_proxy_async_global();
+            t_grid_sum<1>(part, tp.I, red, tot);
+            const double alpha = rho / tot[0];
+            // ---- sweep B ----
+            if (blockIdx.x == 0 && threadIdx.x == 0) ctr[(seq + 2) & 3] = 0u;
+            if (producer) {
+                if (plane0) t_produce<true>(g, tp, t_sm, full, empty, s_item, ctr + (seq & 3), t, false, P.r, nullptr,
+                                            pnew, P.T);
+            } else {
+                t_consume_b<NCW, NPT>(g, tp, T, full, empty, s_item, t, alpha, P.T, P.r, part, ired);
+                fence_proxy_async_global();
+            }
+            ++seq;
+            grid.sync();
+            t = __shfl_sync(0xffffffffu, t, 0);
+            fence_proxy_async_global();
+            t_grid_sum<2>(part, tp.I, red, tot);
+            rz = tot[0];
+            rnorm = sqrt(tot[1]);
+            rho_prev = rho;
+            double* tmp = pold; pold = pnew; pnew = tmp;
+            ++it;
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        P.info->iterations = (status == 1) ? P.maxiter : it;
+        P.info->status = status;
+        P.info->bnorm = bnorm;
+        P.info->rnorm = rnorm;
+    }
+}
+
+}  // namespace tl

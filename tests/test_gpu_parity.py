@@ -357,10 +357,14 @@ np.savez({out!r}, g=state.global_field.values, l=state.local_field.values,
 
 
 @pytest.mark.parametrize("env", [{"TLGPU_MULTI": "0"}, {"TLGPU_NOCACHE": "1", "TLGPU_CGSYNC": "1"},
-                                 {"TLGPU_EXACT_CG": "1"}])
+                                 {"TLGPU_EXACT_CG": "1"},
+                                 {"TLGPU_STREAMING": "1", "TLGPU_TILED_MIN": "1"},
+                                 {"TLGPU_STREAMING": "1", "TLGPU_TILED": "0"}])
 def test_alternative_solver_modes_match_default(env, tmp_path):
     """The non-default device paths (one launch per local solve; no setup cache and
-    cg::grid.sync barriers; scipy-exact two-barrier kernel) give the default run's fields
+    cg::grid.sync barriers; scipy-exact two-barrier kernel; every solve on the streaming
+    path, with the bulk-copy z-march CG loop k_t_cg or the flat k_s_cg, on grids small
+    enough that boundary nodes dominate) give the default run's fields
     to CG rounding with the same counters (env switches are read once per process, so
     each mode runs in a subprocess)."""
     import os
@@ -378,3 +382,67 @@ def test_alternative_solver_modes_match_default(env, tmp_path):
     a, b = runs["default"], runs["mode"]
     assert rel(b["g"], a["g"]) <= 1e-12 and rel(b["l"], a["l"]) <= 1e-12
     np.testing.assert_array_equal(a["c"], b["c"])
+
+
+_TILED_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import paper_2110_12932_b200 as P
+from paper_2110_12932_b200 import _native as N, ops
+cfg = P.load_config({cfg!r})
+problem, lm = P.build_problem(cfg)
+rng = np.random.default_rng(0)
+if {level!r} == "global":
+    grid = problem.global_mesh
+    T = rng.uniform(293.0, 2293.0, grid.n_nodes)
+    pts, pw = problem.global_source(0.0, cfg.dt_macro)
+    load = ops.deposit_load(grid, pts, pw)
+    x, info = ops.step(grid, 9.8, 8440 * 410.0, cfg.dt_macro, N.TL_DIRICHLET_BOTTOM, T, g_const=293.0,
+                       load=load, rtol=1e-12)
+else:
+    T = rng.uniform(293.0, 2293.0, lm.n_nodes)
+    g = np.where(lm.gamma_mask(), rng.uniform(293.0, 900.0, lm.n_nodes), 0.0)
+    src = problem.local_source(2e-6)
+    x, info = ops.step(lm, 9.8, 8440 * 410.0, cfg.dt_macro / cfg.micro_steps, N.TL_DIRICHLET_GAMMA, T, g=g,
+                       gaussian=src.device_args(), rtol=1e-12)
+np.savez({out!r}, x=x, its=info.iterations, status=info.status)
+"""
+
+
+@pytest.mark.parametrize("level", ["global", "local"])
+def test_tiled_cg_loop_cfg3_size_vs_oracle(level, tmp_path):
+    """The bulk-copy z-march CG loop (k_t_cg, default on grids of 20M+ nodes) forced onto
+    the cfg3 grids (6.9M nodes, bottom Dirichlet + deposit; 1.73M nodes, gamma Dirichlet +
+    Gaussian): one implicit step vs the oracle, iterations +-1, and vs the flat k_s_cg."""
+    import os
+    import subprocess
+    import sys
+    cfgp = CONFIGS / "cfg3.cfg"
+    out = {}
+    for tag, extra in (("tiled", {"TLGPU_TILED_MIN": "1"}), ("flat", {"TLGPU_TILED": "0"})):
+        path = tmp_path / f"{tag}.npz"
+        code = _TILED_SCRIPT.format(root=str(ROOT), cfg=str(cfgp), level=level, out=str(path))
+        res = subprocess.run([sys.executable, "-c", code], env={**os.environ, **extra},
+                             capture_output=True, text=True, timeout=900)
+        assert res.returncode == 0, res.stderr[-2000:]
+        out[tag] = np.load(path)
+    cfg = P.load_config(cfgp)
+    problem, lm = P.build_problem(cfg)
+    rng = np.random.default_rng(0)
+    if level == "global":
+        grid = problem.global_mesh
+        T = rng.uniform(293.0, 2293.0, grid.n_nodes)
+        pts, pw = problem.global_source(0.0, cfg.dt_macro)
+        load = ops.deposit_load(grid, pts, pw)
+        ref, its = _oracle_step(grid, N.TL_DIRICHLET_BOTTOM, T, cfg.dt_macro, np.full(grid.n_nodes, 293.0),
+                                load=load)
+    else:
+        T = rng.uniform(293.0, 2293.0, lm.n_nodes)
+        g = np.where(lm.gamma_mask(), rng.uniform(293.0, 900.0, lm.n_nodes), 0.0)
+        src = problem.local_source(2e-6)
+        ref, its = _oracle_step(lm, N.TL_DIRICHLET_GAMMA, T, cfg.dt_macro / cfg.micro_steps, g,
+                                gauss=(cfg.beam, src.center))
+    t = out["tiled"]
+    assert int(t["status"]) == 0 and abs(int(t["its"]) - its) <= 1
+    assert rel(t["x"], ref) <= 1e-12
+    assert int(t["its"]) == int(out["flat"]["its"]) and rel(t["x"], out["flat"]["x"]) <= 1e-13

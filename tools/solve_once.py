@@ -2,7 +2,7 @@
 """One (or a few) device solves of a BASELINE grid through ops.step, for ncu captures.
 
     python tools/solve_once.py cfg3 global [repeats]
-    python tools/solve_once.py cfg3 local  [repeats]
+    python tools/solve_once.py cfg3 local  [repeats] [save.npy]
 """
 import sys
 import time
@@ -36,5 +36,7 @@ for r in range(reps):
         dt = cfg.dt_macro / cfg.micro_steps
         x, info = ops.step(lm, 9.8, 8440 * 410.0, dt, N.TL_DIRICHLET_GAMMA, T, g=g,
                            gaussian=src.device_args(), rtol=1e-12)
+    if len(sys.argv) > 4 and r == reps - 1:
+        np.save(sys.argv[4], x)
     print(f"{cfgname} {level} rep {r}: status {info.status} its {info.iterations} "
           f"true_resid {info.true_resid:.3e} wall {time.time() - t:.2f}s")
