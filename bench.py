@@ -364,15 +364,29 @@ def main():
                 "share_of_step": ms / dev_ms if world == 1 else None}
 
     kloc, kglo = kstats(loc, Nl), kstats(glo, Ng)
-    traffic = None
+    # the dominant kernel: the level whose solves take the larger share of the step
+    lev = "global" if kglo and (not kloc or sum(t for t, _ in glo) > sum(t for t, _ in loc)) else "local"
+    kdom, ndom = (kglo, Ng) if lev == "global" else (kloc, Nl)
+    streaming = "k_s_rhs -> k_t_cg (bulk-copy z-march CG loop, grids of 20M+ nodes) or k_s_cg -> k_s_resid -> k_s_final"
+    kname = {"local": ("local-grid PCG solve: k_pcg_resident_cg (SMEM-resident bricks, all micro solves + corrector "
+                       "of a macro step in one launch) where the grid fits on chip, else the streaming " + streaming),
+             "global": "global-grid PCG solve: k_pcg_resident(_cg) where the grid fits on chip, else the streaming "
+                       + streaming}[lev]
+    traffic, tnote = None, None
     tfile = ROOT / "profiles" / "traffic.json"
     if tfile.exists():
-        traffic = json.loads(tfile.read_text()).get(f"{args.config}_local_pcg_dram_bytes_per_launch")
-    roofline = {"bound": "hbm", "achieved": kloc["achieved_gbs"], "peak": peak, "unit": "GB/s",
-                "frac": kloc["achieved_gbs"] / peak, "traffic": traffic,
-                "kernel": ("local-grid PCG solve: k_pcg_resident_cg (SMEM-resident bricks, all micro solves + "
-                           "corrector of a macro step in one launch) where the grid fits on chip, else the "
-                           "streaming k_s_rhs / k_s_cg / k_s_resid / k_s_final"),
+        tj = json.loads(tfile.read_text())
+        dram = tj.get(f"{args.config}_{lev}_pcg_dram_bytes_per_launch")
+        alg = tj.get(f"{args.config}_{lev}_pcg_alg_bytes_per_launch")
+        if dram and alg:
+            # ncu's launch may run another iteration count: scale its DRAM/algorithmic ratio
+            # to this run's algorithmic bytes per launch
+            per_launch = kdom["alg_bytes_per_solve"] * kdom["solves"] / kdom["launches"]
+            traffic = dram / alg * per_launch
+            tnote = f"ncu DRAM/algorithmic = {dram / alg:.3f} ({tj.get(f'{args.config}_{lev}_pcg_kernel', '')})"
+    roofline = {"bound": "hbm", "achieved": kdom["achieved_gbs"], "peak": peak, "unit": "GB/s",
+                "frac": kdom["achieved_gbs"] / peak, "traffic": traffic, "traffic_note": tnote,
+                "kernel": kname, "level": lev, "nodes": ndom,
                 "peak_source": peak_src,
                 "note": "algorithmic bytes N(64k+32) per solve (SURVEY §8d); cfg2 vectors are L2-resident"}
 
