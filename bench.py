@@ -130,7 +130,7 @@ def cpu_sample(cfg_path: Path, what: str = "global+local"):
     run.solve_local(L, Tl, 0.0, sched.t_micro(0, 1), (1.0 - w) * run.trace_of(L, Tg) + w * trace)
     dof += L.n_nodes
     dt = time.perf_counter() - t0
-    return dof, dt, run.iterations
+    return dof, dt, run.iterations, (run.G.n_nodes, L.n_nodes, sched.micro_per_macro)
 
 
 def _host_threads() -> int:
@@ -147,7 +147,7 @@ def reference_arm(args):
     cfg_path = ROOT / "configs" / f"{args.config}.cfg"
     times, dofs = [], []
     for s in range(args.warmup + args.steps):
-        dof, dt, _ = cpu_sample(cfg_path, what="local")
+        dof, dt, _, (Ng, Nl, m) = cpu_sample(cfg_path, what="local")
         if s >= args.warmup:
             times.append(dt)
             dofs.append(dof)
@@ -158,9 +158,13 @@ def reference_arm(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic (BASELINE {args.config} geometry; uniform initial field, first micro step)",
-        "config": {"workload": f"{args.config}: one local micro solve per step", "config_file": f"configs/{args.config}.cfg"},
+        # the same workload as the device arm; each timed step is a bounded sample of it
+        "config": {"workload": f"{args.config}: two-level multirate macro step (1 global + {m} local "
+                               f"solves + corrector), global {Ng} + local {Nl} nodes",
+                   "config_file": f"configs/{args.config}.cfg", "dof_timesteps_per_step": Ng + m * Nl,
+                   "parallelism": "host CPU"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": _host_threads(), "kind": "port",
-                         "sample": f"one {args.config} local micro solve per step via the literal "
+                         "sample": f"one {args.config} local micro solve ({Nl} DOF-timesteps) per timed step via the literal "
                                    "P1-assembly + scipy-CG port (oracle/assembly.py, bitwise equal to lpbfsim); "
                                    "library-default threading (BLAS may use every host thread; scipy's sparse "
                                    "CG itself is single-threaded)"},
@@ -446,7 +450,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        dof, dt, its = cpu_sample(cfg_path)
+        dof, dt, its, _ = cpu_sample(cfg_path)
         cpu = {"value": dof / dt, "unit": UNIT, "cores": 1, "kind": "port",
                "sample": f"one global + one local implicit step of {args.config} ({dof} DOF-timesteps, "
                          f"{dt:.1f} s) via the literal P1-assembly + scipy-CG port (oracle/assembly.py, "

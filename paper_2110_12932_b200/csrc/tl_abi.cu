@@ -173,21 +173,26 @@ static bool tiled_plan(const tl::Grid& g, int sms, tl::TPlan& tp, size_t& smem) 
     const size_t cap = 220 * 1024;
     tp.NS = (int)std::min<size_t>(tl::kTMaxStages, cap / ((size_t)tp.stage * 8));
     if (tp.NS < 4) return false;
-    // z chunk: about a tenth of a CTA's share of the sweep per item (dynamic balance),
-    // at least TLGPU_TZ planes (default 3)
+    // z chunks of about a tenth of a CTA's share of the sweep per item (at least TLGPU_TZ
+    // planes; measured: a guided tail of 1- and 2-plane items was slower, the per-item
+    // halo planes and reductions cost more than the shorter tail saves)
     int zmin = 3;
     if (const char* e = getenv("TLGPU_TZ")) zmin = std::max(1, atoi(e));
     const double share = (double)g.n / sms;
     int Z = (int)(share / (10.0 * H * NX));
     Z = std::max(zmin, std::min(Z, g.NZ));
-    int C = (g.NZ + Z - 1) / Z;
-    C = std::min(C, std::max(1, 7000 / tp.NB));
-    tp.C = C;
-    tp.I = tp.NB * C;
+    std::vector<int> cz;
+    const int nch = std::max(1, (g.NZ + Z - 1) / Z);
+    for (int c = 0; c < nch; ++c) cz.push_back(g.NZ * (c + 1) / nch - g.NZ * c / nch);
+    if ((int)cz.size() > tl::kTMaxChunks) return false;
+    tp.C = (int)cz.size();
+    tp.I = tp.NB * tp.C;
     if (tp.I > 7000) return false;
+    tp.kb[0] = 0;
+    for (int c = 0; c < tp.C; ++c) tp.kb[c + 1] = (short)(tp.kb[c] + cz[c]);
+    if (tp.kb[tp.C] != g.NZ) return false;
     tp.nsd.init(tp.NS);
     tp.nbd.init(tp.NB);
-    tp.cd.init(tp.C);
     smem = (size_t)tp.NS * tp.stage * 8;
     return true;
 }

@@ -34,6 +34,7 @@
 namespace tl {
 
 constexpr int kTMaxStages = 16;
+constexpr int kTMaxChunks = 96;            // z chunks (guided: large first, small last)
 constexpr int kTPartItems = 4096;          // offset of the item partials in PcgParams::part
 constexpr int kTCounter = 2048;            // offset (in doubles) of the 4 sweep counters
 
@@ -46,7 +47,8 @@ struct TPlan {
     int stage;      // doubles per stage
     int RA;         // sweep A: r at [0, RA), p_old at [RA, 2 RA)
     int RB, RX;     // sweep B: p at [0, RB), x at [RB, RB + RX), r at [RB + RX, RB + 2 RX)
-    FastDiv nsd, nbd, cd;   // division by NS, NB, C
+    FastDiv nsd, nbd;       // division by NS, NB
+    short kb[kTMaxChunks + 1];   // chunk kc = planes [kb[kc], kb[kc + 1])
 };
 
 // Ring slot of position u; parity of its phase in *ph.
@@ -107,8 +109,8 @@ __device__ __forceinline__ TItem t_item(const Grid& g, const TPlan& tp, int item
     TItem it;
     it.j0 = jb * tp.H;
     it.j1 = min(g.NY, it.j0 + tp.H);
-    it.k0 = (int)tp.cd.div((uint32_t)(kc * g.NZ));
-    it.k1 = (int)tp.cd.div((uint32_t)((kc + 1) * g.NZ));
+    it.k0 = tp.kb[kc];
+    it.k1 = tp.kb[kc + 1];
     return it;
 }
 // Aligned (even) start of the node range [a, b) and its byte count rounded up to 16.
@@ -123,7 +125,9 @@ __device__ void t_produce(const Grid& g, const TPlan& tp, double* sm, uint64_t* 
                           int* s_item, unsigned* ctr, uint32_t& t, bool first, const double* r,
                           const double* pold, const double* pc, const double* x) {
     const int NXY = g.NX * g.NY;
-    unsigned next = atomicAdd(ctr, 1u);
+    // the first item of every CTA is static (no counter round trip at the sweep start);
+    // the rest come from the counter, offset by the grid size
+    unsigned next = blockIdx.x;
     while (true) {
         const int item = (int)next;
         if (item >= tp.I) {
@@ -135,7 +139,7 @@ __device__ void t_produce(const Grid& g, const TPlan& tp, double* sm, uint64_t* 
             ++t;
             return;
         }
-        next = atomicAdd(ctr, 1u);       // the next item's id arrives while this one streams
+        next = gridDim.x + atomicAdd(ctr, 1u);   // the next item's id arrives while this one streams
         const TItem it = t_item(g, tp, item);
         const int ks = SWEEP_B ? max(it.k0 - 1, 0) : it.k0;
         const int ke = min(it.k1, g.NZ - 1);
