@@ -269,6 +269,12 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
     }
 
   __shared__ SolveSpec S;                   // this solve's parameters (shared: no registers)
+  // MULTI: a solve's residual sums are reduced at the next solve's first grid barrier (one
+  // barrier less per solve); its outcome record is written then (thread 0 keeps it here)
+  __shared__ SolveInfoDev* pend_info;
+  __shared__ int pend_status, pend_it;
+  __shared__ double pend_bnorm, pend_rnorm;
+  if (threadIdx.x == 0) pend_info = nullptr;
   const int nsp = MULTI ? RP.nspec : 1;
   constexpr int kPS = MULTI ? 1 : 0;        // solve whose phases TLGPU_PROF stamps
   for (int si = 0; si < nsp; ++si) {
@@ -325,7 +331,7 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
         }
         P.b[p] = bv;
         RO[nl] = bv;
-        if (od_surf(od[m])) RP.xr[p] = bv;
+        if (od_surf(od[m])) RP.xw[(size_t)g.n + p] = bv;   // xr may still be read (previous tail)
         const double z = __dmul_rn(T.invd[cls], bv);
         acc[0] += bv * bv;
         acc[1] += bv * z;
@@ -340,6 +346,23 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
         grid_sum_fast<2>(P.part, s2, G, tot);
     }
     if (prof && si == kPS) RP.prof[np++] = global_ns();
+    if (MULTI && si > 0 && b == 0 && pend_info) {
+        // the previous solve's outcome: its residual partials (slots 4, 5) were published
+        // before this solve's first grid barrier
+        const int s2[2] = {4, 5};
+        grid_sum_fast<2>(P.part, s2, G, tot + 4);
+        if (b == 0 && threadIdx.x == 0) {
+            int st = pend_status;
+            const double tres = pend_bnorm > 0.0 ? sqrt(tot[4]) / pend_bnorm : 0.0;
+            if (st == 0 && tot[5] > 0.0) st = 3;
+            if (st == 0 && (!isfinite(tres) || tres > 1e2 * P.rtol)) st = 2;
+            pend_info->iterations = (st == 1) ? P.maxiter : pend_it;
+            pend_info->status = st;
+            pend_info->bnorm = pend_bnorm;
+            pend_info->rnorm = pend_rnorm;
+            pend_info->true_resid = tres;
+        }
+    }
     const double bb = tot[0];
     double gam = tot[1];                    // r0 . u0
     const double bnorm = sqrt(bb);
@@ -356,7 +379,7 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
         for (int t = 0; t < kResKF; ++t) {
             const int e = threadIdx.x + t * kResTPB;
             if (e < nface && FS[e] >= 0) {
-                const double rv = __ldcg(RP.xr + FG[e]);
+                const double rv = __ldcg(RP.xw + (size_t)g.n + FG[e]);
                 RF[e] = rv;
                 US[FS[e]] = __dmul_rn(T.invd[CL[FS[e]]], rv);
             }
@@ -540,6 +563,18 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
         __threadfence();
         fin = true;
         if (threadIdx.x == 0) *RP.tail_count = 0;
+    } else if (MULTI && si + 1 < nsp) {
+        if (threadIdx.x == 0) {
+            P.part[4 * G + b] = res[0];
+            P.part[5 * G + b] = res[1];
+            pend_info = S.info;
+            pend_status = status;
+            pend_it = it;
+            pend_bnorm = bnorm;
+            pend_rnorm = rnorm;
+        }
+        if (prof && si == kPS) { RP.prof[np++] = global_ns(); RP.prof[127] = np; }
+        continue;
     } else {
         if (threadIdx.x == 0) { P.part[0 * G + b] = res[0]; P.part[3 * G + b] = res[1]; }
         grid.sync();
