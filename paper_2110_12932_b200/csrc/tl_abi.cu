@@ -197,11 +197,9 @@ static bool tiled_plan(const tl::Grid& g, int sms, tl::TPlan& tp, size_t& smem) 
     return true;
 }
 
-static cudaError_t launch_t_cg(tl::PcgParams& P, int Gr, int sms, cudaStream_t st, bool& launched) {
+static cudaError_t launch_t_cg(tl::PcgParams& P, int Gr, int sms, cudaStream_t st, bool& launched,
+                               const tl::TPlan& tp, size_t smem) {
     launched = false;
-    tl::TPlan tp{};
-    size_t smem = 0;
-    if (!tiled_enabled() || !tiled_plan(P.g, sms, tp, smem)) return cudaSuccess;
     const int ncw = kTNCW;
     const bool two = tp.H * P.g.NX <= 2 * kTNCW * 32;
     auto kern = two ? tl::k_t_cg<kTNCW, 2> : tl::k_t_cg<kTNCW, 4>;
@@ -218,7 +216,7 @@ static cudaError_t launch_t_cg(tl::PcgParams& P, int Gr, int sms, cudaStream_t s
     if (per_sm < 1) return cudaSuccess;
     e = cudaMemsetAsync(P.part + tl::kTCounter, 0, 4 * sizeof(unsigned), st);
     if (e != cudaSuccess) return e;
-    void* args[] = {&P, &Gr, &tp};
+    void* args[] = {&P, &Gr, (void*)&tp};
     e = cudaLaunchCooperativeKernel((void*)kern, sms, (ncw + 1) * 32, args, smem, st);
     launched = e == cudaSuccess;
     return e;
@@ -228,10 +226,21 @@ static int launch_stream(tl::PcgParams& P, int sms, cudaStream_t st, int64_t* la
     const int minb = split_minb();
     if (minb == 0) return launch_pcg(P, false, sms, st, launches);
     const int Gr = 4 * sms;
+    tl::TPlan tp{};
+    size_t smem = 0;
+    const bool use_tiled = tiled_enabled() && tiled_plan(P.g, sms, tp, smem);
+    // k_t_cg takes r0 = b and x0 = 0 as implied: the RHS writes b only
+    P.light_rhs = use_tiled ? 1 : 0;
     tl::k_s_rhs<<<Gr, tl::kSTPB, 0, st>>>(P);
     cudaError_t e = cudaGetLastError();
     bool tiled = false;
-    if (e == cudaSuccess) e = launch_t_cg(P, Gr, sms, st, tiled);
+    if (e == cudaSuccess && use_tiled) e = launch_t_cg(P, Gr, sms, st, tiled, tp, smem);
+    if (e == cudaSuccess && use_tiled && !tiled) {
+        // no k_t_cg after all (occupancy): rebuild the RHS with r0 and x0 written
+        P.light_rhs = 0;
+        tl::k_s_rhs<<<Gr, tl::kSTPB, 0, st>>>(P);
+        e = cudaGetLastError();
+    }
     if (e == cudaSuccess && !tiled)
         e = minb == 2 ? launch_s_cg<2>(P, Gr, sms, st)
           : minb == 4 ? launch_s_cg<4>(P, Gr, sms, st)
@@ -240,9 +249,10 @@ static int launch_stream(tl::PcgParams& P, int sms, cudaStream_t st, int64_t* la
                        : launch_s_cg<3>(P, Gr, sms, st);
     if (e == cudaSuccess) {
         tl::k_s_resid<<<Gr, tl::kSTPB, 0, st>>>(P);
-        tl::k_s_final<<<Gr, tl::kSTPB, 0, st>>>(P, Gr);
+        tl::k_s_final<<<1, tl::kSTPB, 0, st>>>(P, Gr);
         e = cudaGetLastError();
     }
+    P.light_rhs = 0;
     if (e != cudaSuccess) return fail(TL_E_CUDA, std::string("streaming solve launch: ") + cudaGetErrorString(e));
     if (launches) *launches += 4;
     return TL_OK;

@@ -71,6 +71,7 @@ struct PcgParams {
     double rtol;
     int maxiter;
     SolveInfoDev* info;
+    int light_rhs;       // k_t_cg path: k_s_rhs writes b only (r0 = b and x0 = 0 are implied)
 };
 
 __device__ __forceinline__ double warp_sum(double v) {

@@ -7,8 +7,8 @@
 //
 //   k_s_rhs    constrained RHS b, r = b, x = 0, block partials of ||b||^2 and r.z
 //   k_s_cg     cooperative CG loop: sweep A | grid sync | sweep B | grid sync
-//   k_s_resid  ||A_c x - b|| and non-finite partials (fem.py:286)
-//   k_s_final  x_D = g (fem.py:289-290); block 0 sums the residual partials -> info
+//   k_s_resid  ||A_c x - b|| and non-finite partials (fem.py:286), then x_D = g (:289-290)
+//   k_s_final  one block sums the residual partials -> info
 //
 // Sweep A forms p = z + beta p_old and the alpha denominator p.Ap.  Instead of
 // recomputing p at all seven stencil points (14 loads per node), p.Ap is summed over the
@@ -80,8 +80,10 @@ __global__ void __launch_bounds__(kSTPB) k_s_rhs(PcgParams P) {
             bv += dirichlet_lift(P, T, p, i, j, k, cls);
         }
         P.b[p] = bv;
-        P.r[p] = bv;
-        P.T[p] = 0.0;
+        if (!P.light_rhs) {
+            P.r[p] = bv;
+            P.T[p] = 0.0;
+        }
         acc[0] += bv * bv;
         acc[1] += bv * __dmul_rn(T.invd[cls], bv);
     }
@@ -265,9 +267,13 @@ __global__ void __launch_bounds__(kSTPB) k_s_resid(PcgParams P) {
         const double xp = P.T[p];
         const double ax = (T.nd[cls] == 0.0) ? xp
                                              : apply_free(g, T, p, i, j, k, cls, xp, [&](int q, int) { return P.T[q]; });
-        const double d = ax - P.b[p];
+        const double bv = P.b[p];
+        const double d = ax - bv;
         res[0] += d * d;
         res[1] += isfinite(xp) ? 0.0 : 1.0;
+        // x_D = g = b_D (fem.py:289-290), after this node's own residual term; neighbours
+        // that read x_D here weight it by nd = 0, so either value gives the same sum
+        if (T.nd[cls] == 0.0) P.T[p] = bv;
     }
     block_sum<2>(res, red);
     if (threadIdx.x == 0) {
@@ -276,20 +282,10 @@ __global__ void __launch_bounds__(kSTPB) k_s_resid(PcgParams P) {
     }
 }
 
-// ---- k_s_final: x_D = g = b_D; block 0 turns the residual partials into the outcome ----
+// ---- k_s_final (one block): the residual partials -> the outcome record ----------------
 __global__ void __launch_bounds__(kSTPB) k_s_final(PcgParams P, int Gres) {
-    __shared__ ClassTable T;
     __shared__ double red[2 * 32];
     __shared__ double tot[2];
-    const Grid& g = P.g;
-    build_class_table(T, threadIdx.x, P.mbase, P.cbase, g.dkind);
-    __syncthreads();
-    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < g.n; p += gridDim.x * blockDim.x) {
-        int i, j, k;
-        decode(g, p, i, j, k);
-        if (T.nd[class_of(g, i, j, k)] == 0.0) P.T[p] = P.b[p];
-    }
-    if (blockIdx.x != 0) return;
     const int s[2] = {0, 1};
     grid_sum_wide<2>(P.part, s, Gres, red, tot);
     if (threadIdx.x == 0) {

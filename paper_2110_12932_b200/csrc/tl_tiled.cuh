@@ -119,7 +119,8 @@ __device__ __forceinline__ unsigned t_bytes(int a, int b) { return (unsigned)(((
 
 // ---- producer ---------------------------------------------------------------------------
 // Sweep A stage of plane k: r, p_old rows [j0, min(j1 + 1, NY)); sweep B stage of plane k:
-// p rows [max(j0 - 1, 0), min(j1 + 1, NY)), plus x, r rows [j0, j1) on centre planes.
+// p rows [max(j0 - 1, 0), min(j1 + 1, NY)), plus x, r rows [j0, j1) on centre planes
+// (x == nullptr: x = 0, not loaded).
 template <bool SWEEP_B>
 __device__ void t_produce(const Grid& g, const TPlan& tp, double* sm, uint64_t* full, uint64_t* empty,
                           int* s_item, unsigned* ctr, uint32_t& t, bool first, const double* r,
@@ -161,10 +162,10 @@ __device__ void t_produce(const Grid& g, const TPlan& tp, double* sm, uint64_t* 
                 const bool centre = k >= it.k0 && k < it.k1;
                 const int c = k * NXY + it.j0 * g.NX, d = k * NXY + it.j1 * g.NX;
                 const unsigned nc = centre ? t_bytes(c, d) : 0u;
-                mbar_arrive_tx(&full[s], nb + 2 * nc);
+                mbar_arrive_tx(&full[s], nb + (x ? 2 : 1) * nc);
                 bulk_g2s(st, pc + t_abeg(a), nb, &full[s]);
                 if (centre) {
-                    bulk_g2s(st + tp.RB, x + t_abeg(c), nc, &full[s]);
+                    if (x) bulk_g2s(st + tp.RB, x + t_abeg(c), nc, &full[s]);
                     bulk_g2s(st + tp.RB + tp.RX, r + t_abeg(c), nc, &full[s]);
                 }
             }
@@ -331,7 +332,7 @@ __device__ void t_consume_a(const Grid& g, const TPlan& tp, const ClassTable& T,
 // neighbour below) are the centre values of the previous plane, kept in registers.
 template <int NCW, int NPT>
 __device__ void t_consume_b(const Grid& g, const TPlan& tp, const ClassTable& T, uint64_t* full, uint64_t* empty,
-                            const int* s_item, uint32_t& t, double alpha, double* __restrict__ x,
+                            const int* s_item, uint32_t& t, double alpha, bool xzero, double* __restrict__ x,
                             double* __restrict__ r, double* part, double (*ired)[32]) {
     const int NXY = g.NX * g.NY, sy = g.NX, RX = tp.RX;
     constexpr int NT = NCW * 32;
@@ -389,7 +390,7 @@ __device__ void t_consume_b(const Grid& g, const TPlan& tp, const ClassTable& T,
                     qv = T.diag[cl] * pp - ((T.c[0][cl] * (xm + xp) + T.c[1][cl] * (ym + yp)) + T.c[2][cl] * (zm + zp));
                 }
                 const double iv = T.invd[cl];
-                const double xv = __dadd_rn(t_sm[ox + p], __dmul_rn(alpha, pp));
+                const double xv = __dadd_rn(xzero ? 0.0 : t_sm[ox + p], __dmul_rn(alpha, pp));
                 const double rv = __dsub_rn(t_sm[ox + RX + p], __dmul_rn(alpha, qv));
                 x[p] = xv;
                 r[p] = rv;
@@ -480,10 +481,13 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) k_t_cg(PcgParams P, int Grh
             const double rho = rz;
             const double beta = it > 0 ? rho / rho_prev : 0.0;
             const bool first = it == 0;
+            // light RHS: in the first iteration r0 is b and x0 is 0 (neither was written)
+            const bool light0 = first && P.light_rhs;
+            const double* r0 = light0 ? P.b : P.r;
             // ---- sweep A ----
             if (blockIdx.x == 0 && threadIdx.x == 0) ctr[(seq + 2) & 3] = 0u;
             if (producer) {
-                if (plane0) t_produce<false>(g, tp, t_sm, full, empty, s_item, ctr + (seq & 3), t, first, P.r, pold,
+                if (plane0) t_produce<false>(g, tp, t_sm, full, empty, s_item, ctr + (seq & 3), t, first, r0, pold,
                                              nullptr, nullptr);
             } else {
                 t_consume_a<NCW, NPT>(g, tp, T, full, empty, s_item, t, first, beta, pnew, part, ired);
@@ -498,10 +502,10 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) k_t_cg(PcgParams P, int Grh
             // ---- sweep B ----
             if (blockIdx.x == 0 && threadIdx.x == 0) ctr[(seq + 2) & 3] = 0u;
             if (producer) {
-                if (plane0) t_produce<true>(g, tp, t_sm, full, empty, s_item, ctr + (seq & 3), t, false, P.r, nullptr,
-                                            pnew, P.T);
+                if (plane0) t_produce<true>(g, tp, t_sm, full, empty, s_item, ctr + (seq & 3), t, false, r0, nullptr,
+                                            pnew, light0 ? nullptr : P.T);
             } else {
-                t_consume_b<NCW, NPT>(g, tp, T, full, empty, s_item, t, alpha, P.T, P.r, part, ired);
+                t_consume_b<NCW, NPT>(g, tp, T, full, empty, s_item, t, alpha, light0, P.T, P.r, part, ired);
                 fence_proxy_async_global();
             }
             ++seq;
@@ -516,6 +520,8 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) k_t_cg(PcgParams P, int Grh
             ++it;
         }
     }
+    if (it == 0 && P.light_rhs)             // no iteration ran: x0 = 0 was never written
+        for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < g.n; p += gridDim.x * blockDim.x) P.T[p] = 0.0;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         P.info->iterations = (status == 1) ? P.maxiter : it;
         P.info->status = status;
