@@ -59,6 +59,45 @@ __device__ __forceinline__ void grid_sum_wide(const double* part, const int (&sl
     __syncthreads();
 }
 
+// Node whose class is 13 and whose six neighbours are all free (sweep B's fast test): no
+// Dirichlet lift, the constant-coefficient stencil.
+__device__ __forceinline__ bool s_free_interior(const Grid& g, int i, int j, int k) {
+    return i >= 1 && i <= g.nc[0] - 1 && j >= 1 && j <= g.nc[1] - 1 && k >= 2 && k <= g.nc[2] - 1 &&
+           (g.dkind != kGamma || (i >= 2 && i <= g.nc[0] - 2 && j >= 2 && j <= g.nc[1] - 2));
+}
+
+// RHS at node p (fem.py:129-194 + constrained, 89-105): b written (and r = b, x = 0 unless
+// the k_t_cg path implies them); accumulates b.b and b.z.
+__device__ __forceinline__ void s_rhs_node(const PcgParams& P, const ClassTable& T, int p, double* __restrict__ b,
+                                           double* __restrict__ r, double* __restrict__ x,
+                                           const double* __restrict__ load, double (&acc)[2]) {
+    const Grid& g = P.g;
+    int i, j, k;
+    decode(g, p, i, j, k);
+    double bv;
+    int cls = 13;
+    if (s_free_interior(g, i, j, k)) {
+        bv = T.mass[13] * x[p];
+        if (load) bv += load[p];
+    } else {
+        cls = class_of(g, i, j, k);
+        if (T.nd[cls] == 0.0) {
+            bv = dirichlet_value(P, p);
+        } else {
+            bv = T.mass[cls] * x[p];
+            if (load) bv += load[p];
+            bv += dirichlet_lift(P, T, p, i, j, k, cls);
+        }
+    }
+    b[p] = bv;
+    if (!P.light_rhs) {
+        r[p] = bv;
+        x[p] = 0.0;
+    }
+    acc[0] += bv * bv;
+    acc[1] += bv * __dmul_rn(T.invd[cls], bv);
+}
+
 // ---- k_s_rhs: b, r = b, x = 0; partials [0][blk] = b.b, [1][blk] = r.z ----------------
 __global__ void __launch_bounds__(kSTPB) k_s_rhs(PcgParams P) {
     __shared__ ClassTable T;
@@ -67,26 +106,13 @@ __global__ void __launch_bounds__(kSTPB) k_s_rhs(PcgParams P) {
     build_class_table(T, threadIdx.x, P.mbase, P.cbase, g.dkind);
     __syncthreads();
     double acc[2] = {0.0, 0.0};
-    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < g.n; p += gridDim.x * blockDim.x) {
-        int i, j, k;
-        decode(g, p, i, j, k);
-        const int cls = class_of(g, i, j, k);
-        double bv;
-        if (T.nd[cls] == 0.0) {
-            bv = dirichlet_value(P, p);
-        } else {
-            bv = T.mass[cls] * P.T[p];
-            if (P.load) bv += P.load[p];
-            bv += dirichlet_lift(P, T, p, i, j, k, cls);
-        }
-        P.b[p] = bv;
-        if (!P.light_rhs) {
-            P.r[p] = bv;
-            P.T[p] = 0.0;
-        }
-        acc[0] += bv * bv;
-        acc[1] += bv * __dmul_rn(T.invd[cls], bv);
+    const int stride = gridDim.x * blockDim.x;
+    int p = blockIdx.x * blockDim.x + threadIdx.x;
+    for (; p + stride < g.n; p += 2 * stride) {
+        s_rhs_node(P, T, p, P.b, P.r, P.T, P.load, acc);
+        s_rhs_node(P, T, p + stride, P.b, P.r, P.T, P.load, acc);
     }
+    if (p < g.n) s_rhs_node(P, T, p, P.b, P.r, P.T, P.load, acc);
     block_sum<2>(acc, red);
     if (threadIdx.x == 0) {
         P.part[blockIdx.x] = acc[0];
@@ -252,6 +278,34 @@ __global__ void __launch_bounds__(kSTPB, MINB) k_s_cg(PcgParams P, int Grhs) {
     }
 }
 
+// Residual term of node p: (A_c x - b)_p^2 and the non-finite count; then x_D = g = b_D
+// (fem.py:289-290) after the node's own term (neighbours read x_D with weight nd = 0, so
+// either value gives the same sum).
+__device__ __forceinline__ void s_resid_node(const Grid& g, const ClassTable& T, int p, double* __restrict__ x,
+                                             const double* __restrict__ b, double (&res)[2]) {
+    int i, j, k;
+    decode(g, p, i, j, k);
+    const int sy = g.NX, sz = g.NX * g.NY;
+    const double xp = x[p];
+    const double bv = b[p];
+    double ax;
+    if (s_free_interior(g, i, j, k)) {
+        ax = T.diag[13] * xp - ((T.c[0][13] * (x[p - 1] + x[p + 1]) + T.c[1][13] * (x[p - sy] + x[p + sy])) +
+                                T.c[2][13] * (x[p - sz] + x[p + sz]));
+    } else {
+        const int cls = class_of(g, i, j, k);
+        if (T.nd[cls] == 0.0) {
+            ax = xp;
+            x[p] = bv;
+        } else {
+            ax = apply_free(g, T, p, i, j, k, cls, xp, [&](int q, int) { return x[q]; });
+        }
+    }
+    const double d = ax - bv;
+    res[0] += d * d;
+    res[1] += isfinite(xp) ? 0.0 : 1.0;
+}
+
 // ---- k_s_resid: partials [0][blk] = ||A_c x - b||^2, [1][blk] = non-finite count --------
 __global__ void __launch_bounds__(kSTPB) k_s_resid(PcgParams P) {
     __shared__ ClassTable T;
@@ -260,21 +314,13 @@ __global__ void __launch_bounds__(kSTPB) k_s_resid(PcgParams P) {
     build_class_table(T, threadIdx.x, P.mbase, P.cbase, g.dkind);
     __syncthreads();
     double res[2] = {0.0, 0.0};
-    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < g.n; p += gridDim.x * blockDim.x) {
-        int i, j, k;
-        decode(g, p, i, j, k);
-        const int cls = class_of(g, i, j, k);
-        const double xp = P.T[p];
-        const double ax = (T.nd[cls] == 0.0) ? xp
-                                             : apply_free(g, T, p, i, j, k, cls, xp, [&](int q, int) { return P.T[q]; });
-        const double bv = P.b[p];
-        const double d = ax - bv;
-        res[0] += d * d;
-        res[1] += isfinite(xp) ? 0.0 : 1.0;
-        // x_D = g = b_D (fem.py:289-290), after this node's own residual term; neighbours
-        // that read x_D here weight it by nd = 0, so either value gives the same sum
-        if (T.nd[cls] == 0.0) P.T[p] = bv;
+    const int stride = gridDim.x * blockDim.x;
+    int p = blockIdx.x * blockDim.x + threadIdx.x;
+    for (; p + stride < g.n; p += 2 * stride) {
+        s_resid_node(g, T, p, P.T, P.b, res);
+        s_resid_node(g, T, p + stride, P.T, P.b, res);
     }
+    if (p < g.n) s_resid_node(g, T, p, P.T, P.b, res);
     block_sum<2>(res, red);
     if (threadIdx.x == 0) {
         P.part[blockIdx.x] = res[0];
