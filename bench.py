@@ -107,12 +107,13 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def cpu_sample(cfg_path: Path, what: str = "global+local"):
-    """Reference CPU algorithm (oracle/assembly.py, bitwise-pinned port) on a bounded sample."""
+def cpu_sample(cfg_path, what: str = "global+local"):
+    """Reference CPU algorithm (oracle/assembly.py, bitwise-pinned port) on a bounded sample.
+    ``cfg_path``: a .cfg file or an already built ExperimentConfig."""
     import paper_2110_12932_b200 as P
     from oracle import kuhn
     from oracle.twolevel import OracleRun
-    cfg = P.load_config(cfg_path)
+    cfg = P.load_config(cfg_path) if isinstance(cfg_path, (str, Path)) else cfg_path
     run = OracleRun(cfg, backend="assembly")
     Tg = np.full(run.G.n_nodes, cfg.T_initial)
     L = kuhn.KuhnGrid.from_placement(run.placement0)
@@ -145,6 +146,9 @@ def reference_arm(args):
     if rank != 0:
         return
     cfg_path = ROOT / "configs" / f"{args.config}.cfg"
+    if args.config == "cfg5":                 # config 5: a sample of its first scenario
+        from paper_2110_12932_b200 import scenarios as S
+        cfg_path = S.draw(0, 64)[0].config()
     times, dofs = [], []
     for s in range(args.warmup + args.steps):
         dof, dt, _, (Ng, Nl, m) = cpu_sample(cfg_path, what="local")
@@ -254,6 +258,241 @@ def slab_bench(args):
         dist.destroy_process_group()
 
 
+def kernel_stats(rows, n, dev_ms):
+    """Solve-launch timing rows [(ms, [iterations per solve])] on an n-node grid ->
+    algorithmic HBM throughput N(64k+32) per solve."""
+    if not rows:
+        return None
+    solves = sum(len(its) for _, its in rows)
+    bytes_ = sum(n * (64 * k + 32) for _, its in rows for k in its)
+    ms = sum(t for t, _ in rows)
+    return {"launches": len(rows), "solves": solves, "avg_ms_per_solve": ms / solves,
+            "avg_iterations": float(np.mean([k for _, its in rows for k in its])),
+            "alg_bytes_per_solve": bytes_ / solves, "achieved_gbs": bytes_ / (ms / 1e3) / 1e9,
+            "share_of_step": ms / dev_ms if dev_ms else None}
+
+
+def split_timing(kt, infos):
+    """Pair each timed solve launch with the solve records it produced -> (local, global)."""
+    loc, glo, pos = [], [], 0
+    for ms, lv, ns in kt:
+        its = [inf["iterations"] for inf in infos[pos:pos + ns]]
+        pos += ns
+        (loc if lv == 1 else glo).append((ms, its))
+    return loc, glo
+
+
+def scenario_bench(args):
+    """--config cfg5: BASELINE config 5, the batched scenario sweep.  64 independent runs of
+    the config-2 geometry (parameters from seed 0, paper_2110_12932_b200/scenarios.py),
+    LPT-sharded by DOF-timestep work across the ranks (no data-path collective).  Every
+    scenario of the rank's group is resident at once (one tl_run each, ~0.1 GB); one "step"
+    advances every scenario of the group by one macro step, issued back to back with the
+    runs' streams chained by events so the device executes them in order with no host
+    round trip between scenarios."""
+    import torch
+    import paper_2110_12932_b200 as P
+    from paper_2110_12932_b200 import scenarios as S
+    from paper_2110_12932_b200.schedule import plan_spacetime
+
+    rank, world, local_rank = env_rank()
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    allsc = S.draw(0, 64)[:args.scenarios]
+    group = S.shard(allsc, rank, world)
+    nsteps = args.warmup + 2 * args.steps          # timed steps, then as many e2e steps
+    runs, plans, dofs, nl_m = [], [], [], []
+    for sc in group:
+        cfg = sc.config()
+        problem, lmesh = P.build_problem(cfg, device=local_rank)
+        sched = P.MacroSchedule(cfg.dt_macro, cfg.micro_steps, 0.0, cfg.t_end)
+        if nsteps > sched.n_macro:
+            raise SystemExit(f"scenario {sc.index} has only {sched.n_macro} macro steps")
+        pls, placement, tg, tl = [], lmesh.placement, 0.0, 0.0
+        for k in range(nsteps):
+            pl = plan_spacetime(problem, sched, placement, cfg.path, cfg.policy, tg, tl, k0=k, nsteps=1)
+            pls.append(pl)
+            placement, tg, tl = pl.final_placement, pl.final_t_global, pl.final_t_local
+        run = P.DeviceRun(problem, lmesh)
+        run.initial(P.uniform_field(problem.global_mesh, cfg.T_initial))
+        runs.append(run)
+        plans.append(pls)
+        Ng, Nl = problem.global_mesh.n_nodes, lmesh.n_nodes
+        dofs.append(Ng + sched.micro_per_macro * Nl)
+        nl_m.append((Ng, Nl, sched.micro_per_macro))
+    streams = [torch.cuda.ExternalStream(r.stream(), device=dev) for r in runs]
+    dof_step = sum(dofs)
+
+    def one_step(k, plan_of=None, after=None):
+        """Macro step k of every scenario, device-ordered through event chaining."""
+        prev = None
+        for i, (run, st) in enumerate(zip(runs, streams)):
+            if prev is not None:
+                st.wait_event(prev)
+            run.run(plans[i][k] if plan_of is None else plan_of(i, k))
+            if after is not None:
+                after(i, k)
+            prev = torch.cuda.Event()
+            prev.record(st)
+        return prev
+
+    for k in range(args.warmup):
+        one_step(k)
+    for r in runs:
+        r.sync()
+        r.check_solves(r.take_info())
+        r.set_timing(True)
+        r.take_timing()
+    launches0 = sum(r.launch_count() for r in runs)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev = []
+    with ClockSampler(local_rank) as clocks:
+        wall0 = time.perf_counter()
+        last = None
+        for k in range(args.warmup, args.warmup + args.steps):
+            if not args.no_flush:
+                if last is not None:
+                    streams[0].wait_event(last)
+                runs[0].flush_l2()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e0.record(streams[0])
+            last = one_step(k)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record(streams[-1])
+            ev.append((e0, e1))
+            last = e1
+        for r in runs:
+            r.sync()
+        wall = time.perf_counter() - wall0
+    torch.cuda.synchronize()
+    launches = sum(r.launch_count() for r in runs) - launches0
+    dev_ms = float(sum(a.elapsed_time(b) for a, b in ev))
+    loc_rows, glo_rows = [], []
+    for r in runs:
+        infos = r.take_info()
+        r.check_solves(infos)
+        lo, gl = split_timing(r.take_timing(), infos)
+        loc_rows.extend(lo)
+        glo_rows.extend(gl)
+        r.set_timing(False)
+    if dist is not None:
+        t = torch.tensor([dev_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_ms = float(t.item())
+    total_dof = dof_step * args.steps
+    if dist is not None:
+        t = torch.tensor([float(total_dof)], device=dev, dtype=torch.float64)
+        dist.all_reduce(t)
+        total_dof = float(t.item())
+    value = total_dof / (dev_ms / 1e3)
+
+    # all scenarios share the config-2 grids: pool the solve launches per level
+    Ng, Nl = nl_m[0][0], nl_m[0][1]
+    share_ms = dev_ms if world == 1 else None
+    kloc, kglo = kernel_stats(loc_rows, Nl, share_ms), kernel_stats(glo_rows, Ng, share_ms)
+    peak, peak_src = measured_peak()
+    roofline = {"bound": "hbm", "achieved": kloc["achieved_gbs"], "peak": peak, "unit": "GB/s",
+                "frac": kloc["achieved_gbs"] / peak, "traffic": None,
+                "kernel": "local-grid PCG solves (k_pcg_resident_cg, SMEM-resident bricks, all micro solves "
+                          "+ corrector of a macro step in one launch), pooled over the group's scenarios",
+                "level": "local", "nodes": Nl, "peak_source": peak_src,
+                "note": "algorithmic bytes N(64k+32) per solve (SURVEY §8d); each scenario's grids are "
+                        "L2/SMEM-resident within its own macro step"}
+
+    # ---- e2e through DeviceRun.run: pinned plan uploads, every scenario's local field read back ----
+    def pin(arr, dtype):
+        arr = np.ascontiguousarray(arr, dtype=dtype).reshape(-1)
+        buf = torch.empty(max(arr.nbytes, 1), dtype=torch.uint8, pin_memory=True).numpy().view(dtype)[:arr.size]
+        buf[:] = arr
+        return buf
+
+    ks = list(range(args.warmup + args.steps, nsteps))
+    e2e_plans, h2d = {}, 0
+    for i in range(len(runs)):
+        for k in ks:
+            pl = plans[i][k]
+            pp = type(pl)(macro=pin(pl.macro, pl.macro.dtype), micro=pin(pl.micro, pl.micro.dtype),
+                          dep_points=pin(pl.dep_points, np.float64).reshape(-1, 3),
+                          dep_power=pin(pl.dep_power, np.float64))
+            e2e_plans[i, k] = pp
+            h2d += pp.macro.nbytes + pp.micro.nbytes + pp.dep_points.nbytes + pp.dep_power.nbytes
+    pins = [[torch.empty(nl, dtype=torch.float64, pin_memory=True).numpy() for _ in range(2)]
+            for (_, nl, _) in nl_m]
+    for i, r in enumerate(runs):                  # staging buffers registered before the clock
+        for s in range(2):
+            r.field_async(1, pins[i][s], slot=s)
+            r.field_wait(s)
+    d2h = 0
+
+    def readback(i, k):
+        runs[i].field_async(1, pins[i][k % 2], slot=k % 2)
+
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for s, k in enumerate(ks):
+        one_step(k, plan_of=lambda i, kk: e2e_plans[i, kk], after=readback)
+        d2h += sum(p[k % 2].nbytes for p in pins)
+        if s >= 1:
+            for r in runs:
+                r.field_wait((k - 1) % 2)
+    for r in runs:
+        r.field_wait(ks[-1] % 2)
+    e2e_s = time.perf_counter() - t0
+    for r in runs:
+        r.check_solves(r.take_info())
+    if dist is not None:
+        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": total_dof / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d // len(ks),
+           "d2h_bytes_per_step": d2h // len(ks),
+           "note": "host wall clock (max over ranks) through DeviceRun.run, the next macro steps of every "
+                   "scenario: plan arrays H2D from pinned memory, every scenario's local field D2H to "
+                   "pinned memory each step (double-buffered, overlapped with the following scenarios)"}
+    for r in runs:
+        r.close()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        dof, dt, its, _ = cpu_sample(group[0].config(), what="local")
+        cpu = {"value": dof / dt, "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": f"one local micro solve of scenario {group[0].index} ({dof} DOF-timesteps, {dt:.1f} s) "
+                         "via the literal P1-assembly + scipy-CG port (oracle/assembly.py, bitwise equal to "
+                         "lpbfsim); OPENBLAS_NUM_THREADS=1"}
+    ms = [m for (_, _, m) in nl_m]
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (BASELINE config 5: 64 config-2 scenarios, parameters drawn from seed 0)",
+        "config": {"workload": f"cfg5: batched scenario sweep, {len(allsc)} scenarios of the config-2 geometry "
+                               f"(global {Ng} + local {Nl} nodes, m in {{5,10,20}}) split over {world} GPU(s); "
+                               f"one step = one macro step of every scenario of the group",
+                   "scenarios_rank0": [s.index for s in group],
+                   "micro_rank0": {str(v): ms.count(v) for v in sorted(set(ms))},
+                   "dof_timesteps_per_step_rank0": dof_step,
+                   "macro_steps": f"{args.warmup}..{args.warmup + args.steps - 1} (e2e: the next {args.steps})",
+                   "l2": ("flushed between timed steps; each step also streams every scenario's fields "
+                          f"({len(group)} x ~0.1 GB, larger than L2)") if not args.no_flush else "not flushed",
+                   "parallelism": f"scenario groups x{world}" if world > 1 else "single GPU"},
+        "roofline": roofline, "kernels": {"local_pcg": kloc, "global_pcg": kglo},
+        "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+        "clocks": clocks.summary(), "wall_s_timed_region": wall,
+        "iterations": {"local": kloc["avg_iterations"], "global": kglo["avg_iterations"] if kglo else None},
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -266,6 +505,8 @@ def main():
     ap.add_argument("--skip", type=int, default=0, help="macro steps to run before warm-up")
     ap.add_argument("--slabs", action="store_true",
                     help="global grid split into z-slabs over the ranks (default config cfg4)")
+    ap.add_argument("--scenarios", type=int, default=64,
+                    help="cfg5: how many of the 64 seed-0 scenarios to run (split over the ranks)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
@@ -273,6 +514,8 @@ def main():
         return reference_arm(args)
     if args.slabs:
         return slab_bench(args)
+    if args.config == "cfg5":
+        return scenario_bench(args)
 
     import torch
     import paper_2110_12932_b200 as P
@@ -350,24 +593,9 @@ def main():
     peak, peak_src = measured_peak()
     # pair each timed launch with the solve records it produced (a persistent local
     # launch runs all micro solves + corrector of a macro step)
-    loc, glo, pos = [], [], 0
-    for ms, lv, ns in kt:
-        its = [inf["iterations"] for inf in infos[pos:pos + ns]]
-        pos += ns
-        (loc if lv == 1 else glo).append((ms, its))
-
-    def kstats(rows, n):
-        if not rows:
-            return None
-        solves = sum(len(its) for _, its in rows)
-        bytes_ = sum(n * (64 * k + 32) for _, its in rows for k in its)
-        ms = sum(t for t, _ in rows)
-        return {"launches": len(rows), "solves": solves, "avg_ms_per_solve": ms / solves,
-                "avg_iterations": float(np.mean([k for _, its in rows for k in its])),
-                "alg_bytes_per_solve": bytes_ / solves, "achieved_gbs": bytes_ / (ms / 1e3) / 1e9,
-                "share_of_step": ms / dev_ms if world == 1 else None}
-
-    kloc, kglo = kstats(loc, Nl), kstats(glo, Ng)
+    loc, glo = split_timing(kt, infos)
+    share_ms = dev_ms if world == 1 else None
+    kloc, kglo = kernel_stats(loc, Nl, share_ms), kernel_stats(glo, Ng, share_ms)
     # the dominant kernel: the level whose solves take the larger share of the step
     lev = "global" if kglo and (not kloc or sum(t for t, _ in glo) > sum(t for t, _ in loc)) else "local"
     kdom, ndom = (kglo, Ng) if lev == "global" else (kloc, Nl)
