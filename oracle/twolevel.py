@@ -15,6 +15,8 @@ source => ``interval_source``):
 - ``run_space``       — ``lpbfsim/multirate.py:194-217`` with the one-way pass of
                         ``two_level_iterate`` (``lpbfsim/twolevel.py:299-358``)
 - ``relocate_local``  — ``lpbfsim/scanpath.py:208-248``
+- ``run_reference``   — ``lpbfsim/runner.py:126-163`` → ``fem.solve_monolithic``
+                        (``lpbfsim/fem.py:386-423``): the true beam on one fine grid
 
 Times follow the reference's float bookkeeping exactly (global time accumulates
 ``t + dt``; local micro times come from ``MacroSchedule.t_micro``).
@@ -176,6 +178,33 @@ class OracleRun:
                 if moved is not None:
                     Tl, trace = moved
         return Tg, Tl, placement
+
+    def run_reference(self, h: float | None = None, dt: float | None = None,
+                      n_steps: int | None = None):
+        """Monolithic fine-grid reference: uniform steps on the plate at ``h_reference`` with
+        the Gaussian beam at each target time and the bottom Dirichlet set.  Returns
+        (times, fields)."""
+        cfg = self.cfg
+        h = cfg.h_reference if h is None else h
+        dt = cfg.dt_reference if dt is None else dt
+        n = int(round(cfg.t_end / dt)) if n_steps is None else n_steps
+        gbox = cfg.global_box
+        R = kuhn.KuhnGrid(gbox.lo, gbox.hi, structured_ncells(gbox, h))
+        g = np.full(R.n_nodes, cfg.bc.T_buildplate)
+        T = np.full(R.n_nodes, cfg.T_initial)
+        times, fields = [0.0], [T]
+        for k in range(1, n + 1):
+            t_new = 0.0 + k * dt
+            center = self.local_center(t_new)
+            step_dt = t_new - times[-1]
+            load = kuhn.gaussian_load(R, cfg.beam, center) if center is not None else None
+            op = kuhn.StencilOperator(R, self.kappa, self.rhoc, step_dt, R.bottom_mask())
+            T, its, _ = solve_constrained(op, op.rhs(T, load, g), g, self.rtol)
+            self.iterations.append(("reference", its))
+            self._count("reference_solves")
+            times.append(t_new)
+            fields.append(T)
+        return times, fields
 
     def run_space(self, n_steps: int | None = None, recorder=None):
         cfg = self.cfg

@@ -22,10 +22,12 @@ from .errors import (  # noqa: F401
     NativeLibraryMissing, NonConvergence, PathError, PointOutsideMesh, SolverError, SourceError,
     UnsupportedOnDevice,
 )
-from .fem import BoundarySpec, FieldState, GaussianSource, step_backward_euler, uniform_field  # noqa: F401
+from .fem import (  # noqa: F401
+    BoundarySpec, FieldState, GaussianSource, Trajectory, solve_monolithic, step_backward_euler, uniform_field,
+)
 from .grid import BOTTOM, LATERAL, TOP, StructuredGrid, build_structured_grid  # noqa: F401
 from .multirate import DeviceRun, macro_step, run_space, run_spacetime  # noqa: F401
-from .runner import build_problem, two_level_run, two_level_run_slabs  # noqa: F401
+from .runner import build_problem, reference_bounds, run_reference, two_level_run, two_level_run_slabs  # noqa: F401
 from .stats import RunStats  # noqa: F401
 from .twolevel import (  # noqa: F401
     InterfaceGamma, TwoLevelProblem, TwoLevelState, extract_interface, initial_state, solve_global,

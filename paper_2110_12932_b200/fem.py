@@ -23,7 +23,7 @@ from .errors import SolverError, UnsupportedOnDevice
 from .grid import BOTTOM, TOP, StructuredGrid
 
 __all__ = ["FieldState", "uniform_field", "SolverSettings", "BoundarySpec", "GaussianSource",
-           "step_backward_euler", "device_rtol"]
+           "step_backward_euler", "device_rtol", "Trajectory", "solve_monolithic"]
 
 
 @dataclass(frozen=True)
@@ -158,3 +158,68 @@ def step_backward_euler(state: FieldState, dt: float, mat, source, bounds: Bound
     if stats is not None:
         stats.count("picard_iterations")
     return state.with_values(x, state.time + dt)
+
+
+@dataclass
+class Trajectory:
+    """Fields on one grid at strictly increasing times (``lpbfsim/fem.py:359-383``)."""
+
+    mesh: object
+    times: list = field(default_factory=list)
+    values: list = field(default_factory=list)
+
+    def append(self, state: FieldState):
+        if self.times and state.time <= self.times[-1]:
+            raise SolverError("trajectory times must increase")
+        self.times.append(state.time)
+        self.values.append(state.values)
+
+    def __len__(self):
+        return len(self.times)
+
+    def state(self, idx: int) -> FieldState:
+        return FieldState(self.mesh, self.values[idx], self.times[idx])
+
+    def at_time(self, t: float, tol: float = 1e-9) -> FieldState:
+        arr = np.asarray(self.times)
+        idx = int(np.argmin(np.abs(arr - t)))
+        if abs(arr[idx] - t) > tol * max(1.0, abs(t)):
+            raise SolverError(f"no trajectory frame at t={t:g}")
+        return self.state(idx)
+
+
+class _NullCtx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False
+
+
+def solve_monolithic(mesh, mat, source_at, bounds_at, dt: float, n_steps: int, T_0: FieldState,
+                     settings: SolverSettings = SolverSettings(), latent: bool = True,
+                     latent_mask=None, stats=None, observer=None) -> Trajectory:
+    """Uniform-step single-grid solve (``lpbfsim/fem.py:386-423``): the monolithic fine-grid
+    reference, every step one device solve through ``step_backward_euler``.
+
+    ``source_at(t)`` -> GaussianSource or None, ``bounds_at(t)`` -> BoundarySpec, both at
+    each target time ``T_0.time + k dt`` (the reference's time bookkeeping).
+    """
+    if dt <= 0 or n_steps < 0:
+        raise SolverError("schedule requires dt > 0 and n_steps >= 0")
+    traj = Trajectory(mesh)
+    traj.append(T_0)
+    state = T_0
+    for k in range(1, n_steps + 1):
+        t_new = T_0.time + k * dt
+        timer = stats.timer("reference_solve") if stats is not None else _NullCtx()
+        with timer:
+            state = step_backward_euler(state, t_new - state.time, mat, source_at(t_new),
+                                        bounds_at(t_new), settings, latent=latent,
+                                        latent_mask=latent_mask, stats=stats)
+        if stats is not None:
+            stats.count("reference_solves")
+        traj.append(state)
+        if observer is not None:
+            observer(state)
+    return traj

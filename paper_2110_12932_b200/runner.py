@@ -3,7 +3,8 @@
 ``build_problem(cfg)`` accepts this package's ``ExperimentConfig`` or the
 reference's own (duck-typed: the same field names) and returns the device
 ``TwoLevelProblem`` plus the initial local grid.  ``two_level_run`` is the
-``_two_level_run`` equivalent for the two-level modes.
+``_two_level_run`` equivalent for the two-level modes; ``run_reference`` is the
+monolithic fine-grid reference (``runner.py:126-163``) on the same device solve.
 """
 
 from __future__ import annotations
@@ -14,8 +15,9 @@ from .control import (
     Box, LaserBeam, LocalDomainPolicy, LocalPlacement, Material, ScanPath, Segment, ThermalBC,
     initial_local_box, structured_ncells,
 )
-from .fem import uniform_field
-from .grid import StructuredGrid, build_structured_grid
+from .errors import UnsupportedOnDevice
+from .fem import BoundarySpec, GaussianSource, Trajectory, solve_monolithic, uniform_field
+from .grid import BOTTOM, TOP, StructuredGrid, build_structured_grid
 from .multirate import MacroSchedule, run_space, run_spacetime
 from .stats import RunStats
 from .twolevel import TwoLevelProblem
@@ -134,3 +136,46 @@ def two_level_run_slabs(cfg, stats: RunStats | None = None, n_steps: int | None 
     state = run_spacetime_slabs(problem, sched, lmesh, T0, path=c["path"] if moving else None,
                                 policy=c["policy"], stats=stats, group=group, device=f"cuda:{int(device)}")
     return state, stats
+
+
+def reference_bounds(cfg, mesh) -> BoundarySpec:
+    """``reference_bounds`` (``runner.py:116-123``): bottom Dirichlet T_buildplate, Robin top."""
+    bc = convert_config(cfg)["bc"]
+    return BoundarySpec(bc=bc, robin_tags=(TOP,), radiation=bc.emissivity > 0,
+                        dirichlet_nodes=mesh.nodes_on(BOTTOM), dirichlet_values=bc.T_buildplate)
+
+
+def run_reference(cfg, dt: float | None = None, stats: RunStats | None = None, mesh=None,
+                  observer=None) -> Trajectory:
+    """Monolithic reference (``runner.py:126-163``): the true Gaussian beam on one fine grid
+    (``h_reference``) over the whole plate, uniform steps ``dt_reference``, every step a
+    device solve.  Distinct coarse/fine materials (the reference's PiecewiseMaterial) and
+    latent heat are not on the device path and raise ``UnsupportedOnDevice``."""
+    c = convert_config(cfg)
+    dt = cfg.dt_reference if dt is None else dt
+    mesh = build_structured_grid(c["global_box"], cfg.h_reference) if mesh is None else mesh
+    n_steps = int(round(c["t_end"] / dt))
+    mat, mat_l = c["material"], c["material_local"]
+    if mat_l is not None and mat_l is not mat and not _materials_equal(mat, mat_l):
+        raise UnsupportedOnDevice("a reference with distinct coarse/fine materials (PiecewiseMaterial) "
+                                  "is not on the device path")
+    chi_max = max(mat.chi, mat_l.chi if mat_l is not None else 0.0)
+    latent = cfg.latent_reference != "off" and chi_max > 0
+    path, beam = c["path"], c["beam"]
+    tol = 1e-12 * max(path.t_end, 1.0)
+
+    def source_at(t):                              # ``_local_source_factory`` (runner.py:49-61)
+        if t > path.t_end + tol or t < path.t_start - tol:
+            return None
+        return GaussianSource(beam, tuple(path.position(t)))
+
+    bounds = reference_bounds(cfg, mesh)
+    T0 = uniform_field(mesh, c["T_initial"], time=0.0)
+    return solve_monolithic(mesh, mat, source_at, lambda t: bounds, dt, n_steps, T0,
+                            settings=c["solver"], latent=latent, stats=stats, observer=observer)
+
+
+def _materials_equal(a, b) -> bool:
+    return (np.array_equal(np.asarray(a.conductivity_table), np.asarray(b.conductivity_table))
+            and np.array_equal(np.asarray(a.heat_capacity_table), np.asarray(b.heat_capacity_table))
+            and a.rho == b.rho and a.chi == b.chi)

@@ -17,6 +17,9 @@ comes from calling the reference's own functions:
 - run_*.npz      run_spacetime / run_space with a field-capturing recorder
                  and a CG-iteration counter wrapped around fem._cg
                  — multirate.py:167-217
+- mono_cfg1.npz  runner.run_reference (the monolithic fine-grid reference,
+                 fem.solve_monolithic) on the cfg1 plate, h = 25 um, 8 steps
+                 — runner.py:126-163, fem.py:386-423
 - schedule_*.json local-box origins per macro step from the reference's
                  LocalDomainPolicy / Mesh.translated / DomainEscape clamp,
                  path.position and swept_pieces         — scanpath.py:68-248
@@ -305,8 +308,32 @@ def run_case(name, max_steps, full_at, stride):
     print(f"run_{name}: steps={len(rec['t']) - 1} wall={wall:.1f}s counters={stats.counters}")
 
 
+def monolithic_case(n_steps=8, h=2.5e-5, stride=7):
+    cfg = load_config(CFG / "cfg1_m4.cfg")
+    cfg.h_reference = h
+    cfg.dt_reference = cfg.dt_macro / cfg.micro_steps
+    cfg.t_end = n_steps * cfg.dt_reference
+    stats = RunStats()
+    CG_ITERS.clear()
+    t0 = time.perf_counter()
+    traj = runner.run_reference(cfg, stats=stats)
+    wall = time.perf_counter() - t0
+    TL = cfg.material.T_liquidus
+    vals = [np.asarray(v) for v in traj.values]
+    np.savez_compressed(
+        OUT / "mono_cfg1.npz", t=np.array(traj.times), h=h, dt=cfg.dt_reference, n_steps=n_steps,
+        n_nodes=traj.mesh.n_nodes, sub=np.array([v[::stride] for v in vals]), stride=stride,
+        melt=np.array([np.packbits(v > TL) for v in vals]), last=vals[-1], mid=vals[n_steps // 2],
+        cg_iters=np.array(CG_ITERS), counters=json.dumps(stats.counters), wall=wall,
+        versions=json.dumps(VERS))
+    print(f"mono_cfg1: nodes={traj.mesh.n_nodes} steps={len(vals) - 1} wall={wall:.1f}s "
+          f"max={vals[-1].max():.2f} iters={CG_ITERS} counters={stats.counters}")
+
+
 def main():
     quick = "--quick" in sys.argv
+    if "--monolithic" in sys.argv:
+        return monolithic_case()
     op_case("aniso_local", (1e-4, 2e-4, 3e-4), (2.75e-4, 2.85e-4, 3.44e-4), (2.5e-5, 1.7e-5, 1.1e-5), "local")
     op_case("aniso_global", (0.0, 0.0, 0.0), (1.75e-4, 1.7e-4, 1.1e-4), (2.5e-5, 1.7e-5, 1.1e-5), "global")
     op_case("cfg1_local", (8e-4, 3e-4, 3e-4), (1.2e-3, 7e-4, 5e-4), 1e-5, "local")
@@ -321,6 +348,7 @@ def main():
     run_case("cfg1_m4", None, {1, 2, 10, 40, 80}, 17)
     run_case("cfg1_uniform", None, {1, 80}, 17)
     run_case("cfg2", 2, {1, 2}, 97)
+    monolithic_case()
 
 
 if __name__ == "__main__":

@@ -446,3 +446,25 @@ def test_tiled_cg_loop_cfg3_size_vs_oracle(level, tmp_path):
     assert int(t["status"]) == 0 and abs(int(t["its"]) - its) <= 1
     assert rel(t["x"], ref) <= 1e-12
     assert int(t["its"]) == int(out["flat"]["its"]) and rel(t["x"], out["flat"]["x"]) <= 1e-13
+
+
+def test_monolithic_reference_vs_reference_golden():
+    """run_reference / solve_monolithic (lpbfsim/runner.py:126-163, fem.py:386-423) on the
+    device: the cfg1 plate at h = 25 um, 8 uniform steps, against the reference's output."""
+    z = np.load(GOLDEN / "mono_cfg1.npz")
+    cfg = P.load_config(CONFIGS / "cfg1_m4.cfg")
+    cfg.h_reference = float(z["h"])
+    cfg.dt_reference = float(z["dt"])
+    cfg.t_end = int(z["n_steps"]) * cfg.dt_reference
+    stats = P.RunStats()
+    traj = P.run_reference(cfg, stats=stats)
+    assert traj.mesh.n_nodes == int(z["n_nodes"])
+    assert traj.times == list(z["t"])
+    assert stats.counters == json.loads(str(z["counters"]))
+    s = int(z["stride"])
+    TL = cfg.material.T_liquidus
+    for k, T in enumerate(traj.values):
+        assert rel(T[::s], z["sub"][k]) <= REL
+        np.testing.assert_array_equal(np.packbits(T > TL), z["melt"][k])
+    assert rel(traj.values[-1], z["last"]) <= REL
+    assert rel(traj.at_time(float(z["t"][int(z["n_steps"]) // 2])).values, z["mid"]) <= REL

@@ -172,3 +172,20 @@ def test_forward_edge_pAp_identity(name):
         both = free[lo] & free[hi]
         fwd -= 2.0 * float(np.sum(np.where(both, op.c[a] * Pg[lo] * Pg[hi], 0.0)))
     assert abs(fwd - ref) <= 1e-13 * abs(ref)
+
+
+def test_oracle_monolithic_reference_vs_golden():
+    """Monolithic fine-grid reference (runner.run_reference, fem.solve_monolithic) on the cfg1
+    plate at h = 25 um, 8 steps: the oracle against the reference's own output."""
+    z = np.load(GOLDEN / "mono_cfg1.npz")
+    cfg = P.load_config(CONFIGS / "cfg1_m4.cfg")
+    orc = OracleRun(cfg)
+    times, fields = orc.run_reference(h=float(z["h"]), dt=float(z["dt"]), n_steps=int(z["n_steps"]))
+    assert times == list(z["t"])
+    s = int(z["stride"])
+    TL = cfg.material.T_liquidus
+    for k, T in enumerate(fields):
+        assert np.abs(T[::s] - z["sub"][k]).max() / np.abs(z["sub"][k]).max() <= 1e-12
+        np.testing.assert_array_equal(np.packbits(T > TL), z["melt"][k])
+    assert np.abs(fields[-1] - z["last"]).max() / z["last"].max() <= 1e-12
+    assert [k for _, k in orc.iterations] == list(z["cg_iters"])
