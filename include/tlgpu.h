@@ -146,6 +146,17 @@ int32_t tl_interpolate_host(const tl_grid_desc* global_grid, const double* value
 int32_t tl_interpolate_points_host(const tl_grid_desc* global_grid, const double* values,
                                    const double* points, int64_t npoints, double* out);
 
+/* ---- discrete L2 norms with the P1 mass matrix (fem.mass_matrix / l2_norm,
+ *      fem.py:434-446): out[0] = (a-b)^T M (a-b) (a^T M a when b == NULL),
+ *      out[1] = b^T M b (0 when b == NULL). */
+int32_t tl_mass_norms_host(const tl_grid_desc* grid, const double* a, const double* b, double* out);
+
+/* ---- error_metrics' per-record term (metrics.py:141-150): the reference field on
+ *      ref_grid interpolated at grid's nodes (Mesh.interpolate), then
+ *      out[0] = d^T M d with d = values - P1(ref), out[1] = P1(ref)^T M P1(ref). */
+int32_t tl_error_l2_host(const tl_grid_desc* ref_grid, const double* ref_values, const tl_grid_desc* grid,
+                         const double* values, double* out);
+
 /* ---- deposit scatter: SweptTrackDeposit.load (sources.py:164-172), deterministic. */
 int32_t tl_deposit_host(const tl_grid_desc* grid, const double* points, const double* power,
                         int32_t count, double* load_out);

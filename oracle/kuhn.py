@@ -302,3 +302,28 @@ def swept_samples(beam, pieces, dt: float):
     if not pts_all:
         return np.empty((0, 3)), np.empty(0)
     return np.vstack(pts_all), np.concatenate(pw_all)
+
+
+def mass_norm2(grid: KuhnGrid, v: np.ndarray) -> float:
+    """v^T M v with the P1 mass matrix of the Kuhn tets (``lpbfsim/fem.py:434-446``; the
+    4-point rule is exact for P1 x P1, so M = sum over tets of V/20 (1 + delta_ij)):
+    per tet V/20 (sum v_i^2 + (sum v_i)^2), V = hx hy hz / 6."""
+    nx, ny, nz = (int(c) for c in grid.n)
+    V = np.asarray(v, dtype=np.float64).reshape(nz + 1, ny + 1, nx + 1)
+
+    def corner(bits):
+        return V[(bits >> 2) & 1:(bits >> 2 & 1) + nz, (bits >> 1) & 1:((bits >> 1) & 1) + ny,
+                 bits & 1:(bits & 1) + nx]
+
+    c = [corner(b) for b in range(8)]          # bit a = +1 along axis a (x = bit 0)
+    tot = 0.0
+    for perm in PERMS:
+        verts, acc = [0], 0
+        for ax in perm:
+            acc += 1 << ax
+            verts.append(acc)
+        vs = [c[q] for q in verts]
+        s1 = vs[0] + vs[1] + vs[2] + vs[3]
+        tot += float(np.sum(vs[0] ** 2 + vs[1] ** 2 + vs[2] ** 2 + vs[3] ** 2 + s1 ** 2))
+    h = (np.asarray(grid.hi0) - np.asarray(grid.lo0)) / np.asarray(grid.n)
+    return tot * float(np.prod(h)) / 6.0 / 20.0

@@ -767,6 +767,51 @@ int32_t tl_interpolate_host(const tl_grid_desc* global_grid, const double* value
     return TL_OK;
 }
 
+int32_t tl_mass_norms_host(const tl_grid_desc* grid, const double* a, const double* b, double* out) {
+    if (!grid || !a || !out) return fail(TL_E_INVALID, "null argument");
+    tl::Grid L{};
+    if (int rc = make_grid(*grid, tl::kGamma, L)) return rc;
+    constexpr int kNB = 296;
+    double *da, *db = nullptr, *dpart;
+    int rc = 0;
+    if ((rc = dalloc(&da, L.n)) || (b && (rc = dalloc(&db, L.n))) || (rc = dalloc(&dpart, 2 * kNB))) return rc;
+    TL_CUDA(cudaMemcpy(da, a, sizeof(double) * L.n, cudaMemcpyHostToDevice));
+    if (b) TL_CUDA(cudaMemcpy(db, b, sizeof(double) * L.n, cudaMemcpyHostToDevice));
+    tl::k_mass_norms<<<kNB, 256>>>(L, da, db, dpart);
+    TL_CUDA(cudaGetLastError());
+    double part[2 * kNB];
+    TL_CUDA(cudaMemcpy(part, dpart, sizeof(part), cudaMemcpyDeviceToHost));
+    out[0] = out[1] = 0.0;
+    for (int k = 0; k < kNB; ++k) { out[0] += part[2 * k]; out[1] += part[2 * k + 1]; }
+    cudaFree(da); if (db) cudaFree(db); cudaFree(dpart);
+    return TL_OK;
+}
+
+int32_t tl_error_l2_host(const tl_grid_desc* ref_grid, const double* ref_values, const tl_grid_desc* grid,
+                         const double* values, double* out) {
+    if (!ref_grid || !ref_values || !grid || !values || !out) return fail(TL_E_INVALID, "null argument");
+    tl::Grid G{}, L{};
+    if (int rc = make_grid(*ref_grid, tl::kBottom, G)) return rc;
+    if (int rc = make_grid(*grid, tl::kGamma, L)) return rc;
+    constexpr int kNB = 296;
+    double *dref, *dv, *dri, *dpart;
+    int rc = 0;
+    if ((rc = dalloc(&dref, G.n)) || (rc = dalloc(&dv, L.n)) || (rc = dalloc(&dri, L.n)) ||
+        (rc = dalloc(&dpart, 2 * kNB)))
+        return rc;
+    TL_CUDA(cudaMemcpy(dref, ref_values, sizeof(double) * G.n, cudaMemcpyHostToDevice));
+    TL_CUDA(cudaMemcpy(dv, values, sizeof(double) * L.n, cudaMemcpyHostToDevice));
+    tl::k_interp<<<592, 256>>>(G, dref, L, 0, dri, nullptr);     // reference on the grid's nodes
+    tl::k_mass_norms<<<kNB, 256>>>(L, dv, dri, dpart);
+    TL_CUDA(cudaGetLastError());
+    double part[2 * kNB];
+    TL_CUDA(cudaMemcpy(part, dpart, sizeof(part), cudaMemcpyDeviceToHost));
+    out[0] = out[1] = 0.0;
+    for (int k = 0; k < kNB; ++k) { out[0] += part[2 * k]; out[1] += part[2 * k + 1]; }
+    cudaFree(dref); cudaFree(dv); cudaFree(dri); cudaFree(dpart);
+    return TL_OK;
+}
+
 int32_t tl_interpolate_points_host(const tl_grid_desc* global_grid, const double* values,
                                    const double* points, int64_t npoints, double* out) {
     if (!global_grid || !values || !points || !out || npoints < 0) return fail(TL_E_INVALID, "bad argument");

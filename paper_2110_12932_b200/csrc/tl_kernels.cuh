@@ -12,6 +12,9 @@
 //   k_deposit    SweptTrackDeposit.load scatter (sources.py:164-172), deterministic.
 //   k_melt       max T and melt-node count (T > T_liquidus) of one field.
 //   k_flush      writes a buffer larger than L2 (benchmark hygiene).
+//   k_mass_norms discrete L2 norms v^T M v with the P1 mass matrix (fem.mass_matrix,
+//                fem.py:434-446) of a field difference and of the reference field:
+//                the metrics of metrics.error_metrics (metrics.py:123-165).
 #pragma once
 
 #include <cooperative_groups.h>
@@ -794,6 +797,53 @@ __global__ void k_melt_final(const double* part, int nb, double* out_max, double
         for (int b = 0; b < nb; ++b) { m = fmax(m, part[2 * b]); c += part[2 * b + 1]; }
         *out_max = m;
         *out_cnt = c;
+    }
+}
+
+// v^T M v with the consistent P1 mass matrix of the Kuhn tets: per tet
+// V/20 (sum v_i^2 + (sum v_i)^2), V = hx hy hz / 6 (the 4-point rule of the reference's
+// mass_matrix is exact for P1 x P1).  One thread per cell gathers the 8 corners of
+// d = a - b (d = a when b == nullptr) and of b; the six Kuhn tets of a cell share the
+// main diagonal 000-111 and run 000 -> e_pi0 -> e_pi0 + e_pi1 -> 111.  Per-block partials
+// (fixed order, deterministic) go to part[2 * block + {0, 1}].
+__global__ void k_mass_norms(Grid L, const double* __restrict__ a, const double* __restrict__ b,
+                             double* part) {
+    __shared__ double red[64];
+    const int ncell = L.nc[0] * L.nc[1] * L.nc[2];
+    const int sy = L.NX, sz = L.NX * L.NY;
+    double acc[2] = {0.0, 0.0};
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncell; c += gridDim.x * blockDim.x) {
+        const int ci = c % L.nc[0], t = c / L.nc[0];
+        const int cj = t % L.nc[1], ck = t / L.nc[1];
+        const int p0 = ci + sy * cj + sz * ck;
+        const int off[8] = {0, 1, sy, 1 + sy, sz, 1 + sz, sy + sz, 1 + sy + sz};   // bit a = axis a
+        double d[8], r[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const double av = a[p0 + off[q]];
+            const double bv = b ? b[p0 + off[q]] : 0.0;
+            d[q] = b ? av - bv : av;
+            r[q] = bv;
+        }
+        double sd = 0.0, sr = 0.0;
+        // permutations in itertools order: (0,1,2) (0,2,1) (1,0,2) (1,2,0) (2,0,1) (2,1,0)
+        const int mid[6][2] = {{1, 3}, {1, 5}, {2, 3}, {2, 6}, {4, 5}, {4, 6}};
+#pragma unroll
+        for (int e = 0; e < 6; ++e) {
+            const int v1 = mid[e][0], v2 = mid[e][1];
+            const double s1 = d[0] + d[v1] + d[v2] + d[7];
+            sd += d[0] * d[0] + d[v1] * d[v1] + d[v2] * d[v2] + d[7] * d[7] + s1 * s1;
+            const double s2 = r[0] + r[v1] + r[v2] + r[7];
+            sr += r[0] * r[0] + r[v1] * r[v1] + r[v2] * r[v2] + r[7] * r[7] + s2 * s2;
+        }
+        acc[0] += sd;
+        acc[1] += sr;
+    }
+    block_sum<2>(acc, red);
+    if (threadIdx.x == 0) {
+        const double w = L.h[0] * L.h[1] * L.h[2] / 6.0 / 20.0;
+        part[2 * blockIdx.x] = acc[0] * w;
+        part[2 * blockIdx.x + 1] = acc[1] * w;
     }
 }
 

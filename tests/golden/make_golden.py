@@ -20,6 +20,9 @@ comes from calling the reference's own functions:
 - mono_cfg1.npz  runner.run_reference (the monolithic fine-grid reference,
                  fem.solve_monolithic) on the cfg1 plate, h = 25 um, 8 steps
                  — runner.py:126-163, fem.py:386-423
+- metrics_cfg1.npz fem.l2_norm on random fields (a plain and a translated anisotropic
+                 mesh) and metrics.error_metrics of a 2-macro-step cfg1 two-level run
+                 against run_reference (h = 25 um)  — fem.py:434-446, metrics.py:123-165
 - schedule_*.json local-box origins per macro step from the reference's
                  LocalDomainPolicy / Mesh.translated / DomainEscape clamp,
                  path.position and swept_pieces         — scanpath.py:68-248
@@ -330,10 +333,47 @@ def monolithic_case(n_steps=8, h=2.5e-5, stride=7):
           f"max={vals[-1].max():.2f} iters={CG_ITERS} counters={stats.counters}")
 
 
+def metrics_case(n_macro=2, h_ref=2.5e-5):
+    from lpbfsim import metrics
+    rng = np.random.default_rng(7)
+    norms = []
+    m1 = lmesh.build_structured_mesh(lmesh.Box((1e-4, 2e-4, 3e-4), (4.5e-4, 4.7e-4, 5e-4)),
+                                     (2.5e-5, 1.5e-5, 1e-5))
+    m2 = m1.translated((3.3e-6, -1.7e-5, 0.0))
+    meshes = []
+    for m in (m1, m2):
+        v = rng.uniform(293.0, 2293.0, m.n_nodes)
+        norms.append((list(m.box.lo), list(m.box.hi), list(m.ncells), v, fem.l2_norm(m, v)))
+        meshes.append(m)
+    cfg = load_config(CFG / "cfg1_m4.cfg")
+    cfg.t_end = n_macro * cfg.dt_macro
+    cfg.h_reference = h_ref
+    cfg.dt_reference = cfg.dt_macro / cfg.micro_steps
+    problem, lm = runner.build_problem(cfg)
+    log = metrics.RunLog()
+    T0 = fem.uniform_field(problem.global_mesh, cfg.T_initial, time=0.0)
+    sched = multirate.MacroSchedule(cfg.dt_macro, cfg.micro_steps, 0.0, cfg.t_end)
+    multirate.run_spacetime(problem, sched, lm, T0, path=cfg.path, policy=cfg.policy, recorder=log.record)
+    traj = runner.run_reference(cfg)
+    rep = metrics.error_metrics(log, traj)
+    np.savez_compressed(
+        OUT / "metrics_cfg1.npz",
+        norm_lo=np.array([n[0] for n in norms]), norm_hi=np.array([n[1] for n in norms]),
+        norm_nc=np.array([n[2] for n in norms]), norm_off=np.array([[0.0, 0.0, 0.0], [3.3e-6, -1.7e-5, 0.0]]),
+        norm_v0=norms[0][3], norm_v1=norms[1][3], norm_val=np.array([n[4] for n in norms]),
+        n_macro=n_macro, h_ref=h_ref, times=rep.times, kinds=np.array(rep.kinds), rel_l2=rep.rel_l2,
+        mean_rel_l2=rep.mean_rel_l2, sawtooth=metrics.sawtooth_fraction(rep, cfg.micro_steps),
+        versions=json.dumps(VERS))
+    print(f"metrics_cfg1: norms={[n[4] for n in norms]} records={len(rep.times)} "
+          f"mean={rep.mean_rel_l2:.6e} rel={rep.rel_l2}")
+
+
 def main():
     quick = "--quick" in sys.argv
     if "--monolithic" in sys.argv:
         return monolithic_case()
+    if "--metrics" in sys.argv:
+        return metrics_case()
     op_case("aniso_local", (1e-4, 2e-4, 3e-4), (2.75e-4, 2.85e-4, 3.44e-4), (2.5e-5, 1.7e-5, 1.1e-5), "local")
     op_case("aniso_global", (0.0, 0.0, 0.0), (1.75e-4, 1.7e-4, 1.1e-4), (2.5e-5, 1.7e-5, 1.1e-5), "global")
     op_case("cfg1_local", (8e-4, 3e-4, 3e-4), (1.2e-3, 7e-4, 5e-4), 1e-5, "local")
@@ -349,6 +389,7 @@ def main():
     run_case("cfg1_uniform", None, {1, 80}, 17)
     run_case("cfg2", 2, {1, 2}, 97)
     monolithic_case()
+    metrics_case()
 
 
 if __name__ == "__main__":

@@ -468,3 +468,31 @@ def test_monolithic_reference_vs_reference_golden():
         np.testing.assert_array_equal(np.packbits(T > TL), z["melt"][k])
     assert rel(traj.values[-1], z["last"]) <= REL
     assert rel(traj.at_time(float(z["t"][int(z["n_steps"]) // 2])).values, z["mid"]) <= REL
+
+
+def test_mass_norm_vs_reference_l2_norm():
+    """metrics.l2_norm on the device (k_mass_norms) against the reference's fem.l2_norm."""
+    z = np.load(GOLDEN / "metrics_cfg1.npz")
+    for k in range(2):
+        grid = _grid(z["norm_lo"][0], z["norm_hi"][0], z["norm_nc"][k], z["norm_off"][k])
+        got = P.l2_norm(grid, z[f"norm_v{k}"])
+        assert abs(got - z["norm_val"][k]) <= 1e-13 * z["norm_val"][k]
+
+
+def test_error_metrics_vs_reference():
+    """error_metrics of a 2-macro-step cfg1 two-level run against the monolithic reference
+    (h = 25 um): every record's relative L2 error and the mean as the reference reports them."""
+    z = np.load(GOLDEN / "metrics_cfg1.npz")
+    cfg = P.load_config(CONFIGS / "cfg1_m4.cfg")
+    n = int(z["n_macro"])
+    log = P.RunLog()
+    P.two_level_run(cfg, recorder=log.record, n_steps=n)
+    cfg.t_end = n * cfg.dt_macro
+    cfg.h_reference = float(z["h_ref"])
+    cfg.dt_reference = cfg.dt_macro / cfg.micro_steps
+    rep = P.error_metrics(log, P.run_reference(cfg))
+    assert list(rep.kinds) == list(z["kinds"])
+    np.testing.assert_allclose(rep.times, z["times"], rtol=0, atol=1e-15)
+    np.testing.assert_allclose(rep.rel_l2, z["rel_l2"], rtol=1e-7, atol=1e-12)
+    assert abs(rep.mean_rel_l2 - float(z["mean_rel_l2"])) <= 1e-7 * float(z["mean_rel_l2"])
+    assert P.metrics.sawtooth_fraction(rep, cfg.micro_steps) == float(z["sawtooth"])

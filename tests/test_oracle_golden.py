@@ -189,3 +189,13 @@ def test_oracle_monolithic_reference_vs_golden():
         np.testing.assert_array_equal(np.packbits(T > TL), z["melt"][k])
     assert np.abs(fields[-1] - z["last"]).max() / z["last"].max() <= 1e-12
     assert [k for _, k in orc.iterations] == list(z["cg_iters"])
+
+
+def test_oracle_mass_norm_vs_reference_l2_norm():
+    """fem.l2_norm (P1 mass matrix, lpbfsim/fem.py:434-446) on an anisotropic mesh and its
+    translate: the per-tet restatement the device kernel k_mass_norms follows."""
+    z = np.load(GOLDEN / "metrics_cfg1.npz")
+    for k in range(2):
+        g = kuhn.KuhnGrid(z["norm_lo"][0], z["norm_hi"][0], z["norm_nc"][k], z["norm_off"][k])
+        v = z[f"norm_v{k}"]
+        assert abs(np.sqrt(kuhn.mass_norm2(g, v)) - z["norm_val"][k]) <= 1e-13 * z["norm_val"][k]
