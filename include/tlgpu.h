@@ -146,6 +146,14 @@ int32_t tl_interpolate_host(const tl_grid_desc* global_grid, const double* value
 int32_t tl_interpolate_points_host(const tl_grid_desc* global_grid, const double* values,
                                    const double* points, int64_t npoints, double* out);
 
+/* ---- transmission_load (twolevel.py:159-183) for constant conductivities:
+ *      load_out (dense, global nodes) = sum over the local grid's interface facets
+ *      (LATERAL + BOTTOM, mesh.py:477-523) of jump * dT_local/dn * w_global at 3
+ *      edge-midpoint quadrature points per facet; jump = kappa_global - kappa_local.
+ *      Deterministic scatter (stable sort by node + ordered sums). */
+int32_t tl_transmission_host(const tl_grid_desc* global_grid, const tl_grid_desc* local_grid,
+                             const double* local_values, double jump, double* load_out);
+
 /* ---- discrete L2 norms with the P1 mass matrix (fem.mass_matrix / l2_norm,
  *      fem.py:434-446): out[0] = (a-b)^T M (a-b) (a^T M a when b == NULL),
  *      out[1] = b^T M b (0 when b == NULL). */

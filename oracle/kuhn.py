@@ -327,3 +327,66 @@ def mass_norm2(grid: KuhnGrid, v: np.ndarray) -> float:
         tot += float(np.sum(vs[0] ** 2 + vs[1] ** 2 + vs[2] ** 2 + vs[3] ** 2 + s1 ** 2))
     h = (np.asarray(grid.hi0) - np.asarray(grid.lo0)) / np.asarray(grid.n)
     return tot * float(np.prod(h)) / 6.0 / 20.0
+
+
+def gamma_facets(L: KuhnGrid):
+    """The interface facets of a local grid (``lpbfsim/mesh.py:477-523``: LATERAL + BOTTOM
+    boundary facets) on the structured Kuhn lattice: per boundary face cell two triangles,
+    each the face of one Kuhn tet.  Yields (triangle (3,3) int lattice offsets, axis, side,
+    the two tet vertices along the normal) per facet, as integer node coordinates:
+
+    - low side of axis a (x_a = 0 plane of a cell at cell index 0): tets whose path steps a
+      last, perm (b, c, a) / (c, b, a); facet (v0, v1, v2); dT/dx_a = (T(v3) - T(v2)) / h_a;
+      outward normal -e_a.
+    - high side (x_a = 1 plane of a cell at index n_a - 1): tets stepping a first,
+      perm (a, b, c) / (a, c, b); facet (v1, v2, v3); dT/dx_a = (T(v1) - T(v0)) / h_a;
+      outward normal +e_a.
+    """
+    n = [int(v) for v in L.n]
+    out = []
+    for a, side in ((0, 0), (0, 1), (1, 0), (1, 1), (2, 0)):
+        b, c = [x for x in range(3) if x != a]
+        cells_b, cells_c = range(n[b]), range(n[c])
+        ca = 0 if side == 0 else n[a] - 1
+        perms = ((b, c, a), (c, b, a)) if side == 0 else ((a, b, c), (a, c, b))
+        for jc in cells_c:
+            for jb in cells_b:
+                cell = [0, 0, 0]
+                cell[a], cell[b], cell[c] = ca, jb, jc
+                for perm in perms:
+                    v = tet_vertices(perm) + np.array(cell)
+                    if side == 0:
+                        out.append((v[[0, 1, 2]], a, side, (v[2], v[3])))
+                    else:
+                        out.append((v[[1, 2, 3]], a, side, (v[0], v[1])))
+    return out
+
+
+def transmission_load(G: KuhnGrid, L: KuhnGrid, T_local: np.ndarray, jump: float) -> np.ndarray:
+    """``transmission_load`` (``lpbfsim/twolevel.py:159-183``) for constant conductivities:
+    sum over interface facets and their 3 edge-midpoint quadrature points (weights
+    area/3, ``mesh.py:131-137``) of jump * dT/dn * w_global, scattered with the global
+    Kuhn-P1 barycentrics of each point (``np.add.at`` in facet order)."""
+    NX, NY = int(L.n[0]) + 1, int(L.n[1]) + 1
+    h = L.h
+    lo = L.box_lo
+
+    def nid(v):
+        return int(v[0] + NX * (v[1] + NY * v[2]))
+
+    pts, dens = [], []
+    for tri, a, side, (va, vb) in gamma_facets(L):
+        b, c = [x for x in range(3) if x != a]
+        area = 0.5 * h[b] * h[c]
+        g = (T_local[nid(vb)] - T_local[nid(va)]) / h[a]
+        dTdn = g if side == 1 else -g
+        X = lo + tri * h
+        for (p, q) in ((0, 1), (1, 2), (0, 2)):
+            pts.append(0.5 * (X[p] + X[q]))
+            dens.append(area / 3.0 * jump * dTdn)
+    pts = np.array(pts)
+    dens = np.array(dens)
+    nodes, bary = locate(G, pts)
+    load = np.zeros(G.n_nodes)
+    np.add.at(load, nodes.reshape(-1), (dens[:, None] * bary).reshape(-1))
+    return load

@@ -9,6 +9,7 @@
 //   [k_pcg<true>]        corrector re-solve of the last interval         (multirate.py:149-150)
 //   k_interp (all)       relocation: local = P1(global) at moved nodes  (scanpath.py:243-248)
 // All state stays on the device; the host only enqueues launches.
+#include <cub/cub.cuh>
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -764,6 +765,41 @@ int32_t tl_interpolate_host(const tl_grid_desc* global_grid, const double* value
     TL_CUDA(cudaGetLastError());
     TL_CUDA(cudaMemcpy(out, dout, sizeof(double) * L.n, cudaMemcpyDeviceToHost));
     cudaFree(dv); cudaFree(dout);
+    return TL_OK;
+}
+
+int32_t tl_transmission_host(const tl_grid_desc* global_grid, const tl_grid_desc* local_grid,
+                             const double* local_values, double jump, double* load_out) {
+    if (!global_grid || !local_grid || !local_values || !load_out) return fail(TL_E_INVALID, "null argument");
+    tl::Grid G{}, L{};
+    if (int rc = make_grid(*global_grid, tl::kBottom, G)) return rc;
+    if (int rc = make_grid(*local_grid, tl::kGamma, L)) return rc;
+    const long long nf = 2ll * ((long long)L.nc[1] * L.nc[2] * 2 + (long long)L.nc[0] * L.nc[2] * 2 +
+                                (long long)L.nc[0] * L.nc[1]);
+    const long long ne = 12 * nf;
+    if (ne >= (1ll << 31)) return fail(TL_E_INVALID, "interface too large");
+    double *dT, *dvals, *dload;
+    int *keys, *keys2, *idx, *idx2;
+    int rc = 0;
+    if ((rc = dalloc(&dT, L.n)) || (rc = dalloc(&dvals, ne)) || (rc = dalloc(&dload, G.n)) ||
+        (rc = dalloc(&keys, ne)) || (rc = dalloc(&keys2, ne)) || (rc = dalloc(&idx, ne)) || (rc = dalloc(&idx2, ne)))
+        return rc;
+    TL_CUDA(cudaMemcpy(dT, local_values, sizeof(double) * L.n, cudaMemcpyHostToDevice));
+    TL_CUDA(cudaMemset(dload, 0, sizeof(double) * G.n));
+    tl::k_trans_entries<<<296, 256>>>(G, L, dT, jump, (int)nf, keys, idx, dvals);
+    TL_CUDA(cudaGetLastError());
+    int bits = 1;
+    while ((1ll << bits) < G.n) ++bits;
+    size_t tmp_bytes = 0;
+    TL_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys2, idx, idx2, (int)ne, 0, bits));
+    void* tmp = nullptr;
+    TL_CUDA(cudaMalloc(&tmp, tmp_bytes));
+    TL_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys2, idx, idx2, (int)ne, 0, bits));
+    tl::k_trans_segsum<<<296, 256>>>(keys2, idx2, dvals, (int)ne, dload);
+    TL_CUDA(cudaGetLastError());
+    TL_CUDA(cudaMemcpy(load_out, dload, sizeof(double) * G.n, cudaMemcpyDeviceToHost));
+    cudaFree(tmp); cudaFree(dT); cudaFree(dvals); cudaFree(dload);
+    cudaFree(keys); cudaFree(keys2); cudaFree(idx); cudaFree(idx2);
     return TL_OK;
 }
 

@@ -12,6 +12,9 @@
 //   k_deposit    SweptTrackDeposit.load scatter (sources.py:164-172), deterministic.
 //   k_melt       max T and melt-node count (T > T_liquidus) of one field.
 //   k_flush      writes a buffer larger than L2 (benchmark hygiene).
+//   k_trans_entries / k_trans_segsum  transmission_load (twolevel.py:159-183): the
+//                interface facets' flux-jump functional on global test functions,
+//                scattered deterministically (stable key sort + ordered segment sums).
 //   k_mass_norms discrete L2 norms v^T M v with the P1 mass matrix (fem.mass_matrix,
 //                fem.py:434-446) of a field difference and of the reference field:
 //                the metrics of metrics.error_metrics (metrics.py:123-165).
@@ -672,6 +675,118 @@ __device__ __forceinline__ double p1_eval(const Grid& G, const double* v, double
     const int n3 = n2 + st[o2];
     const double w0 = 1.0 - xi[o0], w1 = xi[o0] - xi[o1], w2 = xi[o1] - xi[o2], w3 = xi[o2];
     return w0 * v[n0] + w1 * v[n1] + w2 * v[n2] + w3 * v[n3];
+}
+
+// Kuhn-P1 location (Mesh.locate, mesh.py:308-339): the 4 vertex ids and barycentrics
+// of the global tet holding (x, y, z); the same cell/tet choice as p1_eval.
+__device__ __forceinline__ void p1_locate(const Grid& G, double x, double y, double z, int (&nd)[4],
+                                          double (&w)[4]) {
+    const double pt[3] = {x, y, z};
+    int c[3];
+    double xi[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        int ci = (int)floor((pt[a] - G.lo0[a]) / G.h[a]);
+        ci = ci < 0 ? 0 : (ci > G.nc[a] - 1 ? G.nc[a] - 1 : ci);
+        c[a] = ci;
+        xi[a] = (pt[a] - node_coord(G, a, ci)) / G.h[a];
+    }
+    int o0 = 0, o1 = 1, o2 = 2;
+    if (xi[o1] > xi[o0]) { int t = o0; o0 = o1; o1 = t; }
+    if (xi[o2] > xi[o1]) { int t = o1; o1 = o2; o2 = t; }
+    if (xi[o1] > xi[o0]) { int t = o0; o0 = o1; o1 = t; }
+    const int st[3] = {1, G.NX, G.NX * G.NY};
+    nd[0] = c[0] + G.NX * (c[1] + G.NY * c[2]);
+    nd[1] = nd[0] + st[o0];
+    nd[2] = nd[1] + st[o1];
+    nd[3] = nd[2] + st[o2];
+    w[0] = 1.0 - xi[o0];
+    w[1] = xi[o0] - xi[o1];
+    w[2] = xi[o1] - xi[o2];
+    w[3] = xi[o2];
+}
+
+// Interface facets of the local grid (extract_interface, mesh.py:477-523: LATERAL +
+// BOTTOM): faces (x lo, x hi, y lo, y hi, z lo); per face cell (jb inner, jc outer) two
+// triangles, each the face of one Kuhn tet; 3 edge-midpoint quadrature points of weight
+// area/3 (mesh.py:131-137).  Low side of axis a: tets stepping a last, perm (b,c,a) /
+// (c,b,a), facet (v0,v1,v2), dT/dn = -(T(v3) - T(v2)) / h_a.  High side: tets stepping a
+// first, perm (a,b,c) / (a,c,b), facet (v1,v2,v3), dT/dn = (T(v1) - T(v0)) / h_a.
+// Entry e = 3 f + q writes 4 (global node, density * barycentric) pairs at 4 e + r.
+__global__ void k_trans_entries(Grid G, Grid L, const double* __restrict__ T, double jump, int nfacet,
+                                int* __restrict__ keys, int* __restrict__ idx, double* __restrict__ vals) {
+    const int faceA[5] = {0, 0, 1, 1, 2}, faceS[5] = {0, 1, 0, 1, 0};
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < 3 * nfacet; e += gridDim.x * blockDim.x) {
+        int f = e / 3;
+        const int q = e - 3 * f;
+        int fi = 0, a = 0, side = 0, b = 0, c = 0, cnt = 0;
+        for (fi = 0; fi < 5; ++fi) {
+            a = faceA[fi];
+            side = faceS[fi];
+            b = a == 0 ? 1 : 0;
+            c = a == 2 ? 1 : 2;
+            cnt = 2 * L.nc[b] * L.nc[c];
+            if (f < cnt) break;
+            f -= cnt;
+        }
+        const int t = f & 1;
+        const int jb = (f >> 1) % L.nc[b], jc = (f >> 1) / L.nc[b];
+        int cell[3];
+        cell[a] = side == 0 ? 0 : L.nc[a] - 1;
+        cell[b] = jb;
+        cell[c] = jc;
+        int perm[3];
+        if (side == 0) { perm[0] = t == 0 ? b : c; perm[1] = t == 0 ? c : b; perm[2] = a; }
+        else { perm[0] = a; perm[1] = t == 0 ? b : c; perm[2] = t == 0 ? c : b; }
+        int v[4][3];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) v[0][d] = cell[d];
+#pragma unroll
+        for (int r = 1; r < 4; ++r) {
+#pragma unroll
+            for (int d = 0; d < 3; ++d) v[r][d] = v[r - 1][d];
+            v[r][perm[r - 1]] += 1;
+        }
+        auto nid = [&](const int* u) { return u[0] + L.NX * (u[1] + L.NY * u[2]); };
+        double dTdn;
+        int tri0;
+        if (side == 0) {
+            dTdn = -(T[nid(v[3])] - T[nid(v[2])]) / L.h[a];
+            tri0 = 0;
+        } else {
+            dTdn = (T[nid(v[1])] - T[nid(v[0])]) / L.h[a];
+            tri0 = 1;
+        }
+        const int pa = q == 2 ? 0 : q, pb = q == 0 ? 1 : 2;      // edges (0,1) (1,2) (0,2)
+        const int* A = v[tri0 + pa];
+        const int* B = v[tri0 + pb];
+        double x[3];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) x[d] = 0.5 * (node_coord(L, d, A[d]) + node_coord(L, d, B[d]));
+        const double dens = 0.5 * L.h[b] * L.h[c] / 3.0 * jump * dTdn;
+        int nd[4];
+        double w[4];
+        p1_locate(G, x[0], x[1], x[2], nd, w);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            keys[4 * e + r] = nd[r];
+            idx[4 * e + r] = 4 * e + r;
+            vals[4 * e + r] = dens * w[r];
+        }
+    }
+}
+
+// Ordered segment sums over the key-sorted entries (stable sort: entry order within a
+// node) -> load[node]; deterministic, no atomics.
+__global__ void k_trans_segsum(const int* __restrict__ skeys, const int* __restrict__ sidx,
+                               const double* __restrict__ vals, int ne, double* __restrict__ load) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < ne; j += gridDim.x * blockDim.x) {
+        const int key = skeys[j];
+        if (j > 0 && skeys[j - 1] == key) continue;
+        double s = 0.0;
+        for (int u = j; u < ne && skeys[u] == key; ++u) s += vals[sidx[u]];
+        load[key] = s;
+    }
 }
 
 // mode 0: all target nodes -> out_all (and gamma nodes also -> out_gamma if non-null)

@@ -26,9 +26,10 @@ from .fem import FieldState, device_rtol
 from .grid import StructuredGrid
 from .ops import raise_for
 from .schedule import Plan, plan_space, plan_spacetime
+from .errors import UnsupportedOnDevice
 from .twolevel import (
-    TwoLevelProblem, TwoLevelState, extract_interface, initial_state, solve_global, solve_local,
-    two_level_iterate,
+    TwoLevelProblem, TwoLevelState, extract_interface, initial_state, relocate_local, solve_global,
+    solve_local, two_level_iterate,
 )
 
 __all__ = ["MacroSchedule", "DeviceRun", "run_spacetime", "run_space", "macro_step",
@@ -40,6 +41,9 @@ class DeviceRun:
 
     def __init__(self, problem: TwoLevelProblem, local_mesh: StructuredGrid):
         problem.check_device_supported()
+        if not problem.one_way:
+            raise UnsupportedOnDevice("the device-resident run is one-way; two-way coupling runs "
+                                      "through the step-level drivers (run_spacetime / run_space)")
         self.problem = problem
         self.local_mesh = local_mesh
         kappa, rcg, rcl = problem.constants()
@@ -248,7 +252,12 @@ def _deliver(run: DeviceRun, problem, plan: Plan, infos, recorder):
 def run_spacetime(problem: TwoLevelProblem, schedule: MacroSchedule, local_mesh: StructuredGrid,
                   T0: FieldState, path=None, policy=None, stats=None, recorder=None,
                   batch: int | None = None) -> TwoLevelState:
-    """Multirate driver over the whole schedule (``multirate.py:167-191``) on the device."""
+    """Multirate driver over the whole schedule (``multirate.py:167-191``) on the device.
+
+    One-way problems run device-resident (``DeviceRun``); two-way coupling runs the
+    reference's loop over the step-level device solves (``_run_spacetime_steps``)."""
+    if not problem.one_way:
+        return _run_spacetime_steps(problem, schedule, local_mesh, T0, path, policy, stats, recorder)
     extract_interface(local_mesh, problem.global_mesh)
     with DeviceRun(problem, local_mesh) as run:
         def plan_fn(placement, tg, tl, k, nsteps, record):
@@ -262,7 +271,10 @@ def run_spacetime(problem: TwoLevelProblem, schedule: MacroSchedule, local_mesh:
 def run_space(problem: TwoLevelProblem, dt: float, n_steps: int, local_mesh: StructuredGrid,
               T0: FieldState, path=None, policy=None, stats=None, recorder=None,
               batch: int | None = None) -> TwoLevelState:
-    """Uniform-step driver (``multirate.py:194-217``) on the device."""
+    """Uniform-step driver (``multirate.py:194-217``) on the device (two-way coupling: the
+    reference's loop over the step-level device solves, ``_run_space_steps``)."""
+    if not problem.one_way:
+        return _run_space_steps(problem, dt, n_steps, local_mesh, T0, path, policy, stats, recorder)
     extract_interface(local_mesh, problem.global_mesh)
     with DeviceRun(problem, local_mesh) as run:
         def plan_fn(placement, tg, tl, k, nsteps, record):
@@ -291,9 +303,11 @@ def interpolate_trace(i: int, m: int, trace_old, trace_pred):
 
 def macro_step(problem, state: TwoLevelState, schedule: MacroSchedule, k: int, stats=None,
                recorder=None) -> TwoLevelState:
-    """One predictor / micro / corrector cycle (``multirate.py:105-164``), one-way branch."""
-    if not (problem.one_way and problem.interval_source):
-        raise SolverError("the device path implements the one-way, interval-source branch only")
+    """One predictor / micro / corrector cycle (``multirate.py:105-164``); the one-way +
+    interval-source corrector re-solves only the last local interval, otherwise the
+    corrector is the relaxed two-level fixed point (``two_level_iterate``)."""
+    if not problem.interval_source:
+        raise SolverError("the device path implements the interval-source (distributed) global source only")
     m = schedule.micro_per_macro
     delta = schedule.dt_micro
     t_next = schedule.t_macro(k + 1)
@@ -313,11 +327,62 @@ def macro_step(problem, state: TwoLevelState, schedule: MacroSchedule, k: int, s
         local = FieldState(local.mesh, local.values, t_i)
         if recorder is not None:
             recorder("micro", t_i, local, None, 0)
-    corrected = solve_local(problem, before_final, delta, state.gamma, trace_pred, stats=stats)
-    corrected = FieldState(corrected.mesh, corrected.values, t_next)
-    if stats is not None:
-        stats.count("coupling_iterations")
-    new_state = TwoLevelState(predicted, corrected, state.gamma, trace_pred)
+    if problem.one_way:
+        corrected = solve_local(problem, before_final, delta, state.gamma, trace_pred, stats=stats)
+        corrected = FieldState(corrected.mesh, corrected.values, t_next)
+        if stats is not None:
+            stats.count("coupling_iterations")
+        new_state = TwoLevelState(predicted, corrected, state.gamma, trace_pred)
+        iters = 1
+    else:
+        new_state, iters = two_level_iterate(problem, state, schedule.dt_macro, local_from=before_final,
+                                             local_dt=delta, transmission_seed=local, trace_start=trace_pred,
+                                             stats=stats)
     if recorder is not None:
-        recorder("macro", t_next, new_state.local_field, new_state.global_field, 1)
+        recorder("macro", t_next, new_state.local_field, new_state.global_field, iters)
     return new_state
+
+
+def _restamp(state: TwoLevelState, t: float) -> TwoLevelState:
+    return TwoLevelState(FieldState(state.global_field.mesh, state.global_field.values, t),
+                         FieldState(state.local_field.mesh, state.local_field.values, t),
+                         state.gamma, state.trace)
+
+
+def _run_spacetime_steps(problem, schedule, local_mesh, T0, path, policy, stats, recorder):
+    """``run_spacetime`` (``multirate.py:167-191``) over the step-level device solves."""
+    problem.check_device_supported()
+    state = initial_state(problem, local_mesh, T0)
+    if recorder is not None:
+        recorder("initial", schedule.t_start, state.local_field, state.global_field, 0)
+    n = schedule.n_macro
+    for k in range(n):
+        state = macro_step(problem, state, schedule, k, stats=stats, recorder=recorder)
+        if policy is not None and path is not None and k < n - 1:
+            t = min(schedule.t_macro(k + 1), path.t_end)
+            moved = relocate_local(state, policy, path.position(t), path.direction(t), problem)
+            if moved is not state and stats is not None:
+                stats.count("relocations")
+            state = moved
+    return state
+
+
+def _run_space_steps(problem, dt, n_steps, local_mesh, T0, path, policy, stats, recorder):
+    """``run_space`` (``multirate.py:194-217``) over the step-level device solves."""
+    problem.check_device_supported()
+    state = initial_state(problem, local_mesh, T0)
+    if recorder is not None:
+        recorder("initial", T0.time, state.local_field, state.global_field, 0)
+    for k in range(n_steps):
+        t_next = T0.time + (k + 1) * dt
+        state, iters = two_level_iterate(problem, state, t_next - state.time, stats=stats)
+        state = _restamp(state, t_next)
+        if recorder is not None:
+            recorder("macro", t_next, state.local_field, state.global_field, iters)
+        if policy is not None and path is not None and k < n_steps - 1:
+            t = min(t_next, path.t_end)
+            moved = relocate_local(state, policy, path.position(t), path.direction(t), problem)
+            if moved is not state and stats is not None:
+                stats.count("relocations")
+            state = moved
+    return state

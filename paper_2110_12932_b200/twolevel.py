@@ -1,9 +1,13 @@
 """Two-level coupling: problem, state, interface, and the step-level solves.
 
-Mirrors ``lpbfsim/twolevel.py`` for the branch the device represents: equal
-conductivities on both levels (so ``one_way`` holds and the interface
-functional ``transmission_load`` is identically zero, ``twolevel.py:101-113,
-175``) with the interval-based swept-track global source.  The opaque source
+Mirrors ``lpbfsim/twolevel.py`` for constant materials with the interval-based
+swept-track global source.  Equal conductivities on both levels (``one_way``,
+``twolevel.py:101-113``) make the interface functional ``transmission_load``
+identically zero (``:175``) and run device-resident (``multirate.DeviceRun``).
+Distinct conductivities (``global_kappa_scale``, "alternate" mode) are the two-way
+coupling of SURVEY §8f row 2: ``transmission_load`` is a device kernel
+(``tl_transmission_host``) and ``two_level_iterate`` is the reference's relaxed
+fixed point over device solves.  The opaque source
 closures of the reference problem (``runner.py:49-81``) are replaced by the
 beam and scan path themselves, so the device can evaluate the sources.
 
@@ -20,12 +24,12 @@ import numpy as np
 
 from .config import CouplingSettings, SolverSettings
 from .control import LaserBeam, ScanPath, ThermalBC, check_immersed, material_constants
-from .errors import CouplingError, UnsupportedOnDevice
+from .errors import CouplingError, CouplingNonConvergence, UnsupportedOnDevice
 from .fem import BoundarySpec, FieldState, GaussianSource, check_linear_problem, step_backward_euler
 from .grid import BOTTOM, TOP, StructuredGrid
 
 __all__ = ["TwoLevelProblem", "TwoLevelState", "InterfaceGamma", "initial_state", "solve_global",
-           "solve_local", "transmission_load", "extract_interface", "two_level_iterate"]
+           "solve_local", "transmission_load", "extract_interface", "two_level_iterate", "relocate_local"]
 
 
 @dataclass(frozen=True)
@@ -147,9 +151,9 @@ class TwoLevelProblem:
             raise UnsupportedOnDevice("Robin convection (h_conv > 0) is not on the device path")
         if self.bc.emissivity > 0:
             raise UnsupportedOnDevice("radiation (emissivity > 0) is not on the device path")
-        if not self.one_way:
-            raise UnsupportedOnDevice("two-way coupling (kappa_global != kappa_local) is SURVEY §8 f "
-                                      "row 2, not on the device path")
+        if not self.one_way and self.mode != "alternate":
+            raise UnsupportedOnDevice("full-mode overlap feedback (coupling mode 'full' with distinct "
+                                      "materials) is not on the device path")
         if not self.interval_source:
             raise UnsupportedOnDevice("only the distributed (swept-track) global source is on the "
                                       "device path")
@@ -173,11 +177,24 @@ def initial_state(problem: TwoLevelProblem, local_mesh: StructuredGrid,
 
 
 def transmission_load(local_field, gamma, global_mesh, mat_global, mat_local) -> np.ndarray:
-    """Interface functional (``twolevel.py:159-183``): exactly zero for equal conductivities."""
-    if not np.array_equal(mat_global.conductivity_table, mat_local.conductivity_table):
-        raise UnsupportedOnDevice("non-zero transmission load (two-way coupling) is not on the "
-                                  "device path")
-    return np.zeros(global_mesh.n_nodes)
+    """Interface functional (``twolevel.py:159-183``): the integral over the interface facets
+    of (kappa_global - kappa_local) dT_local/dn w_global.  Exactly zero for equal
+    conductivities; otherwise one device call (constant conductivities: the jump is a
+    number, ``tl_transmission_host``)."""
+    from . import _native as N
+    if np.array_equal(mat_global.conductivity_table, mat_local.conductivity_table):
+        return np.zeros(global_mesh.n_nodes)
+    kg, _ = material_constants(mat_global)
+    kl, _ = material_constants(mat_local)
+    lmesh = local_field.mesh
+    T = np.ascontiguousarray(local_field.values, dtype=np.float64)
+    if T.shape != (lmesh.n_nodes,):
+        raise CouplingError("local field does not match its mesh")
+    out = np.zeros(global_mesh.n_nodes)
+    gd, ld = global_mesh.desc(), lmesh.desc()
+    N.check(N.lib().tl_transmission_host(N.C.byref(gd), N.C.byref(ld), N.dptr(T), float(kg - kl),
+                                         N.dptr(out)), "transmission_load")
+    return out
 
 
 def solve_global(problem: TwoLevelProblem, state: TwoLevelState, dt: float,
@@ -218,9 +235,11 @@ def solve_local(problem: TwoLevelProblem, local_from: FieldState, dt: float, gam
 def two_level_iterate(problem: TwoLevelProblem, state: TwoLevelState, dt: float,
                       local_from=None, local_dt=None, transmission_seed=None, trace_start=None,
                       stats=None):
-    """One-way pass of ``two_level_iterate`` (``twolevel.py:299-358``)."""
-    if not problem.one_way:
-        raise UnsupportedOnDevice("the relaxed two-way fixed point is not on the device path")
+    """Relaxed fixed point of one coupled step (``twolevel.py:299-358``): repeat {global
+    solve with the latest interface functional; trace; local solve} until the relative
+    trace change is below the coupling tolerance.  One pass when ``one_way``."""
+    import time as _time
+    cs = problem.coupling
     if local_from is None:
         local_from = state.local_field
     if local_dt is None:
@@ -228,15 +247,52 @@ def two_level_iterate(problem: TwoLevelProblem, state: TwoLevelState, dt: float,
     t1 = state.global_field.time + dt
     if abs(local_from.time + local_dt - t1) > 1e-9 * max(abs(t1), 1e-30):
         raise CouplingError("fine and coarse steps must land on the same time")
-    seed = state.local_field if transmission_seed is None else transmission_seed
-    new_global = solve_global(problem, state, dt, seed, stats=stats)
-    trace = state.gamma.trace_of(new_global.values, problem.global_mesh)
-    new_local = solve_local(problem, local_from, local_dt, state.gamma, trace, stats=stats)
+    trace_prev = state.trace if trace_start is None else trace_start
+    latest_local = state.local_field if transmission_seed is None else transmission_seed
+    change = np.inf
     if stats is not None:
-        stats.count("coupling_iterations")
-    out = TwoLevelState(new_global, FieldState(new_local.mesh, new_local.values, t1),
-                        state.gamma, trace)
-    return out, 1
+        t_begin = _time.perf_counter()
+        inner0 = stats.seconds.get("global_solve", 0.0) + stats.seconds.get("local_solve", 0.0)
+    for it in range(1, cs.max_iterations + 1):
+        new_global = solve_global(problem, state, dt, latest_local, stats=stats)
+        raw = state.gamma.trace_of(new_global.values, problem.global_mesh)
+        relax = 1.0 if (it == 1 and trace_start is None) else cs.omega
+        trace = raw if problem.one_way else trace_prev + relax * (raw - trace_prev)
+        new_local = solve_local(problem, local_from, local_dt, state.gamma, trace, stats=stats)
+        scale = max(float(np.linalg.norm(trace)), 1e-12)
+        change = float(np.linalg.norm(trace - trace_prev)) / scale
+        trace_prev = trace
+        latest_local = new_local
+        if stats is not None:
+            stats.count("coupling_iterations")
+        if problem.one_way or change < cs.tolerance:
+            out = TwoLevelState(new_global, FieldState(new_local.mesh, new_local.values, t1),
+                                state.gamma, trace)
+            if stats is not None:
+                inner = (stats.seconds.get("global_solve", 0.0) + stats.seconds.get("local_solve", 0.0)
+                         - inner0)
+                stats.seconds["coupling_overhead"] = (stats.seconds.get("coupling_overhead", 0.0)
+                                                      + max(_time.perf_counter() - t_begin - inner, 0.0))
+            return out, it
+    raise CouplingNonConvergence(cs.max_iterations, change)
+
+
+def relocate_local(state: TwoLevelState, policy, laser, direction, problem: TwoLevelProblem) -> TwoLevelState:
+    """``relocate_local`` (``scanpath.py:208-248``): snapped, clamped move of the local box
+    toward the laser (``LocalPlacement.relocate``); the whole local field and the trace are
+    P1 interpolations of the current global field (device ``k_interp``)."""
+    from .ops import interpolate_to_grid
+    lmesh = state.local_field.mesh
+    moved = lmesh.placement.relocate(policy, laser, direction, problem.global_mesh.box)
+    if moved is None:
+        return state
+    new_mesh = StructuredGrid(moved)
+    gmesh = problem.global_mesh
+    gamma = extract_interface(new_mesh, gmesh)
+    values = interpolate_to_grid(gmesh, state.global_field.values, new_mesh)
+    local = FieldState(new_mesh, values, state.local_field.time)
+    trace = gamma.trace_of(state.global_field.values, gmesh)
+    return TwoLevelState(state.global_field, local, gamma, trace)
 
 
 class _Null:

@@ -23,6 +23,10 @@ comes from calling the reference's own functions:
 - metrics_cfg1.npz fem.l2_norm on random fields (a plain and a translated anisotropic
                  mesh) and metrics.error_metrics of a 2-macro-step cfg1 two-level run
                  against run_reference (h = 25 um)  — fem.py:434-446, metrics.py:123-165
+- transmission_cfg1.npz twolevel.transmission_load on random local fields (initial and
+                 translated local box, kappa_g = 1.5 kappa_l)  — twolevel.py:159-183
+- run_cfg1_twoway.npz  run_spacetime with two-way coupling (global_kappa_scale 1.5,
+                 omega 0.7): the relaxed two_level_iterate corrector  — twolevel.py:299-358
 - schedule_*.json local-box origins per macro step from the reference's
                  LocalDomainPolicy / Mesh.translated / DomainEscape clamp,
                  path.position and swept_pieces         — scanpath.py:68-248
@@ -368,8 +372,33 @@ def metrics_case(n_macro=2, h_ref=2.5e-5):
           f"mean={rep.mean_rel_l2:.6e} rel={rep.rel_l2}")
 
 
+def transmission_case():
+    cfg = load_config(CFG / "cfg1_twoway.cfg")
+    problem, lm = runner.build_problem(cfg)
+    rng = np.random.default_rng(11)
+    out = {}
+    hl = lm.spacing
+    for k, off in enumerate([(0.0, 0.0, 0.0), (3 * hl[0], -2 * hl[1], 0.0)]):
+        mesh = lm if k == 0 else lm.translated(off)
+        gamma = lmesh.extract_interface(mesh, problem.global_mesh)
+        v = rng.uniform(293.0, 2293.0, mesh.n_nodes)
+        load = twolevel.transmission_load(fem.FieldState(mesh, v, 0.0), gamma, problem.global_mesh,
+                                          problem.mat_global, problem.mat_local)
+        out[f"off{k}"] = np.array(off)
+        out[f"v{k}"] = v
+        out[f"load{k}"] = load
+        print(f"transmission case {k}: nnz={np.count_nonzero(load)} sum={load.sum():.6e} "
+              f"max={np.abs(load).max():.6e}")
+    np.savez_compressed(OUT / "transmission_cfg1.npz", box_lo=np.array(lm.box.lo), box_hi=np.array(lm.box.hi),
+                        ncells=np.array(lm.ncells), **out, versions=json.dumps(VERS))
+
+
 def main():
     quick = "--quick" in sys.argv
+    if "--twoway" in sys.argv:
+        transmission_case()
+        run_case("cfg1_twoway", None, {1, 2, 3, 4}, 7)
+        return
     if "--monolithic" in sys.argv:
         return monolithic_case()
     if "--metrics" in sys.argv:
@@ -390,6 +419,8 @@ def main():
     run_case("cfg2", 2, {1, 2}, 97)
     monolithic_case()
     metrics_case()
+    transmission_case()
+    run_case("cfg1_twoway", None, {1, 2, 3, 4}, 7)
 
 
 if __name__ == "__main__":

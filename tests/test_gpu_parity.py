@@ -496,3 +496,43 @@ def test_error_metrics_vs_reference():
     np.testing.assert_allclose(rep.rel_l2, z["rel_l2"], rtol=1e-7, atol=1e-12)
     assert abs(rep.mean_rel_l2 - float(z["mean_rel_l2"])) <= 1e-7 * float(z["mean_rel_l2"])
     assert P.metrics.sawtooth_fraction(rep, cfg.micro_steps) == float(z["sawtooth"])
+
+
+def test_transmission_load_vs_reference():
+    """twolevel.transmission_load on the device (k_trans_entries + stable key sort + ordered
+    segment sums) against the reference, kappa_g = 1.5 kappa_l, initial and translated box."""
+    from paper_2110_12932_b200.twolevel import extract_interface, transmission_load
+    z = np.load(GOLDEN / "transmission_cfg1.npz")
+    cfg = P.load_config(CONFIGS / "cfg1_twoway.cfg")
+    problem, lm = P.build_problem(cfg)
+    assert not problem.one_way
+    for k in range(2):
+        mesh = lm if k == 0 else lm.translated(tuple(z[f"off{k}"]))
+        np.testing.assert_allclose(mesh.box.lo, z["box_lo"] + z[f"off{k}"], rtol=0, atol=1e-15)
+        gamma = extract_interface(mesh, problem.global_mesh)
+        got = transmission_load(P.FieldState(mesh, z[f"v{k}"], 0.0), gamma, problem.global_mesh,
+                                problem.mat_global, problem.mat_local)
+        ref = z[f"load{k}"]
+        assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
+    # run-to-run deterministic
+    again = transmission_load(P.FieldState(mesh, z["v1"], 0.0), gamma, problem.global_mesh,
+                              problem.mat_global, problem.mat_local)
+    np.testing.assert_array_equal(again, got)
+
+
+def test_two_way_coupled_run_vs_reference():
+    """Two-way coupling (global_kappa_scale 1.5, omega 0.7, tol 1e-8): 4 macro steps whose
+    correctors are the relaxed two_level_iterate fixed point, with relocations; counters
+    (coupling iterations included), times, boxes, fields and melt masks as the reference's."""
+    z, cfg, rec, stats = _golden_run("cfg1_twoway")
+    assert stats.counters == json.loads(str(z["counters"]))
+    TL = cfg.material.T_liquidus
+    s = int(z["stride"])
+    for k, (t, Tl, Tg, lo) in enumerate(rec):
+        assert t == z["t"][k]
+        np.testing.assert_array_equal(lo, z["box"][k])
+        assert rel(Tg[::s], z["gsub"][k]) <= REL and rel(Tl[::s], z["lsub"][k]) <= REL
+        np.testing.assert_array_equal(np.packbits(Tg > TL), z["gmelt"][k])
+        np.testing.assert_array_equal(np.packbits(Tl > TL), z["lmelt"][k])
+        if k in z["full_at"]:
+            assert rel(Tg, z[f"g{k}"]) <= REL and rel(Tl, z[f"l{k}"]) <= REL

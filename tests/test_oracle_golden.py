@@ -199,3 +199,20 @@ def test_oracle_mass_norm_vs_reference_l2_norm():
         g = kuhn.KuhnGrid(z["norm_lo"][0], z["norm_hi"][0], z["norm_nc"][k], z["norm_off"][k])
         v = z[f"norm_v{k}"]
         assert abs(np.sqrt(kuhn.mass_norm2(g, v)) - z["norm_val"][k]) <= 1e-13 * z["norm_val"][k]
+
+
+def test_oracle_transmission_load_vs_reference():
+    """twolevel.transmission_load (kappa_g = 1.5 kappa_l) on random local fields, initial and
+    translated local box: the oracle's structured restatement against the reference."""
+    z = np.load(GOLDEN / "transmission_cfg1.npz")
+    cfg = P.load_config(CONFIGS / "cfg1_twoway.cfg")
+    orc = OracleRun(cfg)
+    jump = cfg.material.conductivity_table[0, 1] - cfg.material_local.conductivity_table[0, 1]
+    assert jump != 0.0
+    for k in range(2):
+        L = kuhn.KuhnGrid(z["box_lo"], z["box_hi"], z["ncells"], z[f"off{k}"])
+        got = kuhn.transmission_load(orc.G, L, z[f"v{k}"], jump)
+        ref = z[f"load{k}"]
+        np.testing.assert_array_equal(np.nonzero(np.abs(got) > 1e-14 * np.abs(ref).max())[0],
+                                      np.nonzero(np.abs(ref) > 1e-14 * np.abs(ref).max())[0])
+        assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
