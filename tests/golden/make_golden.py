@@ -398,6 +398,7 @@ def main():
     if "--twoway" in sys.argv:
         transmission_case()
         run_case("cfg1_twoway", None, {1, 2, 3, 4}, 7)
+        run_case("cfg1_twoway_uniform", None, {1, 4}, 7)
         return
     if "--monolithic" in sys.argv:
         return monolithic_case()
@@ -421,6 +422,7 @@ def main():
     metrics_case()
     transmission_case()
     run_case("cfg1_twoway", None, {1, 2, 3, 4}, 7)
+    run_case("cfg1_twoway_uniform", None, {1, 4}, 7)
 
 
 if __name__ == "__main__":
