@@ -27,6 +27,9 @@ comes from calling the reference's own functions:
                  translated local box, kappa_g = 1.5 kappa_l)  — twolevel.py:159-183
 - run_cfg1_twoway.npz  run_spacetime with two-way coupling (global_kappa_scale 1.5,
                  omega 0.7): the relaxed two_level_iterate corrector  — twolevel.py:299-358
+- picard_*.npz   fem.step_backward_euler with temperature-dependent IN625 tables
+                 (Picard loop, latent secant capacity, lagged radiation + convection on
+                 the top face)  — fem.py:197-268,301-355, materials.py:91-134
 - schedule_*.json local-box origins per macro step from the reference's
                  LocalDomainPolicy / Mesh.translated / DomainEscape clamp,
                  path.position and swept_pieces         — scanpath.py:68-248
@@ -393,8 +396,52 @@ def transmission_case():
                         ncells=np.array(lm.ncells), **out, versions=json.dumps(VERS))
 
 
+PICARD_ITERS: list = []
+
+
+def picard_case(name, latent, radiation, h_conv, seed=5):
+    """One nonlinear implicit step on a 1.0 x 0.6 x 0.3 mm plate (h = 25 um) from a heated
+    T_old (a smooth hot spot under the beam), bottom Dirichlet 293 K, Gaussian beam."""
+    rng = np.random.default_rng(seed)
+    m = lmesh.build_structured_mesh(lmesh.Box((0.0, 0.0, 0.0), (1e-3, 6e-4, 3e-4)), 2.5e-5)
+    mat = lpbfsim.materials.load_material(REF / "lpbfsim" / "data" / "in625.mat")
+    if not latent:
+        mat = mat.with_chi(0.0)
+    bc = sources.ThermalBC(h_conv, 0.8 if radiation else 0.0, 293.0, 293.0)
+    beam = sources.LaserBeam(200.0, 0.35, 5e-5, 5e-5, 0.8)
+    X = m.coords
+    c0 = np.array([4.1e-4, 3.1e-4, 3e-4])
+    r2 = ((X - c0) ** 2 / np.array([1.5e-4, 1.2e-4, 1e-4]) ** 2).sum(axis=1)
+    T_old = 293.0 + 1900.0 * np.exp(-r2) + rng.uniform(0.0, 5.0, m.n_nodes)
+    center = np.array([4.6e-4, 3.0e-4, 3e-4])
+    src = lambda pts: sources.gaussian_source_3d(beam, center, pts)  # noqa: E731
+    bounds = fem.BoundarySpec(bc=bc, robin_tags=(lmesh.TOP,), radiation=radiation,
+                              dirichlet_nodes=m.nodes_on(lmesh.BOTTOM), dirichlet_values=293.0)
+    settings = fem.SolverSettings(picard_tol=1e-8, linear_tol=1e-12, linear_solver="cg")
+    stats = RunStats()
+    CG_ITERS.clear()
+    out = fem.step_backward_euler(fem.FieldState(m, T_old, 0.0), 5e-6, mat, src, bounds, settings,
+                                  latent=latent, stats=stats)
+    np.savez_compressed(
+        OUT / f"picard_{name}.npz", lo=[0.0, 0.0, 0.0], hi=[1e-3, 6e-4, 3e-4], h=2.5e-5, dt=5e-6,
+        T_old=T_old, center=center, sol=out.values, latent=latent, radiation=radiation, h_conv=h_conv,
+        k_table=mat.conductivity_table, c_table=mat.heat_capacity_table,
+        mat_scalars=np.array([mat.rho, mat.chi, mat.T_solidus, mat.T_liquidus, mat.S]),
+        picard=stats.counters.get("picard_iterations", 0), cg_iters=np.array(CG_ITERS),
+        versions=json.dumps(VERS))
+    print(f"picard_{name}: picard={stats.counters} cg={CG_ITERS} max={out.values.max():.2f}")
+
+
+def picard_cases():
+    picard_case("tables", latent=False, radiation=False, h_conv=0.0)
+    picard_case("latent", latent=True, radiation=False, h_conv=0.0)
+    picard_case("full", latent=True, radiation=True, h_conv=10.0)
+
+
 def main():
     quick = "--quick" in sys.argv
+    if "--picard" in sys.argv:
+        return picard_cases()
     if "--twoway" in sys.argv:
         transmission_case()
         run_case("cfg1_twoway", None, {1, 2, 3, 4}, 7)
@@ -423,6 +470,7 @@ def main():
     transmission_case()
     run_case("cfg1_twoway", None, {1, 2, 3, 4}, 7)
     run_case("cfg1_twoway_uniform", None, {1, 4}, 7)
+    picard_cases()
 
 
 if __name__ == "__main__":

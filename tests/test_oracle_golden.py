@@ -216,3 +216,29 @@ def test_oracle_transmission_load_vs_reference():
         np.testing.assert_array_equal(np.nonzero(np.abs(got) > 1e-14 * np.abs(ref).max())[0],
                                       np.nonzero(np.abs(ref) > 1e-14 * np.abs(ref).max())[0])
         assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+def picard_material(z):
+    """The reference's IN625 material (tables in K, chi already 0 for the no-latent case)."""
+    rho, chi, Ts, Tl, S = (float(v) for v in z["mat_scalars"])
+    return P.Material(np.array(z["k_table"]), np.array(z["c_table"]), rho, chi, Ts, Tl, S)
+
+
+@pytest.mark.parametrize("name", ["tables", "latent", "full"])
+def test_oracle_picard_step_vs_reference(name):
+    """Temperature-dependent IN625 step (Picard, latent secant, lagged radiation): the
+    stencil restatement (oracle/varcoef.py) against fem.step_backward_euler."""
+    from oracle import varcoef
+    z = np.load(GOLDEN / f"picard_{name}.npz")
+    G = kuhn.KuhnGrid(z["lo"], z["hi"], np.round((z["hi"] - z["lo"]) / z["h"]).astype(int))
+    mat = picard_material(z)
+    beam = P.LaserBeam(200.0, 0.35, 5e-5, 5e-5, 0.8)
+    src = P.GaussianSource(beam, tuple(z["center"]))
+    rad = bool(z["radiation"])
+    robin = (float(z["h_conv"]), 5.670374419e-8 * 0.8 if rad else 0.0, 293.0) if rad or z["h_conv"] > 0 else None
+    dmask = G.bottom_mask().ravel()
+    g = np.full(G.n_nodes, 293.0)
+    x, npic, cg = varcoef.step(G, mat, z["T_old"], float(z["dt"]), src, dmask, g, bool(z["latent"]), robin)
+    assert npic == int(z["picard"])
+    assert cg == list(z["cg_iters"])
+    assert np.abs(x - z["sol"]).max() / np.abs(z["sol"]).max() <= 1e-12
