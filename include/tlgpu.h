@@ -77,6 +77,27 @@ typedef struct {
     int32_t on;            /* 0: no source (laser off / after path end)   */
 } tl_gaussian;
 
+/* Temperature-dependent material (materials.py:40-134): tables in K, piecewise linear
+ * and clamped (np.interp); latent != 0 adds the secant apparent capacity (fem.py:197-211). */
+typedef struct {
+    const double* k_T;
+    const double* k_v;
+    int32_t nk;
+    const double* c_T;
+    const double* c_v;
+    int32_t nc;
+    double rho, chi, S, T_melt;
+    int32_t latent;
+} tl_vc_material;
+
+/* Top-face Robin terms (fem.py:241-268): h_conv, sigma*emissivity (lagged T^3), T_ambient. */
+typedef struct {
+    double h_conv;
+    double sigma_eps;
+    double T_ambient;
+    int32_t on;
+} tl_robin;
+
 /* Whole two-level run: both grids, constant material, BCs, solver settings. */
 typedef struct {
     tl_grid_desc global_grid;
@@ -145,6 +166,17 @@ int32_t tl_interpolate_host(const tl_grid_desc* global_grid, const double* value
 /* ---- P1 interpolation at arbitrary points (Mesh.interpolate). */
 int32_t tl_interpolate_points_host(const tl_grid_desc* global_grid, const double* values,
                                    const double* points, int64_t npoints, double* out);
+
+/* ---- one Picard pass of fem.step_backward_euler for a NONLINEAR problem (fem.py:307-355):
+ *      assemble_system with coefficients frozen at T_lag (fem.py:129-194: temperature-
+ *      dependent kappa / c tables, latent secant capacity, lumped convection + lagged
+ *      radiation on the top face, Gaussian source, extra_load), constrained (fem.py:89-105,
+ *      Dirichlet set given as a node mask with values g), Jacobi-PCG with scipy's
+ *      recurrences (fem.py:271-298).  x_out has x_D = g.  The caller runs the Picard loop. */
+int32_t tl_vc_step_host(const tl_grid_desc* grid, const tl_vc_material* mat, double dt, const double* T_old,
+                        const double* T_lag, const double* extra_load, const tl_gaussian* src, const tl_robin* robin,
+                        const uint8_t* dirichlet_mask, const double* g, double rtol, int32_t maxiter, double* x_out,
+                        tl_solve_info* info);
 
 /* ---- transmission_load (twolevel.py:159-183) for constant conductivities:
  *      load_out (dense, global nodes) = sum over the local grid's interface facets

@@ -45,6 +45,17 @@ class Gaussian(C.Structure):
                 ("center", _d3), ("on", C.c_int32)]
 
 
+class VcMaterial(C.Structure):
+    _fields_ = [("k_T", C.c_void_p), ("k_v", C.c_void_p), ("nk", C.c_int32), ("c_T", C.c_void_p),
+                ("c_v", C.c_void_p), ("nc", C.c_int32), ("rho", C.c_double), ("chi", C.c_double),
+                ("S", C.c_double), ("T_melt", C.c_double), ("latent", C.c_int32)]
+
+
+class Robin(C.Structure):
+    _fields_ = [("h_conv", C.c_double), ("sigma_eps", C.c_double), ("T_ambient", C.c_double),
+                ("on", C.c_int32)]
+
+
 class RunDesc(C.Structure):
     _fields_ = [("global_grid", GridDesc), ("local_grid", GridDesc), ("kappa", C.c_double),
                 ("rho_c_global", C.c_double), ("rho_c_local", C.c_double),
@@ -99,6 +110,9 @@ SIGNATURES = [
     ("tl_deposit_host", C.c_int32, [C.POINTER(GridDesc), _dp, _dp, C.c_int32, _dp]),
     ("tl_mass_norms_host", C.c_int32, [C.POINTER(GridDesc), _dp, _dp, _dp]),
     ("tl_transmission_host", C.c_int32, [C.POINTER(GridDesc), C.POINTER(GridDesc), _dp, C.c_double, _dp]),
+    ("tl_vc_step_host", C.c_int32, [C.POINTER(GridDesc), C.POINTER(VcMaterial), C.c_double, _dp, _dp, _dp,
+                                    C.POINTER(Gaussian), C.POINTER(Robin), C.c_void_p, _dp, C.c_double,
+                                    C.c_int32, _dp, C.POINTER(SolveInfo)]),
     ("tl_error_l2_host", C.c_int32, [C.POINTER(GridDesc), _dp, C.POINTER(GridDesc), _dp, _dp]),
     ("tl_run_create", C.c_int32, [C.POINTER(RunDesc), C.POINTER(_P)]),
     ("tl_run_destroy", C.c_int32, [_P]),

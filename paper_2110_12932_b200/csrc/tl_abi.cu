@@ -11,6 +11,7 @@
 // All state stays on the device; the host only enqueues launches.
 #include <cub/cub.cuh>
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -22,6 +23,7 @@
 #include "tl_stream.cuh"
 #include "tl_tiled.cuh"
 #include "tl_slab.cuh"
+#include "tl_vc.cuh"
 
 namespace {
 
@@ -765,6 +767,113 @@ int32_t tl_interpolate_host(const tl_grid_desc* global_grid, const double* value
     TL_CUDA(cudaGetLastError());
     TL_CUDA(cudaMemcpy(out, dout, sizeof(double) * L.n, cudaMemcpyDeviceToHost));
     cudaFree(dv); cudaFree(dout);
+    return TL_OK;
+}
+
+int32_t tl_vc_step_host(const tl_grid_desc* grid, const tl_vc_material* mat, double dt, const double* T_old,
+                        const double* T_lag, const double* extra_load, const tl_gaussian* src, const tl_robin* robin,
+                        const uint8_t* dirichlet_mask, const double* g, double rtol, int32_t maxiter, double* x_out,
+                        tl_solve_info* info) {
+    if (!grid || !mat || !T_old || !T_lag || !dirichlet_mask || !g || !x_out || !info)
+        return fail(TL_E_INVALID, "null argument");
+    if (!(dt > 0.0)) return fail(TL_E_INVALID, "time step must be positive");
+    if (mat->nk < 2 || mat->nc < 2) return fail(TL_E_INVALID, "material tables need two rows");
+    tl::Grid G{};
+    if (int rc = make_grid(*grid, tl::kBottom, G)) return rc;
+    const int n = G.n;
+    constexpr int kNB = 296, kT = 256;
+    double *dTo, *dTl, *dex = nullptr, *dg, *diag, *wx, *wy, *wz, *b, *x, *r, *z, *pv, *q, *part, *tabs;
+    unsigned char* dm;
+    int rc = 0;
+    if ((rc = dalloc(&dTo, n)) || (rc = dalloc(&dTl, n)) || (extra_load && (rc = dalloc(&dex, n))) ||
+        (rc = dalloc(&dg, n)) || (rc = dalloc(&diag, n)) || (rc = dalloc(&wx, n)) || (rc = dalloc(&wy, n)) ||
+        (rc = dalloc(&wz, n)) || (rc = dalloc(&b, n)) || (rc = dalloc(&x, n)) || (rc = dalloc(&r, n)) ||
+        (rc = dalloc(&z, n)) || (rc = dalloc(&pv, n)) || (rc = dalloc(&q, n)) || (rc = dalloc(&part, 2 * kNB)) ||
+        (rc = dalloc(&tabs, 2 * (mat->nk + mat->nc))))
+        return rc;
+    TL_CUDA(cudaMalloc((void**)&dm, n));
+    TL_CUDA(cudaMemcpy(dTo, T_old, sizeof(double) * n, cudaMemcpyHostToDevice));
+    TL_CUDA(cudaMemcpy(dTl, T_lag, sizeof(double) * n, cudaMemcpyHostToDevice));
+    if (dex) TL_CUDA(cudaMemcpy(dex, extra_load, sizeof(double) * n, cudaMemcpyHostToDevice));
+    TL_CUDA(cudaMemcpy(dg, g, sizeof(double) * n, cudaMemcpyHostToDevice));
+    TL_CUDA(cudaMemcpy(dm, dirichlet_mask, n, cudaMemcpyHostToDevice));
+    TL_CUDA(cudaMemcpy(tabs, mat->k_T, sizeof(double) * mat->nk, cudaMemcpyHostToDevice));
+    TL_CUDA(cudaMemcpy(tabs + mat->nk, mat->k_v, sizeof(double) * mat->nk, cudaMemcpyHostToDevice));
+    TL_CUDA(cudaMemcpy(tabs + 2 * mat->nk, mat->c_T, sizeof(double) * mat->nc, cudaMemcpyHostToDevice));
+    TL_CUDA(cudaMemcpy(tabs + 2 * mat->nk + mat->nc, mat->c_v, sizeof(double) * mat->nc, cudaMemcpyHostToDevice));
+    tl::VcMat M{tabs, tabs + mat->nk, tabs + 2 * mat->nk, tabs + 2 * mat->nk + mat->nc, mat->nk, mat->nc,
+                mat->rho, mat->chi, mat->S, mat->T_melt, mat->latent};
+    tl::Gauss S{};
+    if (src && src->on) {
+        S.peak = src->peak; S.radius = src->radius; S.depth = src->depth;
+        for (int a = 0; a < 3; ++a) S.center[a] = src->center[a];
+        S.on = 1;
+    }
+    tl::VcRobin RB{0.0, 0.0, 0.0, 0};
+    if (robin && robin->on) RB = tl::VcRobin{robin->h_conv, robin->sigma_eps, robin->T_ambient, 1};
+    tl::k_vc_assemble<<<kNB, kT>>>(G, M, dTo, dTl, dex, dt, S, RB, diag, wx, wy, wz, b);
+    tl::k_vc_constrain_b<<<kNB, kT>>>(G, dm, dg, wx, wy, wz, diag, b);
+    tl::k_vc_constrain_w<<<kNB, kT>>>(G, dm, wx, wy, wz);
+    TL_CUDA(cudaGetLastError());
+    std::vector<double> hp(2 * kNB);
+    auto sum = [&](int nv, double* out) -> int {
+        TL_CUDA(cudaMemcpy(hp.data(), part, sizeof(double) * nv * kNB, cudaMemcpyDeviceToHost));
+        for (int k = 0; k < nv; ++k) {
+            double s = 0.0;
+            for (int e = 0; e < kNB; ++e) s += hp[k * kNB + e];
+            out[k] = s;
+        }
+        return TL_OK;
+    };
+    // solve_linear cg branch (fem.py:271-291) with scipy's recurrences
+    double bb[2];
+    tl::k_vc_precond<<<kNB, kT>>>(n, diag, b, z, part);     // r.r of b in slot 1
+    if (int e = sum(2, bb)) return e;
+    const double bnorm = sqrt(bb[1]);
+    info->bnorm = bnorm;
+    info->iterations = 0;
+    info->status = TL_SOLVE_OK;
+    info->rnorm = bnorm;
+    info->true_resid = 0.0;
+    TL_CUDA(cudaMemset(x, 0, sizeof(double) * n));
+    if (bnorm > 0.0) {
+        const double atol = rtol * bnorm;
+        TL_CUDA(cudaMemcpy(r, b, sizeof(double) * n, cudaMemcpyDeviceToDevice));
+        double rr = bb[1], rho_prev = 1.0;
+        int it = 0, status = TL_SOLVE_MAXITER;
+        for (; it < maxiter; ++it) {
+            if (!std::isfinite(rr)) { status = TL_SOLVE_NONFINITE; break; }
+            if (sqrt(rr) < atol) { status = TL_SOLVE_OK; break; }
+            double rz[2];
+            tl::k_vc_precond<<<kNB, kT>>>(n, diag, r, z, part);
+            if (int e = sum(2, rz)) return e;
+            const double rho = rz[0];
+            tl::k_vc_dir<<<kNB, kT>>>(n, z, it > 0 ? rho / rho_prev : 0.0, it == 0 ? 1 : 0, pv);
+            double pq;
+            tl::k_vc_matvec<<<kNB, kT>>>(G, diag, wx, wy, wz, pv, q, part);
+            if (int e = sum(1, &pq)) return e;
+            const double alpha = rho / pq;
+            tl::k_vc_update<<<kNB, kT>>>(n, alpha, pv, q, x, r, part);
+            if (int e = sum(1, &rr)) return e;
+            rho_prev = rho;
+        }
+        if (it >= maxiter) status = TL_SOLVE_MAXITER;
+        info->iterations = it;
+        info->rnorm = sqrt(rr);
+        double tr;
+        tl::k_vc_resid<<<kNB, kT>>>(G, diag, wx, wy, wz, x, b, part);
+        if (int e = sum(1, &tr)) return e;
+        info->true_resid = sqrt(tr) / bnorm;
+        if (status == TL_SOLVE_OK && (!std::isfinite(info->true_resid) || info->true_resid > 1e2 * rtol))
+            status = TL_SOLVE_RESIDUAL;
+        info->status = status;
+    }
+    tl::k_vc_fix<<<kNB, kT>>>(n, dm, dg, x);
+    TL_CUDA(cudaGetLastError());
+    TL_CUDA(cudaMemcpy(x_out, x, sizeof(double) * n, cudaMemcpyDeviceToHost));
+    for (double* pp : {dTo, dTl, dg, diag, wx, wy, wz, b, x, r, z, pv, q, part, tabs}) cudaFree(pp);
+    if (dex) cudaFree(dex);
+    cudaFree(dm);
     return TL_OK;
 }
 

@@ -1,0 +1,304 @@
+// tl_vc.cuh — temperature-dependent implicit step, sm_100a, fp64.
+//
+// assemble_system (lpbfsim/fem.py:129-194) with _material_arrays (:214-238), the secant
+// latent capacity (:197-211) and the lumped convection / lagged-radiation top terms
+// (_add_robin, :241-268), then constrained (:89-105) + Jacobi-PCG with scipy's
+// recurrences (solve_linear, :271-291).  The Picard loop (:307-355) drives one call of
+// tl_vc_step_host per pass.
+//
+// On a Kuhn tet the P1 gradients are axis-aligned along the tet's path (000 -> +e_p0 ->
+// +e_p1 -> 111), so kbar vol grad_i.grad_j couples only consecutive path vertices and the
+// assembled operator is a 7-point stencil with per-edge weights (oracle/varcoef.py):
+//     (A x)_p = diag_p x_p - sum_a (w_a[p] x_{p+e_a} + w_a[p-e_a] x_{p-e_a}).
+// k_vc_assemble computes diag, w and b node by node (gather over the 24 tets touching the
+// node: no atomics, deterministic); the CG vectors are swept by plain grid-stride
+// kernels with fixed-order block partials summed on the host.  This path is a seam-3
+// solver (host buffers in and out), not the device-resident two-level loop.
+#pragma once
+
+#include "tl_kernels.cuh"
+
+namespace tl {
+
+struct VcMat {
+    const double *kT, *kv, *cT, *cv;
+    int nk, nc;
+    double rho, chi, S, Tm;
+    int latent;
+};
+
+struct VcRobin {
+    double h, se, Tamb;
+    int on;
+};
+
+// np.interp: clamped outside the table, linear inside
+__device__ __forceinline__ double vc_interp(double x, const double* xp, const double* fp, int n) {
+    if (!(x > xp[0])) return fp[0];
+    if (!(x < xp[n - 1])) return fp[n - 1];
+    int lo = 0, hi = n - 1;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (xp[mid] <= x) lo = mid; else hi = mid;
+    }
+    const double slope = (fp[lo + 1] - fp[lo]) / (xp[lo + 1] - xp[lo]);
+    return slope * (x - xp[lo]) + fp[lo];
+}
+
+__device__ __forceinline__ double vc_phase(const VcMat& M, double T) {
+    return 0.5 * (1.0 + tanh(M.S * (T - M.Tm)));
+}
+
+__device__ __forceinline__ double vc_phase_deriv(const VcMat& M, double T) {
+    const double ax = fabs(M.S * (T - M.Tm));
+    const double e = exp(-ax);
+    const double s = 2.0 * e / (1.0 + e * e);
+    return 0.5 * M.S * (s * s);
+}
+
+// _latent_slope: chi * secant of the liquid fraction over the step
+__device__ __forceinline__ double vc_latent(const VcMat& M, double T, double T_old) {
+    const double dT = T - T_old;
+    if (fabs(dT) < 1e-6) return M.chi * vc_phase_deriv(M, 0.5 * (T + T_old));
+    return M.chi * ((vc_phase(M, T) - vc_phase(M, T_old)) / dT);
+}
+
+__global__ void k_vc_assemble(Grid g, VcMat M, const double* __restrict__ T_old, const double* __restrict__ T_lag,
+                              const double* __restrict__ extra, double dt, Gauss src, VcRobin rb,
+                              double* __restrict__ diag, double* __restrict__ wx, double* __restrict__ wy,
+                              double* __restrict__ wz, double* __restrict__ b) {
+    const double A = TL_QA, B = TL_QB;
+    const double vol = g.h[0] * g.h[1] * g.h[2] / 6.0;
+    const int perms[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+    const int st[3] = {1, g.NX, g.NX * g.NY};
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < g.n; p += gridDim.x * blockDim.x) {
+        int idx[3];
+        decode(g, p, idx[0], idx[1], idx[2]);
+        double dg = 0.0, bb = 0.0, wf[3] = {0.0, 0.0, 0.0};
+        for (int o = 0; o < 8; ++o) {
+            const int oo[3] = {o & 1, (o >> 1) & 1, (o >> 2) & 1};
+            int cell[3];
+            bool ok = true;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                cell[a] = idx[a] - oo[a];
+                ok = ok && cell[a] >= 0 && cell[a] < g.nc[a];
+            }
+            if (!ok) continue;
+            const int c0 = cell[0] + g.NX * (cell[1] + g.NY * cell[2]);
+            for (int t = 0; t < 6; ++t) {
+                // path offsets; r = position of p on the path
+                int off[4][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+                int r = -1;
+                for (int v = 0; v < 4; ++v) {
+                    if (v > 0) {
+                        for (int a = 0; a < 3; ++a) off[v][a] = off[v - 1][a];
+                        off[v][perms[t][v - 1]] += 1;
+                    }
+                    if (off[v][0] == oo[0] && off[v][1] == oo[1] && off[v][2] == oo[2]) r = v;
+                }
+                if (r < 0) continue;
+                int id[4];
+                double Tl[4], To[4];
+                for (int v = 0; v < 4; ++v) {
+                    id[v] = c0 + off[v][0] * st[0] + off[v][1] * st[1] + off[v][2] * st[2];
+                    Tl[v] = T_lag[id[v]];
+                    To[v] = T_old[id[v]];
+                }
+                double kbar = 0.0, ml = 0.0, qs = 0.0;
+                for (int q = 0; q < 4; ++q) {
+                    double tq = 0.0, tqo = 0.0;
+                    for (int v = 0; v < 4; ++v) {
+                        const double ph = (v == q) ? A : B;
+                        tq += ph * Tl[v];
+                        tqo += ph * To[v];
+                    }
+                    const double kq = vc_interp(tq, M.kT, M.kv, M.nk);
+                    double cq = vc_interp(tq, M.cT, M.cv, M.nc);
+                    if (M.latent) cq += vc_latent(M, tq, tqo);
+                    kbar += 0.25 * kq;
+                    const double phr = (r == q) ? A : B;
+                    ml += 0.25 * (M.rho * cq / dt) * phr;
+                    if (src.on) {
+                        double x[3];
+                        for (int a = 0; a < 3; ++a) {
+                            double s = 0.0;
+                            for (int v = 0; v < 4; ++v)
+                                s += ((v == q) ? A : B) * node_coord(g, a, cell[a] + off[v][a]);
+                            x[a] = s;
+                        }
+                        const double ex = 3.0 * ((x[0] - src.center[0]) / src.radius) * ((x[0] - src.center[0]) / src.radius);
+                        const double ey = 3.0 * ((x[1] - src.center[1]) / src.radius) * ((x[1] - src.center[1]) / src.radius);
+                        const double ez = 3.0 * ((x[2] - src.center[2]) / src.depth) * ((x[2] - src.center[2]) / src.depth);
+                        qs += 0.25 * (src.peak * exp(-(ex + ey + ez))) * phr;
+                    }
+                }
+                ml *= vol;
+                dg += ml;
+                bb += ml * To[r] + qs * vol;
+                if (r > 0) {
+                    const int ax = perms[t][r - 1];
+                    dg += kbar * vol / (g.h[ax] * g.h[ax]);
+                }
+                if (r < 3) {
+                    const int ax = perms[t][r];
+                    const double we = kbar * vol / (g.h[ax] * g.h[ax]);
+                    dg += we;
+                    wf[ax] += we;
+                }
+            }
+        }
+        if (rb.on && idx[2] == g.nc[2]) {
+            // top triangles (0,0)-(1,0)-(1,1) and (0,0)-(0,1)-(1,1) of the top-layer cells
+            const int tri[2][3][2] = {{{0, 0}, {1, 0}, {1, 1}}, {{0, 0}, {0, 1}, {1, 1}}};
+            const double area = 0.5 * g.h[0] * g.h[1];
+            const double load = rb.h * rb.Tamb + rb.se * (rb.Tamb * rb.Tamb * rb.Tamb * rb.Tamb);
+            for (int cj = idx[1] - 1; cj <= idx[1]; ++cj) {
+                for (int ci = idx[0] - 1; ci <= idx[0]; ++ci) {
+                    if (ci < 0 || cj < 0 || ci >= g.nc[0] || cj >= g.nc[1]) continue;
+                    for (int t = 0; t < 2; ++t) {
+                        int me = -1, vid[3];
+                        for (int v = 0; v < 3; ++v) {
+                            const int vi = ci + tri[t][v][0], vj = cj + tri[t][v][1];
+                            vid[v] = vi + g.NX * (vj + g.NY * idx[2]);
+                            if (vi == idx[0] && vj == idx[1]) me = v;
+                        }
+                        if (me < 0) continue;
+                        for (int v = 0; v < 3; ++v) {
+                            if (v == me) continue;
+                            const double tq = 0.5 * (T_lag[vid[me]] + T_lag[vid[v]]);
+                            const double coeff = rb.h + rb.se * (tq * tq * tq);
+                            dg += coeff * 0.5 * area / 3.0;
+                            bb += load * 0.5 * area / 3.0;
+                        }
+                    }
+                }
+            }
+        }
+        if (extra) bb += extra[p];
+        diag[p] = dg;
+        wx[p] = wf[0];
+        wy[p] = wf[1];
+        wz[p] = wf[2];
+        b[p] = bb;
+    }
+}
+
+// constrained(): free rows take their Dirichlet couplings into b; Dirichlet rows -> identity
+__global__ void k_vc_constrain_b(Grid g, const unsigned char* __restrict__ dm, const double* __restrict__ gv,
+                                 const double* __restrict__ wx, const double* __restrict__ wy,
+                                 const double* __restrict__ wz, double* __restrict__ diag, double* __restrict__ b) {
+    const int st[3] = {1, g.NX, g.NX * g.NY};
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < g.n; p += gridDim.x * blockDim.x) {
+        if (dm[p]) { b[p] = gv[p]; diag[p] = 1.0; continue; }
+        int idx[3];
+        decode(g, p, idx[0], idx[1], idx[2]);
+        const double* w[3] = {wx, wy, wz};
+        double add = 0.0;
+        for (int a = 0; a < 3; ++a) {
+            if (idx[a] < g.nc[a] && dm[p + st[a]]) add += w[a][p] * gv[p + st[a]];
+            if (idx[a] > 0 && dm[p - st[a]]) add += w[a][p - st[a]] * gv[p - st[a]];
+        }
+        b[p] += add;
+    }
+}
+
+__global__ void k_vc_constrain_w(Grid g, const unsigned char* __restrict__ dm, double* __restrict__ wx,
+                                 double* __restrict__ wy, double* __restrict__ wz) {
+    const int st[3] = {1, g.NX, g.NX * g.NY};
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < g.n; p += gridDim.x * blockDim.x) {
+        int idx[3];
+        decode(g, p, idx[0], idx[1], idx[2]);
+        double* w[3] = {wx, wy, wz};
+        for (int a = 0; a < 3; ++a)
+            if (dm[p] || (idx[a] < g.nc[a] && dm[p + st[a]])) w[a][p] = 0.0;
+    }
+}
+
+__device__ __forceinline__ double vc_apply(const Grid& g, const double* diag, const double* wx, const double* wy,
+                                           const double* wz, const double* x, int p) {
+    int i, j, k;
+    decode(g, p, i, j, k);
+    const int sy = g.NX, sz = g.NX * g.NY;
+    double y = diag[p] * x[p];
+    if (i < g.nc[0]) y -= wx[p] * x[p + 1];
+    if (i > 0) y -= wx[p - 1] * x[p - 1];
+    if (j < g.nc[1]) y -= wy[p] * x[p + sy];
+    if (j > 0) y -= wy[p - sy] * x[p - sy];
+    if (k < g.nc[2]) y -= wz[p] * x[p + sz];
+    if (k > 0) y -= wz[p - sz] * x[p - sz];
+    return y;
+}
+
+// block partial of sum f(p) (fixed order: grid-stride per thread, warp/ block tree)
+template <int NV>
+__device__ __forceinline__ void vc_block_store(double (&v)[NV], double* part) {
+    __shared__ double red[NV * 32];
+    block_sum<NV>(v, red);
+    if (threadIdx.x == 0)
+        for (int k = 0; k < NV; ++k) part[k * gridDim.x + blockIdx.x] = v[k];
+}
+
+// z = invd r; partials (r.z, r.r)
+__global__ void k_vc_precond(int n, const double* __restrict__ diag, const double* __restrict__ r,
+                             double* __restrict__ z, double* part) {
+    double v[2] = {0.0, 0.0};
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+        const double zz = (1.0 / diag[p]) * r[p];
+        z[p] = zz;
+        v[0] += r[p] * zz;
+        v[1] += r[p] * r[p];
+    }
+    vc_block_store<2>(v, part);
+}
+
+// p = z (first) or p * beta + z
+__global__ void k_vc_dir(int n, const double* __restrict__ z, double beta, int first, double* __restrict__ pv) {
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x)
+        pv[p] = first ? z[p] : pv[p] * beta + z[p];
+}
+
+// q = A p; partial p.q
+__global__ void k_vc_matvec(Grid g, const double* __restrict__ diag, const double* __restrict__ wx,
+                            const double* __restrict__ wy, const double* __restrict__ wz, const double* __restrict__ pv,
+                            double* __restrict__ q, double* part) {
+    double v[1] = {0.0};
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < g.n; p += gridDim.x * blockDim.x) {
+        const double qq = vc_apply(g, diag, wx, wy, wz, pv, p);
+        q[p] = qq;
+        v[0] += pv[p] * qq;
+    }
+    vc_block_store<1>(v, part);
+}
+
+// x += alpha p; r -= alpha q; partial r.r
+__global__ void k_vc_update(int n, double alpha, const double* __restrict__ pv, const double* __restrict__ q,
+                            double* __restrict__ x, double* __restrict__ r, double* part) {
+    double v[1] = {0.0};
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+        x[p] += alpha * pv[p];
+        const double rr = r[p] - alpha * q[p];
+        r[p] = rr;
+        v[0] += rr * rr;
+    }
+    vc_block_store<1>(v, part);
+}
+
+// true residual partial ||A x - b||^2, and x_D = g afterwards
+__global__ void k_vc_resid(Grid g, const double* __restrict__ diag, const double* __restrict__ wx,
+                           const double* __restrict__ wy, const double* __restrict__ wz, const double* __restrict__ x,
+                           const double* __restrict__ b, double* part) {
+    double v[1] = {0.0};
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < g.n; p += gridDim.x * blockDim.x) {
+        const double d = vc_apply(g, diag, wx, wy, wz, x, p) - b[p];
+        v[0] += d * d;
+    }
+    vc_block_store<1>(v, part);
+}
+
+__global__ void k_vc_fix(int n, const unsigned char* __restrict__ dm, const double* __restrict__ gv, double* __restrict__ x) {
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x)
+        if (dm[p]) x[p] = gv[p];
+}
+
+}  // namespace tl

@@ -19,7 +19,7 @@ import numpy as np
 from . import _native as N
 from .config import SolverSettings
 from .control import ThermalBC, material_constants
-from .errors import SolverError, UnsupportedOnDevice
+from .errors import NonConvergence, SolverError, UnsupportedOnDevice
 from .grid import BOTTOM, TOP, StructuredGrid
 
 __all__ = ["FieldState", "uniform_field", "SolverSettings", "BoundarySpec", "GaussianSource",
@@ -127,18 +127,108 @@ def _dirichlet_kind(mesh: StructuredGrid, nodes: np.ndarray) -> int:
     raise UnsupportedOnDevice("the device represents the bottom-face or interface Dirichlet sets only")
 
 
+def problem_is_linear(mat, bounds: BoundarySpec, latent: bool) -> bool:
+    """``_problem_is_linear`` (``fem.py:301-304``)."""
+    radiative = bounds.radiation and bounds.bc.emissivity > 0 and len(bounds.robin_tags) > 0
+    return bool(mat.is_constant) and not radiative and not (latent and mat.chi > 0.0)
+
+
+def _needs_general_path(mat, bounds: BoundarySpec, latent: bool) -> bool:
+    convective = bool(bounds.robin_tags) and bounds.bc.h_conv > 0
+    return convective or not problem_is_linear(mat, bounds, latent)
+
+
+def _step_general(state: FieldState, dt: float, mat, source, bounds: BoundarySpec, settings: SolverSettings,
+                  latent: bool, extra_load, stats) -> FieldState:
+    """``step_backward_euler`` (``fem.py:307-355``) for temperature-dependent tables, latent
+    heat, convection and lagged radiation: the reference's Picard loop (lag damping on
+    stalls) over device passes (``tl_vc_step_host``: assembly, constraint and Jacobi-PCG on
+    the GPU).  The loop control (the relative increment) is computed on the host from the
+    pass's result, as the reference does."""
+    import ctypes as C
+    from .ops import raise_for
+    mesh = state.mesh
+    if any(t != TOP for t in bounds.robin_tags):
+        raise UnsupportedOnDevice("Robin terms are supported on the top face only")
+    rad = bool(bounds.radiation and bounds.bc.emissivity > 0 and bounds.robin_tags)
+    conv = bool(bounds.robin_tags) and bounds.bc.h_conv > 0
+    kt = np.ascontiguousarray(mat.conductivity_table, dtype=np.float64)
+    ct = np.ascontiguousarray(mat.heat_capacity_table, dtype=np.float64)
+    tabs = [np.ascontiguousarray(kt[:, 0]), np.ascontiguousarray(kt[:, 1]),
+            np.ascontiguousarray(ct[:, 0]), np.ascontiguousarray(ct[:, 1])]
+    md = N.VcMaterial(tabs[0].ctypes.data, tabs[1].ctypes.data, len(kt), tabs[2].ctypes.data,
+                      tabs[3].ctypes.data, len(ct), float(mat.rho), float(mat.chi), float(mat.S),
+                      0.5 * (float(mat.T_solidus) + float(mat.T_liquidus)),
+                      1 if (latent and mat.chi > 0.0) else 0)
+    rb = N.Robin(float(bounds.bc.h_conv) if conv else 0.0,
+                 float(bounds.bc.sigma_sb * bounds.bc.emissivity) if rad else 0.0,
+                 float(bounds.bc.T_ambient), 1 if (conv or rad) else 0)
+    src = None
+    if source is not None:
+        peak, radius, depth, center = source.device_args()
+        src = N.Gaussian(float(peak), float(radius), float(depth), (C.c_double * 3)(*map(float, center)), 1)
+    n = mesh.n_nodes
+    dnodes = np.asarray(bounds.dirichlet_nodes, dtype=np.int64)
+    dmask = np.zeros(n, dtype=np.uint8)
+    dmask[dnodes] = 1
+    g = np.zeros(n)
+    g[dnodes] = bounds.dirichlet_array()
+    ld = None if extra_load is None else np.ascontiguousarray(extra_load, dtype=np.float64)
+    if ld is not None and ld.shape != (n,):
+        raise SolverError("extra load does not match the mesh")
+    T_old = np.ascontiguousarray(state.values, dtype=np.float64)
+    desc = mesh.desc()
+    rtol = device_rtol(settings)
+    linear = problem_is_linear(mat, bounds, latent)
+    max_iter = 1 if linear else settings.picard_max_iter
+    T_lag = T_old
+    inc, prev_inc, theta = np.inf, np.inf, 1.0
+    t_new = state.time + dt
+    for it in range(1, max_iter + 1):
+        x = np.empty(n)
+        info = N.SolveInfo()
+        timer = stats.timer("assembly") if stats is not None else None
+        if timer is not None:
+            timer.__enter__()
+        try:
+            N.check(N.lib().tl_vc_step_host(C.byref(desc), C.byref(md), float(dt), N.dptr(T_old), N.dptr(T_lag),
+                                            N.dptr(ld), C.byref(src) if src is not None else None, C.byref(rb),
+                                            dmask.ctypes.data, N.dptr(g), float(rtol), min(20 * n, 2_000_000_000),
+                                            N.dptr(x), C.byref(info)), "step")
+        finally:
+            if timer is not None:
+                timer.__exit__(None, None, None)
+        raise_for(info)
+        if stats is not None:
+            stats.count("picard_iterations")
+        scale = np.linalg.norm(x)
+        inc = np.linalg.norm(x - T_lag) / max(scale, 1e-300)
+        if linear or inc < settings.picard_tol:
+            return state.with_values(x, t_new)
+        if inc >= 0.9 * prev_inc:
+            theta = max(0.25, 0.5 * theta)
+        prev_inc = inc
+        T_lag = np.ascontiguousarray(T_lag + theta * (x - T_lag))
+    raise NonConvergence("Picard iteration", max_iter, inc)
+
+
 def step_backward_euler(state: FieldState, dt: float, mat, source, bounds: BoundarySpec,
                         settings: SolverSettings, latent: bool = False, latent_mask=None,
                         extra_load=None, extra_mass_coeff=None, stats=None) -> FieldState:
-    """One implicit step (``fem.py:307-355``) for a linear problem, on the device."""
+    """One implicit step (``fem.py:307-355``) on the device.  Linear problems with the
+    bottom or interface Dirichlet set take the fused single-kernel solve; temperature-
+    dependent tables, latent heat, convection and radiation take the Picard path
+    (``_step_general``)."""
     from .ops import raise_for, step
     if dt <= 0:
         raise SolverError("time step must be positive")
     if latent_mask is not None or extra_mass_coeff is not None:
         raise UnsupportedOnDevice("latent masks / overlap mass terms are not on the device path")
-    check_linear_problem(mat, bounds, latent)
     if source is not None and not isinstance(source, GaussianSource):
         raise UnsupportedOnDevice("the device evaluates GaussianSource objects, not opaque callables")
+    if _needs_general_path(mat, bounds, latent):
+        return _step_general(state, dt, mat, source, bounds, settings, latent, extra_load, stats)
+    check_linear_problem(mat, bounds, latent)
     mesh = state.mesh
     kind = _dirichlet_kind(mesh, bounds.dirichlet_nodes)
     kappa, rho_c = material_constants(mat)

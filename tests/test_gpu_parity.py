@@ -538,3 +538,28 @@ def test_two_way_coupled_run_vs_reference(name):
         np.testing.assert_array_equal(np.packbits(Tl > TL), z["lmelt"][k])
         if k in z["full_at"]:
             assert rel(Tg, z[f"g{k}"]) <= REL and rel(Tl, z[f"l{k}"]) <= REL
+
+
+@pytest.mark.parametrize("name", ["tables", "latent", "full"])
+def test_picard_step_vs_reference(name):
+    """Temperature-dependent IN625 step on the device (tl_vc_step_host passes under the
+    reference's Picard loop): tables only, + latent secant capacity, + convection and lagged
+    radiation on the top face.  Same Picard pass count, 1e-9 relative L-inf, melt mask."""
+    from .test_oracle_golden import picard_material
+    z = np.load(GOLDEN / f"picard_{name}.npz")
+    grid = P.build_structured_grid(P.Box(tuple(z["lo"]), tuple(z["hi"])), float(z["h"]))
+    mat = picard_material(z)
+    rad = bool(z["radiation"])
+    bounds = P.BoundarySpec(bc=P.ThermalBC(float(z["h_conv"]), 0.8 if rad else 0.0, 293.0, 293.0),
+                            robin_tags=(P.TOP,), radiation=rad,
+                            dirichlet_nodes=grid.nodes_on(P.BOTTOM), dirichlet_values=293.0)
+    beam = P.LaserBeam(200.0, 0.35, 5e-5, 5e-5, 0.8)
+    stats = P.RunStats()
+    out = P.step_backward_euler(P.FieldState(grid, z["T_old"], 0.0), float(z["dt"]), mat,
+                                P.GaussianSource(beam, tuple(z["center"])), bounds,
+                                P.SolverSettings(picard_tol=1e-8, linear_tol=1e-12, linear_solver="cg"),
+                                latent=bool(z["latent"]), stats=stats)
+    assert stats.counters["picard_iterations"] == int(z["picard"])
+    assert rel(out.values, z["sol"]) <= REL
+    TL = mat.T_liquidus
+    np.testing.assert_array_equal(out.values > TL, z["sol"] > TL)
