@@ -254,9 +254,10 @@ def run_spacetime(problem: TwoLevelProblem, schedule: MacroSchedule, local_mesh:
                   batch: int | None = None) -> TwoLevelState:
     """Multirate driver over the whole schedule (``multirate.py:167-191``) on the device.
 
-    One-way problems run device-resident (``DeviceRun``); two-way coupling runs the
-    reference's loop over the step-level device solves (``_run_spacetime_steps``)."""
-    if not problem.one_way:
+    One-way constant-material problems run device-resident (``DeviceRun``); two-way
+    coupling and temperature-dependent physics run the reference's loop over the
+    step-level device solves (``_run_spacetime_steps``)."""
+    if not problem.device_resident:
         return _run_spacetime_steps(problem, schedule, local_mesh, T0, path, policy, stats, recorder)
     extract_interface(local_mesh, problem.global_mesh)
     with DeviceRun(problem, local_mesh) as run:
@@ -273,7 +274,7 @@ def run_space(problem: TwoLevelProblem, dt: float, n_steps: int, local_mesh: Str
               batch: int | None = None) -> TwoLevelState:
     """Uniform-step driver (``multirate.py:194-217``) on the device (two-way coupling: the
     reference's loop over the step-level device solves, ``_run_space_steps``)."""
-    if not problem.one_way:
+    if not problem.device_resident:
         return _run_space_steps(problem, dt, n_steps, local_mesh, T0, path, policy, stats, recorder)
     extract_interface(local_mesh, problem.global_mesh)
     with DeviceRun(problem, local_mesh) as run:
@@ -351,7 +352,7 @@ def _restamp(state: TwoLevelState, t: float) -> TwoLevelState:
 
 def _run_spacetime_steps(problem, schedule, local_mesh, T0, path, policy, stats, recorder):
     """``run_spacetime`` (``multirate.py:167-191``) over the step-level device solves."""
-    problem.check_device_supported()
+    problem.check_device_supported(resident=False)
     state = initial_state(problem, local_mesh, T0)
     if recorder is not None:
         recorder("initial", schedule.t_start, state.local_field, state.global_field, 0)
@@ -369,7 +370,7 @@ def _run_spacetime_steps(problem, schedule, local_mesh, T0, path, policy, stats,
 
 def _run_space_steps(problem, dt, n_steps, local_mesh, T0, path, policy, stats, recorder):
     """``run_space`` (``multirate.py:194-217``) over the step-level device solves."""
-    problem.check_device_supported()
+    problem.check_device_supported(resident=False)
     state = initial_state(problem, local_mesh, T0)
     if recorder is not None:
         recorder("initial", T0.time, state.local_field, state.global_field, 0)

@@ -144,13 +144,21 @@ class TwoLevelProblem:
 
     # -- device support ---------------------------------------------------------
 
-    def check_device_supported(self):
-        check_linear_problem(self.mat_global, None, False)
-        check_linear_problem(self.mat_local, None, True)
-        if self.bc.h_conv > 0:
-            raise UnsupportedOnDevice("Robin convection (h_conv > 0) is not on the device path")
-        if self.bc.emissivity > 0:
-            raise UnsupportedOnDevice("radiation (emissivity > 0) is not on the device path")
+    def check_device_supported(self, resident: bool = True):
+        """``resident``: the device-resident run (``DeviceRun`` / ``tl_run``: constant
+        materials, no latent heat, no top-face Robin terms).  Otherwise the step-level
+        drivers, whose solves take the Picard path for temperature-dependent tables,
+        latent heat, convection and radiation (``fem._step_general``)."""
+        if resident:
+            check_linear_problem(self.mat_global, None, False)
+            check_linear_problem(self.mat_local, None, True)
+            if self.bc.h_conv > 0:
+                raise UnsupportedOnDevice("Robin convection (h_conv > 0) is not on the device-resident path")
+            if self.bc.emissivity > 0:
+                raise UnsupportedOnDevice("radiation (emissivity > 0) is not on the device-resident path")
+        elif not self.one_way and not (self.mat_global.is_constant and self.mat_local.is_constant):
+            raise UnsupportedOnDevice("two-way coupling with temperature-dependent conductivities (a "
+                                      "temperature-dependent transmission jump) is not on the device path")
         if not self.one_way and self.mode != "alternate":
             raise UnsupportedOnDevice("full-mode overlap feedback (coupling mode 'full' with distinct "
                                       "materials) is not on the device path")
@@ -159,6 +167,17 @@ class TwoLevelProblem:
                                       "device path")
         if self.global_mesh.dim != 3:
             raise UnsupportedOnDevice("the device path is 3D only")
+
+    @property
+    def device_resident(self) -> bool:
+        """True when the whole run fits the device-resident one-way loop."""
+        if not self.one_way:
+            return False
+        try:
+            self.check_device_supported(resident=True)
+        except UnsupportedOnDevice:
+            return False
+        return True
 
     def constants(self):
         kg, rcg = material_constants(self.mat_global)
@@ -184,6 +203,8 @@ def transmission_load(local_field, gamma, global_mesh, mat_global, mat_local) ->
     from . import _native as N
     if np.array_equal(mat_global.conductivity_table, mat_local.conductivity_table):
         return np.zeros(global_mesh.n_nodes)
+    if not (mat_global.is_constant and mat_local.is_constant):
+        raise UnsupportedOnDevice("a temperature-dependent transmission jump is not on the device path")
     kg, _ = material_constants(mat_global)
     kl, _ = material_constants(mat_local)
     lmesh = local_field.mesh

@@ -30,6 +30,8 @@ comes from calling the reference's own functions:
 - picard_*.npz   fem.step_backward_euler with temperature-dependent IN625 tables
                  (Picard loop, latent secant capacity, lagged radiation + convection on
                  the top face)  — fem.py:197-268,301-355, materials.py:91-134
+- run_cfg1_tdep.npz two macro steps of cfg1 with a temperature-dependent material,
+                 latent heat, convection and radiation (every solve a Picard loop)
 - schedule_*.json local-box origins per macro step from the reference's
                  LocalDomainPolicy / Mesh.translated / DomainEscape clamp,
                  path.position and swept_pieces         — scanpath.py:68-248
@@ -441,7 +443,9 @@ def picard_cases():
 def main():
     quick = "--quick" in sys.argv
     if "--picard" in sys.argv:
-        return picard_cases()
+        picard_cases()
+        run_case("cfg1_tdep", None, {1, 2}, 7)
+        return
     if "--twoway" in sys.argv:
         transmission_case()
         run_case("cfg1_twoway", None, {1, 2, 3, 4}, 7)
@@ -471,6 +475,7 @@ def main():
     run_case("cfg1_twoway", None, {1, 2, 3, 4}, 7)
     run_case("cfg1_twoway_uniform", None, {1, 4}, 7)
     picard_cases()
+    run_case("cfg1_tdep", None, {1, 2}, 7)
 
 
 if __name__ == "__main__":
