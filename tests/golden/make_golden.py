@@ -32,6 +32,8 @@ comes from calling the reference's own functions:
                  the top face)  — fem.py:197-268,301-355, materials.py:91-134
 - run_cfg1_tdep.npz two macro steps of cfg1 with a temperature-dependent material,
                  latent heat, convection and radiation (every solve a Picard loop)
+- run_track3d.npz the reference's shipped 3D single track (IN625, latent heat,
+                 convection + radiation, direct solver), 3 macro steps, + its tables
 - schedule_*.json local-box origins per macro step from the reference's
                  LocalDomainPolicy / Mesh.translated / DomainEscape clamp,
                  path.position and swept_pieces         — scanpath.py:68-248
@@ -434,6 +436,28 @@ def picard_case(name, latent, radiation, h_conv, seed=5):
     print(f"picard_{name}: picard={stats.counters} cg={CG_ITERS} max={out.values.max():.2f}")
 
 
+def track3d_case():
+    """configs/track3d.cfg (the reference's shipped 3D single track, restated) run by the
+    reference with its own IN625 file; the tables go into the npz for the device test."""
+    import shutil
+    import tempfile
+    global CFG
+    tmp = Path(tempfile.mkdtemp())
+    shutil.copy(CFG / "track3d.cfg", tmp / "track3d.cfg")
+    shutil.copy(REF / "lpbfsim" / "data" / "in625.mat", tmp / "in625.mat")
+    saved, CFG = CFG, tmp
+    try:
+        run_case("track3d", None, {1, 2, 3}, 3)
+    finally:
+        CFG = saved
+    mat = load_config(tmp / "track3d.cfg").material
+    z = dict(np.load(OUT / "run_track3d.npz"))
+    z.update(k_table=mat.conductivity_table, c_table=mat.heat_capacity_table,
+             mat_scalars=np.array([mat.rho, mat.chi, mat.T_solidus, mat.T_liquidus, mat.S]))
+    np.savez_compressed(OUT / "run_track3d.npz", **z)
+    shutil.rmtree(tmp)
+
+
 def picard_cases():
     picard_case("tables", latent=False, radiation=False, h_conv=0.0)
     picard_case("latent", latent=True, radiation=False, h_conv=0.0)
@@ -445,6 +469,7 @@ def main():
     if "--picard" in sys.argv:
         picard_cases()
         run_case("cfg1_tdep", None, {1, 2}, 7)
+        track3d_case()
         return
     if "--twoway" in sys.argv:
         transmission_case()
@@ -476,6 +501,7 @@ def main():
     run_case("cfg1_twoway_uniform", None, {1, 4}, 7)
     picard_cases()
     run_case("cfg1_tdep", None, {1, 2}, 7)
+    track3d_case()
 
 
 if __name__ == "__main__":

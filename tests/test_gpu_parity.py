@@ -565,3 +565,35 @@ def test_picard_step_vs_reference(name):
     assert rel(out.values, z["sol"]) <= REL
     TL = mat.T_liquidus
     np.testing.assert_array_equal(out.values > TL, z["sol"] > TL)
+
+
+def test_track3d_shipped_config_vs_reference(tmp_path):
+    """The reference's shipped 3D single track (configs/track3d.cfg restates it): IN625
+    tables with latent heat, convection + radiation, direct solver, 3 macro steps with
+    relocations, 290 Picard passes.  The IN625 tables come from the golden file."""
+    z = np.load(GOLDEN / "run_track3d.npz")
+    rho, chi, Ts, Tl, S = (float(v) for v in z["mat_scalars"])
+    lines = ["units K", f"rho {rho!r}", f"chi {chi!r}", f"T_solidus {Ts!r}", f"T_liquidus {Tl!r}", f"S {S!r}",
+             "[conductivity]"] + [f"{float(a)!r} {float(b)!r}" for a, b in z["k_table"]] + ["[heat_capacity]"] + \
+            [f"{float(a)!r} {float(b)!r}" for a, b in z["c_table"]]
+    (tmp_path / "in625.mat").write_text("\n".join(lines) + "\n")
+    (tmp_path / "track3d.cfg").write_text((CONFIGS / "track3d.cfg").read_text())
+    cfg = P.load_config(tmp_path / "track3d.cfg")
+    rec = []
+
+    def recorder(kind, t, local, glob, iters):
+        if kind in ("initial", "macro"):
+            rec.append((t, local.values.copy(), glob.values.copy(), local.mesh.box.lo))
+
+    state, stats = P.two_level_run(cfg, recorder=recorder)
+    assert stats.counters == json.loads(str(z["counters"]))
+    TL = cfg.material.T_liquidus
+    s = int(z["stride"])
+    for k, (t, Tl_, Tg, lo) in enumerate(rec):
+        assert t == z["t"][k]
+        np.testing.assert_array_equal(lo, z["box"][k])
+        assert rel(Tg[::s], z["gsub"][k]) <= REL and rel(Tl_[::s], z["lsub"][k]) <= REL
+        np.testing.assert_array_equal(np.packbits(Tg > TL), z["gmelt"][k])
+        np.testing.assert_array_equal(np.packbits(Tl_ > TL), z["lmelt"][k])
+        if k in z["full_at"]:
+            assert rel(Tg, z[f"g{k}"]) <= REL and rel(Tl_, z[f"l{k}"]) <= REL
