@@ -307,8 +307,6 @@ def macro_step(problem, state: TwoLevelState, schedule: MacroSchedule, k: int, s
     """One predictor / micro / corrector cycle (``multirate.py:105-164``); the one-way +
     interval-source corrector re-solves only the last local interval, otherwise the
     corrector is the relaxed two-level fixed point (``two_level_iterate``)."""
-    if not problem.interval_source:
-        raise SolverError("the device path implements the interval-source (distributed) global source only")
     m = schedule.micro_per_macro
     delta = schedule.dt_micro
     t_next = schedule.t_macro(k + 1)
@@ -328,7 +326,7 @@ def macro_step(problem, state: TwoLevelState, schedule: MacroSchedule, k: int, s
         local = FieldState(local.mesh, local.values, t_i)
         if recorder is not None:
             recorder("micro", t_i, local, None, 0)
-    if problem.one_way:
+    if problem.one_way and problem.interval_source:
         corrected = solve_local(problem, before_final, delta, state.gamma, trace_pred, stats=stats)
         corrected = FieldState(corrected.mesh, corrected.values, t_next)
         if stats is not None:

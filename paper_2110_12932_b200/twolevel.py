@@ -115,8 +115,12 @@ class TwoLevelProblem:
         return self.source_global == "distributed"
 
     def global_source(self, t0: float, t1: float, predictor: bool = False):
-        """The swept-track deposit of [t0, t1] as (points, power) or None (``runner.py:75-79``)."""
+        """``_global_source_factory`` (``runner.py:62-81``): "distributed" -> the swept-track
+        deposit of [t0, t1] as (points, power); "gaussian" -> the beam at t1 (a predictor
+        sees it at t0 + 0.75 (t1 - t0)) as a GaussianSource; None when off."""
         from .schedule import swept_samples
+        if self.source_global == "gaussian":
+            return self.local_source(t0 + 0.75 * (t1 - t0) if predictor else t1)
         if self.path is None or self.beam is None:
             return None
         pieces = self.path.swept_pieces(t0, t1)
@@ -162,9 +166,9 @@ class TwoLevelProblem:
         if not self.one_way and self.mode != "alternate":
             raise UnsupportedOnDevice("full-mode overlap feedback (coupling mode 'full' with distinct "
                                       "materials) is not on the device path")
-        if not self.interval_source:
-            raise UnsupportedOnDevice("only the distributed (swept-track) global source is on the "
-                                      "device path")
+        if resident and not self.interval_source:
+            raise UnsupportedOnDevice("the device-resident run uses the distributed (swept-track) "
+                                      "global source; 'gaussian' runs through the step-level drivers")
         if self.global_mesh.dim != 3:
             raise UnsupportedOnDevice("the device path is 3D only")
 
@@ -226,11 +230,14 @@ def solve_global(problem: TwoLevelProblem, state: TwoLevelState, dt: float,
     load = transmission_load(local_for_coupling, state.gamma, problem.global_mesh,
                              problem.mat_global, problem.mat_local)
     dep = problem.global_source(t0, t1, predictor=predictor)
-    if dep is not None:
+    source = None
+    if isinstance(dep, GaussianSource):
+        source = dep
+    elif dep is not None:
         load = load + deposit_load(problem.global_mesh, dep[0], dep[1])
     timer = stats.timer("global_solve") if stats is not None else _Null()
     with timer:
-        out = step_backward_euler(state.global_field, dt, problem.mat_global, None,
+        out = step_backward_euler(state.global_field, dt, problem.mat_global, source,
                                   problem.global_bounds(), problem.solver, latent=False,
                                   extra_load=load, stats=stats)
     if stats is not None:

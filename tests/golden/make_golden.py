@@ -34,6 +34,8 @@ comes from calling the reference's own functions:
                  latent heat, convection and radiation (every solve a Picard loop)
 - run_track3d.npz the reference's shipped 3D single track (IN625, latent heat,
                  convection + radiation, direct solver), 3 macro steps, + its tables
+- run_cfg1_gsrc(_uniform).npz  source_global gaussian (runner.py:64-71): the coarse
+                 level sees the beam itself, the corrector is a coupled re-solve
 - schedule_*.json local-box origins per macro step from the reference's
                  LocalDomainPolicy / Mesh.translated / DomainEscape clamp,
                  path.position and swept_pieces         — scanpath.py:68-248
@@ -471,6 +473,10 @@ def main():
         run_case("cfg1_tdep", None, {1, 2}, 7)
         track3d_case()
         return
+    if "--gsrc" in sys.argv:
+        run_case("cfg1_gsrc", None, {1, 2, 3, 4}, 7)
+        run_case("cfg1_gsrc_uniform", None, {1, 4}, 7)
+        return
     if "--twoway" in sys.argv:
         transmission_case()
         run_case("cfg1_twoway", None, {1, 2, 3, 4}, 7)
@@ -502,6 +508,8 @@ def main():
     picard_cases()
     run_case("cfg1_tdep", None, {1, 2}, 7)
     track3d_case()
+    run_case("cfg1_gsrc", None, {1, 2, 3, 4}, 7)
+    run_case("cfg1_gsrc_uniform", None, {1, 4}, 7)
 
 
 if __name__ == "__main__":

@@ -520,14 +520,17 @@ def test_transmission_load_vs_reference():
     np.testing.assert_array_equal(again, got)
 
 
-@pytest.mark.parametrize("name", ["cfg1_twoway", "cfg1_twoway_uniform", "cfg1_tdep"])
+@pytest.mark.parametrize("name", ["cfg1_twoway", "cfg1_twoway_uniform", "cfg1_tdep", "cfg1_gsrc",
+                                  "cfg1_gsrc_uniform"])
 def test_two_way_coupled_run_vs_reference(name):
     """Two-way coupling (global_kappa_scale 1.5, omega 0.7, tol 1e-8): 4 macro steps whose
     correctors are the relaxed two_level_iterate fixed point, with relocations; counters
     (coupling iterations included), times, boxes, fields and melt masks as the reference's.
     The uniform variant (run_space) iterates every step to the fixed point.  cfg1_tdep: a
     temperature-dependent material with latent heat, convection and radiation (one-way,
-    every solve a Picard loop over tl_vc_step_host passes, 194 passes in 2 macro steps)."""
+    every solve a Picard loop over tl_vc_step_host passes, 194 passes in 2 macro steps).
+    cfg1_gsrc(_uniform): the "gaussian" coarse source (runner.py:64-71; predictor beam at
+    t0 + 0.75 dt), whose corrector re-solves both levels (multirate.py:156-161)."""
     z, cfg, rec, stats = _golden_run(name)
     assert stats.counters == json.loads(str(z["counters"]))
     TL = cfg.material.T_liquidus
