@@ -36,6 +36,8 @@ comes from calling the reference's own functions:
                  convection + radiation, direct solver), 3 macro steps, + its tables
 - run_cfg1_gsrc(_uniform).npz  source_global gaussian (runner.py:64-71): the coarse
                  level sees the beam itself, the corrector is a coupled re-solve
+- experiments.json runner.run_experiment in compare and convergence-study modes:
+                 output files, summaries, study matrix, errors.csv rows
 - schedule_*.json local-box origins per macro step from the reference's
                  LocalDomainPolicy / Mesh.translated / DomainEscape clamp,
                  path.position and swept_pieces         — scanpath.py:68-248
@@ -460,6 +462,31 @@ def track3d_case():
     shutil.rmtree(tmp)
 
 
+def experiments_case():
+    """runner.run_experiment in compare and convergence-study modes (cfg1 variants): the
+    summaries, the study matrix and every run's errors.csv."""
+    import csv as _csv
+    import shutil
+    import tempfile
+    out = {}
+    for name in ("cfg1_compare", "cfg1_study"):
+        tmp = Path(tempfile.mkdtemp())
+        art = runner.run_experiment(load_config(CFG / f"{name}.cfg"), tmp)
+        files = sorted(str(p.relative_to(tmp)) for p in tmp.rglob("*") if p.is_file())
+        errs = {}
+        for f in files:
+            if f.endswith("errors.csv") or f.endswith("study_matrix.csv"):
+                with (tmp / f).open() as fh:
+                    errs[f] = list(_csv.reader(fh))
+        summ = {k: v for k, v in art.summary.items()
+                if not k.startswith("seconds") and "wall" not in k and k not in ("total_seconds", "speedup")}
+        out[name] = {"files": files, "csv": errs, "summary": summ}
+        shutil.rmtree(tmp)
+    out["versions"] = VERS
+    (OUT / "experiments.json").write_text(json.dumps(out, indent=1))
+    print("experiments:", {k: v["summary"] for k, v in out.items() if k != "versions"})
+
+
 def picard_cases():
     picard_case("tables", latent=False, radiation=False, h_conv=0.0)
     picard_case("latent", latent=True, radiation=False, h_conv=0.0)
@@ -473,6 +500,8 @@ def main():
         run_case("cfg1_tdep", None, {1, 2}, 7)
         track3d_case()
         return
+    if "--experiments" in sys.argv:
+        return experiments_case()
     if "--gsrc" in sys.argv:
         run_case("cfg1_gsrc", None, {1, 2, 3, 4}, 7)
         run_case("cfg1_gsrc_uniform", None, {1, 4}, 7)
@@ -510,6 +539,7 @@ def main():
     track3d_case()
     run_case("cfg1_gsrc", None, {1, 2, 3, 4}, 7)
     run_case("cfg1_gsrc_uniform", None, {1, 4}, 7)
+    experiments_case()
 
 
 if __name__ == "__main__":

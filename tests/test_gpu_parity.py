@@ -600,3 +600,36 @@ def test_track3d_shipped_config_vs_reference(tmp_path):
         np.testing.assert_array_equal(np.packbits(Tl_ > TL), z["lmelt"][k])
         if k in z["full_at"]:
             assert rel(Tg, z[f"g{k}"]) <= REL and rel(Tl_, z[f"l{k}"]) <= REL
+
+
+@pytest.mark.parametrize("name", ["cfg1_compare", "cfg1_study"])
+def test_experiment_modes_vs_reference(name, tmp_path):
+    """runner.run_experiment (runner.py:270-440) in compare and convergence-study modes on the
+    device: the same output files, solve counts, study pairs and errors.csv / study_matrix
+    rows (relative L2 errors to 1e-7) as the reference."""
+    import csv
+    from paper_2110_12932_b200.experiment import run_experiment
+    gold = json.loads((GOLDEN / "experiments.json").read_text())[name]
+    art = run_experiment(P.load_config(CONFIGS / f"{name}.cfg"), tmp_path)
+    files = sorted(str(p.relative_to(tmp_path)) for p in tmp_path.rglob("*") if p.is_file())
+    assert files == gold["files"]
+    for k, v in gold["summary"].items():
+        if k == "mean_rel_l2":
+            for kk, vv in v.items():
+                assert abs(art.summary[k][kk] - vv) <= 1e-7 * vv
+        elif k == "pairs":
+            np.testing.assert_allclose(art.summary[k], v, rtol=1e-15)
+        else:
+            assert art.summary[k] == v, k
+    for f, rows in gold["csv"].items():
+        with (tmp_path / f).open() as fh:
+            got = list(csv.reader(fh))
+        assert got[0] == rows[0] and len(got) == len(rows)
+        for a, b in zip(got[1:], rows[1:]):
+            for x, y in zip(a, b):
+                try:
+                    fx, fy = float(x), float(y)
+                except ValueError:
+                    assert x == y
+                    continue
+                assert abs(fx - fy) <= 1e-7 * abs(fy) + 1e-12, (f, a, b)
