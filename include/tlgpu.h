@@ -185,6 +185,11 @@ int32_t tl_vc_step_host(const tl_grid_desc* grid, const tl_vc_material* mat, dou
  *      Deterministic scatter (stable sort by node + ordered sums). */
 int32_t tl_transmission_host(const tl_grid_desc* global_grid, const tl_grid_desc* local_grid,
                              const double* local_values, double jump, double* load_out);
+/* Same with temperature-dependent conductivities: jump = kappa_g(T_qp) - kappa_l(T_qp),
+ * T_qp the local P1 value at the quadrature point (twolevel.py:174-175). */
+int32_t tl_transmission_tables_host(const tl_grid_desc* global_grid, const tl_grid_desc* local_grid,
+                                    const double* local_values, const double* kg_T, const double* kg_v, int32_t nkg,
+                                    const double* kl_T, const double* kl_v, int32_t nkl, double* load_out);
 
 /* ---- discrete L2 norms with the P1 mass matrix (fem.mass_matrix / l2_norm,
  *      fem.py:434-446): out[0] = (a-b)^T M (a-b) (a^T M a when b == NULL),

@@ -110,6 +110,8 @@ SIGNATURES = [
     ("tl_deposit_host", C.c_int32, [C.POINTER(GridDesc), _dp, _dp, C.c_int32, _dp]),
     ("tl_mass_norms_host", C.c_int32, [C.POINTER(GridDesc), _dp, _dp, _dp]),
     ("tl_transmission_host", C.c_int32, [C.POINTER(GridDesc), C.POINTER(GridDesc), _dp, C.c_double, _dp]),
+    ("tl_transmission_tables_host", C.c_int32, [C.POINTER(GridDesc), C.POINTER(GridDesc), _dp, _dp, _dp, C.c_int32,
+                                                _dp, _dp, C.c_int32, _dp]),
     ("tl_vc_step_host", C.c_int32, [C.POINTER(GridDesc), C.POINTER(VcMaterial), C.c_double, _dp, _dp, _dp,
                                     C.POINTER(Gaussian), C.POINTER(Robin), C.c_void_p, _dp, C.c_double,
                                     C.c_int32, _dp, C.POINTER(SolveInfo)]),

@@ -877,8 +877,26 @@ int32_t tl_vc_step_host(const tl_grid_desc* grid, const tl_vc_material* mat, dou
     return TL_OK;
 }
 
+static int transmission_impl(const tl_grid_desc* global_grid, const tl_grid_desc* local_grid,
+                             const double* local_values, double jump, const double* kg_T, const double* kg_v,
+                             int32_t nkg, const double* kl_T, const double* kl_v, int32_t nkl, double* load_out);
+
 int32_t tl_transmission_host(const tl_grid_desc* global_grid, const tl_grid_desc* local_grid,
                              const double* local_values, double jump, double* load_out) {
+    return transmission_impl(global_grid, local_grid, local_values, jump, nullptr, nullptr, 0, nullptr, nullptr, 0,
+                             load_out);
+}
+
+int32_t tl_transmission_tables_host(const tl_grid_desc* global_grid, const tl_grid_desc* local_grid,
+                                    const double* local_values, const double* kg_T, const double* kg_v, int32_t nkg,
+                                    const double* kl_T, const double* kl_v, int32_t nkl, double* load_out) {
+    if (!kg_T || !kg_v || !kl_T || !kl_v || nkg < 2 || nkl < 2) return fail(TL_E_INVALID, "bad conductivity tables");
+    return transmission_impl(global_grid, local_grid, local_values, 0.0, kg_T, kg_v, nkg, kl_T, kl_v, nkl, load_out);
+}
+
+static int transmission_impl(const tl_grid_desc* global_grid, const tl_grid_desc* local_grid,
+                             const double* local_values, double jump, const double* kg_T, const double* kg_v,
+                             int32_t nkg, const double* kl_T, const double* kl_v, int32_t nkl, double* load_out) {
     if (!global_grid || !local_grid || !local_values || !load_out) return fail(TL_E_INVALID, "null argument");
     tl::Grid G{}, L{};
     if (int rc = make_grid(*global_grid, tl::kBottom, G)) return rc;
@@ -895,7 +913,18 @@ int32_t tl_transmission_host(const tl_grid_desc* global_grid, const tl_grid_desc
         return rc;
     TL_CUDA(cudaMemcpy(dT, local_values, sizeof(double) * L.n, cudaMemcpyHostToDevice));
     TL_CUDA(cudaMemset(dload, 0, sizeof(double) * G.n));
-    tl::k_trans_entries<<<296, 256>>>(G, L, dT, jump, (int)nf, keys, idx, dvals);
+    double* dtab = nullptr;
+    tl::KTab kg{nullptr, nullptr, 0}, kl{nullptr, nullptr, 0};
+    if (nkg > 0) {
+        if ((rc = dalloc(&dtab, 2 * (nkg + nkl)))) return rc;
+        TL_CUDA(cudaMemcpy(dtab, kg_T, sizeof(double) * nkg, cudaMemcpyHostToDevice));
+        TL_CUDA(cudaMemcpy(dtab + nkg, kg_v, sizeof(double) * nkg, cudaMemcpyHostToDevice));
+        TL_CUDA(cudaMemcpy(dtab + 2 * nkg, kl_T, sizeof(double) * nkl, cudaMemcpyHostToDevice));
+        TL_CUDA(cudaMemcpy(dtab + 2 * nkg + nkl, kl_v, sizeof(double) * nkl, cudaMemcpyHostToDevice));
+        kg = tl::KTab{dtab, dtab + nkg, nkg};
+        kl = tl::KTab{dtab + 2 * nkg, dtab + 2 * nkg + nkl, nkl};
+    }
+    tl::k_trans_entries<<<296, 256>>>(G, L, dT, jump, kg, kl, (int)nf, keys, idx, dvals);
     TL_CUDA(cudaGetLastError());
     int bits = 1;
     while ((1ll << bits) < G.n) ++bits;
@@ -909,6 +938,7 @@ int32_t tl_transmission_host(const tl_grid_desc* global_grid, const tl_grid_desc
     TL_CUDA(cudaMemcpy(load_out, dload, sizeof(double) * G.n, cudaMemcpyDeviceToHost));
     cudaFree(tmp); cudaFree(dT); cudaFree(dvals); cudaFree(dload);
     cudaFree(keys); cudaFree(keys2); cudaFree(idx); cudaFree(idx2);
+    if (dtab) cudaFree(dtab);
     return TL_OK;
 }
 

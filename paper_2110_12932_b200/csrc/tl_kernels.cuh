@@ -713,8 +713,30 @@ __device__ __forceinline__ void p1_locate(const Grid& G, double x, double y, dou
 // (c,b,a), facet (v0,v1,v2), dT/dn = -(T(v3) - T(v2)) / h_a.  High side: tets stepping a
 // first, perm (a,b,c) / (a,c,b), facet (v1,v2,v3), dT/dn = (T(v1) - T(v0)) / h_a.
 // Entry e = 3 f + q writes 4 (global node, density * barycentric) pairs at 4 e + r.
-__global__ void k_trans_entries(Grid G, Grid L, const double* __restrict__ T, double jump, int nfacet,
-                                int* __restrict__ keys, int* __restrict__ idx, double* __restrict__ vals) {
+// np.interp over a (T, value) table: clamped outside, linear inside (materials.py:91-100)
+struct KTab {
+    const double* T;
+    const double* v;
+    int n;            // 0: no table
+};
+
+__device__ __forceinline__ double tab_interp(double x, const double* xp, const double* fp, int n) {
+    if (!(x > xp[0])) return fp[0];
+    if (!(x < xp[n - 1])) return fp[n - 1];
+    int lo = 0, hi = n - 1;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (xp[mid] <= x) lo = mid; else hi = mid;
+    }
+    const double slope = (fp[lo + 1] - fp[lo]) / (xp[lo + 1] - xp[lo]);
+    return slope * (x - xp[lo]) + fp[lo];
+}
+
+// jump = kappa_global(T_qp) - kappa_local(T_qp) when both tables are given (T_qp: the
+// local P1 value at the quadrature point, the edge midpoint average), else the constant.
+__global__ void k_trans_entries(Grid G, Grid L, const double* __restrict__ T, double jump, KTab kg, KTab kl,
+                                int nfacet, int* __restrict__ keys, int* __restrict__ idx,
+                                double* __restrict__ vals) {
     const int faceA[5] = {0, 0, 1, 1, 2}, faceS[5] = {0, 1, 0, 1, 0};
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < 3 * nfacet; e += gridDim.x * blockDim.x) {
         int f = e / 3;
@@ -763,7 +785,12 @@ __global__ void k_trans_entries(Grid G, Grid L, const double* __restrict__ T, do
         double x[3];
 #pragma unroll
         for (int d = 0; d < 3; ++d) x[d] = 0.5 * (node_coord(L, d, A[d]) + node_coord(L, d, B[d]));
-        const double dens = 0.5 * L.h[b] * L.h[c] / 3.0 * jump * dTdn;
+        double jq = jump;
+        if (kg.n > 0) {
+            const double tq = 0.5 * (T[nid(A)] + T[nid(B)]);
+            jq = tab_interp(tq, kg.T, kg.v, kg.n) - tab_interp(tq, kl.T, kl.v, kl.n);
+        }
+        const double dens = 0.5 * L.h[b] * L.h[c] / 3.0 * jq * dTdn;
         int nd[4];
         double w[4];
         p1_locate(G, x[0], x[1], x[2], nd, w);

@@ -32,17 +32,8 @@ struct VcRobin {
     int on;
 };
 
-// np.interp: clamped outside the table, linear inside
 __device__ __forceinline__ double vc_interp(double x, const double* xp, const double* fp, int n) {
-    if (!(x > xp[0])) return fp[0];
-    if (!(x < xp[n - 1])) return fp[n - 1];
-    int lo = 0, hi = n - 1;
-    while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (xp[mid] <= x) lo = mid; else hi = mid;
-    }
-    const double slope = (fp[lo + 1] - fp[lo]) / (xp[lo + 1] - xp[lo]);
-    return slope * (x - xp[lo]) + fp[lo];
+    return tab_interp(x, xp, fp, n);
 }
 
 __device__ __forceinline__ double vc_phase(const VcMat& M, double T) {

@@ -160,9 +160,6 @@ class TwoLevelProblem:
                 raise UnsupportedOnDevice("Robin convection (h_conv > 0) is not on the device-resident path")
             if self.bc.emissivity > 0:
                 raise UnsupportedOnDevice("radiation (emissivity > 0) is not on the device-resident path")
-        elif not self.one_way and not (self.mat_global.is_constant and self.mat_local.is_constant):
-            raise UnsupportedOnDevice("two-way coupling with temperature-dependent conductivities (a "
-                                      "temperature-dependent transmission jump) is not on the device path")
         if not self.one_way and self.mode != "alternate":
             raise UnsupportedOnDevice("full-mode overlap feedback (coupling mode 'full' with distinct "
                                       "materials) is not on the device path")
@@ -207,18 +204,25 @@ def transmission_load(local_field, gamma, global_mesh, mat_global, mat_local) ->
     from . import _native as N
     if np.array_equal(mat_global.conductivity_table, mat_local.conductivity_table):
         return np.zeros(global_mesh.n_nodes)
-    if not (mat_global.is_constant and mat_local.is_constant):
-        raise UnsupportedOnDevice("a temperature-dependent transmission jump is not on the device path")
-    kg, _ = material_constants(mat_global)
-    kl, _ = material_constants(mat_local)
     lmesh = local_field.mesh
     T = np.ascontiguousarray(local_field.values, dtype=np.float64)
     if T.shape != (lmesh.n_nodes,):
         raise CouplingError("local field does not match its mesh")
     out = np.zeros(global_mesh.n_nodes)
     gd, ld = global_mesh.desc(), lmesh.desc()
-    N.check(N.lib().tl_transmission_host(N.C.byref(gd), N.C.byref(ld), N.dptr(T), float(kg - kl),
-                                         N.dptr(out)), "transmission_load")
+    if mat_global.is_constant and mat_local.is_constant:
+        kg, _ = material_constants(mat_global)
+        kl, _ = material_constants(mat_local)
+        N.check(N.lib().tl_transmission_host(N.C.byref(gd), N.C.byref(ld), N.dptr(T), float(kg - kl),
+                                             N.dptr(out)), "transmission_load")
+        return out
+    tg = np.ascontiguousarray(mat_global.conductivity_table, dtype=np.float64)
+    tl_ = np.ascontiguousarray(mat_local.conductivity_table, dtype=np.float64)
+    cols = [np.ascontiguousarray(tg[:, 0]), np.ascontiguousarray(tg[:, 1]),
+            np.ascontiguousarray(tl_[:, 0]), np.ascontiguousarray(tl_[:, 1])]
+    N.check(N.lib().tl_transmission_tables_host(N.C.byref(gd), N.C.byref(ld), N.dptr(T), N.dptr(cols[0]),
+                                                N.dptr(cols[1]), len(tg), N.dptr(cols[2]), N.dptr(cols[3]),
+                                                len(tl_), N.dptr(out)), "transmission_load")
     return out
 
 

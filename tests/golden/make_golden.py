@@ -38,6 +38,8 @@ comes from calling the reference's own functions:
                  level sees the beam itself, the corrector is a coupled re-solve
 - experiments.json runner.run_experiment in compare and convergence-study modes:
                  output files, summaries, study matrix, errors.csv rows
+- transmission_tdep.npz / run_cfg1_tdep_twoway.npz  two-way coupling with temperature-
+                 dependent conductivity tables (jump evaluated at T_qp)
 - schedule_*.json local-box origins per macro step from the reference's
                  LocalDomainPolicy / Mesh.translated / DomainEscape clamp,
                  path.position and swept_pieces         — scanpath.py:68-248
@@ -493,8 +495,26 @@ def picard_cases():
     picard_case("full", latent=True, radiation=True, h_conv=10.0)
 
 
+def transmission_tdep_case():
+    """transmission_load with temperature-dependent tables (cfg1_tdep_twoway): the jump is
+    kappa_g(T_qp) - kappa_l(T_qp)."""
+    cfg = load_config(CFG / "cfg1_tdep_twoway.cfg")
+    problem, lm = runner.build_problem(cfg)
+    rng = np.random.default_rng(13)
+    gamma = lmesh.extract_interface(lm, problem.global_mesh)
+    v = rng.uniform(293.0, 2293.0, lm.n_nodes)
+    load = twolevel.transmission_load(fem.FieldState(lm, v, 0.0), gamma, problem.global_mesh,
+                                      problem.mat_global, problem.mat_local)
+    np.savez_compressed(OUT / "transmission_tdep.npz", v=v, load=load, versions=json.dumps(VERS))
+    print(f"transmission_tdep: nnz={np.count_nonzero(load)} sum={load.sum():.6e}")
+
+
 def main():
     quick = "--quick" in sys.argv
+    if "--tdep-twoway" in sys.argv:
+        transmission_tdep_case()
+        run_case("cfg1_tdep_twoway", None, {1}, 7)
+        return
     if "--picard" in sys.argv:
         picard_cases()
         run_case("cfg1_tdep", None, {1, 2}, 7)
@@ -540,6 +560,8 @@ def main():
     run_case("cfg1_gsrc", None, {1, 2, 3, 4}, 7)
     run_case("cfg1_gsrc_uniform", None, {1, 4}, 7)
     experiments_case()
+    transmission_tdep_case()
+    run_case("cfg1_tdep_twoway", None, {1}, 7)
 
 
 if __name__ == "__main__":

@@ -514,6 +514,13 @@ def test_transmission_load_vs_reference():
                                 problem.mat_global, problem.mat_local)
         ref = z[f"load{k}"]
         assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
+    # temperature-dependent tables: jump = kappa_g(T_qp) - kappa_l(T_qp)
+    zt = np.load(GOLDEN / "transmission_tdep.npz")
+    cfg_t = P.load_config(CONFIGS / "cfg1_tdep_twoway.cfg")
+    pt, lt = P.build_problem(cfg_t)
+    gt = extract_interface(lt, pt.global_mesh)
+    got_t = transmission_load(P.FieldState(lt, zt["v"], 0.0), gt, pt.global_mesh, pt.mat_global, pt.mat_local)
+    assert np.abs(got_t - zt["load"]).max() <= 1e-12 * np.abs(zt["load"]).max()
     # run-to-run deterministic
     again = transmission_load(P.FieldState(mesh, z["v1"], 0.0), gamma, problem.global_mesh,
                               problem.mat_global, problem.mat_local)
@@ -521,7 +528,7 @@ def test_transmission_load_vs_reference():
 
 
 @pytest.mark.parametrize("name", ["cfg1_twoway", "cfg1_twoway_uniform", "cfg1_tdep", "cfg1_gsrc",
-                                  "cfg1_gsrc_uniform"])
+                                  "cfg1_gsrc_uniform", "cfg1_tdep_twoway"])
 def test_two_way_coupled_run_vs_reference(name):
     """Two-way coupling (global_kappa_scale 1.5, omega 0.7, tol 1e-8): 4 macro steps whose
     correctors are the relaxed two_level_iterate fixed point, with relocations; counters
