@@ -178,6 +178,15 @@ int32_t tl_vc_step_host(const tl_grid_desc* grid, const tl_vc_material* mat, dou
                         const uint8_t* dirichlet_mask, const double* g, double rtol, int32_t maxiter, double* x_out,
                         tl_solve_info* info);
 
+/* ---- full-mode overlap feedback (twolevel.py:186-239) as a dense global load: the
+ *      capacity-difference, conductivity-gradient and source-scaling terms of the local
+ *      field over the global quadrature points inside the local box.  src: the global
+ *      Gaussian at t1 (or NULL / on = 0). */
+int32_t tl_overlap_feedback_host(const tl_grid_desc* global_grid, const tl_grid_desc* local_grid,
+                                 const double* local_new, const double* local_old, double dt,
+                                 const tl_vc_material* mat_global, const tl_vc_material* mat_local,
+                                 const tl_gaussian* src, double* load_out);
+
 /* ---- transmission_load (twolevel.py:159-183) for constant conductivities:
  *      load_out (dense, global nodes) = sum over the local grid's interface facets
  *      (LATERAL + BOTTOM, mesh.py:477-523) of jump * dT_local/dn * w_global at 3

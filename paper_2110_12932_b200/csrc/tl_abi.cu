@@ -881,6 +881,48 @@ static int transmission_impl(const tl_grid_desc* global_grid, const tl_grid_desc
                              const double* local_values, double jump, const double* kg_T, const double* kg_v,
                              int32_t nkg, const double* kl_T, const double* kl_v, int32_t nkl, double* load_out);
 
+int32_t tl_overlap_feedback_host(const tl_grid_desc* global_grid, const tl_grid_desc* local_grid,
+                                 const double* local_new, const double* local_old, double dt,
+                                 const tl_vc_material* mat_global, const tl_vc_material* mat_local,
+                                 const tl_gaussian* src, double* load_out) {
+    if (!global_grid || !local_grid || !local_new || !local_old || !mat_global || !mat_local || !load_out)
+        return fail(TL_E_INVALID, "null argument");
+    if (!(dt > 0.0)) return fail(TL_E_INVALID, "time step must be positive");
+    tl::Grid G{}, L{};
+    if (int rc = make_grid(*global_grid, tl::kBottom, G)) return rc;
+    if (int rc = make_grid(*local_grid, tl::kGamma, L)) return rc;
+    double *dn, *dold, *dload, *tabs;
+    const int ng = 2 * (mat_global->nk + mat_global->nc), nl = 2 * (mat_local->nk + mat_local->nc);
+    int rc = 0;
+    if ((rc = dalloc(&dn, L.n)) || (rc = dalloc(&dold, L.n)) || (rc = dalloc(&dload, G.n)) ||
+        (rc = dalloc(&tabs, ng + nl)))
+        return rc;
+    TL_CUDA(cudaMemcpy(dn, local_new, sizeof(double) * L.n, cudaMemcpyHostToDevice));
+    TL_CUDA(cudaMemcpy(dold, local_old, sizeof(double) * L.n, cudaMemcpyHostToDevice));
+    auto upload = [&](const tl_vc_material* m, double* at, tl::VcMat& M) -> int {
+        TL_CUDA(cudaMemcpy(at, m->k_T, sizeof(double) * m->nk, cudaMemcpyHostToDevice));
+        TL_CUDA(cudaMemcpy(at + m->nk, m->k_v, sizeof(double) * m->nk, cudaMemcpyHostToDevice));
+        TL_CUDA(cudaMemcpy(at + 2 * m->nk, m->c_T, sizeof(double) * m->nc, cudaMemcpyHostToDevice));
+        TL_CUDA(cudaMemcpy(at + 2 * m->nk + m->nc, m->c_v, sizeof(double) * m->nc, cudaMemcpyHostToDevice));
+        M = tl::VcMat{at, at + m->nk, at + 2 * m->nk, at + 2 * m->nk + m->nc, m->nk, m->nc,
+                      m->rho, m->chi, m->S, m->T_melt, m->latent};
+        return TL_OK;
+    };
+    tl::VcMat Mg{}, Ml{};
+    if ((rc = upload(mat_global, tabs, Mg)) || (rc = upload(mat_local, tabs + ng, Ml))) return rc;
+    tl::Gauss S{};
+    if (src && src->on) {
+        S.peak = src->peak; S.radius = src->radius; S.depth = src->depth;
+        for (int a = 0; a < 3; ++a) S.center[a] = src->center[a];
+        S.on = 1;
+    }
+    tl::k_overlap_feedback<<<296, 256>>>(G, L, dn, dold, dt, Mg, Ml, S, dload);
+    TL_CUDA(cudaGetLastError());
+    TL_CUDA(cudaMemcpy(load_out, dload, sizeof(double) * G.n, cudaMemcpyDeviceToHost));
+    cudaFree(dn); cudaFree(dold); cudaFree(dload); cudaFree(tabs);
+    return TL_OK;
+}
+
 int32_t tl_transmission_host(const tl_grid_desc* global_grid, const tl_grid_desc* local_grid,
                              const double* local_values, double jump, double* load_out) {
     return transmission_impl(global_grid, local_grid, local_values, jump, nullptr, nullptr, 0, nullptr, nullptr, 0,

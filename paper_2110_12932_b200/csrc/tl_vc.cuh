@@ -292,4 +292,114 @@ __global__ void k_vc_fix(int n, const unsigned char* __restrict__ dm, const doub
         if (dm[p]) x[p] = gv[p];
 }
 
+// ---------------------------------------------------------------------------------
+// Full-mode overlap feedback (twolevel.py:186-239), gathered per global node: over the 24
+// global tets touching the node and their 4 quadrature points x_q (mesh.py:116-128) that
+// lie in the local box (Box.contains, closed), the local field is located (Kuhn-P1,
+// p1_locate on the local lattice) and
+//   density = -(c_eff_l rho_l k_g/k_l - c_g rho_g) dT/dt
+//             + ((k_g/k_l) dk_l/dT - dk_g/dT) |grad T|^2  [+ (k_g/k_l - 1) Q(x_q)]
+// with c_eff = c + chi f'(T) (materials.effective_capacity) and dk/dT the table segment
+// slope (zero outside the table), scattered as w_q vol density phi_i(x_q).
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ double vc_dkdT(double T, const double* xp, const double* fp, int n) {
+    if (T <= xp[0] || T >= xp[n - 1]) return 0.0;
+    int lo = 0, hi = n - 1;                 // searchsorted(right) - 1
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (xp[mid] <= T) lo = mid; else hi = mid;
+    }
+    return (fp[lo + 1] - fp[lo]) / (xp[lo + 1] - xp[lo]);
+}
+
+__global__ void k_overlap_feedback(Grid G, Grid L, const double* __restrict__ Tn, const double* __restrict__ To,
+                                   double dt, VcMat Mg, VcMat Ml, Gauss src, double* __restrict__ load) {
+    const double A = TL_QA, B = TL_QB;
+    const double vol = G.h[0] * G.h[1] * G.h[2] / 6.0;
+    const int perms[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+    double llo[3], lhi[3];
+    for (int a = 0; a < 3; ++a) {
+        llo[a] = node_coord(L, a, 0);
+        lhi[a] = node_coord(L, a, L.nc[a]);
+    }
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < G.n; p += gridDim.x * blockDim.x) {
+        int idx[3];
+        decode(G, p, idx[0], idx[1], idx[2]);
+        double acc = 0.0;
+        for (int o = 0; o < 8; ++o) {
+            const int oo[3] = {o & 1, (o >> 1) & 1, (o >> 2) & 1};
+            int cell[3];
+            bool ok = true;
+            for (int a = 0; a < 3; ++a) {
+                cell[a] = idx[a] - oo[a];
+                ok = ok && cell[a] >= 0 && cell[a] < G.nc[a];
+            }
+            if (!ok) continue;
+            for (int t = 0; t < 6; ++t) {
+                int off[4][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+                int r = -1;
+                for (int v = 0; v < 4; ++v) {
+                    if (v > 0) {
+                        for (int a = 0; a < 3; ++a) off[v][a] = off[v - 1][a];
+                        off[v][perms[t][v - 1]] += 1;
+                    }
+                    if (off[v][0] == oo[0] && off[v][1] == oo[1] && off[v][2] == oo[2]) r = v;
+                }
+                if (r < 0) continue;
+                for (int q = 0; q < 4; ++q) {
+                    double x[3];
+                    bool in = true;
+                    for (int a = 0; a < 3; ++a) {
+                        double sx = 0.0;
+                        for (int v = 0; v < 4; ++v) sx += ((v == q) ? A : B) * node_coord(G, a, cell[a] + off[v][a]);
+                        x[a] = sx;
+                        in = in && x[a] >= llo[a] && x[a] <= lhi[a];
+                    }
+                    if (!in) continue;
+                    // locate in the local lattice: cell, descending fractional order, barycentrics
+                    int c[3];
+                    double xi[3];
+                    for (int a = 0; a < 3; ++a) {
+                        int ci = (int)floor((x[a] - (L.lo0[a] + L.off[a])) / L.h[a]);
+                        ci = ci < 0 ? 0 : (ci > L.nc[a] - 1 ? L.nc[a] - 1 : ci);
+                        c[a] = ci;
+                        xi[a] = (x[a] - node_coord(L, a, ci)) / L.h[a];
+                    }
+                    int o0 = 0, o1 = 1, o2 = 2;
+                    if (xi[o1] > xi[o0]) { int tt = o0; o0 = o1; o1 = tt; }
+                    if (xi[o2] > xi[o1]) { int tt = o1; o1 = o2; o2 = tt; }
+                    if (xi[o1] > xi[o0]) { int tt = o0; o0 = o1; o1 = tt; }
+                    const int st[3] = {1, L.NX, L.NX * L.NY};
+                    const int n0 = c[0] + L.NX * (c[1] + L.NY * c[2]);
+                    const int n1 = n0 + st[o0], n2 = n1 + st[o1], n3 = n2 + st[o2];
+                    const double w0 = 1.0 - xi[o0], w1 = xi[o0] - xi[o1], w2 = xi[o1] - xi[o2], w3 = xi[o2];
+                    const double Tq = w0 * Tn[n0] + w1 * Tn[n1] + w2 * Tn[n2] + w3 * Tn[n3];
+                    const double Tqo = w0 * To[n0] + w1 * To[n1] + w2 * To[n2] + w3 * To[n3];
+                    double gr[3];
+                    gr[o0] = (Tn[n1] - Tn[n0]) / L.h[o0];
+                    gr[o1] = (Tn[n2] - Tn[n1]) / L.h[o1];
+                    gr[o2] = (Tn[n3] - Tn[n2]) / L.h[o2];
+                    const double gsq = gr[0] * gr[0] + gr[1] * gr[1] + gr[2] * gr[2];
+                    const double kg = tab_interp(Tq, Mg.kT, Mg.kv, Mg.nk);
+                    const double kl = tab_interp(Tq, Ml.kT, Ml.kv, Ml.nk);
+                    const double ratio = kg / kl;
+                    const double ceff = tab_interp(Tq, Ml.cT, Ml.cv, Ml.nc) + Ml.chi * vc_phase_deriv(Ml, Tq);
+                    const double cg = tab_interp(Tq, Mg.cT, Mg.cv, Mg.nc);
+                    const double cap = ceff * Ml.rho * ratio - cg * Mg.rho;
+                    double dens = -cap * ((Tq - Tqo) / dt);
+                    dens += (ratio * vc_dkdT(Tq, Ml.kT, Ml.kv, Ml.nk) - vc_dkdT(Tq, Mg.kT, Mg.kv, Mg.nk)) * gsq;
+                    if (src.on) {
+                        const double ex = 3.0 * ((x[0] - src.center[0]) / src.radius) * ((x[0] - src.center[0]) / src.radius);
+                        const double ey = 3.0 * ((x[1] - src.center[1]) / src.radius) * ((x[1] - src.center[1]) / src.radius);
+                        const double ez = 3.0 * ((x[2] - src.center[2]) / src.depth) * ((x[2] - src.center[2]) / src.depth);
+                        dens += (ratio - 1.0) * (src.peak * exp(-(ex + ey + ez)));
+                    }
+                    acc += 0.25 * vol * dens * ((r == q) ? A : B);
+                }
+            }
+        }
+        load[p] = acc;
+    }
+}
+
 }  // namespace tl

@@ -138,6 +138,18 @@ def _needs_general_path(mat, bounds: BoundarySpec, latent: bool) -> bool:
     return convective or not problem_is_linear(mat, bounds, latent)
 
 
+def vc_material(mat, latent: bool):
+    """``tl_vc_material`` of a material (tables in K); returns (struct, arrays kept alive)."""
+    kt = np.ascontiguousarray(mat.conductivity_table, dtype=np.float64)
+    ct = np.ascontiguousarray(mat.heat_capacity_table, dtype=np.float64)
+    tabs = [np.ascontiguousarray(kt[:, 0]), np.ascontiguousarray(kt[:, 1]),
+            np.ascontiguousarray(ct[:, 0]), np.ascontiguousarray(ct[:, 1])]
+    md = N.VcMaterial(tabs[0].ctypes.data, tabs[1].ctypes.data, len(kt), tabs[2].ctypes.data,
+                      tabs[3].ctypes.data, len(ct), float(mat.rho), float(mat.chi), float(mat.S),
+                      0.5 * (float(mat.T_solidus) + float(mat.T_liquidus)), 1 if latent else 0)
+    return md, tabs
+
+
 def _step_general(state: FieldState, dt: float, mat, source, bounds: BoundarySpec, settings: SolverSettings,
                   latent: bool, extra_load, stats) -> FieldState:
     """``step_backward_euler`` (``fem.py:307-355``) for temperature-dependent tables, latent
@@ -152,14 +164,7 @@ def _step_general(state: FieldState, dt: float, mat, source, bounds: BoundarySpe
         raise UnsupportedOnDevice("Robin terms are supported on the top face only")
     rad = bool(bounds.radiation and bounds.bc.emissivity > 0 and bounds.robin_tags)
     conv = bool(bounds.robin_tags) and bounds.bc.h_conv > 0
-    kt = np.ascontiguousarray(mat.conductivity_table, dtype=np.float64)
-    ct = np.ascontiguousarray(mat.heat_capacity_table, dtype=np.float64)
-    tabs = [np.ascontiguousarray(kt[:, 0]), np.ascontiguousarray(kt[:, 1]),
-            np.ascontiguousarray(ct[:, 0]), np.ascontiguousarray(ct[:, 1])]
-    md = N.VcMaterial(tabs[0].ctypes.data, tabs[1].ctypes.data, len(kt), tabs[2].ctypes.data,
-                      tabs[3].ctypes.data, len(ct), float(mat.rho), float(mat.chi), float(mat.S),
-                      0.5 * (float(mat.T_solidus) + float(mat.T_liquidus)),
-                      1 if (latent and mat.chi > 0.0) else 0)
+    md, tabs = vc_material(mat, latent and mat.chi > 0.0)
     rb = N.Robin(float(bounds.bc.h_conv) if conv else 0.0,
                  float(bounds.bc.sigma_sb * bounds.bc.emissivity) if rad else 0.0,
                  float(bounds.bc.T_ambient), 1 if (conv or rad) else 0)

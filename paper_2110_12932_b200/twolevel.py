@@ -161,8 +161,12 @@ class TwoLevelProblem:
             if self.bc.emissivity > 0:
                 raise UnsupportedOnDevice("radiation (emissivity > 0) is not on the device-resident path")
         if not self.one_way and self.mode != "alternate":
-            raise UnsupportedOnDevice("full-mode overlap feedback (coupling mode 'full' with distinct "
-                                      "materials) is not on the device path")
+            if resident:
+                raise UnsupportedOnDevice("full-mode overlap feedback runs through the step-level drivers")
+            if self.interval_source:
+                raise UnsupportedOnDevice("full-mode overlap feedback evaluates the global source at "
+                                          "quadrature points: it needs source_global gaussian (the swept-"
+                                          "track deposit is not a pointwise source)")
         if resident and not self.interval_source:
             raise UnsupportedOnDevice("the device-resident run uses the distributed (swept-track) "
                                       "global source; 'gaussian' runs through the step-level drivers")
@@ -226,6 +230,37 @@ def transmission_load(local_field, gamma, global_mesh, mat_global, mat_local) ->
     return out
 
 
+def overlap_feedback(problem: TwoLevelProblem, local_new: FieldState, local_old: FieldState, dt: float,
+                     t0: float, t1: float) -> np.ndarray:
+    """``_overlap_feedback`` (``twolevel.py:186-239``): the full-mode overlap terms as a
+    global load, one device call (``tl_overlap_feedback_host``): capacity difference,
+    conductivity-gradient cross terms and the source scaling at the global quadrature
+    points inside the local box."""
+    import ctypes as C
+    from . import _native as N
+    from .fem import vc_material
+    gm, lm = problem.global_mesh, local_new.mesh
+    if local_old.mesh is not lm and not lm.same_lattice(local_old.mesh):
+        raise CouplingError("overlap feedback needs both local fields on one lattice")
+    mg, tg = vc_material(problem.mat_global, False)
+    ml, tl_ = vc_material(problem.mat_local, False)
+    src = problem.global_source(t0, t1)
+    gs = None
+    if src is not None:
+        if not isinstance(src, GaussianSource):
+            raise UnsupportedOnDevice("full-mode overlap feedback needs a pointwise (gaussian) global source")
+        peak, radius, depth, center = src.device_args()
+        gs = N.Gaussian(float(peak), float(radius), float(depth), (C.c_double * 3)(*map(float, center)), 1)
+    Tn = np.ascontiguousarray(local_new.values, dtype=np.float64)
+    To = np.ascontiguousarray(local_old.values, dtype=np.float64)
+    out = np.zeros(gm.n_nodes)
+    gd, ld = gm.desc(), lm.desc()
+    N.check(N.lib().tl_overlap_feedback_host(C.byref(gd), C.byref(ld), N.dptr(Tn), N.dptr(To), float(dt),
+                                             C.byref(mg), C.byref(ml), C.byref(gs) if gs is not None else None,
+                                             N.dptr(out)), "overlap_feedback")
+    return out
+
+
 def solve_global(problem: TwoLevelProblem, state: TwoLevelState, dt: float,
                  local_for_coupling: FieldState, stats=None, predictor: bool = False) -> FieldState:
     """One global backward-Euler step on the device (``twolevel.py:242-271``)."""
@@ -239,6 +274,8 @@ def solve_global(problem: TwoLevelProblem, state: TwoLevelState, dt: float,
         source = dep
     elif dep is not None:
         load = load + deposit_load(problem.global_mesh, dep[0], dep[1])
+    if problem.mode == "full":
+        load = load + overlap_feedback(problem, local_for_coupling, state.local_field, dt, t0, t1)
     timer = stats.timer("global_solve") if stats is not None else _Null()
     with timer:
         out = step_backward_euler(state.global_field, dt, problem.mat_global, source,

@@ -40,6 +40,8 @@ comes from calling the reference's own functions:
                  output files, summaries, study matrix, errors.csv rows
 - transmission_tdep.npz / run_cfg1_tdep_twoway.npz  two-way coupling with temperature-
                  dependent conductivity tables (jump evaluated at T_qp)
+- run_cfg1_full.npz / run_cfg1_tdep_full.npz  coupling mode full: the overlap feedback
+                 terms (twolevel.py:186-239) with constant and temperature-dependent tables
 - schedule_*.json local-box origins per macro step from the reference's
                  LocalDomainPolicy / Mesh.translated / DomainEscape clamp,
                  path.position and swept_pieces         — scanpath.py:68-248
@@ -511,6 +513,10 @@ def transmission_tdep_case():
 
 def main():
     quick = "--quick" in sys.argv
+    if "--full" in sys.argv:
+        run_case("cfg1_full", None, {1, 2, 3, 4}, 7)
+        run_case("cfg1_tdep_full", None, {1}, 7)
+        return
     if "--tdep-twoway" in sys.argv:
         transmission_tdep_case()
         run_case("cfg1_tdep_twoway", None, {1}, 7)
@@ -562,6 +568,8 @@ def main():
     experiments_case()
     transmission_tdep_case()
     run_case("cfg1_tdep_twoway", None, {1}, 7)
+    run_case("cfg1_full", None, {1, 2, 3, 4}, 7)
+    run_case("cfg1_tdep_full", None, {1}, 7)
 
 
 if __name__ == "__main__":

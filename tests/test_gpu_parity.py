@@ -528,7 +528,7 @@ def test_transmission_load_vs_reference():
 
 
 @pytest.mark.parametrize("name", ["cfg1_twoway", "cfg1_twoway_uniform", "cfg1_tdep", "cfg1_gsrc",
-                                  "cfg1_gsrc_uniform", "cfg1_tdep_twoway"])
+                                  "cfg1_gsrc_uniform", "cfg1_tdep_twoway", "cfg1_full", "cfg1_tdep_full"])
 def test_two_way_coupled_run_vs_reference(name):
     """Two-way coupling (global_kappa_scale 1.5, omega 0.7, tol 1e-8): 4 macro steps whose
     correctors are the relaxed two_level_iterate fixed point, with relocations; counters
@@ -537,7 +537,9 @@ def test_two_way_coupled_run_vs_reference(name):
     temperature-dependent material with latent heat, convection and radiation (one-way,
     every solve a Picard loop over tl_vc_step_host passes, 194 passes in 2 macro steps).
     cfg1_gsrc(_uniform): the "gaussian" coarse source (runner.py:64-71; predictor beam at
-    t0 + 0.75 dt), whose corrector re-solves both levels (multirate.py:156-161)."""
+    t0 + 0.75 dt), whose corrector re-solves both levels (multirate.py:156-161).
+    cfg1_full / cfg1_tdep_full: coupling mode full, the overlap feedback load
+    (twolevel.py:186-239) with constant and temperature-dependent tables."""
     z, cfg, rec, stats = _golden_run(name)
     assert stats.counters == json.loads(str(z["counters"]))
     TL = cfg.material.T_liquidus
