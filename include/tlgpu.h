@@ -205,6 +205,12 @@ int32_t tl_transmission_tables_host(const tl_grid_desc* global_grid, const tl_gr
  *      out[1] = b^T M b (0 when b == NULL). */
 int32_t tl_mass_norms_host(const tl_grid_desc* grid, const double* a, const double* b, double* out);
 
+/* ---- masked mass norms (twolevel.masked_mass, twolevel.py:361-373): out[0] = d^T M_in d,
+ *      out[1] = d^T M_out d, d = a - b, M_in over the tets whose centroid lies in the closed
+ *      box [box_lo, box_hi] (consistency_diagnostic, twolevel.py:376-400). */
+int32_t tl_mass_norms_split_host(const tl_grid_desc* grid, const double* a, const double* b, const double* box_lo,
+                                 const double* box_hi, double* out);
+
 /* ---- error_metrics' per-record term (metrics.py:141-150): the reference field on
  *      ref_grid interpolated at grid's nodes (Mesh.interpolate), then
  *      out[0] = d^T M d with d = values - P1(ref), out[1] = P1(ref)^T M P1(ref). */

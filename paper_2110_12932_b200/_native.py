@@ -109,6 +109,7 @@ SIGNATURES = [
     ("tl_interpolate_points_host", C.c_int32, [C.POINTER(GridDesc), _dp, _dp, C.c_int64, _dp]),
     ("tl_deposit_host", C.c_int32, [C.POINTER(GridDesc), _dp, _dp, C.c_int32, _dp]),
     ("tl_mass_norms_host", C.c_int32, [C.POINTER(GridDesc), _dp, _dp, _dp]),
+    ("tl_mass_norms_split_host", C.c_int32, [C.POINTER(GridDesc), _dp, _dp, _dp, _dp, _dp]),
     ("tl_transmission_host", C.c_int32, [C.POINTER(GridDesc), C.POINTER(GridDesc), _dp, C.c_double, _dp]),
     ("tl_overlap_feedback_host", C.c_int32, [C.POINTER(GridDesc), C.POINTER(GridDesc), _dp, _dp, C.c_double,
                                              C.POINTER(VcMaterial), C.POINTER(VcMaterial), C.POINTER(Gaussian),

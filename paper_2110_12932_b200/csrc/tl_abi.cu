@@ -1004,6 +1004,28 @@ int32_t tl_mass_norms_host(const tl_grid_desc* grid, const double* a, const doub
     return TL_OK;
 }
 
+int32_t tl_mass_norms_split_host(const tl_grid_desc* grid, const double* a, const double* b, const double* box_lo,
+                                 const double* box_hi, double* out) {
+    if (!grid || !a || !b || !box_lo || !box_hi || !out) return fail(TL_E_INVALID, "null argument");
+    tl::Grid L{};
+    if (int rc = make_grid(*grid, tl::kBottom, L)) return rc;
+    constexpr int kNB = 296;
+    double *da, *db, *dpart;
+    int rc = 0;
+    if ((rc = dalloc(&da, L.n)) || (rc = dalloc(&db, L.n)) || (rc = dalloc(&dpart, 2 * kNB))) return rc;
+    TL_CUDA(cudaMemcpy(da, a, sizeof(double) * L.n, cudaMemcpyHostToDevice));
+    TL_CUDA(cudaMemcpy(db, b, sizeof(double) * L.n, cudaMemcpyHostToDevice));
+    tl::k_mass_norms_split<<<kNB, 256>>>(L, da, db, box_lo[0], box_lo[1], box_lo[2], box_hi[0], box_hi[1],
+                                         box_hi[2], dpart);
+    TL_CUDA(cudaGetLastError());
+    double part[2 * kNB];
+    TL_CUDA(cudaMemcpy(part, dpart, sizeof(part), cudaMemcpyDeviceToHost));
+    out[0] = out[1] = 0.0;
+    for (int k = 0; k < kNB; ++k) { out[0] += part[2 * k]; out[1] += part[2 * k + 1]; }
+    cudaFree(da); cudaFree(db); cudaFree(dpart);
+    return TL_OK;
+}
+
 int32_t tl_error_l2_host(const tl_grid_desc* ref_grid, const double* ref_values, const tl_grid_desc* grid,
                          const double* values, double* out) {
     if (!ref_grid || !ref_values || !grid || !values || !out) return fail(TL_E_INVALID, "null argument");

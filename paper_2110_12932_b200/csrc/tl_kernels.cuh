@@ -989,6 +989,48 @@ __global__ void k_mass_norms(Grid L, const double* __restrict__ a, const double*
     }
 }
 
+// Masked mass norms (twolevel.masked_mass, twolevel.py:361-373): (a-b)^T M (a-b) over the
+// tets whose centroid lies in the closed box [blo, bhi] -> part[2 blk], the others ->
+// part[2 blk + 1] (consistency_diagnostic's overlap / exterior split, :376-400).
+__global__ void k_mass_norms_split(Grid L, const double* __restrict__ a, const double* __restrict__ b,
+                                   double blo0, double blo1, double blo2, double bhi0, double bhi1, double bhi2,
+                                   double* part) {
+    __shared__ double red[64];
+    const int ncell = L.nc[0] * L.nc[1] * L.nc[2];
+    const int sy = L.NX, sz = L.NX * L.NY;
+    const double blo[3] = {blo0, blo1, blo2}, bhi[3] = {bhi0, bhi1, bhi2};
+    double acc[2] = {0.0, 0.0};
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncell; c += gridDim.x * blockDim.x) {
+        const int ci = c % L.nc[0], t = c / L.nc[0];
+        const int cj = t % L.nc[1], ck = t / L.nc[1];
+        const int cc[3] = {ci, cj, ck};
+        const int p0 = ci + sy * cj + sz * ck;
+        const int off[8] = {0, 1, sy, 1 + sy, sz, 1 + sz, sy + sz, 1 + sy + sz};
+        double d[8];
+        for (int q = 0; q < 8; ++q) d[q] = a[p0 + off[q]] - b[p0 + off[q]];
+        const int mid[6][2] = {{1, 3}, {1, 5}, {2, 3}, {2, 6}, {4, 5}, {4, 6}};
+        for (int e = 0; e < 6; ++e) {
+            const int v[4] = {0, mid[e][0], mid[e][1], 7};
+            bool in = true;
+            for (int ax = 0; ax < 3; ++ax) {
+                double s = 0.0;
+                for (int k = 0; k < 4; ++k) s += node_coord(L, ax, cc[ax] + ((v[k] >> ax) & 1));
+                const double cen = s / 4.0;
+                in = in && cen >= blo[ax] && cen <= bhi[ax];
+            }
+            const double s1 = d[0] + d[v[1]] + d[v[2]] + d[7];
+            const double f = d[0] * d[0] + d[v[1]] * d[v[1]] + d[v[2]] * d[v[2]] + d[7] * d[7] + s1 * s1;
+            acc[in ? 0 : 1] += f;
+        }
+    }
+    block_sum<2>(acc, red);
+    if (threadIdx.x == 0) {
+        const double w = L.h[0] * L.h[1] * L.h[2] / 6.0 / 20.0;
+        part[2 * blockIdx.x] = acc[0] * w;
+        part[2 * blockIdx.x + 1] = acc[1] * w;
+    }
+}
+
 __global__ void k_flush(double* buf, size_t n, double v) {
     for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x)
         buf[e] = v;

@@ -29,7 +29,8 @@ from .fem import BoundarySpec, FieldState, GaussianSource, check_linear_problem,
 from .grid import BOTTOM, TOP, StructuredGrid
 
 __all__ = ["TwoLevelProblem", "TwoLevelState", "InterfaceGamma", "initial_state", "solve_global",
-           "solve_local", "transmission_load", "extract_interface", "two_level_iterate", "relocate_local"]
+           "solve_local", "transmission_load", "extract_interface", "two_level_iterate", "relocate_local",
+           "overlap_feedback", "consistency_diagnostic"]
 
 
 @dataclass(frozen=True)
@@ -362,6 +363,29 @@ def relocate_local(state: TwoLevelState, policy, laser, direction, problem: TwoL
     local = FieldState(new_mesh, values, state.local_field.time)
     trace = gamma.trace_of(state.global_field.values, gmesh)
     return TwoLevelState(state.global_field, local, gamma, trace)
+
+
+def consistency_diagnostic(state: TwoLevelState, reference: FieldState, global_mesh) -> dict:
+    """``consistency_diagnostic`` (``twolevel.py:376-400``): discrete L2 norms of (reference -
+    fine) on the local domain, (reference - coarse) on the global tets whose centroid lies
+    in the local box ("overlap") and outside it ("exterior"); interpolation and the masked
+    mass norms on the device."""
+    from . import _native as N
+    from .ops import interpolate_to_grid
+    lm = state.local_field.mesh
+    out = np.zeros(2)
+    rv = np.ascontiguousarray(reference.values, dtype=np.float64)
+    lv = np.ascontiguousarray(state.local_field.values, dtype=np.float64)
+    rd, ld, gd = reference.mesh.desc(), lm.desc(), global_mesh.desc()
+    N.check(N.lib().tl_error_l2_host(N.C.byref(rd), N.dptr(rv), N.C.byref(ld), N.dptr(lv), N.dptr(out)), "error l2")
+    local = float(np.sqrt(abs(out[0])))
+    ref_g = np.ascontiguousarray(interpolate_to_grid(reference.mesh, rv, global_mesh), dtype=np.float64)
+    gv = np.ascontiguousarray(state.global_field.values, dtype=np.float64)
+    lo = np.ascontiguousarray(lm.box.lo, dtype=np.float64)
+    hi = np.ascontiguousarray(lm.box.hi, dtype=np.float64)
+    N.check(N.lib().tl_mass_norms_split_host(N.C.byref(gd), N.dptr(ref_g), N.dptr(gv), N.dptr(lo), N.dptr(hi),
+                                             N.dptr(out)), "masked mass")
+    return {"local": local, "overlap": float(np.sqrt(abs(out[0]))), "exterior": float(np.sqrt(abs(out[1])))}
 
 
 class _Null:

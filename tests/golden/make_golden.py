@@ -491,6 +491,23 @@ def experiments_case():
     print("experiments:", {k: v["summary"] for k, v in out.items() if k != "versions"})
 
 
+def consistency_case():
+    """twolevel.consistency_diagnostic of the state after 2 macro steps of cfg1_m4 against
+    run_reference at h = 25 um (the final frame)."""
+    cfg = load_config(CFG / "cfg1_m4.cfg")
+    cfg.t_end = 2 * cfg.dt_macro
+    cfg.h_reference = 2.5e-5
+    cfg.dt_reference = cfg.dt_macro / cfg.micro_steps
+    problem, lm = runner.build_problem(cfg)
+    T0 = fem.uniform_field(problem.global_mesh, cfg.T_initial, time=0.0)
+    sched = multirate.MacroSchedule(cfg.dt_macro, cfg.micro_steps, 0.0, cfg.t_end)
+    state = multirate.run_spacetime(problem, sched, lm, T0, path=cfg.path, policy=cfg.policy)
+    traj = runner.run_reference(cfg)
+    d = twolevel.consistency_diagnostic(state, traj.state(len(traj) - 1), problem.global_mesh)
+    (OUT / "consistency_cfg1.json").write_text(json.dumps({"norms": d, "versions": VERS}, indent=1))
+    print("consistency:", d)
+
+
 def picard_cases():
     picard_case("tables", latent=False, radiation=False, h_conv=0.0)
     picard_case("latent", latent=True, radiation=False, h_conv=0.0)
@@ -513,6 +530,8 @@ def transmission_tdep_case():
 
 def main():
     quick = "--quick" in sys.argv
+    if "--consistency" in sys.argv:
+        return consistency_case()
     if "--full" in sys.argv:
         run_case("cfg1_full", None, {1, 2, 3, 4}, 7)
         run_case("cfg1_tdep_full", None, {1}, 7)
@@ -570,6 +589,7 @@ def main():
     run_case("cfg1_tdep_twoway", None, {1}, 7)
     run_case("cfg1_full", None, {1, 2, 3, 4}, 7)
     run_case("cfg1_tdep_full", None, {1}, 7)
+    consistency_case()
 
 
 if __name__ == "__main__":

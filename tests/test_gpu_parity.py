@@ -642,3 +642,20 @@ def test_experiment_modes_vs_reference(name, tmp_path):
                     assert x == y
                     continue
                 assert abs(fx - fy) <= 1e-7 * abs(fy) + 1e-12, (f, a, b)
+
+
+def test_consistency_diagnostic_vs_reference():
+    """twolevel.consistency_diagnostic (masked mass norms on the device) of the state after 2
+    cfg1 macro steps against the monolithic reference at h = 25 um."""
+    from paper_2110_12932_b200.twolevel import consistency_diagnostic
+    gold = json.loads((GOLDEN / "consistency_cfg1.json").read_text())["norms"]
+    cfg = P.load_config(CONFIGS / "cfg1_m4.cfg")
+    state, _ = P.two_level_run(cfg, n_steps=2)
+    cfg.t_end = 2 * cfg.dt_macro
+    cfg.h_reference = 2.5e-5
+    cfg.dt_reference = cfg.dt_macro / cfg.micro_steps
+    traj = P.run_reference(cfg)
+    problem, _ = P.build_problem(cfg)
+    got = consistency_diagnostic(state, traj.state(len(traj) - 1), problem.global_mesh)
+    for k in ("local", "overlap", "exterior"):
+        assert abs(got[k] - gold[k]) <= 1e-6 * gold[k], (k, got[k], gold[k])
