@@ -44,6 +44,12 @@ class InterfaceGamma:
     local: StructuredGrid
     trace_nodes: np.ndarray
 
+    @property
+    def measure(self) -> float:
+        """Total area of the interface facets (``mesh.py:467-469``): lateral + bottom faces."""
+        lx, ly, lz = (float(v) for v in self.local.box.lengths)
+        return lx * ly + 2.0 * (lx * lz + ly * lz)
+
     def trace_of(self, global_field_values, global_mesh) -> np.ndarray:
         from .ops import interpolate_to_grid
         full = interpolate_to_grid(global_mesh, global_field_values, self.local, gamma_only=True)

@@ -659,3 +659,31 @@ def test_consistency_diagnostic_vs_reference():
     got = consistency_diagnostic(state, traj.state(len(traj) - 1), problem.global_mesh)
     for k in ("local", "overlap", "exterior"):
         assert abs(got[k] - gold[k]) <= 1e-6 * gold[k], (k, got[k], gold[k])
+
+
+def test_deposit_integral_is_absorbed_power():
+    """Energy consistency (tests/test_sources.py:99-115): the device deposit of one full
+    swept interval carries P * eta = 179.2 W * 0.38 = 68.096 W (P1 partition of unity)."""
+    from paper_2110_12932_b200.schedule import swept_samples
+    beam = P.LaserBeam(179.2, 0.38, 8.5e-5, 5e-5, 0.8)
+    grid = P.build_structured_grid(P.Box((0.0, 0.0, 0.0), (2.4e-3, 1.2e-3, 6e-4)), 5e-5)
+    dt = 4e-4
+    a = np.array([9e-4, 6e-4, 6e-4])
+    pts, pw = swept_samples(beam, [(a, a + np.array([beam.speed * dt, 0.0, 0.0]))], dt)
+    load = ops.deposit_load(grid, pts, pw)
+    assert load.sum() == pytest.approx(68.096, rel=1e-12)
+
+
+def test_transmission_of_linear_field_is_bottom_flux():
+    """Known answer for the interface functional: T = z on the local grid has dT/dn = -1 on
+    the bottom facets and 0 on the lateral ones, so the global load sums (partition of
+    unity) to -(kappa_g - kappa_l) * Lx * Ly."""
+    from paper_2110_12932_b200.twolevel import extract_interface, transmission_load
+    cfg = P.load_config(CONFIGS / "cfg1_twoway.cfg")
+    problem, lm = P.build_problem(cfg)
+    z = lm.coords[:, 2]
+    load = transmission_load(P.FieldState(lm, z.copy(), 0.0), extract_interface(lm, problem.global_mesh),
+                             problem.global_mesh, problem.mat_global, problem.mat_local)
+    jump = cfg.material.conductivity_table[0, 1] - cfg.material_local.conductivity_table[0, 1]
+    lx, ly, _ = lm.box.lengths
+    assert load.sum() == pytest.approx(-jump * lx * ly, rel=1e-12)

@@ -242,3 +242,12 @@ def test_oracle_picard_step_vs_reference(name):
     assert npic == int(z["picard"])
     assert cg == list(z["cg_iters"])
     assert np.abs(x - z["sol"]).max() / np.abs(z["sol"]).max() <= 1e-12
+
+
+def test_interface_measure_3d():
+    """tests/test_mesh.py:185-189: lateral + bottom facet area of the interface."""
+    from paper_2110_12932_b200.twolevel import extract_interface
+    lm = P.build_structured_grid(P.Box((0, 0, 0), (1.2, 0.5, 0.1)), 0.05)
+    gm = P.build_structured_grid(P.Box((-1, -1, -0.9), (3, 2, 0.1)), 0.2)
+    g = extract_interface(lm, gm)
+    assert g.measure == pytest.approx(1.2 * 0.5 + 2 * (1.2 * 0.1 + 0.5 * 0.1), rel=1e-10)
