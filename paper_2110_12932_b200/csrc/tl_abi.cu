@@ -815,60 +815,29 @@ int32_t tl_vc_step_host(const tl_grid_desc* grid, const tl_vc_material* mat, dou
     tl::k_vc_constrain_b<<<kNB, kT>>>(G, dm, dg, wx, wy, wz, diag, b);
     tl::k_vc_constrain_w<<<kNB, kT>>>(G, dm, wx, wy, wz);
     TL_CUDA(cudaGetLastError());
-    std::vector<double> hp(2 * kNB);
-    auto sum = [&](int nv, double* out) -> int {
-        TL_CUDA(cudaMemcpy(hp.data(), part, sizeof(double) * nv * kNB, cudaMemcpyDeviceToHost));
-        for (int k = 0; k < nv; ++k) {
-            double s = 0.0;
-            for (int e = 0; e < kNB; ++e) s += hp[k * kNB + e];
-            out[k] = s;
-        }
-        return TL_OK;
-    };
-    // solve_linear cg branch (fem.py:271-291) with scipy's recurrences
-    double bb[2];
-    tl::k_vc_precond<<<kNB, kT>>>(n, diag, b, z, part);     // r.r of b in slot 1
-    if (int e = sum(2, bb)) return e;
-    const double bnorm = sqrt(bb[1]);
-    info->bnorm = bnorm;
-    info->iterations = 0;
-    info->status = TL_SOLVE_OK;
-    info->rnorm = bnorm;
-    info->true_resid = 0.0;
-    TL_CUDA(cudaMemset(x, 0, sizeof(double) * n));
-    if (bnorm > 0.0) {
-        const double atol = rtol * bnorm;
-        TL_CUDA(cudaMemcpy(r, b, sizeof(double) * n, cudaMemcpyDeviceToDevice));
-        double rr = bb[1], rho_prev = 1.0;
-        int it = 0, status = TL_SOLVE_MAXITER;
-        for (; it < maxiter; ++it) {
-            if (!std::isfinite(rr)) { status = TL_SOLVE_NONFINITE; break; }
-            if (sqrt(rr) < atol) { status = TL_SOLVE_OK; break; }
-            double rz[2];
-            tl::k_vc_precond<<<kNB, kT>>>(n, diag, r, z, part);
-            if (int e = sum(2, rz)) return e;
-            const double rho = rz[0];
-            tl::k_vc_dir<<<kNB, kT>>>(n, z, it > 0 ? rho / rho_prev : 0.0, it == 0 ? 1 : 0, pv);
-            double pq;
-            tl::k_vc_matvec<<<kNB, kT>>>(G, diag, wx, wy, wz, pv, q, part);
-            if (int e = sum(1, &pq)) return e;
-            const double alpha = rho / pq;
-            tl::k_vc_update<<<kNB, kT>>>(n, alpha, pv, q, x, r, part);
-            if (int e = sum(1, &rr)) return e;
-            rho_prev = rho;
-        }
-        if (it >= maxiter) status = TL_SOLVE_MAXITER;
-        info->iterations = it;
-        info->rnorm = sqrt(rr);
-        double tr;
-        tl::k_vc_resid<<<kNB, kT>>>(G, diag, wx, wy, wz, x, b, part);
-        if (int e = sum(1, &tr)) return e;
-        info->true_resid = sqrt(tr) / bnorm;
-        if (status == TL_SOLVE_OK && (!std::isfinite(info->true_resid) || info->true_resid > 1e2 * rtol))
-            status = TL_SOLVE_RESIDUAL;
-        info->status = status;
-    }
-    tl::k_vc_fix<<<kNB, kT>>>(n, dm, dg, x);
+    // solve_linear cg branch (fem.py:271-291) with scipy's recurrences: one cooperative launch
+    static int per_sm = 0;
+    if (per_sm == 0) TL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tl::k_vc_cg, kT, 0));
+    int dev = 0, sms = 0;
+    TL_CUDA(cudaGetDevice(&dev));
+    TL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int NBc = std::max(1, std::min(per_sm * sms, (n + kT - 1) / kT));
+    double* cpart;
+    tl::SolveInfoDev* dinfo;
+    if ((rc = dalloc(&cpart, 6 * NBc))) return rc;
+    TL_CUDA(cudaMalloc((void**)&dinfo, sizeof(tl::SolveInfoDev)));
+    tl::VcCg C{diag, wx, wy, wz, b, dm, dg, x, r, z, pv, q, cpart, rtol, maxiter, dinfo};
+    void* args[] = {&G, &C};
+    TL_CUDA(cudaLaunchCooperativeKernel((void*)tl::k_vc_cg, NBc, kT, args, 0, 0));
+    tl::SolveInfoDev hinfo{};
+    TL_CUDA(cudaMemcpy(&hinfo, dinfo, sizeof(hinfo), cudaMemcpyDeviceToHost));
+    info->iterations = hinfo.iterations;
+    info->status = hinfo.status;
+    info->bnorm = hinfo.bnorm;
+    info->rnorm = hinfo.rnorm;
+    info->true_resid = hinfo.true_resid;
+    cudaFree(cpart);
+    cudaFree(dinfo);
     TL_CUDA(cudaGetLastError());
     TL_CUDA(cudaMemcpy(x_out, x, sizeof(double) * n, cudaMemcpyDeviceToHost));
     for (double* pp : {dTo, dTl, dg, diag, wx, wy, wz, b, x, r, z, pv, q, part, tabs}) cudaFree(pp);

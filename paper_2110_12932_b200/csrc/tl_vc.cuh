@@ -11,8 +11,8 @@
 // assembled operator is a 7-point stencil with per-edge weights (oracle/varcoef.py):
 //     (A x)_p = diag_p x_p - sum_a (w_a[p] x_{p+e_a} + w_a[p-e_a] x_{p-e_a}).
 // k_vc_assemble computes diag, w and b node by node (gather over the 24 tets touching the
-// node: no atomics, deterministic); the CG vectors are swept by plain grid-stride
-// kernels with fixed-order block partials summed on the host.  This path is a seam-3
+// node: no atomics, deterministic); k_vc_cg runs the whole Jacobi-PCG in one cooperative
+// launch with fixed-order reductions.  This path is a seam-3
 // solver (host buffers in and out), not the device-resident two-level loop.
 #pragma once
 
@@ -221,75 +221,113 @@ __device__ __forceinline__ double vc_apply(const Grid& g, const double* diag, co
     return y;
 }
 
-// block partial of sum f(p) (fixed order: grid-stride per thread, warp/ block tree)
-template <int NV>
-__device__ __forceinline__ void vc_block_store(double (&v)[NV], double* part) {
-    __shared__ double red[NV * 32];
-    block_sum<NV>(v, red);
-    if (threadIdx.x == 0)
-        for (int k = 0; k < NV; ++k) part[k * gridDim.x + blockIdx.x] = v[k];
-}
+// Jacobi-PCG with scipy's recurrences (solve_linear cg, fem.py:271-298) in ONE cooperative
+// launch: three grid barriers per iteration (r.z and r.r; the new direction p, read by the
+// neighbours' stencils; p.q), every reduction a fixed-order block tree plus a fixed-order
+// sum of the block partials that every CTA performs identically (grid_sum), so all CTAs
+// take the same branch and the result is deterministic.  part: 6 slots of gridDim.x.
+struct VcCg {
+    const double *diag, *wx, *wy, *wz, *b;
+    const unsigned char* dm;
+    const double* g;
+    double *x, *r, *z, *p, *q, *part;
+    double rtol;
+    int maxiter;
+    SolveInfoDev* info;
+};
 
-// z = invd r; partials (r.z, r.r)
-__global__ void k_vc_precond(int n, const double* __restrict__ diag, const double* __restrict__ r,
-                             double* __restrict__ z, double* part) {
-    double v[2] = {0.0, 0.0};
-    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
-        const double zz = (1.0 / diag[p]) * r[p];
-        z[p] = zz;
-        v[0] += r[p] * zz;
-        v[1] += r[p] * r[p];
+__global__ void __launch_bounds__(256) k_vc_cg(Grid G, VcCg C) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double red[64];
+    __shared__ double tot[2];
+    const int n = G.n, NB = gridDim.x, b = blockIdx.x;
+    const int t0 = blockIdx.x * blockDim.x + threadIdx.x, ts = gridDim.x * blockDim.x;
+    // ||b||, x = 0, r = b
+    {
+        double v[1] = {0.0};
+        for (int i = t0; i < n; i += ts) {
+            const double bv = C.b[i];
+            C.x[i] = 0.0;
+            C.r[i] = bv;
+            v[0] += bv * bv;
+        }
+        block_sum<1>(v, red);
+        if (threadIdx.x == 0) C.part[0 * NB + b] = v[0];
     }
-    vc_block_store<2>(v, part);
-}
-
-// p = z (first) or p * beta + z
-__global__ void k_vc_dir(int n, const double* __restrict__ z, double beta, int first, double* __restrict__ pv) {
-    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x)
-        pv[p] = first ? z[p] : pv[p] * beta + z[p];
-}
-
-// q = A p; partial p.q
-__global__ void k_vc_matvec(Grid g, const double* __restrict__ diag, const double* __restrict__ wx,
-                            const double* __restrict__ wy, const double* __restrict__ wz, const double* __restrict__ pv,
-                            double* __restrict__ q, double* part) {
-    double v[1] = {0.0};
-    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < g.n; p += gridDim.x * blockDim.x) {
-        const double qq = vc_apply(g, diag, wx, wy, wz, pv, p);
-        q[p] = qq;
-        v[0] += pv[p] * qq;
+    grid.sync();
+    { const int s1[1] = {0}; grid_sum<1>(C.part, s1, NB, tot); }
+    const double bnorm = sqrt(tot[0]);
+    double rr = tot[0], rho_prev = 1.0;
+    int it = 0, status = 0;
+    if (bnorm > 0.0) {
+        const double atol = C.rtol * bnorm;
+        status = 1;
+        for (; it < C.maxiter; ++it) {
+            if (!isfinite(rr)) { status = 3; break; }
+            if (sqrt(rr) < atol) { status = 0; break; }
+            // z = invd r; r.z
+            double v[1] = {0.0};
+            for (int i = t0; i < n; i += ts) {
+                const double zz = (1.0 / C.diag[i]) * C.r[i];
+                C.z[i] = zz;
+                v[0] += C.r[i] * zz;
+            }
+            block_sum<1>(v, red);
+            if (threadIdx.x == 0) C.part[1 * NB + b] = v[0];
+            grid.sync();
+            { const int s1[1] = {1}; grid_sum<1>(C.part, s1, NB, tot); }
+            const double rho = tot[0];
+            const double beta = it > 0 ? rho / rho_prev : 0.0;
+            for (int i = t0; i < n; i += ts) C.p[i] = it == 0 ? C.z[i] : C.p[i] * beta + C.z[i];
+            grid.sync();
+            // q = A p; p.q
+            v[0] = 0.0;
+            for (int i = t0; i < n; i += ts) {
+                const double qq = vc_apply(G, C.diag, C.wx, C.wy, C.wz, C.p, i);
+                C.q[i] = qq;
+                v[0] += C.p[i] * qq;
+            }
+            block_sum<1>(v, red);
+            if (threadIdx.x == 0) C.part[2 * NB + b] = v[0];
+            grid.sync();
+            { const int s1[1] = {2}; grid_sum<1>(C.part, s1, NB, tot); }
+            const double alpha = rho / tot[0];
+            v[0] = 0.0;
+            for (int i = t0; i < n; i += ts) {
+                C.x[i] += alpha * C.p[i];
+                const double rv = C.r[i] - alpha * C.q[i];
+                C.r[i] = rv;
+                v[0] += rv * rv;
+            }
+            block_sum<1>(v, red);
+            if (threadIdx.x == 0) C.part[3 * NB + b] = v[0];
+            grid.sync();
+            { const int s1[1] = {3}; grid_sum<1>(C.part, s1, NB, tot); }
+            rr = tot[0];
+            rho_prev = rho;
+        }
     }
-    vc_block_store<1>(v, part);
-}
-
-// x += alpha p; r -= alpha q; partial r.r
-__global__ void k_vc_update(int n, double alpha, const double* __restrict__ pv, const double* __restrict__ q,
-                            double* __restrict__ x, double* __restrict__ r, double* part) {
+    // true residual ||A x - b|| / ||b||, then x_D = g
     double v[1] = {0.0};
-    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
-        x[p] += alpha * pv[p];
-        const double rr = r[p] - alpha * q[p];
-        r[p] = rr;
-        v[0] += rr * rr;
-    }
-    vc_block_store<1>(v, part);
-}
-
-// true residual partial ||A x - b||^2, and x_D = g afterwards
-__global__ void k_vc_resid(Grid g, const double* __restrict__ diag, const double* __restrict__ wx,
-                           const double* __restrict__ wy, const double* __restrict__ wz, const double* __restrict__ x,
-                           const double* __restrict__ b, double* part) {
-    double v[1] = {0.0};
-    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < g.n; p += gridDim.x * blockDim.x) {
-        const double d = vc_apply(g, diag, wx, wy, wz, x, p) - b[p];
+    for (int i = t0; i < n; i += ts) {
+        const double d = vc_apply(G, C.diag, C.wx, C.wy, C.wz, C.x, i) - C.b[i];
         v[0] += d * d;
     }
-    vc_block_store<1>(v, part);
-}
-
-__global__ void k_vc_fix(int n, const unsigned char* __restrict__ dm, const double* __restrict__ gv, double* __restrict__ x) {
-    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x)
-        if (dm[p]) x[p] = gv[p];
+    block_sum<1>(v, red);
+    if (threadIdx.x == 0) C.part[4 * NB + b] = v[0];
+    grid.sync();
+    { const int s1[1] = {4}; grid_sum<1>(C.part, s1, NB, tot); }
+    for (int i = t0; i < n; i += ts)
+        if (C.dm[i]) C.x[i] = C.g[i];
+    if (b == 0 && threadIdx.x == 0) {
+        const double tres = bnorm > 0.0 ? sqrt(tot[0]) / bnorm : 0.0;
+        if (status == 0 && bnorm > 0.0 && (!isfinite(tres) || tres > 1e2 * C.rtol)) status = 2;
+        C.info->iterations = it;
+        C.info->status = status;
+        C.info->bnorm = bnorm;
+        C.info->rnorm = sqrt(rr);
+        C.info->true_resid = tres;
+    }
 }
 
 // ---------------------------------------------------------------------------------
