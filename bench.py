@@ -493,6 +493,102 @@ def scenario_bench(args):
         dist.destroy_process_group()
 
 
+def picard_bench(args):
+    """--config picard: SURVEY §8f row 1 on a cfg2-local-sized grid (101 x 101 x 51 nodes,
+    h = 5 um): temperature-dependent implicit steps (configs/tdep.mat: kappa(T), c(T),
+    latent heat; convection + lagged radiation on the top face; moving Gaussian beam;
+    bottom Dirichlet) through the public seam fem.step_backward_euler, host buffers in and
+    out.  One step = one Picard-converged implicit step (several device passes, each
+    tl_vc_step_host: assembly + one cooperative Jacobi-PCG launch).  value and e2e are the
+    host wall clock around the public call (the seam takes host arrays); the roofline is
+    the PCG launch timed with CUDA events: N (96 k + 32) algorithmic bytes per pass
+    (SURVEY §8d's 64 B/node/iteration plus the 4 per-node coefficient arrays)."""
+    import torch
+    import paper_2110_12932_b200 as P
+    from oracle import varcoef, kuhn
+
+    rank, world, local_rank = env_rank()
+    torch.cuda.set_device(local_rank)
+    if rank != 0:
+        return
+    mat = P.load_material(ROOT / "configs" / "tdep.mat")
+    box = P.Box((0.0, 0.0, 0.0), (5e-4, 5e-4, 2.5e-4))
+    grid = P.build_structured_grid(box, 5e-6)
+    n = grid.n_nodes
+    X = grid.coords
+    c0 = np.array([2.0e-4, 2.5e-4, 2.5e-4])
+    r2 = ((X - c0) ** 2 / np.array([1.0e-4, 0.8e-4, 0.6e-4]) ** 2).sum(axis=1)
+    T = 293.0 + 1900.0 * np.exp(-r2)
+    bc = P.ThermalBC(10.0, 0.8, 293.0, 293.0)
+    bounds = P.BoundarySpec(bc=bc, robin_tags=(P.TOP,), radiation=True,
+                            dirichlet_nodes=grid.nodes_on(P.BOTTOM), dirichlet_values=293.0)
+    beam = P.LaserBeam(200.0, 0.35, 5e-5, 5e-5, 0.8)
+    settings = P.SolverSettings(picard_tol=1e-8, picard_max_iter=60, linear_tol=1e-12, linear_solver="cg")
+    dt = 2e-6
+    state = P.FieldState(grid, T, 0.0)
+    T_first = T.copy()
+
+    def step(st, k, stats):
+        center = (2.0e-4 + beam.speed * dt * (k + 1), 2.5e-4, 2.5e-4)
+        return P.step_backward_euler(st, dt, mat, P.GaussianSource(beam, center), bounds, settings,
+                                     latent=True, stats=stats)
+
+    for k in range(args.warmup):
+        state = step(state, k, None)
+    stats = P.RunStats()
+    stats.device_log = []
+    walls = []
+    with ClockSampler(local_rank) as clocks:
+        for k in range(args.warmup, args.warmup + args.steps):
+            t0 = time.perf_counter()
+            state = step(state, k, stats)
+            walls.append(time.perf_counter() - t0)
+    wall = sum(walls)
+    passes = stats.counters.get("picard_iterations", 0)
+    cg_ms = sum(ms for ms, _ in stats.device_log)
+    its = [it for _, it in stats.device_log]
+    alg = sum(n * (96 * k + 32) for k in its)
+    peak, peak_src = measured_peak()
+    value = n * args.steps / wall
+    cpu = None
+    if not args.no_cpu_baseline:
+        G = kuhn.KuhnGrid(box.lo, box.hi, grid.ncells)
+        dmask = np.zeros(n, dtype=bool)
+        dmask[grid.nodes_on(P.BOTTOM)] = True
+        g = np.full(n, 293.0)
+        robin = (10.0, bc.sigma_sb * 0.8, 293.0)
+        t0 = time.perf_counter()
+        _, npass, _ = varcoef.step(G, mat, T_first, dt, P.GaussianSource(beam, (2.0e-4 + beam.speed * dt, 2.5e-4,
+                                   2.5e-4)), dmask, g, True, robin, picard_max=60)
+        tc = time.perf_counter() - t0
+        cpu = {"value": n / tc, "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": f"the first step ({npass} Picard passes, {tc:.1f} s) via oracle/varcoef.py (the stencil "
+                         "restatement pinned to the reference's step_backward_euler); OPENBLAS_NUM_THREADS=1"}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (temperature-dependent material configs/tdep.mat, moving Gaussian beam, hot-spot T0)",
+        "config": {"workload": f"picard: temperature-dependent implicit steps on {tuple(int(v) + 1 for v in grid.ncells)} "
+                               f"nodes (cfg2 local grid), Picard loop over device passes",
+                   "picard_passes_per_step": passes / args.steps,
+                   "cg_iterations_per_pass": float(np.mean(its)) if its else None,
+                   "l2": "not flushed (host-buffer seam: every pass uploads T_old / T_lag and reads x back)",
+                   "parallelism": "single GPU"},
+        "roofline": {"bound": "hbm", "achieved": alg / (cg_ms / 1e3) / 1e9 if cg_ms else None, "peak": peak,
+                     "unit": "GB/s", "frac": (alg / (cg_ms / 1e3) / 1e9) / peak if cg_ms else None, "traffic": None,
+                     "kernel": "k_vc_cg (one cooperative Jacobi-PCG launch per Picard pass)",
+                     "share_of_step": cg_ms / 1e3 / wall, "peak_source": peak_src,
+                     "note": "N (96 k + 32) bytes per pass; working set L2-resident at this size"},
+        "cpu_baseline": cpu,
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": int(passes / args.steps * n * 8 * 3),
+                "d2h_bytes_per_step": int(passes / args.steps * n * 8),
+                "note": "host wall clock around fem.step_backward_euler (the seam takes host arrays); value is the same"},
+        "gpu_launches": int(passes * 4), "clocks": clocks.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -516,6 +612,8 @@ def main():
         return slab_bench(args)
     if args.config == "cfg5":
         return scenario_bench(args)
+    if args.config == "picard":
+        return picard_bench(args)
 
     import torch
     import paper_2110_12932_b200 as P

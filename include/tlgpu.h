@@ -187,6 +187,9 @@ int32_t tl_overlap_feedback_host(const tl_grid_desc* global_grid, const tl_grid_
                                  const tl_vc_material* mat_global, const tl_vc_material* mat_local,
                                  const tl_gaussian* src, double* load_out);
 
+/* Device time (CUDA events) of the last tl_vc_step_host's Jacobi-PCG launch (benchmark). */
+int32_t tl_vc_last_cg_ms(float* ms);
+
 /* ---- transmission_load (twolevel.py:159-183) for constant conductivities:
  *      load_out (dense, global nodes) = sum over the local grid's interface facets
  *      (LATERAL + BOTTOM, mesh.py:477-523) of jump * dT_local/dn * w_global at 3

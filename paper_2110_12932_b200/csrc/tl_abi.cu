@@ -770,6 +770,14 @@ int32_t tl_interpolate_host(const tl_grid_desc* global_grid, const double* value
     return TL_OK;
 }
 
+static float g_vc_last_ms = 0.0f;
+
+int32_t tl_vc_last_cg_ms(float* ms) {
+    if (!ms) return fail(TL_E_INVALID, "null argument");
+    *ms = g_vc_last_ms;
+    return TL_OK;
+}
+
 int32_t tl_vc_step_host(const tl_grid_desc* grid, const tl_vc_material* mat, double dt, const double* T_old,
                         const double* T_lag, const double* extra_load, const tl_gaussian* src, const tl_robin* robin,
                         const uint8_t* dirichlet_mask, const double* g, double rtol, int32_t maxiter, double* x_out,
@@ -782,16 +790,40 @@ int32_t tl_vc_step_host(const tl_grid_desc* grid, const tl_vc_material* mat, dou
     if (int rc = make_grid(*grid, tl::kBottom, G)) return rc;
     const int n = G.n;
     constexpr int kNB = 296, kT = 256;
-    double *dTo, *dTl, *dex = nullptr, *dg, *diag, *wx, *wy, *wz, *b, *x, *r, *z, *pv, *q, *part, *tabs;
-    unsigned char* dm;
-    int rc = 0;
-    if ((rc = dalloc(&dTo, n)) || (rc = dalloc(&dTl, n)) || (extra_load && (rc = dalloc(&dex, n))) ||
-        (rc = dalloc(&dg, n)) || (rc = dalloc(&diag, n)) || (rc = dalloc(&wx, n)) || (rc = dalloc(&wy, n)) ||
-        (rc = dalloc(&wz, n)) || (rc = dalloc(&b, n)) || (rc = dalloc(&x, n)) || (rc = dalloc(&r, n)) ||
-        (rc = dalloc(&z, n)) || (rc = dalloc(&pv, n)) || (rc = dalloc(&q, n)) || (rc = dalloc(&part, 2 * kNB)) ||
-        (rc = dalloc(&tabs, 2 * (mat->nk + mat->nc))))
-        return rc;
-    TL_CUDA(cudaMalloc((void**)&dm, n));
+    // device workspace kept across calls (a Picard loop calls this once per pass); grown on demand
+    static double* ws = nullptr;
+    static size_t ws_cap = 0;
+    static unsigned char* dm = nullptr;
+    static double* tabs = nullptr;
+    static double* cpart = nullptr;
+    static tl::SolveInfoDev* dinfo = nullptr;
+    const size_t per = (size_t)n + 2, nt = 2 * (size_t)(mat->nk + mat->nc);
+    const size_t want = 15 * per + nt + 6 * 4096;
+    if (want > ws_cap) {
+        if (ws) { cudaFree(ws); cudaFree(dm); }
+        ws = nullptr;
+        ws_cap = 0;
+        TL_CUDA(cudaMalloc((void**)&ws, sizeof(double) * want));
+        TL_CUDA(cudaMalloc((void**)&dm, per));
+        if (!dinfo) TL_CUDA(cudaMalloc((void**)&dinfo, sizeof(tl::SolveInfoDev)));
+        ws_cap = want;
+    }
+    double* dTo = ws;
+    double* dTl = ws + per;
+    double* dex = extra_load ? ws + 2 * per : nullptr;
+    double* dg = ws + 3 * per;
+    double* diag = ws + 4 * per;
+    double* wx = ws + 5 * per;
+    double* wy = ws + 6 * per;
+    double* wz = ws + 7 * per;
+    double* b = ws + 8 * per;
+    double* x = ws + 9 * per;
+    double* r = ws + 10 * per;
+    double* z = ws + 11 * per;
+    double* pv = ws + 12 * per;
+    double* q = ws + 13 * per;
+    tabs = ws + 15 * per;
+    cpart = tabs + nt;
     TL_CUDA(cudaMemcpy(dTo, T_old, sizeof(double) * n, cudaMemcpyHostToDevice));
     TL_CUDA(cudaMemcpy(dTl, T_lag, sizeof(double) * n, cudaMemcpyHostToDevice));
     if (dex) TL_CUDA(cudaMemcpy(dex, extra_load, sizeof(double) * n, cudaMemcpyHostToDevice));
@@ -822,13 +854,19 @@ int32_t tl_vc_step_host(const tl_grid_desc* grid, const tl_vc_material* mat, dou
     TL_CUDA(cudaGetDevice(&dev));
     TL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const int NBc = std::max(1, std::min(per_sm * sms, (n + kT - 1) / kT));
-    double* cpart;
-    tl::SolveInfoDev* dinfo;
-    if ((rc = dalloc(&cpart, 6 * NBc))) return rc;
-    TL_CUDA(cudaMalloc((void**)&dinfo, sizeof(tl::SolveInfoDev)));
+    if (NBc > 4096) return fail(TL_E_INVALID, "too many CTAs for the reduction workspace");
     tl::VcCg C{diag, wx, wy, wz, b, dm, dg, x, r, z, pv, q, cpart, rtol, maxiter, dinfo};
     void* args[] = {&G, &C};
+    cudaEvent_t e0, e1;
+    TL_CUDA(cudaEventCreate(&e0));
+    TL_CUDA(cudaEventCreate(&e1));
+    TL_CUDA(cudaEventRecord(e0, 0));
     TL_CUDA(cudaLaunchCooperativeKernel((void*)tl::k_vc_cg, NBc, kT, args, 0, 0));
+    TL_CUDA(cudaEventRecord(e1, 0));
+    TL_CUDA(cudaEventSynchronize(e1));
+    TL_CUDA(cudaEventElapsedTime(&g_vc_last_ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
     tl::SolveInfoDev hinfo{};
     TL_CUDA(cudaMemcpy(&hinfo, dinfo, sizeof(hinfo), cudaMemcpyDeviceToHost));
     info->iterations = hinfo.iterations;
@@ -836,13 +874,8 @@ int32_t tl_vc_step_host(const tl_grid_desc* grid, const tl_vc_material* mat, dou
     info->bnorm = hinfo.bnorm;
     info->rnorm = hinfo.rnorm;
     info->true_resid = hinfo.true_resid;
-    cudaFree(cpart);
-    cudaFree(dinfo);
     TL_CUDA(cudaGetLastError());
     TL_CUDA(cudaMemcpy(x_out, x, sizeof(double) * n, cudaMemcpyDeviceToHost));
-    for (double* pp : {dTo, dTl, dg, diag, wx, wy, wz, b, x, r, z, pv, q, part, tabs}) cudaFree(pp);
-    if (dex) cudaFree(dex);
-    cudaFree(dm);
     return TL_OK;
 }
 

@@ -206,6 +206,10 @@ def _step_general(state: FieldState, dt: float, mat, source, bounds: BoundarySpe
         raise_for(info)
         if stats is not None:
             stats.count("picard_iterations")
+            if stats.device_log is not None:
+                ms = C.c_float()
+                N.check(N.lib().tl_vc_last_cg_ms(C.byref(ms)), "timing")
+                stats.device_log.append((float(ms.value), int(info.iterations)))
         scale = np.linalg.norm(x)
         inc = np.linalg.norm(x - T_lag) / max(scale, 1e-300)
         if linear or inc < settings.picard_tol:
