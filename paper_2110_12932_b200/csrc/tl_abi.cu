@@ -798,7 +798,8 @@ int32_t tl_vc_step_host(const tl_grid_desc* grid, const tl_vc_material* mat, dou
     static double* cpart = nullptr;
     static tl::SolveInfoDev* dinfo = nullptr;
     const size_t per = (size_t)n + 2, nt = 2 * (size_t)(mat->nk + mat->nc);
-    const size_t want = 15 * per + nt + 6 * 4096;
+    const size_t ntet = 6 * (size_t)G.nc[0] * G.nc[1] * G.nc[2];
+    const size_t want = 15 * per + nt + 6 * 4096 + 9 * ntet;
     if (want > ws_cap) {
         if (ws) { cudaFree(ws); cudaFree(dm); }
         ws = nullptr;
@@ -824,6 +825,9 @@ int32_t tl_vc_step_host(const tl_grid_desc* grid, const tl_vc_material* mat, dou
     double* q = ws + 13 * per;
     tabs = ws + 15 * per;
     cpart = tabs + nt;
+    double* tk = cpart + 6 * 4096;
+    double* tml = tk + ntet;
+    double* tsrc = tml + 4 * ntet;
     TL_CUDA(cudaMemcpy(dTo, T_old, sizeof(double) * n, cudaMemcpyHostToDevice));
     TL_CUDA(cudaMemcpy(dTl, T_lag, sizeof(double) * n, cudaMemcpyHostToDevice));
     if (dex) TL_CUDA(cudaMemcpy(dex, extra_load, sizeof(double) * n, cudaMemcpyHostToDevice));
@@ -843,7 +847,8 @@ int32_t tl_vc_step_host(const tl_grid_desc* grid, const tl_vc_material* mat, dou
     }
     tl::VcRobin RB{0.0, 0.0, 0.0, 0};
     if (robin && robin->on) RB = tl::VcRobin{robin->h_conv, robin->sigma_eps, robin->T_ambient, 1};
-    tl::k_vc_assemble<<<kNB, kT>>>(G, M, dTo, dTl, dex, dt, S, RB, diag, wx, wy, wz, b);
+    tl::k_vc_tets<<<4 * kNB, kT>>>(G, M, dTo, dTl, dt, S, tk, tml, tsrc);
+    tl::k_vc_assemble<<<kNB, kT>>>(G, tk, tml, tsrc, dTo, dTl, dex, RB, diag, wx, wy, wz, b);
     tl::k_vc_constrain_b<<<kNB, kT>>>(G, dm, dg, wx, wy, wz, diag, b);
     tl::k_vc_constrain_w<<<kNB, kT>>>(G, dm, wx, wy, wz);
     TL_CUDA(cudaGetLastError());

@@ -54,17 +54,85 @@ __device__ __forceinline__ double vc_latent(const VcMat& M, double T, double T_o
     return M.chi * ((vc_phase(M, T) - vc_phase(M, T_old)) / dT);
 }
 
-__global__ void k_vc_assemble(Grid g, VcMat M, const double* __restrict__ T_old, const double* __restrict__ T_lag,
-                              const double* __restrict__ extra, double dt, Gauss src, VcRobin rb,
-                              double* __restrict__ diag, double* __restrict__ wx, double* __restrict__ wy,
-                              double* __restrict__ wz, double* __restrict__ b) {
+// Phase 1, one thread per (cell, tet): kbar, the lumped mass of each vertex (times vol)
+// and the Gaussian load of each vertex (times vol), stored per tet so every tet's
+// quadrature-point material evaluations run once (not once per touching node).
+__global__ void k_vc_tets(Grid g, VcMat M, const double* __restrict__ T_old, const double* __restrict__ T_lag,
+                          double dt, Gauss src, double* __restrict__ tk, double* __restrict__ tml,
+                          double* __restrict__ tsrc) {
     const double A = TL_QA, B = TL_QB;
     const double vol = g.h[0] * g.h[1] * g.h[2] / 6.0;
     const int perms[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
     const int st[3] = {1, g.NX, g.NX * g.NY};
+    const int ncell = g.nc[0] * g.nc[1] * g.nc[2];
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < 6 * ncell; e += gridDim.x * blockDim.x) {
+        const int c = e / 6, t = e - 6 * c;
+        const int ci = c % g.nc[0], cr = c / g.nc[0];
+        const int cell[3] = {ci, cr % g.nc[1], cr / g.nc[1]};
+        const int c0 = cell[0] + g.NX * (cell[1] + g.NY * cell[2]);
+        int off[4][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+        for (int v = 1; v < 4; ++v) {
+            for (int a = 0; a < 3; ++a) off[v][a] = off[v - 1][a];
+            off[v][perms[t][v - 1]] += 1;
+        }
+        double Tl[4], To[4];
+        for (int v = 0; v < 4; ++v) {
+            const int id = c0 + off[v][0] * st[0] + off[v][1] * st[1] + off[v][2] * st[2];
+            Tl[v] = T_lag[id];
+            To[v] = T_old[id];
+        }
+        double kbar = 0.0, ml[4] = {0.0, 0.0, 0.0, 0.0}, qs[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int q = 0; q < 4; ++q) {
+            double tq = 0.0, tqo = 0.0;
+            for (int v = 0; v < 4; ++v) {
+                const double ph = (v == q) ? A : B;
+                tq += ph * Tl[v];
+                tqo += ph * To[v];
+            }
+            const double kq = vc_interp(tq, M.kT, M.kv, M.nk);
+            double cq = vc_interp(tq, M.cT, M.cv, M.nc);
+            if (M.latent) cq += vc_latent(M, tq, tqo);
+            kbar += 0.25 * kq;
+            const double mq = 0.25 * (M.rho * cq / dt);
+            double Qq = 0.0;
+            if (src.on) {
+                double x[3];
+                for (int a = 0; a < 3; ++a) {
+                    double sx = 0.0;
+                    for (int v = 0; v < 4; ++v) sx += ((v == q) ? A : B) * node_coord(g, a, cell[a] + off[v][a]);
+                    x[a] = sx;
+                }
+                const double ex = 3.0 * ((x[0] - src.center[0]) / src.radius) * ((x[0] - src.center[0]) / src.radius);
+                const double ey = 3.0 * ((x[1] - src.center[1]) / src.radius) * ((x[1] - src.center[1]) / src.radius);
+                const double ez = 3.0 * ((x[2] - src.center[2]) / src.depth) * ((x[2] - src.center[2]) / src.depth);
+                Qq = 0.25 * (src.peak * exp(-(ex + ey + ez)));
+            }
+            for (int r = 0; r < 4; ++r) {
+                const double phr = (r == q) ? A : B;
+                ml[r] += mq * phr;
+                qs[r] += Qq * phr;
+            }
+        }
+        tk[e] = kbar;
+        for (int r = 0; r < 4; ++r) {
+            tml[4 * (size_t)e + r] = ml[r] * vol;
+            tsrc[4 * (size_t)e + r] = qs[r] * vol;
+        }
+    }
+}
+
+// Phase 2, one thread per node: gather the 24 touching tets (fixed order, no atomics).
+__global__ void k_vc_assemble(Grid g, const double* __restrict__ tk, const double* __restrict__ tml,
+                              const double* __restrict__ tsrc, const double* __restrict__ T_old,
+                              const double* __restrict__ T_lag, const double* __restrict__ extra, VcRobin rb,
+                              double* __restrict__ diag, double* __restrict__ wx, double* __restrict__ wy,
+                              double* __restrict__ wz, double* __restrict__ b) {
+    const double vol = g.h[0] * g.h[1] * g.h[2] / 6.0;
+    const int perms[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
     for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < g.n; p += gridDim.x * blockDim.x) {
         int idx[3];
         decode(g, p, idx[0], idx[1], idx[2]);
+        const double Top = T_old[p];
         double dg = 0.0, bb = 0.0, wf[3] = {0.0, 0.0, 0.0};
         for (int o = 0; o < 8; ++o) {
             const int oo[3] = {o & 1, (o >> 1) & 1, (o >> 2) & 1};
@@ -76,57 +144,19 @@ __global__ void k_vc_assemble(Grid g, VcMat M, const double* __restrict__ T_old,
                 ok = ok && cell[a] >= 0 && cell[a] < g.nc[a];
             }
             if (!ok) continue;
-            const int c0 = cell[0] + g.NX * (cell[1] + g.NY * cell[2]);
+            const int c = cell[0] + g.nc[0] * (cell[1] + g.nc[1] * cell[2]);
             for (int t = 0; t < 6; ++t) {
-                // path offsets; r = position of p on the path
-                int off[4][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
-                int r = -1;
+                int off[3] = {0, 0, 0}, r = -1;
                 for (int v = 0; v < 4; ++v) {
-                    if (v > 0) {
-                        for (int a = 0; a < 3; ++a) off[v][a] = off[v - 1][a];
-                        off[v][perms[t][v - 1]] += 1;
-                    }
-                    if (off[v][0] == oo[0] && off[v][1] == oo[1] && off[v][2] == oo[2]) r = v;
+                    if (v > 0) off[perms[t][v - 1]] += 1;
+                    if (off[0] == oo[0] && off[1] == oo[1] && off[2] == oo[2]) r = v;
                 }
                 if (r < 0) continue;
-                int id[4];
-                double Tl[4], To[4];
-                for (int v = 0; v < 4; ++v) {
-                    id[v] = c0 + off[v][0] * st[0] + off[v][1] * st[1] + off[v][2] * st[2];
-                    Tl[v] = T_lag[id[v]];
-                    To[v] = T_old[id[v]];
-                }
-                double kbar = 0.0, ml = 0.0, qs = 0.0;
-                for (int q = 0; q < 4; ++q) {
-                    double tq = 0.0, tqo = 0.0;
-                    for (int v = 0; v < 4; ++v) {
-                        const double ph = (v == q) ? A : B;
-                        tq += ph * Tl[v];
-                        tqo += ph * To[v];
-                    }
-                    const double kq = vc_interp(tq, M.kT, M.kv, M.nk);
-                    double cq = vc_interp(tq, M.cT, M.cv, M.nc);
-                    if (M.latent) cq += vc_latent(M, tq, tqo);
-                    kbar += 0.25 * kq;
-                    const double phr = (r == q) ? A : B;
-                    ml += 0.25 * (M.rho * cq / dt) * phr;
-                    if (src.on) {
-                        double x[3];
-                        for (int a = 0; a < 3; ++a) {
-                            double s = 0.0;
-                            for (int v = 0; v < 4; ++v)
-                                s += ((v == q) ? A : B) * node_coord(g, a, cell[a] + off[v][a]);
-                            x[a] = s;
-                        }
-                        const double ex = 3.0 * ((x[0] - src.center[0]) / src.radius) * ((x[0] - src.center[0]) / src.radius);
-                        const double ey = 3.0 * ((x[1] - src.center[1]) / src.radius) * ((x[1] - src.center[1]) / src.radius);
-                        const double ez = 3.0 * ((x[2] - src.center[2]) / src.depth) * ((x[2] - src.center[2]) / src.depth);
-                        qs += 0.25 * (src.peak * exp(-(ex + ey + ez))) * phr;
-                    }
-                }
-                ml *= vol;
+                const size_t e = 6 * (size_t)c + t;
+                const double ml = tml[4 * e + r];
+                const double kbar = tk[e];
                 dg += ml;
-                bb += ml * To[r] + qs * vol;
+                bb += ml * Top + tsrc[4 * e + r];
                 if (r > 0) {
                     const int ax = perms[t][r - 1];
                     dg += kbar * vol / (g.h[ax] * g.h[ax]);
