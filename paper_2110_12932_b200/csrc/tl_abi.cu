@@ -11,6 +11,7 @@
 // All state stays on the device; the host only enqueues launches.
 #include <cub/cub.cuh>
 #include <algorithm>
+#include <mutex>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -790,13 +791,27 @@ int32_t tl_vc_step_host(const tl_grid_desc* grid, const tl_vc_material* mat, dou
     if (int rc = make_grid(*grid, tl::kBottom, G)) return rc;
     const int n = G.n;
     constexpr int kNB = 296, kT = 256;
-    // device workspace kept across calls (a Picard loop calls this once per pass); grown on demand
-    static double* ws = nullptr;
-    static size_t ws_cap = 0;
-    static unsigned char* dm = nullptr;
-    static double* tabs = nullptr;
-    static double* cpart = nullptr;
-    static tl::SolveInfoDev* dinfo = nullptr;
+    // device workspace kept across calls (a Picard loop calls this once per pass); grown on
+    // demand, one per device, calls serialised per process (the workspace is shared)
+    struct VcWs {
+        double* ws = nullptr;
+        size_t cap = 0;
+        unsigned char* dm = nullptr;
+        tl::SolveInfoDev* dinfo = nullptr;
+    };
+    static VcWs wss[64];
+    static std::mutex ws_mu;
+    std::lock_guard<std::mutex> lock(ws_mu);
+    int cur_dev = 0;
+    TL_CUDA(cudaGetDevice(&cur_dev));
+    if (cur_dev < 0 || cur_dev >= 64) return fail(TL_E_INVALID, "device ordinal out of range");
+    VcWs& W = wss[cur_dev];
+    double*& ws = W.ws;
+    size_t& ws_cap = W.cap;
+    unsigned char*& dm = W.dm;
+    tl::SolveInfoDev*& dinfo = W.dinfo;
+    double* tabs = nullptr;
+    double* cpart = nullptr;
     const size_t per = (size_t)n + 2, nt = 2 * (size_t)(mat->nk + mat->nc);
     const size_t ntet = 6 * (size_t)G.nc[0] * G.nc[1] * G.nc[2];
     const size_t want = 15 * per + nt + 6 * 4096 + 9 * ntet;
