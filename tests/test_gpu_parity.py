@@ -687,3 +687,35 @@ def test_transmission_of_linear_field_is_bottom_flux():
     jump = cfg.material.conductivity_table[0, 1] - cfg.material_local.conductivity_table[0, 1]
     lx, ly, _ = lm.box.lengths
     assert load.sum() == pytest.approx(-jump * lx * ly, rel=1e-12)
+
+
+def test_zero_rhs_returns_dirichlet_values():
+    """solve_linear returns zeros for ||b|| = 0 (fem.py:275-276) and re-imposes x_D = g: a
+    cold plate (T_old = 0, no source, g = 0) stays exactly 0 on both device paths."""
+    grid = P.build_structured_grid(P.Box((0.0, 0.0, 0.0), (5e-4, 4e-4, 3e-4)), 5e-5)
+    mat = P.load_material(CONFIGS / "const.mat")
+    bounds = P.BoundarySpec(bc=P.ThermalBC(0.0, 0.0, 293.0, 0.0), robin_tags=(P.TOP,), radiation=False,
+                            dirichlet_nodes=grid.nodes_on(P.BOTTOM), dirichlet_values=0.0)
+    st = P.FieldState(grid, np.zeros(grid.n_nodes), 0.0)
+    out = P.step_backward_euler(st, 1e-5, mat, None, bounds, P.SolverSettings(linear_tol=1e-12, linear_solver="cg"))
+    assert np.all(out.values == 0.0)
+    conv = P.BoundarySpec(bc=P.ThermalBC(10.0, 0.0, 0.0, 0.0), robin_tags=(P.TOP,), radiation=False,
+                          dirichlet_nodes=grid.nodes_on(P.BOTTOM), dirichlet_values=0.0)
+    out2 = P.step_backward_euler(st, 1e-5, mat, None, conv, P.SolverSettings(linear_tol=1e-12, linear_solver="cg"))
+    assert np.all(out2.values == 0.0)
+
+
+def test_picard_nonconvergence_maps_to_reference_exception():
+    """Too few Picard passes raise NonConvergence('Picard iteration', max_iter, inc) as
+    fem.py:355 does (the latent golden case needs 6)."""
+    from .test_oracle_golden import picard_material
+    z = np.load(GOLDEN / "picard_latent.npz")
+    grid = P.build_structured_grid(P.Box(tuple(z["lo"]), tuple(z["hi"])), float(z["h"]))
+    bounds = P.BoundarySpec(bc=P.ThermalBC(0.0, 0.0, 293.0, 293.0), robin_tags=(P.TOP,), radiation=False,
+                            dirichlet_nodes=grid.nodes_on(P.BOTTOM), dirichlet_values=293.0)
+    with pytest.raises(NonConvergence) as exc:
+        P.step_backward_euler(P.FieldState(grid, z["T_old"], 0.0), float(z["dt"]), picard_material(z),
+                              P.GaussianSource(P.LaserBeam(200.0, 0.35, 5e-5, 5e-5, 0.8), tuple(z["center"])),
+                              bounds, P.SolverSettings(picard_tol=1e-8, picard_max_iter=2, linear_tol=1e-12,
+                                                       linear_solver="cg"), latent=True)
+    assert exc.value.iterations == 2 and "Picard" in str(exc.value)
