@@ -187,6 +187,16 @@ int32_t tl_overlap_feedback_host(const tl_grid_desc* global_grid, const tl_grid_
                                  const tl_vc_material* mat_global, const tl_vc_material* mat_local,
                                  const tl_gaussian* src, double* load_out);
 
+/* Same pass for the monolithic reference of a two-material setup (runner.py:141-151):
+ * region = {lo[3], hi[3]}; tets whose centroid lies in the closed region use mat, the others
+ * mat_outside (PiecewiseMaterial, materials.py:161-190; NULL: mat everywhere);
+ * latent_inside_only != 0 restricts the latent term to the region (latent_reference local). */
+int32_t tl_vc_step_region_host(const tl_grid_desc* grid, const tl_vc_material* mat, const tl_vc_material* mat_outside,
+                               const double* region, int32_t latent_inside_only, double dt, const double* T_old,
+                               const double* T_lag, const double* extra_load, const tl_gaussian* src,
+                               const tl_robin* robin, const uint8_t* dirichlet_mask, const double* g, double rtol,
+                               int32_t maxiter, double* x_out, tl_solve_info* info);
+
 /* Device time (CUDA events) of the last tl_vc_step_host's Jacobi-PCG launch (benchmark). */
 int32_t tl_vc_last_cg_ms(float* ms);
 

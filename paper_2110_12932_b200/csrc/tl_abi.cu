@@ -773,6 +773,12 @@ int32_t tl_interpolate_host(const tl_grid_desc* global_grid, const double* value
 
 static float g_vc_last_ms = 0.0f;
 
+int32_t tl_vc_step_region_host(const tl_grid_desc* grid, const tl_vc_material* mat, const tl_vc_material* mat_outside,
+                               const double* region, int32_t latent_inside_only, double dt, const double* T_old,
+                               const double* T_lag, const double* extra_load, const tl_gaussian* src,
+                               const tl_robin* robin, const uint8_t* dirichlet_mask, const double* g, double rtol,
+                               int32_t maxiter, double* x_out, tl_solve_info* info);
+
 int32_t tl_vc_last_cg_ms(float* ms) {
     if (!ms) return fail(TL_E_INVALID, "null argument");
     *ms = g_vc_last_ms;
@@ -783,6 +789,18 @@ int32_t tl_vc_step_host(const tl_grid_desc* grid, const tl_vc_material* mat, dou
                         const double* T_lag, const double* extra_load, const tl_gaussian* src, const tl_robin* robin,
                         const uint8_t* dirichlet_mask, const double* g, double rtol, int32_t maxiter, double* x_out,
                         tl_solve_info* info) {
+    return tl_vc_step_region_host(grid, mat, nullptr, nullptr, 0, dt, T_old, T_lag, extra_load, src, robin,
+                                  dirichlet_mask, g, rtol, maxiter, x_out, info);
+}
+
+int32_t tl_vc_step_region_host(const tl_grid_desc* grid, const tl_vc_material* mat, const tl_vc_material* mat_outside,
+                               const double* region, int32_t latent_inside_only, double dt, const double* T_old,
+                               const double* T_lag, const double* extra_load, const tl_gaussian* src,
+                               const tl_robin* robin, const uint8_t* dirichlet_mask, const double* g, double rtol,
+                               int32_t maxiter, double* x_out, tl_solve_info* info) {
+    if ((mat_outside || latent_inside_only) && !region) return fail(TL_E_INVALID, "region box required");
+    if (mat_outside && (mat_outside->nk < 2 || mat_outside->nc < 2))
+        return fail(TL_E_INVALID, "material tables need two rows");
     if (!grid || !mat || !T_old || !T_lag || !dirichlet_mask || !g || !x_out || !info)
         return fail(TL_E_INVALID, "null argument");
     if (!(dt > 0.0)) return fail(TL_E_INVALID, "time step must be positive");
@@ -812,7 +830,8 @@ int32_t tl_vc_step_host(const tl_grid_desc* grid, const tl_vc_material* mat, dou
     tl::SolveInfoDev*& dinfo = W.dinfo;
     double* tabs = nullptr;
     double* cpart = nullptr;
-    const size_t per = (size_t)n + 2, nt = 2 * (size_t)(mat->nk + mat->nc);
+    const size_t per = (size_t)n + 2, nt_i = 2 * (size_t)(mat->nk + mat->nc);
+    const size_t nt = nt_i + (mat_outside ? 2 * (size_t)(mat_outside->nk + mat_outside->nc) : 0);
     const size_t ntet = 6 * (size_t)G.nc[0] * G.nc[1] * G.nc[2];
     const size_t want = 15 * per + nt + 6 * 4096 + 9 * ntet;
     if (want > ws_cap) {
@@ -854,6 +873,23 @@ int32_t tl_vc_step_host(const tl_grid_desc* grid, const tl_vc_material* mat, dou
     TL_CUDA(cudaMemcpy(tabs + 2 * mat->nk + mat->nc, mat->c_v, sizeof(double) * mat->nc, cudaMemcpyHostToDevice));
     tl::VcMat M{tabs, tabs + mat->nk, tabs + 2 * mat->nk, tabs + 2 * mat->nk + mat->nc, mat->nk, mat->nc,
                 mat->rho, mat->chi, mat->S, mat->T_melt, mat->latent};
+    tl::VcMat Mo = M;
+    tl::VcRegion RG{};
+    if (region) {
+        for (int a2 = 0; a2 < 3; ++a2) { RG.lo[a2] = region[a2]; RG.hi[a2] = region[3 + a2]; }
+        RG.latent_inside = latent_inside_only ? 1 : 0;
+    }
+    if (mat_outside) {
+        double* t2 = tabs + nt_i;
+        const tl_vc_material* m = mat_outside;
+        TL_CUDA(cudaMemcpy(t2, m->k_T, sizeof(double) * m->nk, cudaMemcpyHostToDevice));
+        TL_CUDA(cudaMemcpy(t2 + m->nk, m->k_v, sizeof(double) * m->nk, cudaMemcpyHostToDevice));
+        TL_CUDA(cudaMemcpy(t2 + 2 * m->nk, m->c_T, sizeof(double) * m->nc, cudaMemcpyHostToDevice));
+        TL_CUDA(cudaMemcpy(t2 + 2 * m->nk + m->nc, m->c_v, sizeof(double) * m->nc, cudaMemcpyHostToDevice));
+        Mo = tl::VcMat{t2, t2 + m->nk, t2 + 2 * m->nk, t2 + 2 * m->nk + m->nc, m->nk, m->nc,
+                       m->rho, m->chi, m->S, m->T_melt, m->latent};
+        RG.piecewise = 1;
+    }
     tl::Gauss S{};
     if (src && src->on) {
         S.peak = src->peak; S.radius = src->radius; S.depth = src->depth;
@@ -862,7 +898,7 @@ int32_t tl_vc_step_host(const tl_grid_desc* grid, const tl_vc_material* mat, dou
     }
     tl::VcRobin RB{0.0, 0.0, 0.0, 0};
     if (robin && robin->on) RB = tl::VcRobin{robin->h_conv, robin->sigma_eps, robin->T_ambient, 1};
-    tl::k_vc_tets<<<4 * kNB, kT>>>(G, M, dTo, dTl, dt, S, tk, tml, tsrc);
+    tl::k_vc_tets<<<4 * kNB, kT>>>(G, M, Mo, RG, dTo, dTl, dt, S, tk, tml, tsrc);
     tl::k_vc_assemble<<<kNB, kT>>>(G, tk, tml, tsrc, dTo, dTl, dex, RB, diag, wx, wy, wz, b);
     tl::k_vc_constrain_b<<<kNB, kT>>>(G, dm, dg, wx, wy, wz, diag, b);
     tl::k_vc_constrain_w<<<kNB, kT>>>(G, dm, wx, wy, wz);

@@ -27,6 +27,15 @@ struct VcMat {
     int latent;
 };
 
+// PiecewiseMaterial (materials.py:161-190) over a box region (runner.py:141-151: the tets
+// whose centroid lies in the closed local box take the inside material), and a latent
+// mask restricted to that region (latent_reference local).
+struct VcRegion {
+    double lo[3], hi[3];
+    int piecewise;       // 1: inside tets use Mi, outside Mo
+    int latent_inside;   // 1: latent term only on inside tets
+};
+
 struct VcRobin {
     double h, se, Tamb;
     int on;
@@ -57,9 +66,9 @@ __device__ __forceinline__ double vc_latent(const VcMat& M, double T, double T_o
 // Phase 1, one thread per (cell, tet): kbar, the lumped mass of each vertex (times vol)
 // and the Gaussian load of each vertex (times vol), stored per tet so every tet's
 // quadrature-point material evaluations run once (not once per touching node).
-__global__ void k_vc_tets(Grid g, VcMat M, const double* __restrict__ T_old, const double* __restrict__ T_lag,
-                          double dt, Gauss src, double* __restrict__ tk, double* __restrict__ tml,
-                          double* __restrict__ tsrc) {
+__global__ void k_vc_tets(Grid g, VcMat Mi, VcMat Mo, VcRegion R, const double* __restrict__ T_old,
+                          const double* __restrict__ T_lag, double dt, Gauss src, double* __restrict__ tk,
+                          double* __restrict__ tml, double* __restrict__ tsrc) {
     const double A = TL_QA, B = TL_QB;
     const double vol = g.h[0] * g.h[1] * g.h[2] / 6.0;
     const int perms[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
@@ -81,6 +90,17 @@ __global__ void k_vc_tets(Grid g, VcMat M, const double* __restrict__ T_old, con
             Tl[v] = T_lag[id];
             To[v] = T_old[id];
         }
+        bool inside = true;
+        if (R.piecewise || R.latent_inside) {
+            for (int a = 0; a < 3; ++a) {
+                double sx = 0.0;
+                for (int v = 0; v < 4; ++v) sx += node_coord(g, a, cell[a] + off[v][a]);
+                const double cen = sx / 4.0;
+                inside = inside && cen >= R.lo[a] && cen <= R.hi[a];
+            }
+        }
+        const VcMat& M = (R.piecewise && !inside) ? Mo : Mi;
+        const bool lat_on = M.latent && (!R.latent_inside || inside);
         double kbar = 0.0, ml[4] = {0.0, 0.0, 0.0, 0.0}, qs[4] = {0.0, 0.0, 0.0, 0.0};
         for (int q = 0; q < 4; ++q) {
             double tq = 0.0, tqo = 0.0;
@@ -91,7 +111,7 @@ __global__ void k_vc_tets(Grid g, VcMat M, const double* __restrict__ T_old, con
             }
             const double kq = vc_interp(tq, M.kT, M.kv, M.nk);
             double cq = vc_interp(tq, M.cT, M.cv, M.nc);
-            if (M.latent) cq += vc_latent(M, tq, tqo);
+            if (lat_on) cq += vc_latent(M, tq, tqo);
             kbar += 0.25 * kq;
             const double mq = 0.25 * (M.rho * cq / dt);
             double Qq = 0.0;

@@ -23,7 +23,8 @@ from .errors import NonConvergence, SolverError, UnsupportedOnDevice
 from .grid import BOTTOM, TOP, StructuredGrid
 
 __all__ = ["FieldState", "uniform_field", "SolverSettings", "BoundarySpec", "GaussianSource",
-           "step_backward_euler", "device_rtol", "Trajectory", "solve_monolithic"]
+           "step_backward_euler", "device_rtol", "Trajectory", "solve_monolithic", "PiecewiseMaterial",
+           "RegionMask"]
 
 
 @dataclass(frozen=True)
@@ -127,15 +128,46 @@ def _dirichlet_kind(mesh: StructuredGrid, nodes: np.ndarray) -> int:
     raise UnsupportedOnDevice("the device represents the bottom-face or interface Dirichlet sets only")
 
 
+@dataclass(frozen=True)
+class PiecewiseMaterial:
+    """``materials.PiecewiseMaterial`` (``materials.py:161-190``) on the structured grids: the
+    region is a box (the fixed local box of ``run_reference``, ``runner.py:141-151``), a tet
+    belongs to it when its centroid lies in the closed box."""
+
+    inside: object
+    outside: object
+    box: object
+
+    @property
+    def is_constant(self) -> bool:
+        return bool(self.inside.is_constant and self.outside.is_constant)
+
+    @property
+    def max_chi(self) -> float:
+        return max(self.inside.chi, self.outside.chi)
+
+    @property
+    def T_liquidus(self) -> float:
+        return self.inside.T_liquidus
+
+
+@dataclass(frozen=True)
+class RegionMask:
+    """Element mask "tets whose centroid lies in box" (``runner.py:153-158``: latent_reference local)."""
+
+    box: object
+
+
 def problem_is_linear(mat, bounds: BoundarySpec, latent: bool) -> bool:
     """``_problem_is_linear`` (``fem.py:301-304``)."""
     radiative = bounds.radiation and bounds.bc.emissivity > 0 and len(bounds.robin_tags) > 0
-    return bool(mat.is_constant) and not radiative and not (latent and mat.chi > 0.0)
+    chi = mat.max_chi if isinstance(mat, PiecewiseMaterial) else mat.chi
+    return bool(mat.is_constant) and not radiative and not (latent and chi > 0.0)
 
 
 def _needs_general_path(mat, bounds: BoundarySpec, latent: bool) -> bool:
     convective = bool(bounds.robin_tags) and bounds.bc.h_conv > 0
-    return convective or not problem_is_linear(mat, bounds, latent)
+    return convective or isinstance(mat, PiecewiseMaterial) or not problem_is_linear(mat, bounds, latent)
 
 
 def vc_material(mat, latent: bool):
@@ -151,7 +183,7 @@ def vc_material(mat, latent: bool):
 
 
 def _step_general(state: FieldState, dt: float, mat, source, bounds: BoundarySpec, settings: SolverSettings,
-                  latent: bool, extra_load, stats) -> FieldState:
+                  latent: bool, extra_load, stats, latent_mask=None) -> FieldState:
     """``step_backward_euler`` (``fem.py:307-355``) for temperature-dependent tables, latent
     heat, convection and lagged radiation: the reference's Picard loop (lag damping on
     stalls) over device passes (``tl_vc_step_host``: assembly, constraint and Jacobi-PCG on
@@ -164,7 +196,19 @@ def _step_general(state: FieldState, dt: float, mat, source, bounds: BoundarySpe
         raise UnsupportedOnDevice("Robin terms are supported on the top face only")
     rad = bool(bounds.radiation and bounds.bc.emissivity > 0 and bounds.robin_tags)
     conv = bool(bounds.robin_tags) and bounds.bc.h_conv > 0
-    md, tabs = vc_material(mat, latent and mat.chi > 0.0)
+    region = None
+    mo = None
+    if isinstance(mat, PiecewiseMaterial):
+        md, tabs = vc_material(mat.inside, latent and mat.inside.chi > 0.0)
+        mo, tabs_o = vc_material(mat.outside, latent and mat.outside.chi > 0.0)
+        region = mat.box
+    else:
+        md, tabs = vc_material(mat, latent and mat.chi > 0.0)
+    if latent_mask is not None:
+        if region is not None and (tuple(latent_mask.box.lo), tuple(latent_mask.box.hi)) != (tuple(region.lo), tuple(region.hi)):
+            raise UnsupportedOnDevice("the latent mask and the material region must be the same box")
+        region = latent_mask.box
+    reg = None if region is None else np.array(list(region.lo) + list(region.hi), dtype=np.float64)
     rb = N.Robin(float(bounds.bc.h_conv) if conv else 0.0,
                  float(bounds.bc.sigma_sb * bounds.bc.emissivity) if rad else 0.0,
                  float(bounds.bc.T_ambient), 1 if (conv or rad) else 0)
@@ -196,10 +240,11 @@ def _step_general(state: FieldState, dt: float, mat, source, bounds: BoundarySpe
         if timer is not None:
             timer.__enter__()
         try:
-            N.check(N.lib().tl_vc_step_host(C.byref(desc), C.byref(md), float(dt), N.dptr(T_old), N.dptr(T_lag),
-                                            N.dptr(ld), C.byref(src) if src is not None else None, C.byref(rb),
-                                            dmask.ctypes.data, N.dptr(g), float(rtol), min(20 * n, 2_000_000_000),
-                                            N.dptr(x), C.byref(info)), "step")
+            N.check(N.lib().tl_vc_step_region_host(
+                C.byref(desc), C.byref(md), C.byref(mo) if mo is not None else None, N.dptr(reg),
+                1 if latent_mask is not None else 0, float(dt), N.dptr(T_old), N.dptr(T_lag), N.dptr(ld),
+                C.byref(src) if src is not None else None, C.byref(rb), dmask.ctypes.data, N.dptr(g), float(rtol),
+                min(20 * n, 2_000_000_000), N.dptr(x), C.byref(info)), "step")
         finally:
             if timer is not None:
                 timer.__exit__(None, None, None)
@@ -231,12 +276,15 @@ def step_backward_euler(state: FieldState, dt: float, mat, source, bounds: Bound
     from .ops import raise_for, step
     if dt <= 0:
         raise SolverError("time step must be positive")
-    if latent_mask is not None or extra_mass_coeff is not None:
-        raise UnsupportedOnDevice("latent masks / overlap mass terms are not on the device path")
+    if extra_mass_coeff is not None:
+        raise UnsupportedOnDevice("overlap mass terms are not on the device path")
+    if latent_mask is not None and not isinstance(latent_mask, RegionMask):
+        raise UnsupportedOnDevice("the device takes latent masks as a box region (fem.RegionMask)")
     if source is not None and not isinstance(source, GaussianSource):
         raise UnsupportedOnDevice("the device evaluates GaussianSource objects, not opaque callables")
-    if _needs_general_path(mat, bounds, latent):
-        return _step_general(state, dt, mat, source, bounds, settings, latent, extra_load, stats)
+    if _needs_general_path(mat, bounds, latent) or latent_mask is not None:
+        return _step_general(state, dt, mat, source, bounds, settings, latent, extra_load, stats,
+                             latent_mask=latent_mask)
     check_linear_problem(mat, bounds, latent)
     mesh = state.mesh
     kind = _dirichlet_kind(mesh, bounds.dirichlet_nodes)

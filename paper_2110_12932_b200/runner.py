@@ -16,7 +16,9 @@ from .control import (
     initial_local_box, structured_ncells,
 )
 from .errors import UnsupportedOnDevice
-from .fem import BoundarySpec, GaussianSource, Trajectory, solve_monolithic, uniform_field
+from .fem import (
+    BoundarySpec, GaussianSource, PiecewiseMaterial, RegionMask, Trajectory, solve_monolithic, uniform_field,
+)
 from .grid import BOTTOM, TOP, StructuredGrid, build_structured_grid
 from .multirate import MacroSchedule, run_space, run_spacetime
 from .stats import RunStats
@@ -149,18 +151,26 @@ def run_reference(cfg, dt: float | None = None, stats: RunStats | None = None, m
                   observer=None) -> Trajectory:
     """Monolithic reference (``runner.py:126-163``): the true Gaussian beam on one fine grid
     (``h_reference``) over the whole plate, uniform steps ``dt_reference``, every step a
-    device solve.  Distinct coarse/fine materials (the reference's PiecewiseMaterial) and
-    latent heat are not on the device path and raise ``UnsupportedOnDevice``."""
+    device solve.  Distinct coarse/fine materials become a PiecewiseMaterial over the fixed
+    local box and ``latent_reference local`` a latent RegionMask, as the reference does."""
     c = convert_config(cfg)
     dt = cfg.dt_reference if dt is None else dt
     mesh = build_structured_grid(c["global_box"], cfg.h_reference) if mesh is None else mesh
     n_steps = int(round(c["t_end"] / dt))
     mat, mat_l = c["material"], c["material_local"]
+    region = c["local_box"]
+    material = mat
     if mat_l is not None and mat_l is not mat and not _materials_equal(mat, mat_l):
-        raise UnsupportedOnDevice("a reference with distinct coarse/fine materials (PiecewiseMaterial) "
-                                  "is not on the device path")
+        if region is None:
+            raise ValueError("a reference with distinct coarse/fine materials needs a fixed local box")
+        material = PiecewiseMaterial(mat_l, mat, region)
     chi_max = max(mat.chi, mat_l.chi if mat_l is not None else 0.0)
     latent = cfg.latent_reference != "off" and chi_max > 0
+    latent_mask = None
+    if latent and cfg.latent_reference == "local":
+        if region is None:
+            raise ValueError("latent_reference=local needs a fixed local box")
+        latent_mask = RegionMask(region)
     path, beam = c["path"], c["beam"]
     tol = 1e-12 * max(path.t_end, 1.0)
 
@@ -171,8 +181,9 @@ def run_reference(cfg, dt: float | None = None, stats: RunStats | None = None, m
 
     bounds = reference_bounds(cfg, mesh)
     T0 = uniform_field(mesh, c["T_initial"], time=0.0)
-    return solve_monolithic(mesh, mat, source_at, lambda t: bounds, dt, n_steps, T0,
-                            settings=c["solver"], latent=latent, stats=stats, observer=observer)
+    return solve_monolithic(mesh, material, source_at, lambda t: bounds, dt, n_steps, T0,
+                            settings=c["solver"], latent=latent, latent_mask=latent_mask, stats=stats,
+                            observer=observer)
 
 
 def _materials_equal(a, b) -> bool:

@@ -42,6 +42,8 @@ comes from calling the reference's own functions:
                  dependent conductivity tables (jump evaluated at T_qp)
 - run_cfg1_full.npz / run_cfg1_tdep_full.npz  coupling mode full: the overlap feedback
                  terms (twolevel.py:186-239) with constant and temperature-dependent tables
+- ref_piecewise.npz run_reference with PiecewiseMaterial (fixed local box, distinct
+                 conductivities) and latent_reference local  — runner.py:126-163
 - schedule_*.json local-box origins per macro step from the reference's
                  LocalDomainPolicy / Mesh.translated / DomainEscape clamp,
                  path.position and swept_pieces         — scanpath.py:68-248
@@ -508,6 +510,21 @@ def consistency_case():
     print("consistency:", d)
 
 
+def piecewise_case():
+    """runner.run_reference with distinct coarse/fine materials (PiecewiseMaterial over the
+    fixed local box) and latent heat only inside it (latent_reference local)."""
+    cfg = load_config(CFG / "cfg1_ref_piecewise.cfg")
+    stats = RunStats()
+    CG_ITERS.clear()
+    traj = runner.run_reference(cfg, stats=stats)
+    vals = [np.asarray(v) for v in traj.values]
+    TL = cfg.material.T_liquidus
+    np.savez_compressed(OUT / "ref_piecewise.npz", t=np.array(traj.times), fields=np.array(vals),
+                        melt=np.array([np.packbits(v > TL) for v in vals]), counters=json.dumps(stats.counters),
+                        cg_iters=np.array(CG_ITERS), versions=json.dumps(VERS))
+    print(f"ref_piecewise: nodes={traj.mesh.n_nodes} counters={stats.counters} max={vals[-1].max():.2f}")
+
+
 def picard_cases():
     picard_case("tables", latent=False, radiation=False, h_conv=0.0)
     picard_case("latent", latent=True, radiation=False, h_conv=0.0)
@@ -530,6 +547,8 @@ def transmission_tdep_case():
 
 def main():
     quick = "--quick" in sys.argv
+    if "--piecewise" in sys.argv:
+        return piecewise_case()
     if "--consistency" in sys.argv:
         return consistency_case()
     if "--full" in sys.argv:
@@ -590,6 +609,7 @@ def main():
     run_case("cfg1_full", None, {1, 2, 3, 4}, 7)
     run_case("cfg1_tdep_full", None, {1}, 7)
     consistency_case()
+    piecewise_case()
 
 
 if __name__ == "__main__":

@@ -719,3 +719,19 @@ def test_picard_nonconvergence_maps_to_reference_exception():
                               bounds, P.SolverSettings(picard_tol=1e-8, picard_max_iter=2, linear_tol=1e-12,
                                                        linear_solver="cg"), latent=True)
     assert exc.value.iterations == 2 and "Picard" in str(exc.value)
+
+
+def test_reference_piecewise_material_and_local_latent_vs_reference():
+    """run_reference (runner.py:126-163) with distinct coarse/fine conductivities over a fixed
+    local box (PiecewiseMaterial) and latent heat only inside it (latent_reference local),
+    temperature-dependent tables, convection + radiation: 4 steps, 28 Picard passes."""
+    z = np.load(GOLDEN / "ref_piecewise.npz")
+    cfg = P.load_config(CONFIGS / "cfg1_ref_piecewise.cfg")
+    stats = P.RunStats()
+    traj = P.run_reference(cfg, stats=stats)
+    assert stats.counters == json.loads(str(z["counters"]))
+    assert traj.times == list(z["t"])
+    TL = cfg.material.T_liquidus
+    for k, T in enumerate(traj.values):
+        assert rel(T, z["fields"][k]) <= REL
+        np.testing.assert_array_equal(np.packbits(T > TL), z["melt"][k])
