@@ -30,6 +30,10 @@ from .multirate import DeviceRun, macro_step, run_space, run_spacetime  # noqa: 
 from .runner import build_problem, reference_bounds, run_reference, two_level_run, two_level_run_slabs  # noqa: F401
 from . import experiment, metrics  # noqa: F401
 from .experiment import RunArtifacts, run_compare, run_experiment, run_study  # noqa: F401
+
+# the reference's top-level names (lpbfsim/__init__.py)
+Mesh = StructuredGrid
+MaterialModel = Material
 from .metrics import ErrorReport, RunLog, error_metrics, l2_norm  # noqa: F401
 from .stats import RunStats  # noqa: F401
 from .twolevel import (  # noqa: F401

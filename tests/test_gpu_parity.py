@@ -735,3 +735,16 @@ def test_reference_piecewise_material_and_local_latent_vs_reference():
     for k, T in enumerate(traj.values):
         assert rel(T, z["fields"][k]) <= REL
         np.testing.assert_array_equal(np.packbits(T > TL), z["melt"][k])
+
+
+def test_cli_compare_writes_reference_outputs(tmp_path):
+    """python -m paper_2110_12932_b200 compare <cfg> --out <dir> (lpbfsim/cli.py) on the GPU."""
+    import subprocess
+    import sys
+    out = tmp_path / "cmp"
+    r = subprocess.run([sys.executable, "-m", "paper_2110_12932_b200", "compare", str(CONFIGS / "cfg1_compare.cfg"),
+                        "--out", str(out)], cwd=str(ROOT), capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr
+    assert "mode: compare" in r.stdout
+    files = sorted(str(p.relative_to(out)) for p in out.rglob("*") if p.is_file())
+    assert files == json.loads((GOLDEN / "experiments.json").read_text())["cfg1_compare"]["files"]

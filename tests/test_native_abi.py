@@ -81,3 +81,13 @@ def test_struct_layouts_match_c_compiler(tmp_path):
         assert int(got[f"{cname} size"]) == ctypes.sizeof(py), cname
         for fname, _ in py._fields_:
             assert int(got[f"{cname} {fname}"]) == getattr(py, fname).offset, (cname, fname)
+
+
+def test_cli_parser_and_config_error(tmp_path, capsys):
+    """lpbfsim/cli.py's interface: run / study / compare subcommands; a bad config exits 2."""
+    from paper_2110_12932_b200.cli import build_parser, main
+    p = build_parser()
+    a = p.parse_args(["compare", "configs/cfg1_compare.cfg", "--out", str(tmp_path), "--snapshots", "none"])
+    assert a.command == "compare" and a.snapshots == "none" and a.out == tmp_path
+    assert main(["run", str(tmp_path / "missing.cfg")]) == 2
+    assert "config error" in capsys.readouterr().err
