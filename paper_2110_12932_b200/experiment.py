@@ -7,8 +7,9 @@
 files: ``errors.csv``, ``timing.csv``, ``summary.json``, ``centerline.csv``,
 ``study_matrix.csv``.  Every solve runs on the GPU (``run_reference``,
 ``two_level_run``); error norms use the device metrics (``metrics.error_metrics``).
-VTK snapshots are not written: a cadence other than ``none`` raises
-``UnsupportedOnDevice``.  2D control-line temperatures do not arise (3D only).
+Field snapshots are written as the reference's legacy ASCII VTK files
+(``vtkio.write_vtk``: every macro record, every 10th micro record for ``all`` in 3D).
+2D control-line temperatures do not arise (3D only).
 """
 
 from __future__ import annotations
@@ -20,12 +21,11 @@ from pathlib import Path
 
 import numpy as np
 
-from .errors import UnsupportedOnDevice
 from .metrics import ErrorReport, RunLog, composite_sampler, centerline_profile, error_metrics
 from .runner import build_problem, convert_config, run_reference
 from .stats import RunStats
 
-__all__ = ["RunArtifacts", "run_experiment", "run_study", "run_compare", "study_pairs", "write_csv"]
+__all__ = ["RunArtifacts", "run_experiment", "run_study", "run_compare", "study_pairs", "write_csv", "write_vtk"]
 
 
 @dataclass
@@ -59,11 +59,57 @@ def write_csv(path, header: list, rows):
 
 
 def _cadence(cfg, override):
-    cadence = override if override is not None else cfg.snapshots
-    if cadence != "none":
-        raise UnsupportedOnDevice(f"VTK snapshots (cadence {cadence!r}) are not written by the device "
-                                  "package; set 'snapshots none'")
-    return cadence
+    """``runner._snapshot_cadence`` (``runner.py:212-213``)."""
+    return override if override is not None else cfg.snapshots
+
+
+def write_vtk(path, mesh, point_data: dict | None = None, title: str = "lpbfsim"):
+    """``vtkio.write_vtk`` (``vtkio.py:15-44``): legacy ASCII unstructured grid of the Kuhn
+    tets with nodal scalars."""
+    path = Path(path)
+    path.parent.mkdir(parents=True, exist_ok=True)
+    pts = mesh.coords
+    elems = mesh.elems
+    ne = len(elems)
+    with path.open("w") as f:
+        f.write("# vtk DataFile Version 2.0\n")
+        f.write(f"{title}\n")
+        f.write("ASCII\n")
+        f.write("DATASET UNSTRUCTURED_GRID\n")
+        f.write(f"POINTS {mesh.n_nodes} double\n")
+        for p in pts:
+            f.write(f"{p[0]:.10g} {p[1]:.10g} {p[2]:.10g}\n")
+        f.write(f"\nCELLS {ne} {ne * 5}\n")
+        for e in elems:
+            f.write("4 " + " ".join(str(int(v)) for v in e) + "\n")
+        f.write(f"\nCELL_TYPES {ne}\n")
+        f.write("10\n" * ne)
+        if point_data:
+            f.write(f"\nPOINT_DATA {mesh.n_nodes}\n")
+            for name, values in point_data.items():
+                f.write(f"SCALARS {name} double\n")
+                f.write("LOOKUP_TABLE default\n")
+                for v in np.asarray(values):
+                    f.write(f"{v:.10g}\n")
+
+
+def _write_snapshots(out: Path, cfg, log: RunLog, cadence: str):
+    """``runner._write_snapshots`` (``runner.py:216-233``)."""
+    if cadence == "none":
+        return
+    every = 10 if cadence == "all" else 1
+    micro_seen = 0
+    for r in log.records:
+        if r.kind in ("initial", "macro"):
+            if r.global_field is not None:
+                write_vtk(out / "vtk" / f"global_{r.time:.6e}.vtk", r.global_field.mesh,
+                          {"temperature": r.global_field.values})
+            if r.local is not None:
+                write_vtk(out / "vtk" / f"local_{r.time:.6e}.vtk", r.local.mesh, {"temperature": r.local.values})
+        elif r.kind == "micro" and cadence == "all" and r.local is not None:
+            micro_seen += 1
+            if micro_seen % every == 0:
+                write_vtk(out / "vtk" / f"local_{r.time:.6e}.vtk", r.local.mesh, {"temperature": r.local.values})
 
 
 def _write_errors_csv(out: Path, report: ErrorReport):
@@ -108,11 +154,10 @@ def run_experiment(cfg, out_dir, snapshots: str | None = None, threads: int = 1)
     """``runner.run_experiment`` (``runner.py:270-284``)."""
     out = Path(out_dir)
     out.mkdir(parents=True, exist_ok=True)
-    _cadence(cfg, snapshots)
     if cfg.mode == "reference":
-        return _run_reference_mode(cfg, out)
+        return _run_reference_mode(cfg, out, snapshots)
     if cfg.mode in ("two-level-space", "two-level-spacetime"):
-        return _run_two_level_mode(cfg, out, cfg.mode == "two-level-spacetime")
+        return _run_two_level_mode(cfg, out, cfg.mode == "two-level-spacetime", snapshots)
     if cfg.mode == "convergence-study":
         return run_study(cfg, out, snapshots, threads)
     if cfg.mode == "compare":
@@ -120,17 +165,25 @@ def run_experiment(cfg, out_dir, snapshots: str | None = None, threads: int = 1)
     raise ValueError(f"unhandled mode {cfg.mode}")
 
 
-def _run_reference_mode(cfg, out: Path) -> RunArtifacts:
+def _run_reference_mode(cfg, out: Path, snapshots=None) -> RunArtifacts:
     """``runner.py:287-315``."""
     from .grid import build_structured_grid
     stats = RunStats()
     mesh = build_structured_grid(convert_config(cfg)["global_box"], cfg.h_reference)
+    cadence = _cadence(cfg, snapshots)
     rows = []
+    count = [0]
 
     def observer(state):
+        count[0] += 1
         rows.append((state.time, "macro", 0.0, ""))
+        if cadence == "all" and count[0] % 10 == 0:
+            write_vtk(out / "vtk" / f"reference_{state.time:.6e}.vtk", mesh, {"temperature": state.values})
 
     traj = run_reference(cfg, stats=stats, mesh=mesh, observer=observer)
+    if cadence == "macro":
+        fr = traj.state(len(traj) - 1)
+        write_vtk(out / "vtk" / f"reference_{fr.time:.6e}.vtk", mesh, {"temperature": fr.values})
     write_csv(out / "errors.csv", ["t", "step_kind", "rel_l2_local", "T_star"], rows)
     _write_timing_csv(out, stats)
     final = traj.state(len(traj) - 1)
@@ -140,12 +193,13 @@ def _run_reference_mode(cfg, out: Path) -> RunArtifacts:
     return RunArtifacts(out, RunLog(), stats, None, summary)
 
 
-def _run_two_level_mode(cfg, out: Path, spacetime: bool) -> RunArtifacts:
+def _run_two_level_mode(cfg, out: Path, spacetime: bool, snapshots=None) -> RunArtifacts:
     """``runner.py:318-339``."""
     log, stats, state = _two_level_run(cfg, spacetime)
     rows = [(r.time, r.kind, "", "") for r in log.of_kind("initial", "micro", "macro")]
     write_csv(out / "errors.csv", ["t", "step_kind", "rel_l2_local", "T_star"], rows)
     _write_timing_csv(out, stats)
+    _write_snapshots(out, cfg, log, _cadence(cfg, snapshots))
     final = log.of_kind("macro")[-1]
     _centerline(cfg, composite_sampler(final.local, final.global_field), out, cfg.h_reference)
     summary = {"mode": cfg.mode, "macro_steps": len(log.of_kind("macro")),
@@ -184,6 +238,7 @@ def run_study(cfg, out: Path, snapshots=None, threads: int = 1) -> RunArtifacts:
         sub.mkdir(parents=True, exist_ok=True)
         _write_errors_csv(sub, report)
         _write_timing_csv(sub, run_stats)
+        _write_snapshots(sub, cfg, log, _cadence(cfg, snapshots))
         matrix_rows.append((dt, dt / micro, report.mean_rel_l2))
         reports[(dt, micro)] = report
     write_csv(out / "study_matrix.csv", ["dt_global", "dt_local", "mean_rel_l2"], matrix_rows)
@@ -200,6 +255,7 @@ def run_compare(cfg, out: Path, snapshots=None) -> RunArtifacts:
     log_st, stats_st, _ = _two_level_run(cfg, True)
     wall_st = stats_st.total_seconds
     _write_timing_csv(out / "spacetime", stats_st)
+    _write_snapshots(out / "spacetime", cfg, log_st, _cadence(cfg, snapshots))
     log_sp, stats_sp, _ = _two_level_run(cfg, False)
     wall_sp = stats_sp.total_seconds
     _write_timing_csv(out / "spaceonly", stats_sp)

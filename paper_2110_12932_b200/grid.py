@@ -71,6 +71,35 @@ class StructuredGrid:
         out.setflags(write=False)
         return out
 
+    @cached_property
+    def elems(self) -> np.ndarray:
+        """(n_elems, 4) Kuhn tets in the reference's order (``mesh.py:406-439``): cells x
+        fastest, six tets per cell in ``itertools.permutations`` order with vertices
+        0 -> +e_p0 -> +e_p1 -> 111, the last two vertices swapped where the tet is inverted.
+        Materialised only for output (VTK); no device path reads it."""
+        import itertools
+        nc = [int(v) for v in self.ncells]
+        nn = [v + 1 for v in nc]
+        strides = np.array([1, nn[0], nn[0] * nn[1]], dtype=np.int64)
+        CZ, CY, CX = np.meshgrid(np.arange(nc[2]), np.arange(nc[1]), np.arange(nc[0]), indexing="ij")
+        corner0 = np.stack([CX.ravel(), CY.ravel(), CZ.ravel()], axis=1) @ strides
+        offsets = np.array([[(b >> a) & 1 for a in range(3)] for b in range(8)])
+        corner_ids = corner0[:, None] + offsets @ strides
+        pats = []
+        for perm in itertools.permutations(range(3)):
+            verts, acc = [0], 0
+            for ax in perm:
+                acc += 1 << ax
+                verts.append(acc)
+            pats.append(verts)
+        elems = corner_ids[:, np.array(pats)].reshape(-1, 4).astype(np.int64)
+        X = self.coords
+        J = X[elems[:, 1:]] - X[elems[:, [0]]]
+        flip = np.linalg.det(J) < 0
+        elems[flip, 2:] = elems[flip, 2:][:, ::-1]
+        elems.setflags(write=False)
+        return elems
+
     def nodes_on(self, *tags: int) -> np.ndarray:
         """Sorted node ids of boundary facets with the given tags (``mesh.py:226-230``)."""
         NZ, NY, NX = self.shape

@@ -525,6 +525,16 @@ def piecewise_case():
     print(f"ref_piecewise: nodes={traj.mesh.n_nodes} counters={stats.counters} max={vals[-1].max():.2f}")
 
 
+def vtk_case():
+    """vtkio.write_vtk of a small translated mesh with a nodal field (output format pin)."""
+    from lpbfsim import vtkio
+    m = lmesh.build_structured_mesh(lmesh.Box((1e-4, 2e-4, 0.0), (3.5e-4, 3.5e-4, 1.5e-4)), 5e-5)
+    m = m.translated((1e-5, -2e-5, 0.0))
+    v = np.random.default_rng(21).uniform(293.0, 2293.0, m.n_nodes)
+    vtkio.write_vtk(OUT / "small.vtk", m, {"temperature": v})
+    np.save(OUT / "small_vtk_field.npy", v)
+
+
 def picard_cases():
     picard_case("tables", latent=False, radiation=False, h_conv=0.0)
     picard_case("latent", latent=True, radiation=False, h_conv=0.0)
@@ -547,6 +557,8 @@ def transmission_tdep_case():
 
 def main():
     quick = "--quick" in sys.argv
+    if "--vtk" in sys.argv:
+        return vtk_case()
     if "--piecewise" in sys.argv:
         return piecewise_case()
     if "--consistency" in sys.argv:
@@ -610,6 +622,7 @@ def main():
     run_case("cfg1_tdep_full", None, {1}, 7)
     consistency_case()
     piecewise_case()
+    vtk_case()
 
 
 if __name__ == "__main__":

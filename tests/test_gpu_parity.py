@@ -748,3 +748,20 @@ def test_cli_compare_writes_reference_outputs(tmp_path):
     assert "mode: compare" in r.stdout
     files = sorted(str(p.relative_to(out)) for p in out.rglob("*") if p.is_file())
     assert files == json.loads((GOLDEN / "experiments.json").read_text())["cfg1_compare"]["files"]
+
+
+def test_two_level_mode_writes_macro_snapshots(tmp_path):
+    """run_experiment in two-level-spacetime mode with snapshots 'macro' (runner.py:216-233):
+    one global_ and one local_ VTK file per initial / macro record."""
+    from paper_2110_12932_b200.experiment import run_experiment
+    text = (CONFIGS / "cfg1_m4.cfg").read_text().replace("t_end 2 ms", "t_end 0.05 ms").replace(
+        "snapshots none", "snapshots macro")
+    (tmp_path / "c.cfg").write_text(text)
+    (tmp_path / "const.mat").write_text((CONFIGS / "const.mat").read_text())
+    art = run_experiment(P.load_config(tmp_path / "c.cfg"), tmp_path / "out")
+    names = sorted(p.name for p in (tmp_path / "out" / "vtk").iterdir())
+    times = [0.0, 2.5e-5, 5e-5]
+    assert names == sorted([f"global_{t:.6e}.vtk" for t in times] + [f"local_{t:.6e}.vtk" for t in times])
+    last = art.log.of_kind("macro")[-1]
+    vals = (tmp_path / "out" / "vtk" / f"local_{5e-5:.6e}.vtk").read_text().split("LOOKUP_TABLE default\n")[1].split()
+    np.testing.assert_allclose(np.array(vals, dtype=float), last.local.values, rtol=1e-9)

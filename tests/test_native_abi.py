@@ -91,3 +91,16 @@ def test_cli_parser_and_config_error(tmp_path, capsys):
     assert a.command == "compare" and a.snapshots == "none" and a.out == tmp_path
     assert main(["run", str(tmp_path / "missing.cfg")]) == 2
     assert "config error" in capsys.readouterr().err
+
+
+def test_vtk_writer_matches_reference_file(tmp_path):
+    """experiment.write_vtk (vtkio.write_vtk, vtkio.py:15-44): the reference's own file for a
+    translated 5 x 3 x 3-cell mesh, byte for byte (element order, orientation flips, format)."""
+    import numpy as np
+    import paper_2110_12932_b200 as P
+    from paper_2110_12932_b200.experiment import write_vtk
+    from .conftest import GOLDEN
+    g = P.build_structured_grid(P.Box((1e-4, 2e-4, 0.0), (3.5e-4, 3.5e-4, 1.5e-4)), 5e-5).translated(
+        (1e-5, -2e-5, 0.0))
+    write_vtk(tmp_path / "s.vtk", g, {"temperature": np.load(GOLDEN / "small_vtk_field.npy")})
+    assert (tmp_path / "s.vtk").read_text() == (GOLDEN / "small.vtk").read_text()
