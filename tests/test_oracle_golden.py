@@ -251,3 +251,10 @@ def test_interface_measure_3d():
     gm = P.build_structured_grid(P.Box((-1, -1, -0.9), (3, 2, 0.1)), 0.2)
     g = extract_interface(lm, gm)
     assert g.measure == pytest.approx(1.2 * 0.5 + 2 * (1.2 * 0.1 + 0.5 * 0.1), rel=1e-10)
+
+
+def test_strict_paper_constant():
+    """load_config(strict_paper=True) (lpbfsim/config.py:285-286): the printed Stefan-Boltzmann
+    constant replaces the configured one."""
+    assert P.load_config(CONFIGS / "cfg1_tdep.cfg", strict_paper=True).bc.sigma_sb == 5.87e-8
+    assert P.load_config(CONFIGS / "cfg1_tdep.cfg").bc.sigma_sb == 5.670374419e-8
