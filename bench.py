@@ -498,8 +498,9 @@ def picard_bench(args):
     h = 5 um): temperature-dependent implicit steps (configs/tdep.mat: kappa(T), c(T),
     latent heat; convection + lagged radiation on the top face; moving Gaussian beam;
     bottom Dirichlet) through the public seam fem.step_backward_euler, host buffers in and
-    out.  One step = one Picard-converged implicit step (several device passes, each
-    tl_vc_step_host: assembly + one cooperative Jacobi-PCG launch).  value and e2e are the
+    out.  One step = one Picard-converged implicit step: one tl_vc_picard_host call whose
+    passes (assembly + one cooperative Jacobi-PCG launch + the increment reduction) run on
+    the device.  value and e2e are the
     host wall clock around the public call (the seam takes host arrays); the roofline is
     the PCG launch timed with CUDA events: N (96 k + 32) algorithmic bytes per pass
     (SURVEY §8d's 64 B/node/iteration plus the 4 per-node coefficient arrays)."""
@@ -573,7 +574,7 @@ def picard_bench(args):
                                f"nodes (cfg2 local grid), Picard loop over device passes",
                    "picard_passes_per_step": passes / args.steps,
                    "cg_iterations_per_pass": float(np.mean(its)) if its else None,
-                   "l2": "not flushed (host-buffer seam: every pass uploads T_old / T_lag and reads x back)",
+                   "l2": "not flushed (host-buffer seam: each step uploads its fields and reads the result back)",
                    "parallelism": "single GPU"},
         "roofline": {"bound": "hbm", "achieved": alg / (cg_ms / 1e3) / 1e9 if cg_ms else None, "peak": peak,
                      "unit": "GB/s", "frac": (alg / (cg_ms / 1e3) / 1e9) / peak if cg_ms else None, "traffic": None,
@@ -581,10 +582,12 @@ def picard_bench(args):
                      "share_of_step": cg_ms / 1e3 / wall, "peak_source": peak_src,
                      "note": "N (96 k + 32) bytes per pass; working set L2-resident at this size"},
         "cpu_baseline": cpu,
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": int(passes / args.steps * n * 8 * 3),
-                "d2h_bytes_per_step": int(passes / args.steps * n * 8),
-                "note": "host wall clock around fem.step_backward_euler (the seam takes host arrays); value is the same"},
-        "gpu_launches": int(passes * 5), "clocks": clocks.summary(),
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": int(n * (8 + 8 + 1)),
+                "d2h_bytes_per_step": int(n * 8),
+                "note": "host wall clock around fem.step_backward_euler (the seam takes host arrays: T_old, "
+                        "Dirichlet values and mask up, the converged field down, the Picard loop in between "
+                        "on the device); value is the same"},
+        "gpu_launches": int(passes * 7 - 2 * args.steps), "clocks": clocks.summary(),
     }
     print(json.dumps(line), flush=True)
 

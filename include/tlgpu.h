@@ -197,6 +197,22 @@ int32_t tl_vc_step_region_host(const tl_grid_desc* grid, const tl_vc_material* m
                                const tl_robin* robin, const uint8_t* dirichlet_mask, const double* g, double rtol,
                                int32_t maxiter, double* x_out, tl_solve_info* info);
 
+/* The whole Picard loop of a nonlinear step on the device (fem.py:307-355): passes of
+ * tl_vc_step_region_host starting from T_lag = T_old, the relative increment
+ * ||x - T_lag|| / ||x|| reduced on the device, lag damping theta halved (>= 0.25) when the
+ * increment stalls (>= 0.9 of the previous).  Stops when linear != 0 (one pass), when the
+ * increment drops below picard_tol, after picard_max passes, or at the first pass whose CG
+ * fails (info->status != TL_SOLVE_OK).  passes / pass_iters[picard_max] / pass_ms[picard_max]
+ * report the passes, their CG iterations and PCG launch times; inc_out the last increment
+ * (the caller raises NonConvergence("Picard iteration", ...) when passes == picard_max and
+ * inc_out >= picard_tol). */
+int32_t tl_vc_picard_host(const tl_grid_desc* grid, const tl_vc_material* mat, const tl_vc_material* mat_outside,
+                          const double* region, int32_t latent_inside_only, double dt, const double* T_old,
+                          const double* extra_load, const tl_gaussian* src, const tl_robin* robin,
+                          const uint8_t* dirichlet_mask, const double* g, double rtol, int32_t maxiter, int32_t linear,
+                          double picard_tol, int32_t picard_max, double* x_out, int32_t* passes, int32_t* pass_iters,
+                          float* pass_ms, double* inc_out, tl_solve_info* info);
+
 /* Device time (CUDA events) of the last tl_vc_step_host's Jacobi-PCG launch (benchmark). */
 int32_t tl_vc_last_cg_ms(float* ms);
 

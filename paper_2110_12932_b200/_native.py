@@ -117,6 +117,11 @@ SIGNATURES = [
     ("tl_transmission_tables_host", C.c_int32, [C.POINTER(GridDesc), C.POINTER(GridDesc), _dp, _dp, _dp, C.c_int32,
                                                 _dp, _dp, C.c_int32, _dp]),
     ("tl_vc_last_cg_ms", C.c_int32, [C.POINTER(C.c_float)]),
+    ("tl_vc_picard_host", C.c_int32, [C.POINTER(GridDesc), C.POINTER(VcMaterial), C.POINTER(VcMaterial), _dp,
+                                      C.c_int32, C.c_double, _dp, _dp, C.POINTER(Gaussian), C.POINTER(Robin),
+                                      C.c_void_p, _dp, C.c_double, C.c_int32, C.c_int32, C.c_double, C.c_int32,
+                                      _dp, C.POINTER(C.c_int32), C.c_void_p, C.c_void_p, C.POINTER(C.c_double),
+                                      C.POINTER(SolveInfo)]),
     ("tl_vc_step_region_host", C.c_int32, [C.POINTER(GridDesc), C.POINTER(VcMaterial), C.POINTER(VcMaterial),
                                            _dp, C.c_int32, C.c_double, _dp, _dp, _dp, C.POINTER(Gaussian),
                                            C.POINTER(Robin), C.c_void_p, _dp, C.c_double, C.c_int32, _dp,

@@ -793,11 +793,44 @@ int32_t tl_vc_step_host(const tl_grid_desc* grid, const tl_vc_material* mat, dou
                                   dirichlet_mask, g, rtol, maxiter, x_out, info);
 }
 
+static int vc_impl(const tl_grid_desc* grid, const tl_vc_material* mat, const tl_vc_material* mat_outside,
+                   const double* region, int32_t latent_inside_only, double dt, const double* T_old,
+                   const double* T_lag, const double* extra_load, const tl_gaussian* src, const tl_robin* robin,
+                   const uint8_t* dirichlet_mask, const double* g, double rtol, int32_t maxiter, int32_t linear,
+                   double picard_tol, int32_t picard_max, double* x_out, int32_t* passes, int32_t* pass_iters,
+                   float* pass_ms, double* inc_out, tl_solve_info* info);
+
 int32_t tl_vc_step_region_host(const tl_grid_desc* grid, const tl_vc_material* mat, const tl_vc_material* mat_outside,
                                const double* region, int32_t latent_inside_only, double dt, const double* T_old,
                                const double* T_lag, const double* extra_load, const tl_gaussian* src,
                                const tl_robin* robin, const uint8_t* dirichlet_mask, const double* g, double rtol,
                                int32_t maxiter, double* x_out, tl_solve_info* info) {
+    if (!T_lag) return fail(TL_E_INVALID, "null argument");
+    int32_t passes = 0, it = 0;
+    float ms = 0.0f;
+    double inc = 0.0;
+    return vc_impl(grid, mat, mat_outside, region, latent_inside_only, dt, T_old, T_lag, extra_load, src, robin,
+                   dirichlet_mask, g, rtol, maxiter, 1, 0.0, 1, x_out, &passes, &it, &ms, &inc, info);
+}
+
+int32_t tl_vc_picard_host(const tl_grid_desc* grid, const tl_vc_material* mat, const tl_vc_material* mat_outside,
+                          const double* region, int32_t latent_inside_only, double dt, const double* T_old,
+                          const double* extra_load, const tl_gaussian* src, const tl_robin* robin,
+                          const uint8_t* dirichlet_mask, const double* g, double rtol, int32_t maxiter, int32_t linear,
+                          double picard_tol, int32_t picard_max, double* x_out, int32_t* passes, int32_t* pass_iters,
+                          float* pass_ms, double* inc_out, tl_solve_info* info) {
+    if (!passes || !pass_iters || !pass_ms || !inc_out || picard_max < 1) return fail(TL_E_INVALID, "bad argument");
+    return vc_impl(grid, mat, mat_outside, region, latent_inside_only, dt, T_old, T_old, extra_load, src, robin,
+                   dirichlet_mask, g, rtol, maxiter, linear, picard_tol, picard_max, x_out, passes, pass_iters,
+                   pass_ms, inc_out, info);
+}
+
+static int vc_impl(const tl_grid_desc* grid, const tl_vc_material* mat, const tl_vc_material* mat_outside,
+                   const double* region, int32_t latent_inside_only, double dt, const double* T_old,
+                   const double* T_lag, const double* extra_load, const tl_gaussian* src, const tl_robin* robin,
+                   const uint8_t* dirichlet_mask, const double* g, double rtol, int32_t maxiter, int32_t linear,
+                   double picard_tol, int32_t picard_max, double* x_out, int32_t* passes, int32_t* pass_iters,
+                   float* pass_ms, double* inc_out, tl_solve_info* info) {
     if ((mat_outside || latent_inside_only) && !region) return fail(TL_E_INVALID, "region box required");
     if (mat_outside && (mat_outside->nk < 2 || mat_outside->nc < 2))
         return fail(TL_E_INVALID, "material tables need two rows");
@@ -898,6 +931,9 @@ int32_t tl_vc_step_region_host(const tl_grid_desc* grid, const tl_vc_material* m
     }
     tl::VcRobin RB{0.0, 0.0, 0.0, 0};
     if (robin && robin->on) RB = tl::VcRobin{robin->h_conv, robin->sigma_eps, robin->T_ambient, 1};
+    double inc = INFINITY, prev_inc = INFINITY, theta = 1.0;
+    *passes = 0;
+    for (int pit = 1; pit <= picard_max; ++pit) {
     tl::k_vc_tets<<<4 * kNB, kT>>>(G, M, Mo, RG, dTo, dTl, dt, S, tk, tml, tsrc);
     tl::k_vc_assemble<<<kNB, kT>>>(G, tk, tml, tsrc, dTo, dTl, dex, RB, diag, wx, wy, wz, b);
     tl::k_vc_constrain_b<<<kNB, kT>>>(G, dm, dg, wx, wy, wz, diag, b);
@@ -930,6 +966,26 @@ int32_t tl_vc_step_region_host(const tl_grid_desc* grid, const tl_vc_material* m
     info->bnorm = hinfo.bnorm;
     info->rnorm = hinfo.rnorm;
     info->true_resid = hinfo.true_resid;
+    *passes = pit;
+    pass_iters[pit - 1] = hinfo.iterations;
+    pass_ms[pit - 1] = g_vc_last_ms;
+    if (hinfo.status != 0) break;                 // the caller maps the CG outcome
+    if (linear) break;                            // one pass: linear problem / tl_vc_step_region_host
+    // relative increment (fem.py:346-348), damped lag update (fem.py:350-354)
+    tl::k_vc_inc<<<kNB, kT>>>(n, x, dTl, cpart);
+    TL_CUDA(cudaGetLastError());
+    double hp[2 * kNB];
+    TL_CUDA(cudaMemcpy(hp, cpart, sizeof(hp), cudaMemcpyDeviceToHost));
+    double dd = 0.0, xx = 0.0;
+    for (int k = 0; k < kNB; ++k) { dd += hp[2 * k]; xx += hp[2 * k + 1]; }
+    inc = sqrt(dd) / std::max(sqrt(xx), 1e-300);
+    *inc_out = inc;
+    if (inc < picard_tol || pit == picard_max) break;
+    if (inc >= 0.9 * prev_inc) theta = std::max(0.25, 0.5 * theta);
+    prev_inc = inc;
+    tl::k_vc_lag<<<kNB, kT>>>(n, theta, x, dTl);
+    TL_CUDA(cudaGetLastError());
+    }
     TL_CUDA(cudaGetLastError());
     TL_CUDA(cudaMemcpy(x_out, x, sizeof(double) * n, cudaMemcpyDeviceToHost));
     return TL_OK;

@@ -380,6 +380,25 @@ __global__ void __launch_bounds__(256) k_vc_cg(Grid G, VcCg C) {
     }
 }
 
+// Picard control on the device (fem.py:346-354): partials of ||x - T_lag||^2 and ||x||^2,
+// and the damped lag update T_lag += theta (x - T_lag).
+__global__ void k_vc_inc(int n, const double* __restrict__ x, const double* __restrict__ Tl, double* part) {
+    __shared__ double red[64];
+    double v[2] = {0.0, 0.0};
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const double d = x[i] - Tl[i];
+        v[0] += d * d;
+        v[1] += x[i] * x[i];
+    }
+    block_sum<2>(v, red);
+    if (threadIdx.x == 0) { part[2 * blockIdx.x] = v[0]; part[2 * blockIdx.x + 1] = v[1]; }
+}
+
+__global__ void k_vc_lag(int n, double theta, const double* __restrict__ x, double* __restrict__ Tl) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        Tl[i] = Tl[i] + theta * (x[i] - Tl[i]);
+}
+
 // ---------------------------------------------------------------------------------
 // Full-mode overlap feedback (twolevel.py:186-239), gathered per global node: over the 24
 // global tets touching the node and their 4 quadrature points x_q (mesh.py:116-128) that
