@@ -866,7 +866,7 @@ static int vc_impl(const tl_grid_desc* grid, const tl_vc_material* mat, const tl
     const size_t per = (size_t)n + 2, nt_i = 2 * (size_t)(mat->nk + mat->nc);
     const size_t nt = nt_i + (mat_outside ? 2 * (size_t)(mat_outside->nk + mat_outside->nc) : 0);
     const size_t ntet = 6 * (size_t)G.nc[0] * G.nc[1] * G.nc[2];
-    const size_t want = 15 * per + nt + 6 * 4096 + 9 * ntet;
+    const size_t want = 16 * per + nt + 6 * 4096 + 9 * ntet;
     if (want > ws_cap) {
         if (ws) { cudaFree(ws); cudaFree(dm); }
         ws = nullptr;
@@ -889,8 +889,8 @@ static int vc_impl(const tl_grid_desc* grid, const tl_vc_material* mat, const tl
     double* r = ws + 10 * per;
     double* z = ws + 11 * per;
     double* pv = ws + 12 * per;
-    double* q = ws + 13 * per;
-    tabs = ws + 15 * per;
+    double* q = ws + 14 * per;
+    tabs = ws + 16 * per;                 // p (ws + 12 per) is a ping-pong pair: 12-13, q at 14
     cpart = tabs + nt;
     double* tk = cpart + 6 * 4096;
     double* tml = tk + ntet;

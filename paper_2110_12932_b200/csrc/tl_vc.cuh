@@ -12,7 +12,7 @@
 //     (A x)_p = diag_p x_p - sum_a (w_a[p] x_{p+e_a} + w_a[p-e_a] x_{p-e_a}).
 // k_vc_assemble computes diag, w and b node by node (gather over the 24 tets touching the
 // node: no atomics, deterministic); k_vc_cg runs the whole Jacobi-PCG in one cooperative
-// launch with fixed-order reductions.  This path is a seam-3
+// launch (two grid barriers per iteration) with fixed-order reductions.  This path is a seam-3
 // solver (host buffers in and out), not the device-resident two-level loop.
 #pragma once
 
@@ -272,19 +272,28 @@ __device__ __forceinline__ double vc_apply(const Grid& g, const double* diag, co
 }
 
 // Jacobi-PCG with scipy's recurrences (solve_linear cg, fem.py:271-298) in ONE cooperative
-// launch: three grid barriers per iteration (r.z and r.r; the new direction p, read by the
-// neighbours' stencils; p.q), every reduction a fixed-order block tree plus a fixed-order
-// sum of the block partials that every CTA performs identically (grid_sum), so all CTAs
-// take the same branch and the result is deterministic.  part: 6 slots of gridDim.x.
+// launch with TWO grid barriers per iteration:
+//   U: x += alpha p, r -= alpha q (the previous iteration's update), z = invd r, partials
+//      of r.r and r.z                                          -> barrier, sums
+//   P: p = z (first) or p beta + z (scipy's two roundings), written to the other buffer
+//      of a ping-pong pair; q = A p with the neighbours' new p recomputed from their z and
+//      old p (bitwise the owners' values), partial of p.q     -> barrier, sum
+// Every reduction is a fixed-order block tree plus a fixed-order sum of the block
+// partials that every CTA performs identically (grid_sum), so all CTAs take the same
+// branch and the result is deterministic.  part: 6 slots of gridDim.x.
 struct VcCg {
     const double *diag, *wx, *wy, *wz, *b;
     const unsigned char* dm;
     const double* g;
-    double *x, *r, *z, *p, *q, *part;
+    double *x, *r, *z, *p, *q, *part;     // p: 2 n (ping-pong)
     double rtol;
     int maxiter;
     SolveInfoDev* info;
 };
+
+__device__ __forceinline__ double vc_pnew(const double* z, const double* pold, double beta, bool first, int j) {
+    return first ? z[j] : __dadd_rn(__dmul_rn(pold[j], beta), z[j]);
+}
 
 __global__ void __launch_bounds__(256) k_vc_cg(Grid G, VcCg C) {
     cg::grid_group grid = cg::this_grid();
@@ -292,6 +301,7 @@ __global__ void __launch_bounds__(256) k_vc_cg(Grid G, VcCg C) {
     __shared__ double tot[2];
     const int n = G.n, NB = gridDim.x, b = blockIdx.x;
     const int t0 = blockIdx.x * blockDim.x + threadIdx.x, ts = gridDim.x * blockDim.x;
+    const int sy = G.NX, sz = G.NX * G.NY;
     // ||b||, x = 0, r = b
     {
         double v[1] = {0.0};
@@ -307,53 +317,61 @@ __global__ void __launch_bounds__(256) k_vc_cg(Grid G, VcCg C) {
     grid.sync();
     { const int s1[1] = {0}; grid_sum<1>(C.part, s1, NB, tot); }
     const double bnorm = sqrt(tot[0]);
-    double rr = tot[0], rho_prev = 1.0;
+    double rr = tot[0], rho_prev = 1.0, alpha = 0.0;
     int it = 0, status = 0;
     if (bnorm > 0.0) {
         const double atol = C.rtol * bnorm;
         status = 1;
-        for (; it < C.maxiter; ++it) {
+        for (; it <= C.maxiter; ++it) {
+            double* pcur = C.p + (size_t)(it & 1) * n;          // p of iteration it-1 (read)
+            double* pnew = C.p + (size_t)((it + 1) & 1) * n;    // p of iteration it (written)
+            // U
+            double v[2] = {0.0, 0.0};
+            for (int i = t0; i < n; i += ts) {
+                double rv = C.r[i];
+                if (it > 0) {
+                    C.x[i] += alpha * pcur[i];
+                    rv = rv - alpha * C.q[i];
+                    C.r[i] = rv;
+                }
+                const double zz = (1.0 / C.diag[i]) * rv;
+                C.z[i] = zz;
+                v[0] += rv * rv;
+                v[1] += rv * zz;
+            }
+            block_sum<2>(v, red);
+            if (threadIdx.x == 0) { C.part[1 * NB + b] = v[0]; C.part[2 * NB + b] = v[1]; }
+            grid.sync();
+            { const int s2[2] = {1, 2}; grid_sum<2>(C.part, s2, NB, tot); }
+            if (it > 0) rr = tot[0];
+            if (it == C.maxiter) { status = 1; break; }      // scipy: no test after the last update
             if (!isfinite(rr)) { status = 3; break; }
             if (sqrt(rr) < atol) { status = 0; break; }
-            // z = invd r; r.z
-            double v[1] = {0.0};
+            const double rho = tot[1];
+            const bool first = it == 0;
+            const double beta = first ? 0.0 : rho / rho_prev;
+            // P
+            double w1[1] = {0.0};
             for (int i = t0; i < n; i += ts) {
-                const double zz = (1.0 / C.diag[i]) * C.r[i];
-                C.z[i] = zz;
-                v[0] += C.r[i] * zz;
+                int ii, jj, kk;
+                decode(G, i, ii, jj, kk);
+                const double pi = vc_pnew(C.z, pcur, beta, first, i);
+                pnew[i] = pi;
+                double y = C.diag[i] * pi;
+                if (ii < G.nc[0]) y -= C.wx[i] * vc_pnew(C.z, pcur, beta, first, i + 1);
+                if (ii > 0) y -= C.wx[i - 1] * vc_pnew(C.z, pcur, beta, first, i - 1);
+                if (jj < G.nc[1]) y -= C.wy[i] * vc_pnew(C.z, pcur, beta, first, i + sy);
+                if (jj > 0) y -= C.wy[i - sy] * vc_pnew(C.z, pcur, beta, first, i - sy);
+                if (kk < G.nc[2]) y -= C.wz[i] * vc_pnew(C.z, pcur, beta, first, i + sz);
+                if (kk > 0) y -= C.wz[i - sz] * vc_pnew(C.z, pcur, beta, first, i - sz);
+                C.q[i] = y;
+                w1[0] += pi * y;
             }
-            block_sum<1>(v, red);
-            if (threadIdx.x == 0) C.part[1 * NB + b] = v[0];
-            grid.sync();
-            { const int s1[1] = {1}; grid_sum<1>(C.part, s1, NB, tot); }
-            const double rho = tot[0];
-            const double beta = it > 0 ? rho / rho_prev : 0.0;
-            for (int i = t0; i < n; i += ts) C.p[i] = it == 0 ? C.z[i] : C.p[i] * beta + C.z[i];
-            grid.sync();
-            // q = A p; p.q
-            v[0] = 0.0;
-            for (int i = t0; i < n; i += ts) {
-                const double qq = vc_apply(G, C.diag, C.wx, C.wy, C.wz, C.p, i);
-                C.q[i] = qq;
-                v[0] += C.p[i] * qq;
-            }
-            block_sum<1>(v, red);
-            if (threadIdx.x == 0) C.part[2 * NB + b] = v[0];
-            grid.sync();
-            { const int s1[1] = {2}; grid_sum<1>(C.part, s1, NB, tot); }
-            const double alpha = rho / tot[0];
-            v[0] = 0.0;
-            for (int i = t0; i < n; i += ts) {
-                C.x[i] += alpha * C.p[i];
-                const double rv = C.r[i] - alpha * C.q[i];
-                C.r[i] = rv;
-                v[0] += rv * rv;
-            }
-            block_sum<1>(v, red);
-            if (threadIdx.x == 0) C.part[3 * NB + b] = v[0];
+            block_sum<1>(w1, red);
+            if (threadIdx.x == 0) C.part[3 * NB + b] = w1[0];
             grid.sync();
             { const int s1[1] = {3}; grid_sum<1>(C.part, s1, NB, tot); }
-            rr = tot[0];
+            alpha = rho / tot[0];
             rho_prev = rho;
         }
     }
