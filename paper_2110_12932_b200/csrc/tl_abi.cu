@@ -708,23 +708,50 @@ int32_t tl_step_host(const tl_grid_desc* grid, double kappa, double rho_c, doubl
     const int n = P.g.n;
     set_coeffs(P, kappa, rho_c, dt);
     const size_t nb = sizeof(double) * n;
-    double *T, *b, *r, *p0, *p1, *q, *dA = nullptr, *dB = nullptr, *dload = nullptr, *part;
-    tl::SolveInfoDev* dinfo;
+    // device workspace kept across calls (the step-level drivers call this once per solve);
+    // one per device, grown on demand, calls serialised.  Sub-arrays start on 256-byte
+    // boundaries and carry the 2-element tail the bulk-copy CG loop may touch.
+    struct StepWs {
+        double* ws = nullptr;
+        size_t cap = 0;
+    };
+    static StepWs wss[64];
+    static std::mutex ws_mu;
+    std::lock_guard<std::mutex> lock(ws_mu);
+    if (dev < 0 || dev >= 64) return fail(TL_E_INVALID, "device ordinal out of range");
+    StepWs& W = wss[dev];
+    const size_t per = ((size_t)n + 2 + 31) / 32 * 32;
+    const size_t npart = ((size_t)4 * sms * 32 + 31) / 32 * 32;
+    const size_t nspec = (sizeof(tl::SolveSpec) + sizeof(tl::SolveInfoDev) + 255) / 256 * 32;
+    const size_t want = 13 * per + npart + nspec;
+    if (want > W.cap) {
+        if (W.ws) cudaFree(W.ws);
+        W.ws = nullptr;
+        W.cap = 0;
+        TL_CUDA(cudaMalloc((void**)&W.ws, sizeof(double) * want));
+        W.cap = want;
+    }
+    double* T = W.ws;
+    double* b = W.ws + per;
+    double* r = W.ws + 2 * per;
+    double* p0 = W.ws + 3 * per;
+    double* p1 = W.ws + 4 * per;
+    double* q = W.ws + 5 * per;
+    double* dA = gA ? W.ws + 6 * per : nullptr;
+    double* dB = gA ? W.ws + 7 * per : nullptr;
+    double* dload = load ? W.ws + 8 * per : nullptr;
+    double* xg = W.ws + 9 * per;                       // 4 per
+    double* part = W.ws + 13 * per;
+    tl::SolveSpec* dspec = reinterpret_cast<tl::SolveSpec*>(W.ws + 13 * per + npart);
+    tl::SolveInfoDev* dinfo = reinterpret_cast<tl::SolveInfoDev*>(
+        reinterpret_cast<char*>(dspec) + (sizeof(tl::SolveSpec) + 15) / 16 * 16);
     int rc = 0;
-    if ((rc = dalloc(&T, n)) || (rc = dalloc(&b, n)) || (rc = dalloc(&r, n)) || (rc = dalloc(&p0, n)) ||
-        (rc = dalloc(&p1, n)) || (rc = dalloc(&q, n)) || (rc = dalloc(&part, 4 * sms * 32)) ||
-        (rc = dalloc(&dinfo, 1)))
-        return rc;
     TL_CUDA(cudaMemcpy(T, T_old, nb, cudaMemcpyHostToDevice));
     if (gA) {
-        if ((rc = dalloc(&dA, n)) || (rc = dalloc(&dB, n))) return rc;
         TL_CUDA(cudaMemcpy(dA, gA, nb, cudaMemcpyHostToDevice));
         TL_CUDA(cudaMemcpy(dB, gB ? gB : gA, nb, cudaMemcpyHostToDevice));
     }
-    if (load) {
-        if ((rc = dalloc(&dload, n))) return rc;
-        TL_CUDA(cudaMemcpy(dload, load, nb, cudaMemcpyHostToDevice));
-    }
+    if (load) TL_CUDA(cudaMemcpy(dload, load, nb, cudaMemcpyHostToDevice));
     P.T = T; P.gA = dA; P.gB = dB; P.w = gA ? w : 0.0; P.g_const = g_const; P.load = dload;
     P.b = b; P.r = r; P.p0 = p0; P.p1 = p1; P.q = q; P.part = part;
     P.rtol = rtol; P.maxiter = maxiter; P.info = dinfo;
@@ -734,9 +761,6 @@ int32_t tl_step_host(const tl_grid_desc* grid, double kappa, double rho_c, doubl
         for (int a = 0; a < 3; ++a) P.src.center[a] = src->center[a];
         P.src.on = 1;
     }
-    double* xg = nullptr;
-    tl::SolveSpec* dspec = nullptr;
-    if ((rc = dalloc(&xg, 4 * (size_t)n)) || (rc = dalloc(&dspec, 1))) return rc;
     rc = launch_solve(P, gauss, sms, xg, 0, nullptr, dspec);
     if (rc) return rc;
     TL_CUDA(cudaDeviceSynchronize());
@@ -747,8 +771,6 @@ int32_t tl_step_host(const tl_grid_desc* grid, double kappa, double rho_c, doubl
         info->iterations = hi.iterations; info->status = hi.status; info->bnorm = hi.bnorm;
         info->rnorm = hi.rnorm; info->true_resid = hi.true_resid;
     }
-    cudaFree(T); cudaFree(b); cudaFree(r); cudaFree(p0); cudaFree(p1); cudaFree(q); cudaFree(part);
-    cudaFree(dinfo); cudaFree(xg); cudaFree(dspec); if (dA) cudaFree(dA); if (dB) cudaFree(dB); if (dload) cudaFree(dload);
     return TL_OK;
 }
 
