@@ -1017,6 +1017,31 @@ static int transmission_impl(const tl_grid_desc* global_grid, const tl_grid_desc
                              const double* local_values, double jump, const double* kg_T, const double* kg_v,
                              int32_t nkg, const double* kl_T, const double* kl_v, int32_t nkl, double* load_out);
 
+// Per-device scratch buffers reused across calls of the interface helpers (grown on demand,
+// never shrunk); the caller holds g_scratch_mu for the whole call.
+static std::mutex g_scratch_mu;
+struct Scratch {
+    void* p = nullptr;
+    size_t cap = 0;
+};
+static Scratch g_scratch[64][4];
+
+static int scratch(int slot, size_t bytes, void** out) {
+    int dev = 0;
+    TL_CUDA(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64) return fail(TL_E_INVALID, "device ordinal out of range");
+    Scratch& sc = g_scratch[dev][slot];
+    if (bytes > sc.cap) {
+        if (sc.p) cudaFree(sc.p);
+        sc.p = nullptr;
+        sc.cap = 0;
+        TL_CUDA(cudaMalloc(&sc.p, bytes));
+        sc.cap = bytes;
+    }
+    *out = sc.p;
+    return TL_OK;
+}
+
 int32_t tl_overlap_feedback_host(const tl_grid_desc* global_grid, const tl_grid_desc* local_grid,
                                  const double* local_new, const double* local_old, double dt,
                                  const tl_vc_material* mat_global, const tl_vc_material* mat_local,
@@ -1027,12 +1052,16 @@ int32_t tl_overlap_feedback_host(const tl_grid_desc* global_grid, const tl_grid_
     tl::Grid G{}, L{};
     if (int rc = make_grid(*global_grid, tl::kBottom, G)) return rc;
     if (int rc = make_grid(*local_grid, tl::kGamma, L)) return rc;
-    double *dn, *dold, *dload, *tabs;
     const int ng = 2 * (mat_global->nk + mat_global->nc), nl = 2 * (mat_local->nk + mat_local->nc);
+    std::lock_guard<std::mutex> lock(g_scratch_mu);
+    const size_t pl = ((size_t)L.n + 31) / 32 * 32, pg = ((size_t)G.n + 31) / 32 * 32;
+    void* dbl = nullptr;
     int rc = 0;
-    if ((rc = dalloc(&dn, L.n)) || (rc = dalloc(&dold, L.n)) || (rc = dalloc(&dload, G.n)) ||
-        (rc = dalloc(&tabs, ng + nl)))
-        return rc;
+    if ((rc = scratch(3, sizeof(double) * (2 * pl + pg + ng + nl), &dbl))) return rc;
+    double* dn = static_cast<double*>(dbl);
+    double* dold = dn + pl;
+    double* dload = dold + pl;
+    double* tabs = dload + pg;
     TL_CUDA(cudaMemcpy(dn, local_new, sizeof(double) * L.n, cudaMemcpyHostToDevice));
     TL_CUDA(cudaMemcpy(dold, local_old, sizeof(double) * L.n, cudaMemcpyHostToDevice));
     auto upload = [&](const tl_vc_material* m, double* at, tl::VcMat& M) -> int {
@@ -1055,7 +1084,6 @@ int32_t tl_overlap_feedback_host(const tl_grid_desc* global_grid, const tl_grid_
     tl::k_overlap_feedback<<<296, 256>>>(G, L, dn, dold, dt, Mg, Ml, S, dload);
     TL_CUDA(cudaGetLastError());
     TL_CUDA(cudaMemcpy(load_out, dload, sizeof(double) * G.n, cudaMemcpyDeviceToHost));
-    cudaFree(dn); cudaFree(dold); cudaFree(dload); cudaFree(tabs);
     return TL_OK;
 }
 
@@ -1083,18 +1111,25 @@ static int transmission_impl(const tl_grid_desc* global_grid, const tl_grid_desc
                                 (long long)L.nc[0] * L.nc[1]);
     const long long ne = 12 * nf;
     if (ne >= (1ll << 31)) return fail(TL_E_INVALID, "interface too large");
-    double *dT, *dvals, *dload;
-    int *keys, *keys2, *idx, *idx2;
+    std::lock_guard<std::mutex> lock(g_scratch_mu);
+    const size_t pl = ((size_t)L.n + 31) / 32 * 32, pe = ((size_t)ne + 31) / 32 * 32, pg = ((size_t)G.n + 31) / 32 * 32;
+    const size_t pt = ((size_t)2 * (nkg + nkl) + 31) / 32 * 32;
+    void *dbl = nullptr, *ints = nullptr;
     int rc = 0;
-    if ((rc = dalloc(&dT, L.n)) || (rc = dalloc(&dvals, ne)) || (rc = dalloc(&dload, G.n)) ||
-        (rc = dalloc(&keys, ne)) || (rc = dalloc(&keys2, ne)) || (rc = dalloc(&idx, ne)) || (rc = dalloc(&idx2, ne)))
+    if ((rc = scratch(0, sizeof(double) * (pl + pe + pg + pt), &dbl)) || (rc = scratch(1, sizeof(int) * 4 * pe, &ints)))
         return rc;
+    double* dT = static_cast<double*>(dbl);
+    double* dvals = dT + pl;
+    double* dload = dvals + pe;
+    int* keys = static_cast<int*>(ints);
+    int* keys2 = keys + pe;
+    int* idx = keys2 + pe;
+    int* idx2 = idx + pe;
     TL_CUDA(cudaMemcpy(dT, local_values, sizeof(double) * L.n, cudaMemcpyHostToDevice));
     TL_CUDA(cudaMemset(dload, 0, sizeof(double) * G.n));
-    double* dtab = nullptr;
+    double* dtab = dload + pg;
     tl::KTab kg{nullptr, nullptr, 0}, kl{nullptr, nullptr, 0};
     if (nkg > 0) {
-        if ((rc = dalloc(&dtab, 2 * (nkg + nkl)))) return rc;
         TL_CUDA(cudaMemcpy(dtab, kg_T, sizeof(double) * nkg, cudaMemcpyHostToDevice));
         TL_CUDA(cudaMemcpy(dtab + nkg, kg_v, sizeof(double) * nkg, cudaMemcpyHostToDevice));
         TL_CUDA(cudaMemcpy(dtab + 2 * nkg, kl_T, sizeof(double) * nkl, cudaMemcpyHostToDevice));
@@ -1109,14 +1144,11 @@ static int transmission_impl(const tl_grid_desc* global_grid, const tl_grid_desc
     size_t tmp_bytes = 0;
     TL_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys2, idx, idx2, (int)ne, 0, bits));
     void* tmp = nullptr;
-    TL_CUDA(cudaMalloc(&tmp, tmp_bytes));
+    if ((rc = scratch(2, tmp_bytes + 256, &tmp))) return rc;
     TL_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys2, idx, idx2, (int)ne, 0, bits));
     tl::k_trans_segsum<<<296, 256>>>(keys2, idx2, dvals, (int)ne, dload);
     TL_CUDA(cudaGetLastError());
     TL_CUDA(cudaMemcpy(load_out, dload, sizeof(double) * G.n, cudaMemcpyDeviceToHost));
-    cudaFree(tmp); cudaFree(dT); cudaFree(dvals); cudaFree(dload);
-    cudaFree(keys); cudaFree(keys2); cudaFree(idx); cudaFree(idx2);
-    if (dtab) cudaFree(dtab);
     return TL_OK;
 }
 
