@@ -28,12 +28,11 @@ import threading
 import time
 from pathlib import Path
 
-# the CPU baseline leg of our arm is single-threaded (a 1-core port timing); the reference
-# arm runs with the library defaults, i.e. every host thread BLAS can use
-_REFERENCE_ARM = "--impl=reference" in sys.argv or (
-    "--impl" in sys.argv and sys.argv[sys.argv.index("--impl") + 1:][:1] == ["reference"])
-if not _REFERENCE_ARM:
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+# Both CPU legs run the reference's algorithm single-threaded: its sparse CG (where the
+# time goes) is single-threaded scipy, and BLAS threading only slows the small dense
+# products down (measured here 35k vs 42k DOF-timesteps/s with 8 vs 1
+# OpenBLAS threads on the cfg4 sample) — one thread is the reference's best configuration.
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
@@ -111,27 +110,57 @@ def cpu_sample(cfg_path, what: str = "global+local"):
     """Reference CPU algorithm (oracle/assembly.py, bitwise-pinned port) on a bounded sample.
     ``cfg_path``: a .cfg file or an already built ExperimentConfig."""
     import paper_2110_12932_b200 as P
-    from oracle import kuhn
-    from oracle.twolevel import OracleRun
     cfg = P.load_config(cfg_path) if isinstance(cfg_path, (str, Path)) else cfg_path
-    run = OracleRun(cfg, backend="assembly")
-    Tg = np.full(run.G.n_nodes, cfg.T_initial)
-    L = kuhn.KuhnGrid.from_placement(run.placement0)
-    Tl = kuhn.interpolate(run.G, Tg, L.coords())
-    sched = P.MacroSchedule(cfg.dt_macro, cfg.micro_steps, 0.0, cfg.t_end)
-    t0 = time.perf_counter()
-    dof = 0
-    if "global" in what:
-        Tg2 = run.solve_global(Tg, 0.0, cfg.dt_macro)
-        dof += run.G.n_nodes
-    else:
-        Tg2 = Tg
-    trace = run.trace_of(L, Tg2)
-    w = 1.0 / sched.micro_per_macro
-    run.solve_local(L, Tl, 0.0, sched.t_micro(0, 1), (1.0 - w) * run.trace_of(L, Tg) + w * trace)
-    dof += L.n_nodes
-    dt = time.perf_counter() - t0
-    return dof, dt, run.iterations, (run.G.n_nodes, L.n_nodes, sched.micro_per_macro)
+    smp = LocalSample(cfg, with_global="global" in what)
+    return smp.once()
+
+
+class LocalSample:
+    """A bounded sample of a config's two-level step for the CPU port (oracle/assembly.py:
+    the reference's own algorithm — explicit Kuhn tets, einsum element matrices, COO->CSR,
+    symmetric Dirichlet elimination, scipy CG — bitwise equal to lpbfsim): one local micro
+    solve (the first micro interval of macro step 0, uniform initial field; trace blend and
+    Gaussian as run_spacetime has them) and optionally the global predictor before it.
+
+    ``window``: lateral node count of a column cut out of the config's local grid (same h,
+    same depth, same beam position relative to the box) when the whole local grid is too
+    large for a bounded CPU sample (cfg4: 251 x 251 x 101 nodes)."""
+
+    def __init__(self, cfg, with_global: bool = False, window: int | None = None):
+        import dataclasses
+        import paper_2110_12932_b200 as P
+        from oracle import kuhn
+        from oracle.twolevel import OracleRun
+        if window is not None:
+            pol = cfg.policy
+            size = (window - 1) * cfg.h_local
+            cfg = dataclasses.replace(cfg, policy=dataclasses.replace(
+                pol, box_size=(size, size) + tuple(pol.box_size[2:])))
+        self.cfg, self.with_global = cfg, with_global
+        self.run = OracleRun(cfg, backend="assembly")
+        self.L = kuhn.KuhnGrid.from_placement(self.run.placement0)
+        self.Tg = np.full(self.run.G.n_nodes, cfg.T_initial) if with_global else None
+        self.Tl = np.full(self.L.n_nodes, cfg.T_initial)
+        self.sched = P.MacroSchedule(cfg.dt_macro, cfg.micro_steps, 0.0, cfg.t_end)
+        self.trace0 = np.where(self.L.gamma_mask().ravel(), float(cfg.T_initial), 0.0)   # P1(uniform) on gamma
+        self.shape = tuple(int(c) + 1 for c in self.run.placement0.ncells)
+
+    def once(self):
+        run, L, sched = self.run, self.L, self.sched
+        t0 = time.perf_counter()
+        dof = 0
+        if self.with_global:
+            Tg2 = run.solve_global(self.Tg, 0.0, self.cfg.dt_macro)
+            dof += run.G.n_nodes
+            trace = run.trace_of(L, Tg2)
+            told = run.trace_of(L, self.Tg)
+        else:
+            trace = told = self.trace0          # uniform field: P1 of a constant
+        w = 1.0 / sched.micro_per_macro
+        run.solve_local(L, self.Tl, 0.0, sched.t_micro(0, 1), (1.0 - w) * told + w * trace)
+        dof += L.n_nodes
+        dt = time.perf_counter() - t0
+        return dof, dt, run.iterations, (run.G.n_nodes, L.n_nodes, sched.micro_per_macro)
 
 
 def _host_threads() -> int:
@@ -141,37 +170,82 @@ def _host_threads() -> int:
         return os.cpu_count() or 1
 
 
+def _cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# CPU sample size per config: lateral nodes of the local-grid column (None: whole local grid)
+# for our arm's 1-core cpu_baseline (~10-30 s) and for each step of the reference arm
+# (~2-5 s, so --steps 20 --warmup 5 ends within a few minutes)
+CPU_WINDOW = {"cfg4": (126, 48), "cfg3": (None, 80), "cfg2": (None, None)}
+
+
+def workload(args, world: int):
+    """The bench workload both arms report: config dict, grid sizes, DOF per step."""
+    import paper_2110_12932_b200 as P
+    from paper_2110_12932_b200.control import initial_local_box, structured_ncells
+    cfg = P.load_config(ROOT / "configs" / f"{args.config}.cfg")
+    gn = structured_ncells(cfg.global_box, cfg.h_global)
+    lbox = initial_local_box(cfg.global_box, cfg.h_local, cfg.policy, cfg.path)
+    ln = structured_ncells(lbox, cfg.h_local)
+    Ng, Nl = int(np.prod(np.asarray(gn) + 1)), int(np.prod(np.asarray(ln) + 1))
+    m = int(cfg.micro_steps)
+    dof_step = Ng + m * Nl
+    first = args.skip + args.warmup
+    conf = {"workload": f"{args.config}: two-level multirate macro step (1 global + {m} local solves + "
+                        f"corrector), global {Ng} + local {Nl} nodes",
+            "config_file": f"configs/{args.config}.cfg", "dof_timesteps_per_step": dof_step,
+            "macro_steps": f"{first}..{first + args.steps - 1}",
+            "l2": ("inputs larger than L2 and flushed between timed steps" if Ng * 8 > 126e6
+                   else "flushed between timed steps") if not args.no_flush else "not flushed",
+            "parallelism": f"scenario replicas x{world}" if world > 1 else "single GPU"}
+    return cfg, conf, (Ng, Nl, m)
+
+
 def reference_arm(args):
+    """--impl reference: the reference's CPU algorithm (the literal P1-assembly + scipy-CG
+    port, bitwise equal to lpbfsim) on the host cores, rank 0 only; same metric, unit and
+    config as the device arm; each timed step is a bounded sample of the workload."""
     rank, world, _ = env_rank()
     if rank != 0:
         return
-    cfg_path = ROOT / "configs" / f"{args.config}.cfg"
+    cfg, conf, (Ng, Nl, m) = workload(args, world)
+    win = CPU_WINDOW.get(args.config, (None, None))[1]
     if args.config == "cfg5":                 # config 5: a sample of its first scenario
         from paper_2110_12932_b200 import scenarios as S
-        cfg_path = S.draw(0, 64)[0].config()
+        cfg = S.draw(0, 64)[0].config()
+    smp = LocalSample(cfg, with_global=False, window=win)
     times, dofs = [], []
     for s in range(args.warmup + args.steps):
-        dof, dt, _, (Ng, Nl, m) = cpu_sample(cfg_path, what="local")
+        dof, dt, _, _ = smp.once()
         if s >= args.warmup:
             times.append(dt)
             dofs.append(dof)
     total = sum(times)
     value = sum(dofs) / total
+    what = (f"one {args.config} local micro solve (first micro interval, uniform initial field) on "
+            + (f"a {smp.shape[0]}x{smp.shape[1]}x{smp.shape[2]}-node column of the {args.config} local grid "
+               f"(same h and depth; the whole {Nl}-node local grid would take minutes per sample)"
+               if win else f"the whole {smp.shape[0]}x{smp.shape[1]}x{smp.shape[2]} local grid")
+            + f", {smp.L.n_nodes} DOF-timesteps")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "timed_step": what + "; ms_per_step is the time of that sample, value its DOF-timesteps/s",
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": f"synthetic (BASELINE {args.config} geometry; uniform initial field, first micro step)",
-        # the same workload as the device arm; each timed step is a bounded sample of it
-        "config": {"workload": f"{args.config}: two-level multirate macro step (1 global + {m} local "
-                               f"solves + corrector), global {Ng} + local {Nl} nodes",
-                   "config_file": f"configs/{args.config}.cfg", "dof_timesteps_per_step": Ng + m * Nl,
-                   "parallelism": "host CPU"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": _host_threads(), "kind": "port",
-                         "sample": f"one {args.config} local micro solve ({Nl} DOF-timesteps) per timed step via the literal "
-                                   "P1-assembly + scipy-CG port (oracle/assembly.py, bitwise equal to lpbfsim); "
-                                   "library-default threading (BLAS may use every host thread; scipy's sparse "
-                                   "CG itself is single-threaded)"},
+        "data": f"synthetic (BASELINE {args.config} geometry and scan path)",
+        "config": conf,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
+                         "sample": what + " per timed step via the literal P1-assembly + scipy-CG port "
+                                   "(oracle/assembly.py, bitwise equal to lpbfsim); one thread: the reference is "
+                                   "one sequential process (scipy's sparse CG is single-threaded) and BLAS threads "
+                                   f"only slow it down; host: {_cpu_model()}, {_host_threads()} threads available"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -587,37 +661,15 @@ def picard_bench(args):
                 "note": "host wall clock around fem.step_backward_euler (the seam takes host arrays: T_old, "
                         "Dirichlet values and mask up, the converged field down, the Picard loop in between "
                         "on the device); value is the same"},
-        "gpu_launches": int(passes * 7 - 2 * args.steps), "clocks": clocks.summary(),
+        "gpu_launches": int(passes * 7 - args.steps), "clocks": clocks.summary(),
     }
     print(json.dumps(line), flush=True)
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2")
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-flush", action="store_true")
-    ap.add_argument("--skip", type=int, default=0, help="macro steps to run before warm-up")
-    ap.add_argument("--slabs", action="store_true",
-                    help="global grid split into z-slabs over the ranks (default config cfg4)")
-    ap.add_argument("--scenarios", type=int, default=64,
-                    help="cfg5: how many of the 64 seed-0 scenarios to run (split over the ranks)")
-    args = ap.parse_args()
-    if args.warmup < 3 and args.impl == "ours":
-        args.warmup = 3
-    if args.impl == "reference":
-        return reference_arm(args)
-    if args.slabs:
-        return slab_bench(args)
-    if args.config == "cfg5":
-        return scenario_bench(args)
-    if args.config == "picard":
-        return picard_bench(args)
-
+def device_arm(args):
+    """Our arm at N = 1 (and scenario replicas at N > 1): ``value`` from per-step CUDA events
+    around DeviceRun.run on the run's stream (inputs resident, L2 flushed between steps);
+    ``e2e`` through the public ``run_spacetime`` (recorder=None) over a K-step schedule."""
     import torch
     import paper_2110_12932_b200 as P
     from paper_2110_12932_b200.schedule import plan_spacetime
@@ -629,18 +681,16 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
 
-    cfg_path = ROOT / "configs" / f"{args.config}.cfg"
-    cfg = P.load_config(cfg_path)
+    cfg, conf, (Ng, Nl, m) = workload(args, world)
     problem, lmesh = P.build_problem(cfg, device=local_rank)
     sched = P.MacroSchedule(cfg.dt_macro, cfg.micro_steps, 0.0, cfg.t_end)
-    m = sched.micro_per_macro
-    Ng, Nl = problem.global_mesh.n_nodes, lmesh.n_nodes
+    assert (problem.global_mesh.n_nodes, lmesh.n_nodes, sched.micro_per_macro) == (Ng, Nl, m)
     dof_step = Ng + m * Nl
     nsteps = args.skip + args.warmup + args.steps
     if nsteps > sched.n_macro:
         raise SystemExit(f"{args.config} has only {sched.n_macro} macro steps")
 
-    # per-step plans (host, outside the timed region)
+    # per-step plans (host, outside the timed region of `value`)
     plans = []
     placement, tg, tl = lmesh.placement, 0.0, 0.0
     for k in range(nsteps):
@@ -677,34 +727,26 @@ def main():
         wall = time.perf_counter() - wall0
     torch.cuda.synchronize()
     launches = run.launch_count() - launches0
-    step_ms = [a.elapsed_time(b) for a, b in ev]
-    dev_ms = float(sum(step_ms))
+    dev_ms = float(sum(a.elapsed_time(b) for a, b in ev))
     infos = run.take_info()
     run.check_solves(infos)
     kt = run.take_timing()
     run.set_timing(False)
+    run.close()
     if dist is not None:
         t = torch.tensor([dev_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dev_ms = float(t.item())
-
     value = dof_step * len(timed) * world / (dev_ms / 1e3)
 
-    # ---- roofline of the dominant kernel (k_pcg on the local grid) ----
+    # ---- roofline of the dominant kernel ----
     peak, peak_src = measured_peak()
-    # pair each timed launch with the solve records it produced (a persistent local
-    # launch runs all micro solves + corrector of a macro step)
     loc, glo = split_timing(kt, infos)
     share_ms = dev_ms if world == 1 else None
     kloc, kglo = kernel_stats(loc, Nl, share_ms), kernel_stats(glo, Ng, share_ms)
-    # the dominant kernel: the level whose solves take the larger share of the step
     lev = "global" if kglo and (not kloc or sum(t for t, _ in glo) > sum(t for t, _ in loc)) else "local"
     kdom, ndom = (kglo, Ng) if lev == "global" else (kloc, Nl)
-    streaming = "k_s_rhs -> k_t_cg (bulk-copy z-march CG loop, grids of 20M+ nodes) or k_s_cg -> k_s_resid -> k_s_final"
-    kname = {"local": ("local-grid PCG solve: k_pcg_resident_cg (SMEM-resident bricks, all micro solves + corrector "
-                       "of a macro step in one launch) where the grid fits on chip, else the streaming " + streaming),
-             "global": "global-grid PCG solve: k_pcg_resident(_cg) where the grid fits on chip, else the streaming "
-                       + streaming}[lev]
+    kname = kernel_name(problem, lev, Ng if lev == "global" else Nl)
     traffic, tnote = None, None
     tfile = ROOT / "profiles" / "traffic.json"
     if tfile.exists():
@@ -719,83 +761,35 @@ def main():
             tnote = f"ncu DRAM/algorithmic = {dram / alg:.3f} ({tj.get(f'{args.config}_{lev}_pcg_kernel', '')})"
     roofline = {"bound": "hbm", "achieved": kdom["achieved_gbs"], "peak": peak, "unit": "GB/s",
                 "frac": kdom["achieved_gbs"] / peak, "traffic": traffic, "traffic_note": tnote,
-                "kernel": kname, "level": lev, "nodes": ndom,
-                "peak_source": peak_src,
-                "note": "algorithmic bytes N(64k+32) per solve (SURVEY §8d); cfg2 vectors are L2-resident"}
+                "kernel": kname, "level": lev, "nodes": ndom, "peak_source": peak_src,
+                "note": "algorithmic bytes N(64k+32) per solve (SURVEY §8d) / the solve launches' CUDA-event "
+                        "time on the run's stream"}
 
-    # ---- e2e through the public API: pinned plan upload + field read-back every step ----
-    e2e = None
-    if rank == 0 or True:
-        pin_local = torch.empty(Nl, dtype=torch.float64, pin_memory=True).numpy()
-        e2e_plans = []
-        for pl in timed:
-            pinned = {}
-            for key in ("macro", "micro"):
-                arr = getattr(pl, key)
-                buf = torch.empty(arr.nbytes, dtype=torch.uint8, pin_memory=True).numpy().view(arr.dtype)
-                buf[:] = arr
-                pinned[key] = buf
-            for key in ("dep_points", "dep_power"):
-                arr = np.ascontiguousarray(getattr(pl, key), dtype=np.float64).reshape(-1)
-                buf = torch.empty(max(arr.size, 1), dtype=torch.float64, pin_memory=True).numpy()[:arr.size]
-                buf[:] = arr
-                pinned[key] = buf
-            e2e_plans.append(pinned)
-        # restart from the state after the timed region would differ; rewind a fresh run
-        run2 = P.DeviceRun(problem, lmesh)
-        run2.initial(P.uniform_field(problem.global_mesh, cfg.T_initial))
-        for k in range(args.skip + args.warmup):
-            run2.run(plans[k])
-        run2.sync()
-        h2d = d2h = 0
-        # pipelined read-back: step s's local field goes to pinned buffer s % 2 on a copy
-        # stream while step s+1 computes; the host waits for step s-1's field after
-        # enqueueing step s, and for the last one before the clock stops
-        pins = [pin_local, torch.empty(Nl, dtype=torch.float64, pin_memory=True).numpy()]
-        for k in range(2):                       # staging buffers allocated before the clock
-            run2.field_async(1, pins[k], slot=k)
-            run2.field_wait(k)
-        t0 = time.perf_counter()
-        for s, (pl, pin) in enumerate(zip(timed, e2e_plans)):
-            pl2 = type(pl)(macro=pin["macro"], micro=pin["micro"],
-                           dep_points=pin["dep_points"].reshape(-1, 3), dep_power=pin["dep_power"])
-            run2.run(pl2)
-            run2.field_async(1, pins[s % 2], slot=s % 2)
-            if s >= 1:
-                run2.field_wait((s - 1) % 2)
-            h2d += pin["macro"].nbytes + pin["micro"].nbytes + pin["dep_points"].nbytes + pin["dep_power"].nbytes
-            d2h += pins[s % 2].nbytes
-        run2.field_wait((len(timed) - 1) % 2)
-        e2e_s = time.perf_counter() - t0
-        run2.check_solves(run2.take_info())
-        run2.close()
-        e2e = {"value": dof_step * len(timed) * world / e2e_s, "unit": UNIT,
-               "h2d_bytes_per_step": h2d // len(timed), "d2h_bytes_per_step": d2h // len(timed),
-               "note": "host wall clock through DeviceRun.run per macro step: plan arrays from pinned "
-                       "memory H2D, local field (the melt-pool grid) D2H to pinned memory every step "
-                       "(DeviceRun.field_async, double-buffered: overlapped with the next step; "
-                       "the last step's field is waited for inside the timed region)"}
-    run.close()
+    # ---- e2e through the public API: run_spacetime(recorder=None) over a K-step schedule ----
+    e2e = e2e_run_spacetime(args, cfg, problem, lmesh, dof_step, world, local_rank)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        dof, dt, its, _ = cpu_sample(cfg_path)
+        win = CPU_WINDOW.get(args.config, (None, None))[0]
+        smp = LocalSample(cfg, with_global=win is None, window=win)
+        dof, dt, _, _ = smp.once()
+        what = ("one global + one local implicit step" if win is None else
+                f"one local micro solve on a {smp.shape[0]}x{smp.shape[1]}x{smp.shape[2]}-node column of the "
+                f"{args.config} local grid (same h and depth)")
+        note = "" if win is None else (f"; the {Ng}-node global solve is infeasible on the CPU port (SURVEY §8d: "
+                                       "cfg3's global mesh alone needed 55.8 GB and 87-149 s per step)"
+                                       if args.config == "cfg4" else "")
         cpu = {"value": dof / dt, "unit": UNIT, "cores": 1, "kind": "port",
-               "sample": f"one global + one local implicit step of {args.config} ({dof} DOF-timesteps, "
-                         f"{dt:.1f} s) via the literal P1-assembly + scipy-CG port (oracle/assembly.py, "
-                         "bitwise equal to lpbfsim); OPENBLAS_NUM_THREADS=1"}
+               "sample": f"{what} of {args.config} ({dof} DOF-timesteps, {dt:.1f} s) via the literal P1-assembly + "
+                         "scipy-CG port (oracle/assembly.py, bitwise equal to lpbfsim); OPENBLAS_NUM_THREADS=1"
+                         + note + f"; host CPU: {_cpu_model()}"}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": len(timed),
         "warmup": args.warmup, "ms_per_step": dev_ms / len(timed), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (BASELINE config 2 scan path and geometry; no dataset involved)",
-        "config": {"workload": f"{args.config}: two-level multirate macro step (1 global + {m} local "
-                               f"solves + corrector), global {Ng} + local {Nl} nodes",
-                   "config_file": f"configs/{args.config}.cfg", "dof_timesteps_per_step": dof_step,
-                   "macro_steps": f"{args.skip + args.warmup}..{nsteps - 1}",
-                   "l2": "flushed between timed steps" if not args.no_flush else "not flushed",
-                   "parallelism": f"scenario replicas x{world}" if world > 1 else "single GPU"},
+        "data": f"synthetic (BASELINE {args.config} scan path and geometry; no dataset involved)",
+        "config": conf,
         "roofline": roofline, "kernels": {"local_pcg": kloc, "global_pcg": kglo},
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         "clocks": clocks.summary(), "wall_s_timed_region": wall,
@@ -807,6 +801,93 @@ def main():
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def kernel_name(problem, level: str, n: int) -> str:
+    tiled = "k_s_rhs -> k_t_cg (bulk-copy z-march CG loop) -> k_s_resid -> k_s_final"
+    flat = "k_s_rhs -> k_s_cg (flat streaming CG loop) -> k_s_resid -> k_s_final"
+    if n >= 20_000_000:
+        return f"{level}-grid PCG solve: {tiled}"
+    if n >= 1_000_000:
+        return f"{level}-grid PCG solve: {flat} (k_t_cg from 20M nodes)"
+    if level == "local":
+        return ("local-grid PCG solves: k_pcg_resident_cg (SMEM-resident bricks, all micro solves + corrector "
+                "of a macro step in one launch)")
+    return "global-grid PCG solve: k_pcg_resident_cg (SMEM-resident bricks, x in global memory)"
+
+
+def e2e_run_spacetime(args, cfg, problem, lmesh, dof_step, world, local_rank):
+    """Wall clock of the public call a user makes, ``run_spacetime(problem, schedule,
+    local_mesh, T0, path, policy, recorder=None)`` over a K-macro-step schedule from the
+    initial state: host planning (overlapped with the device by windows), the plan arrays
+    H2D every step, the device run, every step's solve records D2H (checked against
+    non-convergence), the final local field and trace D2H (the global field stays on the
+    device until read: DeviceFieldState).  One untimed call over W steps first (allocation,
+    setup caches); the device run is reused from the driver's pool."""
+    import torch
+    import paper_2110_12932_b200 as P
+    from paper_2110_12932_b200 import multirate as MR
+    T0 = P.uniform_field(problem.global_mesh, cfg.T_initial)
+    K, W = args.steps, max(1, args.warmup)
+    warm = MR.MacroSchedule(cfg.dt_macro, cfg.micro_steps, 0.0, W * cfg.dt_macro)
+    st = P.run_spacetime(problem, warm, lmesh, T0, path=cfg.path, policy=cfg.policy)
+    del st
+    sched = MR.MacroSchedule(cfg.dt_macro, cfg.micro_steps, 0.0, K * cfg.dt_macro)
+    stats = P.RunStats()
+    pooled = list(MR._POOL.values())
+    for r in pooled:
+        r.h2d_bytes = r.d2h_bytes = 0
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    state = P.run_spacetime(problem, sched, lmesh, T0, path=cfg.path, policy=cfg.policy, stats=stats,
+                            recorder=None)
+    lv = state.local_field.values
+    e2e_s = time.perf_counter() - t0
+    assert np.isfinite(lv).all() and stats.counters["global_solves"] == K
+    h2d = sum(r.h2d_bytes for r in MR._POOL.values()) // K
+    d2h = sum(r.d2h_bytes for r in MR._POOL.values()) // K
+    del state
+    MR.release_device_runs()
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([e2e_s], device=torch.device("cuda", local_rank), dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    return {"value": dof_step * K * world / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "seconds": e2e_s, "steps": K,
+            "note": f"host wall clock (max over ranks) of one public run_spacetime(..., recorder=None) call over a "
+                    f"{K}-macro-step schedule from the initial state (macro steps 0..{K - 1}; value times steps "
+                    f"{args.skip + args.warmup}..): host planning overlapped with the device in windows, the plan "
+                    "arrays (macro/micro records, <=144 deposit samples) H2D every step, the solve records D2H and "
+                    "checked, the final local field + trace D2H; the global field stays device-resident until read"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg4")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--skip", type=int, default=0, help="macro steps to run before warm-up")
+    ap.add_argument("--slabs", action="store_true",
+                    help="global grid split into z-slabs over the ranks (default config cfg4)")
+    ap.add_argument("--scenarios", type=int, default=64,
+                    help="cfg5: how many of the 64 seed-0 scenarios to run (split over the ranks)")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        return reference_arm(args)
+    if args.slabs:
+        return slab_bench(args)
+    if args.config == "cfg5":
+        return scenario_bench(args)
+    if args.config == "picard":
+        return picard_bench(args)
+    return device_arm(args)
 
 
 if __name__ == "__main__":

@@ -254,7 +254,8 @@ int32_t tl_deposit_host(const tl_grid_desc* grid, const double* points, const do
 int32_t tl_run_create(const tl_run_desc* desc, tl_run** out);
 int32_t tl_run_destroy(tl_run* run);
 /* initial_state (twolevel.py:145-156): global = T0 everywhere, local = P1(global),
- * trace = P1(global) on gamma. */
+ * trace = P1(global) on gamma.  Resets the local box to the initial placement of the
+ * run's descriptor, so a run can be reused for another schedule of the same problem. */
 int32_t tl_run_initial(tl_run* run, double T0);
 /* Upload a global field and re-derive local field + trace (initial_state with a
  * non-uniform T0). */

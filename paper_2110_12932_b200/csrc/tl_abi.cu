@@ -11,7 +11,10 @@
 // All state stays on the device; the host only enqueues launches.
 #include <cub/cub.cuh>
 #include <algorithm>
+#include <initializer_list>
+#include <map>
 #include <mutex>
+#include <utility>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -25,6 +28,23 @@
 #include "tl_tiled.cuh"
 #include "tl_slab.cuh"
 #include "tl_vc.cuh"
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device, per-function attribute:
+// remember the largest size set for each (device, kernel) and raise it when needed.
+static cudaError_t ensure_smem_attr(const void* fn, size_t bytes) {
+    if (bytes <= 48 * 1024) return cudaSuccess;
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, size_t> set;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lock(mu);
+    size_t& have = set[{dev, fn}];
+    if (bytes <= have) return cudaSuccess;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) have = bytes;
+    return e;
+}
 
 namespace {
 
@@ -94,8 +114,8 @@ int launch_pcg(tl::PcgParams& P, bool gauss, int sms, cudaStream_t st, int64_t* 
     void* args[] = {&P};
     cudaError_t e;
     if (gauss) {
-        if (smem > 48 * 1024)
-            cudaFuncSetAttribute(tl::k_pcg<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        e = ensure_smem_attr((const void*)tl::k_pcg<true>, smem);
+        if (e != cudaSuccess) return fail(TL_E_CUDA, cudaGetErrorString(e));
         e = cudaLaunchCooperativeKernel((void*)tl::k_pcg<true>, blocks, tl::kTPB, args, smem, st);
     } else {
         e = cudaLaunchCooperativeKernel((void*)tl::k_pcg<false>, blocks, tl::kTPB, args, smem, st);
@@ -191,7 +211,7 @@ static bool tiled_plan(const tl::Grid& g, int sms, tl::TPlan& tp, size_t& smem) 
     if ((int)cz.size() > tl::kTMaxChunks) return false;
     tp.C = (int)cz.size();
     tp.I = tp.NB * tp.C;
-    if (tp.I > 7000) return false;
+    if (tp.I > tl::kTMaxItems) return false;
     tp.kb[0] = 0;
     for (int c = 0; c < tp.C; ++c) tp.kb[c + 1] = (short)(tp.kb[c] + cz[c]);
     if (tp.kb[tp.C] != g.NZ) return false;
@@ -207,13 +227,8 @@ static cudaError_t launch_t_cg(tl::PcgParams& P, int Gr, int sms, cudaStream_t s
     const int ncw = kTNCW;
     const bool two = tp.H * P.g.NX <= 2 * kTNCW * 32;
     auto kern = two ? tl::k_t_cg<kTNCW, 2> : tl::k_t_cg<kTNCW, 4>;
-    static thread_local size_t smem_set[2] = {0, 0};
-    cudaError_t e = cudaSuccess;
-    if (smem > smem_set[two]) {
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        smem_set[two] = smem;
-    }
+    cudaError_t e = ensure_smem_attr((const void*)kern, smem);
+    if (e != cudaSuccess) return e;
     int per_sm = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (ncw + 1) * 32, smem);
     if (e != cudaSuccess) return e;
@@ -349,12 +364,8 @@ static bool exact_cg() {
 template <bool GAUSS, int NPT, bool MULTI, bool XG = false>
 static cudaError_t launch_rescg_t(tl::ResCGParams& RP, int G, size_t smem, cudaStream_t st) {
     auto fn = tl::k_pcg_resident_cg<GAUSS, NPT, MULTI, XG>;
-    static thread_local bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kResSmemCap);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
+    cudaError_t e = ensure_smem_attr((const void*)fn, kResSmemCap);
+    if (e != cudaSuccess) return e;
     void* args[] = {&RP};
     return cudaLaunchCooperativeKernel((void*)fn, G, tl::kResTPB, args, smem, st);
 }
@@ -388,12 +399,8 @@ static unsigned long long* prof_buffer() {
 template <bool GAUSS, int NPT>
 static cudaError_t launch_res_t(tl::ResParams& RP, int G, size_t smem, cudaStream_t st) {
     auto fn = tl::k_pcg_resident<GAUSS, NPT>;
-    static thread_local bool attr_set = false;      // attribute set once per instantiation
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kResSmemCap);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
+    cudaError_t e = ensure_smem_attr((const void*)fn, kResSmemCap);
+    if (e != cudaSuccess) return e;
     void* args[] = {&RP};
     return cudaLaunchCooperativeKernel((void*)fn, G, tl::kResTPB, args, smem, st);
 }
@@ -575,8 +582,7 @@ static int launch_solve(tl::PcgParams& P, bool gauss, int sms, double* xg, cudaS
         // plain kernel, then the lean (non-Gaussian) cooperative solve adds it
         double* gl = xg + P.g.n;
         const size_t smem = gauss_smem(P.g);
-        if (smem > 48 * 1024)
-            cudaFuncSetAttribute(tl::k_gauss_load, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        TL_CUDA(ensure_smem_attr((const void*)tl::k_gauss_load, smem));
         tl::k_gauss_load<<<2 * sms, 256, smem, st>>>(P.g, P.src, P.mbase, P.T, gl);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return fail(TL_E_CUDA, std::string("k_gauss_load: ") + cudaGetErrorString(e));
@@ -714,6 +720,7 @@ int32_t tl_step_host(const tl_grid_desc* grid, double kappa, double rho_c, doubl
     struct StepWs {
         double* ws = nullptr;
         size_t cap = 0;
+        cudaStream_t st = nullptr;      // the step's own stream: no device-wide synchronisation
     };
     static StepWs wss[64];
     static std::mutex ws_mu;
@@ -721,7 +728,7 @@ int32_t tl_step_host(const tl_grid_desc* grid, double kappa, double rho_c, doubl
     if (dev < 0 || dev >= 64) return fail(TL_E_INVALID, "device ordinal out of range");
     StepWs& W = wss[dev];
     const size_t per = ((size_t)n + 2 + 31) / 32 * 32;
-    const size_t npart = ((size_t)4 * sms * 32 + 31) / 32 * 32;
+    const size_t npart = tl::kPartLen;
     const size_t nspec = (sizeof(tl::SolveSpec) + sizeof(tl::SolveInfoDev) + 255) / 256 * 32;
     const size_t want = 13 * per + npart + nspec;
     if (want > W.cap) {
@@ -731,6 +738,8 @@ int32_t tl_step_host(const tl_grid_desc* grid, double kappa, double rho_c, doubl
         TL_CUDA(cudaMalloc((void**)&W.ws, sizeof(double) * want));
         W.cap = want;
     }
+    if (!W.st) TL_CUDA(cudaStreamCreateWithFlags(&W.st, cudaStreamNonBlocking));
+    cudaStream_t st = W.st;
     double* T = W.ws;
     double* b = W.ws + per;
     double* r = W.ws + 2 * per;
@@ -746,12 +755,12 @@ int32_t tl_step_host(const tl_grid_desc* grid, double kappa, double rho_c, doubl
     tl::SolveInfoDev* dinfo = reinterpret_cast<tl::SolveInfoDev*>(
         reinterpret_cast<char*>(dspec) + (sizeof(tl::SolveSpec) + 15) / 16 * 16);
     int rc = 0;
-    TL_CUDA(cudaMemcpy(T, T_old, nb, cudaMemcpyHostToDevice));
+    TL_CUDA(cudaMemcpyAsync(T, T_old, nb, cudaMemcpyHostToDevice, st));
     if (gA) {
-        TL_CUDA(cudaMemcpy(dA, gA, nb, cudaMemcpyHostToDevice));
-        TL_CUDA(cudaMemcpy(dB, gB ? gB : gA, nb, cudaMemcpyHostToDevice));
+        TL_CUDA(cudaMemcpyAsync(dA, gA, nb, cudaMemcpyHostToDevice, st));
+        TL_CUDA(cudaMemcpyAsync(dB, gB ? gB : gA, nb, cudaMemcpyHostToDevice, st));
     }
-    if (load) TL_CUDA(cudaMemcpy(dload, load, nb, cudaMemcpyHostToDevice));
+    if (load) TL_CUDA(cudaMemcpyAsync(dload, load, nb, cudaMemcpyHostToDevice, st));
     P.T = T; P.gA = dA; P.gB = dB; P.w = gA ? w : 0.0; P.g_const = g_const; P.load = dload;
     P.b = b; P.r = r; P.p0 = p0; P.p1 = p1; P.q = q; P.part = part;
     P.rtol = rtol; P.maxiter = maxiter; P.info = dinfo;
@@ -761,15 +770,38 @@ int32_t tl_step_host(const tl_grid_desc* grid, double kappa, double rho_c, doubl
         for (int a = 0; a < 3; ++a) P.src.center[a] = src->center[a];
         P.src.on = 1;
     }
-    rc = launch_solve(P, gauss, sms, xg, 0, nullptr, dspec);
+    rc = launch_solve(P, gauss, sms, xg, st, nullptr, dspec);
     if (rc) return rc;
-    TL_CUDA(cudaDeviceSynchronize());
     tl::SolveInfoDev hi{};
-    TL_CUDA(cudaMemcpy(&hi, dinfo, sizeof(hi), cudaMemcpyDeviceToHost));
-    TL_CUDA(cudaMemcpy(x_out, T, nb, cudaMemcpyDeviceToHost));
+    TL_CUDA(cudaMemcpyAsync(&hi, dinfo, sizeof(hi), cudaMemcpyDeviceToHost, st));
+    TL_CUDA(cudaMemcpyAsync(x_out, T, nb, cudaMemcpyDeviceToHost, st));
+    TL_CUDA(cudaStreamSynchronize(st));
     if (info) {
         info->iterations = hi.iterations; info->status = hi.status; info->bnorm = hi.bnorm;
         info->rnorm = hi.rnorm; info->true_resid = hi.true_resid;
+    }
+    return TL_OK;
+}
+
+static std::mutex g_scratch_mu;
+static int scratch(int slot, size_t bytes, void** out);
+
+// Carve `k` device arrays out of scratch slot 3 (256-byte aligned sub-ranges, +2 elements
+// each as dalloc gives); the caller holds g_scratch_mu for the whole call.
+struct Carve {
+    size_t n;
+    size_t elem;
+    void** out;
+};
+static int scratch_arrays(std::initializer_list<Carve> arrs) {
+    size_t total = 0;
+    for (const Carve& c : arrs) total += ((c.n + 2) * c.elem + 255) / 256 * 256;
+    void* base = nullptr;
+    if (int rc = scratch(3, std::max<size_t>(total, 256), &base)) return rc;
+    char* p = static_cast<char*>(base);
+    for (const Carve& c : arrs) {
+        *c.out = p;
+        p += ((c.n + 2) * c.elem + 255) / 256 * 256;
     }
     return TL_OK;
 }
@@ -781,15 +813,14 @@ int32_t tl_interpolate_host(const tl_grid_desc* global_grid, const double* value
     if (int rc = make_grid(*global_grid, tl::kBottom, G)) return rc;
     if (int rc = make_grid(*target, tl::kGamma, L)) return rc;
     double *dv, *dout;
-    int rc = 0;
-    if ((rc = dalloc(&dv, G.n)) || (rc = dalloc(&dout, L.n))) return rc;
+    std::lock_guard<std::mutex> lock(g_scratch_mu);
+    if (int rc = scratch_arrays({{(size_t)G.n, 8, (void**)&dv}, {(size_t)L.n, 8, (void**)&dout}})) return rc;
     TL_CUDA(cudaMemcpy(dv, values, sizeof(double) * G.n, cudaMemcpyHostToDevice));
     TL_CUDA(cudaMemcpy(dout, out, sizeof(double) * L.n, cudaMemcpyHostToDevice));
     tl::k_interp<<<592, 256>>>(G, dv, L, gamma_only ? 1 : 0, gamma_only ? nullptr : dout,
                                gamma_only ? dout : nullptr);
     TL_CUDA(cudaGetLastError());
     TL_CUDA(cudaMemcpy(out, dout, sizeof(double) * L.n, cudaMemcpyDeviceToHost));
-    cudaFree(dv); cudaFree(dout);
     return TL_OK;
 }
 
@@ -870,6 +901,7 @@ static int vc_impl(const tl_grid_desc* grid, const tl_vc_material* mat, const tl
         double* ws = nullptr;
         size_t cap = 0;
         unsigned char* dm = nullptr;
+        size_t dm_cap = 0;              // the mask grows with n, not with `want`
         tl::SolveInfoDev* dinfo = nullptr;
     };
     static VcWs wss[64];
@@ -890,14 +922,20 @@ static int vc_impl(const tl_grid_desc* grid, const tl_vc_material* mat, const tl
     const size_t ntet = 6 * (size_t)G.nc[0] * G.nc[1] * G.nc[2];
     const size_t want = 16 * per + nt + 6 * 4096 + 9 * ntet;
     if (want > ws_cap) {
-        if (ws) { cudaFree(ws); cudaFree(dm); }
+        if (ws) cudaFree(ws);
         ws = nullptr;
         ws_cap = 0;
         TL_CUDA(cudaMalloc((void**)&ws, sizeof(double) * want));
-        TL_CUDA(cudaMalloc((void**)&dm, per));
-        if (!dinfo) TL_CUDA(cudaMalloc((void**)&dinfo, sizeof(tl::SolveInfoDev)));
         ws_cap = want;
     }
+    if (per > W.dm_cap) {
+        if (dm) cudaFree(dm);
+        dm = nullptr;
+        W.dm_cap = 0;
+        TL_CUDA(cudaMalloc((void**)&dm, per));
+        W.dm_cap = per;
+    }
+    if (!dinfo) TL_CUDA(cudaMalloc((void**)&dinfo, sizeof(tl::SolveInfoDev)));
     double* dTo = ws;
     double* dTl = ws + per;
     double* dex = extra_load ? ws + 2 * per : nullptr;
@@ -1019,7 +1057,6 @@ static int transmission_impl(const tl_grid_desc* global_grid, const tl_grid_desc
 
 // Per-device scratch buffers reused across calls of the interface helpers (grown on demand,
 // never shrunk); the caller holds g_scratch_mu for the whole call.
-static std::mutex g_scratch_mu;
 struct Scratch {
     void* p = nullptr;
     size_t cap = 0;
@@ -1158,8 +1195,11 @@ int32_t tl_mass_norms_host(const tl_grid_desc* grid, const double* a, const doub
     if (int rc = make_grid(*grid, tl::kGamma, L)) return rc;
     constexpr int kNB = 296;
     double *da, *db = nullptr, *dpart;
-    int rc = 0;
-    if ((rc = dalloc(&da, L.n)) || (b && (rc = dalloc(&db, L.n))) || (rc = dalloc(&dpart, 2 * kNB))) return rc;
+    std::lock_guard<std::mutex> lock(g_scratch_mu);
+    if (int rc = scratch_arrays({{(size_t)L.n, 8, (void**)&da}, {b ? (size_t)L.n : 0, 8, (void**)&db},
+                                 {2 * (size_t)kNB, 8, (void**)&dpart}}))
+        return rc;
+    if (!b) db = nullptr;
     TL_CUDA(cudaMemcpy(da, a, sizeof(double) * L.n, cudaMemcpyHostToDevice));
     if (b) TL_CUDA(cudaMemcpy(db, b, sizeof(double) * L.n, cudaMemcpyHostToDevice));
     tl::k_mass_norms<<<kNB, 256>>>(L, da, db, dpart);
@@ -1168,7 +1208,6 @@ int32_t tl_mass_norms_host(const tl_grid_desc* grid, const double* a, const doub
     TL_CUDA(cudaMemcpy(part, dpart, sizeof(part), cudaMemcpyDeviceToHost));
     out[0] = out[1] = 0.0;
     for (int k = 0; k < kNB; ++k) { out[0] += part[2 * k]; out[1] += part[2 * k + 1]; }
-    cudaFree(da); if (db) cudaFree(db); cudaFree(dpart);
     return TL_OK;
 }
 
@@ -1179,8 +1218,10 @@ int32_t tl_mass_norms_split_host(const tl_grid_desc* grid, const double* a, cons
     if (int rc = make_grid(*grid, tl::kBottom, L)) return rc;
     constexpr int kNB = 296;
     double *da, *db, *dpart;
-    int rc = 0;
-    if ((rc = dalloc(&da, L.n)) || (rc = dalloc(&db, L.n)) || (rc = dalloc(&dpart, 2 * kNB))) return rc;
+    std::lock_guard<std::mutex> lock(g_scratch_mu);
+    if (int rc = scratch_arrays({{(size_t)L.n, 8, (void**)&da}, {(size_t)L.n, 8, (void**)&db},
+                                 {2 * (size_t)kNB, 8, (void**)&dpart}}))
+        return rc;
     TL_CUDA(cudaMemcpy(da, a, sizeof(double) * L.n, cudaMemcpyHostToDevice));
     TL_CUDA(cudaMemcpy(db, b, sizeof(double) * L.n, cudaMemcpyHostToDevice));
     tl::k_mass_norms_split<<<kNB, 256>>>(L, da, db, box_lo[0], box_lo[1], box_lo[2], box_hi[0], box_hi[1],
@@ -1190,7 +1231,6 @@ int32_t tl_mass_norms_split_host(const tl_grid_desc* grid, const double* a, cons
     TL_CUDA(cudaMemcpy(part, dpart, sizeof(part), cudaMemcpyDeviceToHost));
     out[0] = out[1] = 0.0;
     for (int k = 0; k < kNB; ++k) { out[0] += part[2 * k]; out[1] += part[2 * k + 1]; }
-    cudaFree(da); cudaFree(db); cudaFree(dpart);
     return TL_OK;
 }
 
@@ -1202,9 +1242,9 @@ int32_t tl_error_l2_host(const tl_grid_desc* ref_grid, const double* ref_values,
     if (int rc = make_grid(*grid, tl::kGamma, L)) return rc;
     constexpr int kNB = 296;
     double *dref, *dv, *dri, *dpart;
-    int rc = 0;
-    if ((rc = dalloc(&dref, G.n)) || (rc = dalloc(&dv, L.n)) || (rc = dalloc(&dri, L.n)) ||
-        (rc = dalloc(&dpart, 2 * kNB)))
+    std::lock_guard<std::mutex> lock(g_scratch_mu);
+    if (int rc = scratch_arrays({{(size_t)G.n, 8, (void**)&dref}, {(size_t)L.n, 8, (void**)&dv},
+                                 {(size_t)L.n, 8, (void**)&dri}, {2 * (size_t)kNB, 8, (void**)&dpart}}))
         return rc;
     TL_CUDA(cudaMemcpy(dref, ref_values, sizeof(double) * G.n, cudaMemcpyHostToDevice));
     TL_CUDA(cudaMemcpy(dv, values, sizeof(double) * L.n, cudaMemcpyHostToDevice));
@@ -1215,7 +1255,6 @@ int32_t tl_error_l2_host(const tl_grid_desc* ref_grid, const double* ref_values,
     TL_CUDA(cudaMemcpy(part, dpart, sizeof(part), cudaMemcpyDeviceToHost));
     out[0] = out[1] = 0.0;
     for (int k = 0; k < kNB; ++k) { out[0] += part[2 * k]; out[1] += part[2 * k + 1]; }
-    cudaFree(dref); cudaFree(dv); cudaFree(dri); cudaFree(dpart);
     return TL_OK;
 }
 
@@ -1225,14 +1264,15 @@ int32_t tl_interpolate_points_host(const tl_grid_desc* global_grid, const double
     tl::Grid G{};
     if (int rc = make_grid(*global_grid, tl::kBottom, G)) return rc;
     double *dv, *dp, *dout;
-    int rc = 0;
-    if ((rc = dalloc(&dv, G.n)) || (rc = dalloc(&dp, 3 * npoints)) || (rc = dalloc(&dout, npoints))) return rc;
+    std::lock_guard<std::mutex> lock(g_scratch_mu);
+    if (int rc = scratch_arrays({{(size_t)G.n, 8, (void**)&dv}, {3 * (size_t)npoints, 8, (void**)&dp},
+                                 {(size_t)npoints, 8, (void**)&dout}}))
+        return rc;
     TL_CUDA(cudaMemcpy(dv, values, sizeof(double) * G.n, cudaMemcpyHostToDevice));
     TL_CUDA(cudaMemcpy(dp, points, sizeof(double) * 3 * npoints, cudaMemcpyHostToDevice));
     if (npoints > 0) tl::k_interp_pts<<<296, 256>>>(G, dv, dp, npoints, dout);
     TL_CUDA(cudaGetLastError());
     TL_CUDA(cudaMemcpy(out, dout, sizeof(double) * npoints, cudaMemcpyDeviceToHost));
-    cudaFree(dv); cudaFree(dp); cudaFree(dout);
     return TL_OK;
 }
 
@@ -1244,9 +1284,10 @@ int32_t tl_deposit_host(const tl_grid_desc* grid, const double* points, const do
     if (int rc = make_grid(*grid, tl::kBottom, G)) return rc;
     double *dl, *dp, *dw;
     int *prev, *prevn;
-    int rc = 0;
-    if ((rc = dalloc(&dl, G.n)) || (rc = dalloc(&dp, 3 * count)) || (rc = dalloc(&dw, count)) ||
-        (rc = dalloc(&prev, tl::kDepMax)) || (rc = dalloc(&prevn, 1)))
+    std::lock_guard<std::mutex> lock(g_scratch_mu);
+    if (int rc = scratch_arrays({{(size_t)G.n, 8, (void**)&dl}, {3 * (size_t)count, 8, (void**)&dp},
+                                 {(size_t)count, 8, (void**)&dw}, {(size_t)tl::kDepMax, 4, (void**)&prev},
+                                 {1, 4, (void**)&prevn}}))
         return rc;
     TL_CUDA(cudaMemset(dl, 0, sizeof(double) * G.n));
     TL_CUDA(cudaMemset(prevn, 0, sizeof(int)));
@@ -1257,7 +1298,6 @@ int32_t tl_deposit_host(const tl_grid_desc* grid, const double* points, const do
     tl::k_deposit<<<1, 1024>>>(G, dp, dw, count, dl, prev, prevn, 0, G.n);
     TL_CUDA(cudaGetLastError());
     TL_CUDA(cudaMemcpy(load_out, dl, sizeof(double) * G.n, cudaMemcpyDeviceToHost));
-    cudaFree(dl); cudaFree(dp); cudaFree(dw); cudaFree(prev); cudaFree(prevn);
     return TL_OK;
 }
 
@@ -1289,7 +1329,7 @@ int32_t tl_run_create(const tl_run_desc* desc, tl_run** out) {
         (rc = dalloc(&R->loadg, ng)) || (rc = dalloc(&R->Tl, nl)) || (rc = dalloc(&R->bl, nl)) ||
         (rc = dalloc(&R->rl, nl)) || (rc = dalloc(&R->pl0, nl)) || (rc = dalloc(&R->pl1, nl)) ||
         (rc = dalloc(&R->ql, nl)) || (rc = dalloc(&R->tr_old, nl)) || (rc = dalloc(&R->tr_pred, nl)) ||
-        (rc = dalloc(&R->Tl_before, nl)) || (rc = dalloc(&R->part, 4 * R->sms * 32)) ||
+        (rc = dalloc(&R->Tl_before, nl)) || (rc = dalloc(&R->part, tl::kPartLen)) ||
         (rc = dalloc(&R->dep_prev, tl::kDepMax)) || (rc = dalloc(&R->dep_prev_n, 1)) ||
         (rc = dalloc(&R->melt, 4)) || (rc = dalloc(&R->melt_part, 2 * 1184)) ||
         (rc = dalloc(&R->xg, 4 * (size_t)std::max(ng, nl))) || (rc = dalloc(&R->d_specs, 64))) {
@@ -1350,6 +1390,7 @@ static int run_interp_local(tl_run* R, int mode, double* out_all, double* out_ga
 int32_t tl_run_initial(tl_run* R, double T0) {
     if (!R) return fail(TL_E_INVALID, "null run");
     TL_CUDA(cudaSetDevice(R->device));
+    for (int a = 0; a < 3; ++a) R->L.off[a] = R->desc.local_grid.offset[a];   // initial placement
     tl::k_fill<<<4 * R->sms, 256, 0, R->stream>>>(R->Tg, R->G.n, T0);
     ++R->launches;
     TL_CUDA(cudaGetLastError());
@@ -1359,6 +1400,7 @@ int32_t tl_run_initial(tl_run* R, double T0) {
 int32_t tl_run_set_global(tl_run* R, const double* Tg_host, int64_t n) {
     if (!R || !Tg_host || n != R->G.n) return fail(TL_E_INVALID, "global field size mismatch");
     TL_CUDA(cudaSetDevice(R->device));
+    for (int a = 0; a < 3; ++a) R->L.off[a] = R->desc.local_grid.offset[a];   // initial placement
     TL_CUDA(cudaMemcpyAsync(R->Tg, Tg_host, sizeof(double) * n, cudaMemcpyHostToDevice, R->stream));
     return run_interp_local(R, 0, R->Tl, R->tr_old);
 }
@@ -1480,11 +1522,7 @@ static int local_multi(tl_run* R, const tl_macro_plan& mp, const tl_micro_plan* 
         TL_CUDA(cudaMemcpyAsync(R->d_srcs, R->h_srcs.data(), sizeof(tl::Gauss) * ns, cudaMemcpyHostToDevice,
                                 R->stream));
         const size_t smem = gauss_smem(R->L);
-        static bool attr = false;
-        if (!attr && smem > 48 * 1024) {
-            cudaFuncSetAttribute(tl::k_gauss_loads, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            attr = true;
-        }
+        TL_CUDA(ensure_smem_attr((const void*)tl::k_gauss_loads, smem));
         // the box of each solve is ~15 % of the local grid: spread it over the whole GPU
         const dim3 grid((unsigned)std::max(1, (8 * R->sms + ns - 1) / ns), (unsigned)ns);
         tl::k_gauss_loads<<<grid, 256, smem, R->stream>>>(R->L, R->d_specs + 1, R->d_srcs,
@@ -1865,8 +1903,7 @@ int32_t tl_slab_rhs(const tl_slab* s, const tl_gaussian* src) {
         S.src.on = 1;
         const size_t smem = gauss_smem(S.g);
         if (smem > 200 * 1024) return fail(TL_E_INVALID, "grid too long for Gaussian tables");
-        if (smem > 48 * 1024)
-            cudaFuncSetAttribute(tl::k_slab_rhs<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        TL_CUDA(ensure_smem_attr((const void*)tl::k_slab_rhs<true>, smem));
         tl::k_slab_rhs<true><<<blocks, tl::kSlabTPB, smem, st>>>(S);
     } else {
         tl::k_slab_rhs<false><<<blocks, tl::kSlabTPB, 0, st>>>(S);

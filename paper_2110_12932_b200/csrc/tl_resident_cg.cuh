@@ -150,6 +150,10 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
     // grid_allreduce epochs count from the counter value before this launch's first
     // grid.sync (no CTA can arrive at a grid_allreduce before every CTA passed that sync)
     unsigned bar_target = RP.bar_count ? __ldcg(RP.bar_count) : 0u;
+    // the CG loop has ONE grid barrier per iteration, so its partials alternate between two
+    // slot groups (8G.. and 11G..): a CTA that runs ahead into the next reduction never
+    // overwrites partials a slower CTA is still summing (nor the pre-loop slots 0..2)
+    unsigned lep = 0;
     const int bxi = b % RP.ng[0], byi = (b / RP.ng[0]) % RP.ng[1], bzi = b / (RP.ng[0] * RP.ng[1]);
     const int x0 = RP.off[0][bxi], y0 = RP.off[1][byi], z0 = RP.off[2][bzi];
     const int lx = RP.off[0][bxi + 1] - x0, ly = RP.off[1][byi + 1] - y0, lz = RP.off[2][bzi + 1] - z0;
@@ -485,22 +489,24 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
                 TL_STAMP(104)
                 if (RP.prof && si == kPS && it == 3 && threadIdx.x == 0) RP.prof[256 + b] = global_ns();
                 bar_target += (unsigned)G;
-                grid_allreduce<3>(d3, red, P.part, G, RP.bar_count, bar_target, tot);
+                grid_allreduce<3>(d3, red, P.part + (8 + 3 * (lep & 1u)) * G, G, RP.bar_count, bar_target, tot);
                 TL_STAMP(105)
                 TL_STAMP(106)
             } else {
+            double* lp = P.part + (8 + 3 * (lep & 1u)) * G;
             block_sum<3>(d3, red);
-            if (threadIdx.x == 0) { P.part[0 * G + b] = d3[0]; P.part[1 * G + b] = d3[1]; P.part[2 * G + b] = d3[2]; }
+            if (threadIdx.x == 0) { lp[0 * G + b] = d3[0]; lp[1 * G + b] = d3[1]; lp[2 * G + b] = d3[2]; }
             TL_STAMP(104)
             if (RP.prof && si == kPS && it == 3 && threadIdx.x == 0) RP.prof[256 + b] = global_ns();   // arrival per CTA
             grid.sync();
             TL_STAMP(105)
             {
                 const int s3[3] = {0, 1, 2};
-                grid_sum_fast<3>(P.part, s3, G, tot);
+                grid_sum_fast<3>(lp, s3, G, tot);
             }
             TL_STAMP(106)
             }
+            ++lep;
 #undef TL_STAMP
             if (prof && si == kPS && it < 100) RP.prof[np++] = global_ns();
             gam = tot[0];

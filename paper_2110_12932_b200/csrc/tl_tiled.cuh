@@ -36,6 +36,7 @@ namespace tl {
 constexpr int kTMaxStages = 16;
 constexpr int kTMaxChunks = 96;            // z chunks (guided: large first, small last)
 constexpr int kTPartItems = 4096;          // offset of the item partials in PcgParams::part
+constexpr int kTMaxItems = 7000;           // sweep A: slot 0, sweep B: slots 1, 2 (3 * kTMaxItems)
 constexpr int kTCounter = 2048;            // offset (in doubles) of the 4 sweep counters
 
 struct TPlan {
@@ -505,14 +506,16 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) k_t_cg(PcgParams P, int Grh
                 if (plane0) t_produce<true>(g, tp, t_sm, full, empty, s_item, ctr + (seq & 3), t, false, r0, nullptr,
                                             pnew, light0 ? nullptr : P.T);
             } else {
-                t_consume_b<NCW, NPT>(g, tp, T, full, empty, s_item, t, alpha, light0, P.T, P.r, part, ired);
+                // sweep B's item partials go to slots 1, 2: a CTA that is still summing sweep
+                // A's slot-0 partials after the barrier must not see them overwritten
+                t_consume_b<NCW, NPT>(g, tp, T, full, empty, s_item, t, alpha, light0, P.T, P.r, part + tp.I, ired);
                 fence_proxy_async_global();
             }
             ++seq;
             grid.sync();
             t = __shfl_sync(0xffffffffu, t, 0);
             fence_proxy_async_global();
-            t_grid_sum<2>(part, tp.I, red, tot);
+            t_grid_sum<2>(part + tp.I, tp.I, red, tot);
             rz = tot[0];
             rnorm = sqrt(tot[1]);
             rho_prev = rho;

@@ -48,8 +48,34 @@ class FieldState:
         return FieldState(self.mesh, values, self.time if time is None else time)
 
 
+class UniformFieldState(FieldState):
+    """``uniform_field``'s result: a constant field whose value array is built only when
+    read (a 201M-node initial field need not exist on the host for the device to start
+    from it; ``DeviceRun.initial`` takes ``.uniform_value``)."""
+
+    def __init__(self, mesh, value: float, time: float = 0.0):
+        value = float(value)
+        if not np.isfinite(value):
+            raise SolverError("field contains non-finite values")
+        object.__setattr__(self, "mesh", mesh)
+        object.__setattr__(self, "time", float(time))
+        object.__setattr__(self, "uniform_value", value)
+        object.__setattr__(self, "_v", None)
+
+    @property
+    def values(self) -> np.ndarray:
+        if self._v is None:
+            v = np.full(self.mesh.n_nodes, self.uniform_value)
+            v.setflags(write=False)
+            object.__setattr__(self, "_v", v)
+        return self._v
+
+    def __reduce__(self):
+        return (UniformFieldState, (self.mesh, self.uniform_value, self.time))
+
+
 def uniform_field(mesh, value: float, time: float = 0.0) -> FieldState:
-    return FieldState(mesh, np.full(mesh.n_nodes, float(value)), time)
+    return UniformFieldState(mesh, value, time)
 
 
 @dataclass(frozen=True)
@@ -187,8 +213,9 @@ def _step_general(state: FieldState, dt: float, mat, source, bounds: BoundarySpe
     """``step_backward_euler`` (``fem.py:307-355``) for temperature-dependent tables, latent
     heat, convection and lagged radiation: the reference's Picard loop (lag damping on
     stalls) over device passes (``tl_vc_step_host``: assembly, constraint and Jacobi-PCG on
-    the GPU).  The loop control (the relative increment) is computed on the host from the
-    pass's result, as the reference does."""
+    the GPU).  The whole loop runs in one call (``tl_vc_picard_host``): the relative
+    increment ||x - T_lag|| / ||x|| is reduced on the device and the damped lag update is a
+    kernel; the host maps the outcome to the reference's exceptions."""
     import ctypes as C
     from .ops import raise_for
     mesh = state.mesh
@@ -230,6 +257,10 @@ def _step_general(state: FieldState, dt: float, mat, source, bounds: BoundarySpe
     rtol = device_rtol(settings)
     linear = problem_is_linear(mat, bounds, latent)
     max_iter = 1 if linear else settings.picard_max_iter
+    if max_iter < 1:
+        # the reference's loop body never runs and it raises with an infinite increment
+        # (fem.py:331-355)
+        raise NonConvergence("Picard iteration", max_iter, float("inf"))
     t_new = state.time + dt
     x = np.empty(n)
     info = N.SolveInfo()
@@ -253,10 +284,12 @@ def _step_general(state: FieldState, dt: float, mat, source, bounds: BoundarySpe
             timer.__exit__(None, None, None)
     passes = int(npass.value)
     cg_failed = info.status != N.TL_SOLVE_OK
+    ok = passes - (1 if cg_failed else 0)
     if stats is not None:
-        stats.count("picard_iterations", passes - (1 if cg_failed else 0))
+        stats.count("picard_iterations", ok)
+        # one entry per successful pass, like picard_iterations (the failed pass raises)
         if stats.device_log is not None:
-            stats.device_log.extend((float(mss[k]), int(its[k])) for k in range(passes))
+            stats.device_log.extend((float(mss[k]), int(its[k])) for k in range(ok))
     raise_for(info)
     if linear or inc.value < settings.picard_tol:
         return state.with_values(x, t_new)

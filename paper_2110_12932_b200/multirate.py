@@ -15,7 +15,9 @@ Drop-in for ``lpbfsim.multirate`` (``lpbfsim/multirate.py``):
 from __future__ import annotations
 
 import ctypes as C
+import threading
 import time
+import weakref
 
 import numpy as np
 
@@ -32,8 +34,28 @@ from .twolevel import (
     solve_local, two_level_iterate,
 )
 
-__all__ = ["MacroSchedule", "DeviceRun", "run_spacetime", "run_space", "macro_step",
-           "predictor_global", "interpolate_trace"]
+__all__ = ["MacroSchedule", "DeviceRun", "DeviceFieldState", "run_spacetime", "run_space", "macro_step",
+           "predictor_global", "interpolate_trace", "release_device_runs"]
+
+
+def _run_desc(problem: TwoLevelProblem, local_mesh: StructuredGrid) -> N.RunDesc:
+    kappa, rcg, rcl = problem.constants()
+    beam = problem.beam
+    desc = N.RunDesc()
+    desc.global_grid = problem.global_mesh.desc()
+    desc.local_grid = local_mesh.desc()
+    desc.kappa = kappa
+    desc.rho_c_global = rcg
+    desc.rho_c_local = rcl
+    desc.T_buildplate = problem.bc.T_buildplate
+    if beam is not None:
+        desc.beam_peak, desc.beam_radius, desc.beam_depth = beam.gaussian_peak, beam.radius, beam.depth
+    desc.rtol = device_rtol(problem.solver)
+    desc.maxiter_factor = 20                 # fem.py:285
+    desc.max_micro = 64
+    desc.max_deposit = 512
+    desc.device = problem.device
+    return desc
 
 
 class DeviceRun:
@@ -46,34 +68,38 @@ class DeviceRun:
                                       "through the step-level drivers (run_spacetime / run_space)")
         self.problem = problem
         self.local_mesh = local_mesh
-        kappa, rcg, rcl = problem.constants()
-        beam = problem.beam
-        desc = N.RunDesc()
-        desc.global_grid = problem.global_mesh.desc()
-        desc.local_grid = local_mesh.desc()
-        desc.kappa = kappa
-        desc.rho_c_global = rcg
-        desc.rho_c_local = rcl
-        desc.T_buildplate = problem.bc.T_buildplate
-        if beam is not None:
-            desc.beam_peak, desc.beam_radius, desc.beam_depth = beam.gaussian_peak, beam.radius, beam.depth
-        desc.rtol = device_rtol(problem.solver)
-        desc.maxiter_factor = 20                 # fem.py:285
-        desc.max_micro = 64
-        desc.max_deposit = 512
-        desc.device = problem.device
+        desc = _run_desc(problem, local_mesh)
         self._h = C.c_void_p()
         N.check(N.lib().tl_run_create(C.byref(desc), C.byref(self._h)), "tl_run_create")
         self.n_global = problem.global_mesh.n_nodes
         self.n_local = local_mesh.n_nodes
         self.solve_log: list = []
+        self.key = bytes(desc)
+        self.h2d_bytes = 0                # host->device bytes issued (plans, uploads)
+        self.d2h_bytes = 0                # device->host bytes read (fields, solve records)
+        # device-backed result fields not yet read back: materialised before the run's
+        # state changes (initial / run / close), so they always see the values they named
+        self._lazy = weakref.WeakSet()
 
     # -- lifecycle -----------------------------------------------------------------
 
     def close(self):
         if self._h:
+            self._materialize_lazy()
             N.lib().tl_run_destroy(self._h)
             self._h = C.c_void_p()
+
+    def _materialize_lazy(self):
+        for f in list(self._lazy):
+            f._materialize()
+        self._lazy.clear()
+
+    def lazy_field(self, which: int, mesh, time: float) -> "DeviceFieldState":
+        """The run's current field `which` as a FieldState whose values are read back on
+        first access (or before the run's state next changes)."""
+        f = DeviceFieldState(mesh, time, self, which)
+        self._lazy.add(f)
+        return f
 
     def __del__(self):
         try:
@@ -91,6 +117,11 @@ class DeviceRun:
     # -- state -----------------------------------------------------------------------
 
     def initial(self, T0: FieldState):
+        self._materialize_lazy()
+        u = getattr(T0, "uniform_value", None)
+        if u is not None:
+            N.check(N.lib().tl_run_initial(self._h, float(u)), "tl_run_initial")
+            return
         v = np.asarray(T0.values)
         if v.size and np.all(v == v.flat[0]):
             N.check(N.lib().tl_run_initial(self._h, float(v.flat[0])), "tl_run_initial")
@@ -102,6 +133,7 @@ class DeviceRun:
         n = self.n_global if which == 0 else self.n_local
         out = np.empty(n) if out is None else out
         N.check(N.lib().tl_run_get_field(self._h, which, N.dptr(out), n), "tl_run_get_field")
+        self.d2h_bytes += out.nbytes
         return out
 
     def field_async(self, which: int, out: np.ndarray, slot: int = 0) -> None:
@@ -122,10 +154,13 @@ class DeviceRun:
         return out
 
     def run(self, plan: Plan):
+        if self._lazy:
+            self._materialize_lazy()
         macro = np.ascontiguousarray(plan.macro)
         micro = np.ascontiguousarray(plan.micro)
         pts = np.ascontiguousarray(plan.dep_points.reshape(-1), dtype=np.float64)
         pw = np.ascontiguousarray(plan.dep_power, dtype=np.float64)
+        self.h2d_bytes += macro.nbytes + micro.nbytes + pts.nbytes + pw.nbytes
         N.check(N.lib().tl_run_macro_steps(
             self._h, macro.ctypes.data_as(C.c_void_p), len(macro), micro.ctypes.data_as(C.c_void_p),
             len(micro), N.dptr(pts), N.dptr(pw), len(pw)), "tl_run_macro_steps")
@@ -142,6 +177,7 @@ class DeviceRun:
             out.extend({"iterations": buf[e].iterations, "status": buf[e].status,
                         "bnorm": buf[e].bnorm, "rnorm": buf[e].rnorm,
                         "true_resid": buf[e].true_resid} for e in range(cnt.value))
+            self.d2h_bytes += cnt.value * C.sizeof(N.SolveInfo)
             if cnt.value < 4096:
                 break
         self.solve_log.extend(out)
@@ -187,6 +223,79 @@ class DeviceRun:
         N.check(N.lib().tl_run_flush_l2(self._h), "flush")
 
 
+class DeviceFieldState(FieldState):
+    """A FieldState whose values still live on the device (device-resident
+    fields are materialised as numpy only when asked).  ``values`` reads the field back on
+    first access; the owning run materialises it before its state changes.  The device
+    solve already checked the field for non-finite values (the true-residual pass counts
+    them, ``fem.py:50-51``)."""
+
+    def __init__(self, mesh, time: float, run: "DeviceRun", which: int):
+        object.__setattr__(self, "mesh", mesh)
+        object.__setattr__(self, "time", float(time))
+        object.__setattr__(self, "_run", run)
+        object.__setattr__(self, "_which", which)
+        object.__setattr__(self, "_v", None)
+
+    def _materialize(self):
+        if self._v is None:
+            v = self._run.field(self._which)
+            v.setflags(write=False)
+            object.__setattr__(self, "_v", v)
+            object.__setattr__(self, "_run", None)
+        return self._v
+
+    @property
+    def values(self) -> np.ndarray:
+        return self._materialize()
+
+    @property
+    def on_device(self) -> bool:
+        return self._v is None
+
+    def __reduce__(self):
+        return (FieldState, (self.mesh, self.values, self.time))
+
+
+# One idle tl_run per problem descriptor, reused by the next run_spacetime / run_space call
+# of the same problem (a cfg4 run holds ~10 GB: allocation and release are not per call).
+_POOL: dict = {}
+_POOL_LOCK = threading.Lock()
+_POOL_MAX = 2
+
+
+def _acquire_run(problem, local_mesh) -> DeviceRun:
+    key = bytes(_run_desc(problem, local_mesh))
+    with _POOL_LOCK:
+        run = _POOL.pop(key, None)
+    if run is None or not run._h:
+        return DeviceRun(problem, local_mesh)
+    run.problem, run.local_mesh = problem, local_mesh      # same device descriptor
+    return run
+
+
+def _release_run(run: DeviceRun) -> None:
+    evict = []
+    with _POOL_LOCK:
+        old = _POOL.pop(run.key, None)
+        if old is not None and old is not run:
+            evict.append(old)
+        _POOL[run.key] = run
+        while len(_POOL) > _POOL_MAX:
+            evict.append(_POOL.pop(next(iter(_POOL))))
+    for r in evict:
+        r.close()
+
+
+def release_device_runs() -> None:
+    """Free the idle device runs kept for reuse (results not yet read back are read first)."""
+    with _POOL_LOCK:
+        runs = list(_POOL.values())
+        _POOL.clear()
+    for r in runs:
+        r.close()
+
+
 def _merge_counters(stats, counters: dict):
     if stats is None:
         return
@@ -196,7 +305,14 @@ def _merge_counters(stats, counters: dict):
 
 def _drive(problem, run: DeviceRun, plan_fn, local_mesh, T0, stats, recorder, t_initial,
            batch: int | None):
-    """Shared driver: plan on the host, execute on the device, deliver records."""
+    """Shared driver: plan on the host, execute on the device, deliver records.
+
+    Without a recorder the schedule is planned in growing windows (1, 2, 4, ... up to
+    ``batch`` or 32 macro steps) and each window is enqueued before the next one is
+    planned, so the host planning overlaps the device executing the previous window;
+    a window's solve records are checked after the next window has been planned.  With
+    a recorder every macro step is one window (its snapshots are delivered before the
+    next step overwrites them)."""
     gmesh = problem.global_mesh
     run.initial(T0)
     if recorder is not None:
@@ -205,30 +321,39 @@ def _drive(problem, run: DeviceRun, plan_fn, local_mesh, T0, stats, recorder, t_
     t0 = time.perf_counter()
     k = 0
     placement, tg, tl = local_mesh.placement, T0.time, T0.time
-    last_plan = None
+    last_plan = pending = None
+    window, cap = 1, (batch or 32)
     while True:
-        plan = plan_fn(placement, tg, tl, k, 1 if recorder is not None else batch,
-                       recorder is not None)
+        nsteps = 1 if recorder is not None else window
+        plan = plan_fn(placement, tg, tl, k, nsteps, recorder is not None)
+        if pending is not None:                  # the previous window: outcome + counters
+            infos = run.take_info()
+            run.check_solves(infos)
+            _merge_counters(stats, pending.counters)
+            pending = None
         if plan.n_steps == 0:
             break
         run.run(plan)
-        infos = run.take_info()
-        run.check_solves(infos)
-        _merge_counters(stats, plan.counters)
         if recorder is not None:
+            infos = run.take_info()
+            run.check_solves(infos)
+            _merge_counters(stats, plan.counters)
             _deliver(run, problem, plan, infos, recorder)
+        else:
+            pending = plan
         placement, tg, tl = plan.final_placement, plan.final_t_global, plan.final_t_local
         k += plan.n_steps
         last_plan = plan
-        if batch is None and recorder is None:
-            break
+        window = min(2 * window, cap)
     if stats is not None:
         stats.seconds["device_run"] = stats.seconds.get("device_run", 0.0) + time.perf_counter() - t0
     final_local = StructuredGrid(placement)
-    gv, lv = run.field(0), run.field(1)
+    lv = run.field(1)
     gamma = extract_interface(final_local, gmesh)
     trace = run.field(2)[gamma.trace_nodes]
-    return TwoLevelState(FieldState(gmesh, gv, tg), FieldState(final_local, lv, tl), gamma, trace), last_plan
+    # the global field stays on the device until the caller reads it
+    gfield = run.lazy_field(0, gmesh, tg)
+    return TwoLevelState(gfield, FieldState(final_local, lv, tl), gamma, trace), last_plan
 
 
 def _deliver(run: DeviceRun, problem, plan: Plan, infos, recorder):
@@ -260,12 +385,15 @@ def run_spacetime(problem: TwoLevelProblem, schedule: MacroSchedule, local_mesh:
     if not problem.device_resident:
         return _run_spacetime_steps(problem, schedule, local_mesh, T0, path, policy, stats, recorder)
     extract_interface(local_mesh, problem.global_mesh)
-    with DeviceRun(problem, local_mesh) as run:
+    run = _acquire_run(problem, local_mesh)
+    try:
         def plan_fn(placement, tg, tl, k, nsteps, record):
             return plan_spacetime(problem, schedule, placement, path, policy, tg, tl, k0=k,
                                   nsteps=nsteps, record=record)
         state, _ = _drive(problem, run, plan_fn, local_mesh, T0, stats, recorder,
                           schedule.t_start, batch)
+    finally:
+        _release_run(run)
     return state
 
 
@@ -277,11 +405,14 @@ def run_space(problem: TwoLevelProblem, dt: float, n_steps: int, local_mesh: Str
     if not problem.device_resident:
         return _run_space_steps(problem, dt, n_steps, local_mesh, T0, path, policy, stats, recorder)
     extract_interface(local_mesh, problem.global_mesh)
-    with DeviceRun(problem, local_mesh) as run:
+    run = _acquire_run(problem, local_mesh)
+    try:
         def plan_fn(placement, tg, tl, k, nsteps, record):
             return plan_space(problem, dt, n_steps, placement, path, policy, T0.time, tg, k0=k,
                               nsteps=nsteps, record=record)
         state, _ = _drive(problem, run, plan_fn, local_mesh, T0, stats, recorder, T0.time, batch)
+    finally:
+        _release_run(run)
     return state
 
 

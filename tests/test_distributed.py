@@ -1,5 +1,5 @@
 """Host-side multi-rank logic on CPU (gloo, world_size 2): scenario sharding (config 5)
-and the max-over-ranks timing reduction bench.py uses."""
+and the max-over-ranks timing reduction bench.py uses (bench.env_rank / all_reduce MAX)."""
 
 import os
 import socket
@@ -8,7 +8,7 @@ import pytest
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2110_12932_b200 import dist as D
+import torch
 from paper_2110_12932_b200 import scenarios as S
 
 
@@ -52,12 +52,17 @@ def _worker(rank, world, port, q):
                       WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        r, w, lr = D.world_from_env()
+        import bench
+        r, w, lr = bench.env_rank()
         mine = S.shard(S.draw(), r, w)
         gathered = [None] * w
         dist.all_gather_object(gathered, [s.index for s in mine])
-        tmax = D.max_over_ranks(10.0 * (r + 1))
-        total = D.sum_over_ranks(sum(s.dof_timesteps for s in mine))
+        t = torch.tensor([10.0 * (r + 1)], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tmax = float(t.item())
+        t = torch.tensor([float(sum(s.dof_timesteps for s in mine))], dtype=torch.float64)
+        dist.all_reduce(t)
+        total = float(t.item())
         q.put((r, gathered, tmax, total))
     finally:
         dist.destroy_process_group()

@@ -14,6 +14,8 @@ from paper_2110_12932_b200 import scenarios as S
 from paper_2110_12932_b200.schedule import plan_spacetime
 from oracle.twolevel import OracleRun
 
+from .conftest import assert_mask
+
 pytestmark = pytest.mark.gpu
 REL = 1e-9
 # seed-0 draws: scenario 0 has m = 5, scenario 5 m = 20 (tests/test_distributed.py pins the draw)
@@ -59,7 +61,8 @@ def test_scenario_steps_vs_oracle(idx):
     assert len(got) == len(ref) == n + 1
     for (Tl, Tg), (Rl, Rg) in zip(got, ref):
         assert rel(Tg, Rg) <= REL and rel(Tl, Rl) <= REL
-        assert np.array_equal(Tg > TL, Rg > TL) and np.array_equal(Tl > TL, Rl > TL)
+        assert_mask(None, Tg, Rg, TL)
+        assert_mask(None, Tl, Rl, TL)
 
 
 def test_interleaved_resident_runs_match_solo_runs():
