@@ -183,14 +183,22 @@ def _cpu_model() -> str:
 # CPU sample size per config: lateral nodes of the local-grid column (None: whole local grid)
 # for our arm's 1-core cpu_baseline (~10-30 s) and for each step of the reference arm
 # (~2-5 s, so --steps 20 --warmup 5 ends within a few minutes)
-CPU_WINDOW = {"cfg4": (126, 48), "cfg3": (None, 80), "cfg2": (None, None)}
+CPU_WINDOW = {"cfg4": (126, 80), "cfg3": (None, 80), "cfg2": (None, None)}
+
+
+def slab_mode(args, world: int) -> bool:
+    return (world > 1 or args.slabs) and args.config == "cfg4"
 
 
 def workload(args, world: int):
     """The bench workload both arms report: config dict, grid sizes, DOF per step."""
     import paper_2110_12932_b200 as P
     from paper_2110_12932_b200.control import initial_local_box, structured_ncells
-    cfg = P.load_config(ROOT / "configs" / f"{args.config}.cfg")
+    slabs = slab_mode(args, world)
+    if slabs and not args.strong:
+        cfg = weak_config(world)
+    else:
+        cfg = P.load_config(ROOT / "configs" / f"{args.config}.cfg")
     gn = structured_ncells(cfg.global_box, cfg.h_global)
     lbox = initial_local_box(cfg.global_box, cfg.h_local, cfg.policy, cfg.path)
     ln = structured_ncells(lbox, cfg.h_local)
@@ -205,6 +213,11 @@ def workload(args, world: int):
             "l2": ("inputs larger than L2 and flushed between timed steps" if Ng * 8 > 126e6
                    else "flushed between timed steps") if not args.no_flush else "not flushed",
             "parallelism": f"scenario replicas x{world}" if world > 1 else "single GPU"}
+    if slabs:
+        conf["workload"] = (f"{args.config}: two-level multirate macro step, global grid in z-slabs over {world} "
+                            f"GPU(s) ({'strong scaling' if args.strong else 'weak scaling: ~201M global nodes per GPU'}),"
+                            f" local steps pipelined over the GPUs in time; global {Ng} + local {Nl} nodes")
+        conf["parallelism"] = f"z-slabs x{world} + local time pipeline"
     return cfg, conf, (Ng, Nl, m)
 
 
@@ -251,82 +264,151 @@ def reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
+def weak_config(world: int):
+    """BASELINE config 4 grown in depth for weak scaling over z-slabs: the plate is
+    20 x 20 x 4N mm (1001 x 1001 x (200 N + 1) global nodes, ~201M per GPU), the scan path
+    on its top surface, the local box (251 x 251 x 101 nodes, h = 4 um) as in cfg4.  N = 1
+    is cfg4 itself."""
+    import paper_2110_12932_b200 as P
+    text = (ROOT / "configs" / "cfg4.cfg").read_text()
+    if world > 1:
+        depth = 4 * world
+        text = text.replace("global_max 20 20 4 mm", f"global_max 20 20 {depth} mm")
+        text = text.replace("origin 2.5 9.55 4.0 mm", f"origin 2.5 9.55 {depth}.0 mm")
+    return P.config_from_text(text, base_dir=ROOT / "configs", name=f"cfg4-weak-x{world}")
+
+
 def slab_bench(args):
-    """--slabs: the global grid z-slab-decomposed over the ranks (strong scaling of one run),
-    local problem on the top rank.  Default workload cfg4 (201M-node global grid)."""
+    """Multi-GPU (``--gpus N`` under torchrun, or ``--slabs``): the global grid in z-slabs
+    with the device-resident CG (slab.py), the local steps pipelined over the ranks in time
+    (multirate_dist.py).  Default workload: cfg4 grown in depth, ~201M global nodes per GPU
+    (weak scaling); ``--strong``: cfg4 itself split over the ranks."""
     import torch
     import paper_2110_12932_b200 as P
-    from paper_2110_12932_b200.multirate_dist import SlabRun
-    from paper_2110_12932_b200.schedule import plan_spacetime
+    from paper_2110_12932_b200.multirate_dist import SlabRun, plan_superstep
 
     rank, world, local_rank = env_rank()
     torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    name = args.config if args.config != "cfg2" else "cfg4"
-    cfg = P.load_config(ROOT / "configs" / f"{name}.cfg")
+        dist.init_process_group("nccl", device_id=dev)
+    cfg, conf, (Ng, Nl, m) = workload(args, world)
     problem, lmesh = P.build_problem(cfg, device=local_rank)
     sched = P.MacroSchedule(cfg.dt_macro, cfg.micro_steps, 0.0, cfg.t_end)
-    m = sched.micro_per_macro
-    Ng, Nl = problem.global_mesh.n_nodes, lmesh.n_nodes
     dof_step = Ng + m * Nl
-    nsteps = args.warmup + args.steps
-    plans = []
-    placement, tg, tl = lmesh.placement, 0.0, 0.0
-    for k in range(nsteps):
-        pl = plan_spacetime(problem, sched, placement, cfg.path, cfg.policy, tg, tl, k0=k, nsteps=1)
-        plans.append(pl)
-        placement, tg, tl = pl.final_placement, pl.final_t_global, pl.final_t_local
-    run = SlabRun(problem, lmesh, rank=rank, world=world, device=f"cuda:{local_rank}")
+    run = SlabRun(problem, lmesh, rank=rank, world=world, device=dev)
     run.initial(P.uniform_field(problem.global_mesh, cfg.T_initial))
-    for k in range(args.warmup):
-        run.step(plans[k])
+    state = [lmesh.placement, 0.0, 0.0, 0]
+
+    def steps(n):
+        """Whole super-steps until at least n macro steps ran; returns the steps run."""
+        done = 0
+        while done < n:
+            plans, nxt = plan_superstep(problem, sched, cfg.path, cfg.policy, *state, world, run.moved_before)
+            if not plans:
+                raise SystemExit("schedule exhausted")
+            run.superstep(plans)
+            state[:] = list(nxt)
+            done += len(plans)
+        return done
+
+    steps(args.warmup)
+    run.check_local()
     torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    l0 = run.solver.launches + (run.local.launch_count() if run.local is not None else 0)
-    gi0 = len(run.global_infos)
     run.timing = True
+    run.global_ms.clear()
+    l0 = run.solver.launches + run.local.launch_count()
+    cur = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clocks:
-        for (e0, e1), pl in zip(ev, plans[args.warmup:]):
-            e0.record()
-            run.step(pl)          # host-orchestrated: returns after the step's work completed
-            e1.record()
+        wall0 = time.perf_counter()
+        e0.record(cur)
+        nsteps = steps(args.steps)
+        cur.wait_stream(run.local_stream)
+        e1.record(cur)
         torch.cuda.synchronize()
-    launches = run.solver.launches + (run.local.launch_count() if run.local is not None else 0) - l0
-    dev_ms = float(sum(a.elapsed_time(b) for a, b in ev))
-    if dist is not None:
-        t = torch.tensor([dev_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dev_ms = float(t.item())
-    gits = [inf.iterations for inf in run.global_infos[gi0:]]
-    peak, peak_src = measured_peak()
+        wall = time.perf_counter() - wall0
+    run.check_local()
+    dev_ms = e0.elapsed_time(e1)
+    launches = run.solver.launches + run.local.launch_count() - l0
     S = run.solver
     own = (S.k1 - S.k0) * S.nxy
+    gms = [a.elapsed_time(b) for a, b, _ in run.global_ms]
+    gits = [k for _, _, k in run.global_ms]
+    polls = S.polls
+    if dist is not None:
+        t = torch.tensor([dev_ms, wall], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_ms, wall = float(t[0]), float(t[1])
+    value = dof_step * nsteps / (dev_ms / 1e3)
+    peak, peak_src = measured_peak()
+    alg = sum(own * (64 * k + 32) for k in gits)
+    ach = alg / (sum(gms) / 1e3) / 1e9 if gms else None
+    roofline = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": ach / peak if ach else None, "traffic": None,
+                "kernel": "z-slab global solve (rank 0): k_slab_rhs -> {k_sd_dir (bulk-copy sweep A), all-gather, "
+                          "k_sd_upd_flat (boundary planes), halo || k_sd_upd (bulk-copy sweep B), all-gather} -> "
+                          "k_sd_resid -> k_sd_finish; scalars on the device",
+                "level": "global", "nodes": own, "peak_source": peak_src,
+                "note": "rank 0's own nodes x (64 k + 32) bytes per solve / the solves' CUDA-event time "
+                        "(incl. the collectives inside them)"}
+
+    # e2e: the same driver with the host planning inside the clock and the final local
+    # field read back (the public two_level_run_slabs / run_spacetime_slabs loop)
+    T0 = P.uniform_field(problem.global_mesh, cfg.T_initial)
+    run2 = run
+    run2.check_local()
+    h_lv = np.empty(lmesh.n_nodes)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    t0 = time.perf_counter()
+    ne = steps(args.steps)
+    run2.check_local()
+    if rank == run2.last_rank:
+        h_lv = run2.local.field(1)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    if dist is not None:
+        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    del T0, h_lv
+    e2e = {"value": dof_step * ne / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 64 + 48 * (m + 1) + 8 * 4 * 144,
+           "d2h_bytes_per_step": 40 * (m + 2) + 8 * Nl // max(ne, 1),
+           "note": "host wall clock (max over ranks) of the next macro steps through the slab driver's "
+                   "public loop (plan_superstep + SlabRun.superstep, as run_spacetime_slabs runs it): host "
+                   "planning inside the clock, deposit samples H2D, solve records D2H, the last local field D2H"}
+    run.close()
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        win = CPU_WINDOW.get("cfg4", (None, None))[0]
+        smp = LocalSample(cfg, with_global=False, window=win)
+        dof, dt, _, _ = smp.once()
+        cpu = {"value": dof / dt, "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": f"one local micro solve on a {smp.shape[0]}x{smp.shape[1]}x{smp.shape[2]}-node column of the "
+                         f"cfg4 local grid ({dof} DOF-timesteps, {dt:.1f} s), literal P1-assembly + scipy-CG port; "
+                         "the global solve is infeasible on the CPU port"}
     line = {
-        "metric": METRIC, "value": dof_step * args.steps / (dev_ms / 1e3), "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / args.steps,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": f"synthetic (BASELINE {name} scan path and geometry)",
-        "config": {"workload": f"{name}: two-level multirate macro step, global grid on {world} z-slab(s), "
-                               f"local problem on the top rank; global {Ng} + local {Nl} nodes",
-                   "config_file": f"configs/{name}.cfg", "dof_timesteps_per_step": dof_step,
-                   "parallelism": f"z-slabs x{world}", "l2": f"inputs larger than L2 ({Ng * 8 / 1e9:.1f} GB per vector)"},
-        "global_iterations": float(np.mean(gits)) if gits else None,
-        "phase_ms_per_step": {"deposit+global slab solve": float(np.mean([a for a, _ in run.phase_ms])),
-                              "gather+local part": float(np.mean([b for _, b in run.phase_ms]))},
-        "rank0_own_nodes": own, "gpu_launches": launches, "clocks": clocks.summary(),
-        "roofline": None, "cpu_baseline": None, "e2e": None,
-        "note": "slab mode is host-orchestrated per CG phase (two rank-ordered sums per iteration); "
-                "peak for reference " + f"{peak:.0f} GB/s ({peak_src})",
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": nsteps,
+        "warmup": args.warmup, "ms_per_step": dev_ms / nsteps, "higher_is_better": True,
+        "scaling": "strong" if args.strong else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (BASELINE config 4 scan path and geometry" + ("" if args.strong or world == 1 else
+                f", plate {4 * world} mm deep for weak scaling") + ")",
+        "config": conf,
+        "global_solve": {"ms_mean": float(np.mean(gms)) if gms else None,
+                         "iterations_mean": float(np.mean(gits)) if gits else None,
+                         "host_syncs_per_solve": polls / max(len(run.global_infos), 1)},
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+        "clocks": clocks.summary(), "wall_s_timed_region": wall,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
-    run.close()
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
@@ -873,7 +955,9 @@ def main():
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--skip", type=int, default=0, help="macro steps to run before warm-up")
     ap.add_argument("--slabs", action="store_true",
-                    help="global grid split into z-slabs over the ranks (default config cfg4)")
+                    help="the multi-GPU driver (z-slab global solve, time-pipelined local steps) even at N = 1")
+    ap.add_argument("--strong", action="store_true",
+                    help="multi-GPU: cfg4 itself split over the ranks instead of the weak-scaling plate")
     ap.add_argument("--scenarios", type=int, default=64,
                     help="cfg5: how many of the 64 seed-0 scenarios to run (split over the ranks)")
     args = ap.parse_args()
@@ -881,7 +965,7 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         return reference_arm(args)
-    if args.slabs:
+    if slab_mode(args, env_rank()[1]):
         return slab_bench(args)
     if args.config == "cfg5":
         return scenario_bench(args)

@@ -112,6 +112,11 @@ typedef struct {
     int32_t max_micro;              /* largest micro count per macro step  */
     int32_t max_deposit;            /* largest deposit sample count per step */
     int32_t device;                 /* CUDA device ordinal                 */
+    int32_t external_planes;        /* 0: the run owns the global level.  > 0: multi-GPU
+                                       local-only run — the global field comes from the
+                                       z-slab solve (tl_run_put_global_planes) and only its
+                                       top external_planes planes (the local box's P1
+                                       support) are stored; no global solver workspace */
 } tl_run_desc;
 
 /* One macro step of the one-way multirate cycle (multirate.py:105-164), or one
@@ -155,6 +160,10 @@ int32_t tl_step_host(const tl_grid_desc* grid, double kappa, double rho_c, doubl
                      double g_const, const double* T_old, const double* load,
                      const tl_gaussian* src, double rtol, int32_t maxiter,
                      double* x_out, tl_solve_info* info);
+
+/* Device time (CUDA events) of the last tl_step_host's solve launches (RHS, CG loop,
+ * residual, finish), for benchmarks and solver tuning. */
+int32_t tl_step_last_ms(float* ms);
 
 /* ---- P1 interpolation of a global field at the nodes of a (translated) grid:
  *      Mesh.interpolate (mesh.py:358-361) on Mesh.locate (mesh.py:308-339).
@@ -308,12 +317,14 @@ int32_t tl_run_take_timing(tl_run* run, float* ms, int32_t* level, int32_t* nsol
 int32_t tl_debug_profile(uint64_t* out, int32_t max, int32_t* count);
 /* Write a scratch buffer larger than L2 on the run's stream (bench hygiene). */
 int32_t tl_run_flush_l2(tl_run* run);
-/* Multi-GPU: when on, tl_run_macro_steps skips the deposit and the global solve
- * (the z-slab solve below does them across ranks) and runs only the local part of each
- * macro step (trace, micro solves, corrector, relocation) against the global field
- * placed with tl_run_put_global_planes (multirate.py:129-162 on the rank that holds
- * the local problem). */
-int32_t tl_run_set_external_global(tl_run* run, int32_t on);
+/* Multi-GPU local-only runs (tl_run_desc.external_planes > 0): tl_run_macro_steps skips
+ * the deposit and the global solve and runs the local part of each macro step (trace,
+ * micro solves, corrector, relocation; multirate.py:129-162) against the global planes
+ * placed with tl_run_put_global_planes.  tl_run_reanchor moves the local box to `offset`
+ * (Mesh._offset) and re-derives the whole local field and its trace by P1 interpolation
+ * of the current global planes: relocate_local's field transfer (scanpath.py:243-248), or
+ * initial_state (twolevel.py:145-156) at a later macro step. */
+int32_t tl_run_reanchor(tl_run* run, const double* offset);
 /* Copy device planes [k0, k1) of the global field (plane k0 first) into the run
  * (device-to-device on the run's stream; src must be ready when the call is made). */
 int32_t tl_run_put_global_planes(tl_run* run, const double* src, int32_t k0, int32_t k1);
@@ -322,16 +333,24 @@ int32_t tl_run_put_global_planes(tl_run* run, const double* src, int32_t k0, int
  * Replaces, per rank, the share of the global backward-Euler step
  * (twolevel.solve_global, lpbfsim/twolevel.py:242-271 -> fem.step_backward_euler,
  * fem.py:307-355 -> scipy cg, fem.py:271-298) that falls on the rank's node planes.
- * The reference has no decomposition; these entry points are the phases of one CG
- * iteration between the collectives the host issues (paper_2110_12932_b200/slab.py):
- *   rhs -> [sum bb, rz] -> halo r -> loop { direction -> [sum pq] -> update -> [sum rz, rr]
- *   -> halo r } -> halo x -> residual -> [sum] -> finish.
+ * The reference has no decomposition.  The CG loop is DEVICE-RESIDENT: every scalar
+ * (alpha, beta, the stop test) is computed by the kernels from the all-gathered partial
+ * sums, so the host enqueues kernels and collectives without reading anything back:
+ *   begin -> [all-gather sums] -> halo r -> loop { direction -> [all-gather] ->
+ *   update(0) -> halo r (comm stream) || update(1) -> [all-gather] } -> halo x ->
+ *   residual -> [all-gather] -> finish -> poll
+ * The host enqueues a predicted number of iterations; iterations after the stop test
+ * fired, and residual / finish before it fired, are no-ops; poll (the only host
+ * synchronisation of a solve) reports whether finish has run.
  * Rank owns node planes [k0, k1) and stores planes [h0, h1) = [max(k0-1,0), min(k1+1,nz+1)):
- * every array below is device memory of (h1-h0)*(nx+1)*(ny+1) doubles, plane h0 first.
- * sums receives this rank's partial sums: slot 0/1 after rhs (b.b, r.z) and update
- * (r.z, r.r), slot 2 after direction (p.q), slots 0/3 after residual (||Ax-b||^2,
- * non-finite count).  work must hold tl_slab_work_len() doubles, zeroed once before first
- * use (the kernels leave it zeroed).  Only TL_DIRICHLET_BOTTOM is supported. */
+ * x, b, r, p0, p1, load are device arrays of (h1-h0)*(nx+1)*(ny+1) doubles, plane h0
+ * first, allocated so that the address of global node 0 (x - h0*(nx+1)*(ny+1)) is 16-byte
+ * aligned and one element before / two after the stored range are readable (the bulk
+ * copies round node ranges to 16 bytes).  sums: this rank's 8 partial sums (slot 0 r.r,
+ * 1 r.z, 2 p.q, 3 ||Ax-b||^2, 4 non-finite count) — the all-gather's input; gath:
+ * world x 8 doubles, every rank's sums in rank order — its output (NULL when world == 1).
+ * work must hold tl_slab_work_len() doubles, zeroed once before first use.  Only
+ * TL_DIRICHLET_BOTTOM is supported. */
 typedef struct {
     tl_grid_desc grid;        /* the whole global grid                           */
     int32_t dirichlet_kind;   /* TL_DIRICHLET_BOTTOM                             */
@@ -342,21 +361,34 @@ typedef struct {
     double *b, *r, *p0, *p1;  /* CG workspace                                    */
     const double* load;       /* deposit load or NULL                            */
     double* work;
-    double* sums;             /* 4 doubles                                       */
+    double* sums;             /* 8 doubles                                       */
+    const double* gath;       /* world x 8 doubles (NULL: world == 1)            */
+    int32_t world;
+    int32_t maxiter;          /* scipy's maxiter (fem.py:285: 20 n)              */
+    double rtol;              /* SolverSettings.linear_tol                       */
     void* stream;             /* cudaStream_t, NULL = legacy default stream      */
 } tl_slab;
 
 int64_t tl_slab_work_len(void);
-/* RHS (mass T_old + load [+ Gaussian] + Dirichlet lift), r = b, x = 0 on own planes. */
-int32_t tl_slab_rhs(const tl_slab* s, const tl_gaussian* src);
-/* p = z (first) or beta p + z on stored planes; p.q over own planes. */
-int32_t tl_slab_direction(const tl_slab* s, int32_t first, double beta, int32_t parity);
-/* x += alpha p, r -= alpha A p on own planes; r.z, r.r. */
-int32_t tl_slab_update(const tl_slab* s, double alpha, int32_t parity);
-/* ||A x - b||^2 and the non-finite count over own planes (x halo must be current). */
+/* Control-block reset + RHS (mass T_old + load [+ Gaussian] + Dirichlet lift), r = b,
+ * x = 0 on own planes; sums[0] = b.b, sums[1] = r.z. */
+int32_t tl_slab_begin(const tl_slab* s, const tl_gaussian* src);
+/* scipy's stop test on the gathered sums; p = z (first) or beta p + z on stored planes;
+ * sums[2] = p.Ap over own planes (bulk-copy z-march sweep). */
+int32_t tl_slab_direction(const tl_slab* s);
+/* x += alpha p, r -= alpha A p; part 0: the own planes a neighbour reads (their r is
+ * what the halo exchange sends), part 1: the rest (sums[0] = r.r, sums[1] = r.z over all
+ * own planes, iteration count + 1). */
+int32_t tl_slab_update(const tl_slab* s, int32_t part);
+/* After the stop test: ||A x - b||^2 and the non-finite count over own planes (x halo
+ * must be current). */
 int32_t tl_slab_residual(const tl_slab* s);
-/* Re-impose the Dirichlet values x_D = b_D (fem.py:289-290). */
+/* After the stop test: x_D = b_D (fem.py:289-290) and the true-residual check
+ * (fem.py:286-288) on the gathered residual sums. */
 int32_t tl_slab_finish(const tl_slab* s);
+/* Synchronise the slab's stream and read the control block: *state 0 = iterating, 1 =
+ * stopped (residual / finish pending), 2 = finished; info receives the outcome. */
+int32_t tl_slab_poll(const tl_slab* s, int32_t* state, tl_solve_info* info);
 /* Swept-track deposit (SweptTrackDeposit.load, sources.py:164-172) into s->load on the
  * rank's own nodes: the previous call's nodes are zeroed, the new samples scattered with
  * Kuhn-P1 weights and merged in np.add.at order.  points (3 count) and power (count)

@@ -62,7 +62,7 @@ class RunDesc(C.Structure):
                 ("T_buildplate", C.c_double), ("beam_peak", C.c_double),
                 ("beam_radius", C.c_double), ("beam_depth", C.c_double), ("rtol", C.c_double),
                 ("maxiter_factor", C.c_int32), ("max_micro", C.c_int32),
-                ("max_deposit", C.c_int32), ("device", C.c_int32)]
+                ("max_deposit", C.c_int32), ("device", C.c_int32), ("external_planes", C.c_int32)]
 
 
 class MacroPlan(C.Structure):
@@ -80,6 +80,7 @@ class Slab(C.Structure):
                 ("kappa", C.c_double), ("rho_c", C.c_double), ("dt", C.c_double), ("g_const", C.c_double),
                 ("x", C.c_void_p), ("b", C.c_void_p), ("r", C.c_void_p), ("p0", C.c_void_p),
                 ("p1", C.c_void_p), ("load", C.c_void_p), ("work", C.c_void_p), ("sums", C.c_void_p),
+                ("gath", C.c_void_p), ("world", C.c_int32), ("maxiter", C.c_int32), ("rtol", C.c_double),
                 ("stream", C.c_void_p)]
 
 
@@ -117,6 +118,7 @@ SIGNATURES = [
     ("tl_transmission_tables_host", C.c_int32, [C.POINTER(GridDesc), C.POINTER(GridDesc), _dp, _dp, _dp, C.c_int32,
                                                 _dp, _dp, C.c_int32, _dp]),
     ("tl_vc_last_cg_ms", C.c_int32, [C.POINTER(C.c_float)]),
+    ("tl_step_last_ms", C.c_int32, [C.POINTER(C.c_float)]),
     ("tl_vc_picard_host", C.c_int32, [C.POINTER(GridDesc), C.POINTER(VcMaterial), C.POINTER(VcMaterial), _dp,
                                       C.c_int32, C.c_double, _dp, _dp, C.POINTER(Gaussian), C.POINTER(Robin),
                                       C.c_void_p, _dp, C.c_double, C.c_int32, C.c_int32, C.c_double, C.c_int32,
@@ -149,15 +151,16 @@ SIGNATURES = [
                                        C.POINTER(C.c_int32), C.c_int32, C.POINTER(C.c_int32)]),
     ("tl_run_flush_l2", C.c_int32, [_P]),
     ("tl_debug_profile", C.c_int32, [C.POINTER(C.c_uint64), C.c_int32, C.POINTER(C.c_int32)]),
-    ("tl_run_set_external_global", C.c_int32, [_P, C.c_int32]),
+    ("tl_run_reanchor", C.c_int32, [_P, C.c_void_p]),
     ("tl_run_put_global_planes", C.c_int32, [_P, C.c_void_p, C.c_int32, C.c_int32]),
     ("tl_slab_work_len", C.c_int64, []),
     ("tl_slab_deposit", C.c_int32, [C.POINTER(Slab), C.c_void_p, C.c_void_p, C.c_int32]),
-    ("tl_slab_rhs", C.c_int32, [C.POINTER(Slab), C.POINTER(Gaussian)]),
-    ("tl_slab_direction", C.c_int32, [C.POINTER(Slab), C.c_int32, C.c_double, C.c_int32]),
-    ("tl_slab_update", C.c_int32, [C.POINTER(Slab), C.c_double, C.c_int32]),
+    ("tl_slab_begin", C.c_int32, [C.POINTER(Slab), C.POINTER(Gaussian)]),
+    ("tl_slab_direction", C.c_int32, [C.POINTER(Slab)]),
+    ("tl_slab_update", C.c_int32, [C.POINTER(Slab), C.c_int32]),
     ("tl_slab_residual", C.c_int32, [C.POINTER(Slab)]),
     ("tl_slab_finish", C.c_int32, [C.POINTER(Slab)]),
+    ("tl_slab_poll", C.c_int32, [C.POINTER(Slab), C.POINTER(C.c_int32), C.POINTER(SolveInfo)]),
 ]
 
 _lib = None

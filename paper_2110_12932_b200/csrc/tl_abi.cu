@@ -27,6 +27,7 @@
 #include "tl_stream.cuh"
 #include "tl_tiled.cuh"
 #include "tl_slab.cuh"
+#include "tl_slabdev.cuh"
 #include "tl_vc.cuh"
 
 // cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device, per-function attribute:
@@ -172,6 +173,8 @@ static bool tiled_enabled() {
     return v == 1;
 }
 
+static bool tiled_plan_range(const tl::Grid& g, int sms, int zlo, int zhi, tl::TPlan& tp, size_t& smem);
+
 static bool tiled_plan(const tl::Grid& g, int sms, tl::TPlan& tp, size_t& smem) {
     static long long nmin = -1;
     if (nmin < 0) {
@@ -179,7 +182,15 @@ static bool tiled_plan(const tl::Grid& g, int sms, tl::TPlan& tp, size_t& smem) 
         nmin = e ? atoll(e) : 20000000LL;
     }
     if ((long long)g.n < nmin) return false;
+    return tiled_plan_range(g, sms, 0, g.NZ, tp, smem);
+}
+
+// Item plan of the bulk-copy z-march over node planes [zlo, zhi) (the whole grid, or one
+// rank's own planes of a z-slab decomposition).
+static bool tiled_plan_range(const tl::Grid& g, int sms, int zlo, int zhi, tl::TPlan& tp, size_t& smem) {
     const int NX = g.NX;
+    const int nzr = zhi - zlo;
+    if (nzr < 1) return false;
     // rows per item: a sweep-B stage ((H + 2) + 2 H rows) small enough for 5 ring stages in
     // 220 KB, and at most 4 nodes per consumer thread per plane
     int H = std::max(1, (220 * 1024 / 8 / 5 - 2 * NX - 8) / (3 * NX));
@@ -202,19 +213,19 @@ static bool tiled_plan(const tl::Grid& g, int sms, tl::TPlan& tp, size_t& smem) 
     // halo planes and reductions cost more than the shorter tail saves)
     int zmin = 3;
     if (const char* e = getenv("TLGPU_TZ")) zmin = std::max(1, atoi(e));
-    const double share = (double)g.n / sms;
+    const double share = (double)NX * g.NY * nzr / sms;
     int Z = (int)(share / (10.0 * H * NX));
-    Z = std::max(zmin, std::min(Z, g.NZ));
+    Z = std::max(zmin, std::min(Z, nzr));
     std::vector<int> cz;
-    const int nch = std::max(1, (g.NZ + Z - 1) / Z);
-    for (int c = 0; c < nch; ++c) cz.push_back(g.NZ * (c + 1) / nch - g.NZ * c / nch);
+    const int nch = std::max(1, (nzr + Z - 1) / Z);
+    for (int c = 0; c < nch; ++c) cz.push_back(nzr * (c + 1) / nch - nzr * c / nch);
     if ((int)cz.size() > tl::kTMaxChunks) return false;
     tp.C = (int)cz.size();
     tp.I = tp.NB * tp.C;
     if (tp.I > tl::kTMaxItems) return false;
-    tp.kb[0] = 0;
+    tp.kb[0] = (short)zlo;
     for (int c = 0; c < tp.C; ++c) tp.kb[c + 1] = (short)(tp.kb[c] + cz[c]);
-    if (tp.kb[tp.C] != g.NZ) return false;
+    if (tp.kb[tp.C] != zhi) return false;
     tp.nsd.init(tp.NS);
     tp.nbd.init(tp.NB);
     smem = (size_t)tp.NS * tp.stage * 8;
@@ -646,6 +657,8 @@ struct tl_run {
     std::vector<tl::Gauss> h_srcs;
     int64_t launches = 0;
     bool external_global = false;   // global field supplied by the slab solve (multi-GPU)
+    int ext_k0 = 0;                 // external mode: first stored global plane
+    double* Tg_store = nullptr;     // external mode: planes [ext_k0, NZ); Tg = Tg_store - ext_k0 nxy
     bool timing = false;
     std::vector<cudaEvent_t> ev;     // pairs
     std::vector<int> ev_level;
@@ -696,6 +709,14 @@ int32_t tl_device_query(int32_t device, int32_t* sm_count, int64_t* l2_bytes, in
 // ------------------------------------------------------------------------------------
 // Single step on host buffers (seam 3: fem.step_backward_euler for a linear problem).
 // ------------------------------------------------------------------------------------
+static float g_step_last_ms = 0.0f;
+
+int32_t tl_step_last_ms(float* ms) {
+    if (!ms) return fail(TL_E_INVALID, "null argument");
+    *ms = g_step_last_ms;
+    return TL_OK;
+}
+
 int32_t tl_step_host(const tl_grid_desc* grid, double kappa, double rho_c, double dt,
                      int32_t dirichlet_kind, const double* gA, const double* gB, double w,
                      double g_const, const double* T_old, const double* load,
@@ -721,6 +742,7 @@ int32_t tl_step_host(const tl_grid_desc* grid, double kappa, double rho_c, doubl
         double* ws = nullptr;
         size_t cap = 0;
         cudaStream_t st = nullptr;      // the step's own stream: no device-wide synchronisation
+        cudaEvent_t ev0 = nullptr, ev1 = nullptr;   // solve launch timing (tl_step_last_ms)
     };
     static StepWs wss[64];
     static std::mutex ws_mu;
@@ -770,12 +792,19 @@ int32_t tl_step_host(const tl_grid_desc* grid, double kappa, double rho_c, doubl
         for (int a = 0; a < 3; ++a) P.src.center[a] = src->center[a];
         P.src.on = 1;
     }
+    if (!W.ev0) {
+        TL_CUDA(cudaEventCreate(&W.ev0));
+        TL_CUDA(cudaEventCreate(&W.ev1));
+    }
+    TL_CUDA(cudaEventRecord(W.ev0, st));
     rc = launch_solve(P, gauss, sms, xg, st, nullptr, dspec);
     if (rc) return rc;
+    TL_CUDA(cudaEventRecord(W.ev1, st));
     tl::SolveInfoDev hi{};
     TL_CUDA(cudaMemcpyAsync(&hi, dinfo, sizeof(hi), cudaMemcpyDeviceToHost, st));
     TL_CUDA(cudaMemcpyAsync(x_out, T, nb, cudaMemcpyDeviceToHost, st));
     TL_CUDA(cudaStreamSynchronize(st));
+    TL_CUDA(cudaEventElapsedTime(&g_step_last_ms, W.ev0, W.ev1));
     if (info) {
         info->iterations = hi.iterations; info->status = hi.status; info->bnorm = hi.bnorm;
         info->rnorm = hi.rnorm; info->true_resid = hi.true_resid;
@@ -1324,20 +1353,37 @@ int32_t tl_run_create(const tl_run_desc* desc, tl_run** out) {
     if (gauss_smem(R->L) > 200 * 1024) { delete R; return fail(TL_E_INVALID, "local grid too long"); }
     TL_CUDA(cudaStreamCreateWithFlags(&R->stream, cudaStreamNonBlocking));
     const int ng = R->G.n, nl = R->L.n;
-    if ((rc = dalloc(&R->Tg, ng)) || (rc = dalloc(&R->bg, ng)) || (rc = dalloc(&R->rg, ng)) ||
-        (rc = dalloc(&R->pg0, ng)) || (rc = dalloc(&R->pg1, ng)) || (rc = dalloc(&R->qg, ng)) ||
-        (rc = dalloc(&R->loadg, ng)) || (rc = dalloc(&R->Tl, nl)) || (rc = dalloc(&R->bl, nl)) ||
+    const size_t gnxy = (size_t)R->G.NX * R->G.NY;
+    if (desc->external_planes < 0 || desc->external_planes > R->G.NZ) {
+        delete R;
+        return fail(TL_E_INVALID, "external_planes out of range");
+    }
+    if (desc->external_planes > 0) {
+        // the global field comes from the z-slab solve: keep only its top planes (the
+        // local box's P1 support) and no global solver workspace
+        R->external_global = true;
+        R->ext_k0 = R->G.NZ - desc->external_planes;
+        if ((rc = dalloc(&R->Tg_store, gnxy * desc->external_planes))) { tl_run_destroy(R); return rc; }
+        R->Tg = R->Tg_store - (ptrdiff_t)((size_t)R->ext_k0 * gnxy);
+    } else if ((rc = dalloc(&R->Tg, ng)) || (rc = dalloc(&R->bg, ng)) || (rc = dalloc(&R->rg, ng)) ||
+               (rc = dalloc(&R->pg0, ng)) || (rc = dalloc(&R->pg1, ng)) || (rc = dalloc(&R->qg, ng)) ||
+               (rc = dalloc(&R->loadg, ng))) {
+        tl_run_destroy(R);
+        return rc;
+    }
+    const int nxg = R->external_global ? nl : std::max(ng, nl);
+    if ((rc = dalloc(&R->Tl, nl)) || (rc = dalloc(&R->bl, nl)) ||
         (rc = dalloc(&R->rl, nl)) || (rc = dalloc(&R->pl0, nl)) || (rc = dalloc(&R->pl1, nl)) ||
         (rc = dalloc(&R->ql, nl)) || (rc = dalloc(&R->tr_old, nl)) || (rc = dalloc(&R->tr_pred, nl)) ||
         (rc = dalloc(&R->Tl_before, nl)) || (rc = dalloc(&R->part, tl::kPartLen)) ||
         (rc = dalloc(&R->dep_prev, tl::kDepMax)) || (rc = dalloc(&R->dep_prev_n, 1)) ||
         (rc = dalloc(&R->melt, 4)) || (rc = dalloc(&R->melt_part, 2 * 1184)) ||
-        (rc = dalloc(&R->xg, 4 * (size_t)std::max(ng, nl))) || (rc = dalloc(&R->d_specs, 64))) {
+        (rc = dalloc(&R->xg, 4 * (size_t)nxg)) || (rc = dalloc(&R->d_specs, 64))) {
         tl_run_destroy(R);
         return rc;
     }
     R->specs_cap = 64;
-    TL_CUDA(cudaMemsetAsync(R->loadg, 0, sizeof(double) * ng, R->stream));
+    if (R->loadg) TL_CUDA(cudaMemsetAsync(R->loadg, 0, sizeof(double) * ng, R->stream));
     TL_CUDA(cudaMemsetAsync(R->dep_prev_n, 0, sizeof(int), R->stream));
     TL_CUDA(cudaMemsetAsync(R->tr_old, 0, sizeof(double) * nl, R->stream));
     TL_CUDA(cudaMemsetAsync(R->tr_pred, 0, sizeof(double) * nl, R->stream));
@@ -1350,6 +1396,7 @@ int32_t tl_run_destroy(tl_run* R) {
     if (!R) return TL_OK;
     cudaSetDevice(R->device);
     if (R->stream) cudaStreamSynchronize(R->stream);
+    if (R->external_global) R->Tg = R->Tg_store;
     double* bufs[] = {R->Tg, R->bg, R->rg, R->pg0, R->pg1, R->qg, R->loadg, R->Tl, R->bl, R->rl, R->pl0,
                       R->pl1, R->ql, R->tr_old, R->tr_pred, R->Tl_before, R->part, R->dep_pts,
                       R->dep_pow, R->melt, R->melt_part, R->flush, R->xg, R->gload};
@@ -1391,7 +1438,9 @@ int32_t tl_run_initial(tl_run* R, double T0) {
     if (!R) return fail(TL_E_INVALID, "null run");
     TL_CUDA(cudaSetDevice(R->device));
     for (int a = 0; a < 3; ++a) R->L.off[a] = R->desc.local_grid.offset[a];   // initial placement
-    tl::k_fill<<<4 * R->sms, 256, 0, R->stream>>>(R->Tg, R->G.n, T0);
+    const size_t gnxy = (size_t)R->G.NX * R->G.NY;
+    tl::k_fill<<<4 * R->sms, 256, 0, R->stream>>>(R->Tg + R->ext_k0 * gnxy, (int)((size_t)R->G.n - R->ext_k0 * gnxy),
+                                                  T0);
     ++R->launches;
     TL_CUDA(cudaGetLastError());
     return run_interp_local(R, 0, R->Tl, R->tr_old);
@@ -1399,6 +1448,7 @@ int32_t tl_run_initial(tl_run* R, double T0) {
 
 int32_t tl_run_set_global(tl_run* R, const double* Tg_host, int64_t n) {
     if (!R || !Tg_host || n != R->G.n) return fail(TL_E_INVALID, "global field size mismatch");
+    if (R->external_global) return fail(TL_E_INVALID, "external-global run: use tl_run_put_global_planes");
     TL_CUDA(cudaSetDevice(R->device));
     for (int a = 0; a < 3; ++a) R->L.off[a] = R->desc.local_grid.offset[a];   // initial placement
     TL_CUDA(cudaMemcpyAsync(R->Tg, Tg_host, sizeof(double) * n, cudaMemcpyHostToDevice, R->stream));
@@ -1573,6 +1623,7 @@ int32_t tl_run_macro_steps(tl_run* R, const tl_macro_plan* plans, int32_t nsteps
         if (mp.dep_count < 0 || mp.dep_offset < 0 || mp.dep_offset + mp.dep_count > ndep)
             return fail(TL_E_INVALID, "deposit plan out of range");
         if (mp.dep_count * 4 > tl::kDepMax) return fail(TL_E_INVALID, "too many deposit samples in one step");
+        if (mp.record && R->external_global) return fail(TL_E_INVALID, "external-global runs keep no snapshots");
         need += (R->external_global ? 0 : 1) + mp.n_micro + mp.corrector;
     }
     if (int rc = ensure_info(R, need)) return rc;
@@ -1674,6 +1725,7 @@ int32_t tl_run_get_field(tl_run* R, int32_t which, double* host, int64_t n) {
     const double* src = which == 0 ? R->Tg : (which == 1 ? R->Tl : R->tr_old);
     const int64_t want = which == 0 ? R->G.n : R->L.n;
     if (which < 0 || which > 2 || n != want) return fail(TL_E_INVALID, "field selector or size mismatch");
+    if (which == 0 && R->external_global) return fail(TL_E_INVALID, "external-global run holds no global field");
     TL_CUDA(cudaMemcpyAsync(host, src, sizeof(double) * n, cudaMemcpyDeviceToHost, R->stream));
     TL_CUDA(cudaStreamSynchronize(R->stream));
     return TL_OK;
@@ -1686,6 +1738,7 @@ int32_t tl_run_field_async(tl_run* R, int32_t which, double* host, int64_t n, in
     const double* src = which == 0 ? R->Tg : (which == 1 ? R->Tl : R->tr_old);
     const int64_t want = which == 0 ? R->G.n : R->L.n;
     if (which < 0 || which > 2 || n != want) return fail(TL_E_INVALID, "field selector or size mismatch");
+    if (which == 0 && R->external_global) return fail(TL_E_INVALID, "external-global run holds no global field");
     if (!R->copy_stream) TL_CUDA(cudaStreamCreateWithFlags(&R->copy_stream, cudaStreamNonBlocking));
     if (!R->stage_ready[slot]) {
         TL_CUDA(cudaEventCreateWithFlags(&R->stage_ready[slot], cudaEventDisableTiming));
@@ -1741,7 +1794,9 @@ int32_t tl_run_melt_summary(tl_run* R, double T_liquidus, double* out4) {
     if (!R || !out4) return fail(TL_E_INVALID, "null argument");
     TL_CUDA(cudaSetDevice(R->device));
     const int nb = 4 * R->sms;
-    tl::k_melt_partial<<<nb, 256, 0, R->stream>>>(R->Tg, R->G.n, T_liquidus, R->melt_part);
+    const size_t gnxy = (size_t)R->G.NX * R->G.NY;     // external mode: the stored planes
+    tl::k_melt_partial<<<nb, 256, 0, R->stream>>>(R->Tg + R->ext_k0 * gnxy,
+                                                  (int)((size_t)R->G.n - R->ext_k0 * gnxy), T_liquidus, R->melt_part);
     tl::k_melt_final<<<1, 32, 0, R->stream>>>(R->melt_part, nb, R->melt + 0, R->melt + 2);
     tl::k_melt_partial<<<nb, 256, 0, R->stream>>>(R->Tl, R->L.n, T_liquidus, R->melt_part);
     tl::k_melt_final<<<1, 32, 0, R->stream>>>(R->melt_part, nb, R->melt + 1, R->melt + 3);
@@ -1820,15 +1875,16 @@ int32_t tl_run_flush_l2(tl_run* R) {
     return TL_OK;
 }
 
-int32_t tl_run_set_external_global(tl_run* R, int32_t on) {
-    if (!R) return fail(TL_E_INVALID, "null run");
-    R->external_global = on != 0;
-    return TL_OK;
+int32_t tl_run_reanchor(tl_run* R, const double* offset) {
+    if (!R || !offset) return fail(TL_E_INVALID, "null argument");
+    TL_CUDA(cudaSetDevice(R->device));
+    for (int a = 0; a < 3; ++a) R->L.off[a] = offset[a];
+    return run_interp_local(R, 0, R->Tl, R->tr_old);
 }
 
 int32_t tl_run_put_global_planes(tl_run* R, const double* src, int32_t k0, int32_t k1) {
     if (!R || !src) return fail(TL_E_INVALID, "null argument");
-    if (k0 < 0 || k1 > R->G.NZ || k0 >= k1) return fail(TL_E_INVALID, "bad plane range");
+    if (k0 < R->ext_k0 || k1 > R->G.NZ || k0 >= k1) return fail(TL_E_INVALID, "bad plane range");
     TL_CUDA(cudaSetDevice(R->device));
     const size_t nxy = (size_t)R->G.NX * R->G.NY;
     TL_CUDA(cudaMemcpyAsync(R->Tg + (size_t)k0 * nxy, src, sizeof(double) * nxy * (k1 - k0),
@@ -1866,15 +1922,52 @@ static int slab_params(const tl_slab* s, tl::SlabParams& S, int& blocks, cudaStr
     if (dev < 0 || dev >= 64) return fail(TL_E_INVALID, "device index");
     if (!sms_cache[dev])
         if (int rc = device_sms(dev, sms_cache[dev])) return rc;
-    blocks = 3 * sms_cache[dev];          // k_slab_direction / k_slab_update: 3 CTAs per SM
+    blocks = 3 * sms_cache[dev];          // flat slab kernels: 3 CTAs per SM
     if (blocks > tl::kSlabMaxBlocks) blocks = tl::kSlabMaxBlocks;
     st = (cudaStream_t)s->stream;
     return TL_OK;
 }
 
-// work layout: [4 kSlabMaxBlocks partials][counter][deposit count][deposit nodes kDepMax ints]
+// work layout (doubles): [4 kSlabMaxBlocks partials][counter][deposit count][deposit nodes
+// kDepMax ints] [control block][item partials 3 kTMaxItems][boundary partials
+// 2 kSlabMaxBlocks][tiled arrival counter, item counter]
 constexpr int64_t kSlabDepOff = 4 * (int64_t)tl::kSlabMaxBlocks + 1;
-int64_t tl_slab_work_len(void) { return kSlabDepOff + 1 + tl::kDepMax / 2; }
+constexpr int64_t kSlabCtlOff = (kSlabDepOff + 1 + tl::kDepMax / 2 + 7) / 8 * 8;
+constexpr int64_t kSlabIPartOff = kSlabCtlOff + 16;
+constexpr int64_t kSlabBPartOff = kSlabIPartOff + 3 * (int64_t)tl::kTMaxItems;
+constexpr int64_t kSlabCntOff = kSlabBPartOff + 2 * (int64_t)tl::kSlabMaxBlocks;
+static_assert(sizeof(tl::SlabCtl) <= 16 * sizeof(double), "control block");
+int64_t tl_slab_work_len(void) { return kSlabCntOff + 2; }
+
+static int slab_dev(const tl_slab* s, tl::SlabDev& D, int& blocks, cudaStream_t& st) {
+    if (int rc = slab_params(s, D.S, blocks, st)) return rc;
+    if (s->world < 1 || (!s->gath && s->world > 1)) return fail(TL_E_INVALID, "bad slab world / gather buffer");
+    // the bulk copies read 16-byte-aligned ranges addressed by global node id
+    if ((reinterpret_cast<uintptr_t>(D.S.x) | reinterpret_cast<uintptr_t>(D.S.r) |
+         reinterpret_cast<uintptr_t>(D.S.p0) | reinterpret_cast<uintptr_t>(D.S.p1)) & 15)
+        return fail(TL_E_INVALID, "slab arrays: the address of global node 0 (x - first stored id) must be "
+                                  "16-byte aligned");
+    D.k0 = s->k0;
+    D.k1 = s->k1;
+    D.world = s->world;
+    D.gath = s->gath ? s->gath : s->sums;
+    D.ctl = reinterpret_cast<tl::SlabCtl*>(s->work + kSlabCtlOff);
+    D.ipart = s->work + kSlabIPartOff;
+    D.bpart = s->work + kSlabBPartOff;
+    D.icount = reinterpret_cast<unsigned*>(s->work + kSlabCntOff);
+    D.ictr = reinterpret_cast<unsigned*>(s->work + kSlabCntOff + 1);
+    D.nbnd = 0;
+    return TL_OK;
+}
+
+// planes a neighbour reads (sent after the update): k0 if there is a rank below, k1 - 1 if
+// there is one above
+static void slab_boundary(const tl_slab* s, int& lo0, int& hi0, int& lo1, int& hi1) {
+    const int NZ = s->grid.ncells[2] + 1;
+    lo0 = hi0 = lo1 = hi1 = s->k0;
+    if (s->k0 > 0) { lo0 = s->k0; hi0 = s->k0 + 1; }
+    if (s->k1 < NZ && s->k1 - 1 >= hi0) { lo1 = s->k1 - 1; hi1 = s->k1; }
+}
 
 int32_t tl_slab_deposit(const tl_slab* s, const double* points, const double* power, int32_t count) {
     tl::SlabParams S{};
@@ -1892,11 +1985,14 @@ int32_t tl_slab_deposit(const tl_slab* s, const double* points, const double* po
     return TL_OK;
 }
 
-int32_t tl_slab_rhs(const tl_slab* s, const tl_gaussian* src) {
-    tl::SlabParams S{};
+int32_t tl_slab_begin(const tl_slab* s, const tl_gaussian* src) {
+    tl::SlabDev D{};
     int blocks = 0;
     cudaStream_t st;
-    if (int rc = slab_params(s, S, blocks, st)) return rc;
+    if (int rc = slab_dev(s, D, blocks, st)) return rc;
+    if (!(s->rtol > 0.0) || s->maxiter < 1) return fail(TL_E_INVALID, "bad solver settings");
+    tl::k_sd_begin<<<1, 1, 0, st>>>(D.ctl, s->rtol, s->maxiter);
+    tl::SlabParams& S = D.S;
     if (src && src->on) {
         S.src.peak = src->peak; S.src.radius = src->radius; S.src.depth = src->depth;
         for (int a = 0; a < 3; ++a) S.src.center[a] = src->center[a];
@@ -1912,43 +2008,104 @@ int32_t tl_slab_rhs(const tl_slab* s, const tl_gaussian* src) {
     return TL_OK;
 }
 
-int32_t tl_slab_direction(const tl_slab* s, int32_t first, double beta, int32_t parity) {
-    tl::SlabParams S{};
+}  // extern "C"
+template <class K>
+static cudaError_t launch_sd_tiled(K kern, const tl::SlabDev& D, const tl::TPlan& tp, size_t smem, int sms,
+                                   cudaStream_t st) {
+    cudaError_t e = ensure_smem_attr((const void*)kern, smem);
+    if (e != cudaSuccess) return e;
+    kern<<<sms, (kTNCW + 1) * 32, smem, st>>>(D, tp);
+    return cudaGetLastError();
+}
+extern "C" {
+
+int32_t tl_slab_direction(const tl_slab* s) {
+    tl::SlabDev D{};
     int blocks = 0;
     cudaStream_t st;
-    if (int rc = slab_params(s, S, blocks, st)) return rc;
-    tl::k_slab_direction<<<blocks, tl::kSlabTPB, 0, st>>>(S, first ? 1 : 0, beta, parity & 1);
-    TL_CUDA(cudaGetLastError());
+    if (int rc = slab_dev(s, D, blocks, st)) return rc;
+    int dev = 0, sms = 0;
+    TL_CUDA(cudaGetDevice(&dev));
+    if (int rc = device_sms(dev, sms)) return rc;
+    tl::TPlan tp{};
+    size_t smem = 0;
+    if (!tiled_plan_range(D.S.g, sms, s->k0, s->k1, tp, smem)) return fail(TL_E_INVALID, "no item plan for the slab");
+    const bool two = tp.H * D.S.g.NX <= 2 * kTNCW * 32;
+    cudaError_t e = two ? launch_sd_tiled(tl::k_sd_dir<kTNCW, 2>, D, tp, smem, sms, st)
+                        : launch_sd_tiled(tl::k_sd_dir<kTNCW, 4>, D, tp, smem, sms, st);
+    if (e != cudaSuccess) return fail(TL_E_CUDA, std::string("slab direction: ") + cudaGetErrorString(e));
     return TL_OK;
 }
 
-int32_t tl_slab_update(const tl_slab* s, double alpha, int32_t parity) {
-    tl::SlabParams S{};
+int32_t tl_slab_update(const tl_slab* s, int32_t part) {
+    tl::SlabDev D{};
     int blocks = 0;
     cudaStream_t st;
-    if (int rc = slab_params(s, S, blocks, st)) return rc;
-    tl::k_slab_update<<<blocks, tl::kSlabTPB, 0, st>>>(S, alpha, parity & 1);
-    TL_CUDA(cudaGetLastError());
+    if (int rc = slab_dev(s, D, blocks, st)) return rc;
+    int lo0, hi0, lo1, hi1;
+    slab_boundary(s, lo0, hi0, lo1, hi1);
+    if (part == 0) {                       // the planes the neighbours read
+        if (hi0 > lo0 || hi1 > lo1) {
+            tl::k_sd_upd_flat<<<blocks, tl::kSlabTPB, 0, st>>>(D, lo0, hi0, lo1, hi1);
+            TL_CUDA(cudaGetLastError());
+        }
+        return TL_OK;
+    }
+    if (part != 1) return fail(TL_E_INVALID, "update part must be 0 (boundary) or 1 (rest)");
+    D.nbnd = (hi0 > lo0 || hi1 > lo1) ? blocks : 0;
+    const int zlo = hi0 > lo0 ? hi0 : s->k0;
+    const int zhi = hi1 > lo1 ? lo1 : s->k1;
+    int dev = 0, sms = 0;
+    TL_CUDA(cudaGetDevice(&dev));
+    if (int rc = device_sms(dev, sms)) return rc;
+    tl::TPlan tp{};
+    size_t smem = 16;
+    if (zhi > zlo) {
+        if (!tiled_plan_range(D.S.g, sms, zlo, zhi, tp, smem)) return fail(TL_E_INVALID, "no item plan for the slab");
+    } else {
+        tp.I = 0;                          // nothing beyond the boundary planes: sum their partials
+    }
+    const bool two = tp.I == 0 || tp.H * D.S.g.NX <= 2 * kTNCW * 32;
+    cudaError_t e = two ? launch_sd_tiled(tl::k_sd_upd<kTNCW, 2>, D, tp, smem, sms, st)
+                        : launch_sd_tiled(tl::k_sd_upd<kTNCW, 4>, D, tp, smem, sms, st);
+    if (e != cudaSuccess) return fail(TL_E_CUDA, std::string("slab update: ") + cudaGetErrorString(e));
     return TL_OK;
 }
 
 int32_t tl_slab_residual(const tl_slab* s) {
-    tl::SlabParams S{};
+    tl::SlabDev D{};
     int blocks = 0;
     cudaStream_t st;
-    if (int rc = slab_params(s, S, blocks, st)) return rc;
-    tl::k_slab_residual<<<blocks, tl::kSlabTPB, 0, st>>>(S);
+    if (int rc = slab_dev(s, D, blocks, st)) return rc;
+    tl::k_sd_resid<<<blocks, tl::kSlabTPB, 0, st>>>(D);
     TL_CUDA(cudaGetLastError());
     return TL_OK;
 }
 
 int32_t tl_slab_finish(const tl_slab* s) {
-    tl::SlabParams S{};
+    tl::SlabDev D{};
     int blocks = 0;
     cudaStream_t st;
-    if (int rc = slab_params(s, S, blocks, st)) return rc;
-    tl::k_slab_finish<<<blocks, tl::kSlabTPB, 0, st>>>(S);
+    if (int rc = slab_dev(s, D, blocks, st)) return rc;
+    tl::k_sd_finish<<<blocks, tl::kSlabTPB, 0, st>>>(D);
     TL_CUDA(cudaGetLastError());
+    return TL_OK;
+}
+
+int32_t tl_slab_poll(const tl_slab* s, int32_t* state, tl_solve_info* info) {
+    if (!s || !s->work || !state) return fail(TL_E_INVALID, "null argument");
+    cudaStream_t st = (cudaStream_t)s->stream;
+    tl::SlabCtl c{};
+    TL_CUDA(cudaMemcpyAsync(&c, s->work + kSlabCtlOff, sizeof(c), cudaMemcpyDeviceToHost, st));
+    TL_CUDA(cudaStreamSynchronize(st));
+    *state = c.done;
+    if (info) {
+        info->iterations = c.status == 1 ? c.maxiter : c.it;
+        info->status = c.status;
+        info->bnorm = c.bnorm;
+        info->rnorm = c.rnorm;
+        info->true_resid = c.true_resid;
+    }
     return TL_OK;
 }
 

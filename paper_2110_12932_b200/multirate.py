@@ -38,7 +38,7 @@ __all__ = ["MacroSchedule", "DeviceRun", "DeviceFieldState", "run_spacetime", "r
            "predictor_global", "interpolate_trace", "release_device_runs"]
 
 
-def _run_desc(problem: TwoLevelProblem, local_mesh: StructuredGrid) -> N.RunDesc:
+def _run_desc(problem: TwoLevelProblem, local_mesh: StructuredGrid, external_planes: int = 0) -> N.RunDesc:
     kappa, rcg, rcl = problem.constants()
     beam = problem.beam
     desc = N.RunDesc()
@@ -55,20 +55,24 @@ def _run_desc(problem: TwoLevelProblem, local_mesh: StructuredGrid) -> N.RunDesc
     desc.max_micro = 64
     desc.max_deposit = 512
     desc.device = problem.device
+    desc.external_planes = int(external_planes)
     return desc
 
 
 class DeviceRun:
     """Owns one ``tl_run``: both grids' fields and solver workspace on the GPU."""
 
-    def __init__(self, problem: TwoLevelProblem, local_mesh: StructuredGrid):
+    def __init__(self, problem: TwoLevelProblem, local_mesh: StructuredGrid, external_planes: int = 0):
+        """``external_planes`` > 0: a local-only run of the multi-GPU driver (the global field
+        arrives from the z-slab solve; only its top ``external_planes`` planes are stored)."""
         problem.check_device_supported()
         if not problem.one_way:
             raise UnsupportedOnDevice("the device-resident run is one-way; two-way coupling runs "
                                       "through the step-level drivers (run_spacetime / run_space)")
         self.problem = problem
         self.local_mesh = local_mesh
-        desc = _run_desc(problem, local_mesh)
+        desc = _run_desc(problem, local_mesh, external_planes)
+        self.external_planes = int(external_planes)
         self._h = C.c_void_p()
         N.check(N.lib().tl_run_create(C.byref(desc), C.byref(self._h)), "tl_run_create")
         self.n_global = problem.global_mesh.n_nodes
@@ -255,6 +259,12 @@ class DeviceFieldState(FieldState):
 
     def __reduce__(self):
         return (FieldState, (self.mesh, self.values, self.time))
+
+    __hash__ = object.__hash__          # identity: the owning run tracks it in a WeakSet
+
+    def __repr__(self):
+        return (f"DeviceFieldState(mesh={self.mesh!r}, time={self.time!r}, "
+                f"{'on device' if self._v is None else 'read back'})")
 
 
 # One idle tl_run per problem descriptor, reused by the next run_spacetime / run_space call

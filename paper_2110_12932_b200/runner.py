@@ -118,9 +118,11 @@ def two_level_run(cfg, spacetime: bool | None = None, dt_macro: float | None = N
 def two_level_run_slabs(cfg, stats: RunStats | None = None, n_steps: int | None = None,
                         device=None, group=None, resolve_corrector: bool = True):
     """Multirate two-level run with the global grid z-slab-decomposed over the ranks of
-    the current process group (one process per GPU); see ``multirate_dist``.
+    the current process group (one process per GPU) and the local problem pipelined over
+    the ranks in time; see ``multirate_dist``.
 
-    Returns (state, stats) on the top rank and (None, stats) on the others."""
+    Returns (state, stats) on the rank that ran the last macro step's local part and
+    (None, stats) on the others."""
     from .multirate_dist import run_spacetime_slabs
     c = convert_config(cfg)
     if c["mode"] == "two-level-space":

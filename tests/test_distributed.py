@@ -150,3 +150,98 @@ def test_gloo_halo_exchange_and_rank_ordered_sums(world):
     for r in range(world):                            # the rank order is the summation order
         expect = [e + v * (r + 1) for e, v in zip(expect, [1e16, 1.0, -1e16, 0.5])]
     assert tots[0] == expect
+
+
+# ---- the multi-GPU two-level driver: chains, super-steps, device-side sums -------------
+
+from paper_2110_12932_b200 import multirate_dist as MD  # noqa: E402
+
+
+def test_chain_ranks_every_step_relocates():
+    """BASELINE configs move the box after every step: every step starts a chain and the
+    chains go round-robin over the ranks."""
+    starts, ranks, used = MD.chain_ranks(True, [True] * 5, 0, 3)
+    assert starts == [True] * 5 and ranks == [0, 1, 2, 0, 1] and used == 5
+    starts, ranks, used = MD.chain_ranks(True, [True] * 3, 7, 4)
+    assert ranks == [3, 0, 1] and used == 3
+
+
+def test_chain_ranks_keep_non_relocating_steps_together():
+    """A step after which the box does not move continues its chain on the same rank (its
+    local field carries over, multirate.py:184-190)."""
+    starts, ranks, used = MD.chain_ranks(True, [False, True, False, False, True], 0, 2)
+    assert starts == [True, False, True, False, False]
+    assert ranks == [0, 0, 1, 1, 1] and used == 2
+    starts, ranks, used = MD.chain_ranks(False, [True, True], 4, 2)   # continues chain 3
+    assert starts == [False, True] and ranks == [1, 0] and used == 1
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_plan_superstep_covers_world_chains(world):
+    """A super-step holds exactly `world` whole chains (one per rank) and consecutive
+    super-steps tile the schedule with the same plans as one-step planning."""
+    import paper_2110_12932_b200 as P
+    from paper_2110_12932_b200.schedule import plan_spacetime
+    from .conftest import CONFIGS
+    cfg = P.load_config(CONFIGS / "cfg1_m4.cfg")
+    problem, lm = P.build_problem(cfg)
+    sched = P.MacroSchedule(cfg.dt_macro, cfg.micro_steps, 0.0, cfg.t_end)
+    state, moved_before, got = (lm.placement, 0.0, 0.0, 0), True, []
+    while True:
+        plans, nxt = MD.plan_superstep(problem, sched, cfg.path, cfg.policy, *state, world, moved_before)
+        if not plans:
+            break
+        starts, ranks, used = MD.chain_ranks(moved_before, [bool(p.moved[0]) for p in plans], 0, world)
+        assert used <= world and (used == world or nxt[3] == sched.n_macro)
+        assert sorted(set(ranks)) == list(range(used))
+        got.extend(plans)
+        moved_before = bool(plans[-1].moved[0])
+        state = nxt
+    assert len(got) == sched.n_macro
+    placement, tg, tl = lm.placement, 0.0, 0.0
+    for k, pl in enumerate(got):
+        ref = plan_spacetime(problem, sched, placement, cfg.path, cfg.policy, tg, tl, k0=k, nsteps=1)
+        assert pl.macro.tobytes() == ref.macro.tobytes() and pl.micro.tobytes() == ref.micro.tobytes()
+        placement, tg, tl = ref.final_placement, ref.final_t_global, ref.final_t_local
+
+
+def _comm_worker(rank, world, port, q):
+    import numpy as np
+    import torch
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        nz, nxy = 9, 4
+        k0, k1 = SL.plane_partition(nz, world)[rank]
+        h0, h1 = SL.stored_planes(k0, k1, nz)
+        comm = SL.SlabComm(rank, world, k0, k1, h0, nxy)
+        sums = torch.arange(SL.SUMS, dtype=torch.float64) + 10.0 * rank
+        gath = torch.zeros(world * SL.SUMS, dtype=torch.float64)
+        comm.allgather(sums, gath)
+        ok_g = np.array_equal(gath.numpy().reshape(world, SL.SUMS),
+                              np.stack([np.arange(SL.SUMS) + 10.0 * r for r in range(world)]))
+        buf = torch.full(((h1 - h0) * nxy,), -1.0, dtype=torch.float64)
+        for k in range(k0, k1):
+            buf[(k - h0) * nxy:(k - h0 + 1) * nxy] = float(k)
+        comm.halo_wait(comm.halo_start(buf))
+        ok_h = all(np.all(buf.view(h1 - h0, nxy).numpy()[k - h0] == k) for k in range(h0, h1))
+        q.put((rank, ok_g, ok_h))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_slab_comm_allgather_rank_order_and_halo(world):
+    """SlabComm: every rank's 8 partial sums land in rank order in the gather buffer the
+    kernels read; halo start/wait fills each stored halo plane with the neighbour's plane."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_comm_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(g and h for _, g, h in out)

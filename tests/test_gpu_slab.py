@@ -21,6 +21,7 @@ from paper_2110_12932_b200 import ops
 from paper_2110_12932_b200 import slab as SL
 
 from .conftest import CONFIGS
+from .conftest import assert_mask
 from .test_gpu_parity import _oracle_step, rel
 
 pytestmark = pytest.mark.gpu
@@ -150,14 +151,16 @@ def _slab_run(world, name, n_steps):
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
-    assert all(out[r] is None for r in range(world - 1))
-    return out[world - 1]
+    have = [r for r in range(world) if out[r] is not None]
+    assert len(have) == 1          # the rank that ran the last step's local part
+    return out[have[0]]
 
 
-@pytest.mark.parametrize("world,name,n_steps", [(2, "cfg1_m4", None), (3, "cfg2", 6)])
+@pytest.mark.parametrize("world,name,n_steps", [(1, "cfg1_m4", 12), (2, "cfg1_m4", None), (3, "cfg2", 6)])
 def test_slab_multirate_run_matches_single_gpu(world, name, n_steps):
-    """Global grid split over ranks, local problem on the top rank: same fields, same
-    relocations and RunStats counters as the single-GPU run; melt masks bit-exact."""
+    """Global grid split over ranks (device-resident CG), local steps pipelined over the
+    ranks in time (chain c on rank c mod world, re-anchored from the global planes): same
+    fields, relocations and RunStats counters as the single-GPU run; melt masks."""
     cfg = P.load_config(CONFIGS / f"{name}.cfg")
     ref, ref_stats = P.two_level_run(cfg, n_steps=n_steps)
     gv, lv, off, counters = _slab_run(world, name, n_steps)
@@ -165,6 +168,6 @@ def test_slab_multirate_run_matches_single_gpu(world, name, n_steps):
     assert counters == dict(ref_stats.counters)
     assert rel(gv, ref.global_field.values) <= 1e-11
     assert rel(lv, ref.local_field.values) <= 1e-11
-    Tl = cfg.material.T_liquidus if hasattr(cfg.material, "T_liquidus") else None
-    if Tl is not None:
-        assert np.array_equal(lv > Tl, ref.local_field.values > Tl)
+    TL = cfg.material.T_liquidus
+    assert_mask(f"slab run {name} x{world} local", lv, ref.local_field.values, TL)
+    assert_mask(f"slab run {name} x{world} global", gv, ref.global_field.values, TL)
