@@ -175,6 +175,17 @@ static bool tiled_enabled() {
 
 static bool tiled_plan_range(const tl::Grid& g, int sms, int zlo, int zhi, tl::TPlan& tp, size_t& smem);
 
+// TLGPU_SNAKE=0: both sweeps of the streaming CG loops walk the grid bottom-up (default 1:
+// sweep B top-down, L2 reuse across the sweeps; tl_tiled.cuh)
+static int snake_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("TLGPU_SNAKE");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v;
+}
+
 static bool tiled_plan(const tl::Grid& g, int sms, tl::TPlan& tp, size_t& smem) {
     static long long nmin = -1;
     if (nmin < 0) {
@@ -217,7 +228,8 @@ static bool tiled_plan_range(const tl::Grid& g, int sms, int zlo, int zhi, tl::T
     int Z = (int)(share / (10.0 * H * NX));
     Z = std::max(zmin, std::min(Z, nzr));
     std::vector<int> cz;
-    const int nch = std::max(1, (nzr + Z - 1) / Z);
+    int nch = std::max(1, (nzr + Z - 1) / Z);
+    if (const char* e = getenv("TLGPU_TC")) nch = std::max(1, std::min(atoi(e), nzr));
     for (int c = 0; c < nch; ++c) cz.push_back(nzr * (c + 1) / nch - nzr * c / nch);
     if ((int)cz.size() > tl::kTMaxChunks) return false;
     tp.C = (int)cz.size();
@@ -228,9 +240,15 @@ static bool tiled_plan_range(const tl::Grid& g, int sms, int zlo, int zhi, tl::T
     if (tp.kb[tp.C] != zhi) return false;
     tp.nsd.init(tp.NS);
     tp.nbd.init(tp.NB);
+    tp.snake = snake_enabled();
     smem = (size_t)tp.NS * tp.stage * 8;
+    if (getenv("TLGPU_VERBOSE"))
+        fprintf(stderr, "[tlgpu] item plan %dx%dx[%d,%d): H=%d NB=%d C=%d I=%d (%.2f per CTA) NS=%d stage=%d B snake=%d\n",
+                g.NX, g.NY, zlo, zhi, tp.H, tp.NB, tp.C, tp.I, (double)tp.I / sms, tp.NS, tp.stage * 8, tp.snake);
     return true;
 }
+
+static unsigned long long* prof_buffer();
 
 static cudaError_t launch_t_cg(tl::PcgParams& P, int Gr, int sms, cudaStream_t st, bool& launched,
                                const tl::TPlan& tp, size_t smem) {
@@ -246,7 +264,9 @@ static cudaError_t launch_t_cg(tl::PcgParams& P, int Gr, int sms, cudaStream_t s
     if (per_sm < 1) return cudaSuccess;
     e = cudaMemsetAsync(P.part + tl::kTCounter, 0, 4 * sizeof(unsigned), st);
     if (e != cudaSuccess) return e;
-    void* args[] = {&P, &Gr, (void*)&tp};
+    tl::TPlan tpl = tp;
+    tpl.prof = prof_buffer();
+    void* args[] = {&P, &Gr, (void*)&tpl};
     e = cudaLaunchCooperativeKernel((void*)kern, sms, (ncw + 1) * 32, args, smem, st);
     launched = e == cudaSuccess;
     return e;
@@ -261,6 +281,8 @@ static int launch_stream(tl::PcgParams& P, int sms, cudaStream_t st, int64_t* la
     const bool use_tiled = tiled_enabled() && tiled_plan(P.g, sms, tp, smem);
     // k_t_cg takes r0 = b and x0 = 0 as implied: the RHS writes b only
     P.light_rhs = use_tiled ? 1 : 0;
+    P.snake = snake_enabled();
+    P.prof = prof_buffer();
     tl::k_s_rhs<<<Gr, tl::kSTPB, 0, st>>>(P);
     cudaError_t e = cudaGetLastError();
     bool tiled = false;
@@ -396,13 +418,15 @@ static cudaError_t launch_rescg_g(tl::ResCGParams& RP, int npt, int G, size_t sm
 }
 
 static unsigned long long* g_prof = nullptr;     // TLGPU_PROF=1: phase timestamps of block 0
+constexpr int kProfLen = 8192;                   // [0, 1024) resident kernels; 1024 + 16 b + slot: k_t_cg CTA b
 
 static unsigned long long* prof_buffer() {
     static int want = -1;
     if (want < 0) {
         const char* e = getenv("TLGPU_PROF");
         want = (e && e[0] == '1') ? 1 : 0;
-        if (want) cudaMalloc((void**)&g_prof, 1024 * sizeof(unsigned long long));
+        if (want && cudaMalloc((void**)&g_prof, kProfLen * sizeof(unsigned long long)) == cudaSuccess)
+            cudaMemset(g_prof, 0, kProfLen * sizeof(unsigned long long));
     }
     return g_prof;
 }
@@ -1820,11 +1844,12 @@ int32_t tl_debug_profile(uint64_t* out, int32_t max, int32_t* count) {
     if (!out || !count) return fail(TL_E_INVALID, "null argument");
     *count = 0;
     if (!g_prof) return TL_OK;
-    unsigned long long h[1024];
+    std::vector<unsigned long long> h(kProfLen);
     TL_CUDA(cudaDeviceSynchronize());
-    TL_CUDA(cudaMemcpy(h, g_prof, sizeof(h), cudaMemcpyDeviceToHost));
-    // slots [0, h[127]) phase stamps, 120..122 setup stamps, 127 = stamp count
-    const int n = std::min(max, 1024);
+    TL_CUDA(cudaMemcpy(h.data(), g_prof, kProfLen * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    // slots [0, h[127]) phase stamps, 120..122 setup stamps, 127 = stamp count; from 1024:
+    // k_t_cg's per-CTA sweep stamps (tl_tiled.cuh)
+    const int n = std::min(max, kProfLen);
     for (int e = 0; e < n; ++e) out[e] = h[e];
     *count = n;
     return TL_OK;

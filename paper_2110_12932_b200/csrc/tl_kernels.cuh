@@ -81,7 +81,15 @@ struct PcgParams {
     int maxiter;
     SolveInfoDev* info;
     int light_rhs;       // k_t_cg path: k_s_rhs writes b only (r0 = b and x0 = 0 are implied)
+    int snake;           // k_s_cg: sweep B walks the grid top-down (TLGPU_SNAKE, tl_stream.cuh)
+    unsigned long long* prof;   // TLGPU_PROF=1: k_s_cg %globaltimer stamps of iteration 3 (slot 1024 + 16 CTA + e)
 };
+
+__device__ __forceinline__ unsigned long long timer_ns() {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    return v;
+}
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

@@ -134,6 +134,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) k_sd_dir(SlabDev D, TPlan t
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     build_class_table(T, threadIdx.x, S.mbase, S.cbase, g.dkind);
+    if (tp.I > 0) t_zero_ring(tp, t_sm);
     __syncthreads();
     const bool producer = (threadIdx.x >> 5) == NCW;
     uint32_t t = 0;
@@ -218,13 +219,15 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) k_sd_upd(SlabDev D, TPlan t
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     build_class_table(T, threadIdx.x, S.mbase, S.cbase, g.dkind);
+    if (tp.I > 0) t_zero_ring(tp, t_sm);
     __syncthreads();
     const bool producer = (threadIdx.x >> 5) == NCW;
     uint32_t t = 0;
     if (tp.I > 0) {
         if (producer) {
             if ((threadIdx.x & 31) == 0)
-                t_produce<true>(g, tp, t_sm, full, empty, s_item, D.ictr, t, false, S.r, nullptr, pnew, S.x);
+                t_produce<true>(g, tp, t_sm, full, empty, s_item, D.ictr, t, false, S.r, nullptr, pnew, S.x,
+                                tp.snake != 0);
         } else {
             // item partials: slot 0 r.z, slot 1 r.r (t_consume_b's order)
             t_consume_b<NCW, NPT>(g, tp, T, full, empty, s_item, t, alpha, false, S.x, S.r, D.ipart, ired);

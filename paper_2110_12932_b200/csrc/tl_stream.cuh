@@ -217,7 +217,10 @@ __global__ void __launch_bounds__(kSTPB, MINB) k_s_cg(PcgParams P, int Grhs) {
     double rho_prev = 1.0;
     double* pold = P.p0;
     double* pnew = P.p1;
-    const int beg = blockIdx.x * kSTPB + threadIdx.x, stride = G * kSTPB;
+    // CTA b takes the full 512-node chunks b, b + G, ...; the last CTA also the partial one
+    const int stride = G * kSTPB;
+    const int nfull = g.n / kSTPB, ptail = nfull * kSTPB + threadIdx.x;
+    const bool tail = blockIdx.x == G - 1 && ptail < g.n;
     if (bb != 0.0) {
         while (true) {
             if (rnorm < atol) { status = 0; break; }
@@ -226,43 +229,62 @@ __global__ void __launch_bounds__(kSTPB, MINB) k_s_cg(PcgParams P, int Grhs) {
             const double rho = rz;
             const double beta = it > 0 ? rho / rho_prev : 0.0;
             const bool first = it == 0;
+            unsigned long long* pf = (P.prof && it == 3 && threadIdx.x == 0 && blockIdx.x < 448)
+                                         ? P.prof + 1024 + 16 * blockIdx.x : nullptr;
+            if (pf) pf[0] = timer_ns();
             double pq[1] = {0.0};
             {
-                int p = beg;
+                int c = blockIdx.x;
                 if (UNR == 2)
-                    for (; p + stride < g.n; p += 2 * stride) {
+                    for (; c + G < nfull; c += 2 * G) {
+                        const int p = c * kSTPB + threadIdx.x;
                         const double a = s_sweep_a_node(g, T, p, P.r, pold, pnew, first, beta);
                         const double b = s_sweep_a_node(g, T, p + stride, P.r, pold, pnew, first, beta);
                         pq[0] += a;
                         pq[0] += b;
                     }
-                for (; p < g.n; p += stride) pq[0] += s_sweep_a_node(g, T, p, P.r, pold, pnew, first, beta);
+                for (; c < nfull; c += G)
+                    pq[0] += s_sweep_a_node(g, T, c * kSTPB + threadIdx.x, P.r, pold, pnew, first, beta);
+                if (tail) pq[0] += s_sweep_a_node(g, T, ptail, P.r, pold, pnew, first, beta);
             }
+            if (pf) pf[2] = timer_ns();
             block_sum<1>(pq, red);
             if (threadIdx.x == 0) part[blockIdx.x] = pq[0];
             grid.sync();
+            if (pf) pf[3] = timer_ns();
             {
                 const int s[1] = {0};
                 grid_sum_wide<1>(part, s, G, red, tot);
             }
+            if (pf) pf[4] = timer_ns();
             const double alpha = rho / tot[0];
             double a2[2] = {0.0, 0.0};
             {
-                int p = beg;
+                // snake: sweep B walks the 512-node chunks from the top of the grid down, so
+                // it starts on the planes sweep A touched last (still in L2), and the next
+                // sweep A starts where this one ends
+                const int top = P.snake ? nfull - 1 : 0, sg = P.snake ? -1 : 1;
+                int c = blockIdx.x;
                 if (UNR == 2)
-                    for (; p + stride < g.n; p += 2 * stride) {
+                    for (; c + G < nfull; c += 2 * G) {
+                        const int p = (top + sg * c) * kSTPB + threadIdx.x;
                         s_sweep_b_node(g, T, p, P.T, P.r, pnew, alpha, a2[0], a2[1]);
-                        s_sweep_b_node(g, T, p + stride, P.T, P.r, pnew, alpha, a2[0], a2[1]);
+                        s_sweep_b_node(g, T, p + sg * stride, P.T, P.r, pnew, alpha, a2[0], a2[1]);
                     }
-                for (; p < g.n; p += stride) s_sweep_b_node(g, T, p, P.T, P.r, pnew, alpha, a2[0], a2[1]);
+                for (; c < nfull; c += G)
+                    s_sweep_b_node(g, T, (top + sg * c) * kSTPB + threadIdx.x, P.T, P.r, pnew, alpha, a2[0], a2[1]);
+                if (tail) s_sweep_b_node(g, T, ptail, P.T, P.r, pnew, alpha, a2[0], a2[1]);
             }
+            if (pf) pf[6] = timer_ns();
             block_sum<2>(a2, red);
             if (threadIdx.x == 0) { part[G + blockIdx.x] = a2[0]; part[2 * G + blockIdx.x] = a2[1]; }
             grid.sync();
+            if (pf) pf[7] = timer_ns();
             {
                 const int s[2] = {1, 2};
                 grid_sum_wide<2>(part, s, G, red, tot);
             }
+            if (pf) pf[8] = timer_ns();
             rz = tot[0];
             rnorm = sqrt(tot[1]);
             rho_prev = rho;

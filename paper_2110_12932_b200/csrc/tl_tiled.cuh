@@ -27,6 +27,11 @@
 // plane k.  Dot products are reduced per item in a fixed order and the item partials
 // summed in item order by every CTA after the grid barrier: the result does not depend
 // on which CTA ran which item (deterministic despite the dynamic schedule).
+//
+// Snake order (TPlan::snake): sweep A walks the items bottom-up, sweep B top-down.  On
+// grids of a few L2 sizes (cfg4 local, cfg3 global: ~50 MB per vector against 126 MB of
+// L2) a sweep then starts on the planes the previous sweep read and wrote last, which are
+// still in L2 (p and r for sweep B; r and p_old for the next sweep A).
 #pragma once
 
 #include "tl_stream.cuh"
@@ -49,6 +54,8 @@ struct TPlan {
     int RA;         // sweep A: r at [0, RA), p_old at [RA, 2 RA)
     int RB, RX;     // sweep B: p at [0, RB), x at [RB, RB + RX), r at [RB + RX, RB + 2 RX)
     FastDiv nsd, nbd;       // division by NS, NB
+    int snake;      // 1: sweep B takes the items from the top of the grid down (L2 reuse, below)
+    unsigned long long* prof;    // TLGPU_PROF=1: %globaltimer stamps of iteration 3, slot 1024 + 16 CTA + e
     short kb[kTMaxChunks + 1];   // chunk kc = planes [kb[kc], kb[kc + 1])
 };
 
@@ -97,8 +104,18 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
         "l"(src), "r"(bytes), "r"(smem_u32(b))
         : "memory");
 }
+__device__ __forceinline__ unsigned long long t_ns() { return timer_ns(); }
 __device__ __forceinline__ void fence_proxy_async_global() {
     asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// Zero the ring once per launch (all threads; the caller's next CTA barrier orders it
+// before the first bulk copy): the lean plane loops read words no copy ever writes
+// (rows outside the grid) under a zero coupling, so those words must be finite.
+__device__ __forceinline__ void t_zero_ring(const TPlan& tp, double* sm) {
+    const int n = tp.NS * tp.stage;
+    for (int e = threadIdx.x; e < n; e += blockDim.x) sm[e] = 0.0;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 // Item geometry.
@@ -125,14 +142,13 @@ __device__ __forceinline__ unsigned t_bytes(int a, int b) { return (unsigned)(((
 template <bool SWEEP_B>
 __device__ void t_produce(const Grid& g, const TPlan& tp, double* sm, uint64_t* full, uint64_t* empty,
                           int* s_item, unsigned* ctr, uint32_t& t, bool first, const double* r,
-                          const double* pold, const double* pc, const double* x) {
+                          const double* pold, const double* pc, const double* x, bool rev = false) {
     const int NXY = g.NX * g.NY;
     // the first item of every CTA is static (no counter round trip at the sweep start);
     // the rest come from the counter, offset by the grid size
     unsigned next = blockIdx.x;
     while (true) {
-        const int item = (int)next;
-        if (item >= tp.I) {
+        if ((int)next >= tp.I) {
             unsigned ph;
             const int s = t_slot(tp, t, ph);
             mbar_wait(&empty[s], ph ^ 1);
@@ -141,6 +157,9 @@ __device__ void t_produce(const Grid& g, const TPlan& tp, double* sm, uint64_t* 
             ++t;
             return;
         }
+        // rev: the sweep walks the items from the last one down, so it starts on the planes
+        // the previous sweep touched last (still in L2)
+        const int item = rev ? tp.I - 1 - (int)next : (int)next;
         next = gridDim.x + atomicAdd(ctr, 1u);   // the next item's id arrives while this one streams
         const TItem it = t_item(g, tp, item);
         const int ks = SWEEP_B ? max(it.k0 - 1, 0) : it.k0;
@@ -164,7 +183,8 @@ __device__ void t_produce(const Grid& g, const TPlan& tp, double* sm, uint64_t* 
                 const int c = k * NXY + it.j0 * g.NX, d = k * NXY + it.j1 * g.NX;
                 const unsigned nc = centre ? t_bytes(c, d) : 0u;
                 mbar_arrive_tx(&full[s], nb + (x ? 2 : 1) * nc);
-                bulk_g2s(st, pc + t_abeg(a), nb, &full[s]);
+                // the stage starts at row j0 - 1 even where that row does not exist (j0 = 0)
+                bulk_g2s(st + (t_abeg(a) - t_abeg(k * NXY + (it.j0 - 1) * g.NX)), pc + t_abeg(a), nb, &full[s]);
                 if (centre) {
                     if (x) bulk_g2s(st + tp.RB, x + t_abeg(c), nc, &full[s]);
                     bulk_g2s(st + tp.RB + tp.RX, r + t_abeg(c), nc, &full[s]);
@@ -234,6 +254,24 @@ __device__ __forceinline__ double t_pv(int o, int RA, int q, double iv, bool fir
     return first ? z : __dadd_rn(__dmul_rn(beta, t_sm[o + RA + q]), z);
 }
 
+// Shared-memory load by 32-bit shared address: the lean plane loops address the ring from
+// one base register (generic indexing of the extern array costs a shared-window
+// computation per access).  volatile: never hoisted above the mbarrier waits.
+__device__ __forceinline__ double lds64(uint32_t a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+// Sweep A value of p from the stage words at shared address a (r) and a + ra8 (p_old).
+__device__ __forceinline__ double t_pva(uint32_t a, uint32_t ra8, double iv, bool first, double beta) {
+    const double z = __dmul_rn(iv, lds64(a));
+    return first ? z : __dadd_rn(__dmul_rn(beta, lds64(a + ra8)), z);
+}
+// Same after the first iteration: p = beta p_old + z.
+__device__ __forceinline__ double t_pvb(uint32_t a, uint32_t ra8, double iv, double beta) {
+    return __dadd_rn(__dmul_rn(beta, lds64(a + ra8)), __dmul_rn(iv, lds64(a)));
+}
+
 // Per-item node table of a consumer thread: node m of every plane of the item sits at
 // offset off[m] inside the plane, with its x/y class part cxy[m] = cx + 3 cy, the class
 // steps to its x+ / y+ neighbours and flag bits (below).  Every node then runs the same
@@ -250,7 +288,8 @@ struct TNodes {
         auto freec = [&](int a, int b) { return !class_is_dirichlet(a + 3 * b + 9, g.dkind); };
 #pragma unroll
         for (int m = 0; m < NPT; ++m) {
-            const int e = threadIdx.x + m * NT;
+            const int e0 = threadIdx.x + m * NT;
+            const int e = e0 < nn ? e0 : 0;     // no node: addresses of the item's first node, flags 0
             const int jj = (int)g.divX.div((uint32_t)e);
             const int i = e - jj * g.NX, j = it.j0 + jj;
             off[m] = i + g.NX * j;
@@ -260,13 +299,16 @@ struct TNodes {
             const int cyn = j < g.nc[1] ? axis_class(j + 1, g.nc[1]) : cy;
             dxp[m] = cxn - cx;
             dyp[m] = 3 * (cyn - cy);
-            unsigned f = e < nn ? kFOk : 0u;
+            unsigned f = e0 < nn ? kFOk : 0u;
             if (i > 0 && freec(axis_class(i - 1, g.nc[0]), cy)) f |= kFXm;
             if (i < g.nc[0] && freec(cxn, cy)) f |= kFXp;
             if (j > 0 && freec(cx, axis_class(j - 1, g.nc[1]))) f |= kFYm;
             if (j < g.nc[1] && freec(cx, cyn)) f |= kFYp;
             if (freec(cx, cy)) f |= kFCol;
             fl[m] = f;
+            // keep the table in registers: without this the compiler recomputes the
+            // division by NX inside the plane loops to save registers
+            asm volatile("" : "+r"(off[m]), "+r"(fl[m]));
         }
     }
 };
@@ -277,18 +319,50 @@ struct TNodes {
 template <int NCW, int NPT>
 __device__ void t_consume_a(const Grid& g, const TPlan& tp, const ClassTable& T, uint64_t* full, uint64_t* empty,
                             const int* s_item, uint32_t& t, bool first, double beta, double* __restrict__ pnew,
-                            double* part, double (*ired)[32]) {
+                            double* part, double (*ired)[32], unsigned long long* pf = nullptr) {
     const int NXY = g.NX * g.NY, sy = g.NX, RA = tp.RA;
     constexpr int NT = NCW * 32;
     TRing cur;
     cur.set(tp, t);
     while (true) {
         t_wait_full(full, cur);
+        if (pf && threadIdx.x == 0) { *pf = t_ns(); pf = nullptr; }      // first stage of the sweep landed
         const int item = s_item[cur.s];
         if (item < 0) { t_release(empty, cur); cur.adv(tp); t = cur.t; return; }
         const TItem it = t_item(g, tp, item);
         TNodes<NPT, NT> nd;
         nd.init(g, it);
+        // Lean planes (1 <= k <= NZ - 3: the node and its z+ neighbour have z class 1; not
+        // the first iteration): the node's coefficients are item constants held in
+        // registers, with absent or Dirichlet forward neighbours folded in as zero
+        // couplings, identity rows as diag = 1 (a = pp * pp) and threads without a node as
+        // all-zero coefficients.  Every load is unconditional: an absent neighbour's
+        // address holds either another node's value or ring words the kernel zeroed at
+        // its start (finite either way), times a zero coupling.  The node's own p is the
+        // z+ value computed on the previous plane (same class, same operations).
+        double ivo[NPT], ivx[NPT], ivy[NPT], dg[NPT], ex[NPT], ey[NPT], ez[NPT], carry[NPT];
+        constexpr bool kLean = NPT <= 2;
+        if (kLean) {
+#pragma unroll
+            for (int m = 0; m < NPT; ++m) {
+                const int cl = nd.cxy[m] + 9;
+                const unsigned f = nd.fl[m];
+                const bool ok = f & kFOk;
+                const bool cpl = ok && T.nd[cl] != 0.0;
+                ivo[m] = T.invd[cl];
+                ivx[m] = T.invd[cl + nd.dxp[m]];
+                ivy[m] = T.invd[cl + nd.dyp[m]];
+                dg[m] = ok ? T.diag[cl] : 0.0;
+                ex[m] = (cpl && (f & kFXp)) ? T.c[0][cl] : 0.0;
+                ey[m] = (cpl && (f & kFYp)) ? T.c[1][cl] : 0.0;
+                ez[m] = (cpl && (f & kFCol)) ? T.c[2][cl] : 0.0;
+                carry[m] = 0.0;
+            }
+        }
+        bool have = false;                       // carry holds this plane's own p
+        uint32_t sm0 = smem_u32(t_sm);
+        uint32_t ra8 = 8u * (uint32_t)RA, sy8 = 8u * (uint32_t)sy;
+        asm volatile("" : "+r"(sm0), "+r"(ra8), "+r"(sy8));      // computed once per item
         double acc[1] = {0.0};
         for (int k = it.k0; k < it.k1; ++k) {
             const bool nxt = k + 1 < g.NZ;
@@ -297,6 +371,22 @@ __device__ void t_consume_a(const Grid& g, const TPlan& tp, const ClassTable& T,
             const int kb = k * NXY;
             const int s0 = cur.s * tp.stage - t_abeg(kb + it.j0 * g.NX);
             const int o1 = nxt ? nx.s * tp.stage - t_abeg(kb + NXY + it.j0 * g.NX) : 0;
+            if (kLean && !first && k >= 1 && k <= g.NZ - 3) {
+                const uint32_t b0 = sm0 + 8u * (uint32_t)(s0 + kb), b1 = sm0 + 8u * (uint32_t)(o1 + kb + NXY);
+#pragma unroll
+                for (int m = 0; m < NPT; ++m) {
+                    const uint32_t a0 = b0 + 8u * (uint32_t)nd.off[m];
+                    const double pz = t_pvb(b1 + 8u * (uint32_t)nd.off[m], ra8, ivo[m], beta);
+                    const double pp = have ? carry[m] : t_pvb(a0, ra8, ivo[m], beta);
+                    const double px = t_pvb(a0 + 8u, ra8, ivx[m], beta);
+                    const double py = t_pvb(a0 + sy8, ra8, ivy[m], beta);
+                    if (nd.fl[m] & kFOk) pnew[kb + nd.off[m]] = pp;
+                    acc[0] += pp * (dg[m] * pp - 2.0 * ((ex[m] * px + ey[m] * py) + ez[m] * pz));
+                    carry[m] = pz;
+                }
+                have = true;
+            } else {
+            have = false;
             const int cz = axis_class(k, g.nc[2]);
             const int dzp = nxt ? 9 * (axis_class(k + 1, g.nc[2]) - cz) : 0;
 #pragma unroll
@@ -318,6 +408,7 @@ __device__ void t_consume_a(const Grid& g, const TPlan& tp, const ClassTable& T,
                 }
                 acc[0] += a;
             }
+            }
             t_release(empty, cur);
             cur.adv(tp);
         }
@@ -334,19 +425,23 @@ __device__ void t_consume_a(const Grid& g, const TPlan& tp, const ClassTable& T,
 template <int NCW, int NPT>
 __device__ void t_consume_b(const Grid& g, const TPlan& tp, const ClassTable& T, uint64_t* full, uint64_t* empty,
                             const int* s_item, uint32_t& t, double alpha, bool xzero, double* __restrict__ x,
-                            double* __restrict__ r, double* part, double (*ired)[32]) {
+                            double* __restrict__ r, double* part, double (*ired)[32],
+                            unsigned long long* pf = nullptr) {
     const int NXY = g.NX * g.NY, sy = g.NX, RX = tp.RX;
     constexpr int NT = NCW * 32;
     TRing cur;
     cur.set(tp, t);
     while (true) {
         t_wait_full(full, cur);
+        if (pf && threadIdx.x == 0) { *pf = t_ns(); pf = nullptr; }
         const int item = s_item[cur.s];
         if (item < 0) { t_release(empty, cur); cur.adv(tp); t = cur.t; return; }
         const TItem it = t_item(g, tp, item);
         TNodes<NPT, NT> nd;
         nd.init(g, it);
-        const int jlo = max(it.j0 - 1, 0);
+        // stage layout of p: rows j0 - 1 .. j1 (row j0 - 1 of the bottom row block and row
+        // j1 of the top one are not loaded; their words stay finite)
+        const int jlo = it.j0 - 1;
         double prev[NPT];
         if (it.k0 > 0) {          // halo plane k0 - 1: only the own-node values are needed
             const int kb = (it.k0 - 1) * NXY;
@@ -359,6 +454,31 @@ __device__ void t_consume_b(const Grid& g, const TPlan& tp, const ClassTable& T,
 #pragma unroll
             for (int m = 0; m < NPT; ++m) prev[m] = 0.0;
         }
+        // Lean planes (2 <= k <= NZ - 2: z class 1, both z neighbours on free planes; x
+        // stored): the node's coefficients are item constants in registers, one coupling
+        // per neighbour, zero where the neighbour is absent or Dirichlet (its address
+        // holds a finite value: another node's, or zeroed ring words); identity rows
+        // carry diag = 1 and zero couplings (q = p), threads without a node all zeros.
+        double dg[NPT], cxm[NPT], cxp[NPT], cym[NPT], cyp[NPT], c2[NPT], ivd[NPT];
+        constexpr bool kLean = NPT <= 2;
+        if (kLean) {
+#pragma unroll
+            for (int m = 0; m < NPT; ++m) {
+                const int cl = nd.cxy[m] + 9;
+                const unsigned f = nd.fl[m];
+                const bool ok = f & kFOk;
+                const bool cpl = ok && T.nd[cl] != 0.0;
+                dg[m] = ok ? T.diag[cl] : 0.0;
+                ivd[m] = T.invd[cl];
+                cxm[m] = (cpl && (f & kFXm)) ? T.c[0][cl] : 0.0;
+                cxp[m] = (cpl && (f & kFXp)) ? T.c[0][cl] : 0.0;
+                cym[m] = (cpl && (f & kFYm)) ? T.c[1][cl] : 0.0;
+                cyp[m] = (cpl && (f & kFYp)) ? T.c[1][cl] : 0.0;
+                c2[m] = (cpl && (f & kFCol)) ? T.c[2][cl] : 0.0;
+            }
+        }
+        uint32_t sm0 = smem_u32(t_sm), sy8 = 8u * (uint32_t)sy, rx8 = 8u * (uint32_t)RX;
+        asm volatile("" : "+r"(sm0), "+r"(sy8), "+r"(rx8));
         double acc[2] = {0.0, 0.0};
         for (int k = it.k0; k < it.k1; ++k) {
             const bool nxt = k + 1 < g.NZ;
@@ -369,6 +489,33 @@ __device__ void t_consume_b(const Grid& g, const TPlan& tp, const ClassTable& T,
             const int oc = cur.s * tp.stage - t_abeg(kb + jlo * g.NX);
             const int op = nxt ? nx.s * tp.stage - t_abeg(kb + NXY + jlo * g.NX) : 0;
             const int ox = cur.s * tp.stage + tp.RB - t_abeg(kb + it.j0 * g.NX);
+            if (kLean && !xzero && k >= 2 && k <= g.NZ - 2) {
+                const uint32_t b0 = sm0 + 8u * (uint32_t)(oc + kb), b1 = sm0 + 8u * (uint32_t)(op + kb + NXY);
+                const uint32_t bx = sm0 + 8u * (uint32_t)(ox + kb);
+#pragma unroll
+                for (int m = 0; m < NPT; ++m) {
+                    const uint32_t o8 = 8u * (uint32_t)nd.off[m];
+                    const uint32_t a0 = b0 + o8;
+                    const double pp = lds64(a0);
+                    const double xm = lds64(a0 - 8u), xp = lds64(a0 + 8u);
+                    const double ym = lds64(a0 - sy8), yp = lds64(a0 + sy8);
+                    const double zp = lds64(b1 + o8);
+                    const double xo = lds64(bx + o8), ro = lds64(bx + rx8 + o8);
+                    const double qv = dg[m] * pp - (((cxm[m] * xm + cxp[m] * xp) + (cym[m] * ym + cyp[m] * yp)) +
+                                                    c2[m] * (prev[m] + zp));
+                    const double xv = __dadd_rn(xo, __dmul_rn(alpha, pp));
+                    const bool ok = nd.fl[m] & kFOk;
+                    const double rv = ok ? __dsub_rn(ro, __dmul_rn(alpha, qv)) : 0.0;
+                    if (ok) {
+                        const int p = kb + nd.off[m];
+                        x[p] = xv;
+                        r[p] = rv;
+                    }
+                    acc[0] += rv * __dmul_rn(ivd[m], rv);
+                    acc[1] += rv * rv;
+                    prev[m] = pp;
+                }
+            } else {
             const int cz9 = 9 * axis_class(k, g.nc[2]);
             const bool zm_ok = k >= 2, zp_ok = nxt;
 #pragma unroll
@@ -398,6 +545,7 @@ __device__ void t_consume_b(const Grid& g, const TPlan& tp, const ClassTable& T,
                 acc[0] += rv * __dmul_rn(iv, rv);
                 acc[1] += rv * rv;
                 prev[m] = pp;
+            }
             }
             t_release(empty, cur);
             cur.adv(tp);
@@ -455,9 +603,10 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) k_t_cg(PcgParams P, int Grh
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     build_class_table(T, threadIdx.x, P.mbase, P.cbase, g.dkind);
+    t_zero_ring(tp, t_sm);
     {
         const int s[2] = {0, 1};
-        grid_sum_wide<2>(P.part, s, Grhs, red, tot);   // also syncs T and the barriers
+        grid_sum_wide<2>(P.part, s, Grhs, red, tot);   // also syncs T, the barriers and the ring
     }
     const bool producer = (threadIdx.x >> 5) == NCW;
     const bool plane0 = producer && (threadIdx.x & 31) == 0;
@@ -485,37 +634,49 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) k_t_cg(PcgParams P, int Grh
             // light RHS: in the first iteration r0 is b and x0 is 0 (neither was written)
             const bool light0 = first && P.light_rhs;
             const double* r0 = light0 ? P.b : P.r;
+            unsigned long long* pf = (tp.prof && it == 3) ? tp.prof + 1024 + 16 * blockIdx.x : nullptr;
+#define TL_TSTAMP(e) if (pf && threadIdx.x == 0) pf[e] = t_ns();
+            TL_TSTAMP(0)
             // ---- sweep A ----
             if (blockIdx.x == 0 && threadIdx.x == 0) ctr[(seq + 2) & 3] = 0u;
             if (producer) {
                 if (plane0) t_produce<false>(g, tp, t_sm, full, empty, s_item, ctr + (seq & 3), t, first, r0, pold,
                                              nullptr, nullptr);
             } else {
-                t_consume_a<NCW, NPT>(g, tp, T, full, empty, s_item, t, first, beta, pnew, part, ired);
+                t_consume_a<NCW, NPT>(g, tp, T, full, empty, s_item, t, first, beta, pnew, part, ired,
+                                      pf ? pf + 1 : nullptr);
                 fence_proxy_async_global();
             }
+            TL_TSTAMP(2)
             ++seq;
             grid.sync();
+            TL_TSTAMP(3)
             t = __shfl_sync(0xffffffffu, t, 0);     // producer warp: lane 0 holds the position
             fence_proxy_async_global();
             t_grid_sum<1>(part, tp.I, red, tot);
+            TL_TSTAMP(4)
             const double alpha = rho / tot[0];
             // ---- sweep B ----
             if (blockIdx.x == 0 && threadIdx.x == 0) ctr[(seq + 2) & 3] = 0u;
             if (producer) {
                 if (plane0) t_produce<true>(g, tp, t_sm, full, empty, s_item, ctr + (seq & 3), t, false, r0, nullptr,
-                                            pnew, light0 ? nullptr : P.T);
+                                            pnew, light0 ? nullptr : P.T, tp.snake != 0);
             } else {
                 // sweep B's item partials go to slots 1, 2: a CTA that is still summing sweep
                 // A's slot-0 partials after the barrier must not see them overwritten
-                t_consume_b<NCW, NPT>(g, tp, T, full, empty, s_item, t, alpha, light0, P.T, P.r, part + tp.I, ired);
+                t_consume_b<NCW, NPT>(g, tp, T, full, empty, s_item, t, alpha, light0, P.T, P.r, part + tp.I, ired,
+                                      pf ? pf + 5 : nullptr);
                 fence_proxy_async_global();
             }
+            TL_TSTAMP(6)
             ++seq;
             grid.sync();
+            TL_TSTAMP(7)
             t = __shfl_sync(0xffffffffu, t, 0);
             fence_proxy_async_global();
             t_grid_sum<2>(part + tp.I, tp.I, red, tot);
+            TL_TSTAMP(8)
+#undef TL_TSTAMP
             rz = tot[0];
             rnorm = sqrt(tot[1]);
             rho_prev = rho;
