@@ -156,13 +156,8 @@ static cudaError_t launch_s_cg(tl::PcgParams& P, int Gr, int sms, cudaStream_t s
 }
 
 // ---- z-marching CG loop on bulk copies (tl_tiled.cuh) --------------------------------
-// Default CG loop of the streaming solve; TLGPU_TILED=0 falls back to k_s_cg.  Tile plan:
-// grids of at least TLGPU_TILED_MIN nodes (default 20M: measured faster than k_s_cg on
-// the 201M-node cfg4 grid, slower on the 6-7M-node cfg3 / cfg4-local grids whose ~40 us
-// sweeps do not amortise the per-sweep pipeline fill and item reduction).  H full x-rows
-// per item so that five sweep-B stages fit in 220 KB and a consumer thread has at most 4
-// nodes per plane, z chunks of about a tenth of a CTA's share (at least TLGPU_TZ planes),
-// as many ring stages as fit in 220 KB (at least 4).  TLGPU_TH overrides H.
+// Default CG loop of the streaming solve; TLGPU_TILED=0 falls back to k_s_cg, and grids
+// below TLGPU_TILED_MIN nodes (default 1M) use k_s_cg too.  Item plan: tiled_plan_range.
 constexpr int kTNCW = 16;                      // consumer warps of k_t_cg
 static bool tiled_enabled() {
     static int v = -1;
@@ -190,7 +185,7 @@ static bool tiled_plan(const tl::Grid& g, int sms, tl::TPlan& tp, size_t& smem) 
     static long long nmin = -1;
     if (nmin < 0) {
         const char* e = getenv("TLGPU_TILED_MIN");
-        nmin = e ? atoll(e) : 20000000LL;
+        nmin = e ? atoll(e) : 1000000LL;
     }
     if ((long long)g.n < nmin) return false;
     return tiled_plan_range(g, sms, 0, g.NZ, tp, smem);
@@ -198,46 +193,69 @@ static bool tiled_plan(const tl::Grid& g, int sms, tl::TPlan& tp, size_t& smem) 
 
 // Item plan of the bulk-copy z-march over node planes [zlo, zhi) (the whole grid, or one
 // rank's own planes of a z-slab decomposition).
+//
+// An item is H full x-rows by one z chunk.  The plan minimises a cost model fitted to
+// sweeps of the BASELINE grids (tools/tune_snake.sh, tools/sweep_profile.py):
+//   cost(H, C) = waves * (Z + 2) * plane,   waves = ceil(NB * C / CTAs),  Z = ceil(planes / C)
+//   plane      = max(512 * ceil(H NX / 512), H NX (1 + 0.6 / H))
+// - items are taken dynamically but are all about the same size, so a sweep lasts `waves`
+//   items per CTA: balance (items a multiple of the CTA count) dominates;
+// - an item costs about 2 planes beyond its own (halo plane, pipeline fill, reduction, tail);
+// - a plane costs its consumer slots (512 threads take one node each per slot) or its ring
+//   traffic including the halo rows, whichever is larger.
+// Constraints: H NX <= 2 x 512 nodes per plane where possible (the lean plane loops keep two
+// nodes' coefficients per thread in registers; up to 4 x 512 otherwise), at least 4 ring
+// stages in 220 KB.  TLGPU_TH / TLGPU_TC / TLGPU_TZ override H, the chunk count and the
+// smallest chunk.
 static bool tiled_plan_range(const tl::Grid& g, int sms, int zlo, int zhi, tl::TPlan& tp, size_t& smem) {
     const int NX = g.NX;
     const int nzr = zhi - zlo;
     if (nzr < 1) return false;
-    // rows per item: a sweep-B stage ((H + 2) + 2 H rows) small enough for 5 ring stages in
-    // 220 KB, and at most 4 nodes per consumer thread per plane
-    int H = std::max(1, (220 * 1024 / 8 / 5 - 2 * NX - 8) / (3 * NX));
-    H = std::max(1, std::min(H, 4 * kTNCW * 32 / NX));
-    if (const char* e = getenv("TLGPU_TH")) H = std::max(1, atoi(e));
-    H = std::min(H, g.NY);
-    if (H * NX > 4 * kTNCW * 32) return false;
+    auto even = [](int v) { return (v + 1) & ~1; };
+    const size_t cap = 220 * 1024;
+    auto stage_of = [&](int H) {
+        const int RA = even((H + 1) * NX + 2), RB = even((H + 2) * NX + 2), RX = even(H * NX + 2);
+        return (std::max(2 * RA, RB + 2 * RX) + 15) & ~15;
+    };
+    auto stages_of = [&](int H) { return (int)std::min<size_t>(tl::kTMaxStages, cap / ((size_t)stage_of(H) * 8)); };
+    const int npt_max = NX <= 2 * kTNCW * 32 ? 2 : 4;
+    int Hmax = std::min(g.NY, npt_max * kTNCW * 32 / NX);
+    while (Hmax >= 1 && stages_of(Hmax) < 4) --Hmax;
+    if (Hmax < 1) return false;
+    int zmin = 2;
+    if (const char* e = getenv("TLGPU_TZ")) zmin = std::max(1, atoi(e));
+    int H = 0, nch = 0;
+    double best = 1e300;
+    for (int h = 1; h <= Hmax; ++h) {
+        const int NB = (g.NY + h - 1) / h;
+        const int slots = (h * NX + kTNCW * 32 - 1) / (kTNCW * 32);
+        const double plane = std::max((double)slots * kTNCW * 32, (double)h * NX * (1.0 + 0.6 / h));
+        for (int c = 1; c <= std::min(nzr, tl::kTMaxChunks); ++c) {
+            const int Z = (nzr + c - 1) / c;
+            if (Z < zmin && c > 1) break;
+            const long long I = (long long)NB * c;
+            if (I > tl::kTMaxItems) break;
+            const long long waves = (I + sms - 1) / sms;
+            const double cost = (double)waves * (Z + 2.0) * plane;
+            if (cost < best * (1.0 - 1e-9)) { best = cost; H = h; nch = c; }
+        }
+    }
+    if (H == 0) return false;
+    if (const char* e = getenv("TLGPU_TH")) H = std::max(1, std::min(atoi(e), Hmax));
+    if (const char* e = getenv("TLGPU_TC")) nch = std::max(1, std::min(atoi(e), std::min(nzr, tl::kTMaxChunks)));
     tp.H = H;
     tp.NB = (g.NY + H - 1) / H;
-    auto even = [](int v) { return (v + 1) & ~1; };
     tp.RA = even((H + 1) * NX + 2);
     tp.RB = even((H + 2) * NX + 2);
     tp.RX = even(H * NX + 2);
-    tp.stage = (std::max(2 * tp.RA, tp.RB + 2 * tp.RX) + 15) & ~15;
-    const size_t cap = 220 * 1024;
-    tp.NS = (int)std::min<size_t>(tl::kTMaxStages, cap / ((size_t)tp.stage * 8));
+    tp.stage = stage_of(H);
+    tp.NS = stages_of(H);
     if (tp.NS < 4) return false;
-    // z chunks of about a tenth of a CTA's share of the sweep per item (at least TLGPU_TZ
-    // planes; measured: a guided tail of 1- and 2-plane items was slower, the per-item
-    // halo planes and reductions cost more than the shorter tail saves)
-    int zmin = 3;
-    if (const char* e = getenv("TLGPU_TZ")) zmin = std::max(1, atoi(e));
-    const double share = (double)NX * g.NY * nzr / sms;
-    int Z = (int)(share / (10.0 * H * NX));
-    Z = std::max(zmin, std::min(Z, nzr));
-    std::vector<int> cz;
-    int nch = std::max(1, (nzr + Z - 1) / Z);
-    if (const char* e = getenv("TLGPU_TC")) nch = std::max(1, std::min(atoi(e), nzr));
-    for (int c = 0; c < nch; ++c) cz.push_back(nzr * (c + 1) / nch - nzr * c / nch);
-    if ((int)cz.size() > tl::kTMaxChunks) return false;
-    tp.C = (int)cz.size();
+    tp.C = nch;
     tp.I = tp.NB * tp.C;
     if (tp.I > tl::kTMaxItems) return false;
     tp.kb[0] = (short)zlo;
-    for (int c = 0; c < tp.C; ++c) tp.kb[c + 1] = (short)(tp.kb[c] + cz[c]);
-    if (tp.kb[tp.C] != zhi) return false;
+    for (int c = 0; c < tp.C; ++c) tp.kb[c + 1] = (short)(zlo + (long long)nzr * (c + 1) / nch);
     tp.nsd.init(tp.NS);
     tp.nbd.init(tp.NB);
     tp.snake = snake_enabled();
@@ -1520,7 +1538,69 @@ static int ensure_snapshots(tl_run* R, int nl) {
     return TL_OK;
 }
 
-static int local_solve(tl_run* R, double* T, const tl_micro_plan& mp) {
+// True when every solve of the local grid takes the streaming path (no resident kernel
+// fits it, with or without Gaussian tables).
+static bool local_streams(tl_run* R) {
+    if (force_streaming()) return split_minb() != 0;
+    if (split_minb() == 0) return false;
+    BrickPlan bp;
+    if (cg_fits(R->L, true, R->sms, bp) || cg_fits(R->L, false, R->sms, bp)) return false;
+    return !plan_bricks(R->L, true, R->sms, 200 * 1024, false).ok && !plan_bricks(R->L, false, R->sms, 200 * 1024, false).ok;
+}
+
+// Streaming local grid: the Gaussian loads of all ns solves of a macro step by ONE
+// k_gauss_loads launch, dense over the box where the term can change the RHS (bitwise the
+// RHS of the per-solve k_gauss_load; tl_resident_cg.cuh), read by k_s_rhs through
+// PcgParams::bload / bbox.  Replaces a full-grid pass (T read, load written) per solve and
+// the load read of every RHS.
+static int stream_gauss_loads(tl_run* R, const tl_macro_plan& mp, const tl_micro_plan* micro, int ns) {
+    if (R->specs_cap < ns + 1) {
+        if (R->d_specs) cudaFree(R->d_specs);
+        R->d_specs = nullptr;
+        if (int rc = dalloc(&R->d_specs, ns + 1)) return rc;
+        R->specs_cap = ns + 1;
+    }
+    if (R->gload_cap < ns) {
+        if (R->gload) cudaFree(R->gload);
+        if (R->d_srcs) cudaFree(R->d_srcs);
+        R->gload = nullptr;
+        R->d_srcs = nullptr;
+        if (int rc = dalloc(&R->gload, (size_t)ns * R->L.n)) return rc;
+        if (int rc = dalloc(&R->d_srcs, ns)) return rc;
+        R->gload_cap = ns;
+    }
+    R->h_specs.assign(ns, tl::SolveSpec{});
+    R->h_srcs.assign(ns, tl::Gauss{});
+    const double V = R->L.h[0] * R->L.h[1] * R->L.h[2];
+    bool any = false;
+    for (int e = 0; e < ns; ++e) {
+        const tl_micro_plan& up = micro[mp.micro_offset + e];
+        tl::SolveSpec& sp = R->h_specs[e];
+        sp.mbase = (R->desc.rho_c_local / up.dt) * V / 24.0;
+        sp.src.peak = R->desc.beam_peak;
+        sp.src.radius = R->desc.beam_radius;
+        sp.src.depth = R->desc.beam_depth;
+        for (int a = 0; a < 3; ++a) sp.src.center[a] = up.center[a];
+        sp.src.on = up.source_on ? 1 : 0;
+        R->h_srcs[e] = sp.src;
+        any = any || sp.src.on;
+    }
+    if (!any) return TL_OK;
+    TL_CUDA(cudaMemcpyAsync(R->d_specs + 1, R->h_specs.data(), sizeof(tl::SolveSpec) * ns, cudaMemcpyHostToDevice,
+                            R->stream));
+    TL_CUDA(cudaMemcpyAsync(R->d_srcs, R->h_srcs.data(), sizeof(tl::Gauss) * ns, cudaMemcpyHostToDevice, R->stream));
+    const size_t smem = gauss_smem(R->L);
+    TL_CUDA(ensure_smem_attr((const void*)tl::k_gauss_loads, smem));
+    const dim3 grid((unsigned)std::max(1, (8 * R->sms + ns - 1) / ns), (unsigned)ns);
+    tl::k_gauss_loads<<<grid, 256, smem, R->stream>>>(R->L, R->d_specs + 1, R->d_srcs, 0.5 * R->desc.T_buildplate,
+                                                      R->gload);
+    TL_CUDA(cudaGetLastError());
+    ++R->launches;
+    return TL_OK;
+}
+
+// boxed >= 0: this solve's Gaussian load was precomputed as entry `boxed` of stream_gauss_loads.
+static int local_solve(tl_run* R, double* T, const tl_micro_plan& mp, int boxed = -1) {
     tl::PcgParams P{};
     base_params(R, P, true, mp.dt);
     P.T = T;
@@ -1529,6 +1609,11 @@ static int local_solve(tl_run* R, double* T, const tl_micro_plan& mp) {
     P.w = mp.w;
     P.load = nullptr;
     bool gauss = mp.source_on != 0;
+    if (gauss && boxed >= 0) {
+        P.bload = R->gload + (size_t)boxed * R->L.n;
+        P.bbox = (R->d_specs + 1 + boxed)->box;
+        gauss = false;
+    }
     if (gauss) {
         P.src.peak = R->desc.beam_peak; P.src.radius = R->desc.beam_radius; P.src.depth = R->desc.beam_depth;
         for (int a = 0; a < 3; ++a) P.src.center[a] = mp.center[a];
@@ -1638,6 +1723,9 @@ int32_t tl_run_macro_steps(tl_run* R, const tl_macro_plan* plans, int32_t nsteps
     const char* mv = getenv("TLGPU_MULTI");
     const bool multi = !(mv && mv[0] == '0') && cg_fits(R->L, false, R->sms, lbp) &&
                        !(lbp.xglob && getenv("TLGPU_NOCACHE"));
+    // TLGPU_BOXLOAD=0: per-solve k_gauss_load over the whole local grid (streaming path)
+    const char* bv = getenv("TLGPU_BOXLOAD");
+    const bool lstream = !(bv && bv[0] == '0') && !multi && local_streams(R);
 
     int need = 0;
     for (int s = 0; s < nsteps; ++s) {
@@ -1692,6 +1780,9 @@ int32_t tl_run_macro_steps(tl_run* R, const tl_macro_plan* plans, int32_t nsteps
         // -- trace of the predicted global field on gamma --
         if (int rc = run_interp_local(R, 1, nullptr, R->tr_pred)) return rc;
         // -- micro steps (+ corrector): one persistent launch when the local grid fits --
+        const bool boxed = !multi && lstream;
+        if (boxed)
+            if (int rc = stream_gauss_loads(R, mp, micro, mp.n_micro + (mp.corrector ? 1 : 0))) return rc;
         if (multi) {
             if (int rc = local_multi(R, mp, micro, lbp)) return rc;
         } else
@@ -1701,13 +1792,14 @@ int32_t tl_run_macro_steps(tl_run* R, const tl_macro_plan* plans, int32_t nsteps
                 tl::k_copy<<<4 * R->sms, 256, 0, R->stream>>>(R->Tl, R->Tl_before, R->L.n);
                 ++R->launches;
             }
-            if (int rc = local_solve(R, R->Tl, up)) return rc;
+            if (int rc = local_solve(R, R->Tl, up, boxed ? i : -1)) return rc;
             if (mp.record)
                 TL_CUDA(cudaMemcpyAsync(R->snap_l[i], R->Tl, sizeof(double) * R->L.n, cudaMemcpyDeviceToDevice, R->stream));
         }
         if (mp.corrector && !multi) {
             // corrector: re-solve the last micro interval from before_final with trace_pred
-            if (int rc = local_solve(R, R->Tl_before, micro[mp.micro_offset + mp.n_micro])) return rc;
+            if (int rc = local_solve(R, R->Tl_before, micro[mp.micro_offset + mp.n_micro], boxed ? mp.n_micro : -1))
+                return rc;
             std::swap(R->Tl, R->Tl_before);
             if (mp.record)
                 TL_CUDA(cudaMemcpyAsync(R->snap_l[mp.n_micro], R->Tl, sizeof(double) * R->L.n, cudaMemcpyDeviceToDevice, R->stream));

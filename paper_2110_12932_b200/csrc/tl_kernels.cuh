@@ -73,6 +73,10 @@ struct PcgParams {
     const double* gB;
     double w, g_const;
     const double* load;  // dense extra load or nullptr
+    // streaming solves of a run: Gaussian load precomputed by k_gauss_loads, dense over the
+    // box bbox = [i0, i1) x [j0, j1) x [k0, k1) (device memory; x fastest), or nullptr
+    const double* bload;
+    const int* bbox;
     Gauss src;
     // workspace
     double *b, *r, *p0, *p1, *q;

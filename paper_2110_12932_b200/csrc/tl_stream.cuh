@@ -68,17 +68,24 @@ __device__ __forceinline__ bool s_free_interior(const Grid& g, int i, int j, int
 
 // RHS at node p (fem.py:129-194 + constrained, 89-105): b written (and r = b, x = 0 unless
 // the k_t_cg path implies them); accumulates b.b and b.z.
-__device__ __forceinline__ void s_rhs_node(const PcgParams& P, const ClassTable& T, int p, double* __restrict__ b,
-                                           double* __restrict__ r, double* __restrict__ x,
-                                           const double* __restrict__ load, double (&acc)[2]) {
+__device__ __forceinline__ void s_rhs_node(const PcgParams& P, const ClassTable& T, const int* box, int p,
+                                           double* __restrict__ b, double* __restrict__ r,
+                                           double* __restrict__ x, const double* __restrict__ load,
+                                           double (&acc)[2]) {
     const Grid& g = P.g;
     int i, j, k;
     decode(g, p, i, j, k);
+    // the precomputed Gaussian load of the node (0 outside the box; Dirichlet nodes hold 0)
+    auto boxload = [&]() -> double {
+        if (i < box[0] || i >= box[1] || j < box[2] || j >= box[3] || k < box[4] || k >= box[5]) return 0.0;
+        return P.bload[(i - box[0]) + (box[1] - box[0]) * ((j - box[2]) + (box[3] - box[2]) * (k - box[4]))];
+    };
     double bv;
     int cls = 13;
     if (s_free_interior(g, i, j, k)) {
         bv = T.mass[13] * x[p];
         if (load) bv += load[p];
+        if (P.bload) bv += boxload();
     } else {
         cls = class_of(g, i, j, k);
         if (T.nd[cls] == 0.0) {
@@ -86,6 +93,7 @@ __device__ __forceinline__ void s_rhs_node(const PcgParams& P, const ClassTable&
         } else {
             bv = T.mass[cls] * x[p];
             if (load) bv += load[p];
+            if (P.bload) bv += boxload();
             bv += dirichlet_lift(P, T, p, i, j, k, cls);
         }
     }
@@ -102,17 +110,19 @@ __device__ __forceinline__ void s_rhs_node(const PcgParams& P, const ClassTable&
 __global__ void __launch_bounds__(kSTPB) k_s_rhs(PcgParams P) {
     __shared__ ClassTable T;
     __shared__ double red[2 * 32];
+    __shared__ int box[6];
     const Grid& g = P.g;
     build_class_table(T, threadIdx.x, P.mbase, P.cbase, g.dkind);
+    if (threadIdx.x >= 32 && threadIdx.x < 38) box[threadIdx.x - 32] = P.bload ? P.bbox[threadIdx.x - 32] : 0;
     __syncthreads();
     double acc[2] = {0.0, 0.0};
     const int stride = gridDim.x * blockDim.x;
     int p = blockIdx.x * blockDim.x + threadIdx.x;
     for (; p + stride < g.n; p += 2 * stride) {
-        s_rhs_node(P, T, p, P.b, P.r, P.T, P.load, acc);
-        s_rhs_node(P, T, p + stride, P.b, P.r, P.T, P.load, acc);
+        s_rhs_node(P, T, box, p, P.b, P.r, P.T, P.load, acc);
+        s_rhs_node(P, T, box, p + stride, P.b, P.r, P.T, P.load, acc);
     }
-    if (p < g.n) s_rhs_node(P, T, p, P.b, P.r, P.T, P.load, acc);
+    if (p < g.n) s_rhs_node(P, T, box, p, P.b, P.r, P.T, P.load, acc);
     block_sum<2>(acc, red);
     if (threadIdx.x == 0) {
         P.part[blockIdx.x] = acc[0];

@@ -413,12 +413,16 @@ np.savez({out!r}, g=state.global_field.values, l=state.local_field.values,
 @pytest.mark.parametrize("env", [{"TLGPU_MULTI": "0"}, {"TLGPU_NOCACHE": "1", "TLGPU_CGSYNC": "1"},
                                  {"TLGPU_EXACT_CG": "1"},
                                  {"TLGPU_STREAMING": "1", "TLGPU_TILED_MIN": "1"},
-                                 {"TLGPU_STREAMING": "1", "TLGPU_TILED": "0"}])
+                                 {"TLGPU_STREAMING": "1", "TLGPU_TILED": "0"},
+                                 {"TLGPU_STREAMING": "1", "TLGPU_TILED_MIN": "1", "TLGPU_BOXLOAD": "0",
+                                  "TLGPU_SNAKE": "0"},
+                                 {"TLGPU_STREAMING": "1", "TLGPU_TILED": "0", "TLGPU_SNAKE": "0"}])
 def test_alternative_solver_modes_match_default(env, tmp_path):
     """The non-default device paths (one launch per local solve; no setup cache and
     cg::grid.sync barriers; scipy-exact two-barrier kernel; every solve on the streaming
     path, with the bulk-copy z-march CG loop k_t_cg or the flat k_s_cg, on grids small
-    enough that boundary nodes dominate) give the default run's fields
+    enough that boundary nodes dominate; the same with per-solve full-grid Gaussian loads
+    and both sweeps bottom-up) give the default run's fields
     to CG rounding with the same counters (env switches are read once per process, so
     each mode runs in a subprocess)."""
     import os
