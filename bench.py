@@ -384,6 +384,22 @@ def slab_bench(args):
            "note": "host wall clock (max over ranks) of the next macro steps through the slab driver's "
                    "public loop (plan_superstep + SlabRun.superstep, as run_spacetime_slabs runs it): host "
                    "planning inside the clock, deposit samples H2D, solve records D2H, the last local field D2H"}
+    # the global solve timed alone (no local step in flight on the other stream): three more
+    # solves of the current field, all ranks together, CUDA events on the solve's stream
+    run.check_local()
+    alone = []
+    for _ in range(3):
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(cur)
+        inf = S.step(cfg.dt_macro, problem.bc.T_buildplate, with_load=False)
+        b.record(cur)
+        torch.cuda.synchronize()
+        alone.append((a.elapsed_time(b), inf.iterations))
+    alone_ms = float(np.mean([t for t, _ in alone]))
+    alone_gbs = sum(own * (64 * k + 32) for _, k in alone) / (sum(t for t, _ in alone) / 1e3) / 1e9
     run.close()
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -403,7 +419,12 @@ def slab_bench(args):
         "config": conf,
         "global_solve": {"ms_mean": float(np.mean(gms)) if gms else None,
                          "iterations_mean": float(np.mean(gits)) if gits else None,
-                         "host_syncs_per_solve": polls / max(len(run.global_infos), 1)},
+                         "host_syncs_per_solve": polls / max(len(run.global_infos), 1),
+                         "alone_ms": alone_ms, "alone_iterations": float(np.mean([k for _, k in alone])),
+                         "alone_gbs": alone_gbs, "alone_frac": alone_gbs / peak,
+                         "note": "ms_mean: inside the step, with the previous step's local solves running "
+                                 "concurrently on the local stream; alone_*: the same solve with nothing else "
+                                 "on the device (rank 0's own nodes x (64 k + 32) bytes / its event time)"},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         "clocks": clocks.summary(), "wall_s_timed_region": wall,
     }

@@ -293,7 +293,15 @@ static cudaError_t launch_t_cg(tl::PcgParams& P, int Gr, int sms, cudaStream_t s
 static int launch_stream(tl::PcgParams& P, int sms, cudaStream_t st, int64_t* launches) {
     const int minb = split_minb();
     if (minb == 0) return launch_pcg(P, false, sms, st, launches);
-    const int Gr = 4 * sms;
+    // one resident wave of each pass (a grid larger than what fits leaves a thin second wave)
+    static thread_local int occ_rhs = 0, occ_res = 0;
+    if (occ_rhs == 0) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_rhs, tl::k_s_rhs, tl::kSTPB, 0) != cudaSuccess || occ_rhs < 1)
+            occ_rhs = 1;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_res, tl::k_s_resid, tl::kSTPB, 0) != cudaSuccess || occ_res < 1)
+            occ_res = 1;
+    }
+    const int Gr = std::min(4, occ_rhs) * sms, Gq = std::min(4, occ_res) * sms;
     tl::TPlan tp{};
     size_t smem = 0;
     const bool use_tiled = tiled_enabled() && tiled_plan(P.g, sms, tp, smem);
@@ -318,8 +326,8 @@ static int launch_stream(tl::PcgParams& P, int sms, cudaStream_t st, int64_t* la
           : minb == 32 ? launch_s_cg<3, 2>(P, Gr, sms, st)
                        : launch_s_cg<3>(P, Gr, sms, st);
     if (e == cudaSuccess) {
-        tl::k_s_resid<<<Gr, tl::kSTPB, 0, st>>>(P);
-        tl::k_s_final<<<1, tl::kSTPB, 0, st>>>(P, Gr);
+        tl::k_s_resid<<<Gq, tl::kSTPB, 0, st>>>(P);
+        tl::k_s_final<<<1, tl::kSTPB, 0, st>>>(P, Gq);
         e = cudaGetLastError();
     }
     P.light_rhs = 0;
@@ -2204,7 +2212,7 @@ int32_t tl_slab_finish(const tl_slab* s) {
     int blocks = 0;
     cudaStream_t st;
     if (int rc = slab_dev(s, D, blocks, st)) return rc;
-    tl::k_sd_finish<<<blocks, tl::kSlabTPB, 0, st>>>(D);
+    tl::k_sd_finish<<<1, 32, 0, st>>>(D);
     TL_CUDA(cudaGetLastError());
     return TL_OK;
 }

@@ -88,9 +88,13 @@ __global__ void __launch_bounds__(kSlabTPB) k_slab_rhs(SlabParams S) {
     for (int p = S.own_lo + blockIdx.x * blockDim.x + threadIdx.x; p < S.own_hi; p += stride) {
         int i, j, k;
         decode(g, p, i, j, k);
-        const int cls = class_of(g, i, j, k);
+        int cls = 13;
         double bv;
-        if (T.nd[cls] == 0.0) {
+        if (!GAUSS && s_free_interior(g, i, j, k)) {
+            // class 13, all neighbours free: no lift (the same sum as the general branch)
+            bv = T.mass[13] * S.x[p];
+            if (S.load) bv += S.load[p];
+        } else if (T.nd[cls = class_of(g, i, j, k)] == 0.0) {
             bv = S.g_const;
         } else {
             bv = T.mass[cls] * S.x[p];

@@ -22,7 +22,8 @@
 //                   adds boundary + item partials in a fixed order -> sums[0] = r.r,
 //                   sums[1] = r.z; it += 1
 //   [halo x] k_sd_resid (if done): ||A x - b||^2, non-finite count -> sums[3], sums[4]
-//   [all-gather] k_sd_finish (if done): x_D = b_D, the reference's true-residual check
+//   [all-gather] k_sd_finish (if done): the reference's true-residual check (x_D = b_D is
+//                   written by k_sd_resid)
 //
 // Every CTA of every rank computes each scalar from the same gathered values in the same
 // order, so all ranks take bitwise the same branch and the iteration count does not
@@ -275,35 +276,17 @@ __global__ void __launch_bounds__(kSlabTPB) k_sd_resid(SlabDev D) {
     __syncthreads();
     double res[2] = {0.0, 0.0};
     const int stride = gridDim.x * blockDim.x;
-    for (int p = S.own_lo + blockIdx.x * blockDim.x + threadIdx.x; p < S.own_hi; p += stride) {
-        int i, j, k;
-        decode(g, p, i, j, k);
-        const int cls = class_of(g, i, j, k);
-        const double xp = S.x[p];
-        double ax;
-        if (T.nd[cls] == 0.0) ax = xp;
-        else ax = apply_free(g, T, p, i, j, k, cls, xp, [&](int q, int) { return S.x[q]; });
-        const double d = ax - S.b[p];
-        res[0] += d * d;
-        res[1] += isfinite(xp) ? 0.0 : 1.0;
-    }
+    // s_resid_node: interior fast path; also re-imposes x_D = b_D (fem.py:289-290) after the
+    // node's own term (neighbours read x_D with weight 0, so either value gives the same sum)
+    for (int p = S.own_lo + blockIdx.x * blockDim.x + threadIdx.x; p < S.own_hi; p += stride)
+        s_resid_node(g, T, p, S.x, S.b, res);
     const int s[2] = {3, 4};
     slab_reduce<2>(S, s, res, red);
 }
 
 __global__ void __launch_bounds__(kSlabTPB) k_sd_finish(SlabDev D) {
-    __shared__ ClassTable T;
-    const SlabParams& S = D.S;
-    const Grid& g = S.g;
     if (!__ldcg(&D.ctl->done)) return;
-    build_class_table(T, threadIdx.x, S.mbase, S.cbase, g.dkind);
-    __syncthreads();
-    const int stride = gridDim.x * blockDim.x;
-    for (int p = S.own_lo + blockIdx.x * blockDim.x + threadIdx.x; p < S.own_hi; p += stride) {
-        int i, j, k;
-        decode(g, p, i, j, k);
-        if (T.nd[class_of(g, i, j, k)] == 0.0) S.x[p] = S.b[p];
-    }
+    // (x_D = b_D was written by k_sd_resid)
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         // the reference's post-check (fem.py:286-288) and FieldState's finite check
         const double bnorm = D.ctl->bnorm;

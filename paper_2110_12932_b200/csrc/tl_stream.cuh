@@ -107,7 +107,7 @@ __device__ __forceinline__ void s_rhs_node(const PcgParams& P, const ClassTable&
 }
 
 // ---- k_s_rhs: b, r = b, x = 0; partials [0][blk] = b.b, [1][blk] = r.z ----------------
-__global__ void __launch_bounds__(kSTPB) k_s_rhs(PcgParams P) {
+__global__ void __launch_bounds__(kSTPB, 3) k_s_rhs(PcgParams P) {
     __shared__ ClassTable T;
     __shared__ double red[2 * 32];
     __shared__ int box[6];
@@ -339,7 +339,7 @@ __device__ __forceinline__ void s_resid_node(const Grid& g, const ClassTable& T,
 }
 
 // ---- k_s_resid: partials [0][blk] = ||A_c x - b||^2, [1][blk] = non-finite count --------
-__global__ void __launch_bounds__(kSTPB) k_s_resid(PcgParams P) {
+__global__ void __launch_bounds__(kSTPB, 3) k_s_resid(PcgParams P) {
     __shared__ ClassTable T;
     __shared__ double red[2 * 32];
     const Grid& g = P.g;

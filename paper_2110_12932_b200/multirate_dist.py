@@ -103,6 +103,12 @@ class SlabRun:
 
     def close(self):
         if self.local is not None:
+            # the window buffers were recorded on the local run's stream (record_stream):
+            # release them to the allocator while that stream still exists
+            import torch
+            self.old.clear()
+            torch.cuda.synchronize(self.solver.device)
+            torch.cuda.empty_cache()
             self.local.close()
             self.local = None
 
