@@ -862,6 +862,11 @@ def device_arm(args):
             per_launch = kdom["alg_bytes_per_solve"] * kdom["solves"] / kdom["launches"]
             traffic = dram / alg * per_launch
             tnote = f"ncu DRAM/algorithmic = {dram / alg:.3f} ({tj.get(f'{args.config}_{lev}_pcg_kernel', '')})"
+    if tfile.exists():                   # ncu DRAM / algorithmic bytes of each level's CG launch
+        for kk, lv in ((kloc, "local"), (kglo, "global")):
+            d_, a_ = tj.get(f"{args.config}_{lv}_pcg_dram_bytes_per_launch"), tj.get(f"{args.config}_{lv}_pcg_alg_bytes_per_launch")
+            if kk and d_ and a_:
+                kk["ncu_dram_over_algorithmic"] = d_ / a_
     roofline = {"bound": "hbm", "achieved": kdom["achieved_gbs"], "peak": peak, "unit": "GB/s",
                 "frac": kdom["achieved_gbs"] / peak, "traffic": traffic, "traffic_note": tnote,
                 "kernel": kname, "level": lev, "nodes": ndom, "peak_source": peak_src,
