@@ -1,18 +1,20 @@
 #!/usr/bin/env python
 """Benchmark: DOF-timesteps/s of the two-level multirate heat solve (BASELINE.json metric).
 
-Workload (N=1): BASELINE config 2 — 5-track alternating scan, global 121x121x41
-(600,281 nodes, h = 25 um), local 101x101x51 (520,251 nodes, h = 5 um), multirate
-m = 10, fp64, Jacobi-PCG rtol 1e-12.  One "step" = one macro step of
-``run_spacetime``: 1 global solve + 10 micro local solves + the corrector
-re-solve + trace + relocation, i.e. N_g + m N_l = 5,802,791 DOF-timesteps
+Workload (N=1, no flags): BASELINE config 4 at one GPU, the largest single-GPU
+configuration — global 1001x1001x201 (201,402,201 nodes, h = 20 um), local 251x251x101
+(6,363,101 nodes, h = 4 um), multirate m = 10, fp64, Jacobi-PCG rtol 1e-12.  One "step" =
+one macro step of ``run_spacetime``: 1 global solve + 10 micro local solves + the
+corrector re-solve + trace + relocation, i.e. N_g + m N_l = 265,033,211 DOF-timesteps
 (the corrector re-solve is performed but not counted).
+``--config cfg2|cfg3`` time the smaller BASELINE configs the same way, ``--config cfg5`` the
+64-scenario sweep, ``--config picard`` the temperature-dependent step.
 
-N > 1 (torchrun): every rank runs its own independent scenario replica on its GPU
-(scenario sharding, no data-path collective, weak scaling); timing is the max
-over ranks of the device time.  ``--impl reference`` times the reference's CPU
-algorithm (the literal P1-assembly + scipy-CG port in oracle/assembly.py, pinned
-bit-for-bit to the reference) on rank 0.
+N > 1 (torchrun): the global grid in z-slabs over the ranks with the device-resident CG,
+the local steps pipelined over the ranks in time (slab_bench; weak scaling on cfg4 grown in
+depth, ``--strong`` for cfg4 itself); timing is the max over ranks of the device time.
+``--impl reference`` times the reference's CPU algorithm (the literal P1-assembly +
+scipy-CG port in oracle/assembly.py, pinned bit-for-bit to the reference) on rank 0.
 
 Prints one JSON line.
 """

@@ -506,6 +506,55 @@ def test_tiled_cg_loop_cfg3_size_vs_oracle(level, tmp_path):
     assert int(t["its"]) == int(out["flat"]["its"]) and rel(t["x"], out["flat"]["x"]) <= 1e-13
 
 
+_REPEAT_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import paper_2110_12932_b200 as P
+from paper_2110_12932_b200 import _native as N, ops
+cfg = P.load_config({cfg!r})
+problem, lm = P.build_problem(cfg)
+rng = np.random.default_rng(1)
+grid = problem.global_mesh
+Tg = rng.uniform(293.0, 2293.0, grid.n_nodes)
+pts, pw = problem.global_source(0.0, cfg.dt_macro)
+load = ops.deposit_load(grid, pts, pw)
+Tl = rng.uniform(293.0, 2293.0, lm.n_nodes)
+g = np.where(lm.gamma_mask(), rng.uniform(293.0, 900.0, lm.n_nodes), 0.0)
+src = problem.local_source(2e-6)
+first = None
+for rep in range({reps}):
+    xg, ig = ops.step(grid, 9.8, 8440 * 410.0, cfg.dt_macro, N.TL_DIRICHLET_BOTTOM, Tg, g_const=293.0,
+                      load=load, rtol=1e-12)
+    xl, il = ops.step(lm, 9.8, 8440 * 410.0, cfg.dt_macro / cfg.micro_steps, N.TL_DIRICHLET_GAMMA, Tl, g=g,
+                      gaussian=src.device_args(), rtol=1e-12)
+    assert ig.status == 0 and il.status == 0
+    cur = (xg.copy(), xl.copy(), ig.iterations, il.iterations)
+    if first is None:
+        first = cur
+    else:
+        assert cur[2:] == first[2:], (cur[2:], first[2:])
+        assert np.array_equal(cur[0], first[0]) and np.array_equal(cur[1], first[1]), rep
+print("repeatable", first[2], first[3])
+"""
+
+
+@pytest.mark.parametrize("env", [{}, {"TLGPU_TILED": "0"}, {"TLGPU_SNAKE": "0", "TLGPU_TH": "2", "TLGPU_TC": "9"}])
+def test_streaming_paths_bitwise_repeatable(env):
+    """Race stress of the hand-rolled synchronisation (compute-sanitizer is closed on this
+    GPU pool): the bulk-copy z-march CG loop (mbarrier ring, dynamic item counter, per-item
+    partial sums, cooperative grid barriers) and the flat CG loop, five solves each of the
+    cfg3 global (6.9M nodes) and local (1.7M nodes) grids in one process: every bit of the
+    solution and the iteration counts must repeat whatever CTA ran which item."""
+    import os
+    import subprocess
+    import sys
+    code = _REPEAT_SCRIPT.format(root=str(ROOT), cfg=str(CONFIGS / "cfg3.cfg"), reps=5)
+    res = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True, text=True,
+                         timeout=900)
+    assert res.returncode == 0, res.stderr[-2000:]
+    assert "repeatable" in res.stdout
+
+
 def test_monolithic_reference_vs_reference_golden():
     """run_reference / solve_monolithic (lpbfsim/runner.py:126-163, fem.py:386-423) on the
     device: the cfg1 plate at h = 25 um, 8 uniform steps, against the reference's output."""
