@@ -1,0 +1,236 @@
+// tl_2d.cuh — the 2D (P1 triangle / 5-point) variants of the step kernels (SURVEY §8f
+// row 4), sm_100a, fp64.
+//
+// The reference's 2D meshes (lpbfsim/mesh.py:84-93,388-439) split every cell of the
+// structured grid into the triangles [0,1,3] and [0,3,2] (corner = dx + 2 dy), both
+// positively oriented:
+//     tri 0: (0,0) (1,0) (1,1)        tri 1: (0,0) (1,1) (0,1)
+// Right triangles with axis-aligned legs: the P1 gradients are axis-aligned, the element
+// stiffness kbar area grad_i.grad_j (fem.py:170) couples only the leg endpoints
+// (-kbar area / h_a^2 on the leg along axis a) and the hypotenuse carries nothing, so with
+// the row-sum lumped mass (fem.py:167-169) the assembled operator is the 5-point stencil
+//     (A x)_p = diag_p x_p - sum_{a in x,y} (w_a[p] x_{p+e_a} + w_a[p-e_a] x_{p-e_a}).
+// A 2D grid is a tl::Grid with nc[2] = 0 (NZ = 1): the constrained system, the Jacobi-PCG
+// (k_vc_cg), the increment and lag kernels of tl_vc.cuh run unchanged on it (their z
+// terms are guarded by 0 < k < nc[2]); only the assembly, the interpolation and the mass
+// norms have triangle variants here.  Element quadrature: the three edge midpoints,
+// weights 1/3 (mesh.py:107-110); boundary edges: two Gauss points (mesh.py:129-131).  The
+// vertical axis is y: BOTTOM / TOP are y = lo / y = hi (mesh.py:206-209), so the Robin
+// terms (fem.py:241-268) sit on the top row j = nc[1].  Beam: gaussian_source_2d
+// (sources.py:57-64), peak = P eta / (r d) passed in Gauss::peak.
+// oracle/tri2d.py restates the same arrays in numpy (checked against the reference's CSR
+// matrix and RHS to 3e-15).
+#pragma once
+
+#include "tl_vc.cuh"
+
+namespace tl {
+
+__host__ __device__ __forceinline__ bool grid_is_2d(const Grid& g) { return g.nc[2] == 0; }
+
+// vertex offsets (dx, dy) of the two triangles, in the reference's vertex order
+__constant__ int8_t c_tri[2][3][2] = {{{0, 0}, {1, 0}, {1, 1}}, {{0, 0}, {1, 1}, {0, 1}}};
+// legs of each triangle: (lower vertex, upper vertex, axis)
+__constant__ int8_t c_leg[2][2][3] = {{{0, 1, 0}, {1, 2, 1}}, {{0, 2, 1}, {2, 1, 0}}};
+// barycentric quadrature points (rows) of the triangle rule
+__constant__ double c_qphi2[3][3] = {{0.5, 0.5, 0.0}, {0.0, 0.5, 0.5}, {0.5, 0.0, 0.5}};
+
+// Phase 1, one thread per (cell, triangle): kbar, the lumped mass of each vertex (times
+// area) and the Gaussian load of each vertex (times area); slots of 4 per element as in 3D.
+__global__ void k_vc_tris(Grid g, VcMat Mi, VcMat Mo, VcRegion R, const double* __restrict__ T_old,
+                          const double* __restrict__ T_lag, double dt, Gauss src, double* __restrict__ tk,
+                          double* __restrict__ tml, double* __restrict__ tsrc) {
+    const double area = 0.5 * g.h[0] * g.h[1];
+    const int ncell = g.nc[0] * g.nc[1];
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < 2 * ncell; e += gridDim.x * blockDim.x) {
+        const int c = e >> 1, t = e & 1;
+        const int cell[2] = {c % g.nc[0], c / g.nc[0]};
+        double Tl[3], To[3];
+        for (int v = 0; v < 3; ++v) {
+            const int id = (cell[0] + c_tri[t][v][0]) + g.NX * (cell[1] + c_tri[t][v][1]);
+            Tl[v] = T_lag[id];
+            To[v] = T_old[id];
+        }
+        bool inside = true;
+        if (R.piecewise || R.latent_inside) {
+            for (int a = 0; a < 2; ++a) {
+                double sx = 0.0;
+                for (int v = 0; v < 3; ++v) sx += node_coord(g, a, cell[a] + c_tri[t][v][a]);
+                const double cen = sx / 3.0;
+                inside = inside && cen >= R.lo[a] && cen <= R.hi[a];
+            }
+        }
+        const VcMat& M = (R.piecewise && !inside) ? Mo : Mi;
+        const bool lat_on = M.latent && (!R.latent_inside || inside);
+        const double w3 = 1.0 / 3.0;
+        double kbar = 0.0, ml[3] = {0.0, 0.0, 0.0}, qs[3] = {0.0, 0.0, 0.0};
+        for (int q = 0; q < 3; ++q) {
+            double tq = 0.0, tqo = 0.0;
+            for (int v = 0; v < 3; ++v) {
+                tq += c_qphi2[q][v] * Tl[v];
+                tqo += c_qphi2[q][v] * To[v];
+            }
+            const double kq = vc_interp(tq, M.kT, M.kv, M.nk);
+            double cq = vc_interp(tq, M.cT, M.cv, M.nc);
+            if (lat_on) cq += vc_latent(M, tq, tqo);
+            kbar += w3 * kq;
+            const double mq = w3 * (M.rho * cq / dt);
+            double Qq = 0.0;
+            if (src.on) {
+                double x[2];
+                for (int a = 0; a < 2; ++a) {
+                    double sx = 0.0;
+                    for (int v = 0; v < 3; ++v) sx += c_qphi2[q][v] * node_coord(g, a, cell[a] + c_tri[t][v][a]);
+                    x[a] = sx;
+                }
+                const double ux = (x[0] - src.center[0]) / src.radius, uy = (x[1] - src.center[1]) / src.depth;
+                Qq = w3 * (src.peak * exp(-(ux * ux + uy * uy)));
+            }
+            for (int r = 0; r < 3; ++r) {
+                ml[r] += mq * c_qphi2[q][r];
+                qs[r] += Qq * c_qphi2[q][r];
+            }
+        }
+        tk[e] = kbar;
+        for (int r = 0; r < 3; ++r) {
+            tml[4 * (size_t)e + r] = ml[r] * area;
+            tsrc[4 * (size_t)e + r] = qs[r] * area;
+        }
+    }
+}
+
+// Phase 2, one thread per node: gather the (up to six) triangles touching the node in a
+// fixed order (no atomics), then the lumped Robin terms of the adjacent top edges.
+__global__ void k_vc_assemble2(Grid g, const double* __restrict__ tk, const double* __restrict__ tml,
+                               const double* __restrict__ tsrc, const double* __restrict__ T_old,
+                               const double* __restrict__ T_lag, const double* __restrict__ extra, VcRobin rb,
+                               double* __restrict__ diag, double* __restrict__ wx, double* __restrict__ wy,
+                               double* __restrict__ wz, double* __restrict__ b) {
+    const double area = 0.5 * g.h[0] * g.h[1];
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < g.n; p += gridDim.x * blockDim.x) {
+        const int i = p % g.NX, j = p / g.NX;
+        const double Top = T_old[p];
+        double dg = 0.0, bb = 0.0, wf[2] = {0.0, 0.0};
+        for (int o = 0; o < 4; ++o) {
+            const int oi = o & 1, oj = o >> 1;
+            const int ci = i - oi, cj = j - oj;
+            if (ci < 0 || cj < 0 || ci >= g.nc[0] || cj >= g.nc[1]) continue;
+            const int c = ci + g.nc[0] * cj;
+            for (int t = 0; t < 2; ++t) {
+                int r = -1;
+                for (int v = 0; v < 3; ++v)
+                    if (c_tri[t][v][0] == oi && c_tri[t][v][1] == oj) r = v;
+                if (r < 0) continue;
+                const size_t e = 2 * (size_t)c + t;
+                const double ml = tml[4 * e + r];
+                const double kbar = tk[e];
+                dg += ml;
+                bb += ml * Top + tsrc[4 * e + r];
+                for (int l = 0; l < 2; ++l) {
+                    const int va = c_leg[t][l][0], vb = c_leg[t][l][1], ax = c_leg[t][l][2];
+                    if (r != va && r != vb) continue;
+                    const double we = kbar * area / (g.h[ax] * g.h[ax]);
+                    dg += we;
+                    if (r == va) wf[ax] += we;      // the leg's lower node holds its weight
+                }
+            }
+        }
+        if (rb.on && j == g.nc[1]) {
+            // top edges [il, il + 1]; facet nodes in the reference's order (right, left):
+            // the facet of [n00, n11, n01] that omits vertex 0 (mesh.py:190-192)
+            const double g2 = 0.5 / sqrt(3.0);
+            const double fphi[2][2] = {{0.5 + g2, 0.5 - g2}, {0.5 - g2, 0.5 + g2}};
+            const double load = rb.h * rb.Tamb + rb.se * (rb.Tamb * rb.Tamb * rb.Tamb * rb.Tamb);
+            for (int il = i - 1; il <= i; ++il) {
+                if (il < 0 || il >= g.nc[0]) continue;
+                const double Tr = T_lag[(il + 1) + g.NX * j], Tleft = T_lag[il + g.NX * j];
+                const int me = (il + 1 == i) ? 0 : 1;
+                for (int q = 0; q < 2; ++q) {
+                    const double tq = fphi[q][0] * Tr + fphi[q][1] * Tleft;
+                    const double coeff = rb.h + rb.se * (tq * tq * tq);
+                    dg += 0.5 * coeff * fphi[q][me] * g.h[0];
+                    bb += 0.5 * load * fphi[q][me] * g.h[0];
+                }
+            }
+        }
+        if (extra) bb += extra[p];
+        diag[p] = dg;
+        wx[p] = wf[0];
+        wy[p] = wf[1];
+        wz[p] = 0.0;
+        b[p] = bb;
+    }
+}
+
+// P1 interpolant of v on the triangle lattice at (x, y) (Mesh.locate / interpolate,
+// mesh.py:308-361): cell by floor (clipped), triangle 0 where xi >= eta (the first
+// candidate wins ties; on the diagonal both give the same value), P1 inside it.
+__device__ __forceinline__ double p1_eval2(const Grid& G, const double* v, double x, double y) {
+    const double pt[2] = {x, y};
+    int c[2];
+    double xi[2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+        int ci = (int)floor((pt[a] - (G.lo0[a] + G.off[a])) / G.h[a]);
+        ci = ci < 0 ? 0 : (ci > G.nc[a] - 1 ? G.nc[a] - 1 : ci);
+        c[a] = ci;
+        xi[a] = (pt[a] - node_coord(G, a, ci)) / G.h[a];
+    }
+    const int p0 = c[0] + G.NX * c[1];
+    const double v00 = v[p0], v11 = v[p0 + G.NX + 1];
+    if (xi[0] >= xi[1]) return (1.0 - xi[0]) * v00 + (xi[0] - xi[1]) * v[p0 + 1] + xi[1] * v11;
+    return (1.0 - xi[1]) * v00 + xi[0] * v11 + (xi[1] - xi[0]) * v[p0 + G.NX];
+}
+
+// Global field at the nodes of a 2D local lattice (trace, relocation, error metrics);
+// gamma_only: lateral (i = 0, NX-1) and bottom (j = 0) nodes only, the others untouched.
+__global__ void k_interp2(Grid G, Grid L, const double* __restrict__ vg, double* __restrict__ out, int gamma_only) {
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < L.n; p += gridDim.x * blockDim.x) {
+        const int i = p % L.NX, j = p / L.NX;
+        if (gamma_only && !(i == 0 || i == L.nc[0] || j == 0)) continue;
+        out[p] = p1_eval2(G, vg, node_coord(L, 0, i), node_coord(L, 1, j));
+    }
+}
+
+__global__ void k_interp_pts2(Grid G, const double* __restrict__ vg, const double* __restrict__ pts, int npts,
+                              double* __restrict__ out) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < npts; e += gridDim.x * blockDim.x)
+        out[e] = p1_eval2(G, vg, pts[2 * e], pts[2 * e + 1]);
+}
+
+// v^T M v with the consistent P1 mass matrix of the triangles (fem.mass_matrix,
+// fem.py:434-446): per triangle area/12 (sum v_i^2 + (sum v_i)^2); d = a - b (d = a when
+// b == nullptr) -> part[2 blk], b -> part[2 blk + 1].
+__global__ void k_mass_norms2(Grid L, const double* __restrict__ a, const double* __restrict__ b, double* part) {
+    __shared__ double red[64];
+    const int ncell = L.nc[0] * L.nc[1];
+    double acc[2] = {0.0, 0.0};
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncell; c += gridDim.x * blockDim.x) {
+        const int p0 = (c % L.nc[0]) + L.NX * (c / L.nc[0]);
+        const int off[4] = {0, 1, L.NX, L.NX + 1};
+        double d[4], r[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const double av = a[p0 + off[q]];
+            const double bv = b ? b[p0 + off[q]] : 0.0;
+            d[q] = b ? av - bv : av;
+            r[q] = bv;
+        }
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+            const int m = t == 0 ? 1 : 2;          // (0,0) m (1,1): the triangle's third corner
+            const double s1 = d[0] + d[m] + d[3];
+            acc[0] += d[0] * d[0] + d[m] * d[m] + d[3] * d[3] + s1 * s1;
+            const double s2 = r[0] + r[m] + r[3];
+            acc[1] += r[0] * r[0] + r[m] * r[m] + r[3] * r[3] + s2 * s2;
+        }
+    }
+    block_sum<2>(acc, red);
+    if (threadIdx.x == 0) {
+        const double w = 0.5 * L.h[0] * L.h[1] / 12.0;
+        part[2 * blockIdx.x] = acc[0] * w;
+        part[2 * blockIdx.x + 1] = acc[1] * w;
+    }
+}
+
+}  // namespace tl

@@ -29,6 +29,7 @@
 #include "tl_slab.cuh"
 #include "tl_slabdev.cuh"
 #include "tl_vc.cuh"
+#include "tl_2d.cuh"
 
 // cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device, per-function attribute:
 // remember the largest size set for each (device, kernel) and raise it when needed.
@@ -63,8 +64,16 @@ int fail(int code, const std::string& msg) {
             return fail(TL_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));       \
     } while (0)
 
-int make_grid(const tl_grid_desc& d, int dkind, tl::Grid& g) {
-    for (int a = 0; a < 3; ++a) {
+// allow2d: a descriptor with ncells[2] == 0 is a 2D grid (NZ = 1; csrc/tl_2d.cuh); only the
+// entry points with triangle variants accept it.
+int make_grid(const tl_grid_desc& d, int dkind, tl::Grid& g, bool allow2d = false) {
+    const int dim = (allow2d && d.ncells[2] == 0) ? 2 : 3;
+    if (dim == 2) {
+        g.nc[2] = 0;
+        g.lo0[2] = g.hi0[2] = g.off[2] = g.step[2] = 0.0;
+        g.h[2] = 1.0;
+    }
+    for (int a = 0; a < dim; ++a) {
         if (d.ncells[a] < 1) return fail(TL_E_INVALID, "grid needs at least one cell per axis");
         if (!(d.hi0[a] > d.lo0[a])) return fail(TL_E_INVALID, "degenerate grid box");
         g.nc[a] = d.ncells[a];
@@ -889,13 +898,17 @@ int32_t tl_interpolate_host(const tl_grid_desc* global_grid, const double* value
                             const tl_grid_desc* target, int32_t gamma_only, double* out) {
     if (!global_grid || !values || !target || !out) return fail(TL_E_INVALID, "null argument");
     tl::Grid G{}, L{};
-    if (int rc = make_grid(*global_grid, tl::kBottom, G)) return rc;
-    if (int rc = make_grid(*target, tl::kGamma, L)) return rc;
+    if (int rc = make_grid(*global_grid, tl::kBottom, G, true)) return rc;
+    if (int rc = make_grid(*target, tl::kGamma, L, true)) return rc;
+    if (tl::grid_is_2d(G) != tl::grid_is_2d(L)) return fail(TL_E_INVALID, "grids of different dimension");
     double *dv, *dout;
     std::lock_guard<std::mutex> lock(g_scratch_mu);
     if (int rc = scratch_arrays({{(size_t)G.n, 8, (void**)&dv}, {(size_t)L.n, 8, (void**)&dout}})) return rc;
     TL_CUDA(cudaMemcpy(dv, values, sizeof(double) * G.n, cudaMemcpyHostToDevice));
     TL_CUDA(cudaMemcpy(dout, out, sizeof(double) * L.n, cudaMemcpyHostToDevice));
+    if (tl::grid_is_2d(G))
+        tl::k_interp2<<<296, 256>>>(G, L, dv, dout, gamma_only ? 1 : 0);
+    else
     tl::k_interp<<<592, 256>>>(G, dv, L, gamma_only ? 1 : 0, gamma_only ? nullptr : dout,
                                gamma_only ? dout : nullptr);
     TL_CUDA(cudaGetLastError());
@@ -971,7 +984,7 @@ static int vc_impl(const tl_grid_desc* grid, const tl_vc_material* mat, const tl
     if (!(dt > 0.0)) return fail(TL_E_INVALID, "time step must be positive");
     if (mat->nk < 2 || mat->nc < 2) return fail(TL_E_INVALID, "material tables need two rows");
     tl::Grid G{};
-    if (int rc = make_grid(*grid, tl::kBottom, G)) return rc;
+    if (int rc = make_grid(*grid, tl::kBottom, G, true)) return rc;
     const int n = G.n;
     constexpr int kNB = 296, kT = 256;
     // device workspace kept across calls (a Picard loop calls this once per pass); grown on
@@ -998,7 +1011,8 @@ static int vc_impl(const tl_grid_desc* grid, const tl_vc_material* mat, const tl
     double* cpart = nullptr;
     const size_t per = (size_t)n + 2, nt_i = 2 * (size_t)(mat->nk + mat->nc);
     const size_t nt = nt_i + (mat_outside ? 2 * (size_t)(mat_outside->nk + mat_outside->nc) : 0);
-    const size_t ntet = 6 * (size_t)G.nc[0] * G.nc[1] * G.nc[2];
+    const bool two_d = tl::grid_is_2d(G);
+    const size_t ntet = two_d ? 2 * (size_t)G.nc[0] * G.nc[1] : 6 * (size_t)G.nc[0] * G.nc[1] * G.nc[2];
     const size_t want = 16 * per + nt + 6 * 4096 + 9 * ntet;
     if (want > ws_cap) {
         if (ws) cudaFree(ws);
@@ -1073,8 +1087,13 @@ static int vc_impl(const tl_grid_desc* grid, const tl_vc_material* mat, const tl
     double inc = INFINITY, prev_inc = INFINITY, theta = 1.0;
     *passes = 0;
     for (int pit = 1; pit <= picard_max; ++pit) {
+    if (two_d) {
+        tl::k_vc_tris<<<4 * kNB, kT>>>(G, M, Mo, RG, dTo, dTl, dt, S, tk, tml, tsrc);
+        tl::k_vc_assemble2<<<kNB, kT>>>(G, tk, tml, tsrc, dTo, dTl, dex, RB, diag, wx, wy, wz, b);
+    } else {
     tl::k_vc_tets<<<4 * kNB, kT>>>(G, M, Mo, RG, dTo, dTl, dt, S, tk, tml, tsrc);
     tl::k_vc_assemble<<<kNB, kT>>>(G, tk, tml, tsrc, dTo, dTl, dex, RB, diag, wx, wy, wz, b);
+    }
     tl::k_vc_constrain_b<<<kNB, kT>>>(G, dm, dg, wx, wy, wz, diag, b);
     tl::k_vc_constrain_w<<<kNB, kT>>>(G, dm, wx, wy, wz);
     TL_CUDA(cudaGetLastError());
@@ -1271,7 +1290,7 @@ static int transmission_impl(const tl_grid_desc* global_grid, const tl_grid_desc
 int32_t tl_mass_norms_host(const tl_grid_desc* grid, const double* a, const double* b, double* out) {
     if (!grid || !a || !out) return fail(TL_E_INVALID, "null argument");
     tl::Grid L{};
-    if (int rc = make_grid(*grid, tl::kGamma, L)) return rc;
+    if (int rc = make_grid(*grid, tl::kGamma, L, true)) return rc;
     constexpr int kNB = 296;
     double *da, *db = nullptr, *dpart;
     std::lock_guard<std::mutex> lock(g_scratch_mu);
@@ -1281,7 +1300,8 @@ int32_t tl_mass_norms_host(const tl_grid_desc* grid, const double* a, const doub
     if (!b) db = nullptr;
     TL_CUDA(cudaMemcpy(da, a, sizeof(double) * L.n, cudaMemcpyHostToDevice));
     if (b) TL_CUDA(cudaMemcpy(db, b, sizeof(double) * L.n, cudaMemcpyHostToDevice));
-    tl::k_mass_norms<<<kNB, 256>>>(L, da, db, dpart);
+    if (tl::grid_is_2d(L)) tl::k_mass_norms2<<<kNB, 256>>>(L, da, db, dpart);
+    else tl::k_mass_norms<<<kNB, 256>>>(L, da, db, dpart);
     TL_CUDA(cudaGetLastError());
     double part[2 * kNB];
     TL_CUDA(cudaMemcpy(part, dpart, sizeof(part), cudaMemcpyDeviceToHost));
@@ -1317,8 +1337,9 @@ int32_t tl_error_l2_host(const tl_grid_desc* ref_grid, const double* ref_values,
                          const double* values, double* out) {
     if (!ref_grid || !ref_values || !grid || !values || !out) return fail(TL_E_INVALID, "null argument");
     tl::Grid G{}, L{};
-    if (int rc = make_grid(*ref_grid, tl::kBottom, G)) return rc;
-    if (int rc = make_grid(*grid, tl::kGamma, L)) return rc;
+    if (int rc = make_grid(*ref_grid, tl::kBottom, G, true)) return rc;
+    if (int rc = make_grid(*grid, tl::kGamma, L, true)) return rc;
+    if (tl::grid_is_2d(G) != tl::grid_is_2d(L)) return fail(TL_E_INVALID, "grids of different dimension");
     constexpr int kNB = 296;
     double *dref, *dv, *dri, *dpart;
     std::lock_guard<std::mutex> lock(g_scratch_mu);
@@ -1327,8 +1348,13 @@ int32_t tl_error_l2_host(const tl_grid_desc* ref_grid, const double* ref_values,
         return rc;
     TL_CUDA(cudaMemcpy(dref, ref_values, sizeof(double) * G.n, cudaMemcpyHostToDevice));
     TL_CUDA(cudaMemcpy(dv, values, sizeof(double) * L.n, cudaMemcpyHostToDevice));
+    if (tl::grid_is_2d(G)) {
+        tl::k_interp2<<<296, 256>>>(G, L, dref, dri, 0);
+        tl::k_mass_norms2<<<kNB, 256>>>(L, dv, dri, dpart);
+    } else {
     tl::k_interp<<<592, 256>>>(G, dref, L, 0, dri, nullptr);     // reference on the grid's nodes
     tl::k_mass_norms<<<kNB, 256>>>(L, dv, dri, dpart);
+    }
     TL_CUDA(cudaGetLastError());
     double part[2 * kNB];
     TL_CUDA(cudaMemcpy(part, dpart, sizeof(part), cudaMemcpyDeviceToHost));
@@ -1341,14 +1367,17 @@ int32_t tl_interpolate_points_host(const tl_grid_desc* global_grid, const double
                                    const double* points, int64_t npoints, double* out) {
     if (!global_grid || !values || !points || !out || npoints < 0) return fail(TL_E_INVALID, "bad argument");
     tl::Grid G{};
-    if (int rc = make_grid(*global_grid, tl::kBottom, G)) return rc;
+    if (int rc = make_grid(*global_grid, tl::kBottom, G, true)) return rc;
+    const int pd = tl::grid_is_2d(G) ? 2 : 3;          // doubles per point
     double *dv, *dp, *dout;
     std::lock_guard<std::mutex> lock(g_scratch_mu);
-    if (int rc = scratch_arrays({{(size_t)G.n, 8, (void**)&dv}, {3 * (size_t)npoints, 8, (void**)&dp},
+    if (int rc = scratch_arrays({{(size_t)G.n, 8, (void**)&dv}, {pd * (size_t)npoints, 8, (void**)&dp},
                                  {(size_t)npoints, 8, (void**)&dout}}))
         return rc;
     TL_CUDA(cudaMemcpy(dv, values, sizeof(double) * G.n, cudaMemcpyHostToDevice));
-    TL_CUDA(cudaMemcpy(dp, points, sizeof(double) * 3 * npoints, cudaMemcpyHostToDevice));
+    TL_CUDA(cudaMemcpy(dp, points, sizeof(double) * pd * npoints, cudaMemcpyHostToDevice));
+    if (npoints > 0 && pd == 2) tl::k_interp_pts2<<<296, 256>>>(G, dv, dp, (int)npoints, dout);
+    else
     if (npoints > 0) tl::k_interp_pts<<<296, 256>>>(G, dv, dp, npoints, dout);
     TL_CUDA(cudaGetLastError());
     TL_CUDA(cudaMemcpy(out, dout, sizeof(double) * npoints, cudaMemcpyDeviceToHost));
