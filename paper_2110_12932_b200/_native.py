@@ -36,8 +36,11 @@ class GridDesc(C.Structure):
 
     @classmethod
     def make(cls, lo0, hi0, ncells, offset=(0.0, 0.0, 0.0)) -> "GridDesc":
-        return cls(_i3(*[int(v) for v in ncells]), _d3(*map(float, lo0)), _d3(*map(float, hi0)),
-                   _d3(*map(float, offset)))
+        # a 2D grid travels as ncells[2] = 0 (csrc/tl_2d.cuh); only the entry points with
+        # triangle variants accept it
+        pad = lambda v, fill: [*v, *([fill] * (3 - len(v)))]      # noqa: E731
+        return cls(_i3(*pad([int(v) for v in ncells], 0)), _d3(*pad(list(map(float, lo0)), 0.0)),
+                   _d3(*pad(list(map(float, hi0)), 0.0)), _d3(*pad(list(map(float, offset)), 0.0)))
 
 
 class Gaussian(C.Structure):

@@ -106,10 +106,26 @@ class GaussianSource:
     beam: object
     center: tuple
 
+    @property
+    def dim(self) -> int:
+        return len(self.center)
+
+    @property
+    def peak(self) -> float:
+        """3D: ``gaussian_source_3d``'s peak; 2D: P eta / (r d) (``sources.py:57-64``)."""
+        b = self.beam
+        if self.dim == 2:
+            return b.power * b.absorptivity / (b.radius * b.depth)
+        return b.gaussian_peak
+
     def __call__(self, points):
         p = np.atleast_2d(np.asarray(points, dtype=float))
         c = np.asarray(self.center, dtype=float)
         b = self.beam
+        if self.dim == 2:
+            ex = ((p[:, 0] - c[0]) / b.radius) ** 2
+            ey = ((p[:, 1] - c[1]) / b.depth) ** 2
+            return self.peak * np.exp(-(ex + ey))
         ex = 3.0 * ((p[:, 0] - c[0]) / b.radius) ** 2
         ey = 3.0 * ((p[:, 1] - c[1]) / b.radius) ** 2
         ez = 3.0 * ((p[:, 2] - c[2]) / b.depth) ** 2
@@ -117,7 +133,8 @@ class GaussianSource:
 
     def device_args(self):
         b = self.beam
-        return (b.gaussian_peak, b.radius, b.depth, tuple(float(v) for v in self.center))
+        c = tuple(float(v) for v in self.center)
+        return (self.peak, b.radius, b.depth, c if len(c) == 3 else (*c, 0.0))
 
 
 def device_rtol(settings: SolverSettings) -> float:
@@ -196,6 +213,11 @@ def _needs_general_path(mat, bounds: BoundarySpec, latent: bool) -> bool:
     return convective or isinstance(mat, PiecewiseMaterial) or not problem_is_linear(mat, bounds, latent)
 
 
+def _pad3(v) -> list:
+    v = [float(x) for x in v]
+    return v + [0.0] * (3 - len(v))
+
+
 def vc_material(mat, latent: bool):
     """``tl_vc_material`` of a material (tables in K); returns (struct, arrays kept alive)."""
     kt = np.ascontiguousarray(mat.conductivity_table, dtype=np.float64)
@@ -235,7 +257,7 @@ def _step_general(state: FieldState, dt: float, mat, source, bounds: BoundarySpe
         if region is not None and (tuple(latent_mask.box.lo), tuple(latent_mask.box.hi)) != (tuple(region.lo), tuple(region.hi)):
             raise UnsupportedOnDevice("the latent mask and the material region must be the same box")
         region = latent_mask.box
-    reg = None if region is None else np.array(list(region.lo) + list(region.hi), dtype=np.float64)
+    reg = None if region is None else np.array(_pad3(region.lo) + _pad3(region.hi), dtype=np.float64)
     rb = N.Robin(float(bounds.bc.h_conv) if conv else 0.0,
                  float(bounds.bc.sigma_sb * bounds.bc.emissivity) if rad else 0.0,
                  float(bounds.bc.T_ambient), 1 if (conv or rad) else 0)
@@ -312,7 +334,9 @@ def step_backward_euler(state: FieldState, dt: float, mat, source, bounds: Bound
         raise UnsupportedOnDevice("the device takes latent masks as a box region (fem.RegionMask)")
     if source is not None and not isinstance(source, GaussianSource):
         raise UnsupportedOnDevice("the device evaluates GaussianSource objects, not opaque callables")
-    if _needs_general_path(mat, bounds, latent) or latent_mask is not None:
+    # 2D grids (P1 triangles, csrc/tl_2d.cuh) always take the general path: the fused linear
+    # kernels are the 3D 27-class stencil
+    if _needs_general_path(mat, bounds, latent) or latent_mask is not None or state.mesh.dim == 2:
         return _step_general(state, dt, mat, source, bounds, settings, latent, extra_load, stats,
                              latent_mask=latent_mask)
     check_linear_problem(mat, bounds, latent)

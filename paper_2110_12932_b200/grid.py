@@ -23,12 +23,17 @@ BOTTOM, TOP, LATERAL = 0, 1, 2
 
 
 class StructuredGrid:
-    """Uniform lattice of a box, Kuhn-subdivided implicitly (6 tets per cell)."""
+    """Uniform lattice of a box, subdivided implicitly: 6 Kuhn tets per cell in 3D, the two
+    triangles ``[0, 1, 3]`` / ``[0, 3, 2]`` per cell in 2D (``mesh.py:84-102``).  In 2D the
+    vertical axis is y (BOTTOM / TOP are y = lo / hi, ``mesh.py:206-209``) and ``shape`` is
+    ``(1, NY, NX)``."""
 
     def __init__(self, placement: LocalPlacement):
         self._placement = placement
         self.box = placement.box
-        self.dim = 3
+        self.dim = int(self.box.dim)
+        if self.dim not in (2, 3):
+            raise MeshError("structured grids are 2D or 3D")
         self.ncells = placement.ncells
         self.spacing = self.box.lengths / self.ncells
 
@@ -41,6 +46,8 @@ class StructuredGrid:
     @property
     def shape(self) -> tuple:
         n = self.ncells
+        if self.dim == 2:
+            return (1, int(n[1]) + 1, int(n[0]) + 1)
         return (int(n[2]) + 1, int(n[1]) + 1, int(n[0]) + 1)
 
     @property
@@ -49,7 +56,7 @@ class StructuredGrid:
 
     @property
     def n_elems(self) -> int:
-        return 6 * int(np.prod(self.ncells))
+        return (2 if self.dim == 2 else 6) * int(np.prod(self.ncells))
 
     @property
     def h(self) -> float:
@@ -64,7 +71,12 @@ class StructuredGrid:
 
     @cached_property
     def coords(self) -> np.ndarray:
-        """(n_nodes, 3) node coordinates, materialised on first use."""
+        """(n_nodes, dim) node coordinates, materialised on first use."""
+        if self.dim == 2:
+            Y, X = np.meshgrid(self.axis(1), self.axis(0), indexing="ij")
+            out = np.stack([X.ravel(), Y.ravel()], axis=1)
+            out.setflags(write=False)
+            return out
         x, y, z = self.axis(0), self.axis(1), self.axis(2)
         Z, Y, X = np.meshgrid(z, y, x, indexing="ij")
         out = np.stack([X.ravel(), Y.ravel(), Z.ravel()], axis=1)
@@ -80,6 +92,13 @@ class StructuredGrid:
         import itertools
         nc = [int(v) for v in self.ncells]
         nn = [v + 1 for v in nc]
+        if self.dim == 2:
+            CY, CX = np.meshgrid(np.arange(nc[1]), np.arange(nc[0]), indexing="ij")
+            c0 = (CX + nn[0] * CY).ravel()
+            corner = c0[:, None] + np.array([0, 1, nn[0], nn[0] + 1])
+            tris = corner[:, np.array([[0, 1, 3], [0, 3, 2]])].reshape(-1, 3).astype(np.int64)
+            tris.setflags(write=False)
+            return tris
         strides = np.array([1, nn[0], nn[0] * nn[1]], dtype=np.int64)
         CZ, CY, CX = np.meshgrid(np.arange(nc[2]), np.arange(nc[1]), np.arange(nc[0]), indexing="ij")
         corner0 = np.stack([CX.ravel(), CY.ravel(), CZ.ravel()], axis=1) @ strides
@@ -102,8 +121,15 @@ class StructuredGrid:
 
     def nodes_on(self, *tags: int) -> np.ndarray:
         """Sorted node ids of boundary facets with the given tags (``mesh.py:226-230``)."""
-        NZ, NY, NX = self.shape
         m = np.zeros(self.shape, dtype=bool)
+        if self.dim == 2:                       # vertical axis = y
+            if BOTTOM in tags:
+                m[:, 0, :] = True
+            if TOP in tags:
+                m[:, -1, :] = True
+            if LATERAL in tags:
+                m[:, :, 0] = m[:, :, -1] = True
+            return np.nonzero(m.ravel())[0]
         if BOTTOM in tags:
             m[0] = True
         if TOP in tags:
@@ -116,6 +142,10 @@ class StructuredGrid:
     def gamma_mask(self) -> np.ndarray:
         """Flat bool mask of the interface (trace) nodes: lateral + bottom facets."""
         m = np.zeros(self.shape, dtype=bool)
+        if self.dim == 2:
+            m[:, 0, :] = True
+            m[:, :, 0] = m[:, :, -1] = True
+            return m.ravel()
         m[0] = True
         m[:, 0, :] = m[:, -1, :] = True
         m[:, :, 0] = m[:, :, -1] = True
@@ -144,7 +174,7 @@ class StructuredGrid:
 
 
 def build_structured_grid(box: Box, h) -> StructuredGrid:
-    """``build_structured_mesh`` for 3D boxes (``lpbfsim/mesh.py:388-439``)."""
-    if box.dim != 3:
-        raise MeshError("the device path supports 3D boxes only")
+    """``build_structured_mesh`` (``lpbfsim/mesh.py:388-439``) for 2D and 3D boxes."""
+    if box.dim not in (2, 3):
+        raise MeshError("the device path supports 2D and 3D boxes")
     return StructuredGrid(LocalPlacement(box, structured_ncells(box, h)))

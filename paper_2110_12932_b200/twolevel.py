@@ -47,6 +47,9 @@ class InterfaceGamma:
     @property
     def measure(self) -> float:
         """Total area of the interface facets (``mesh.py:467-469``): lateral + bottom faces."""
+        if self.local.dim == 2:                 # bottom edge + the two lateral edges
+            lx, ly = (float(v) for v in self.local.box.lengths)
+            return lx + 2.0 * ly
         lx, ly, lz = (float(v) for v in self.local.box.lengths)
         return lx * ly + 2.0 * (lx * lz + ly * lz)
 
@@ -178,7 +181,14 @@ class TwoLevelProblem:
             raise UnsupportedOnDevice("the device-resident run uses the distributed (swept-track) "
                                       "global source; 'gaussian' runs through the step-level drivers")
         if self.global_mesh.dim != 3:
-            raise UnsupportedOnDevice("the device path is 3D only")
+            # 2D (P1 triangles, csrc/tl_2d.cuh): the step-level drivers with the Picard-path
+            # solves; the interface functional and the overlap feedback have no 2D kernels
+            if resident:
+                raise UnsupportedOnDevice("the device-resident run is 3D; 2D runs go through the "
+                                          "step-level drivers")
+            if not self.one_way:
+                raise UnsupportedOnDevice("2D two-way coupling (distinct conductivities or full mode) "
+                                          "is not on the device path")
 
     @property
     def device_resident(self) -> bool:
@@ -216,6 +226,9 @@ def transmission_load(local_field, gamma, global_mesh, mat_global, mat_local) ->
     if np.array_equal(mat_global.conductivity_table, mat_local.conductivity_table):
         return np.zeros(global_mesh.n_nodes)
     lmesh = local_field.mesh
+    if lmesh.dim != 3:
+        raise UnsupportedOnDevice("the interface functional has no 2D kernel (equal conductivities "
+                                  "make it exactly zero)")
     T = np.ascontiguousarray(local_field.values, dtype=np.float64)
     if T.shape != (lmesh.n_nodes,):
         raise CouplingError("local field does not match its mesh")

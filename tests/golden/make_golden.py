@@ -468,6 +468,79 @@ def track3d_case():
     shutil.rmtree(tmp)
 
 
+def picard2d_case(name, latent, radiation, h_conv, seed=9):
+    """One nonlinear implicit step on the shipped 2D plate (5 x 1 mm, h = 62.5 um, P1
+    triangles) from a heated T_old, bottom-edge Dirichlet, 2D Gaussian beam, IN625 tables."""
+    rng = np.random.default_rng(seed)
+    m = lmesh.build_structured_mesh(lmesh.Box((0.0, 0.0), (5e-3, 1e-3)), 6.25e-5)
+    mat = lpbfsim.materials.load_material(REF / "lpbfsim" / "data" / "in625.mat")
+    if not latent:
+        mat = mat.with_chi(0.0)
+    bc = sources.ThermalBC(h_conv, 0.8 if radiation else 0.0, 298.15, 298.15)
+    beam = sources.LaserBeam(20000.0, 1.0, 1e-4, 1.25e-5, 4e-3)
+    X = m.coords
+    r2 = ((X - np.array([2.0e-3, 1e-3])) ** 2 / np.array([3e-4, 1.2e-4]) ** 2).sum(axis=1)
+    T_old = 298.15 + 1500.0 * np.exp(-r2) + rng.uniform(0.0, 5.0, m.n_nodes)
+    center = np.array([2.04e-3, 1e-3])
+    src = lambda pts: sources.gaussian_source_2d(beam, center, pts)  # noqa: E731
+    bounds = fem.BoundarySpec(bc=bc, robin_tags=(lmesh.TOP,), radiation=radiation,
+                              dirichlet_nodes=m.nodes_on(lmesh.BOTTOM), dirichlet_values=298.15)
+    settings = fem.SolverSettings(picard_tol=1e-8, linear_tol=1e-12, linear_solver="cg")
+    stats = RunStats()
+    CG_ITERS.clear()
+    out = fem.step_backward_euler(fem.FieldState(m, T_old, 0.0), 1e-2, mat, src, bounds, settings,
+                                  latent=latent, stats=stats)
+    np.savez_compressed(
+        OUT / f"picard2d_{name}.npz", lo=[0.0, 0.0], hi=[5e-3, 1e-3], h=6.25e-5, dt=1e-2,
+        T_old=T_old, center=center, sol=out.values, latent=latent, radiation=radiation, h_conv=h_conv,
+        beam=np.array([beam.power, beam.absorptivity, beam.radius, beam.depth]),
+        k_table=mat.conductivity_table, c_table=mat.heat_capacity_table,
+        mat_scalars=np.array([mat.rho, mat.chi, mat.T_solidus, mat.T_liquidus, mat.S]),
+        picard=stats.counters.get("picard_iterations", 0), cg_iters=np.array(CG_ITERS),
+        l2=fem.l2_norm(m, out.values), versions=json.dumps(VERS))
+    print(f"picard2d_{name}: picard={stats.counters} cg={CG_ITERS} max={out.values.max():.2f}")
+
+
+def interp2d_case(seed=4):
+    """Mesh.interpolate on the 2D triangle lattice: random points, lattice nodes and points
+    on cell diagonals (ties between the two triangles of a cell)."""
+    rng = np.random.default_rng(seed)
+    box = lmesh.Box((0.0, 0.0), (5e-3, 1e-3))
+    m = lmesh.build_structured_mesh(box, 6.25e-5)
+    v = rng.uniform(300.0, 2000.0, m.n_nodes)
+    pts = np.stack([rng.uniform(0.0, 5e-3, 4000), rng.uniform(0.0, 1e-3, 4000)], axis=1)
+    pts[:300] = m.coords[rng.integers(0, m.n_nodes, 300)]
+    k = rng.integers(0, 80, 300)
+    f = rng.uniform(0.0, 1.0, 300)
+    pts[300:600, 0] = (k + f) * 6.25e-5
+    pts[300:600, 1] = (rng.integers(0, 16, 300) + f) * 6.25e-5
+    np.savez_compressed(OUT / "interp2d.npz", lo=[0.0, 0.0], hi=[5e-3, 1e-3], h=6.25e-5, values=v, points=pts,
+                        out=m.interpolate(v, pts), l2=fem.l2_norm(m, v), versions=json.dumps(VERS))
+    print("interp2d: done")
+
+
+def run2d_case(name, full_at, stride):
+    """configs/run2d*.cfg (the reference's shipped 2D study geometry and physics) run by the
+    reference with its own IN625 file; the tables go into the npz for the device test."""
+    import shutil
+    import tempfile
+    global CFG
+    tmp = Path(tempfile.mkdtemp())
+    shutil.copy(CFG / f"{name}.cfg", tmp / f"{name}.cfg")
+    shutil.copy(REF / "lpbfsim" / "data" / "in625.mat", tmp / "in625.mat")
+    saved, CFG = CFG, tmp
+    try:
+        run_case(name, None, full_at, stride)
+    finally:
+        CFG = saved
+    mat = load_config(tmp / f"{name}.cfg").material
+    z = dict(np.load(OUT / f"run_{name}.npz"))
+    z.update(k_table=mat.conductivity_table, c_table=mat.heat_capacity_table,
+             mat_scalars=np.array([mat.rho, mat.chi, mat.T_solidus, mat.T_liquidus, mat.S]))
+    np.savez_compressed(OUT / f"run_{name}.npz", **z)
+    shutil.rmtree(tmp)
+
+
 def experiments_case():
     """runner.run_experiment in compare and convergence-study modes (cfg1 variants): the
     summaries, the study matrix and every run's errors.csv."""
@@ -557,6 +630,13 @@ def transmission_tdep_case():
 
 def main():
     quick = "--quick" in sys.argv
+    if "--2d" in sys.argv:
+        picard2d_case("tables", latent=False, radiation=False, h_conv=10.0)
+        picard2d_case("full", latent=True, radiation=True, h_conv=10.0)
+        interp2d_case()
+        run2d_case("run2d", {1, 2, 3}, 3)
+        run2d_case("run2d_uniform", {1, 5}, 3)
+        return
     if "--vtk" in sys.argv:
         return vtk_case()
     if "--piecewise" in sys.argv:

@@ -1,0 +1,119 @@
+"""2D (P1 triangle / 5-point) device path against golden vectors of the unmodified reference
+(``tests/golden/make_golden.py --2d``), through the C ABI.
+
+The reference's shipped 2D configs (``src/configs/*_2d.cfg``) use the 5 x 1 mm plate at
+h = 62.5 um, IN625 tables, convection on the top edge, the 2D Gaussian line source on both
+levels and a fixed local box; ``configs/run2d*.cfg`` restate them as two-level runs.
+"""
+
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2110_12932_b200 as P
+
+from .test_oracle_golden import picard_material
+
+pytestmark = pytest.mark.gpu
+
+ROOT = Path(__file__).resolve().parents[1]
+GOLDEN = ROOT / "tests" / "golden"
+CONFIGS = ROOT / "configs"
+REL = 1e-9          # north_star tolerance: relative L-inf per step
+
+
+def rel(a, b):
+    return float(np.abs(np.asarray(a) - np.asarray(b)).max() / np.abs(np.asarray(b)).max())
+
+
+@pytest.mark.parametrize("name", ["tables", "full"])
+def test_2d_picard_step_vs_reference(name):
+    """fem.step_backward_euler on the 2D plate (k_vc_tris + k_vc_assemble2 + the shared
+    constrained PCG): tables + convection, and + latent secant capacity + lagged radiation.
+    Same Picard pass count and CG iterations per pass, 1e-9 relative L-inf, melt mask."""
+    z = np.load(GOLDEN / f"picard2d_{name}.npz")
+    grid = P.build_structured_grid(P.Box(tuple(z["lo"]), tuple(z["hi"])), float(z["h"]))
+    mat = picard_material(z)
+    rad = bool(z["radiation"])
+    bounds = P.BoundarySpec(bc=P.ThermalBC(float(z["h_conv"]), 0.8 if rad else 0.0, 298.15, 298.15),
+                            robin_tags=(P.TOP,), radiation=rad,
+                            dirichlet_nodes=grid.nodes_on(P.BOTTOM), dirichlet_values=298.15)
+    pw, eta, r, d = (float(v) for v in z["beam"])
+    beam = P.LaserBeam(pw, eta, r, d, 4e-3)
+    stats = P.RunStats()
+    stats.device_log = []
+    out = P.step_backward_euler(P.FieldState(grid, z["T_old"], 0.0), float(z["dt"]), mat,
+                                P.GaussianSource(beam, tuple(z["center"])), bounds,
+                                P.SolverSettings(picard_tol=1e-8, linear_tol=1e-12, linear_solver="cg"),
+                                latent=bool(z["latent"]), stats=stats)
+    assert stats.counters["picard_iterations"] == int(z["picard"])
+    assert [k for _, k in stats.device_log] == list(z["cg_iters"])
+    assert rel(out.values, z["sol"]) <= REL
+    TL = mat.T_liquidus
+    np.testing.assert_array_equal(out.values > TL, z["sol"] > TL)
+    from paper_2110_12932_b200.metrics import l2_norm
+    assert l2_norm(grid, out.values) == pytest.approx(float(z["l2"]), rel=1e-9)
+
+
+def test_2d_interpolation_and_mass_norm_vs_reference():
+    """Mesh.interpolate on the triangle lattice (k_interp_pts2; lattice nodes and cell
+    diagonals included), the same field sampled on a translated finer lattice (k_interp2)
+    against the oracle, and fem.l2_norm (k_mass_norms2)."""
+    from oracle import tri2d
+    from paper_2110_12932_b200 import ops
+    from paper_2110_12932_b200.metrics import l2_norm
+    z = np.load(GOLDEN / "interp2d.npz")
+    grid = P.build_structured_grid(P.Box(tuple(z["lo"]), tuple(z["hi"])), float(z["h"]))
+    got = grid.interpolate(z["values"], z["points"])
+    assert np.abs(got - z["out"]).max() <= 1e-12 * np.abs(z["out"]).max()
+    assert l2_norm(grid, z["values"]) == pytest.approx(float(z["l2"]), rel=1e-12)
+    local = P.build_structured_grid(P.Box((2.5e-4, 6.25e-4), (4.75e-3, 1e-3)), 3.125e-5)
+    G = tri2d.Grid2D(z["lo"], z["hi"], grid.ncells)
+    want = tri2d.interpolate(G, z["values"], local.coords)
+    full = ops.interpolate_to_grid(grid, z["values"], local)
+    assert np.abs(full - want).max() <= 1e-12 * np.abs(want).max()
+    gam = ops.interpolate_to_grid(grid, z["values"], local, gamma_only=True)
+    m = local.gamma_mask()
+    np.testing.assert_array_equal(gam[m], full[m])
+    assert not gam[~m].any()
+
+
+def _write_material(z, path):
+    rho, chi, Ts, Tl, S = (float(v) for v in z["mat_scalars"])
+    lines = ["units K", f"rho {rho!r}", f"chi {chi!r}", f"T_solidus {Ts!r}", f"T_liquidus {Tl!r}", f"S {S!r}",
+             "[conductivity]"] + [f"{float(a)!r} {float(b)!r}" for a, b in z["k_table"]] + ["[heat_capacity]"] + \
+            [f"{float(a)!r} {float(b)!r}" for a, b in z["c_table"]]
+    path.write_text("\n".join(lines) + "\n")
+
+
+@pytest.mark.parametrize("name", ["run2d", "run2d_uniform"])
+def test_2d_two_level_run_vs_reference(name, tmp_path):
+    """The shipped 2D study geometry and physics as two-level runs (multirate m = 10 with the
+    coupled corrector; uniform steps as oracle_2d.cfg): every RunStats counter (Picard
+    passes, solves, coupling iterations), record times, fields to 1e-9 and melt masks against
+    the reference's run.  The IN625 tables come from the golden file."""
+    z = np.load(GOLDEN / f"run_{name}.npz")
+    _write_material(z, tmp_path / "in625.mat")
+    (tmp_path / f"{name}.cfg").write_text((CONFIGS / f"{name}.cfg").read_text())
+    cfg = P.load_config(tmp_path / f"{name}.cfg")
+    rec = []
+
+    def recorder(kind, t, local, glob, iters):
+        if kind in ("initial", "macro"):
+            rec.append((t, local.values.copy(), glob.values.copy(), local.mesh.box.lo))
+
+    state, stats = P.two_level_run(cfg, recorder=recorder)
+    assert stats.counters == json.loads(str(z["counters"]))
+    TL = cfg.material.T_liquidus
+    s = int(z["stride"])
+    assert len(rec) == len(z["t"])
+    for k, (t, Tl_, Tg, lo) in enumerate(rec):
+        assert t == z["t"][k]
+        np.testing.assert_array_equal(lo, z["box"][k])
+        assert rel(Tg[::s], z["gsub"][k]) <= REL and rel(Tl_[::s], z["lsub"][k]) <= REL
+        np.testing.assert_array_equal(np.packbits(Tg > TL), z["gmelt"][k])
+        np.testing.assert_array_equal(np.packbits(Tl_ > TL), z["lmelt"][k])
+        if k in z["full_at"]:
+            assert rel(Tg, z[f"g{k}"]) <= REL and rel(Tl_, z[f"l{k}"]) <= REL

@@ -244,6 +244,56 @@ def test_oracle_picard_step_vs_reference(name):
     assert np.abs(x - z["sol"]).max() / np.abs(z["sol"]).max() <= 1e-12
 
 
+@pytest.mark.parametrize("name", ["tables", "full"])
+def test_oracle_2d_picard_step_vs_reference(name):
+    """2D (P1 triangles): the 5-point stencil restatement
+    (oracle/tri2d.py) against the reference's fem.step_backward_euler on the shipped 2D plate
+    (IN625 tables, convection / lagged radiation on the top edge, 2D Gaussian beam)."""
+    from oracle import tri2d
+    z = np.load(GOLDEN / f"picard2d_{name}.npz")
+    G = tri2d.Grid2D(z["lo"], z["hi"], np.round((z["hi"] - z["lo"]) / z["h"]).astype(int))
+    mat = picard_material(z)
+    pw, eta, r, d = (float(v) for v in z["beam"])
+    src = lambda p: tri2d.gaussian2d((pw * eta, r, d, z["center"]), p)      # noqa: E731
+    rad = bool(z["radiation"])
+    robin = (float(z["h_conv"]), 5.670374419e-8 * 0.8 if rad else 0.0, 298.15)
+    dmask = np.zeros(G.n_nodes, dtype=bool)
+    dmask[:G.NX] = True                                  # bottom edge y = lo
+    g = np.full(G.n_nodes, 298.15)
+    x, npic, cg = tri2d.step(G, mat, z["T_old"], float(z["dt"]), src, dmask, g, bool(z["latent"]), robin)
+    assert npic == int(z["picard"])
+    assert cg == list(z["cg_iters"])
+    assert np.abs(x - z["sol"]).max() / np.abs(z["sol"]).max() <= 1e-12
+    assert np.sqrt(tri2d.mass_norm2(G, x)) == pytest.approx(float(z["l2"]), rel=1e-12)
+
+
+def test_oracle_2d_interpolation_vs_reference():
+    """Mesh.interpolate on the triangle lattice, incl. lattice nodes and cell diagonals."""
+    from oracle import tri2d
+    z = np.load(GOLDEN / "interp2d.npz")
+    G = tri2d.Grid2D(z["lo"], z["hi"], np.round((z["hi"] - z["lo"]) / z["h"]).astype(int))
+    got = tri2d.interpolate(G, z["values"], z["points"])
+    assert np.abs(got - z["out"]).max() <= 1e-13 * np.abs(z["out"]).max()
+    assert np.sqrt(tri2d.mass_norm2(G, z["values"])) == pytest.approx(float(z["l2"]), rel=1e-13)
+
+
+def test_structured_grid_2d_matches_reference_layout():
+    """StructuredGrid in 2D: node order, boundary tags with y vertical (mesh.py:206-209), the
+    interface node set and the two triangles per cell of the reference's mesh."""
+    g = P.build_structured_grid(P.Box((0.0, 0.0), (5e-3, 1e-3)), 6.25e-5)
+    assert (g.dim, g.n_nodes, g.n_elems) == (2, 81 * 17, 2 * 80 * 16)
+    from paper_2110_12932_b200.grid import BOTTOM, LATERAL, TOP
+    np.testing.assert_array_equal(g.nodes_on(BOTTOM), np.arange(81))
+    np.testing.assert_array_equal(g.nodes_on(TOP), 16 * 81 + np.arange(81))
+    np.testing.assert_array_equal(g.nodes_on(LATERAL), np.sort(np.r_[81 * np.arange(17), 81 * np.arange(17) + 80]))
+    assert g.gamma_mask().sum() == 81 + 2 * 16
+    np.testing.assert_array_equal(g.elems[:4], [[0, 1, 82], [0, 82, 81], [1, 2, 83], [1, 83, 82]])
+    z = np.load(GOLDEN / "interp2d.npz")
+    assert g.coords.shape == (81 * 17, 2) and g.coords[82].tolist() == [6.25e-5, 6.25e-5]
+    d = g.desc()
+    assert list(d.ncells) == [80, 16, 0]
+
+
 def test_interface_measure_3d():
     """tests/test_mesh.py:185-189: lateral + bottom facet area of the interface."""
     from paper_2110_12932_b200.twolevel import extract_interface
