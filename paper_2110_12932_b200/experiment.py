@@ -140,6 +140,23 @@ def _two_level_run(cfg, spacetime: bool, dt_macro=None, micro=None):
     return log, stats, state
 
 
+def _t_star_fn(cfg, log: RunLog):
+    """``runner._t_star_fn`` (``runner.py:166-178``): the 2D studies' control-line temperature
+    of a record, sampled from the fine field where it covers and the coarse one elsewhere."""
+    if cfg.dimension != 2 or cfg.control_line_y is None:
+        return None
+    from .metrics import control_temperature
+    gb = convert_config(cfg)["global_box"]
+    x0, x1 = gb.lo[0], gb.hi[0]
+    dx = cfg.h_global / 2
+
+    def t_star(record):
+        glob = record.global_field or log.latest_global_at(record.time)
+        return control_temperature(composite_sampler(record.local, glob), cfg.control_line_y, (x0, x1), dx)
+
+    return t_star
+
+
 def _centerline(cfg, sample, out: Path, dx: float):
     y, z = cfg.centerline_y, cfg.centerline_z
     if y is None:
@@ -233,7 +250,7 @@ def run_study(cfg, out: Path, snapshots=None, threads: int = 1) -> RunArtifacts:
     matrix_rows, reports = [], {}
     for dt, micro in pairs:
         log, run_stats, _ = _two_level_run(cfg, True, dt_macro=dt, micro=micro)
-        report = error_metrics(log, reference)
+        report = error_metrics(log, reference, t_star_of=_t_star_fn(cfg, log))
         sub = out / f"dt_{dt:g}" / f"micro_{dt / micro:g}"
         sub.mkdir(parents=True, exist_ok=True)
         _write_errors_csv(sub, report)

@@ -566,6 +566,42 @@ def experiments_case():
     print("experiments:", {k: v["summary"] for k, v in out.items() if k != "versions"})
 
 
+def experiments2d_case():
+    """runner.run_experiment on the reference's shipped 2D configs (configs/oracle2d.cfg,
+    configs/study2d.cfg restate them) with its own IN625 file: summaries, study matrix,
+    errors.csv incl. the control-line temperature T_star; the tables go into the json."""
+    import csv as _csv
+    import shutil
+    import tempfile
+    out = {}
+    for name in ("oracle2d", "study2d"):
+        tmp = Path(tempfile.mkdtemp())
+        shutil.copy(CFG / f"{name}.cfg", tmp / f"{name}.cfg")
+        shutil.copy(REF / "lpbfsim" / "data" / "in625.mat", tmp / "in625.mat")
+        cfg = load_config(tmp / f"{name}.cfg")
+        res = tmp / "out"
+        t0 = time.perf_counter()
+        art = runner.run_experiment(cfg, res)
+        wall = time.perf_counter() - t0
+        files = sorted(str(p.relative_to(res)) for p in res.rglob("*") if p.is_file())
+        errs = {}
+        for f in files:
+            if f.endswith("errors.csv") or f.endswith("study_matrix.csv"):
+                with (res / f).open() as fh:
+                    errs[f] = list(_csv.reader(fh))
+        summ = {k: v for k, v in art.summary.items()
+                if not k.startswith("seconds") and "wall" not in k and k not in ("total_seconds", "speedup")}
+        mat = cfg.material
+        out[name] = {"files": files, "csv": errs, "summary": summ, "reference_wall_s": wall,
+                     "k_table": np.asarray(mat.conductivity_table).tolist(),
+                     "c_table": np.asarray(mat.heat_capacity_table).tolist(),
+                     "mat_scalars": [mat.rho, mat.chi, mat.T_solidus, mat.T_liquidus, mat.S]}
+        shutil.rmtree(tmp)
+        print(f"experiment {name}: {wall:.1f}s {summ}")
+    out["versions"] = VERS
+    (OUT / "experiments2d.json").write_text(json.dumps(out, indent=1))
+
+
 def consistency_case():
     """twolevel.consistency_diagnostic of the state after 2 macro steps of cfg1_m4 against
     run_reference at h = 25 um (the final frame)."""
@@ -636,7 +672,10 @@ def main():
         interp2d_case()
         run2d_case("run2d", {1, 2, 3}, 3)
         run2d_case("run2d_uniform", {1, 5}, 3)
+        experiments2d_case()
         return
+    if "--2d-experiments" in sys.argv:
+        return experiments2d_case()
     if "--vtk" in sys.argv:
         return vtk_case()
     if "--piecewise" in sys.argv:

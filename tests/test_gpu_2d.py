@@ -117,3 +117,44 @@ def test_2d_two_level_run_vs_reference(name, tmp_path):
         np.testing.assert_array_equal(np.packbits(Tl_ > TL), z["lmelt"][k])
         if k in z["full_at"]:
             assert rel(Tg, z[f"g{k}"]) <= REL and rel(Tl_, z[f"l{k}"]) <= REL
+
+
+@pytest.mark.parametrize("name", ["oracle2d", "study2d"])
+def test_2d_shipped_experiments_vs_reference(name, tmp_path):
+    """runner.run_experiment on the reference's shipped 2D configs (oracle_2d.cfg: the
+    coupled pair reproduces the monolithic solve; study_2d.cfg: coarse-step sweep against
+    the monolithic reference): the same output files, solve counts, study pairs and
+    errors.csv / study_matrix rows (relative L2 errors and the control-line temperature
+    T_star) as the reference.  Relative L2 errors are differences of two solutions: they are
+    compared to 1e-7 relative plus 2e-9 absolute (oracle2d's are ~3e-10, the solver noise)."""
+    import csv
+    from paper_2110_12932_b200.experiment import run_experiment
+    gold = json.loads((GOLDEN / "experiments2d.json").read_text())[name]
+    z = {"mat_scalars": gold["mat_scalars"], "k_table": gold["k_table"], "c_table": gold["c_table"]}
+    _write_material(z, tmp_path / "in625.mat")
+    (tmp_path / f"{name}.cfg").write_text((CONFIGS / f"{name}.cfg").read_text())
+    out = tmp_path / "out"
+    art = run_experiment(P.load_config(tmp_path / f"{name}.cfg"), out)
+    files = sorted(str(p.relative_to(out)) for p in out.rglob("*") if p.is_file())
+    assert files == gold["files"]
+    for k, v in gold["summary"].items():
+        if k == "mean_rel_l2":
+            for kk, vv in v.items():
+                assert abs(art.summary[k][kk] - vv) <= 1e-7 * vv + 2e-9
+        elif k == "pairs":
+            np.testing.assert_allclose(art.summary[k], v, rtol=1e-15)
+        else:
+            assert art.summary[k] == v, k
+    for f, rows in gold["csv"].items():
+        with (out / f).open() as fh:
+            got = list(csv.reader(fh))
+        assert got[0] == rows[0] and len(got) == len(rows)
+        for a, b in zip(got[1:], rows[1:]):
+            for col, (x, y) in enumerate(zip(a, b)):
+                try:
+                    fx, fy = float(x), float(y)
+                except ValueError:
+                    assert x == y
+                    continue
+                slack = 2e-9 if "rel_l2" in got[0][col] or "mean" in got[0][col] else 1e-12
+                assert abs(fx - fy) <= 1e-7 * abs(fy) + slack, (f, got[0][col], a, b)
