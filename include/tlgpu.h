@@ -130,7 +130,11 @@ typedef struct {
     int32_t n_micro;                /* local solves that advance time      */
     int32_t corrector;              /* 1: re-solve the last micro interval (multirate.py:149) */
     int32_t relocate;               /* 1: local box moves after this step  */
-    int32_t record;                 /* 1: keep predictor + micro fields as snapshots */
+    int32_t record;                 /* 0: no snapshots; 1: keep the predictor + every micro field;
+                                       > 1 (bit 0 set): snapshot decimation (runner.py:216-233) -
+                                       micro field i is kept only if bit i + 1 is set (i >= 30:
+                                       always); the predictor and the step's final local field
+                                       are kept whenever record != 0 */
     double new_offset[3];           /* local offset after the move          */
 } tl_macro_plan;
 

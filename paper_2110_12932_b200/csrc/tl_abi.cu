@@ -1663,6 +1663,13 @@ static int local_solve(tl_run* R, double* T, const tl_micro_plan& mp, int boxed 
     return timed_end(R);
 }
 
+// Snapshot decimation (tl_macro_plan::record): 1 keeps every micro field; a larger value
+// keeps micro field i only if bit i + 1 is set (indices >= 30 are always kept).  The
+// predicted global field and the step's final local field are kept whenever record != 0.
+static inline bool keep_micro(int record, int i) {
+    return record == 1 || i >= 30 || ((record >> (i + 1)) & 1);
+}
+
 // All micro solves of one macro step (+ the corrector) as one k_pcg_resident_cg launch.
 static int local_multi(tl_run* R, const tl_macro_plan& mp, const tl_micro_plan* micro,
                        const BrickPlan& bp) {
@@ -1709,7 +1716,7 @@ static int local_multi(tl_run* R, const tl_macro_plan& mp, const tl_micro_plan* 
         sp.snap = nullptr;
         if (mp.record) {
             if (int rc = ensure_snapshots(R, ns)) return rc;
-            sp.snap = R->snap_l[e];
+            if (e == ns - 1 || keep_micro(mp.record, e)) sp.snap = R->snap_l[e];
         }
     }
     TL_CUDA(cudaMemcpyAsync(R->d_specs + 1, R->h_specs.data(), sizeof(tl::SolveSpec) * ns,
@@ -1830,7 +1837,7 @@ int32_t tl_run_macro_steps(tl_run* R, const tl_macro_plan* plans, int32_t nsteps
                 ++R->launches;
             }
             if (int rc = local_solve(R, R->Tl, up, boxed ? i : -1)) return rc;
-            if (mp.record)
+            if (mp.record && ((i == mp.n_micro - 1 && !mp.corrector) || keep_micro(mp.record, i)))
                 TL_CUDA(cudaMemcpyAsync(R->snap_l[i], R->Tl, sizeof(double) * R->L.n, cudaMemcpyDeviceToDevice, R->stream));
         }
         if (mp.corrector && !multi) {

@@ -65,10 +65,13 @@ def _cadence(cfg, override):
 
 def write_vtk(path, mesh, point_data: dict | None = None, title: str = "lpbfsim"):
     """``vtkio.write_vtk`` (``vtkio.py:15-44``): legacy ASCII unstructured grid of the Kuhn
-    tets with nodal scalars."""
+    tets (3D) or the triangles (2D, z = 0) with nodal scalars."""
     path = Path(path)
     path.parent.mkdir(parents=True, exist_ok=True)
     pts = mesh.coords
+    if mesh.dim == 2:
+        pts = np.column_stack([pts, np.zeros(len(pts))])
+    nv = mesh.dim + 1
     elems = mesh.elems
     ne = len(elems)
     with path.open("w") as f:
@@ -79,11 +82,11 @@ def write_vtk(path, mesh, point_data: dict | None = None, title: str = "lpbfsim"
         f.write(f"POINTS {mesh.n_nodes} double\n")
         for p in pts:
             f.write(f"{p[0]:.10g} {p[1]:.10g} {p[2]:.10g}\n")
-        f.write(f"\nCELLS {ne} {ne * 5}\n")
+        f.write(f"\nCELLS {ne} {ne * (nv + 1)}\n")
         for e in elems:
-            f.write("4 " + " ".join(str(int(v)) for v in e) + "\n")
+            f.write(f"{nv} " + " ".join(str(int(v)) for v in e) + "\n")
         f.write(f"\nCELL_TYPES {ne}\n")
-        f.write("10\n" * ne)
+        f.write(("5\n" if mesh.dim == 2 else "10\n") * ne)
         if point_data:
             f.write(f"\nPOINT_DATA {mesh.n_nodes}\n")
             for name, values in point_data.items():
@@ -97,7 +100,7 @@ def _write_snapshots(out: Path, cfg, log: RunLog, cadence: str):
     """``runner._write_snapshots`` (``runner.py:216-233``)."""
     if cadence == "none":
         return
-    every = 10 if cadence == "all" else 1
+    every = 10 if cfg.dimension == 3 and cadence == "all" else 1
     micro_seen = 0
     for r in log.records:
         if r.kind in ("initial", "macro"):
@@ -106,9 +109,9 @@ def _write_snapshots(out: Path, cfg, log: RunLog, cadence: str):
                           {"temperature": r.global_field.values})
             if r.local is not None:
                 write_vtk(out / "vtk" / f"local_{r.time:.6e}.vtk", r.local.mesh, {"temperature": r.local.values})
-        elif r.kind == "micro" and cadence == "all" and r.local is not None:
-            micro_seen += 1
-            if micro_seen % every == 0:
+        elif r.kind == "micro" and cadence == "all":
+            micro_seen += 1                 # decimated records (local None) count too
+            if micro_seen % every == 0 and r.local is not None:
                 write_vtk(out / "vtk" / f"local_{r.time:.6e}.vtk", r.local.mesh, {"temperature": r.local.values})
 
 
@@ -132,11 +135,42 @@ def _write_timing_csv(out: Path, stats: RunStats):
     write_csv(out / "timing.csv", ["phase", "seconds", "count"], rows)
 
 
-def _two_level_run(cfg, spacetime: bool, dt_macro=None, micro=None):
-    """``runner._two_level_run`` (``runner.py:236-257``): (log, stats, state)."""
+class DecimatingRecorder:
+    """Recorder for the experiment modes that reads only the micro fields its outputs need
+    (snapshot decimation on the device, ``runner.py:216-233``): ``micro_every`` = 1 every
+    micro field (error metrics), k > 1 every k-th one (VTK cadence "all" in 3D), 0 none
+    (cadences "macro" / "none").  The drivers ask ``wants`` once per micro record, in order;
+    records whose field is not wanted arrive with ``local=None`` and are logged as such."""
+
+    def __init__(self, log: RunLog, micro_every: int = 1):
+        self.log = log
+        self.micro_every = int(micro_every)
+        self._seen = 0
+
+    def wants(self, kind: str, time: float) -> bool:
+        if kind != "micro":
+            return True
+        self._seen += 1
+        return self.micro_every > 0 and self._seen % self.micro_every == 0
+
+    def __call__(self, kind, time, local, global_field, iterations):
+        self.log.record(kind, time, local, global_field, iterations)
+
+
+def _micro_every(cfg, cadence: str) -> int:
+    """Which micro fields ``_write_snapshots`` reads for a cadence (``runner.py:219-233``)."""
+    if cadence != "all":
+        return 0
+    return 10 if cfg.dimension == 3 else 1
+
+
+def _two_level_run(cfg, spacetime: bool, dt_macro=None, micro=None, micro_every: int = 1):
+    """``runner._two_level_run`` (``runner.py:236-257``): (log, stats, state).  ``micro_every``:
+    the micro fields the caller will read (DecimatingRecorder)."""
     from .runner import two_level_run
     log = RunLog()
-    state, stats = two_level_run(cfg, spacetime=spacetime, dt_macro=dt_macro, micro=micro, recorder=log.record)
+    rec = log.record if micro_every == 1 else DecimatingRecorder(log, micro_every)
+    state, stats = two_level_run(cfg, spacetime=spacetime, dt_macro=dt_macro, micro=micro, recorder=rec)
     return log, stats, state
 
 
@@ -194,7 +228,7 @@ def _run_reference_mode(cfg, out: Path, snapshots=None) -> RunArtifacts:
     def observer(state):
         count[0] += 1
         rows.append((state.time, "macro", 0.0, ""))
-        if cadence == "all" and count[0] % 10 == 0:
+        if cadence == "all" and count[0] % (1 if cfg.dimension == 2 else 10) == 0:
             write_vtk(out / "vtk" / f"reference_{state.time:.6e}.vtk", mesh, {"temperature": state.values})
 
     traj = run_reference(cfg, stats=stats, mesh=mesh, observer=observer)
@@ -212,7 +246,8 @@ def _run_reference_mode(cfg, out: Path, snapshots=None) -> RunArtifacts:
 
 def _run_two_level_mode(cfg, out: Path, spacetime: bool, snapshots=None) -> RunArtifacts:
     """``runner.py:318-339``."""
-    log, stats, state = _two_level_run(cfg, spacetime)
+    cadence = _cadence(cfg, snapshots)
+    log, stats, state = _two_level_run(cfg, spacetime, micro_every=_micro_every(cfg, cadence))
     rows = [(r.time, r.kind, "", "") for r in log.of_kind("initial", "micro", "macro")]
     write_csv(out / "errors.csv", ["t", "step_kind", "rel_l2_local", "T_star"], rows)
     _write_timing_csv(out, stats)
@@ -269,11 +304,11 @@ def run_study(cfg, out: Path, snapshots=None, threads: int = 1) -> RunArtifacts:
 def run_compare(cfg, out: Path, snapshots=None) -> RunArtifacts:
     """Multirate against uniform-step two-level timing (``runner.py:406-440``)."""
     out = Path(out)
-    log_st, stats_st, _ = _two_level_run(cfg, True)
+    log_st, stats_st, _ = _two_level_run(cfg, True, micro_every=_micro_every(cfg, _cadence(cfg, snapshots)))
     wall_st = stats_st.total_seconds
     _write_timing_csv(out / "spacetime", stats_st)
     _write_snapshots(out / "spacetime", cfg, log_st, _cadence(cfg, snapshots))
-    log_sp, stats_sp, _ = _two_level_run(cfg, False)
+    log_sp, stats_sp, _ = _two_level_run(cfg, False, micro_every=0)
     wall_sp = stats_sp.total_seconds
     _write_timing_csv(out / "spaceonly", stats_sp)
     summary = {

@@ -154,6 +154,7 @@ class DeviceRun:
     def snapshot(self, which: int, index: int = 0) -> np.ndarray:
         n = self.n_global if which == 0 else self.n_local
         out = np.empty(n)
+        self.d2h_bytes += out.nbytes
         N.check(N.lib().tl_run_get_snapshot(self._h, which, index, N.dptr(out), n), "snapshot")
         return out
 
@@ -343,12 +344,15 @@ def _drive(problem, run: DeviceRun, plan_fn, local_mesh, T0, stats, recorder, t_
             pending = None
         if plan.n_steps == 0:
             break
+        keep = None
+        if recorder is not None:
+            keep = _decimate(plan, recorder)
         run.run(plan)
         if recorder is not None:
             infos = run.take_info()
             run.check_solves(infos)
             _merge_counters(stats, plan.counters)
-            _deliver(run, problem, plan, infos, recorder)
+            _deliver(run, problem, plan, infos, recorder, keep)
         else:
             pending = plan
         placement, tg, tl = plan.final_placement, plan.final_t_global, plan.final_t_local
@@ -366,7 +370,29 @@ def _drive(problem, run: DeviceRun, plan_fn, local_mesh, T0, stats, recorder, t_
     return TwoLevelState(gfield, FieldState(final_local, lv, tl), gamma, trace), last_plan
 
 
-def _deliver(run: DeviceRun, problem, plan: Plan, infos, recorder):
+def _decimate(plan: Plan, recorder):
+    """Snapshot decimation (``runner.py:216-233``: the experiment modes write every 10th micro
+    field, or none): a recorder with a ``wants(kind, time) -> bool`` method is asked once per
+    micro record, in order, whether it will read that record's field; the answers go to the
+    device as the macro plan's ``record`` mask (fields nobody reads are neither snapshotted
+    on the device nor copied to the host; their records arrive with ``local=None``).
+    Returns the answers, or None for a plain recorder (every field delivered)."""
+    wants = getattr(recorder, "wants", None)
+    if wants is None or plan.mode != "spacetime":
+        return None
+    keep = [bool(wants("micro", ti)) for ti in plan.micro_times[0]]
+    mask = 1
+    for i, k in enumerate(keep):
+        if k or i >= 30:
+            mask |= 1 << (i + 1)
+            keep[i] = True
+    if all(keep):
+        mask = 1
+    plan.macro["record"][0] = mask
+    return keep
+
+
+def _deliver(run: DeviceRun, problem, plan: Plan, infos, recorder, keep=None):
     """Replay the recorder calls of one macro step from the device snapshots."""
     gmesh = problem.global_mesh
     mp = plan.macro[0]
@@ -377,6 +403,9 @@ def _deliver(run: DeviceRun, problem, plan: Plan, infos, recorder):
     if spacetime:
         recorder("predictor", t_next, None, FieldState(gmesh, gpred, plan.t_global[0]), 0)
         for i, ti in enumerate(plan.micro_times[0]):
+            if keep is not None and not keep[i]:
+                recorder("micro", ti, None, None, 0)          # decimated: nobody reads this field
+                continue
             recorder("micro", ti, FieldState(local_mesh, run.snapshot(1, i), ti), None, 0)
     n = int(mp["n_micro"]) - 1 + int(mp["corrector"])
     lfinal = run.snapshot(1, n)

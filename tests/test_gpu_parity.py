@@ -872,3 +872,44 @@ def test_two_level_mode_writes_macro_snapshots(tmp_path):
     last = art.log.of_kind("macro")[-1]
     vals = (tmp_path / "out" / "vtk" / f"local_{5e-5:.6e}.vtk").read_text().split("LOOKUP_TABLE default\n")[1].split()
     np.testing.assert_allclose(np.array(vals, dtype=float), last.local.values, rtol=1e-9)
+
+
+def test_snapshot_decimation_on_device():
+    """Snapshot decimation (runner.py:216-233): a recorder that declares
+    which micro fields it reads (DecimatingRecorder.wants) gets exactly those, the others
+    arrive with local=None and are neither snapshotted on the device nor copied to the host;
+    every record's kind and time, the macro fields and the final state are those of the
+    full recorder, bit for bit."""
+    from paper_2110_12932_b200 import multirate as MR
+    from paper_2110_12932_b200.experiment import DecimatingRecorder
+    from paper_2110_12932_b200.metrics import RunLog
+    cfg = P.load_config(CONFIGS / "cfg1_m4.cfg")
+
+    def run(every):
+        MR.release_device_runs()
+        log = RunLog()
+        rec = log.record if every is None else DecimatingRecorder(log, every)
+        state, _ = P.two_level_run(cfg, recorder=rec, n_steps=6)
+        d2h = sum(r.d2h_bytes for r in MR._POOL.values())
+        return log, state, d2h
+
+    full, sf, b_full = run(None)
+    for every in (0, 3):
+        log, s, b = run(every)
+        assert [(r.kind, r.time) for r in log.records] == [(r.kind, r.time) for r in full.records]
+        seen = 0
+        for a, r in zip(log.records, full.records):
+            if a.kind == "micro":
+                seen += 1
+                if every and seen % every == 0:
+                    np.testing.assert_array_equal(a.local.values, r.local.values)
+                else:
+                    assert a.local is None
+            elif a.kind in ("initial", "macro"):
+                np.testing.assert_array_equal(a.local.values, r.local.values)
+                np.testing.assert_array_equal(a.global_field.values, r.global_field.values)
+        np.testing.assert_array_equal(s.local_field.values, sf.local_field.values)
+        np.testing.assert_array_equal(s.global_field.values, sf.global_field.values)
+        assert b < b_full
+    n_l = full.records[0].local.mesh.n_nodes
+    assert b_full - run(0)[2] >= 6 * 4 * n_l * 8          # 4 micro fields per macro step not copied
