@@ -167,7 +167,10 @@ static cudaError_t launch_s_cg(tl::PcgParams& P, int Gr, int sms, cudaStream_t s
 // ---- z-marching CG loop on bulk copies (tl_tiled.cuh) --------------------------------
 // Default CG loop of the streaming solve; TLGPU_TILED=0 falls back to k_s_cg, and grids
 // below TLGPU_TILED_MIN nodes (default 1M) use k_s_cg too.  Item plan: tiled_plan_range.
-constexpr int kTNCW = 16;                      // consumer warps of k_t_cg
+// consumer warps of k_t_cg: 16 (+ producer = 17 warps) or 19 (20 warps), both at 96 registers;
+// the item planner picks per grid (more warps hide more latency, fewer leave less of a
+// half-empty second consumer slot on narrow planes)
+constexpr int kTNCWs[2] = {16, 19};
 static bool tiled_enabled() {
     static int v = -1;
     if (v < 0) {
@@ -227,29 +230,35 @@ static bool tiled_plan_range(const tl::Grid& g, int sms, int zlo, int zhi, tl::T
         return (std::max(2 * RA, RB + 2 * RX) + 15) & ~15;
     };
     auto stages_of = [&](int H) { return (int)std::min<size_t>(tl::kTMaxStages, cap / ((size_t)stage_of(H) * 8)); };
-    const int npt_max = NX <= 2 * kTNCW * 32 ? 2 : 4;
-    int Hmax = std::min(g.NY, npt_max * kTNCW * 32 / NX);
-    while (Hmax >= 1 && stages_of(Hmax) < 4) --Hmax;
-    if (Hmax < 1) return false;
     int zmin = 2;
     if (const char* e = getenv("TLGPU_TZ")) zmin = std::max(1, atoi(e));
-    int H = 0, nch = 0;
+    int want_ncw = 0;
+    if (const char* e = getenv("TLGPU_NCW")) want_ncw = atoi(e);
+    int H = 0, nch = 0, ncw = 0, Hmax = 0;
     double best = 1e300;
-    for (int h = 1; h <= Hmax; ++h) {
-        const int NB = (g.NY + h - 1) / h;
-        const int slots = (h * NX + kTNCW * 32 - 1) / (kTNCW * 32);
-        const double plane = std::max((double)slots * kTNCW * 32, (double)h * NX * (1.0 + 0.6 / h));
-        for (int c = 1; c <= std::min(nzr, tl::kTMaxChunks); ++c) {
-            const int Z = (nzr + c - 1) / c;
-            if (Z < zmin && c > 1) break;
-            const long long I = (long long)NB * c;
-            if (I > tl::kTMaxItems) break;
-            const long long waves = (I + sms - 1) / sms;
-            const double cost = (double)waves * (Z + 2.0) * plane;
-            if (cost < best * (1.0 - 1e-9)) { best = cost; H = h; nch = c; }
+    for (int w = 0; w < 2; ++w) {
+        const int nw = kTNCWs[w];
+        if (want_ncw && want_ncw != nw) continue;
+        const int npt_max = NX <= 2 * nw * 32 ? 2 : 4;
+        int hmax = std::min(g.NY, npt_max * nw * 32 / NX);
+        while (hmax >= 1 && stages_of(hmax) < 4) --hmax;
+        for (int h = 1; h <= hmax; ++h) {
+            const int NB = (g.NY + h - 1) / h;
+            const int slots = (h * NX + nw * 32 - 1) / (nw * 32);
+            const double plane = std::max((double)slots * nw * 32, (double)h * NX * (1.0 + 0.6 / h));
+            for (int c = 1; c <= std::min(nzr, tl::kTMaxChunks); ++c) {
+                const int Z = (nzr + c - 1) / c;
+                if (Z < zmin && c > 1) break;
+                const long long I = (long long)NB * c;
+                if (I > tl::kTMaxItems) break;
+                const long long waves = (I + sms - 1) / sms;
+                const double cost = (double)waves * (Z + 2.0) * plane;
+                if (cost < best * (1.0 - 1e-9)) { best = cost; H = h; nch = c; ncw = nw; Hmax = hmax; }
+            }
         }
     }
     if (H == 0) return false;
+    tp.ncw = ncw;
     if (const char* e = getenv("TLGPU_TH")) H = std::max(1, std::min(atoi(e), Hmax));
     if (const char* e = getenv("TLGPU_TC")) nch = std::max(1, std::min(atoi(e), std::min(nzr, tl::kTMaxChunks)));
     tp.H = H;
@@ -270,8 +279,9 @@ static bool tiled_plan_range(const tl::Grid& g, int sms, int zlo, int zhi, tl::T
     tp.snake = snake_enabled();
     smem = (size_t)tp.NS * tp.stage * 8;
     if (getenv("TLGPU_VERBOSE"))
-        fprintf(stderr, "[tlgpu] item plan %dx%dx[%d,%d): H=%d NB=%d C=%d I=%d (%.2f per CTA) NS=%d stage=%d B snake=%d\n",
-                g.NX, g.NY, zlo, zhi, tp.H, tp.NB, tp.C, tp.I, (double)tp.I / sms, tp.NS, tp.stage * 8, tp.snake);
+        fprintf(stderr, "[tlgpu] item plan %dx%dx[%d,%d): H=%d NB=%d C=%d I=%d (%.2f per CTA) NS=%d stage=%d B snake=%d "
+                "consumer warps=%d\n",
+                g.NX, g.NY, zlo, zhi, tp.H, tp.NB, tp.C, tp.I, (double)tp.I / sms, tp.NS, tp.stage * 8, tp.snake, tp.ncw);
     return true;
 }
 
@@ -280,9 +290,9 @@ static unsigned long long* prof_buffer();
 static cudaError_t launch_t_cg(tl::PcgParams& P, int Gr, int sms, cudaStream_t st, bool& launched,
                                const tl::TPlan& tp, size_t smem) {
     launched = false;
-    const int ncw = kTNCW;
-    const bool two = tp.H * P.g.NX <= 2 * kTNCW * 32;
-    auto kern = two ? tl::k_t_cg<kTNCW, 2> : tl::k_t_cg<kTNCW, 4>;
+    const int ncw = tp.ncw;
+    const bool two = tp.H * P.g.NX <= 2 * ncw * 32;
+    auto kern = ncw == 16 ? (two ? tl::k_t_cg<16, 2> : tl::k_t_cg<16, 4>) : (two ? tl::k_t_cg<19, 2> : tl::k_t_cg<19, 4>);
     cudaError_t e = ensure_smem_attr((const void*)kern, smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
@@ -2175,7 +2185,7 @@ static cudaError_t launch_sd_tiled(K kern, const tl::SlabDev& D, const tl::TPlan
                                    cudaStream_t st) {
     cudaError_t e = ensure_smem_attr((const void*)kern, smem);
     if (e != cudaSuccess) return e;
-    kern<<<sms, (kTNCW + 1) * 32, smem, st>>>(D, tp);
+    kern<<<sms, (tp.ncw + 1) * 32, smem, st>>>(D, tp);
     return cudaGetLastError();
 }
 extern "C" {
@@ -2191,9 +2201,11 @@ int32_t tl_slab_direction(const tl_slab* s) {
     tl::TPlan tp{};
     size_t smem = 0;
     if (!tiled_plan_range(D.S.g, sms, s->k0, s->k1, tp, smem)) return fail(TL_E_INVALID, "no item plan for the slab");
-    const bool two = tp.H * D.S.g.NX <= 2 * kTNCW * 32;
-    cudaError_t e = two ? launch_sd_tiled(tl::k_sd_dir<kTNCW, 2>, D, tp, smem, sms, st)
-                        : launch_sd_tiled(tl::k_sd_dir<kTNCW, 4>, D, tp, smem, sms, st);
+    const bool two = tp.H * D.S.g.NX <= 2 * tp.ncw * 32;
+    cudaError_t e = tp.ncw == 16 ? (two ? launch_sd_tiled(tl::k_sd_dir<16, 2>, D, tp, smem, sms, st)
+                                        : launch_sd_tiled(tl::k_sd_dir<16, 4>, D, tp, smem, sms, st))
+                                 : (two ? launch_sd_tiled(tl::k_sd_dir<19, 2>, D, tp, smem, sms, st)
+                                        : launch_sd_tiled(tl::k_sd_dir<19, 4>, D, tp, smem, sms, st));
     if (e != cudaSuccess) return fail(TL_E_CUDA, std::string("slab direction: ") + cudaGetErrorString(e));
     return TL_OK;
 }
@@ -2226,9 +2238,12 @@ int32_t tl_slab_update(const tl_slab* s, int32_t part) {
     } else {
         tp.I = 0;                          // nothing beyond the boundary planes: sum their partials
     }
-    const bool two = tp.I == 0 || tp.H * D.S.g.NX <= 2 * kTNCW * 32;
-    cudaError_t e = two ? launch_sd_tiled(tl::k_sd_upd<kTNCW, 2>, D, tp, smem, sms, st)
-                        : launch_sd_tiled(tl::k_sd_upd<kTNCW, 4>, D, tp, smem, sms, st);
+    if (tp.I == 0) tp.ncw = 16;
+    const bool two = tp.I == 0 || tp.H * D.S.g.NX <= 2 * tp.ncw * 32;
+    cudaError_t e = tp.ncw == 16 ? (two ? launch_sd_tiled(tl::k_sd_upd<16, 2>, D, tp, smem, sms, st)
+                                        : launch_sd_tiled(tl::k_sd_upd<16, 4>, D, tp, smem, sms, st))
+                                 : (two ? launch_sd_tiled(tl::k_sd_upd<19, 2>, D, tp, smem, sms, st)
+                                        : launch_sd_tiled(tl::k_sd_upd<19, 4>, D, tp, smem, sms, st));
     if (e != cudaSuccess) return fail(TL_E_CUDA, std::string("slab update: ") + cudaGetErrorString(e));
     return TL_OK;
 }

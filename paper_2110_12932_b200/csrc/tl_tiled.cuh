@@ -54,6 +54,7 @@ struct TPlan {
     int RA;         // sweep A: r at [0, RA), p_old at [RA, 2 RA)
     int RB, RX;     // sweep B: p at [0, RB), x at [RB, RB + RX), r at [RB + RX, RB + 2 RX)
     FastDiv nsd, nbd;       // division by NS, NB
+    int ncw;        // consumer warps of the kernel instance this plan is for (host side)
     int snake;      // 1: sweep B takes the items from the top of the grid down (L2 reuse, below)
     unsigned long long* prof;    // TLGPU_PROF=1: %globaltimer stamps of iteration 3, slot 1024 + 16 CTA + e
     short kb[kTMaxChunks + 1];   // chunk kc = planes [kb[kc], kb[kc + 1])

@@ -53,6 +53,11 @@ class Scenario:
     def config(self, base_dir=None) -> ExperimentConfig:
         """The scenario as an ExperimentConfig (config-2 geometry, reference .cfg format)."""
         base = Path(base_dir) if base_dir is not None else Path(__file__).resolve().parent.parent / "configs"
+        return config_from_text(self.config_text(base), base, f"cfg5_{self.index}")
+
+    def config_text(self, base_dir=None) -> str:
+        """The scenario's .cfg text (readable by the reference's own ``load_config`` too)."""
+        base = Path(base_dir) if base_dir is not None else Path(__file__).resolve().parent.parent / "configs"
         text = (base / "cfg2.cfg").read_text()
         y0 = 1.5 - 2 * self.hatch * 1e3
         repl = {
@@ -68,7 +73,7 @@ class Scenario:
         for a, b in repl.items():
             assert a in text, a
             text = text.replace(a, b)
-        return config_from_text(text, base, f"cfg5_{self.index}")
+        return text
 
 
 def draw(seed: int = 0, n: int = 64) -> list[Scenario]:
