@@ -279,6 +279,18 @@ int32_t tl_run_set_global(tl_run* run, const double* Tg_host, int64_t n);
 int32_t tl_run_macro_steps(tl_run* run, const tl_macro_plan* plans, int32_t nsteps,
                            const tl_micro_plan* micro, int32_t nmicro,
                            const double* dep_points, const double* dep_power, int32_t ndep);
+/* Batched runs (BASELINE config 5; runner.py:376-380 is the reference's concurrency point):
+ * ONE macro step of `nruns` (<= 64) runs on one device whose local grids have one shape.
+ * plans[r] is run r's macro plan (record must be 0), micro[r] / nmicro[r] its micro plans,
+ * dep_*[r] / ndep[r] its deposit samples.  The global parts run per run; the i-th micro
+ * solve (and the corrector) of all runs is one batched streaming solve, the systems
+ * advancing in lockstep with their own scalars, stop tests and iteration counts.  Enqueued
+ * on runs[0]'s stream; the other runs' streams are ordered around it.  Outcomes go to each
+ * run's info log as usual. */
+int32_t tl_runs_macro_step(tl_run** runs, int32_t nruns, const tl_macro_plan* plans,
+                           const tl_micro_plan* const* micro, const int32_t* nmicro,
+                           const double* const* dep_points, const double* const* dep_power,
+                           const int32_t* ndep);
 /* Snapshots kept by the last macro step with plan.record = 1:
  * which 0 = predicted global field, 1 = local field after micro step `index`
  * (index == n_micro: corrector result). */

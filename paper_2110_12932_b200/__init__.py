@@ -26,7 +26,7 @@ from .fem import (  # noqa: F401
     BoundarySpec, FieldState, GaussianSource, Trajectory, solve_monolithic, step_backward_euler, uniform_field,
 )
 from .grid import BOTTOM, LATERAL, TOP, StructuredGrid, build_structured_grid  # noqa: F401
-from .multirate import DeviceRun, macro_step, run_space, run_spacetime  # noqa: F401
+from .multirate import BatchedRuns, DeviceRun, macro_step, run_space, run_spacetime  # noqa: F401
 from .runner import build_problem, reference_bounds, run_reference, two_level_run, two_level_run_slabs  # noqa: F401
 from . import experiment, metrics  # noqa: F401
 from .experiment import RunArtifacts, run_compare, run_experiment, run_study  # noqa: F401

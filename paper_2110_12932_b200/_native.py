@@ -140,6 +140,7 @@ SIGNATURES = [
     ("tl_run_initial", C.c_int32, [_P, C.c_double]),
     ("tl_run_set_global", C.c_int32, [_P, _dp, C.c_int64]),
     ("tl_run_macro_steps", C.c_int32, [_P, _P, C.c_int32, _P, C.c_int32, _dp, _dp, C.c_int32]),
+    ("tl_runs_macro_step", C.c_int32, [_P, C.c_int32, _P, _P, _P, _P, _P, _P]),
     ("tl_run_get_snapshot", C.c_int32, [_P, C.c_int32, C.c_int32, _dp, C.c_int64]),
     ("tl_run_sync", C.c_int32, [_P]),
     ("tl_run_get_field", C.c_int32, [_P, C.c_int32, _dp, C.c_int64]),

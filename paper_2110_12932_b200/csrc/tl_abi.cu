@@ -1646,9 +1646,9 @@ static int stream_gauss_loads(tl_run* R, const tl_macro_plan& mp, const tl_micro
     return TL_OK;
 }
 
-// boxed >= 0: this solve's Gaussian load was precomputed as entry `boxed` of stream_gauss_loads.
-static int local_solve(tl_run* R, double* T, const tl_micro_plan& mp, int boxed = -1) {
-    tl::PcgParams P{};
+// Parameters of one local solve from T; boxed >= 0: its Gaussian load was precomputed as
+// entry `boxed` of stream_gauss_loads.  Returns whether an in-kernel Gaussian is still needed.
+static bool local_params(tl_run* R, double* T, const tl_micro_plan& mp, int boxed, tl::PcgParams& P) {
     base_params(R, P, true, mp.dt);
     P.T = T;
     P.gA = R->tr_old;
@@ -1667,6 +1667,12 @@ static int local_solve(tl_run* R, double* T, const tl_micro_plan& mp, int boxed 
         P.src.on = 1;
     }
     P.info = R->info + R->info_n++;
+    return gauss;
+}
+
+static int local_solve(tl_run* R, double* T, const tl_micro_plan& mp, int boxed = -1) {
+    tl::PcgParams P{};
+    const bool gauss = local_params(R, T, mp, boxed, P);
     if (int rc = timed_begin(R, 1)) return rc;
     if (int rc = launch_solve(P, gauss, R->sms, R->xg, R->stream, &R->launches, R->d_specs, nullptr, &R->cache_l))
         return rc;
@@ -1764,6 +1770,50 @@ static int local_multi(tl_run* R, const tl_macro_plan& mp, const tl_micro_plan* 
     return timed_end(R);
 }
 
+// One macro step's global part (twolevel.solve_global + the predicted trace) on the run's
+// stream: deposit, implicit step, snapshot, trace interpolation.
+static int step_global_phase(tl_run* R, const tl_macro_plan& mp) {
+    // -- global predictor (twolevel.solve_global): deposit + implicit step --
+    if (!R->external_global) {
+    tl::k_deposit<<<1, 1024, 0, R->stream>>>(R->G, R->dep_pts + 3 * (size_t)mp.dep_offset,
+                                             R->dep_pow + mp.dep_offset, mp.dep_count, R->loadg,
+                                             R->dep_prev, R->dep_prev_n, 0, R->G.n);
+    ++R->launches;
+    TL_CUDA(cudaGetLastError());
+    tl::PcgParams P{};
+    base_params(R, P, false, mp.dt_global);
+    P.T = R->Tg;
+    P.gA = nullptr;
+    P.g_const = R->desc.T_buildplate;
+    P.load = R->loadg;
+    P.info = R->info + R->info_n++;
+    if (int rc = timed_begin(R, 0)) return rc;
+    if (int rc = launch_solve(P, false, R->sms, R->xg, R->stream, &R->launches, R->d_specs, nullptr,
+                              &R->cache_g))
+        return rc;
+    if (int rc = timed_end(R)) return rc;
+    }
+    if (mp.record) {
+        if (int rc = ensure_snapshots(R, mp.n_micro + mp.corrector)) return rc;
+        TL_CUDA(cudaMemcpyAsync(R->snap_g, R->Tg, sizeof(double) * R->G.n, cudaMemcpyDeviceToDevice, R->stream));
+        R->snap_n = mp.n_micro + mp.corrector;
+    }
+    // -- trace of the predicted global field on gamma --
+    if (int rc = run_interp_local(R, 1, nullptr, R->tr_pred)) return rc;
+    return TL_OK;
+}
+
+// End of a macro step: the converged trace, then the relocation (scanpath.relocate_local).
+static int step_finish_phase(tl_run* R, const tl_macro_plan& mp) {
+    // converged trace at the macro instant = trace_pred
+    std::swap(R->tr_old, R->tr_pred);
+    if (mp.relocate) {
+        for (int a = 0; a < 3; ++a) R->L.off[a] = mp.new_offset[a];
+        if (int rc = run_interp_local(R, 0, R->Tl, R->tr_old)) return rc;
+    }
+    return TL_OK;
+}
+
 int32_t tl_run_macro_steps(tl_run* R, const tl_macro_plan* plans, int32_t nsteps,
                            const tl_micro_plan* micro, int32_t nmicro, const double* dep_points,
                            const double* dep_power, int32_t ndep) {
@@ -1806,33 +1856,7 @@ int32_t tl_run_macro_steps(tl_run* R, const tl_macro_plan* plans, int32_t nsteps
     }
     for (int s = 0; s < nsteps; ++s) {
         const tl_macro_plan& mp = plans[s];
-        // -- global predictor (twolevel.solve_global): deposit + implicit step --
-        if (!R->external_global) {
-        tl::k_deposit<<<1, 1024, 0, R->stream>>>(R->G, R->dep_pts + 3 * (size_t)mp.dep_offset,
-                                                 R->dep_pow + mp.dep_offset, mp.dep_count, R->loadg,
-                                                 R->dep_prev, R->dep_prev_n, 0, R->G.n);
-        ++R->launches;
-        TL_CUDA(cudaGetLastError());
-        tl::PcgParams P{};
-        base_params(R, P, false, mp.dt_global);
-        P.T = R->Tg;
-        P.gA = nullptr;
-        P.g_const = R->desc.T_buildplate;
-        P.load = R->loadg;
-        P.info = R->info + R->info_n++;
-        if (int rc = timed_begin(R, 0)) return rc;
-        if (int rc = launch_solve(P, false, R->sms, R->xg, R->stream, &R->launches, R->d_specs, nullptr,
-                                  &R->cache_g))
-            return rc;
-        if (int rc = timed_end(R)) return rc;
-        }
-        if (mp.record) {
-            if (int rc = ensure_snapshots(R, mp.n_micro + mp.corrector)) return rc;
-            TL_CUDA(cudaMemcpyAsync(R->snap_g, R->Tg, sizeof(double) * R->G.n, cudaMemcpyDeviceToDevice, R->stream));
-            R->snap_n = mp.n_micro + mp.corrector;
-        }
-        // -- trace of the predicted global field on gamma --
-        if (int rc = run_interp_local(R, 1, nullptr, R->tr_pred)) return rc;
+        if (int rc = step_global_phase(R, mp)) return rc;
         // -- micro steps (+ corrector): one persistent launch when the local grid fits --
         const bool boxed = !multi && lstream;
         if (boxed)
@@ -1858,16 +1882,170 @@ int32_t tl_run_macro_steps(tl_run* R, const tl_macro_plan* plans, int32_t nsteps
             if (mp.record)
                 TL_CUDA(cudaMemcpyAsync(R->snap_l[mp.n_micro], R->Tl, sizeof(double) * R->L.n, cudaMemcpyDeviceToDevice, R->stream));
         }
-        // converged trace at the macro instant = trace_pred
-        std::swap(R->tr_old, R->tr_pred);
-        // -- relocation (scanpath.relocate_local) --
-        if (mp.relocate) {
-            for (int a = 0; a < 3; ++a) R->L.off[a] = mp.new_offset[a];
-            if (int rc = run_interp_local(R, 0, R->Tl, R->tr_old)) return rc;
-        }
+        if (int rc = step_finish_phase(R, mp)) return rc;
     }
     TL_CUDA(cudaGetLastError());
     return TL_OK;
+}
+
+// ---- batched runs (BASELINE config 5) ------------------------------------------------
+// One macro step of a group of runs whose local grids have one shape: the global parts run
+// per run, the i-th micro solve (and the corrector) of ALL runs is one batched solve
+// (k_sb_rhs -> k_tb_cg -> k_sb_resid -> k_sb_final, tl_tiled.cuh).  Everything is enqueued
+// on the first run's stream; the other runs' streams are ordered before and after it.
+static tl::PcgParams* g_batch_dev[64] = {nullptr};
+static unsigned* g_batch_ctr[64] = {nullptr};
+
+static int batched_solve(std::vector<tl::PcgParams>& Ps, int dev, int sms, cudaStream_t st, int64_t* launches) {
+    const int B = (int)Ps.size();
+    if (B == 0) return TL_OK;
+    if (B > tl::kTBMax) return fail(TL_E_INVALID, "too many systems in one batched solve");
+    tl::TPlan tp{};
+    size_t smem = 0;
+    if (!tiled_plan_range(Ps[0].g, sms, 0, Ps[0].g.NZ, tp, smem)) return fail(TL_E_INVALID, "no item plan for the batch");
+    if ((long long)tp.I * B > 2000000000ll / 4) return fail(TL_E_INVALID, "batch too large");
+    tp.iid.init((uint32_t)tp.I);
+    if (!g_batch_dev[dev]) {
+        TL_CUDA(cudaMalloc((void**)&g_batch_dev[dev], sizeof(tl::PcgParams) * tl::kTBMax));
+        TL_CUDA(cudaMalloc((void**)&g_batch_ctr[dev], 4 * sizeof(unsigned)));
+    }
+    tl::PcgParams* dPs = g_batch_dev[dev];
+    for (auto& P : Ps) {
+        P.light_rhs = 1;
+        P.snake = snake_enabled();
+        P.prof = nullptr;
+    }
+    // stream-ordered after the previous batched solve's kernels; the pageable source is
+    // staged before the call returns
+    TL_CUDA(cudaMemcpyAsync(dPs, Ps.data(), sizeof(tl::PcgParams) * B, cudaMemcpyHostToDevice, st));
+    static thread_local int occ_rhs = 0, occ_res = 0;
+    if (occ_rhs == 0) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_rhs, tl::k_sb_rhs, tl::kSTPB, 0) != cudaSuccess || occ_rhs < 1)
+            occ_rhs = 1;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_res, tl::k_sb_resid, tl::kSTPB, 0) != cudaSuccess || occ_res < 1)
+            occ_res = 1;
+    }
+    // blocks per system: the batch fills the device together
+    const int per = std::max(1, (std::min(4, occ_rhs) * sms + B - 1) / B);
+    const int Gr = std::min(per, (Ps[0].g.n + tl::kSTPB - 1) / tl::kSTPB);
+    const int perq = std::max(1, (std::min(4, occ_res) * sms + B - 1) / B);
+    const int Gq = std::min(perq, (Ps[0].g.n + tl::kSTPB - 1) / tl::kSTPB);
+    tl::k_sb_rhs<<<dim3(Gr, B), tl::kSTPB, 0, st>>>(dPs);
+    TL_CUDA(cudaGetLastError());
+    TL_CUDA(cudaMemsetAsync(g_batch_ctr[dev], 0, 4 * sizeof(unsigned), st));
+    const bool two = tp.H * Ps[0].g.NX <= 2 * tp.ncw * 32;
+    auto kern = tp.ncw == 16 ? (two ? tl::k_tb_cg<16, 2> : tl::k_tb_cg<16, 4>) : (two ? tl::k_tb_cg<19, 2> : tl::k_tb_cg<19, 4>);
+    TL_CUDA(ensure_smem_attr((const void*)kern, smem));
+    int Bv = B, Grv = Gr;
+    unsigned* ctr = g_batch_ctr[dev];
+    void* args[] = {&dPs, &Bv, &Grv, (void*)&tp, &ctr};
+    TL_CUDA(cudaLaunchCooperativeKernel((void*)kern, sms, (tp.ncw + 1) * 32, args, smem, st));
+    tl::k_sb_resid<<<dim3(Gq, B), tl::kSTPB, 0, st>>>(dPs);
+    tl::k_sb_final<<<B, tl::kSTPB, 0, st>>>(dPs, Gq);
+    TL_CUDA(cudaGetLastError());
+    if (launches) *launches += 4;
+    return TL_OK;
+}
+
+int32_t tl_runs_macro_step(tl_run** runs, int32_t nruns, const tl_macro_plan* plans,
+                           const tl_micro_plan* const* micro, const int32_t* nmicro,
+                           const double* const* dep_points, const double* const* dep_power, const int32_t* ndep) {
+    if (!runs || nruns < 1 || !plans || !micro || !nmicro || !dep_points || !dep_power || !ndep)
+        return fail(TL_E_INVALID, "null argument");
+    if (nruns > tl::kTBMax) return fail(TL_E_INVALID, "at most 64 runs per batched step");
+    tl_run* R0 = runs[0];
+    TL_CUDA(cudaSetDevice(R0->device));
+    for (int r = 0; r < nruns; ++r) {
+        tl_run* R = runs[r];
+        const tl_macro_plan& mp = plans[r];
+        if (!R || R->device != R0->device) return fail(TL_E_INVALID, "batched runs must share a device");
+        for (int a = 0; a < 3; ++a)
+            if (R->L.nc[a] != R0->L.nc[a]) return fail(TL_E_INVALID, "batched runs need local grids of one shape");
+        if (R->external_global) return fail(TL_E_INVALID, "batched runs hold their own global field");
+        if (mp.record) return fail(TL_E_INVALID, "batched steps keep no snapshots");
+        if (mp.n_micro < 1 || mp.micro_offset < 0 || mp.micro_offset + mp.n_micro + mp.corrector > nmicro[r])
+            return fail(TL_E_INVALID, "micro plan out of range");
+        if (mp.dep_count < 0 || mp.dep_offset < 0 || mp.dep_offset + mp.dep_count > ndep[r])
+            return fail(TL_E_INVALID, "deposit plan out of range");
+        if (mp.dep_count * 4 > tl::kDepMax) return fail(TL_E_INVALID, "too many deposit samples in one step");
+        if (int rc = ensure_info(R, 1 + mp.n_micro + mp.corrector)) return rc;
+    }
+    // one stream for the whole step: the other runs' streams first catch up with it
+    cudaStream_t S = R0->stream;
+    std::vector<cudaStream_t> own(nruns);
+    cudaEvent_t ev;
+    TL_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    for (int r = 0; r < nruns; ++r) {
+        own[r] = runs[r]->stream;
+        if (r > 0) {
+            TL_CUDA(cudaEventRecord(ev, own[r]));
+            TL_CUDA(cudaStreamWaitEvent(S, ev, 0));
+        }
+        runs[r]->stream = S;
+    }
+    int rc = TL_OK;
+    auto restore = [&]() {
+        cudaEventRecord(ev, S);
+        for (int r = 0; r < nruns; ++r) {
+            runs[r]->stream = own[r];
+            if (r > 0) cudaStreamWaitEvent(own[r], ev, 0);
+        }
+        cudaEventDestroy(ev);
+    };
+    int max_m = 0;
+    for (int r = 0; r < nruns && rc == TL_OK; ++r) {
+        tl_run* R = runs[r];
+        const tl_macro_plan& mp = plans[r];
+        if (ndep[r] > R->dep_cap) {
+            if (R->dep_pts) cudaFree(R->dep_pts);
+            if (R->dep_pow) cudaFree(R->dep_pow);
+            R->dep_pts = nullptr; R->dep_pow = nullptr; R->dep_cap = 0;
+            if ((rc = dalloc(&R->dep_pts, 3 * (size_t)ndep[r])) || (rc = dalloc(&R->dep_pow, ndep[r]))) break;
+            R->dep_cap = ndep[r];
+        }
+        if (ndep[r] > 0) {
+            cudaMemcpyAsync(R->dep_pts, dep_points[r], sizeof(double) * 3 * ndep[r], cudaMemcpyHostToDevice, S);
+            cudaMemcpyAsync(R->dep_pow, dep_power[r], sizeof(double) * ndep[r], cudaMemcpyHostToDevice, S);
+        }
+        if ((rc = step_global_phase(R, mp))) break;
+        if ((rc = stream_gauss_loads(R, mp, micro[r], mp.n_micro + (mp.corrector ? 1 : 0)))) break;
+        max_m = std::max(max_m, mp.n_micro);
+    }
+    std::vector<tl::PcgParams> Ps;
+    for (int i = 0; i < max_m && rc == TL_OK; ++i) {
+        Ps.clear();
+        for (int r = 0; r < nruns; ++r) {
+            tl_run* R = runs[r];
+            const tl_macro_plan& mp = plans[r];
+            if (i >= mp.n_micro) continue;
+            if (i == mp.n_micro - 1 && mp.corrector) {
+                tl::k_copy<<<4 * R->sms, 256, 0, S>>>(R->Tl, R->Tl_before, R->L.n);
+                ++R->launches;
+            }
+            tl::PcgParams P{};
+            local_params(R, R->Tl, micro[r][mp.micro_offset + i], i, P);
+            Ps.push_back(P);
+        }
+        rc = batched_solve(Ps, R0->device, R0->sms, S, &R0->launches);
+    }
+    if (rc == TL_OK) {                      // correctors: the last micro interval again, from before_final
+        Ps.clear();
+        for (int r = 0; r < nruns; ++r) {
+            tl_run* R = runs[r];
+            const tl_macro_plan& mp = plans[r];
+            if (!mp.corrector) continue;
+            tl::PcgParams P{};
+            local_params(R, R->Tl_before, micro[r][mp.micro_offset + mp.n_micro], mp.n_micro, P);
+            Ps.push_back(P);
+        }
+        rc = batched_solve(Ps, R0->device, R0->sms, S, &R0->launches);
+        for (int r = 0; r < nruns; ++r)
+            if (plans[r].corrector) std::swap(runs[r]->Tl, runs[r]->Tl_before);
+    }
+    for (int r = 0; r < nruns && rc == TL_OK; ++r) rc = step_finish_phase(runs[r], plans[r]);
+    restore();
+    if (rc == TL_OK && cudaGetLastError() != cudaSuccess) rc = fail(TL_E_CUDA, "batched macro step launch failed");
+    return rc;
 }
 
 int32_t tl_run_get_snapshot(tl_run* R, int32_t which, int32_t index, double* host, int64_t n) {

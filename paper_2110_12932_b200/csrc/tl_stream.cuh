@@ -107,7 +107,7 @@ __device__ __forceinline__ void s_rhs_node(const PcgParams& P, const ClassTable&
 }
 
 // ---- k_s_rhs: b, r = b, x = 0; partials [0][blk] = b.b, [1][blk] = r.z ----------------
-__global__ void __launch_bounds__(kSTPB, 3) k_s_rhs(PcgParams P) {
+__device__ __forceinline__ void s_rhs_block(const PcgParams& P) {
     __shared__ ClassTable T;
     __shared__ double red[2 * 32];
     __shared__ int box[6];
@@ -128,6 +128,18 @@ __global__ void __launch_bounds__(kSTPB, 3) k_s_rhs(PcgParams P) {
         P.part[blockIdx.x] = acc[0];
         P.part[gridDim.x + blockIdx.x] = acc[1];
     }
+}
+
+__global__ void __launch_bounds__(kSTPB, 3) k_s_rhs(PcgParams P) { s_rhs_block(P); }
+
+// Batched (config 5): grid = (blocks per system, systems); system blockIdx.y from Ps.
+__global__ void __launch_bounds__(kSTPB, 3) k_sb_rhs(const PcgParams* Ps) {
+    __shared__ __align__(16) unsigned char pbuf[sizeof(PcgParams)];      // (PcgParams has default member initialisers)
+    PcgParams& P = *reinterpret_cast<PcgParams*>(pbuf);
+    for (int e = threadIdx.x; e < (int)(sizeof(PcgParams) / 4); e += blockDim.x)
+        reinterpret_cast<uint32_t*>(pbuf)[e] = reinterpret_cast<const uint32_t*>(Ps + blockIdx.y)[e];
+    __syncthreads();
+    s_rhs_block(P);
 }
 
 // Sweep A at node p: p_p = z (+ beta p_old) written; returns p_p (A p)_p restricted to the
@@ -339,7 +351,7 @@ __device__ __forceinline__ void s_resid_node(const Grid& g, const ClassTable& T,
 }
 
 // ---- k_s_resid: partials [0][blk] = ||A_c x - b||^2, [1][blk] = non-finite count --------
-__global__ void __launch_bounds__(kSTPB, 3) k_s_resid(PcgParams P) {
+__device__ __forceinline__ void s_resid_block(const PcgParams& P) {
     __shared__ ClassTable T;
     __shared__ double red[2 * 32];
     const Grid& g = P.g;
@@ -360,8 +372,19 @@ __global__ void __launch_bounds__(kSTPB, 3) k_s_resid(PcgParams P) {
     }
 }
 
+__global__ void __launch_bounds__(kSTPB, 3) k_s_resid(PcgParams P) { s_resid_block(P); }
+
+__global__ void __launch_bounds__(kSTPB, 3) k_sb_resid(const PcgParams* Ps) {
+    __shared__ __align__(16) unsigned char pbuf[sizeof(PcgParams)];      // (PcgParams has default member initialisers)
+    PcgParams& P = *reinterpret_cast<PcgParams*>(pbuf);
+    for (int e = threadIdx.x; e < (int)(sizeof(PcgParams) / 4); e += blockDim.x)
+        reinterpret_cast<uint32_t*>(pbuf)[e] = reinterpret_cast<const uint32_t*>(Ps + blockIdx.y)[e];
+    __syncthreads();
+    s_resid_block(P);
+}
+
 // ---- k_s_final (one block): the residual partials -> the outcome record ----------------
-__global__ void __launch_bounds__(kSTPB) k_s_final(PcgParams P, int Gres) {
+__device__ __forceinline__ void s_final_block(const PcgParams& P, int Gres) {
     __shared__ double red[2 * 32];
     __shared__ double tot[2];
     const int s[2] = {0, 1};
@@ -375,6 +398,17 @@ __global__ void __launch_bounds__(kSTPB) k_s_final(PcgParams P, int Gres) {
         P.info->status = status;
         P.info->true_resid = tres;
     }
+}
+
+__global__ void __launch_bounds__(kSTPB) k_s_final(PcgParams P, int Gres) { s_final_block(P, Gres); }
+
+__global__ void __launch_bounds__(kSTPB) k_sb_final(const PcgParams* Ps, int Gres) {
+    __shared__ __align__(16) unsigned char pbuf[sizeof(PcgParams)];
+    PcgParams& P = *reinterpret_cast<PcgParams*>(pbuf);
+    for (int e = threadIdx.x; e < (int)(sizeof(PcgParams) / 4); e += blockDim.x)
+        reinterpret_cast<uint32_t*>(pbuf)[e] = reinterpret_cast<const uint32_t*>(Ps + blockIdx.x)[e];
+    __syncthreads();
+    s_final_block(P, Gres);
 }
 
 }  // namespace tl

@@ -55,6 +55,7 @@ struct TPlan {
     int RB, RX;     // sweep B: p at [0, RB), x at [RB, RB + RX), r at [RB + RX, RB + 2 RX)
     FastDiv nsd, nbd;       // division by NS, NB
     int ncw;        // consumer warps of the kernel instance this plan is for (host side)
+    FastDiv iid;    // division by I (batched solves: global item = system * I + item)
     int snake;      // 1: sweep B takes the items from the top of the grid down (L2 reuse, below)
     unsigned long long* prof;    // TLGPU_PROF=1: %globaltimer stamps of iteration 3, slot 1024 + 16 CTA + e
     short kb[kTMaxChunks + 1];   // chunk kc = planes [kb[kc], kb[kc + 1])
@@ -119,6 +120,21 @@ __device__ __forceinline__ void t_zero_ring(const TPlan& tp, double* sm) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// Batched solves (BASELINE config 5: many scenarios on grids of one shape): B independent
+// systems advance in lockstep through one sweep; the global item id is system * I + item,
+// a finished system's items are skipped, and each item takes its arrays, coefficients and
+// scalars from its system.
+constexpr int kTBMax = 64;                 // systems per batched launch
+struct TBatchCtx {
+    const PcgParams* Ps;                   // the systems (device memory; one grid shape)
+    const int* done;                       // per system: finished (shared memory)
+    const double* alpha;                   // per-system scalars of this iteration (shared memory)
+    const double* beta;
+    int B;
+    int parity;                            // iteration parity: p_old = parity ? p1 : p0
+    int light0;                            // first iteration: r0 = b, x0 = 0 implied
+};
+
 // Item geometry.
 struct TItem {
     int j0, j1, k0, k1;
@@ -140,16 +156,18 @@ __device__ __forceinline__ unsigned t_bytes(int a, int b) { return (unsigned)(((
 // Sweep A stage of plane k: r, p_old rows [j0, min(j1 + 1, NY)); sweep B stage of plane k:
 // p rows [max(j0 - 1, 0), min(j1 + 1, NY)), plus x, r rows [j0, j1) on centre planes
 // (x == nullptr: x = 0, not loaded).
-template <bool SWEEP_B>
+template <bool SWEEP_B, bool BATCH = false>
 __device__ void t_produce(const Grid& g, const TPlan& tp, double* sm, uint64_t* full, uint64_t* empty,
                           int* s_item, unsigned* ctr, uint32_t& t, bool first, const double* r,
-                          const double* pold, const double* pc, const double* x, bool rev = false) {
+                          const double* pold, const double* pc, const double* x, bool rev = false,
+                          const TBatchCtx* bc = nullptr) {
     const int NXY = g.NX * g.NY;
+    const int Itot = BATCH ? bc->B * tp.I : tp.I;
     // the first item of every CTA is static (no counter round trip at the sweep start);
     // the rest come from the counter, offset by the grid size
     unsigned next = blockIdx.x;
     while (true) {
-        if ((int)next >= tp.I) {
+        if ((int)next >= Itot) {
             unsigned ph;
             const int s = t_slot(tp, t, ph);
             mbar_wait(&empty[s], ph ^ 1);
@@ -160,8 +178,19 @@ __device__ void t_produce(const Grid& g, const TPlan& tp, double* sm, uint64_t* 
         }
         // rev: the sweep walks the items from the last one down, so it starts on the planes
         // the previous sweep touched last (still in L2)
-        const int item = rev ? tp.I - 1 - (int)next : (int)next;
+        const int gitem = rev ? Itot - 1 - (int)next : (int)next;
         next = gridDim.x + atomicAdd(ctr, 1u);   // the next item's id arrives while this one streams
+        int item = gitem;
+        if (BATCH) {
+            const int sy_ = (int)tp.iid.div((uint32_t)gitem);
+            item = gitem - sy_ * tp.I;
+            if (bc->done[sy_]) continue;
+            const PcgParams& Q = bc->Ps[sy_];
+            r = bc->light0 ? Q.b : Q.r;
+            pold = bc->parity ? Q.p1 : Q.p0;
+            pc = bc->parity ? Q.p0 : Q.p1;
+            x = bc->light0 ? nullptr : Q.T;
+        }
         const TItem it = t_item(g, tp, item);
         const int ks = SWEEP_B ? max(it.k0 - 1, 0) : it.k0;
         const int ke = min(it.k1, g.NZ - 1);
@@ -169,7 +198,7 @@ __device__ void t_produce(const Grid& g, const TPlan& tp, double* sm, uint64_t* 
             unsigned ph;
             const int s = t_slot(tp, t, ph);
             mbar_wait(&empty[s], ph ^ 1);
-            if (k == ks) s_item[s] = item;
+            if (k == ks) s_item[s] = gitem;
             double* st = sm + (size_t)s * tp.stage;
             if (!SWEEP_B) {
                 const int a = k * NXY + it.j0 * g.NX, b = k * NXY + min(it.j1 + 1, g.NY) * g.NX;
@@ -317,19 +346,40 @@ struct TNodes {
 // ---- consumers: sweep A ------------------------------------------------------------------
 // p = z (+ beta p_old) and its p.Ap contribution over the node and its free forward
 // neighbours (s_sweep_a_node, one expression for every class).
-template <int NCW, int NPT>
-__device__ void t_consume_a(const Grid& g, const TPlan& tp, const ClassTable& T, uint64_t* full, uint64_t* empty,
+// Batched consumers: the item's system selects the arrays, the scalars and the class table
+// (rebuilt in shared memory when the system changes; every consumer warp walks the same
+// item sequence, so the named barriers around the rebuild are uniform).
+template <int NCW>
+__device__ __forceinline__ void t_batch_table(const Grid& g, ClassTable& T, const PcgParams& Q) {
+    asm volatile("bar.sync 1, %0;" ::"r"(NCW * 32) : "memory");
+    build_class_table(T, threadIdx.x, Q.mbase, Q.cbase, g.dkind);
+    asm volatile("bar.sync 1, %0;" ::"r"(NCW * 32) : "memory");
+}
+
+template <int NCW, int NPT, bool BATCH = false>
+__device__ void t_consume_a(const Grid& g, const TPlan& tp, ClassTable& T, uint64_t* full, uint64_t* empty,
                             const int* s_item, uint32_t& t, bool first, double beta, double* __restrict__ pnew,
-                            double* part, double (*ired)[32], unsigned long long* pf = nullptr) {
+                            double* part, double (*ired)[32], unsigned long long* pf = nullptr,
+                            const TBatchCtx* bc = nullptr) {
     const int NXY = g.NX * g.NY, sy = g.NX, RA = tp.RA;
     constexpr int NT = NCW * 32;
+    int cur_sys = -1;
     TRing cur;
     cur.set(tp, t);
     while (true) {
         t_wait_full(full, cur);
         if (pf && threadIdx.x == 0) { *pf = t_ns(); pf = nullptr; }      // first stage of the sweep landed
-        const int item = s_item[cur.s];
+        int item = s_item[cur.s];
         if (item < 0) { t_release(empty, cur); cur.adv(tp); t = cur.t; return; }
+        if (BATCH) {
+            const int sy_ = (int)tp.iid.div((uint32_t)item);
+            item -= sy_ * tp.I;
+            const PcgParams& Q = bc->Ps[sy_];
+            if (sy_ != cur_sys) { t_batch_table<NCW>(g, T, Q); cur_sys = sy_; }
+            pnew = bc->parity ? Q.p0 : Q.p1;
+            beta = bc->beta[sy_];
+            part = Q.part + kTPartItems;
+        }
         const TItem it = t_item(g, tp, item);
         TNodes<NPT, NT> nd;
         nd.init(g, it);
@@ -423,20 +473,31 @@ __device__ void t_consume_a(const Grid& g, const TPlan& tp, const ClassTable& T,
 // q = A_c p (apply_free, one expression for every class), x += alpha p, r -= alpha q.
 // Holds stages k and k+1; the p values of plane k-1 at the thread's own nodes (its z
 // neighbour below) are the centre values of the previous plane, kept in registers.
-template <int NCW, int NPT>
-__device__ void t_consume_b(const Grid& g, const TPlan& tp, const ClassTable& T, uint64_t* full, uint64_t* empty,
+template <int NCW, int NPT, bool BATCH = false>
+__device__ void t_consume_b(const Grid& g, const TPlan& tp, ClassTable& T, uint64_t* full, uint64_t* empty,
                             const int* s_item, uint32_t& t, double alpha, bool xzero, double* __restrict__ x,
                             double* __restrict__ r, double* part, double (*ired)[32],
-                            unsigned long long* pf = nullptr) {
+                            unsigned long long* pf = nullptr, const TBatchCtx* bc = nullptr) {
     const int NXY = g.NX * g.NY, sy = g.NX, RX = tp.RX;
     constexpr int NT = NCW * 32;
+    int cur_sys = -1;
     TRing cur;
     cur.set(tp, t);
     while (true) {
         t_wait_full(full, cur);
         if (pf && threadIdx.x == 0) { *pf = t_ns(); pf = nullptr; }
-        const int item = s_item[cur.s];
+        int item = s_item[cur.s];
         if (item < 0) { t_release(empty, cur); cur.adv(tp); t = cur.t; return; }
+        if (BATCH) {
+            const int sy_ = (int)tp.iid.div((uint32_t)item);
+            item -= sy_ * tp.I;
+            const PcgParams& Q = bc->Ps[sy_];
+            if (sy_ != cur_sys) { t_batch_table<NCW>(g, T, Q); cur_sys = sy_; }
+            x = Q.T;
+            r = Q.r;
+            alpha = bc->alpha[sy_];
+            part = Q.part + kTPartItems + tp.I;
+        }
         const TItem it = t_item(g, tp, item);
         TNodes<NPT, NT> nd;
         nd.init(g, it);
@@ -692,6 +753,158 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) k_t_cg(PcgParams P, int Grh
         P.info->status = status;
         P.info->bnorm = bnorm;
         P.info->rnorm = rnorm;
+    }
+}
+
+// ---- k_tb_cg: B independent solves on grids of one shape, in lockstep (config 5) ---------
+// The scenarios of BASELINE config 5 share the geometry, so the i-th micro solve of all of
+// them is ONE launch: the sweeps stream every active system's planes (global item =
+// system * I + item), the two grid barriers of an iteration are shared by all systems, and
+// each system keeps its own scalars, stop test and iteration count (finished systems drop
+// out of the sweeps).  A cfg2-sized solve alone is L2-resident and barrier-bound; 64 of
+// them together are an HBM-sized stream (33M nodes) whose barriers amortise over the batch.
+// Per-system arithmetic is k_t_cg's: the same item plan gives bitwise the same iterates.
+// Per-system sums: warp w adds the partials of systems w, w + nw, ... (lane-strided in a
+// fixed order, then the butterfly), every CTA identically.
+template <int NV>
+__device__ __forceinline__ void tb_sums(const PcgParams* Ps, int B, const int* skip, int off, int stride, int count,
+                                        double (*out)[kTBMax]) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int s = w; s < B; s += nw) {
+        if (skip && skip[s]) continue;
+        const double* part = Ps[s].part + off;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            double acc = 0.0;
+            for (int b = lane; b < count; b += 32) acc += __ldcg(part + v * stride + b);
+            acc = warp_sum(acc);
+            if (lane == 0) out[v][s] = acc;
+        }
+    }
+    __syncthreads();
+}
+
+template <int NCW, int NPT>
+__global__ void __launch_bounds__((NCW + 1) * 32, 1) k_tb_cg(const PcgParams* Ps, int B, int Grhs, TPlan tp,
+                                                             unsigned* ctr) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ ClassTable T;
+    __shared__ __align__(16) unsigned char gbuf[sizeof(Grid)];          // (Grid has default member initialisers)
+    Grid& g = *reinterpret_cast<Grid*>(gbuf);
+    __shared__ double ired[2][32];
+    __shared__ __align__(8) uint64_t full[kTMaxStages], empty[kTMaxStages];
+    __shared__ int s_item[kTMaxStages];
+    __shared__ double s_alpha[kTBMax], s_beta[kTBMax], s_rho[kTBMax], s_rhop[kTBMax], s_atol[kTBMax];
+    __shared__ double s_rnorm[kTBMax], s_bnorm[kTBMax], s_sum[2][kTBMax];
+    __shared__ int s_done[kTBMax], s_status[kTBMax], s_its[kTBMax], s_active;
+    for (int e = threadIdx.x; e < (int)(sizeof(Grid) / 4); e += blockDim.x)
+        reinterpret_cast<uint32_t*>(gbuf)[e] = reinterpret_cast<const uint32_t*>(&Ps[0].g)[e];
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < tp.NS; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NCW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    t_zero_ring(tp, t_sm);
+    __syncthreads();
+    tb_sums<2>(Ps, B, nullptr, 0, Grhs, Grhs, s_sum);        // b.b and r0.z of every system
+    if (threadIdx.x < B) {
+        const int s = threadIdx.x;
+        const double bb = s_sum[0][s];
+        s_bnorm[s] = sqrt(bb);
+        s_atol[s] = Ps[s].rtol * s_bnorm[s];
+        s_rnorm[s] = s_bnorm[s];
+        s_rho[s] = s_sum[1][s];
+        s_rhop[s] = 1.0;
+        s_done[s] = bb == 0.0 ? 1 : 0;          // b = 0: x = 0 (fem.py:275-276)
+        s_status[s] = 0;
+        s_its[s] = 0;
+    }
+    __syncthreads();
+    const bool producer = (threadIdx.x >> 5) == NCW;
+    const bool plane0 = producer && (threadIdx.x & 31) == 0;
+    int it = 0;
+    uint32_t t = 0;
+    unsigned seq = 0;
+    while (true) {
+        if (threadIdx.x < B && !s_done[threadIdx.x]) {
+            const int s = threadIdx.x;
+            int st = -1;
+            if (s_rnorm[s] < s_atol[s]) st = 0;
+            else if (!isfinite(s_rnorm[s])) st = 3;
+            else if (it >= Ps[s].maxiter) st = 1;
+            if (st >= 0) {
+                s_done[s] = 1;
+                s_status[s] = st;
+                s_its[s] = st == 1 ? Ps[s].maxiter : it;
+            } else {
+                s_beta[s] = it > 0 ? s_rho[s] / s_rhop[s] : 0.0;
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int a = 0;
+            for (int s = 0; s < B; ++s) a += s_done[s] ? 0 : 1;
+            s_active = a;
+        }
+        __syncthreads();
+        if (s_active == 0) break;
+        const bool first = it == 0;
+        TBatchCtx bc{Ps, s_done, s_alpha, s_beta, B, it & 1, first ? 1 : 0};
+        // ---- sweep A ----
+        if (blockIdx.x == 0 && threadIdx.x == 0) ctr[(seq + 2) & 3] = 0u;
+        if (producer) {
+            if (plane0) t_produce<false, true>(g, tp, t_sm, full, empty, s_item, ctr + (seq & 3), t, first, nullptr,
+                                               nullptr, nullptr, nullptr, false, &bc);
+        } else {
+            t_consume_a<NCW, NPT, true>(g, tp, T, full, empty, s_item, t, first, 0.0, nullptr, nullptr, ired, nullptr,
+                                        &bc);
+            fence_proxy_async_global();
+        }
+        ++seq;
+        grid.sync();
+        t = __shfl_sync(0xffffffffu, t, 0);
+        fence_proxy_async_global();
+        tb_sums<1>(Ps, B, s_done, kTPartItems, tp.I, tp.I, s_sum);
+        if (threadIdx.x < B && !s_done[threadIdx.x]) s_alpha[threadIdx.x] = s_rho[threadIdx.x] / s_sum[0][threadIdx.x];
+        __syncthreads();
+        // ---- sweep B ----
+        if (blockIdx.x == 0 && threadIdx.x == 0) ctr[(seq + 2) & 3] = 0u;
+        if (producer) {
+            if (plane0) t_produce<true, true>(g, tp, t_sm, full, empty, s_item, ctr + (seq & 3), t, false, nullptr,
+                                              nullptr, nullptr, nullptr, tp.snake != 0, &bc);
+        } else {
+            t_consume_b<NCW, NPT, true>(g, tp, T, full, empty, s_item, t, 0.0, first, nullptr, nullptr, nullptr, ired,
+                                        nullptr, &bc);
+            fence_proxy_async_global();
+        }
+        ++seq;
+        grid.sync();
+        t = __shfl_sync(0xffffffffu, t, 0);
+        fence_proxy_async_global();
+        tb_sums<2>(Ps, B, s_done, kTPartItems + tp.I, tp.I, tp.I, s_sum);
+        if (threadIdx.x < B && !s_done[threadIdx.x]) {
+            const int s = threadIdx.x;
+            s_rhop[s] = s_rho[s];
+            s_rho[s] = s_sum[0][s];
+            s_rnorm[s] = sqrt(s_sum[1][s]);
+        }
+        __syncthreads();
+        ++it;
+    }
+    // systems that ran no iteration (b = 0): x0 = 0 was never written (light RHS)
+    for (int s = 0; s < B; ++s)
+        if (s_its[s] == 0 && s_status[s] != 1)
+            for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < g.n; p += gridDim.x * blockDim.x) Ps[s].T[p] = 0.0;
+    if (blockIdx.x == 0 && threadIdx.x < B) {
+        const int s = threadIdx.x;
+        SolveInfoDev* info = Ps[s].info;
+        info->iterations = s_its[s];
+        info->status = s_status[s];
+        info->bnorm = s_bnorm[s];
+        info->rnorm = s_rnorm[s];
     }
 }
 

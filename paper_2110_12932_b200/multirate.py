@@ -268,6 +268,54 @@ class DeviceFieldState(FieldState):
                 f"{'on device' if self._v is None else 'read back'})")
 
 
+class BatchedRuns:
+    """BASELINE config 5 (``runner.py:376-380`` is the reference's concurrency point): a group
+    of resident runs on local grids of ONE shape, advanced one macro step at a time with the
+    i-th micro solve (and the corrector) of all runs batched into one streaming solve
+    (``tl_runs_macro_step``, ``k_tb_cg``).  The systems advance in lockstep, each with its
+    own scalars, stop test and iteration count; outcomes go to every run's info log."""
+
+    def __init__(self, runs):
+        self.runs = list(runs)
+        if not 1 <= len(self.runs) <= 64:
+            raise ValueError("a batch holds 1..64 runs")
+        self._handles = (C.c_void_p * len(self.runs))(*[r._h for r in self.runs])
+
+    def step(self, plans):
+        """One macro step of every run; ``plans[r]`` is a one-step Plan of run r (no recorder)."""
+        n = len(self.runs)
+        if len(plans) != n:
+            raise ValueError("one plan per run")
+        keep = []
+        macro = np.zeros(n, dtype=plans[0].macro.dtype)
+        micro_p, nmicro, pts_p, pw_p, ndep = ((C.c_void_p * n)(), (C.c_int32 * n)(), (C.c_void_p * n)(),
+                                              (C.c_void_p * n)(), (C.c_int32 * n)())
+        for r, (run, pl) in enumerate(zip(self.runs, plans)):
+            if pl.n_steps != 1:
+                raise ValueError("batched steps take one-step plans")
+            if run._lazy:
+                run._materialize_lazy()
+            macro[r] = pl.macro[0]
+            mi = np.ascontiguousarray(pl.micro)
+            pts = np.ascontiguousarray(pl.dep_points.reshape(-1), dtype=np.float64)
+            pw = np.ascontiguousarray(pl.dep_power, dtype=np.float64)
+            keep.extend((mi, pts, pw))
+            micro_p[r], nmicro[r] = mi.ctypes.data, len(mi)
+            pts_p[r], pw_p[r], ndep[r] = (pts.ctypes.data if len(pw) else None, pw.ctypes.data if len(pw) else None,
+                                          len(pw))
+            run.h2d_bytes += macro[r:r + 1].nbytes + mi.nbytes + pts.nbytes + pw.nbytes
+        N.check(N.lib().tl_runs_macro_step(self._handles, n, macro.ctypes.data_as(C.c_void_p), micro_p, nmicro,
+                                           pts_p, pw_p, ndep), "tl_runs_macro_step")
+
+    def sync(self):
+        for r in self.runs:
+            r.sync()
+
+    def check(self):
+        for r in self.runs:
+            r.check_solves(r.take_info())
+
+
 # One idle tl_run per problem descriptor, reused by the next run_spacetime / run_space call
 # of the same problem (a cfg4 run holds ~10 GB: allocation and release are not per call).
 _POOL: dict = {}

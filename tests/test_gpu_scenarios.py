@@ -97,3 +97,53 @@ def test_interleaved_resident_runs_match_solo_runs():
         np.testing.assert_array_equal(r.field(0), g)
         np.testing.assert_array_equal(r.field(1), l)
         r.close()
+
+
+def test_batched_runs_match_solo_runs():
+    """BatchedRuns (tl_runs_macro_step / k_tb_cg): three scenarios with different sub-cycle
+    ratios (m = 5, 20, 10) and beams stepped together, the i-th micro solve of all of them
+    one batched streaming solve; against the same scenarios stepped alone on the default
+    (SMEM-resident) kernels: fields to CG rounding (1e-11), the same iteration counts to
+    +-1, the same melt masks; and run-to-run bitwise."""
+    n = 3
+    pick = (0, 5, 1)
+    setups = [_setup(i, n) for i in pick]
+    solo = []
+    for sc, cfg, problem, lmesh, plans in setups:
+        with P.DeviceRun(problem, lmesh) as run:
+            run.initial(P.uniform_field(problem.global_mesh, cfg.T_initial))
+            its = []
+            for pl in plans:
+                run.run(pl)
+                its.append([d["iterations"] for d in run.take_info()])
+            solo.append((run.field(0), run.field(1), its))
+
+    def batched():
+        runs = []
+        for sc, cfg, problem, lmesh, plans in setups:
+            r = P.DeviceRun(problem, lmesh)
+            r.initial(P.uniform_field(problem.global_mesh, cfg.T_initial))
+            runs.append(r)
+        B = P.BatchedRuns(runs)
+        its = [[] for _ in runs]
+        for k in range(n):
+            B.step([s[4][k] for s in setups])
+            for i, r in enumerate(runs):
+                infos = r.take_info()
+                r.check_solves(infos)
+                its[i].append([d["iterations"] for d in infos])
+        out = [(r.field(0), r.field(1)) for r in runs]
+        for r in runs:
+            r.close()
+        return out, its
+
+    got, its = batched()
+    again, _ = batched()
+    for (g, l), (g2, l2), (sg, sl, sits), it, (sc, cfg, *_rest) in zip(got, again, solo, its, setups):
+        np.testing.assert_array_equal(g, g2)
+        np.testing.assert_array_equal(l, l2)
+        assert rel(g, sg) <= 1e-11 and rel(l, sl) <= 1e-11
+        TL = cfg.material.T_liquidus
+        assert_mask(None, l, sl, TL)
+        for a, b in zip(it, sits):
+            assert len(a) == len(b) and max(abs(x - y) for x, y in zip(a, b)) <= 1
