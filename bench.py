@@ -505,9 +505,22 @@ def scenario_bench(args):
         nl_m.append((Ng, Nl, sched.micro_per_macro))
     streams = [torch.cuda.ExternalStream(r.stream(), device=dev) for r in runs]
     dof_step = sum(dofs)
+    batched = not args.no_batch
+    batch = P.BatchedRuns(runs) if batched else None
 
     def one_step(k, plan_of=None, after=None):
-        """Macro step k of every scenario, device-ordered through event chaining."""
+        """Macro step k of every scenario.  Batched (default): one tl_runs_macro_step call, the
+        i-th micro solve of all scenarios one streaming solve on the first run's stream (the
+        other runs' streams are ordered after it).  --no-batch: one run after the other,
+        device-ordered through event chaining."""
+        if batched:
+            batch.step([plans[i][k] if plan_of is None else plan_of(i, k) for i in range(len(runs))])
+            if after is not None:
+                for i in range(len(runs)):
+                    after(i, k)
+            prev = torch.cuda.Event()
+            prev.record(streams[0])
+            return prev
         prev = None
         for i, (run, st) in enumerate(zip(runs, streams)):
             if prev is not None:
@@ -543,7 +556,7 @@ def scenario_bench(args):
             e0.record(streams[0])
             last = one_step(k)
             e1 = torch.cuda.Event(enable_timing=True)
-            e1.record(streams[-1])
+            e1.record(streams[0] if batched else streams[-1])
             ev.append((e0, e1))
             last = e1
         for r in runs:
@@ -553,13 +566,28 @@ def scenario_bench(args):
     launches = sum(r.launch_count() for r in runs) - launches0
     dev_ms = float(sum(a.elapsed_time(b) for a, b in ev))
     loc_rows, glo_rows = [], []
-    for r in runs:
+    for i, r in enumerate(runs):
         infos = r.take_info()
         r.check_solves(infos)
-        lo, gl = split_timing(r.take_timing(), infos)
-        loc_rows.extend(lo)
-        glo_rows.extend(gl)
+        if batched:
+            # only the global solves are timed per run; a step's records are [global, micro..., corrector]
+            per = 1 + nl_m[i][2] + 1
+            kt = r.take_timing()
+            assert len(infos) == per * args.steps and len(kt) == args.steps, (len(infos), len(kt))
+            for s_, (ms, lv, ns) in enumerate(kt):
+                glo_rows.append((ms, [infos[s_ * per]["iterations"]]))
+                loc_rows.append((0.0, [inf["iterations"] for inf in infos[s_ * per + 1:(s_ + 1) * per]]))
+        else:
+            lo, gl = split_timing(r.take_timing(), infos)
+            loc_rows.extend(lo)
+            glo_rows.extend(gl)
         r.set_timing(False)
+    if batched:
+        # the batched local solves' time: the step time minus the (timed) global solves; spread
+        # over the system-solves for the per-solve figures
+        loc_ms = dev_ms - sum(t for t, _ in glo_rows)
+        nsolve = sum(len(its) for _, its in loc_rows)
+        loc_rows = [(loc_ms * len(its) / nsolve, its) for _, its in loc_rows]
     if dist is not None:
         t = torch.tensor([dev_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -578,11 +606,17 @@ def scenario_bench(args):
     peak, peak_src = measured_peak()
     roofline = {"bound": "hbm", "achieved": kloc["achieved_gbs"], "peak": peak, "unit": "GB/s",
                 "frac": kloc["achieved_gbs"] / peak, "traffic": None,
-                "kernel": "local-grid PCG solves (k_pcg_resident_cg, SMEM-resident bricks, all micro solves "
-                          "+ corrector of a macro step in one launch), pooled over the group's scenarios",
+                "kernel": ("batched local-grid PCG solves: the i-th micro solve of every scenario of the group in "
+                           "one launch sequence k_sb_rhs -> k_tb_cg (bulk-copy z-march CG loop over all systems, in "
+                           "lockstep) -> k_sb_resid -> k_sb_final") if batched else
+                          ("local-grid PCG solves (k_pcg_resident_cg, SMEM-resident bricks, all micro solves "
+                           "+ corrector of a macro step in one launch), pooled over the group's scenarios"),
                 "level": "local", "nodes": Nl, "peak_source": peak_src,
-                "note": "algorithmic bytes N(64k+32) per solve (SURVEY §8d); each scenario's grids are "
-                        "L2/SMEM-resident within its own macro step"}
+                "note": ("algorithmic bytes N(64k+32) per system-solve (SURVEY §8d) / (the steps' CUDA-event time "
+                         "minus the per-run timed global solves): includes the Gaussian-load, interpolation and "
+                         "deposit launches of the step") if batched else
+                        ("algorithmic bytes N(64k+32) per solve (SURVEY §8d); each scenario's grids are "
+                         "L2/SMEM-resident within its own macro step")}
 
     # ---- e2e through DeviceRun.run: pinned plan uploads, every scenario's local field read back ----
     def pin(arr, dtype):
@@ -659,6 +693,7 @@ def scenario_bench(args):
                    "macro_steps": f"{args.warmup}..{args.warmup + args.steps - 1} (e2e: the next {args.steps})",
                    "l2": ("flushed between timed steps; each step also streams every scenario's fields "
                           f"({len(group)} x ~0.1 GB, larger than L2)") if not args.no_flush else "not flushed",
+                   "batched_solves": batched,
                    "parallelism": f"scenario groups x{world}" if world > 1 else "single GPU"},
         "roofline": roofline, "kernels": {"local_pcg": kloc, "global_pcg": kglo},
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
@@ -986,6 +1021,8 @@ def main():
                     help="the multi-GPU driver (z-slab global solve, time-pipelined local steps) even at N = 1")
     ap.add_argument("--strong", action="store_true",
                     help="multi-GPU: cfg4 itself split over the ranks instead of the weak-scaling plate")
+    ap.add_argument("--no-batch", action="store_true",
+                    help="cfg5: one scenario after the other (SMEM-resident kernels) instead of batched solves")
     ap.add_argument("--scenarios", type=int, default=64,
                     help="cfg5: how many of the 64 seed-0 scenarios to run (split over the ranks)")
     args = ap.parse_args()

@@ -180,7 +180,7 @@ static bool tiled_enabled() {
     return v == 1;
 }
 
-static bool tiled_plan_range(const tl::Grid& g, int sms, int zlo, int zhi, tl::TPlan& tp, size_t& smem);
+static bool tiled_plan_range(const tl::Grid& g, int sms, int zlo, int zhi, tl::TPlan& tp, size_t& smem, int nsys = 1);
 
 // TLGPU_SNAKE=0: both sweeps of the streaming CG loops walk the grid bottom-up (default 1:
 // sweep B top-down, L2 reuse across the sweeps; tl_tiled.cuh)
@@ -215,11 +215,13 @@ static bool tiled_plan(const tl::Grid& g, int sms, tl::TPlan& tp, size_t& smem) 
 // - an item costs about 2 planes beyond its own (halo plane, pipeline fill, reduction, tail);
 // - a plane costs its consumer slots (512 threads take one node each per slot) or its ring
 //   traffic including the halo rows, whichever is larger.
+// A batched solve (k_tb_cg) sweeps nsys systems of this shape together: its item count is
+// nsys times the plan's, so it takes fewer, larger items per system.
 // Constraints: H NX <= 2 x 512 nodes per plane where possible (the lean plane loops keep two
 // nodes' coefficients per thread in registers; up to 4 x 512 otherwise), at least 4 ring
 // stages in 220 KB.  TLGPU_TH / TLGPU_TC / TLGPU_TZ override H, the chunk count and the
 // smallest chunk.
-static bool tiled_plan_range(const tl::Grid& g, int sms, int zlo, int zhi, tl::TPlan& tp, size_t& smem) {
+static bool tiled_plan_range(const tl::Grid& g, int sms, int zlo, int zhi, tl::TPlan& tp, size_t& smem, int nsys) {
     const int NX = g.NX;
     const int nzr = zhi - zlo;
     if (nzr < 1) return false;
@@ -251,7 +253,7 @@ static bool tiled_plan_range(const tl::Grid& g, int sms, int zlo, int zhi, tl::T
                 if (Z < zmin && c > 1) break;
                 const long long I = (long long)NB * c;
                 if (I > tl::kTMaxItems) break;
-                const long long waves = (I + sms - 1) / sms;
+                const long long waves = (I * nsys + sms - 1) / sms;     // nsys: systems of a batched solve
                 const double cost = (double)waves * (Z + 2.0) * plane;
                 if (cost < best * (1.0 - 1e-9)) { best = cost; H = h; nch = c; ncw = nw; Hmax = hmax; }
             }
@@ -291,8 +293,11 @@ static cudaError_t launch_t_cg(tl::PcgParams& P, int Gr, int sms, cudaStream_t s
                                const tl::TPlan& tp, size_t smem) {
     launched = false;
     const int ncw = tp.ncw;
-    const bool two = tp.H * P.g.NX <= 2 * ncw * 32;
-    auto kern = ncw == 16 ? (two ? tl::k_t_cg<16, 2> : tl::k_t_cg<16, 4>) : (two ? tl::k_t_cg<19, 2> : tl::k_t_cg<19, 4>);
+    // nodes per consumer thread per plane: 1, 2 (lean plane loops) or 4
+    const int nodes = tp.H * P.g.NX;
+    const int npt = nodes <= ncw * 32 ? 1 : (nodes <= 2 * ncw * 32 ? 2 : 4);
+    auto kern = ncw == 16 ? (npt == 1 ? tl::k_t_cg<16, 1> : npt == 2 ? tl::k_t_cg<16, 2> : tl::k_t_cg<16, 4>)
+                          : (npt == 1 ? tl::k_t_cg<19, 1> : npt == 2 ? tl::k_t_cg<19, 2> : tl::k_t_cg<19, 4>);
     cudaError_t e = ensure_smem_attr((const void*)kern, smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
@@ -1902,7 +1907,7 @@ static int batched_solve(std::vector<tl::PcgParams>& Ps, int dev, int sms, cudaS
     if (B > tl::kTBMax) return fail(TL_E_INVALID, "too many systems in one batched solve");
     tl::TPlan tp{};
     size_t smem = 0;
-    if (!tiled_plan_range(Ps[0].g, sms, 0, Ps[0].g.NZ, tp, smem)) return fail(TL_E_INVALID, "no item plan for the batch");
+    if (!tiled_plan_range(Ps[0].g, sms, 0, Ps[0].g.NZ, tp, smem, B)) return fail(TL_E_INVALID, "no item plan for the batch");
     if ((long long)tp.I * B > 2000000000ll / 4) return fail(TL_E_INVALID, "batch too large");
     tp.iid.init((uint32_t)tp.I);
     if (!g_batch_dev[dev]) {
@@ -1933,8 +1938,10 @@ static int batched_solve(std::vector<tl::PcgParams>& Ps, int dev, int sms, cudaS
     tl::k_sb_rhs<<<dim3(Gr, B), tl::kSTPB, 0, st>>>(dPs);
     TL_CUDA(cudaGetLastError());
     TL_CUDA(cudaMemsetAsync(g_batch_ctr[dev], 0, 4 * sizeof(unsigned), st));
-    const bool two = tp.H * Ps[0].g.NX <= 2 * tp.ncw * 32;
-    auto kern = tp.ncw == 16 ? (two ? tl::k_tb_cg<16, 2> : tl::k_tb_cg<16, 4>) : (two ? tl::k_tb_cg<19, 2> : tl::k_tb_cg<19, 4>);
+    const int nodes = tp.H * Ps[0].g.NX;
+    const int npt = nodes <= tp.ncw * 32 ? 1 : (nodes <= 2 * tp.ncw * 32 ? 2 : 4);
+    auto kern = tp.ncw == 16 ? (npt == 1 ? tl::k_tb_cg<16, 1> : npt == 2 ? tl::k_tb_cg<16, 2> : tl::k_tb_cg<16, 4>)
+                             : (npt == 1 ? tl::k_tb_cg<19, 1> : npt == 2 ? tl::k_tb_cg<19, 2> : tl::k_tb_cg<19, 4>);
     TL_CUDA(ensure_smem_attr((const void*)kern, smem));
     int Bv = B, Grv = Gr;
     unsigned* ctr = g_batch_ctr[dev];
