@@ -570,24 +570,29 @@ def scenario_bench(args):
         infos = r.take_info()
         r.check_solves(infos)
         if batched:
-            # only the global solves are timed per run; a step's records are [global, micro..., corrector]
+            # the batched solves are timed on the first run (level 0: the global solves of all
+            # runs, level 1: one batched local solve); a run's records per step are
+            # [global, micro..., corrector]
             per = 1 + nl_m[i][2] + 1
-            kt = r.take_timing()
-            assert len(infos) == per * args.steps and len(kt) == args.steps, (len(infos), len(kt))
-            for s_, (ms, lv, ns) in enumerate(kt):
-                glo_rows.append((ms, [infos[s_ * per]["iterations"]]))
-                loc_rows.append((0.0, [inf["iterations"] for inf in infos[s_ * per + 1:(s_ + 1) * per]]))
+            assert len(infos) == per * args.steps, (len(infos), per)
+            g_its = [infos[s_ * per]["iterations"] for s_ in range(args.steps)]
+            l_its = [inf["iterations"] for s_ in range(args.steps) for inf in infos[s_ * per + 1:(s_ + 1) * per]]
+            glo_rows.append((0.0, g_its))
+            loc_rows.append((0.0, l_its))
+            if i == 0:
+                kt0 = r.take_timing()
         else:
             lo, gl = split_timing(r.take_timing(), infos)
             loc_rows.extend(lo)
             glo_rows.extend(gl)
         r.set_timing(False)
     if batched:
-        # the batched local solves' time: the step time minus the (timed) global solves; spread
-        # over the system-solves for the per-solve figures
-        loc_ms = dev_ms - sum(t for t, _ in glo_rows)
-        nsolve = sum(len(its) for _, its in loc_rows)
-        loc_rows = [(loc_ms * len(its) / nsolve, its) for _, its in loc_rows]
+        # CUDA-event time of the batched launches (RHS -> CG loop -> residual -> finish), per level,
+        # spread over the system-solves for the per-solve figures
+        for rows, lv in ((glo_rows, 0), (loc_rows, 1)):
+            ms = sum(t for t, l, _ in kt0 if l == lv)
+            nsolve = sum(len(its) for _, its in rows)
+            rows[:] = [(ms * len(its) / nsolve, its) for _, its in rows]
     if dist is not None:
         t = torch.tensor([dev_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -612,9 +617,8 @@ def scenario_bench(args):
                           ("local-grid PCG solves (k_pcg_resident_cg, SMEM-resident bricks, all micro solves "
                            "+ corrector of a macro step in one launch), pooled over the group's scenarios"),
                 "level": "local", "nodes": Nl, "peak_source": peak_src,
-                "note": ("algorithmic bytes N(64k+32) per system-solve (SURVEY §8d) / (the steps' CUDA-event time "
-                         "minus the per-run timed global solves): includes the Gaussian-load, interpolation and "
-                         "deposit launches of the step") if batched else
+                "note": ("algorithmic bytes N(64k+32) per system-solve (SURVEY §8d) / the CUDA-event time of the "
+                         "batched solve launches") if batched else
                         ("algorithmic bytes N(64k+32) per solve (SURVEY §8d); each scenario's grids are "
                          "L2/SMEM-resident within its own macro step")}
 

@@ -2014,11 +2014,48 @@ int32_t tl_runs_macro_step(tl_run** runs, int32_t nruns, const tl_macro_plan* pl
             cudaMemcpyAsync(R->dep_pts, dep_points[r], sizeof(double) * 3 * ndep[r], cudaMemcpyHostToDevice, S);
             cudaMemcpyAsync(R->dep_pow, dep_power[r], sizeof(double) * ndep[r], cudaMemcpyHostToDevice, S);
         }
-        if ((rc = step_global_phase(R, mp))) break;
-        if ((rc = stream_gauss_loads(R, mp, micro[r], mp.n_micro + (mp.corrector ? 1 : 0)))) break;
+        // global predictor: the deposit per run, the implicit steps of all runs batched below
+        tl::k_deposit<<<1, 1024, 0, S>>>(R->G, R->dep_pts + 3 * (size_t)mp.dep_offset, R->dep_pow + mp.dep_offset,
+                                         mp.dep_count, R->loadg, R->dep_prev, R->dep_prev_n, 0, R->G.n);
+        ++R->launches;
         max_m = std::max(max_m, mp.n_micro);
     }
     std::vector<tl::PcgParams> Ps;
+    bool same_global = true;
+    for (int r = 1; r < nruns; ++r)
+        for (int a = 0; a < 3; ++a) same_global = same_global && runs[r]->G.nc[a] == R0->G.nc[a];
+    if (rc == TL_OK && same_global) {
+        for (int r = 0; r < nruns; ++r) {
+            tl_run* R = runs[r];
+            tl::PcgParams P{};
+            base_params(R, P, false, plans[r].dt_global);
+            P.T = R->Tg;
+            P.gA = nullptr;
+            P.g_const = R->desc.T_buildplate;
+            P.load = R->loadg;
+            P.info = R->info + R->info_n++;
+            Ps.push_back(P);
+        }
+        if ((rc = timed_begin(R0, 0, nruns)) == TL_OK && (rc = batched_solve(Ps, R0->device, R0->sms, S, &R0->launches)) == TL_OK)
+            rc = timed_end(R0);
+    } else if (rc == TL_OK) {
+        for (int r = 0; r < nruns && rc == TL_OK; ++r) {      // global grids differ: one solve per run
+            tl_run* R = runs[r];
+            tl::PcgParams P{};
+            base_params(R, P, false, plans[r].dt_global);
+            P.T = R->Tg;
+            P.gA = nullptr;
+            P.g_const = R->desc.T_buildplate;
+            P.load = R->loadg;
+            P.info = R->info + R->info_n++;
+            rc = launch_solve(P, false, R->sms, R->xg, S, &R->launches, R->d_specs, nullptr, &R->cache_g);
+        }
+    }
+    for (int r = 0; r < nruns && rc == TL_OK; ++r) {
+        tl_run* R = runs[r];
+        if ((rc = run_interp_local(R, 1, nullptr, R->tr_pred))) break;        // predicted trace on gamma
+        rc = stream_gauss_loads(R, plans[r], micro[r], plans[r].n_micro + (plans[r].corrector ? 1 : 0));
+    }
     for (int i = 0; i < max_m && rc == TL_OK; ++i) {
         Ps.clear();
         for (int r = 0; r < nruns; ++r) {
@@ -2033,7 +2070,9 @@ int32_t tl_runs_macro_step(tl_run** runs, int32_t nruns, const tl_macro_plan* pl
             local_params(R, R->Tl, micro[r][mp.micro_offset + i], i, P);
             Ps.push_back(P);
         }
-        rc = batched_solve(Ps, R0->device, R0->sms, S, &R0->launches);
+        if ((rc = timed_begin(R0, 1, (int)Ps.size())) == TL_OK &&
+            (rc = batched_solve(Ps, R0->device, R0->sms, S, &R0->launches)) == TL_OK)
+            rc = timed_end(R0);
     }
     if (rc == TL_OK) {                      // correctors: the last micro interval again, from before_final
         Ps.clear();
@@ -2045,7 +2084,9 @@ int32_t tl_runs_macro_step(tl_run** runs, int32_t nruns, const tl_macro_plan* pl
             local_params(R, R->Tl_before, micro[r][mp.micro_offset + mp.n_micro], mp.n_micro, P);
             Ps.push_back(P);
         }
-        rc = batched_solve(Ps, R0->device, R0->sms, S, &R0->launches);
+        if (!Ps.empty() && (rc = timed_begin(R0, 1, (int)Ps.size())) == TL_OK &&
+            (rc = batched_solve(Ps, R0->device, R0->sms, S, &R0->launches)) == TL_OK)
+            rc = timed_end(R0);
         for (int r = 0; r < nruns; ++r)
             if (plans[r].corrector) std::swap(runs[r]->Tl, runs[r]->Tl_before);
     }
