@@ -602,6 +602,34 @@ def experiments2d_case():
     (OUT / "experiments2d.json").write_text(json.dumps(out, indent=1))
 
 
+def compare3d_case():
+    """runner.run_experiment on the reference's shipped compare_3d.cfg (configs/compare3d.cfg
+    restates it) with its own IN625 file: the compare summary (solve counts of both schemes)
+    plus the final fields of the multirate run; the tables go into the npz."""
+    import shutil
+    import tempfile
+    tmp = Path(tempfile.mkdtemp())
+    shutil.copy(CFG / "compare3d.cfg", tmp / "compare3d.cfg")
+    shutil.copy(REF / "lpbfsim" / "data" / "in625.mat", tmp / "in625.mat")
+    cfg = load_config(tmp / "compare3d.cfg")
+    t0 = time.perf_counter()
+    art = runner.run_experiment(cfg, tmp / "out")
+    wall = time.perf_counter() - t0
+    files = sorted(str(p.relative_to(tmp / "out")) for p in (tmp / "out").rglob("*") if p.is_file())
+    summ = {k: v for k, v in art.summary.items() if "wall" not in k and k != "speedup"}
+    final = art.log.of_kind("macro")[-1]
+    mat = cfg.material
+    np.savez_compressed(OUT / "compare3d.npz", files=json.dumps(files), summary=json.dumps(summ),
+                        counters=json.dumps(art.stats.counters), t=final.time,
+                        local=final.local.values, glob=final.global_field.values,
+                        box=np.array(final.local.mesh.box.lo), wall=wall, speedup=art.summary["speedup"],
+                        k_table=mat.conductivity_table, c_table=mat.heat_capacity_table,
+                        mat_scalars=np.array([mat.rho, mat.chi, mat.T_solidus, mat.T_liquidus, mat.S]),
+                        versions=json.dumps(VERS))
+    shutil.rmtree(tmp)
+    print(f"compare3d: {wall:.1f}s {summ} counters={art.stats.counters}")
+
+
 def consistency_case():
     """twolevel.consistency_diagnostic of the state after 2 macro steps of cfg1_m4 against
     run_reference at h = 25 um (the final frame)."""
@@ -676,6 +704,8 @@ def main():
         return
     if "--2d-experiments" in sys.argv:
         return experiments2d_case()
+    if "--compare3d" in sys.argv:
+        return compare3d_case()
     if "--vtk" in sys.argv:
         return vtk_case()
     if "--piecewise" in sys.argv:

@@ -676,11 +676,14 @@ def test_picard_step_vs_reference(name):
                             dirichlet_nodes=grid.nodes_on(P.BOTTOM), dirichlet_values=293.0)
     beam = P.LaserBeam(200.0, 0.35, 5e-5, 5e-5, 0.8)
     stats = P.RunStats()
+    stats.device_log = []
     out = P.step_backward_euler(P.FieldState(grid, z["T_old"], 0.0), float(z["dt"]), mat,
                                 P.GaussianSource(beam, tuple(z["center"])), bounds,
                                 P.SolverSettings(picard_tol=1e-8, linear_tol=1e-12, linear_solver="cg"),
                                 latent=bool(z["latent"]), stats=stats)
     assert stats.counters["picard_iterations"] == int(z["picard"])
+    # the reference's CG iterations of every Picard pass (k_vc_cg mirrors scipy's recurrences)
+    assert [k for _, k in stats.device_log] == list(z["cg_iters"])
     assert rel(out.values, z["sol"]) <= REL
     TL = mat.T_liquidus
     assert_mask(None, out.values, z["sol"], TL)
@@ -913,3 +916,36 @@ def test_snapshot_decimation_on_device():
         assert b < b_full
     n_l = full.records[0].local.mesh.n_nodes
     assert b_full - run(0)[2] >= 6 * 4 * n_l * 8          # 4 micro fields per macro step not copied
+
+
+def test_compare3d_shipped_config_vs_reference(tmp_path):
+    """The reference's shipped multi-track timing comparison (src/configs/compare_3d.cfg,
+    restated as configs/compare3d.cfg): compare mode, IN625 tables with latent heat,
+    convection + radiation, 10 alternating tracks with a moving local box, the reference's
+    default DIRECT linear solver (fem.py:277-281), which the device serves with CG at rtol
+    1e-14.  Same output files, solve counts of both schemes and RunStats counters (1765
+    Picard passes); the multirate run's final fields to 1e-9 with bit-exact melt masks."""
+    from paper_2110_12932_b200.experiment import run_experiment
+    z = np.load(GOLDEN / "compare3d.npz")
+    rho, chi, Ts, Tl, S = (float(v) for v in z["mat_scalars"])
+    lines = ["units K", f"rho {rho!r}", f"chi {chi!r}", f"T_solidus {Ts!r}", f"T_liquidus {Tl!r}", f"S {S!r}",
+             "[conductivity]"] + [f"{float(a)!r} {float(b)!r}" for a, b in z["k_table"]] + ["[heat_capacity]"] + \
+            [f"{float(a)!r} {float(b)!r}" for a, b in z["c_table"]]
+    (tmp_path / "in625.mat").write_text("\n".join(lines) + "\n")
+    (tmp_path / "compare3d.cfg").write_text((CONFIGS / "compare3d.cfg").read_text())
+    cfg = P.load_config(tmp_path / "compare3d.cfg")
+    assert cfg.solver.linear_solver == "direct"
+    out = tmp_path / "out"
+    art = run_experiment(cfg, out)
+    files = sorted(str(p.relative_to(out)) for p in out.rglob("*") if p.is_file())
+    assert files == json.loads(str(z["files"]))
+    for k, v in json.loads(str(z["summary"])).items():
+        assert art.summary[k] == v, k
+    assert art.stats.counters == json.loads(str(z["counters"]))
+    final = art.log.of_kind("macro")[-1]
+    assert final.time == float(z["t"])
+    np.testing.assert_array_equal(final.local.mesh.box.lo, z["box"])
+    assert rel(final.local.values, z["local"]) <= REL and rel(final.global_field.values, z["glob"]) <= REL
+    TL = cfg.material.T_liquidus
+    assert_mask(None, final.local.values, z["local"], TL)
+    assert_mask(None, final.global_field.values, z["glob"], TL)
