@@ -8,6 +8,7 @@ cfg2 first 2 macro steps).
 """
 
 import json
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -308,3 +309,42 @@ def test_strict_paper_constant():
     constant replaces the configured one."""
     assert P.load_config(CONFIGS / "cfg1_tdep.cfg", strict_paper=True).bc.sigma_sb == 5.87e-8
     assert P.load_config(CONFIGS / "cfg1_tdep.cfg").bc.sigma_sb == 5.670374419e-8
+
+
+@pytest.mark.skipif(not Path("/root/reference/pkg/src/lpbfsim").exists(),
+                    reason="the reference package is only present in the build container")
+@pytest.mark.parametrize("name", ["cfg1_m4", "cfg2", "cfg1_twoway", "cfg1_tdep"])
+def test_reference_experiment_config_through_convert_config(name):
+    """the reference's own ExperimentConfig (lpbfsim.config.load_config) goes
+    through runner.convert_config / build_problem (lpbfsim/runner.py:51-113) and gives the same
+    device problem as this package's loader: grids, materials, beam, BCs, path, policy,
+    solver and coupling settings, schedule."""
+    import sys
+    sys.path.insert(0, "/root/reference/pkg/src")
+    try:
+        from lpbfsim.config import load_config as ref_load
+    finally:
+        sys.path.pop(0)
+    from paper_2110_12932_b200.runner import convert_config
+    ref_cfg = ref_load(CONFIGS / f"{name}.cfg")
+    a, b = convert_config(ref_cfg), convert_config(P.load_config(CONFIGS / f"{name}.cfg"))
+    assert a.keys() == b.keys()
+    for k in a:
+        va, vb = a[k], b[k]
+        if k in ("material", "material_local"):
+            np.testing.assert_array_equal(va.conductivity_table, vb.conductivity_table)
+            np.testing.assert_array_equal(va.heat_capacity_table, vb.heat_capacity_table)
+            assert (va.rho, va.chi, va.T_solidus, va.T_liquidus, va.S) == (vb.rho, vb.chi, vb.T_solidus, vb.T_liquidus, vb.S)
+        elif k == "path":
+            assert [(s.start, s.end, s.speed, s.t_start) for s in va.segments] == \
+                   [(s.start, s.end, s.speed, s.t_start) for s in vb.segments]
+        elif k == "policy":
+            assert (va is None) == (vb is None)
+            if va is not None:
+                assert (tuple(va.box_size), va.laser_fraction) == (tuple(vb.box_size), vb.laser_fraction)
+        else:
+            assert va == vb, k
+    pa, la = P.build_problem(ref_cfg)
+    pb, lb = P.build_problem(P.load_config(CONFIGS / f"{name}.cfg"))
+    assert pa.global_mesh.same_lattice(pb.global_mesh) and la.same_lattice(lb)
+    assert (pa.one_way, pa.interval_source, pa.mode) == (pb.one_way, pb.interval_source, pb.mode)
