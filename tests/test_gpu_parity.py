@@ -416,13 +416,17 @@ np.savez({out!r}, g=state.global_field.values, l=state.local_field.values,
                                  {"TLGPU_STREAMING": "1", "TLGPU_TILED": "0"},
                                  {"TLGPU_STREAMING": "1", "TLGPU_TILED_MIN": "1", "TLGPU_BOXLOAD": "0",
                                   "TLGPU_SNAKE": "0"},
-                                 {"TLGPU_STREAMING": "1", "TLGPU_TILED": "0", "TLGPU_SNAKE": "0"}])
+                                 {"TLGPU_STREAMING": "1", "TLGPU_TILED": "0", "TLGPU_SNAKE": "0"},
+                                 {"TLGPU_STREAMING": "1", "TLGPU_TILED_MIN": "1", "TLGPU_TH": "2", "TLGPU_NCW": "19"},
+                                 {"TLGPU_STREAMING": "1", "TLGPU_TILED_MIN": "1", "TLGPU_TH": "12", "TLGPU_NCW": "16",
+                                  "TLGPU_TC": "3"}])
 def test_alternative_solver_modes_match_default(env, tmp_path):
     """The non-default device paths (one launch per local solve; no setup cache and
     cg::grid.sync barriers; scipy-exact two-barrier kernel; every solve on the streaming
     path, with the bulk-copy z-march CG loop k_t_cg or the flat k_s_cg, on grids small
     enough that boundary nodes dominate; the same with per-solve full-grid Gaussian loads
-    and both sweeps bottom-up) give the default run's fields
+    and both sweeps bottom-up; the one-node-per-thread kernel variant with 19 consumer warps
+    and a 12-row, 3-chunk item plan with 16) give the default run's fields
     to CG rounding with the same counters (env switches are read once per process, so
     each mode runs in a subprocess)."""
     import os
@@ -538,7 +542,8 @@ print("repeatable", first[2], first[3])
 """
 
 
-@pytest.mark.parametrize("env", [{}, {"TLGPU_TILED": "0"}, {"TLGPU_SNAKE": "0", "TLGPU_TH": "2", "TLGPU_TC": "9"}])
+@pytest.mark.parametrize("env", [{}, {"TLGPU_TILED": "0"}, {"TLGPU_SNAKE": "0", "TLGPU_TH": "2", "TLGPU_TC": "9"},
+                                 {"TLGPU_NCW": "19", "TLGPU_TH": "2"}])
 def test_streaming_paths_bitwise_repeatable(env):
     """Race stress of the hand-rolled synchronisation (compute-sanitizer is closed on this
     GPU pool): the bulk-copy z-march CG loop (mbarrier ring, dynamic item counter, per-item
@@ -553,6 +558,40 @@ def test_streaming_paths_bitwise_repeatable(env):
                          timeout=900)
     assert res.returncode == 0, res.stderr[-2000:]
     assert "repeatable" in res.stdout
+
+
+def test_tiled_cg_loop_wide_grid_vs_oracle(tmp_path):
+    """A grid wider than two consumer slots (NX = 1301 > 2 x 608): k_t_cg's general plane
+    loops with four nodes per thread (no lean path), one bottom-Dirichlet step with a
+    deposit-like load against the oracle."""
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import paper_2110_12932_b200 as P
+from paper_2110_12932_b200 import _native as N, ops
+grid = P.build_structured_grid(P.Box((0.0, 0.0, 0.0), (2.6e-2, 1.6e-4, 1.6e-4)), 2e-5)
+rng = np.random.default_rng(2)
+T = rng.uniform(293.0, 2293.0, grid.n_nodes)
+load = rng.uniform(0.0, 1e-6, grid.n_nodes)
+x, info = ops.step(grid, 9.8, 8440 * 410.0, 2e-5, N.TL_DIRICHLET_BOTTOM, T, g_const=293.0, load=load, rtol=1e-12)
+np.savez({out!r}, x=x, T=T, load=load, its=info.iterations, status=info.status, shape=np.array(grid.shape))
+"""
+    out = tmp_path / "wide.npz"
+    res = subprocess.run([sys.executable, "-c", code.format(root=str(ROOT), out=str(out))],
+                         env={**os.environ, "TLGPU_STREAMING": "1", "TLGPU_TILED_MIN": "1", "TLGPU_VERBOSE": "1"},
+                         capture_output=True,
+                         text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    assert "item plan 1301x9x" in res.stderr, res.stderr[-500:]
+    z = np.load(out)
+    grid = P.build_structured_grid(P.Box((0.0, 0.0, 0.0), (2.6e-2, 1.6e-4, 1.6e-4)), 2e-5)
+    assert tuple(z["shape"]) == grid.shape == (9, 9, 1301)
+    ref, its = _oracle_step(grid, N.TL_DIRICHLET_BOTTOM, z["T"], 2e-5, np.full(grid.n_nodes, 293.0), load=z["load"])
+    assert int(z["status"]) == 0 and abs(int(z["its"]) - its) <= 1
+    assert rel(z["x"], ref) <= 1e-12
 
 
 def test_monolithic_reference_vs_reference_golden():
