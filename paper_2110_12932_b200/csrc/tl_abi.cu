@@ -716,6 +716,8 @@ struct tl_run {
     double* melt = nullptr; double* melt_part = nullptr; double* melt_host = nullptr;
     double* snap_g = nullptr; std::vector<double*> snap_l; int snap_n = 0;
     double* xg = nullptr;            // exchange array of the resident kernels (4 n)
+    void* batch_dev = nullptr;       // batched solves led by this run: parameter buffer, sweep counters
+    unsigned* batch_ctr = nullptr;
     tl::SolveSpec* d_specs = nullptr; int specs_cap = 0;
     ResCache cache_g, cache_l;       // resident-kernel setup caches (global / local grid)
     // asynchronous field read-back (tl_run_field_async): staging copies + copy stream
@@ -1501,6 +1503,8 @@ int32_t tl_run_destroy(tl_run* R) {
     if (R->info) cudaFree(R->info);
     if (R->d_specs) cudaFree(R->d_specs);
     if (R->d_srcs) cudaFree(R->d_srcs);
+    if (R->batch_dev) cudaFree(R->batch_dev);
+    if (R->batch_ctr) cudaFree(R->batch_ctr);
     if (R->snap_g) cudaFree(R->snap_g);
     for (cudaEvent_t e : R->ev) cudaEventDestroy(e);
     for (double* b : R->snap_l) cudaFree(b);
@@ -1898,10 +1902,7 @@ int32_t tl_run_macro_steps(tl_run* R, const tl_macro_plan* plans, int32_t nsteps
 // per run, the i-th micro solve (and the corrector) of ALL runs is one batched solve
 // (k_sb_rhs -> k_tb_cg -> k_sb_resid -> k_sb_final, tl_tiled.cuh).  Everything is enqueued
 // on the first run's stream; the other runs' streams are ordered before and after it.
-static tl::PcgParams* g_batch_dev[64] = {nullptr};
-static unsigned* g_batch_ctr[64] = {nullptr};
-
-static int batched_solve(std::vector<tl::PcgParams>& Ps, int dev, int sms, cudaStream_t st, int64_t* launches) {
+static int batched_solve(std::vector<tl::PcgParams>& Ps, tl_run* R0, int sms, cudaStream_t st, int64_t* launches) {
     const int B = (int)Ps.size();
     if (B == 0) return TL_OK;
     if (B > tl::kTBMax) return fail(TL_E_INVALID, "too many systems in one batched solve");
@@ -1910,11 +1911,12 @@ static int batched_solve(std::vector<tl::PcgParams>& Ps, int dev, int sms, cudaS
     if (!tiled_plan_range(Ps[0].g, sms, 0, Ps[0].g.NZ, tp, smem, B)) return fail(TL_E_INVALID, "no item plan for the batch");
     if ((long long)tp.I * B > 2000000000ll / 4) return fail(TL_E_INVALID, "batch too large");
     tp.iid.init((uint32_t)tp.I);
-    if (!g_batch_dev[dev]) {
-        TL_CUDA(cudaMalloc((void**)&g_batch_dev[dev], sizeof(tl::PcgParams) * tl::kTBMax));
-        TL_CUDA(cudaMalloc((void**)&g_batch_ctr[dev], 4 * sizeof(unsigned)));
+    // the parameter buffer belongs to the first run: ordered by its stream
+    if (!R0->batch_dev) {
+        TL_CUDA(cudaMalloc((void**)&R0->batch_dev, sizeof(tl::PcgParams) * tl::kTBMax));
+        TL_CUDA(cudaMalloc((void**)&R0->batch_ctr, 4 * sizeof(unsigned)));
     }
-    tl::PcgParams* dPs = g_batch_dev[dev];
+    tl::PcgParams* dPs = static_cast<tl::PcgParams*>(R0->batch_dev);
     for (auto& P : Ps) {
         P.light_rhs = 1;
         P.snake = snake_enabled();
@@ -1937,14 +1939,14 @@ static int batched_solve(std::vector<tl::PcgParams>& Ps, int dev, int sms, cudaS
     const int Gq = std::min(perq, (Ps[0].g.n + tl::kSTPB - 1) / tl::kSTPB);
     tl::k_sb_rhs<<<dim3(Gr, B), tl::kSTPB, 0, st>>>(dPs);
     TL_CUDA(cudaGetLastError());
-    TL_CUDA(cudaMemsetAsync(g_batch_ctr[dev], 0, 4 * sizeof(unsigned), st));
+    TL_CUDA(cudaMemsetAsync(R0->batch_ctr, 0, 4 * sizeof(unsigned), st));
     const int nodes = tp.H * Ps[0].g.NX;
     const int npt = nodes <= tp.ncw * 32 ? 1 : (nodes <= 2 * tp.ncw * 32 ? 2 : 4);
     auto kern = tp.ncw == 16 ? (npt == 1 ? tl::k_tb_cg<16, 1> : npt == 2 ? tl::k_tb_cg<16, 2> : tl::k_tb_cg<16, 4>)
                              : (npt == 1 ? tl::k_tb_cg<19, 1> : npt == 2 ? tl::k_tb_cg<19, 2> : tl::k_tb_cg<19, 4>);
     TL_CUDA(ensure_smem_attr((const void*)kern, smem));
     int Bv = B, Grv = Gr;
-    unsigned* ctr = g_batch_ctr[dev];
+    unsigned* ctr = R0->batch_ctr;
     void* args[] = {&dPs, &Bv, &Grv, (void*)&tp, &ctr};
     TL_CUDA(cudaLaunchCooperativeKernel((void*)kern, sms, (tp.ncw + 1) * 32, args, smem, st));
     tl::k_sb_resid<<<dim3(Gq, B), tl::kSTPB, 0, st>>>(dPs);
@@ -2036,7 +2038,7 @@ int32_t tl_runs_macro_step(tl_run** runs, int32_t nruns, const tl_macro_plan* pl
             P.info = R->info + R->info_n++;
             Ps.push_back(P);
         }
-        if ((rc = timed_begin(R0, 0, nruns)) == TL_OK && (rc = batched_solve(Ps, R0->device, R0->sms, S, &R0->launches)) == TL_OK)
+        if ((rc = timed_begin(R0, 0, nruns)) == TL_OK && (rc = batched_solve(Ps, R0, R0->sms, S, &R0->launches)) == TL_OK)
             rc = timed_end(R0);
     } else if (rc == TL_OK) {
         for (int r = 0; r < nruns && rc == TL_OK; ++r) {      // global grids differ: one solve per run
@@ -2071,7 +2073,7 @@ int32_t tl_runs_macro_step(tl_run** runs, int32_t nruns, const tl_macro_plan* pl
             Ps.push_back(P);
         }
         if ((rc = timed_begin(R0, 1, (int)Ps.size())) == TL_OK &&
-            (rc = batched_solve(Ps, R0->device, R0->sms, S, &R0->launches)) == TL_OK)
+            (rc = batched_solve(Ps, R0, R0->sms, S, &R0->launches)) == TL_OK)
             rc = timed_end(R0);
     }
     if (rc == TL_OK) {                      // correctors: the last micro interval again, from before_final
@@ -2085,7 +2087,7 @@ int32_t tl_runs_macro_step(tl_run** runs, int32_t nruns, const tl_macro_plan* pl
             Ps.push_back(P);
         }
         if (!Ps.empty() && (rc = timed_begin(R0, 1, (int)Ps.size())) == TL_OK &&
-            (rc = batched_solve(Ps, R0->device, R0->sms, S, &R0->launches)) == TL_OK)
+            (rc = batched_solve(Ps, R0, R0->sms, S, &R0->launches)) == TL_OK)
             rc = timed_end(R0);
         for (int r = 0; r < nruns; ++r)
             if (plans[r].corrector) std::swap(runs[r]->Tl, runs[r]->Tl_before);
