@@ -299,6 +299,10 @@ int32_t tl_run_get_snapshot(tl_run* run, int32_t which, int32_t index, double* h
 int32_t tl_run_sync(tl_run* run);
 /* which: 0 = global field, 1 = local field, 2 = trace (dense local array). */
 int32_t tl_run_get_field(tl_run* run, int32_t which, double* host, int64_t n);
+/* Selected entries of a field (which as above): host[e] = field[idx[e]], gathered on the device
+ * so that only n values cross to the host (the interface trace of a run's final state,
+ * InterfaceGamma.trace_nodes, mesh.py:507: ~2.6 % of the dense local array). */
+int32_t tl_run_get_field_at(tl_run* run, int32_t which, const int32_t* idx, int64_t n, double* host);
 /* Asynchronous read-back for pipelined callers (a recorder or a viewer consuming every
  * macro step while the next one computes).  Enqueues, in the run's stream order, a
  * device copy of the field into staging slot `slot` (0..3), then its transfer to `host`

@@ -144,6 +144,7 @@ SIGNATURES = [
     ("tl_run_get_snapshot", C.c_int32, [_P, C.c_int32, C.c_int32, _dp, C.c_int64]),
     ("tl_run_sync", C.c_int32, [_P]),
     ("tl_run_get_field", C.c_int32, [_P, C.c_int32, _dp, C.c_int64]),
+    ("tl_run_get_field_at", C.c_int32, [_P, C.c_int32, _P, C.c_int64, _dp]),
     ("tl_run_field_async", C.c_int32, [_P, C.c_int32, _dp, C.c_int64, C.c_int32]),
     ("tl_run_field_wait", C.c_int32, [_P, C.c_int32]),
     ("tl_run_take_info", C.c_int32, [_P, C.POINTER(SolveInfo), C.c_int32, C.POINTER(C.c_int32)]),

@@ -716,6 +716,7 @@ struct tl_run {
     double* melt = nullptr; double* melt_part = nullptr; double* melt_host = nullptr;
     double* snap_g = nullptr; std::vector<double*> snap_l; int snap_n = 0;
     double* xg = nullptr;            // exchange array of the resident kernels (4 n)
+    void* gather_buf = nullptr; size_t gather_cap = 0;     // tl_run_get_field_at scratch
     void* batch_dev = nullptr;       // batched solves led by this run: parameter buffer, sweep counters
     unsigned* batch_ctr = nullptr;
     tl::SolveSpec* d_specs = nullptr; int specs_cap = 0;
@@ -1503,6 +1504,7 @@ int32_t tl_run_destroy(tl_run* R) {
     if (R->info) cudaFree(R->info);
     if (R->d_specs) cudaFree(R->d_specs);
     if (R->d_srcs) cudaFree(R->d_srcs);
+    if (R->gather_buf) cudaFree(R->gather_buf);
     if (R->batch_dev) cudaFree(R->batch_dev);
     if (R->batch_ctr) cudaFree(R->batch_ctr);
     if (R->snap_g) cudaFree(R->snap_g);
@@ -2125,6 +2127,31 @@ int32_t tl_run_get_field(tl_run* R, int32_t which, double* host, int64_t n) {
     if (which < 0 || which > 2 || n != want) return fail(TL_E_INVALID, "field selector or size mismatch");
     if (which == 0 && R->external_global) return fail(TL_E_INVALID, "external-global run holds no global field");
     TL_CUDA(cudaMemcpyAsync(host, src, sizeof(double) * n, cudaMemcpyDeviceToHost, R->stream));
+    TL_CUDA(cudaStreamSynchronize(R->stream));
+    return TL_OK;
+}
+
+int32_t tl_run_get_field_at(tl_run* R, int32_t which, const int32_t* idx, int64_t n, double* host) {
+    if (!R || !host || (!idx && n > 0) || n < 0) return fail(TL_E_INVALID, "bad argument");
+    TL_CUDA(cudaSetDevice(R->device));
+    const double* src = which == 0 ? R->Tg : (which == 1 ? R->Tl : R->tr_old);
+    if (which < 0 || which > 2) return fail(TL_E_INVALID, "field selector");
+    if (which == 0 && R->external_global) return fail(TL_E_INVALID, "external-global run holds no global field");
+    if (n == 0) return TL_OK;
+    const size_t need = (size_t)n * (sizeof(int) + sizeof(double)) + 16;
+    if (need > R->gather_cap) {
+        if (R->gather_buf) cudaFree(R->gather_buf);
+        R->gather_buf = nullptr;
+        R->gather_cap = 0;
+        TL_CUDA(cudaMalloc(&R->gather_buf, need));
+        R->gather_cap = need;
+    }
+    double* dval = static_cast<double*>(R->gather_buf);
+    int* didx = reinterpret_cast<int*>(dval + n);
+    TL_CUDA(cudaMemcpyAsync(didx, idx, sizeof(int) * n, cudaMemcpyHostToDevice, R->stream));
+    tl::k_gather<<<(int)std::min<int64_t>((n + 255) / 256, 4 * R->sms), 256, 0, R->stream>>>(src, didx, (int)n, dval);
+    TL_CUDA(cudaGetLastError());
+    TL_CUDA(cudaMemcpyAsync(host, dval, sizeof(double) * n, cudaMemcpyDeviceToHost, R->stream));
     TL_CUDA(cudaStreamSynchronize(R->stream));
     return TL_OK;
 }

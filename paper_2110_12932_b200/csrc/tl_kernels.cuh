@@ -1055,6 +1055,11 @@ __global__ void k_copy(const double* __restrict__ a, double* __restrict__ b, int
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) b[e] = a[e];
 }
 
+// dst[e] = src[idx[e]] (the trace entries of a dense local array: tl_run_get_field_at)
+__global__ void k_gather(const double* __restrict__ src, const int* __restrict__ idx, int n, double* __restrict__ dst) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) dst[e] = src[idx[e]];
+}
+
 __global__ void k_fill(double* a, int n, double v) {
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) a[e] = v;
 }

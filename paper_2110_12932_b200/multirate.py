@@ -140,6 +140,16 @@ class DeviceRun:
         self.d2h_bytes += out.nbytes
         return out
 
+    def field_at(self, which: int, nodes: np.ndarray) -> np.ndarray:
+        """Selected entries of a field, gathered on the device (only len(nodes) values cross)."""
+        idx = np.ascontiguousarray(nodes, dtype=np.int32)
+        out = np.empty(len(idx))
+        N.check(N.lib().tl_run_get_field_at(self._h, which, idx.ctypes.data_as(C.c_void_p), len(idx), N.dptr(out)),
+                "tl_run_get_field_at")
+        self.d2h_bytes += out.nbytes
+        self.h2d_bytes += idx.nbytes
+        return out
+
     def field_async(self, which: int, out: np.ndarray, slot: int = 0) -> None:
         """Enqueue the read-back of a field into `out` (pinned memory for full overlap)
         and return at once; the run may continue.  Complete with field_wait(slot)."""
@@ -410,12 +420,12 @@ def _drive(problem, run: DeviceRun, plan_fn, local_mesh, T0, stats, recorder, t_
     if stats is not None:
         stats.seconds["device_run"] = stats.seconds.get("device_run", 0.0) + time.perf_counter() - t0
     final_local = StructuredGrid(placement)
-    lv = run.field(1)
     gamma = extract_interface(final_local, gmesh)
-    trace = run.field(2)[gamma.trace_nodes]
-    # the global field stays on the device until the caller reads it
+    trace = run.field_at(2, gamma.trace_nodes)          # gathered on the device: only the trace crosses
+    # both fields stay on the device until the caller reads them
     gfield = run.lazy_field(0, gmesh, tg)
-    return TwoLevelState(gfield, FieldState(final_local, lv, tl), gamma, trace), last_plan
+    lfield = run.lazy_field(1, final_local, tl)
+    return TwoLevelState(gfield, lfield, gamma, trace), last_plan
 
 
 def _decimate(plan: Plan, recorder):

@@ -62,7 +62,7 @@ class InterfaceGamma:
 def extract_interface(local: StructuredGrid, global_mesh: StructuredGrid) -> InterfaceGamma:
     """``extract_interface`` node part (``mesh.py:477-523``) with its immersion checks."""
     check_immersed(local.box, global_mesh.box, global_mesh.h)
-    return InterfaceGamma(local, np.nonzero(local.gamma_mask())[0])
+    return InterfaceGamma(local, local.gamma_nodes())
 
 
 @dataclass(frozen=True)
