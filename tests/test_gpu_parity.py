@@ -328,6 +328,24 @@ def test_streaming_local_step_cfg3_size_vs_oracle():
     assert rel(x, ref) <= 1e-12
 
 
+def test_streaming_local_step_cfg4_size_vs_oracle():
+    """cfg4 local grid (251 x 251 x 101 = 6.36M nodes, 37 % of the headline step: k_t_cg with
+    4-row items, gamma Dirichlet data, Gaussian load) vs the oracle: one micro step."""
+    cfg = P.load_config(CONFIGS / "cfg4.cfg")
+    problem, lm = P.build_problem(cfg)
+    assert lm.n_nodes == 6363101
+    rng = np.random.default_rng(3)
+    T = rng.uniform(293.0, 2293.0, lm.n_nodes)
+    g = np.where(lm.gamma_mask(), rng.uniform(293.0, 900.0, lm.n_nodes), 0.0)
+    src = problem.local_source(2e-6)
+    dt = cfg.dt_macro / cfg.micro_steps
+    x, info = ops.step(lm, 9.8, 8440 * 410.0, dt, N.TL_DIRICHLET_GAMMA, T, g=g,
+                       gaussian=src.device_args(), rtol=1e-12)
+    ref, its = _oracle_step(lm, N.TL_DIRICHLET_GAMMA, T, dt, g, gauss=(cfg.beam, src.center))
+    assert info.status == 0 and abs(info.iterations - its) <= 1
+    assert rel(x, ref) <= 1e-12
+
+
 def test_cfg3_three_macro_steps_vs_oracle():
     """cfg3 (6.9M-node global grid on the streaming solve, 1.7M-node local grid, m = 10):
     3 macro steps with a relocation after each but the last, against OracleRun: every
