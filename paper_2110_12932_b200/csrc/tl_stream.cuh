@@ -66,47 +66,45 @@ __device__ __forceinline__ bool s_free_interior(const Grid& g, int i, int j, int
            (g.dkind != kGamma || (i >= 2 && i <= g.nc[0] - 2 && j >= 2 && j <= g.nc[1] - 2));
 }
 
-// RHS at node p (fem.py:129-194 + constrained, 89-105): b written (and r = b, x = 0 unless
-// the k_t_cg path implies them); accumulates b.b and b.z.
-__device__ __forceinline__ void s_rhs_node(const PcgParams& P, const ClassTable& T, const int* box, int p,
-                                           double* __restrict__ b, double* __restrict__ r,
-                                           double* __restrict__ x, const double* __restrict__ load,
-                                           double (&acc)[2]) {
+// RHS value at node p = (i, j, k) from its T_old and dense-load values (fem.py:129-194 +
+// constrained, 89-105); cls returns the node's class.
+__device__ __forceinline__ double s_rhs_value(const PcgParams& P, const ClassTable& T, const int* box, int p, int i,
+                                              int j, int k, double told, double loadv, int& cls) {
     const Grid& g = P.g;
-    int i, j, k;
-    decode(g, p, i, j, k);
     // the precomputed Gaussian load of the node (0 outside the box; Dirichlet nodes hold 0)
     auto boxload = [&]() -> double {
         if (i < box[0] || i >= box[1] || j < box[2] || j >= box[3] || k < box[4] || k >= box[5]) return 0.0;
         return P.bload[(i - box[0]) + (box[1] - box[0]) * ((j - box[2]) + (box[3] - box[2]) * (k - box[4]))];
     };
     double bv;
-    int cls = 13;
+    cls = 13;
     if (s_free_interior(g, i, j, k)) {
-        bv = T.mass[13] * x[p];
-        if (load) bv += load[p];
+        bv = T.mass[13] * told;
+        if (P.load) bv += loadv;
         if (P.bload) bv += boxload();
     } else {
         cls = class_of(g, i, j, k);
         if (T.nd[cls] == 0.0) {
             bv = dirichlet_value(P, p);
         } else {
-            bv = T.mass[cls] * x[p];
-            if (load) bv += load[p];
+            bv = T.mass[cls] * told;
+            if (P.load) bv += loadv;
             if (P.bload) bv += boxload();
             bv += dirichlet_lift(P, T, p, i, j, k, cls);
         }
     }
-    b[p] = bv;
-    if (!P.light_rhs) {
-        r[p] = bv;
-        x[p] = 0.0;
-    }
-    acc[0] += bv * bv;
-    acc[1] += bv * __dmul_rn(T.invd[cls], bv);
+    return bv;
 }
 
-// ---- k_s_rhs: b, r = b, x = 0; partials [0][blk] = b.b, [1][blk] = r.z ----------------
+__device__ __forceinline__ double2 ld2(const double* a) { return *reinterpret_cast<const double2*>(a); }
+__device__ __forceinline__ void st2(double* a, double v0, double v1) {
+    *reinterpret_cast<double2*>(a) = make_double2(v0, v1);
+}
+
+// ---- k_s_rhs: b (and r = b, x = 0 unless the k_t_cg path implies them); partials
+// [0][blk] = b.b, [1][blk] = r.z.  A thread takes the node pairs (2q, 2q + 1) of a grid-
+// stride loop with 16-byte loads and stores (the arrays are 16-byte aligned and padded):
+// half the memory instructions of a node-per-trip loop, twice the bytes in flight per thread.
 __device__ __forceinline__ void s_rhs_block(const PcgParams& P) {
     __shared__ ClassTable T;
     __shared__ double red[2 * 32];
@@ -116,13 +114,42 @@ __device__ __forceinline__ void s_rhs_block(const PcgParams& P) {
     if (threadIdx.x >= 32 && threadIdx.x < 38) box[threadIdx.x - 32] = P.bload ? P.bbox[threadIdx.x - 32] : 0;
     __syncthreads();
     double acc[2] = {0.0, 0.0};
-    const int stride = gridDim.x * blockDim.x;
-    int p = blockIdx.x * blockDim.x + threadIdx.x;
-    for (; p + stride < g.n; p += 2 * stride) {
-        s_rhs_node(P, T, box, p, P.b, P.r, P.T, P.load, acc);
-        s_rhs_node(P, T, box, p + stride, P.b, P.r, P.T, P.load, acc);
+    // (the dense load may sit at an odd offset of a workspace: 8-byte loads then)
+    const bool lal = (reinterpret_cast<uintptr_t>(P.load) & 15) == 0;
+    const int npair = g.n >> 1;
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < npair; q += gridDim.x * blockDim.x) {
+        const int p = 2 * q;
+        const double2 tv = ld2(P.T + p);
+        const double2 lv = !P.load ? make_double2(0.0, 0.0)
+                           : (lal ? ld2(P.load + p) : make_double2(P.load[p], P.load[p + 1]));
+        int i, j, k, c0, c1;
+        decode(g, p, i, j, k);
+        const double b0 = s_rhs_value(P, T, box, p, i, j, k, tv.x, lv.x, c0);
+        if (++i == g.NX) decode(g, p + 1, i, j, k);          // the pair straddles a row end
+        const double b1 = s_rhs_value(P, T, box, p + 1, i, j, k, tv.y, lv.y, c1);
+        st2(P.b + p, b0, b1);
+        if (!P.light_rhs) {
+            st2(P.r + p, b0, b1);
+            st2(P.T + p, 0.0, 0.0);
+        }
+        acc[0] += b0 * b0;
+        acc[1] += b0 * __dmul_rn(T.invd[c0], b0);
+        acc[0] += b1 * b1;
+        acc[1] += b1 * __dmul_rn(T.invd[c1], b1);
     }
-    if (p < g.n) s_rhs_node(P, T, box, p, P.b, P.r, P.T, P.load, acc);
+    if ((g.n & 1) && blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {      // the odd last node
+        const int p = g.n - 1;
+        int i, j, k, c0;
+        decode(g, p, i, j, k);
+        const double b0 = s_rhs_value(P, T, box, p, i, j, k, P.T[p], P.load ? P.load[p] : 0.0, c0);
+        P.b[p] = b0;
+        if (!P.light_rhs) {
+            P.r[p] = b0;
+            P.T[p] = 0.0;
+        }
+        acc[0] += b0 * b0;
+        acc[1] += b0 * __dmul_rn(T.invd[c0], b0);
+    }
     block_sum<2>(acc, red);
     if (threadIdx.x == 0) {
         P.part[blockIdx.x] = acc[0];
