@@ -208,11 +208,11 @@ static bool tiled_plan(const tl::Grid& g, int sms, tl::TPlan& tp, size_t& smem) 
 //
 // An item is H full x-rows by one z chunk.  The plan minimises a cost model fitted to
 // sweeps of the BASELINE grids (tools/tune_snake.sh, tools/sweep_profile.py):
-//   cost(H, C) = waves * (Z + 2) * plane,   waves = ceil(NB * C / CTAs),  Z = ceil(planes / C)
+//   cost(H, C) = waves * (Z + o) * plane,   waves = ceil(NB * C / CTAs),  Z = planes / C,  o = 2 or 0.5
 //   plane      = max(512 * ceil(H NX / 512), H NX (1 + 0.6 / H))
 // - items are taken dynamically but are all about the same size, so a sweep lasts `waves`
 //   items per CTA: balance (items a multiple of the CTA count) dominates;
-// - an item costs about 2 planes beyond its own (halo plane, pipeline fill, reduction, tail);
+// - an item costs o planes beyond its own (halo plane, pipeline fill, reduction, tail: see below);
 // - a plane costs its consumer slots (512 threads take one node each per slot) or its ring
 //   traffic including the halo rows, whichever is larger.
 // A batched solve (k_tb_cg) sweeps nsys systems of this shape together: its item count is
@@ -234,6 +234,12 @@ static bool tiled_plan_range(const tl::Grid& g, int sms, int zlo, int zhi, tl::T
     auto stages_of = [&](int H) { return (int)std::min<size_t>(tl::kTMaxStages, cap / ((size_t)stage_of(H) * 8)); };
     int zmin = 2;
     if (const char* e = getenv("TLGPU_TZ")) zmin = std::max(1, atoi(e));
+    // what an item costs beyond its own planes, in planes: ~2 on grids of a few L2 sizes
+    // (halo planes, pipeline fill and drain show with 1-4 items per CTA), ~0.5 on sweeps
+    // far larger than L2 (tens of items per CTA: the producer streams the next item while
+    // the current one computes; cfg4 global: C = 5 chunks 39.1 ms, C = 1 40.0 ms, C = 13 40.0 ms)
+    const double sweep_bytes = 40.0 * (double)NX * g.NY * nzr * nsys;
+    const double item_planes = sweep_bytes > 1e9 ? 0.5 : 2.0;
     int want_ncw = 0;
     if (const char* e = getenv("TLGPU_NCW")) want_ncw = atoi(e);
     int H = 0, nch = 0, ncw = 0, Hmax = 0;
@@ -254,7 +260,7 @@ static bool tiled_plan_range(const tl::Grid& g, int sms, int zlo, int zhi, tl::T
                 const long long I = (long long)NB * c;
                 if (I > tl::kTMaxItems) break;
                 const long long waves = (I * nsys + sms - 1) / sms;     // nsys: systems of a batched solve
-                const double cost = (double)waves * (Z + 2.0) * plane;
+                const double cost = (double)waves * ((double)nzr / c + item_planes) * plane;
                 if (cost < best * (1.0 - 1e-9)) { best = cost; H = h; nch = c; ncw = nw; Hmax = hmax; }
             }
         }

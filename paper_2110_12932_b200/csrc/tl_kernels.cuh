@@ -32,7 +32,7 @@ constexpr int kTPB = 512;                  // threads per block of k_pcg
 constexpr int kMaxTab = 4096;              // Gaussian table entries per axis (cells)
 // length (doubles) of PcgParams::part: resident slots (< 4096), k_s_cg partials at 4096,
 // k_t_cg counters at 2048 and item partials at 4096 + 3 * kTMaxItems
-constexpr int kPartLen = 4096 + 3 * 7000 + 1024;
+constexpr int kPartLen = 4096 + 3 * 16384 + 1024;
 
 // 4-point tet rule (mesh.py:116-128) and the six per-axis fractional offsets a
 // Kuhn-tet quadrature point can take inside its cell: {b, 2b, 3b, a, a+b, a+2b}.

@@ -41,7 +41,7 @@ namespace tl {
 constexpr int kTMaxStages = 16;
 constexpr int kTMaxChunks = 96;            // z chunks (guided: large first, small last)
 constexpr int kTPartItems = 4096;          // offset of the item partials in PcgParams::part
-constexpr int kTMaxItems = 7000;           // sweep A: slot 0, sweep B: slots 1, 2 (3 * kTMaxItems)
+constexpr int kTMaxItems = 16384;          // sweep A: slot 0, sweep B: slots 1, 2 (3 * kTMaxItems)
 constexpr int kTCounter = 2048;            // offset (in doubles) of the 4 sweep counters
 
 struct TPlan {
