@@ -715,11 +715,12 @@ def picard_bench(args):
     """--config picard: SURVEY §8f row 1 on a cfg2-local-sized grid (101 x 101 x 51 nodes,
     h = 5 um): temperature-dependent implicit steps (configs/tdep.mat: kappa(T), c(T),
     latent heat; convection + lagged radiation on the top face; moving Gaussian beam;
-    bottom Dirichlet) through the public seam fem.step_backward_euler, host buffers in and
-    out.  One step = one Picard-converged implicit step: one tl_vc_picard_host call whose
+    bottom Dirichlet) through the public seam fem.step_backward_euler, the field left on the
+    device between steps.  One step = one Picard-converged implicit step: one
+    tl_vc_picard_nodes_host call whose
     passes (assembly + one cooperative Jacobi-PCG launch + the increment reduction) run on
-    the device.  value and e2e are the
-    host wall clock around the public call (the seam takes host arrays); the roofline is
+    the device.  value is the host wall clock around the public call, e2e the same with the
+    field read back after every step; the roofline is
     the PCG launch timed with CUDA events: N (96 k + 32) algorithmic bytes per pass
     (SURVEY §8d's 64 B/node/iteration plus the 4 per-node coefficient arrays)."""
     import torch
@@ -754,15 +755,27 @@ def picard_bench(args):
 
     for k in range(args.warmup):
         state = step(state, k, None)
+    from paper_2110_12932_b200 import _native as N
     stats = P.RunStats()
     stats.device_log = []
     walls = []
+    N.host_traffic(reset=True)
     with ClockSampler(local_rank) as clocks:
         for k in range(args.warmup, args.warmup + args.steps):
             t0 = time.perf_counter()
             state = step(state, k, stats)
             walls.append(time.perf_counter() - t0)
     wall = sum(walls)
+    dev_h2d, dev_d2h = N.host_traffic(reset=True)
+    # e2e: the same steps with the converged field read back to the host after every step
+    e2e_walls = []
+    for k in range(args.warmup + args.steps, args.warmup + 2 * args.steps):
+        t0 = time.perf_counter()
+        state = step(state, k, None)
+        _ = state.values
+        e2e_walls.append(time.perf_counter() - t0)
+    e2e_wall = sum(e2e_walls)
+    e2e_h2d, e2e_d2h = N.host_traffic(reset=True)
     passes = stats.counters.get("picard_iterations", 0)
     cg_ms = sum(ms for ms, _ in stats.device_log)
     its = [it for _, it in stats.device_log]
@@ -792,7 +805,8 @@ def picard_bench(args):
                                f"nodes (cfg2 local grid), Picard loop over device passes",
                    "picard_passes_per_step": passes / args.steps,
                    "cg_iterations_per_pass": float(np.mean(its)) if its else None,
-                   "l2": "not flushed (host-buffer seam: each step uploads its fields and reads the result back)",
+                   "l2": "not flushed (step-level seam: the field goes from step to step on the device)",
+                   "pcie_bytes_per_step": {"h2d": dev_h2d // args.steps, "d2h": dev_d2h // args.steps},
                    "parallelism": "single GPU"},
         "roofline": {"bound": "hbm", "achieved": alg / (cg_ms / 1e3) / 1e9 if cg_ms else None, "peak": peak,
                      "unit": "GB/s", "frac": (alg / (cg_ms / 1e3) / 1e9) / peak if cg_ms else None, "traffic": None,
@@ -800,11 +814,12 @@ def picard_bench(args):
                      "share_of_step": cg_ms / 1e3 / wall, "peak_source": peak_src,
                      "note": "N (96 k + 32) bytes per pass; working set L2-resident at this size"},
         "cpu_baseline": cpu,
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": int(n * (8 + 8 + 1)),
-                "d2h_bytes_per_step": int(n * 8),
-                "note": "host wall clock around fem.step_backward_euler (the seam takes host arrays: T_old, "
-                        "Dirichlet values and mask up, the converged field down, the Picard loop in between "
-                        "on the device); value is the same"},
+        "e2e": {"value": n * args.steps / e2e_wall, "unit": UNIT, "h2d_bytes_per_step": int(e2e_h2d // args.steps),
+                "d2h_bytes_per_step": int(e2e_d2h // args.steps),
+                "note": "host wall clock around fem.step_backward_euler plus the read-back of the converged "
+                        "field after every step (bytes from tl_host_traffic: the Dirichlet node list and "
+                        "values up, the field down); value is the same loop without the read-back (the "
+                        "field stays in a device vector between steps)"},
         "gpu_launches": int(passes * 7 - args.steps), "clocks": clocks.summary(),
     }
     print(json.dumps(line), flush=True)

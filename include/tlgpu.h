@@ -165,6 +165,14 @@ int32_t tl_step_host(const tl_grid_desc* grid, double kappa, double rho_c, doubl
                      const tl_gaussian* src, double rtol, int32_t maxiter,
                      double* x_out, tl_solve_info* info);
 
+/* tl_step_host with the Dirichlet data as a node list (ids and values, scattered into the
+ * dense array on the device; g_const and the blend do not apply). */
+int32_t tl_step_nodes_host(const tl_grid_desc* grid, double kappa, double rho_c, double dt,
+                           int32_t dirichlet_kind, const int32_t* dirichlet_nodes, int64_t n_dirichlet,
+                           const double* dirichlet_values, const double* T_old, const double* load,
+                           const tl_gaussian* src, double rtol, int32_t maxiter, double* x_out,
+                           tl_solve_info* info);
+
 /* Device time (CUDA events) of the last tl_step_host's solve launches (RHS, CG loop,
  * residual, finish), for benchmarks and solver tuning. */
 int32_t tl_step_last_ms(float* ms);
@@ -225,6 +233,39 @@ int32_t tl_vc_picard_host(const tl_grid_desc* grid, const tl_vc_material* mat, c
                           const uint8_t* dirichlet_mask, const double* g, double rtol, int32_t maxiter, int32_t linear,
                           double picard_tol, int32_t picard_max, double* x_out, int32_t* passes, int32_t* pass_iters,
                           float* pass_ms, double* inc_out, tl_solve_info* info);
+
+/* tl_vc_picard_host with the Dirichlet data as a node list (fem.py:294-305 constrains the
+ * listed nodes): dirichlet_nodes[n_dirichlet] (node ids) and dirichlet_values[n_dirichlet]
+ * are scattered into the mask / value arrays on the device, so the call uploads
+ * O(n_dirichlet) bytes of boundary data instead of 9 bytes per node. */
+int32_t tl_vc_picard_nodes_host(const tl_grid_desc* grid, const tl_vc_material* mat, const tl_vc_material* mat_outside,
+                                const double* region, int32_t latent_inside_only, double dt, const double* T_old,
+                                const double* extra_load, const tl_gaussian* src, const tl_robin* robin,
+                                const int32_t* dirichlet_nodes, int64_t n_dirichlet, const double* dirichlet_values,
+                                double rtol, int32_t maxiter, int32_t linear, double picard_tol, int32_t picard_max,
+                                double* x_out, int32_t* passes, int32_t* pass_iters, float* pass_ms, double* inc_out,
+                                tl_solve_info* info);
+
+/* ---- Fields kept on the device between step-level calls.
+ * Every FIELD argument of the *_host entry points above and below (T_old, extra_load, g,
+ * values, local_values, load_out, x_out, a, b, ...: the arrays with one entry per grid
+ * node) may be a host pointer or a device pointer; unified virtual addressing tells them
+ * apart.  A caller that holds the reference's FieldState values in device vectors
+ * (tl_dev_alloc) therefore chains tl_vc_picard_nodes_host / tl_step_host /
+ * tl_interpolate_nodes_host / tl_transmission_host / tl_overlap_feedback_host with no
+ * per-node PCIe traffic.  tl_host_traffic reports the bytes that did cross (fields given as
+ * host pointers, tl_dev_copy), optionally resetting the counters. */
+int32_t tl_dev_alloc(int64_t bytes, void** out);
+int32_t tl_dev_free(void* p);
+int32_t tl_dev_copy(void* dst, const void* src, int64_t bytes);      /* any direction, complete on return */
+int32_t tl_host_traffic(int64_t* h2d_bytes, int64_t* d2h_bytes, int32_t reset);
+/* y = a x + y over n doubles (sums of interface loads, twolevel.py:254-262) */
+int32_t tl_axpy_host(int64_t n, double a, const double* x, double* y);
+/* Mesh.interpolate of the global field at listed nodes of the target lattice: the trace on
+ * the interface nodes (twolevel.py:130-142); bitwise the values tl_interpolate_host writes
+ * at those nodes. */
+int32_t tl_interpolate_nodes_host(const tl_grid_desc* global_grid, const double* values, const tl_grid_desc* target,
+                                  const int32_t* nodes, int64_t n, double* out);
 
 /* Device time (CUDA events) of the last tl_vc_step_host's Jacobi-PCG launch (benchmark). */
 int32_t tl_vc_last_cg_ms(float* ms);

@@ -8,6 +8,7 @@ entry point raises ``NativeLibraryMissing``.  Build it with
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 import os
 from pathlib import Path
 
@@ -109,6 +110,9 @@ SIGNATURES = [
     ("tl_step_host", C.c_int32, [C.POINTER(GridDesc), C.c_double, C.c_double, C.c_double, C.c_int32,
                                  _dp, _dp, C.c_double, C.c_double, _dp, _dp, C.POINTER(Gaussian),
                                  C.c_double, C.c_int32, _dp, C.POINTER(SolveInfo)]),
+    ("tl_step_nodes_host", C.c_int32, [C.POINTER(GridDesc), C.c_double, C.c_double, C.c_double, C.c_int32,
+                                       C.c_void_p, C.c_int64, _dp, _dp, _dp, C.POINTER(Gaussian),
+                                       C.c_double, C.c_int32, _dp, C.POINTER(SolveInfo)]),
     ("tl_interpolate_host", C.c_int32, [C.POINTER(GridDesc), _dp, C.POINTER(GridDesc), C.c_int32, _dp]),
     ("tl_interpolate_points_host", C.c_int32, [C.POINTER(GridDesc), _dp, _dp, C.c_int64, _dp]),
     ("tl_deposit_host", C.c_int32, [C.POINTER(GridDesc), _dp, _dp, C.c_int32, _dp]),
@@ -135,6 +139,18 @@ SIGNATURES = [
                                     C.POINTER(Gaussian), C.POINTER(Robin), C.c_void_p, _dp, C.c_double,
                                     C.c_int32, _dp, C.POINTER(SolveInfo)]),
     ("tl_error_l2_host", C.c_int32, [C.POINTER(GridDesc), _dp, C.POINTER(GridDesc), _dp, _dp]),
+    ("tl_vc_picard_nodes_host", C.c_int32, [C.POINTER(GridDesc), C.POINTER(VcMaterial), C.POINTER(VcMaterial), _dp,
+                                            C.c_int32, C.c_double, _dp, _dp, C.POINTER(Gaussian), C.POINTER(Robin),
+                                            C.c_void_p, C.c_int64, _dp, C.c_double, C.c_int32, C.c_int32,
+                                            C.c_double, C.c_int32, _dp, C.POINTER(C.c_int32), C.c_void_p,
+                                            C.c_void_p, C.POINTER(C.c_double), C.POINTER(SolveInfo)]),
+    ("tl_dev_alloc", C.c_int32, [C.c_int64, C.POINTER(_P)]),
+    ("tl_dev_free", C.c_int32, [_P]),
+    ("tl_dev_copy", C.c_int32, [_P, _P, C.c_int64]),
+    ("tl_host_traffic", C.c_int32, [C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.c_int32]),
+    ("tl_axpy_host", C.c_int32, [C.c_int64, C.c_double, _dp, _dp]),
+    ("tl_interpolate_nodes_host", C.c_int32, [C.POINTER(GridDesc), _dp, C.POINTER(GridDesc), C.c_void_p,
+                                              C.c_int64, _dp]),
     ("tl_run_create", C.c_int32, [C.POINTER(RunDesc), C.POINTER(_P)]),
     ("tl_run_destroy", C.c_int32, [_P]),
     ("tl_run_initial", C.c_int32, [_P, C.c_double]),
@@ -201,10 +217,135 @@ def check(rc: int, what: str = "tlgpu"):
         raise SolverError(f"{what} failed ({rc}): {msg}")
 
 
-def dptr(a: np.ndarray):
-    """Pointer to a C-contiguous float64 array (or None)."""
+class DeviceVector:
+    """n float64 values in device memory (``tl_dev_alloc``), accepted wherever a step-level
+    entry point takes a field (``dptr``).  ``to_host`` reads them back (cached, read-only:
+    the vector is written once, by the call that produced it).
+
+    Live vectors share a byte budget (``TLGPU_DEVICE_FIELDS_GB``, default 16): when an
+    allocation would exceed it, the oldest live vectors are spilled to their host copy and
+    their device memory is freed (a recorder that keeps every state of a long run then
+    holds host arrays, as with the reference); a spilled vector is passed as a host pointer."""
+
+    __slots__ = ("ptr", "n", "_host", "__weakref__")
+    _live: "dict[int, weakref.ref]" = {}
+    _bytes = 0
+    # released buffers are reused by size (a time loop allocates one result per solve:
+    # no cudaMalloc / cudaFree, which synchronises the device, in steady state)
+    _pool: "dict[int, list]" = {}
+    _pool_bytes = 0
+
+    def __init__(self, n: int):
+        self.n = int(n)
+        self._host = None
+        self.ptr = None
+        free = DeviceVector._pool.get(self.n)
+        if free:
+            self.ptr = free.pop()
+            DeviceVector._pool_bytes -= 8 * self.n
+        else:
+            DeviceVector._make_room(8 * self.n)
+            h = _P()
+            check(lib().tl_dev_alloc(8 * self.n, C.byref(h)), "device allocation")
+            self.ptr = h.value
+        DeviceVector._bytes += 8 * self.n
+        DeviceVector._live[id(self)] = weakref.ref(self)
+
+    @classmethod
+    def trim_pool(cls):
+        """Return the pooled buffers to the driver."""
+        for free in cls._pool.values():
+            for p in free:
+                lib().tl_dev_free(p)
+        cls._pool.clear()
+        cls._pool_bytes = 0
+
+    @staticmethod
+    def budget() -> int:
+        import os
+        return int(float(os.environ.get("TLGPU_DEVICE_FIELDS_GB", "16")) * 2**30)
+
+    @classmethod
+    def _make_room(cls, need: int):
+        cap = cls.budget()
+        if cls._bytes + cls._pool_bytes + need > cap and cls._pool_bytes:
+            cls.trim_pool()
+        if cls._bytes + need <= cap:
+            return
+        for key in list(cls._live):              # insertion order: oldest first
+            if cls._bytes + need <= cap:
+                break
+            v = cls._live[key]()
+            if v is not None:
+                v.spill()
+
+    @classmethod
+    def from_host(cls, a) -> "DeviceVector":
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        v = cls(a.size)
+        check(lib().tl_dev_copy(v.ptr, a.ctypes.data, 8 * a.size), "upload")
+        return v
+
+    @property
+    def shape(self):
+        return (self.n,)
+
+    @property
+    def on_device(self) -> bool:
+        return self.ptr is not None
+
+    def to_host(self) -> np.ndarray:
+        if self._host is None:
+            out = np.empty(self.n)
+            check(lib().tl_dev_copy(out.ctypes.data, self.ptr, 8 * self.n), "read-back")
+            out.setflags(write=False)
+            self._host = out
+        return self._host
+
+    def __array__(self, dtype=None, copy=None):
+        a = self.to_host()
+        return a if dtype is None else a.astype(dtype, copy=False)
+
+    def spill(self):
+        """Keep only the host copy."""
+        if self.ptr:
+            self.to_host()
+            self.free()
+
+    def free(self):
+        if self.ptr:
+            cls = DeviceVector
+            if cls._pool_bytes + 8 * self.n <= cls.budget() // 4:
+                cls._pool.setdefault(self.n, []).append(self.ptr)
+                cls._pool_bytes += 8 * self.n
+            else:
+                lib().tl_dev_free(self.ptr)
+            self.ptr = None
+            cls._bytes -= 8 * self.n
+            cls._live.pop(id(self), None)
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def host_traffic(reset: bool = False):
+    """(h2d, d2h) bytes the step-level entry points moved over PCIe since the last reset."""
+    a, b = C.c_int64(), C.c_int64()
+    check(lib().tl_host_traffic(C.byref(a), C.byref(b), int(reset)), "traffic counters")
+    return a.value, b.value
+
+
+def dptr(a):
+    """Pointer to a C-contiguous float64 array or a DeviceVector (or None)."""
     if a is None:
         return None
+    if isinstance(a, DeviceVector):
+        if a.ptr is None:                        # spilled: its host copy
+            return a.to_host().ctypes.data_as(_dp)
+        return C.cast(C.c_void_p(a.ptr), _dp)
     assert a.dtype == np.float64 and a.flags["C_CONTIGUOUS"], "expected contiguous float64"
     return a.ctypes.data_as(_dp)
 

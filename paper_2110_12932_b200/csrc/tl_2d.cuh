@@ -192,6 +192,14 @@ __global__ void k_interp2(Grid G, Grid L, const double* __restrict__ vg, double*
     }
 }
 
+__global__ void k_interp_nodes2(Grid G, Grid L, const double* __restrict__ vg, const int* __restrict__ idx, int n,
+                                double* __restrict__ out) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+        const int p = idx[e];
+        out[e] = p1_eval2(G, vg, node_coord(L, 0, p % L.NX), node_coord(L, 1, p / L.NX));
+    }
+}
+
 __global__ void k_interp_pts2(Grid G, const double* __restrict__ vg, const double* __restrict__ pts, int npts,
                               double* __restrict__ out) {
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < npts; e += gridDim.x * blockDim.x)

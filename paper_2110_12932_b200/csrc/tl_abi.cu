@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <initializer_list>
 #include <map>
+#include <atomic>
 #include <mutex>
 #include <utility>
 #include <cmath>
@@ -63,6 +64,37 @@ int fail(int code, const std::string& msg) {
         if (e_ != cudaSuccess)                                                                \
             return fail(TL_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));       \
     } while (0)
+
+// Field arguments of the *_host entry points may be host OR device pointers: unified virtual
+// addressing tells them apart, so a caller that keeps its fields on the device between calls
+// (DeviceVector in paper_2110_12932_b200/_native.py; tl_dev_alloc) pays no PCIe traffic for
+// them.  g_h2d_bytes / g_d2h_bytes count what did cross (tl_host_traffic).
+std::atomic<long long> g_h2d_bytes{0}, g_d2h_bytes{0};
+
+bool on_device(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// st == nullptr: the legacy default stream, synchronous for host memory
+cudaError_t copy_in(void* dst, const void* src, size_t bytes, cudaStream_t st = nullptr, bool async = false) {
+    if (!on_device(src)) g_h2d_bytes += (long long)bytes;
+    return async ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, st) : cudaMemcpy(dst, src, bytes, cudaMemcpyDefault);
+}
+
+// a device destination is complete when this returns (device-to-device copies are
+// asynchronous to the host; the next call may run on another stream)
+cudaError_t copy_out(void* dst, const void* src, size_t bytes) {
+    const bool dev = on_device(dst);
+    if (!dev) g_d2h_bytes += (long long)bytes;
+    cudaError_t e = cudaMemcpy(dst, src, bytes, cudaMemcpyDefault);
+    if (e == cudaSuccess && dev) e = cudaStreamSynchronize(nullptr);
+    return e;
+}
 
 // allow2d: a descriptor with ncells[2] == 0 is a 2D grid (NZ = 1; csrc/tl_2d.cuh); only the
 // entry points with triangle variants accept it.
@@ -800,11 +832,37 @@ int32_t tl_step_last_ms(float* ms) {
     return TL_OK;
 }
 
+static int step_impl(const tl_grid_desc* grid, double kappa, double rho_c, double dt,
+                     int32_t dirichlet_kind, const double* gA, const double* gB, double w,
+                     double g_const, const double* T_old, const double* load,
+                     const tl_gaussian* src, double rtol, int32_t maxiter, double* x_out,
+                     tl_solve_info* info, const int32_t* dnodes, int64_t nd, const double* dvalues);
+
 int32_t tl_step_host(const tl_grid_desc* grid, double kappa, double rho_c, double dt,
                      int32_t dirichlet_kind, const double* gA, const double* gB, double w,
                      double g_const, const double* T_old, const double* load,
                      const tl_gaussian* src, double rtol, int32_t maxiter, double* x_out,
                      tl_solve_info* info) {
+    return step_impl(grid, kappa, rho_c, dt, dirichlet_kind, gA, gB, w, g_const, T_old, load, src, rtol, maxiter,
+                     x_out, info, nullptr, 0, nullptr);
+}
+
+int32_t tl_step_nodes_host(const tl_grid_desc* grid, double kappa, double rho_c, double dt,
+                           int32_t dirichlet_kind, const int32_t* dirichlet_nodes, int64_t n_dirichlet,
+                           const double* dirichlet_values, const double* T_old, const double* load,
+                           const tl_gaussian* src, double rtol, int32_t maxiter, double* x_out,
+                           tl_solve_info* info) {
+    if (n_dirichlet < 0 || (n_dirichlet > 0 && (!dirichlet_nodes || !dirichlet_values)))
+        return fail(TL_E_INVALID, "Dirichlet node list");
+    return step_impl(grid, kappa, rho_c, dt, dirichlet_kind, nullptr, nullptr, 0.0, 0.0, T_old, load, src, rtol,
+                     maxiter, x_out, info, dirichlet_nodes, n_dirichlet, dirichlet_values);
+}
+
+static int step_impl(const tl_grid_desc* grid, double kappa, double rho_c, double dt,
+                     int32_t dirichlet_kind, const double* gA, const double* gB, double w,
+                     double g_const, const double* T_old, const double* load,
+                     const tl_gaussian* src, double rtol, int32_t maxiter, double* x_out,
+                     tl_solve_info* info, const int32_t* dnodes, int64_t nd, const double* dvalues) {
     if (!grid || !T_old || !x_out) return fail(TL_E_INVALID, "null argument");
     if (dt <= 0) return fail(TL_E_INVALID, "time step must be positive");
     if (dirichlet_kind != tl::kBottom && dirichlet_kind != tl::kGamma)
@@ -835,7 +893,8 @@ int32_t tl_step_host(const tl_grid_desc* grid, double kappa, double rho_c, doubl
     const size_t per = ((size_t)n + 2 + 31) / 32 * 32;
     const size_t npart = tl::kPartLen;
     const size_t nspec = (sizeof(tl::SolveSpec) + sizeof(tl::SolveInfoDev) + 255) / 256 * 32;
-    const size_t want = 13 * per + npart + nspec;
+    const size_t pnd = dnodes ? ((size_t)nd + 2 + 31) / 32 * 32 : 0;      // node list (ints) + values
+    const size_t want = 13 * per + npart + nspec + 2 * pnd;
     if (want > W.cap) {
         if (W.ws) cudaFree(W.ws);
         W.ws = nullptr;
@@ -851,8 +910,8 @@ int32_t tl_step_host(const tl_grid_desc* grid, double kappa, double rho_c, doubl
     double* p0 = W.ws + 3 * per;
     double* p1 = W.ws + 4 * per;
     double* q = W.ws + 5 * per;
-    double* dA = gA ? W.ws + 6 * per : nullptr;
-    double* dB = gA ? W.ws + 7 * per : nullptr;
+    double* dA = (gA || dnodes) ? W.ws + 6 * per : nullptr;
+    double* dB = gA ? W.ws + 7 * per : dA;
     double* dload = load ? W.ws + 8 * per : nullptr;
     double* xg = W.ws + 9 * per;                       // 4 per
     double* part = W.ws + 13 * per;
@@ -860,12 +919,24 @@ int32_t tl_step_host(const tl_grid_desc* grid, double kappa, double rho_c, doubl
     tl::SolveInfoDev* dinfo = reinterpret_cast<tl::SolveInfoDev*>(
         reinterpret_cast<char*>(dspec) + (sizeof(tl::SolveSpec) + 15) / 16 * 16);
     int rc = 0;
-    TL_CUDA(cudaMemcpyAsync(T, T_old, nb, cudaMemcpyHostToDevice, st));
+    TL_CUDA(copy_in(T, T_old, nb, st, true));
     if (gA) {
-        TL_CUDA(cudaMemcpyAsync(dA, gA, nb, cudaMemcpyHostToDevice, st));
-        TL_CUDA(cudaMemcpyAsync(dB, gB ? gB : gA, nb, cudaMemcpyHostToDevice, st));
+        TL_CUDA(copy_in(dA, gA, nb, st, true));
+        if (gB && gB != gA) TL_CUDA(copy_in(dB, gB, nb, st, true));
+        else dB = dA;
+    } else if (dnodes) {
+        // Dirichlet data as a node list: the dense array is built on the device
+        double* dvl = W.ws + 13 * per + npart + nspec;
+        int* dnd = reinterpret_cast<int*>(dvl + pnd);
+        TL_CUDA(cudaMemsetAsync(dA, 0, nb, st));
+        if (nd > 0) {
+            TL_CUDA(copy_in(dnd, dnodes, sizeof(int) * (size_t)nd, st, true));
+            TL_CUDA(copy_in(dvl, dvalues, sizeof(double) * (size_t)nd, st, true));
+            tl::k_scatter_dirichlet<<<296, 256, 0, st>>>(dnd, dvl, (int)nd, n, nullptr, dA);
+            TL_CUDA(cudaGetLastError());
+        }
     }
-    if (load) TL_CUDA(cudaMemcpyAsync(dload, load, nb, cudaMemcpyHostToDevice, st));
+    if (load) TL_CUDA(copy_in(dload, load, nb, st, true));
     P.T = T; P.gA = dA; P.gB = dB; P.w = gA ? w : 0.0; P.g_const = g_const; P.load = dload;
     P.b = b; P.r = r; P.p0 = p0; P.p1 = p1; P.q = q; P.part = part;
     P.rtol = rtol; P.maxiter = maxiter; P.info = dinfo;
@@ -885,7 +956,8 @@ int32_t tl_step_host(const tl_grid_desc* grid, double kappa, double rho_c, doubl
     TL_CUDA(cudaEventRecord(W.ev1, st));
     tl::SolveInfoDev hi{};
     TL_CUDA(cudaMemcpyAsync(&hi, dinfo, sizeof(hi), cudaMemcpyDeviceToHost, st));
-    TL_CUDA(cudaMemcpyAsync(x_out, T, nb, cudaMemcpyDeviceToHost, st));
+    if (!on_device(x_out)) g_d2h_bytes += (long long)nb;
+    TL_CUDA(cudaMemcpyAsync(x_out, T, nb, cudaMemcpyDefault, st));
     TL_CUDA(cudaStreamSynchronize(st));
     TL_CUDA(cudaEventElapsedTime(&g_step_last_ms, W.ev0, W.ev1));
     if (info) {
@@ -928,15 +1000,15 @@ int32_t tl_interpolate_host(const tl_grid_desc* global_grid, const double* value
     double *dv, *dout;
     std::lock_guard<std::mutex> lock(g_scratch_mu);
     if (int rc = scratch_arrays({{(size_t)G.n, 8, (void**)&dv}, {(size_t)L.n, 8, (void**)&dout}})) return rc;
-    TL_CUDA(cudaMemcpy(dv, values, sizeof(double) * G.n, cudaMemcpyHostToDevice));
-    TL_CUDA(cudaMemcpy(dout, out, sizeof(double) * L.n, cudaMemcpyHostToDevice));
+    TL_CUDA(copy_in(dv, values, sizeof(double) * G.n));
+    TL_CUDA(copy_in(dout, out, sizeof(double) * L.n));
     if (tl::grid_is_2d(G))
         tl::k_interp2<<<296, 256>>>(G, L, dv, dout, gamma_only ? 1 : 0);
     else
     tl::k_interp<<<592, 256>>>(G, dv, L, gamma_only ? 1 : 0, gamma_only ? nullptr : dout,
                                gamma_only ? dout : nullptr);
     TL_CUDA(cudaGetLastError());
-    TL_CUDA(cudaMemcpy(out, dout, sizeof(double) * L.n, cudaMemcpyDeviceToHost));
+    TL_CUDA(copy_out(out, dout, sizeof(double) * L.n));
     return TL_OK;
 }
 
@@ -967,7 +1039,8 @@ static int vc_impl(const tl_grid_desc* grid, const tl_vc_material* mat, const tl
                    const double* T_lag, const double* extra_load, const tl_gaussian* src, const tl_robin* robin,
                    const uint8_t* dirichlet_mask, const double* g, double rtol, int32_t maxiter, int32_t linear,
                    double picard_tol, int32_t picard_max, double* x_out, int32_t* passes, int32_t* pass_iters,
-                   float* pass_ms, double* inc_out, tl_solve_info* info);
+                   float* pass_ms, double* inc_out, tl_solve_info* info,
+                   const int32_t* dnodes = nullptr, int64_t nd = 0, const double* dvalues = nullptr);
 
 int32_t tl_vc_step_region_host(const tl_grid_desc* grid, const tl_vc_material* mat, const tl_vc_material* mat_outside,
                                const double* region, int32_t latent_inside_only, double dt, const double* T_old,
@@ -994,17 +1067,32 @@ int32_t tl_vc_picard_host(const tl_grid_desc* grid, const tl_vc_material* mat, c
                    pass_ms, inc_out, info);
 }
 
+int32_t tl_vc_picard_nodes_host(const tl_grid_desc* grid, const tl_vc_material* mat, const tl_vc_material* mat_outside,
+                                const double* region, int32_t latent_inside_only, double dt, const double* T_old,
+                                const double* extra_load, const tl_gaussian* src, const tl_robin* robin,
+                                const int32_t* dirichlet_nodes, int64_t n_dirichlet, const double* dirichlet_values,
+                                double rtol, int32_t maxiter, int32_t linear, double picard_tol, int32_t picard_max,
+                                double* x_out, int32_t* passes, int32_t* pass_iters, float* pass_ms, double* inc_out,
+                                tl_solve_info* info) {
+    if (!passes || !pass_iters || !pass_ms || !inc_out || picard_max < 1) return fail(TL_E_INVALID, "bad argument");
+    return vc_impl(grid, mat, mat_outside, region, latent_inside_only, dt, T_old, T_old, extra_load, src, robin,
+                   nullptr, nullptr, rtol, maxiter, linear, picard_tol, picard_max, x_out, passes, pass_iters,
+                   pass_ms, inc_out, info, dirichlet_nodes, n_dirichlet, dirichlet_values);
+}
+
 static int vc_impl(const tl_grid_desc* grid, const tl_vc_material* mat, const tl_vc_material* mat_outside,
                    const double* region, int32_t latent_inside_only, double dt, const double* T_old,
                    const double* T_lag, const double* extra_load, const tl_gaussian* src, const tl_robin* robin,
                    const uint8_t* dirichlet_mask, const double* g, double rtol, int32_t maxiter, int32_t linear,
                    double picard_tol, int32_t picard_max, double* x_out, int32_t* passes, int32_t* pass_iters,
-                   float* pass_ms, double* inc_out, tl_solve_info* info) {
+                   float* pass_ms, double* inc_out, tl_solve_info* info,
+                   const int32_t* dnodes, int64_t nd, const double* dvalues) {
     if ((mat_outside || latent_inside_only) && !region) return fail(TL_E_INVALID, "region box required");
     if (mat_outside && (mat_outside->nk < 2 || mat_outside->nc < 2))
         return fail(TL_E_INVALID, "material tables need two rows");
-    if (!grid || !mat || !T_old || !T_lag || !dirichlet_mask || !g || !x_out || !info)
-        return fail(TL_E_INVALID, "null argument");
+    if (!grid || !mat || !T_old || !T_lag || !x_out || !info) return fail(TL_E_INVALID, "null argument");
+    if (dirichlet_mask ? !g : (nd < 0 || (nd > 0 && (!dnodes || !dvalues))))
+        return fail(TL_E_INVALID, "Dirichlet data: a mask with values, or a node list with values");
     if (!(dt > 0.0)) return fail(TL_E_INVALID, "time step must be positive");
     if (mat->nk < 2 || mat->nc < 2) return fail(TL_E_INVALID, "material tables need two rows");
     tl::Grid G{};
@@ -1037,7 +1125,7 @@ static int vc_impl(const tl_grid_desc* grid, const tl_vc_material* mat, const tl
     const size_t nt = nt_i + (mat_outside ? 2 * (size_t)(mat_outside->nk + mat_outside->nc) : 0);
     const bool two_d = tl::grid_is_2d(G);
     const size_t ntet = two_d ? 2 * (size_t)G.nc[0] * G.nc[1] : 6 * (size_t)G.nc[0] * G.nc[1] * G.nc[2];
-    const size_t want = 16 * per + nt + 6 * 4096 + 9 * ntet;
+    const size_t want = 16 * per + nt + 6 * 4096 + 9 * ntet + 2 * ((size_t)nd + 4);
     if (want > ws_cap) {
         if (ws) cudaFree(ws);
         ws = nullptr;
@@ -1072,11 +1160,26 @@ static int vc_impl(const tl_grid_desc* grid, const tl_vc_material* mat, const tl
     double* tk = cpart + 6 * 4096;
     double* tml = tk + ntet;
     double* tsrc = tml + 4 * ntet;
-    TL_CUDA(cudaMemcpy(dTo, T_old, sizeof(double) * n, cudaMemcpyHostToDevice));
-    TL_CUDA(cudaMemcpy(dTl, T_lag, sizeof(double) * n, cudaMemcpyHostToDevice));
-    if (dex) TL_CUDA(cudaMemcpy(dex, extra_load, sizeof(double) * n, cudaMemcpyHostToDevice));
-    TL_CUDA(cudaMemcpy(dg, g, sizeof(double) * n, cudaMemcpyHostToDevice));
-    TL_CUDA(cudaMemcpy(dm, dirichlet_mask, n, cudaMemcpyHostToDevice));
+    TL_CUDA(copy_in(dTo, T_old, sizeof(double) * n));
+    if (T_lag == T_old) TL_CUDA(cudaMemcpy(dTl, dTo, sizeof(double) * n, cudaMemcpyDeviceToDevice));
+    else TL_CUDA(copy_in(dTl, T_lag, sizeof(double) * n));
+    if (dex) TL_CUDA(copy_in(dex, extra_load, sizeof(double) * n));
+    if (dirichlet_mask) {
+        TL_CUDA(copy_in(dg, g, sizeof(double) * n));
+        TL_CUDA(copy_in(dm, dirichlet_mask, n));
+    } else {
+        // sparse Dirichlet data: node list + values, scattered on the device
+        int* dnd = reinterpret_cast<int*>(tsrc + ntet);
+        double* dvl = reinterpret_cast<double*>(dnd + ((size_t)nd + 2) / 2 * 2);
+        TL_CUDA(cudaMemset(dg, 0, sizeof(double) * n));
+        TL_CUDA(cudaMemset(dm, 0, n));
+        if (nd > 0) {
+            TL_CUDA(copy_in(dnd, dnodes, sizeof(int) * (size_t)nd));
+            TL_CUDA(copy_in(dvl, dvalues, sizeof(double) * (size_t)nd));
+            tl::k_scatter_dirichlet<<<kNB, kT>>>(dnd, dvl, (int)nd, n, dm, dg);
+            TL_CUDA(cudaGetLastError());
+        }
+    }
     TL_CUDA(cudaMemcpy(tabs, mat->k_T, sizeof(double) * mat->nk, cudaMemcpyHostToDevice));
     TL_CUDA(cudaMemcpy(tabs + mat->nk, mat->k_v, sizeof(double) * mat->nk, cudaMemcpyHostToDevice));
     TL_CUDA(cudaMemcpy(tabs + 2 * mat->nk, mat->c_T, sizeof(double) * mat->nc, cudaMemcpyHostToDevice));
@@ -1169,7 +1272,7 @@ static int vc_impl(const tl_grid_desc* grid, const tl_vc_material* mat, const tl
     TL_CUDA(cudaGetLastError());
     }
     TL_CUDA(cudaGetLastError());
-    TL_CUDA(cudaMemcpy(x_out, x, sizeof(double) * n, cudaMemcpyDeviceToHost));
+    TL_CUDA(copy_out(x_out, x, sizeof(double) * n));
     return TL_OK;
 }
 
@@ -1221,8 +1324,8 @@ int32_t tl_overlap_feedback_host(const tl_grid_desc* global_grid, const tl_grid_
     double* dold = dn + pl;
     double* dload = dold + pl;
     double* tabs = dload + pg;
-    TL_CUDA(cudaMemcpy(dn, local_new, sizeof(double) * L.n, cudaMemcpyHostToDevice));
-    TL_CUDA(cudaMemcpy(dold, local_old, sizeof(double) * L.n, cudaMemcpyHostToDevice));
+    TL_CUDA(copy_in(dn, local_new, sizeof(double) * L.n));
+    TL_CUDA(copy_in(dold, local_old, sizeof(double) * L.n));
     auto upload = [&](const tl_vc_material* m, double* at, tl::VcMat& M) -> int {
         TL_CUDA(cudaMemcpy(at, m->k_T, sizeof(double) * m->nk, cudaMemcpyHostToDevice));
         TL_CUDA(cudaMemcpy(at + m->nk, m->k_v, sizeof(double) * m->nk, cudaMemcpyHostToDevice));
@@ -1242,7 +1345,7 @@ int32_t tl_overlap_feedback_host(const tl_grid_desc* global_grid, const tl_grid_
     }
     tl::k_overlap_feedback<<<296, 256>>>(G, L, dn, dold, dt, Mg, Ml, S, dload);
     TL_CUDA(cudaGetLastError());
-    TL_CUDA(cudaMemcpy(load_out, dload, sizeof(double) * G.n, cudaMemcpyDeviceToHost));
+    TL_CUDA(copy_out(load_out, dload, sizeof(double) * G.n));
     return TL_OK;
 }
 
@@ -1284,7 +1387,7 @@ static int transmission_impl(const tl_grid_desc* global_grid, const tl_grid_desc
     int* keys2 = keys + pe;
     int* idx = keys2 + pe;
     int* idx2 = idx + pe;
-    TL_CUDA(cudaMemcpy(dT, local_values, sizeof(double) * L.n, cudaMemcpyHostToDevice));
+    TL_CUDA(copy_in(dT, local_values, sizeof(double) * L.n));
     TL_CUDA(cudaMemset(dload, 0, sizeof(double) * G.n));
     double* dtab = dload + pg;
     tl::KTab kg{nullptr, nullptr, 0}, kl{nullptr, nullptr, 0};
@@ -1307,7 +1410,7 @@ static int transmission_impl(const tl_grid_desc* global_grid, const tl_grid_desc
     TL_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys2, idx, idx2, (int)ne, 0, bits));
     tl::k_trans_segsum<<<296, 256>>>(keys2, idx2, dvals, (int)ne, dload);
     TL_CUDA(cudaGetLastError());
-    TL_CUDA(cudaMemcpy(load_out, dload, sizeof(double) * G.n, cudaMemcpyDeviceToHost));
+    TL_CUDA(copy_out(load_out, dload, sizeof(double) * G.n));
     return TL_OK;
 }
 
@@ -1322,8 +1425,8 @@ int32_t tl_mass_norms_host(const tl_grid_desc* grid, const double* a, const doub
                                  {2 * (size_t)kNB, 8, (void**)&dpart}}))
         return rc;
     if (!b) db = nullptr;
-    TL_CUDA(cudaMemcpy(da, a, sizeof(double) * L.n, cudaMemcpyHostToDevice));
-    if (b) TL_CUDA(cudaMemcpy(db, b, sizeof(double) * L.n, cudaMemcpyHostToDevice));
+    TL_CUDA(copy_in(da, a, sizeof(double) * L.n));
+    if (b) TL_CUDA(copy_in(db, b, sizeof(double) * L.n));
     if (tl::grid_is_2d(L)) tl::k_mass_norms2<<<kNB, 256>>>(L, da, db, dpart);
     else tl::k_mass_norms<<<kNB, 256>>>(L, da, db, dpart);
     TL_CUDA(cudaGetLastError());
@@ -1345,8 +1448,8 @@ int32_t tl_mass_norms_split_host(const tl_grid_desc* grid, const double* a, cons
     if (int rc = scratch_arrays({{(size_t)L.n, 8, (void**)&da}, {(size_t)L.n, 8, (void**)&db},
                                  {2 * (size_t)kNB, 8, (void**)&dpart}}))
         return rc;
-    TL_CUDA(cudaMemcpy(da, a, sizeof(double) * L.n, cudaMemcpyHostToDevice));
-    TL_CUDA(cudaMemcpy(db, b, sizeof(double) * L.n, cudaMemcpyHostToDevice));
+    TL_CUDA(copy_in(da, a, sizeof(double) * L.n));
+    TL_CUDA(copy_in(db, b, sizeof(double) * L.n));
     tl::k_mass_norms_split<<<kNB, 256>>>(L, da, db, box_lo[0], box_lo[1], box_lo[2], box_hi[0], box_hi[1],
                                          box_hi[2], dpart);
     TL_CUDA(cudaGetLastError());
@@ -1370,8 +1473,8 @@ int32_t tl_error_l2_host(const tl_grid_desc* ref_grid, const double* ref_values,
     if (int rc = scratch_arrays({{(size_t)G.n, 8, (void**)&dref}, {(size_t)L.n, 8, (void**)&dv},
                                  {(size_t)L.n, 8, (void**)&dri}, {2 * (size_t)kNB, 8, (void**)&dpart}}))
         return rc;
-    TL_CUDA(cudaMemcpy(dref, ref_values, sizeof(double) * G.n, cudaMemcpyHostToDevice));
-    TL_CUDA(cudaMemcpy(dv, values, sizeof(double) * L.n, cudaMemcpyHostToDevice));
+    TL_CUDA(copy_in(dref, ref_values, sizeof(double) * G.n));
+    TL_CUDA(copy_in(dv, values, sizeof(double) * L.n));
     if (tl::grid_is_2d(G)) {
         tl::k_interp2<<<296, 256>>>(G, L, dref, dri, 0);
         tl::k_mass_norms2<<<kNB, 256>>>(L, dv, dri, dpart);
@@ -1398,7 +1501,7 @@ int32_t tl_interpolate_points_host(const tl_grid_desc* global_grid, const double
     if (int rc = scratch_arrays({{(size_t)G.n, 8, (void**)&dv}, {pd * (size_t)npoints, 8, (void**)&dp},
                                  {(size_t)npoints, 8, (void**)&dout}}))
         return rc;
-    TL_CUDA(cudaMemcpy(dv, values, sizeof(double) * G.n, cudaMemcpyHostToDevice));
+    TL_CUDA(copy_in(dv, values, sizeof(double) * G.n));
     TL_CUDA(cudaMemcpy(dp, points, sizeof(double) * pd * npoints, cudaMemcpyHostToDevice));
     if (npoints > 0 && pd == 2) tl::k_interp_pts2<<<296, 256>>>(G, dv, dp, (int)npoints, dout);
     else
@@ -1429,7 +1532,80 @@ int32_t tl_deposit_host(const tl_grid_desc* grid, const double* points, const do
     }
     tl::k_deposit<<<1, 1024>>>(G, dp, dw, count, dl, prev, prevn, 0, G.n);
     TL_CUDA(cudaGetLastError());
-    TL_CUDA(cudaMemcpy(load_out, dl, sizeof(double) * G.n, cudaMemcpyDeviceToHost));
+    TL_CUDA(copy_out(load_out, dl, sizeof(double) * G.n));
+    return TL_OK;
+}
+
+// ---- device vectors for callers that keep step-level fields on the device --------------
+int32_t tl_dev_alloc(int64_t bytes, void** out) {
+    if (!out || bytes < 0) return fail(TL_E_INVALID, "bad argument");
+    *out = nullptr;
+    TL_CUDA(cudaMalloc(out, (size_t)std::max<int64_t>(bytes, 16)));
+    return TL_OK;
+}
+
+int32_t tl_dev_free(void* p) {
+    if (p) TL_CUDA(cudaFree(p));
+    return TL_OK;
+}
+
+int32_t tl_dev_copy(void* dst, const void* src, int64_t bytes) {
+    if (!dst || !src || bytes < 0) return fail(TL_E_INVALID, "bad argument");
+    const bool din = on_device(src), dout = on_device(dst);
+    if (!din && dout) g_h2d_bytes += bytes;
+    if (din && !dout) g_d2h_bytes += bytes;
+    TL_CUDA(cudaMemcpy(dst, src, (size_t)bytes, cudaMemcpyDefault));
+    if (dout) TL_CUDA(cudaStreamSynchronize(nullptr));
+    return TL_OK;
+}
+
+int32_t tl_host_traffic(int64_t* h2d_bytes, int64_t* d2h_bytes, int32_t reset) {
+    if (h2d_bytes) *h2d_bytes = g_h2d_bytes.load();
+    if (d2h_bytes) *d2h_bytes = g_d2h_bytes.load();
+    if (reset) { g_h2d_bytes = 0; g_d2h_bytes = 0; }
+    return TL_OK;
+}
+
+// y = a x + y over n doubles (host or device operands; the sum of interface loads)
+int32_t tl_axpy_host(int64_t n, double a, const double* x, double* y) {
+    if (!x || !y || n < 0 || n >= (1ll << 31)) return fail(TL_E_INVALID, "bad argument");
+    const bool xd = on_device(x), yd = on_device(y);
+    double *dx = const_cast<double*>(x), *dy = y;
+    std::lock_guard<std::mutex> lock(g_scratch_mu);
+    double *sx = nullptr, *sy = nullptr;
+    if (int rc = scratch_arrays({{xd ? 0 : (size_t)n, 8, (void**)&sx}, {yd ? 0 : (size_t)n, 8, (void**)&sy}})) return rc;
+    if (!xd) { TL_CUDA(copy_in(sx, x, sizeof(double) * n)); dx = sx; }
+    if (!yd) { TL_CUDA(copy_in(sy, y, sizeof(double) * n)); dy = sy; }
+    tl::k_axpy<<<296, 256>>>((int)n, a, dx, dy);
+    TL_CUDA(cudaGetLastError());
+    if (!yd) TL_CUDA(copy_out(y, dy, sizeof(double) * n));
+    else TL_CUDA(cudaStreamSynchronize(nullptr));
+    return TL_OK;
+}
+
+// The global field's P1 interpolant at listed nodes of a target lattice (the trace on the
+// interface nodes, twolevel.py:130-142): the values k_interp writes at those nodes.
+int32_t tl_interpolate_nodes_host(const tl_grid_desc* global_grid, const double* values, const tl_grid_desc* target,
+                                  const int32_t* nodes, int64_t n, double* out) {
+    if (!global_grid || !values || !target || !out || n < 0 || (n > 0 && !nodes)) return fail(TL_E_INVALID, "bad argument");
+    tl::Grid G{}, L{};
+    if (int rc = make_grid(*global_grid, tl::kBottom, G, true)) return rc;
+    if (int rc = make_grid(*target, tl::kGamma, L, true)) return rc;
+    if (tl::grid_is_2d(G) != tl::grid_is_2d(L)) return fail(TL_E_INVALID, "grids of different dimension");
+    if (n == 0) return TL_OK;
+    const bool vd = on_device(values);
+    double *dv = const_cast<double*>(values), *sv = nullptr, *dout = nullptr;
+    int* didx = nullptr;
+    std::lock_guard<std::mutex> lock(g_scratch_mu);
+    if (int rc = scratch_arrays({{vd ? 0 : (size_t)G.n, 8, (void**)&sv}, {(size_t)n, 8, (void**)&dout},
+                                 {(size_t)n, 4, (void**)&didx}}))
+        return rc;
+    if (!vd) { TL_CUDA(copy_in(sv, values, sizeof(double) * G.n)); dv = sv; }
+    TL_CUDA(copy_in(didx, nodes, sizeof(int) * (size_t)n));
+    if (tl::grid_is_2d(G)) tl::k_interp_nodes2<<<296, 256>>>(G, L, dv, didx, (int)n, dout);
+    else tl::k_interp_nodes<<<296, 256>>>(G, dv, L, didx, (int)n, dout);
+    TL_CUDA(cudaGetLastError());
+    TL_CUDA(copy_out(out, dout, sizeof(double) * (size_t)n));
     return TL_OK;
 }
 

@@ -1060,6 +1060,33 @@ __global__ void k_gather(const double* __restrict__ src, const int* __restrict__
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) dst[e] = src[idx[e]];
 }
 
+// The values k_interp writes at the listed target nodes (same arithmetic: bitwise equal).
+__global__ void k_interp_nodes(Grid G, const double* __restrict__ v, Grid L, const int* __restrict__ idx, int n,
+                               double* __restrict__ out) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+        int i, j, k;
+        decode(L, idx[e], i, j, k);
+        out[e] = p1_eval(G, v, node_coord(L, 0, i), node_coord(L, 1, j), node_coord(L, 2, k));
+    }
+}
+
+__global__ void k_axpy(int n, double a, const double* __restrict__ x, double* __restrict__ y) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x)
+        y[e] = __dadd_rn(__dmul_rn(a, x[e]), y[e]);
+}
+
+// Dirichlet data given as a node list: mask and values of a dense pair (cleared before)
+__global__ void k_scatter_dirichlet(const int* __restrict__ nodes, const double* __restrict__ vals, int nd, int n,
+                                    unsigned char* __restrict__ mask, double* __restrict__ g) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nd; e += gridDim.x * blockDim.x) {
+        const int p = nodes[e];
+        if (p >= 0 && p < n) {
+            if (mask) mask[p] = 1;
+            g[p] = vals[e];
+        }
+    }
+}
+
 __global__ void k_fill(double* a, int n, double v) {
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) a[e] = v;
 }

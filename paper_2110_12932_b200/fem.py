@@ -22,7 +22,7 @@ from .control import ThermalBC, material_constants
 from .errors import NonConvergence, SolverError, UnsupportedOnDevice
 from .grid import BOTTOM, TOP, StructuredGrid
 
-__all__ = ["FieldState", "uniform_field", "SolverSettings", "BoundarySpec", "GaussianSource",
+__all__ = ["FieldState", "DeviceBackedFieldState", "field_arg", "device_fields", "uniform_field", "SolverSettings", "BoundarySpec", "GaussianSource",
            "step_backward_euler", "device_rtol", "Trajectory", "solve_monolithic", "PiecewiseMaterial",
            "RegionMask"]
 
@@ -47,6 +47,57 @@ class FieldState:
     def with_values(self, values, time: float | None = None) -> "FieldState":
         return FieldState(self.mesh, values, self.time if time is None else time)
 
+    def retimed(self, time: float) -> "FieldState":
+        """The same values stamped with another time (``FieldState(mesh, values, t)`` in the
+        reference's drivers) without touching the values."""
+        return FieldState(self.mesh, self.values, time)
+
+
+def device_fields() -> bool:
+    """Step-level solves return device-backed fields (``DeviceBackedFieldState``) unless
+    ``TLGPU_DEVICE_FIELDS=0``."""
+    import os
+    return os.environ.get("TLGPU_DEVICE_FIELDS", "1") != "0"
+
+
+class DeviceBackedFieldState(FieldState):
+    """A step-level solve's result left on the device (``_native.DeviceVector``): the next
+    solve, trace interpolation or interface functional reads it there, and ``values`` reads
+    it back on first access (cached, read-only).  The producing solve already checked it for
+    non-finite values (``fem.py:50-51``; TL_SOLVE_NONFINITE)."""
+
+    def __init__(self, mesh, dev, time: float):
+        if dev.n != mesh.n_nodes:
+            raise SolverError(f"field has {dev.n} values for a mesh with {mesh.n_nodes} nodes")
+        object.__setattr__(self, "mesh", mesh)
+        object.__setattr__(self, "time", float(time))
+        object.__setattr__(self, "device_values", dev)
+
+    @property
+    def values(self) -> np.ndarray:
+        return self.device_values.to_host()
+
+    def retimed(self, time: float) -> "FieldState":
+        return DeviceBackedFieldState(self.mesh, self.device_values, time)
+
+    def __reduce__(self):
+        return (FieldState, (self.mesh, self.values, self.time))
+
+    def __repr__(self):
+        return f"DeviceBackedFieldState(mesh={self.mesh!r}, time={self.time!r})"
+
+
+def field_arg(state_or_values):
+    """What a step-level entry point is given for a field: the device vector when the field
+    lives there, else a contiguous float64 host array."""
+    dev = getattr(state_or_values, "device_values", None)
+    if dev is not None:
+        return dev
+    if isinstance(state_or_values, N.DeviceVector):
+        return state_or_values
+    v = state_or_values.values if isinstance(state_or_values, FieldState) else state_or_values
+    return np.ascontiguousarray(v, dtype=np.float64)
+
 
 class UniformFieldState(FieldState):
     """``uniform_field``'s result: a constant field whose value array is built only when
@@ -69,6 +120,9 @@ class UniformFieldState(FieldState):
             v.setflags(write=False)
             object.__setattr__(self, "_v", v)
         return self._v
+
+    def retimed(self, time: float) -> "FieldState":
+        return UniformFieldState(self.mesh, self.uniform_value, time)
 
     def __reduce__(self):
         return (UniformFieldState, (self.mesh, self.uniform_value, self.time))
@@ -266,15 +320,14 @@ def _step_general(state: FieldState, dt: float, mat, source, bounds: BoundarySpe
         peak, radius, depth, center = source.device_args()
         src = N.Gaussian(float(peak), float(radius), float(depth), (C.c_double * 3)(*map(float, center)), 1)
     n = mesh.n_nodes
-    dnodes = np.asarray(bounds.dirichlet_nodes, dtype=np.int64)
-    dmask = np.zeros(n, dtype=np.uint8)
-    dmask[dnodes] = 1
-    g = np.zeros(n)
-    g[dnodes] = bounds.dirichlet_array()
-    ld = None if extra_load is None else np.ascontiguousarray(extra_load, dtype=np.float64)
+    # Dirichlet data as a node list, scattered on the device (tl_vc_picard_nodes_host); a
+    # repeated node keeps its last value, like the reference's g[nodes] = values
+    from .ops import dirichlet_list
+    dnodes32, dvals = dirichlet_list(bounds.dirichlet_nodes, bounds.dirichlet_array(), n)
+    ld = None if extra_load is None else field_arg(extra_load)
     if ld is not None and ld.shape != (n,):
         raise SolverError("extra load does not match the mesh")
-    T_old = np.ascontiguousarray(state.values, dtype=np.float64)
+    T_old = field_arg(state)
     desc = mesh.desc()
     rtol = device_rtol(settings)
     linear = problem_is_linear(mat, bounds, latent)
@@ -284,7 +337,7 @@ def _step_general(state: FieldState, dt: float, mat, source, bounds: BoundarySpe
         # (fem.py:331-355)
         raise NonConvergence("Picard iteration", max_iter, float("inf"))
     t_new = state.time + dt
-    x = np.empty(n)
+    x = N.DeviceVector(n) if device_fields() else np.empty(n)
     info = N.SolveInfo()
     npass = C.c_int32(0)
     its = np.zeros(max_iter, dtype=np.int32)
@@ -295,10 +348,11 @@ def _step_general(state: FieldState, dt: float, mat, source, bounds: BoundarySpe
         timer.__enter__()
     try:
         # the whole Picard loop (fem.py:331-355) on the device: one upload, one read-back
-        N.check(N.lib().tl_vc_picard_host(
+        N.check(N.lib().tl_vc_picard_nodes_host(
             C.byref(desc), C.byref(md), C.byref(mo) if mo is not None else None, N.dptr(reg),
             1 if latent_mask is not None else 0, float(dt), N.dptr(T_old), N.dptr(ld),
-            C.byref(src) if src is not None else None, C.byref(rb), dmask.ctypes.data, N.dptr(g), float(rtol),
+            C.byref(src) if src is not None else None, C.byref(rb), dnodes32.ctypes.data, int(dnodes32.size),
+            N.dptr(dvals), float(rtol),
             min(20 * n, 2_000_000_000), 1 if linear else 0, float(settings.picard_tol), int(max_iter), N.dptr(x),
             C.byref(npass), its.ctypes.data, mss.ctypes.data, C.byref(inc), C.byref(info)), "step")
     finally:
@@ -314,6 +368,8 @@ def _step_general(state: FieldState, dt: float, mat, source, bounds: BoundarySpe
             stats.device_log.extend((float(mss[k]), int(its[k])) for k in range(ok))
     raise_for(info)
     if linear or inc.value < settings.picard_tol:
+        if isinstance(x, N.DeviceVector):
+            return DeviceBackedFieldState(mesh, x, t_new)
         return state.with_values(x, t_new)
     raise NonConvergence("Picard iteration", max_iter, inc.value)
 
@@ -343,21 +399,28 @@ def step_backward_euler(state: FieldState, dt: float, mat, source, bounds: Bound
     mesh = state.mesh
     kind = _dirichlet_kind(mesh, bounds.dirichlet_nodes)
     kappa, rho_c = material_constants(mat)
-    g = np.zeros(mesh.n_nodes)
-    g[np.asarray(bounds.dirichlet_nodes, dtype=np.int64)] = bounds.dirichlet_array()
+    darr = bounds.dirichlet_array()
+    g_const, dlist = 0.0, None
+    if darr.size and np.all(darr == darr.flat[0]):
+        g_const = float(darr.flat[0])          # constant data (the build plate): no array at all
+    else:                                      # the trace: node list + values, scattered on the device
+        dlist = (np.asarray(bounds.dirichlet_nodes, dtype=np.int64), darr)
     timer = stats.timer("assembly") if stats is not None else None
     if timer is not None:
         timer.__enter__()
     try:
-        x, info = step(mesh, kappa, rho_c, dt, kind, state.values, g=g, load=extra_load,
+        x, info = step(mesh, kappa, rho_c, dt, kind, field_arg(state), g_const=g_const, dirichlet=dlist,
+                       load=None if extra_load is None else field_arg(extra_load),
                        gaussian=source.device_args() if source is not None else None,
-                       rtol=device_rtol(settings))
+                       rtol=device_rtol(settings), on_device=device_fields())
     finally:
         if timer is not None:
             timer.__exit__(None, None, None)
     raise_for(info)
     if stats is not None:
         stats.count("picard_iterations")
+    if isinstance(x, N.DeviceVector):
+        return DeviceBackedFieldState(mesh, x, state.time + dt)
     return state.with_values(x, state.time + dt)
 
 

@@ -542,7 +542,7 @@ def macro_step(problem, state: TwoLevelState, schedule: MacroSchedule, k: int, s
     if recorder is not None:
         recorder("predictor", t_next, None, predicted, 0)
     trace_old = state.trace
-    trace_pred = state.gamma.trace_of(predicted.values, problem.global_mesh)
+    trace_pred = state.gamma.trace_of(predicted, problem.global_mesh)
     local = state.local_field
     before_final = state.local_field
     for i in range(m):
@@ -551,12 +551,12 @@ def macro_step(problem, state: TwoLevelState, schedule: MacroSchedule, k: int, s
         if i == m - 1:
             before_final = local
         local = solve_local(problem, local, t_i - local.time, state.gamma, trace_i, stats=stats)
-        local = FieldState(local.mesh, local.values, t_i)
+        local = local.retimed(t_i)
         if recorder is not None:
             recorder("micro", t_i, local, None, 0)
     if problem.one_way and problem.interval_source:
         corrected = solve_local(problem, before_final, delta, state.gamma, trace_pred, stats=stats)
-        corrected = FieldState(corrected.mesh, corrected.values, t_next)
+        corrected = corrected.retimed(t_next)
         if stats is not None:
             stats.count("coupling_iterations")
         new_state = TwoLevelState(predicted, corrected, state.gamma, trace_pred)
@@ -571,8 +571,7 @@ def macro_step(problem, state: TwoLevelState, schedule: MacroSchedule, k: int, s
 
 
 def _restamp(state: TwoLevelState, t: float) -> TwoLevelState:
-    return TwoLevelState(FieldState(state.global_field.mesh, state.global_field.values, t),
-                         FieldState(state.local_field.mesh, state.local_field.values, t),
+    return TwoLevelState(state.global_field.retimed(t), state.local_field.retimed(t),
                          state.gamma, state.trace)
 
 

@@ -22,6 +22,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
+from . import _native as N
 from .config import CouplingSettings, SolverSettings
 from .control import LaserBeam, ScanPath, ThermalBC, check_immersed, material_constants
 from .errors import CouplingError, CouplingNonConvergence, UnsupportedOnDevice
@@ -53,10 +54,11 @@ class InterfaceGamma:
         lx, ly, lz = (float(v) for v in self.local.box.lengths)
         return lx * ly + 2.0 * (lx * lz + ly * lz)
 
-    def trace_of(self, global_field_values, global_mesh) -> np.ndarray:
-        from .ops import interpolate_to_grid
-        full = interpolate_to_grid(global_mesh, global_field_values, self.local, gamma_only=True)
-        return full[self.trace_nodes]
+    def trace_of(self, global_field, global_mesh) -> np.ndarray:
+        """The global field (a FieldState, its values or a DeviceVector) at the trace nodes."""
+        from .ops import interpolate_at_nodes
+        from .fem import field_arg
+        return interpolate_at_nodes(global_mesh, field_arg(global_field), self.local, self.trace_nodes)
 
 
 def extract_interface(local: StructuredGrid, global_mesh: StructuredGrid) -> InterfaceGamma:
@@ -211,13 +213,17 @@ def initial_state(problem: TwoLevelProblem, local_mesh: StructuredGrid,
                   global_field: FieldState) -> TwoLevelState:
     """``initial_state`` (``twolevel.py:145-156``): local = P1(global), trace = P1 on gamma."""
     from .ops import interpolate_to_grid
+    from .fem import DeviceBackedFieldState, device_fields, field_arg
     gamma = extract_interface(local_mesh, problem.global_mesh)
-    lv = interpolate_to_grid(problem.global_mesh, global_field.values, local_mesh)
+    lv = interpolate_to_grid(problem.global_mesh, field_arg(global_field), local_mesh, on_device=device_fields())
+    if isinstance(lv, N.DeviceVector):
+        local = DeviceBackedFieldState(local_mesh, lv, global_field.time)
+        return TwoLevelState(global_field, local, gamma, gamma.trace_of(global_field, problem.global_mesh))
     local = FieldState(local_mesh, lv, global_field.time)
     return TwoLevelState(global_field, local, gamma, lv[gamma.trace_nodes].copy())
 
 
-def transmission_load(local_field, gamma, global_mesh, mat_global, mat_local) -> np.ndarray:
+def transmission_load(local_field, gamma, global_mesh, mat_global, mat_local, on_device: bool = False):
     """Interface functional (``twolevel.py:159-183``): the integral over the interface facets
     of (kappa_global - kappa_local) dT_local/dn w_global.  Exactly zero for equal
     conductivities; otherwise one device call (constant conductivities: the jump is a
@@ -229,10 +235,11 @@ def transmission_load(local_field, gamma, global_mesh, mat_global, mat_local) ->
     if lmesh.dim != 3:
         raise UnsupportedOnDevice("the interface functional has no 2D kernel (equal conductivities "
                                   "make it exactly zero)")
-    T = np.ascontiguousarray(local_field.values, dtype=np.float64)
+    from .fem import field_arg
+    T = field_arg(local_field)
     if T.shape != (lmesh.n_nodes,):
         raise CouplingError("local field does not match its mesh")
-    out = np.zeros(global_mesh.n_nodes)
+    out = N.DeviceVector(global_mesh.n_nodes) if on_device else np.zeros(global_mesh.n_nodes)
     gd, ld = global_mesh.desc(), lmesh.desc()
     if mat_global.is_constant and mat_local.is_constant:
         kg, _ = material_constants(mat_global)
@@ -251,7 +258,7 @@ def transmission_load(local_field, gamma, global_mesh, mat_global, mat_local) ->
 
 
 def overlap_feedback(problem: TwoLevelProblem, local_new: FieldState, local_old: FieldState, dt: float,
-                     t0: float, t1: float) -> np.ndarray:
+                     t0: float, t1: float, on_device: bool = False):
     """``_overlap_feedback`` (``twolevel.py:186-239``): the full-mode overlap terms as a
     global load, one device call (``tl_overlap_feedback_host``): capacity difference,
     conductivity-gradient cross terms and the source scaling at the global quadrature
@@ -271,9 +278,10 @@ def overlap_feedback(problem: TwoLevelProblem, local_new: FieldState, local_old:
             raise UnsupportedOnDevice("full-mode overlap feedback needs a pointwise (gaussian) global source")
         peak, radius, depth, center = src.device_args()
         gs = N.Gaussian(float(peak), float(radius), float(depth), (C.c_double * 3)(*map(float, center)), 1)
-    Tn = np.ascontiguousarray(local_new.values, dtype=np.float64)
-    To = np.ascontiguousarray(local_old.values, dtype=np.float64)
-    out = np.zeros(gm.n_nodes)
+    from .fem import field_arg
+    Tn = field_arg(local_new)
+    To = field_arg(local_old)
+    out = N.DeviceVector(gm.n_nodes) if on_device else np.zeros(gm.n_nodes)
     gd, ld = gm.desc(), lm.desc()
     N.check(N.lib().tl_overlap_feedback_host(C.byref(gd), C.byref(ld), N.dptr(Tn), N.dptr(To), float(dt),
                                              C.byref(mg), C.byref(ml), C.byref(gs) if gs is not None else None,
@@ -284,18 +292,24 @@ def overlap_feedback(problem: TwoLevelProblem, local_new: FieldState, local_old:
 def solve_global(problem: TwoLevelProblem, state: TwoLevelState, dt: float,
                  local_for_coupling: FieldState, stats=None, predictor: bool = False) -> FieldState:
     """One global backward-Euler step on the device (``twolevel.py:242-271``)."""
-    from .ops import deposit_load
+    from .ops import add_loads, deposit_load
+    from .fem import device_fields
     t0, t1 = state.global_field.time, state.global_field.time + dt
-    load = transmission_load(local_for_coupling, state.gamma, problem.global_mesh,
-                             problem.mat_global, problem.mat_local)
+    dev = device_fields()
+    # equal conductivities: the interface functional is exactly zero (no load at all)
+    load = None
+    if not np.array_equal(problem.mat_global.conductivity_table, problem.mat_local.conductivity_table):
+        load = transmission_load(local_for_coupling, state.gamma, problem.global_mesh,
+                                 problem.mat_global, problem.mat_local, on_device=dev)
     dep = problem.global_source(t0, t1, predictor=predictor)
     source = None
     if isinstance(dep, GaussianSource):
         source = dep
     elif dep is not None:
-        load = load + deposit_load(problem.global_mesh, dep[0], dep[1])
+        load = add_loads(load, deposit_load(problem.global_mesh, dep[0], dep[1], on_device=dev))
     if problem.mode == "full":
-        load = load + overlap_feedback(problem, local_for_coupling, state.local_field, dt, t0, t1)
+        load = add_loads(load, overlap_feedback(problem, local_for_coupling, state.local_field, dt, t0, t1,
+                                                on_device=dev))
     timer = stats.timer("global_solve") if stats is not None else _Null()
     with timer:
         out = step_backward_euler(state.global_field, dt, problem.mat_global, source,
@@ -344,7 +358,7 @@ def two_level_iterate(problem: TwoLevelProblem, state: TwoLevelState, dt: float,
         inner0 = stats.seconds.get("global_solve", 0.0) + stats.seconds.get("local_solve", 0.0)
     for it in range(1, cs.max_iterations + 1):
         new_global = solve_global(problem, state, dt, latest_local, stats=stats)
-        raw = state.gamma.trace_of(new_global.values, problem.global_mesh)
+        raw = state.gamma.trace_of(new_global, problem.global_mesh)
         relax = 1.0 if (it == 1 and trace_start is None) else cs.omega
         trace = raw if problem.one_way else trace_prev + relax * (raw - trace_prev)
         new_local = solve_local(problem, local_from, local_dt, state.gamma, trace, stats=stats)
@@ -355,8 +369,7 @@ def two_level_iterate(problem: TwoLevelProblem, state: TwoLevelState, dt: float,
         if stats is not None:
             stats.count("coupling_iterations")
         if problem.one_way or change < cs.tolerance:
-            out = TwoLevelState(new_global, FieldState(new_local.mesh, new_local.values, t1),
-                                state.gamma, trace)
+            out = TwoLevelState(new_global, new_local.retimed(t1), state.gamma, trace)
             if stats is not None:
                 inner = (stats.seconds.get("global_solve", 0.0) + stats.seconds.get("local_solve", 0.0)
                          - inner0)
@@ -378,9 +391,13 @@ def relocate_local(state: TwoLevelState, policy, laser, direction, problem: TwoL
     new_mesh = StructuredGrid(moved)
     gmesh = problem.global_mesh
     gamma = extract_interface(new_mesh, gmesh)
-    values = interpolate_to_grid(gmesh, state.global_field.values, new_mesh)
-    local = FieldState(new_mesh, values, state.local_field.time)
-    trace = gamma.trace_of(state.global_field.values, gmesh)
+    from .fem import DeviceBackedFieldState, device_fields, field_arg
+    values = interpolate_to_grid(gmesh, field_arg(state.global_field), new_mesh, on_device=device_fields())
+    if isinstance(values, N.DeviceVector):
+        local = DeviceBackedFieldState(new_mesh, values, state.local_field.time)
+    else:
+        local = FieldState(new_mesh, values, state.local_field.time)
+    trace = gamma.trace_of(state.global_field, gmesh)
     return TwoLevelState(state.global_field, local, gamma, trace)
 
 
