@@ -555,9 +555,11 @@ __global__ void __launch_bounds__(kTPB, 2) k_pcg(PcgParams P) {
         status = 0;   // fem.py:275-276: zero solution
     } else {
         while (true) {
+            // scipy's cg: `for it in range(maxiter): if ||r|| < atol: return ok`, failure when
+            // the loop runs out -- the limit is tested before the residual
+            if (it >= P.maxiter) { status = 1; break; }
             if (rnorm < atol) { status = 0; break; }
             if (!isfinite(rnorm)) { status = 3; break; }
-            if (it >= P.maxiter) { status = 1; break; }
             const double rho = rz;
             const double beta = it > 0 ? rho / rho_prev : 0.0;
             const bool first = it == 0;

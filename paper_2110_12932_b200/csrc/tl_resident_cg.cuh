@@ -416,9 +416,11 @@ __global__ void __launch_bounds__(kResTPB, 1) k_pcg_resident_cg(ResCGParams RP) 
         double gam_prev = 1.0, alpha_prev = 1.0;
         while (true) {
             rnorm = sqrt(rr);
+            // scipy's cg: `for it in range(maxiter): if ||r|| < atol: return ok`, failure when
+            // the loop runs out -- the limit is tested before the residual
+            if (it >= P.maxiter) { status = 1; break; }
             if (rnorm < atol) { status = 0; break; }
             if (!isfinite(rnorm)) { status = 3; break; }
-            if (it >= P.maxiter) { status = 1; break; }
             const bool first = it == 0;
             const double beta = first ? 0.0 : gam / gam_prev;
             const double alpha = first ? gam / dlt : gam / (dlt - beta * gam / alpha_prev);

@@ -109,9 +109,9 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) k_sd_dir(SlabDev D, TPlan t
     const double rtol = __ldcg(&D.ctl->rtol);
     int status = -1;
     if (it == 0 && rr == 0.0) status = 0;                 // b = 0: x = 0 (fem.py:275-276)
+    else if (it >= __ldcg(&D.ctl->maxiter)) status = 1;   // scipy: the limit before the residual
     else if (rnorm < rtol * bnorm) status = 0;
     else if (!isfinite(rnorm)) status = 3;
-    else if (it >= __ldcg(&D.ctl->maxiter)) status = 1;
     if (status >= 0) {
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             D.ctl->status = status;

@@ -272,9 +272,11 @@ __global__ void __launch_bounds__(kSTPB, MINB) k_s_cg(PcgParams P, int Grhs) {
     const bool tail = blockIdx.x == G - 1 && ptail < g.n;
     if (bb != 0.0) {
         while (true) {
+            // scipy's cg: `for it in range(maxiter): if ||r|| < atol: return ok`, failure when
+            // the loop runs out -- the limit is tested before the residual
+            if (it >= P.maxiter) { status = 1; break; }
             if (rnorm < atol) { status = 0; break; }
             if (!isfinite(rnorm)) { status = 3; break; }
-            if (it >= P.maxiter) { status = 1; break; }
             const double rho = rz;
             const double beta = it > 0 ? rho / rho_prev : 0.0;
             const bool first = it == 0;

@@ -687,9 +687,11 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) k_t_cg(PcgParams P, int Grh
     unsigned seq = 0;        // sweep sequence number (counter slot seq & 3)
     if (bb != 0.0) {
         while (true) {
+            // scipy's cg: `for it in range(maxiter): if ||r|| < atol: return ok`, failure when
+            // the loop runs out -- the limit is tested before the residual
+            if (it >= P.maxiter) { status = 1; break; }
             if (rnorm < atol) { status = 0; break; }
             if (!isfinite(rnorm)) { status = 3; break; }
-            if (it >= P.maxiter) { status = 1; break; }
             const double rho = rz;
             const double beta = it > 0 ? rho / rho_prev : 0.0;
             const bool first = it == 0;
@@ -832,9 +834,9 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) k_tb_cg(const PcgParams* Ps
         if (threadIdx.x < B && !s_done[threadIdx.x]) {
             const int s = threadIdx.x;
             int st = -1;
-            if (s_rnorm[s] < s_atol[s]) st = 0;
+            if (it >= Ps[s].maxiter) st = 1;              // scipy: the limit before the residual
+            else if (s_rnorm[s] < s_atol[s]) st = 0;
             else if (!isfinite(s_rnorm[s])) st = 3;
-            else if (it >= Ps[s].maxiter) st = 1;
             if (st >= 0) {
                 s_done[s] = 1;
                 s_status[s] = st;

@@ -82,6 +82,101 @@ def test_nonconvergence_maps_to_reference_exception():
     assert exc.value.iterations == 2
 
 
+_LIMIT_SCRIPT = r"""
+import sys, json, numpy as np
+sys.path.insert(0, {root!r})
+import paper_2110_12932_b200 as P
+from paper_2110_12932_b200 import _native as N, ops
+from paper_2110_12932_b200.control import LocalPlacement
+from paper_2110_12932_b200.grid import StructuredGrid
+z = np.load({golden!r})
+grid = StructuredGrid(LocalPlacement(P.Box(tuple(z["lo"]), tuple(z["hi"])), np.asarray(z["ncells"])))
+out = []
+for maxiter in {limits!r}:
+    x, info = ops.step(grid, 9.8, 8440 * 410.0, float(z["dt"]), N.TL_DIRICHLET_BOTTOM, z["T_old"],
+                       g_const=293.0, load=z["extra"], rtol=1e-12, maxiter=maxiter)
+    out.append([int(info.status), int(info.iterations)])
+print(json.dumps(out))
+"""
+
+
+@pytest.mark.parametrize("env", [{}, {"TLGPU_EXACT_CG": "1"}, {"TLGPU_STREAMING": "1", "TLGPU_TILED_MIN": "1"},
+                                 {"TLGPU_STREAMING": "1", "TLGPU_TILED": "0"}])
+def test_linear_cg_at_the_iteration_limit_follows_scipy(env):
+    """scipy's cg tests ||r|| < atol at the top of each of its maxiter loop passes and reports
+    failure when the loop runs out (``fem.py:283-288`` then raises NonConvergence): a solve
+    that needs `its` iterations fails with maxiter = its and converges with maxiter = its + 1.
+    Every linear kernel family (SMEM-resident CG-CG, the scipy-exact two-barrier kernel, the
+    bulk-copy streaming loop, the flat streaming loop) against the oracle's scipy mirror;
+    solver switches are read once per process, so each runs in a subprocess."""
+    import os
+    import subprocess
+    import sys
+    from oracle.pcg import solve_constrained
+    z = np.load(GOLDEN / "op_cfg1_global.npz")
+    grid = _grid(z["lo"], z["hi"], z["ncells"])
+    G = kuhn.KuhnGrid(grid.placement.box0.lo, grid.placement.box0.hi, grid.ncells, grid.placement.offset)
+    op = kuhn.StencilOperator(G, 9.8, 8440 * 410.0, float(z["dt"]), G.bottom_mask())
+    g = np.full(grid.n_nodes, 293.0)
+    _, its, _ = solve_constrained(op, op.rhs(z["T_old"], z["extra"], g), g, 1e-12)
+    code = _LIMIT_SCRIPT.format(root=str(ROOT), golden=str(GOLDEN / "op_cfg1_global.npz"), limits=[3, its, its + 1])
+    res = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True, text=True,
+                         timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    got = json.loads(res.stdout.strip().splitlines()[-1])
+    assert got == [[N.TL_SOLVE_MAXITER, 3], [N.TL_SOLVE_MAXITER, its], [N.TL_SOLVE_OK, its]], (got, its)
+
+
+def test_vc_cg_at_the_iteration_limit_follows_scipy():
+    """The same rule for the variable-coefficient Jacobi-PCG (k_vc_cg) of the Picard path,
+    against the oracle's assembly + scipy mirror (nothing exercised the vc
+    path at maxiter)."""
+    import ctypes as C
+    from oracle import varcoef
+    from oracle.pcg import cg_mirror
+    from .test_oracle_golden import picard_material
+    z = np.load(GOLDEN / "picard_tables.npz")
+    grid = P.build_structured_grid(P.Box(tuple(z["lo"]), tuple(z["hi"])), float(z["h"]))
+    mat = picard_material(z)
+    G = kuhn.KuhnGrid(grid.box.lo, grid.box.hi, grid.ncells)
+    n = grid.n_nodes
+    nodes = grid.nodes_on(P.BOTTOM)
+    dmask = np.zeros(n, dtype=bool)
+    dmask[nodes] = True
+    g = np.full(n, 293.0)
+    diag, w, b = varcoef.assemble(G, mat, z["T_old"], z["T_old"], float(z["dt"]), None, False, None)
+    dc, wc, bc = varcoef.constrained(G, diag, w, b, dmask, g)
+    xref, info0, its = cg_mirror(lambda v: varcoef.apply(G, dc, wc, v), bc, 1.0 / dc, 1e-12, 20 * n)
+    assert info0 == 0 and its > 3
+    md, _tabs = P.fem.vc_material(mat, False)
+    desc = grid.desc()
+    rb = N.Robin(0.0, 0.0, 293.0, 0)
+    idx = np.ascontiguousarray(nodes, dtype=np.int32)
+    vals = np.full(idx.size, 293.0)
+    T_old = np.ascontiguousarray(z["T_old"], dtype=np.float64)
+
+    def solve(maxiter):
+        x = np.empty(n)
+        info = N.SolveInfo()
+        npass, inc = C.c_int32(0), C.c_double(0.0)
+        its_ = np.zeros(1, dtype=np.int32)
+        ms = np.zeros(1, dtype=np.float32)
+        N.check(N.lib().tl_vc_picard_nodes_host(
+            C.byref(desc), C.byref(md), None, None, 0, float(z["dt"]), N.dptr(T_old), None, None, C.byref(rb),
+            idx.ctypes.data, idx.size, N.dptr(vals), 1e-12, int(maxiter), 1, 1e-8, 1, N.dptr(x), C.byref(npass),
+            its_.ctypes.data, ms.ctypes.data, C.byref(inc), C.byref(info)), "step")
+        return x, info
+
+    for maxiter, status in ((3, N.TL_SOLVE_MAXITER), (its, N.TL_SOLVE_MAXITER), (its + 1, N.TL_SOLVE_OK)):
+        x, info = solve(maxiter)
+        assert info.status == status, (maxiter, its, info.status, info.iterations)
+        assert info.iterations == min(maxiter, its)
+    assert rel(x, np.where(dmask, g, xref)) <= REL
+    with pytest.raises(NonConvergence) as exc:
+        ops.raise_for(solve(its)[1])
+    assert exc.value.iterations == its
+
+
 def test_interpolation_points_vs_golden():
     z = np.load(GOLDEN / "interp.npz")
     box = P.Box(tuple(z["lo"]), tuple(z["hi"]))

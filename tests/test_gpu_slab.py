@@ -122,6 +122,24 @@ def test_slab_single_rank_cfg3_streaming_size():
     assert rel(x, ref) <= 1e-12
 
 
+def test_slab_solve_at_the_iteration_limit_follows_scipy():
+    """The device-resident slab CG stops like scipy's cg: with maxiter = the iterations the
+    solve needs it reports failure, with one more it converges (same rule as the fused
+    kernels, tests/test_gpu_parity.py::test_linear_cg_at_the_iteration_limit_follows_scipy)."""
+    import torch
+    cfg, grid, T, load, _ = _case("cfg1_m4", 0, False)
+    _, info, _ = _single("cfg1_m4", 0, False)
+    its = info.iterations
+    for maxiter, status in ((its, N.TL_SOLVE_MAXITER), (its + 1, N.TL_SOLVE_OK), (2, N.TL_SOLVE_MAXITER)):
+        S = SL.SlabGlobalSolver(grid, 9.8, 8440 * 410.0, rank=0, world=1, device="cuda:0", rtol=1e-12,
+                                maxiter=maxiter)
+        S.set_own(S.x, T)
+        S.set_own(S.load, load)
+        got = S.step(cfg.dt_macro, 293.0, with_load=True)
+        torch.cuda.synchronize()
+        assert got.status == status and got.iterations == min(maxiter, its), (maxiter, its, got)
+
+
 # ---- whole multirate runs with the global grid on slabs ----------------------------
 
 def _run_worker(rank, world, port, name, n_steps, q):
