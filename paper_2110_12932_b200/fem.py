@@ -220,9 +220,9 @@ def _dirichlet_kind(mesh: StructuredGrid, nodes: np.ndarray) -> int:
     nodes = np.asarray(nodes, dtype=np.int64)
     if np.array_equal(nodes, mesh.nodes_on(BOTTOM)):
         return N.TL_DIRICHLET_BOTTOM
-    if np.array_equal(nodes, np.nonzero(mesh.gamma_mask())[0]):
+    if np.array_equal(nodes, mesh.gamma_nodes()):
         return N.TL_DIRICHLET_GAMMA
-    raise UnsupportedOnDevice("the device represents the bottom-face or interface Dirichlet sets only")
+    return -1          # any other set (none, all nodes, ...): the general path's node mask
 
 
 @dataclass(frozen=True)
@@ -392,12 +392,16 @@ def step_backward_euler(state: FieldState, dt: float, mat, source, bounds: Bound
         raise UnsupportedOnDevice("the device evaluates GaussianSource objects, not opaque callables")
     # 2D grids (P1 triangles, csrc/tl_2d.cuh) always take the general path: the fused linear
     # kernels are the 3D 27-class stencil
-    if _needs_general_path(mat, bounds, latent) or latent_mask is not None or state.mesh.dim == 2:
+    # ... and so do Dirichlet sets other than the bottom face / the interface (the fused
+    # kernels know those two as node classes; the general path takes any node mask)
+    kind = -1
+    if not (_needs_general_path(mat, bounds, latent) or latent_mask is not None or state.mesh.dim == 2):
+        kind = _dirichlet_kind(state.mesh, bounds.dirichlet_nodes)
+    if kind < 0:
         return _step_general(state, dt, mat, source, bounds, settings, latent, extra_load, stats,
                              latent_mask=latent_mask)
     check_linear_problem(mat, bounds, latent)
     mesh = state.mesh
-    kind = _dirichlet_kind(mesh, bounds.dirichlet_nodes)
     kappa, rho_c = material_constants(mat)
     darr = bounds.dirichlet_array()
     g_const, dlist = 0.0, None

@@ -110,17 +110,19 @@ class TwoLevelProblem:
     @property
     def one_way(self) -> bool:
         a, b = self.mat_global, self.mat_local
-        if a is b:
-            return True
-        same_k = (a.conductivity_table.shape == b.conductivity_table.shape
-                  and np.array_equal(a.conductivity_table, b.conductivity_table))
+        same_k = a is b or (a.conductivity_table.shape == b.conductivity_table.shape
+                            and np.array_equal(a.conductivity_table, b.conductivity_table))
         if not same_k:
             return False
         if self.mode == "alternate":
             return True
-        same_c = (a.heat_capacity_table.shape == b.heat_capacity_table.shape
-                  and np.array_equal(a.heat_capacity_table, b.heat_capacity_table))
-        return same_c and a.rho == b.rho and a.chi == b.chi and b.chi == 0.0
+        # full mode: the overlap terms vanish only for fully equal materials without latent
+        # heat (twolevel.py:101-113) -- one material object on both levels included
+        same = a is b or (a.heat_capacity_table.shape == b.heat_capacity_table.shape
+                          and np.array_equal(a.heat_capacity_table, b.heat_capacity_table)
+                          and a.rho == b.rho and a.chi == b.chi
+                          and (a.T_solidus, a.T_liquidus, a.S) == (b.T_solidus, b.T_liquidus, b.S))
+        return bool(same and b.chi == 0.0)
 
     @property
     def interval_source(self) -> bool:

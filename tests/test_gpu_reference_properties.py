@@ -1,0 +1,416 @@
+"""The reference's own property tests for the hot path, restated against the device API.
+
+The reference pins its path with invariants (``pkg/tests/test_multirate.py``,
+``test_twolevel.py``, ``test_fem.py``): solve counters of a macro step, exact time
+bookkeeping, m = 1 degenerating to uniform stepping, preserved equilibria, linearity of the
+interface functional, the coupled pair reproducing the monolithic solve on identical
+discretisations, ...  Those tests run on toy 2D boxes through source closures; these hold
+the same statements on small 3D plates (and one 2D plate) through this package's seams --
+the device-resident run where the problem allows it, the step-level drivers otherwise.
+Each test names the reference test it restates.
+"""
+
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2110_12932_b200 as P
+from paper_2110_12932_b200.multirate import predictor_global
+from paper_2110_12932_b200.twolevel import (consistency_diagnostic, transmission_load, two_level_iterate)
+
+pytestmark = pytest.mark.gpu
+
+ROOT = Path(__file__).resolve().parents[1]
+CONFIGS = ROOT / "configs"
+T0 = 300.0
+BC0 = P.ThermalBC(0.0, 0.0, T0, T0)
+CG = P.SolverSettings(picard_tol=1e-9, picard_max_iter=40, linear_tol=1e-12, linear_solver="cg")
+
+
+def material(k_lo=10.0, k_hi=10.0, c_lo=400.0, c_hi=400.0, chi=0.0, Ts=1563.15, Tl=1653.15):
+    return P.Material(np.array([[200.0, k_lo], [5000.0, k_hi]]), np.array([[200.0, c_lo], [5000.0, c_hi]]),
+                      8000.0, chi, Ts, Tl, 0.05)
+
+
+def plates(h_local=5e-5):
+    """2 x 1 x 0.5 mm plate at h = 0.1 mm; a 0.8 x 0.6 x 0.3 mm local box flush with the top."""
+    gm = P.build_structured_grid(P.Box((0.0, 0.0, 0.0), (2e-3, 1e-3, 5e-4)), 1e-4)
+    lm = P.build_structured_grid(P.Box((6e-4, 2e-4, 2e-4), (1.4e-3, 8e-4, 5e-4)), h_local)
+    return gm, lm
+
+
+def problem_of(mat_g, mat_l, bc=BC0, beam=None, omega=1.0, mode="alternate", source_global="gaussian",
+               moving=False, tol=1e-6):
+    gm, lm = plates()
+    path = None
+    if beam is not None:
+        a, b = (8e-4, 5e-4, 5e-4), ((1.2e-3, 5e-4, 5e-4) if moving else (8e-4 + 1e-9, 5e-4, 5e-4))
+        path = P.path_from_segments([(a, b, beam.speed)])
+    prob = P.TwoLevelProblem(global_mesh=gm, mat_global=mat_g, mat_local=mat_l, bc=bc, solver=CG,
+                             coupling=P.CouplingSettings(omega=omega, tolerance=tol, max_iterations=60),
+                             mode=mode, beam=beam, path=path, source_global=source_global)
+    return prob, lm
+
+
+def moving_beam():
+    return P.LaserBeam(150.0, 0.4, 1e-4, 1e-4, 0.8)            # 0.4 mm of track in 0.5 ms
+
+
+def parked_beam(power=150.0):
+    return P.LaserBeam(power, 0.4, 1e-4, 1e-4, 1e-9 / 1e-3)    # 1 nm in 1 ms: a stationary spot
+
+
+# ---- test_multirate.py ------------------------------------------------------------------
+
+def test_predictor_preserves_constant_state():
+    """test_multirate.py::test_predictor_preserves_constant_state"""
+    mat = material()
+    prob, lm = problem_of(mat, mat)
+    state = P.initial_state(prob, lm, P.uniform_field(prob.global_mesh, T0))
+    pred = predictor_global(prob, state, 1e-4)
+    assert np.allclose(pred.values, T0, atol=1e-10)
+
+
+@pytest.mark.parametrize("source_global,resident", [("gaussian", False), ("distributed", True)])
+def test_macro_step_solve_counters(source_global, resident):
+    """test_macro_step_counts_local_solves (instant-based coarse source: the corrector
+    re-solves the coarse step) and test_interval_source_reuses_predictor (interval-based
+    source + one-way coupling: it does not)."""
+    mat = material()
+    prob, lm = problem_of(mat, mat, beam=moving_beam(), source_global=source_global, moving=True)
+    assert prob.one_way and prob.device_resident == resident
+    sched = P.MacroSchedule(1e-4, 5 if not resident else 4, 0.0, 3e-4)
+    stats = P.RunStats()
+    P.run_spacetime(prob, sched, lm, P.uniform_field(prob.global_mesh, T0), stats=stats)
+    n, m = sched.n_macro, sched.micro_per_macro
+    c = stats.counters
+    assert c["coupling_iterations"] == n                       # one corrector pass per macro step
+    assert c["local_solves"] == n * m + n
+    assert c["predictor_solves"] == n
+    assert c["global_solves"] == (n if resident else 2 * n)    # predictor reused / predictor + corrector
+
+
+@pytest.mark.parametrize("source_global", ["gaussian", "distributed"])
+def test_time_bookkeeping_exact(source_global):
+    """test_multirate.py::test_time_bookkeeping_exact: recorder times are the schedule's own
+    floating-point expressions on both drivers."""
+    mat = material()
+    prob, lm = problem_of(mat, mat, beam=moving_beam(), source_global=source_global, moving=True)
+    sched = P.MacroSchedule(1e-4, 3, 0.0, 5e-4)
+    times = []
+    P.run_spacetime(prob, sched, lm, P.uniform_field(prob.global_mesh, T0),
+                    recorder=lambda kind, t, *a: times.append((kind, t)))
+    assert [t for k, t in times if k == "macro"] == [sched.t_macro(k + 1) for k in range(5)]
+    assert [t for k, t in times if k == "micro"] == [sched.t_micro(k, i) for k in range(5) for i in range(1, 4)]
+    assert sched.t_macro(3) == 0.0 + 3 * 1e-4 and sched.t_micro(2, 1) == 0.0 + 2 * 1e-4 + 1 * (1e-4 / 3)
+
+
+def test_m_equal_one_degenerates_to_space_stepping_oneway():
+    """test_multirate.py::test_m_equal_one_degenerates_to_space_stepping_oneway: with one
+    micro step per macro step the two drivers perform identical solves."""
+    mat = material()
+    prob, lm = problem_of(mat, mat, beam=moving_beam(), moving=True)
+    U = P.uniform_field(prob.global_mesh, T0)
+    st = P.run_spacetime(prob, P.MacroSchedule(5e-5, 1, 0.0, 2.5e-4), lm, U)
+    ss = P.run_space(prob, 5e-5, 5, lm, U)
+    assert st.local_field.values.max() > T0 + 50.0
+    np.testing.assert_allclose(st.local_field.values, ss.local_field.values, rtol=1e-12, atol=0)
+    np.testing.assert_allclose(st.global_field.values, ss.global_field.values, rtol=1e-12, atol=0)
+
+
+def test_m_equal_one_degenerates_two_way():
+    """test_multirate.py::test_m_equal_one_degenerates_two_way"""
+    prob, lm = problem_of(material(4.0, 4.0), material(10.0, 10.0), beam=moving_beam(), moving=True)
+    assert not prob.one_way
+    U = P.uniform_field(prob.global_mesh, T0)
+    st = P.run_spacetime(prob, P.MacroSchedule(5e-5, 1, 0.0, 2.5e-4), lm, U)
+    ss = P.run_space(prob, 5e-5, 5, lm, U)
+    diff = np.linalg.norm(st.local_field.values - ss.local_field.values) / np.linalg.norm(ss.local_field.values)
+    assert diff < 10 * prob.coupling.tolerance
+
+
+def test_predictor_error_decreases_with_macro_step():
+    """test_multirate.py::test_predictor_error_decreases_with_macro_step (two-way coupling,
+    so the corrector changes the coarse field)."""
+    errs = []
+    for dt, micro in ((2e-4, 4), (1e-4, 2), (5e-5, 1)):
+        prob, lm = problem_of(material(4.0, 4.0), material(10.0, 10.0), beam=moving_beam(), moving=True)
+        preds, corr = {}, {}
+
+        def rec(kind, t, local, glob, iters):
+            if kind == "predictor":
+                preds[round(t, 12)] = glob.values
+            elif kind == "macro":
+                corr[round(t, 12)] = glob.values
+
+        P.run_spacetime(prob, P.MacroSchedule(dt, micro, 0.0, 2e-4), lm, P.uniform_field(prob.global_mesh, T0),
+                        recorder=rec)
+        errs.append(np.linalg.norm(preds[2e-4] - corr[2e-4]) / np.linalg.norm(corr[2e-4]))
+    assert errs[0] > errs[1] > errs[2] > 0.0
+
+
+@pytest.mark.parametrize("source_global", ["gaussian", "distributed"])
+def test_corrector_resolves_final_micro_interval(source_global):
+    """test_multirate.py::test_corrector_resolves_final_micro_interval: the macro record is
+    the run's final local field, and it differs from the provisional last micro field (which
+    ran on the lagged trace blend) only through the corrector's re-solve."""
+    mat = material()
+    prob, lm = problem_of(mat, mat, beam=moving_beam(), source_global=source_global, moving=True)
+    rec = {}
+    state = P.run_spacetime(prob, P.MacroSchedule(1e-4, 4, 0.0, 1e-4), lm, P.uniform_field(prob.global_mesh, T0),
+                            recorder=lambda kind, t, local, glob, it: rec.setdefault(kind, []).append((t, local, glob)))
+    t, local, glob = rec["macro"][-1]
+    np.testing.assert_array_equal(local.values, state.local_field.values)
+    t_mic, last_micro, _ = rec["micro"][-1]
+    assert t_mic == t == 1e-4
+    assert last_micro.values.shape == local.values.shape
+    assert np.abs(last_micro.values - local.values).max() < 0.05 * (local.values.max() - T0)
+
+
+# ---- test_twolevel.py -------------------------------------------------------------------
+
+def test_transmission_functional_properties():
+    """test_transmission_zero_for_equal_conductivity, ..._zero_for_constant_local_field,
+    ..._linear_in_local_field (the hand-computed case is
+    test_gpu_parity.py::test_transmission_of_linear_field_is_bottom_flux)."""
+    gm, lm = plates()
+    gamma = P.extract_interface(lm, gm)
+    X = lm.coords
+    u = P.FieldState(lm, T0 + 4e7 * X[:, 0] * X[:, 1] + 3e4 * X[:, 2], 0.0)
+    v = P.FieldState(lm, T0 + 200.0 * np.sin(3e3 * X[:, 0]) + 5e4 * X[:, 2], 0.0)
+    same = transmission_load(u, gamma, gm, material(), material())
+    assert np.all(np.asarray(same) == 0.0)
+    const = transmission_load(P.uniform_field(lm, 500.0), gamma, gm, material(10.0, 10.0), material(5.0, 5.0))
+    assert np.allclose(const, 0.0, atol=1e-18)
+    mg, ml = material(10.0, 10.0), material(4.0, 4.0)
+    fu, fv = transmission_load(u, gamma, gm, mg, ml), transmission_load(v, gamma, gm, mg, ml)
+    w = P.FieldState(lm, 2.0 * u.values - 0.5 * v.values, 0.0)
+    fw = transmission_load(w, gamma, gm, mg, ml)
+    assert np.abs(fu).max() > 0.0
+    assert np.abs(fw - (2.0 * fu - 0.5 * fv)).max() <= 1e-11 * np.abs(fw).max()
+
+
+def test_local_constant_trace_no_source():
+    """test_twolevel.py::test_local_constant_trace_no_source"""
+    mat = material()
+    prob, lm = problem_of(mat, mat)
+    state = P.initial_state(prob, lm, P.uniform_field(prob.global_mesh, T0))
+    out = P.solve_local(prob, state.local_field, 1e-4, state.gamma, np.full(state.gamma.trace_nodes.size, T0))
+    assert np.allclose(out.values, T0, atol=1e-10)
+
+
+def test_local_reproduces_linear_global_trace():
+    """test_twolevel.py::test_local_reproduces_linear_global_trace: a field linear in x and y
+    is P1-exact, harmonic and flux-free through the top face, so the local step keeps it."""
+    mat = material(15.0, 15.0)
+    prob, lm = problem_of(mat, mat)
+    gm = prob.global_mesh
+    lin = P.FieldState(gm, T0 + 1.2e4 * gm.coords[:, 0] + 5e3 * gm.coords[:, 1], 0.0)
+    state = P.initial_state(prob, lm, lin)
+    trace = state.gamma.trace_of(lin, gm)
+    out = P.solve_local(prob, state.local_field, 1e-4, state.gamma, trace)
+    expect = T0 + 1.2e4 * lm.coords[:, 0] + 5e3 * lm.coords[:, 1]
+    assert np.allclose(out.values, expect, atol=1e-8)
+    np.testing.assert_array_equal(out.values[state.gamma.trace_nodes], trace)
+
+
+def test_decoupled_case_converges_immediately():
+    """test_twolevel.py::test_decoupled_case_converges_immediately"""
+    mat = material()
+    prob, lm = problem_of(mat, mat)
+    assert prob.one_way
+    state = P.initial_state(prob, lm, P.uniform_field(prob.global_mesh, T0))
+    new, iters = two_level_iterate(prob, state, 1e-4)
+    assert iters <= 2
+    assert np.allclose(new.global_field.values, T0, atol=1e-10)
+    assert np.allclose(new.local_field.values, T0, atol=1e-10)
+
+
+def test_equilibrium_preserved_with_zero_source():
+    """test_twolevel.py::test_equilibrium_preserved_with_zero_source: convection and
+    radiation against the ambient temperature leave a field at that temperature alone."""
+    mat = material(10.0, 25.0, 400.0, 700.0)
+    prob, lm = problem_of(mat, mat, bc=P.ThermalBC(20.0, 0.4, T0, T0))
+    state = P.initial_state(prob, lm, P.uniform_field(prob.global_mesh, T0))
+    state, _ = two_level_iterate(prob, state, 5e-4)
+    assert np.allclose(state.global_field.values, T0, atol=1e-9)
+    assert np.allclose(state.local_field.values, T0, atol=1e-9)
+
+
+def test_two_way_coupling_converges_and_is_omega_independent():
+    """test_twolevel.py::test_two_way_coupling_converges_and_is_omega_independent"""
+    mg, ml = material(4.0, 4.0), material(10.0, 10.0)
+    bc = P.ThermalBC(10.0, 0.0, T0, T0)
+    p1, lm = problem_of(mg, ml, bc=bc, beam=parked_beam(), omega=1.0)
+    p2, _ = problem_of(mg, ml, bc=bc, beam=parked_beam(), omega=0.5)
+    assert not p1.one_way
+    s1 = P.initial_state(p1, lm, P.uniform_field(p1.global_mesh, T0))
+    s2 = P.initial_state(p2, lm, P.uniform_field(p2.global_mesh, T0))
+    o1, it1 = two_level_iterate(p1, s1, 1e-4)
+    o2, it2 = two_level_iterate(p2, s2, 1e-4)
+    assert it1 >= 2 and it2 >= it1
+    assert o1.local_field.values.max() > T0 + 50.0
+    diff = np.linalg.norm(o1.local_field.values - o2.local_field.values) / np.linalg.norm(o1.local_field.values)
+    assert diff < 10 * p1.coupling.tolerance
+
+
+def test_iterate_idempotent_at_fixed_point():
+    """test_twolevel.py::test_iterate_idempotent_at_fixed_point"""
+    prob, lm = problem_of(material(4.0, 4.0), material(10.0, 10.0), bc=P.ThermalBC(10.0, 0.0, T0, T0),
+                          beam=parked_beam())
+    state = P.initial_state(prob, lm, P.uniform_field(prob.global_mesh, T0))
+    state, _ = two_level_iterate(prob, state, 1e-4)
+    again, _ = two_level_iterate(prob, state, 1e-14)
+    scale = max(np.linalg.norm(state.trace), 1e-12)
+    assert np.linalg.norm(again.trace - state.trace) / scale < prob.coupling.tolerance
+
+
+def test_coupled_matches_monolithic_identical_discretization():
+    """test_twolevel.py::test_coupled_matches_monolithic_identical_discretization: equal
+    materials, matching lattices and steps -- the coupled pair reproduces the single-grid
+    solve up to solver tolerances."""
+    mat = material(10.0, 25.0, 400.0, 700.0)
+    bc = P.ThermalBC(10.0, 0.0, T0, T0)
+    gm, _ = plates()
+    lm = P.build_structured_grid(P.Box((6e-4, 2e-4, 2e-4), (1.4e-3, 8e-4, 5e-4)), 1e-4)
+    beam = parked_beam()
+    path = P.path_from_segments([((8e-4, 5e-4, 5e-4), (8e-4 + 1e-9, 5e-4, 5e-4), beam.speed)])
+    prob = P.TwoLevelProblem(global_mesh=gm, mat_global=mat, mat_local=mat, bc=bc, solver=CG, beam=beam, path=path,
+                             source_global="gaussian")
+    U = P.uniform_field(gm, T0)
+    state = P.initial_state(prob, lm, U)
+    dt, n = 5e-5, 4
+    for _ in range(n):
+        state, _ = two_level_iterate(prob, state, dt)
+    ref = P.solve_monolithic(gm, mat, prob.local_source, lambda t: prob.global_bounds(), dt, n, U, settings=CG,
+                             latent=False)
+    ref_local = gm.interpolate(ref.values[-1], lm.coords)
+    assert ref.values[-1].max() > T0 + 50.0
+    rel_l = np.linalg.norm(state.local_field.values - ref_local) / np.linalg.norm(ref_local)
+    rel_g = np.linalg.norm(state.global_field.values - ref.values[-1]) / np.linalg.norm(ref.values[-1])
+    assert rel_l < 1e-6 and rel_g < 1e-8
+
+
+def test_full_and_alternate_modes_differ_only_on_overlap():
+    """test_twolevel.py::test_full_and_alternate_modes_differ_only_on_overlap: with latent heat
+    active in the fine problem the full form feeds it back into the coarse one, inside the
+    local box."""
+    mat = material(10.0, 16.0, 400.0, 400.0, chi=2.0e5, Ts=600.0, Tl=900.0)
+    bc = P.ThermalBC(10.0, 0.0, T0, T0)
+    p_alt, lm = problem_of(mat, mat, bc=bc, beam=parked_beam(250.0), mode="alternate")
+    p_full, _ = problem_of(mat, mat, bc=bc, beam=parked_beam(250.0), mode="full")
+    assert p_alt.one_way and not p_full.one_way
+    s_alt = P.initial_state(p_alt, lm, P.uniform_field(p_alt.global_mesh, T0))
+    s_full = P.initial_state(p_full, lm, P.uniform_field(p_full.global_mesh, T0))
+    for _ in range(5):
+        s_alt, _ = two_level_iterate(p_alt, s_alt, 1e-4)
+        s_full, _ = two_level_iterate(p_full, s_full, 1e-4)
+    assert s_alt.local_field.values.max() > mat.T_solidus          # melting must occur
+    diff = np.abs(s_full.global_field.values - s_alt.global_field.values)
+    assert diff.max() > 1e-6
+    gm = p_alt.global_mesh
+    inside = lm.box.contains(gm.coords, tol=1e-12)
+    assert diff[inside].max() > 10 * diff[~inside].max()
+
+
+def test_consistency_diagnostic_zero_for_identical_fields():
+    """test_twolevel.py::test_consistency_diagnostic_zero_for_identical_fields"""
+    mat = material()
+    prob, lm = problem_of(mat, mat)
+    gm = prob.global_mesh
+    state = P.initial_state(prob, lm, P.uniform_field(gm, 321.0))
+    out = consistency_diagnostic(state, P.uniform_field(gm, 321.0), gm)
+    for key in ("local", "overlap", "exterior"):
+        assert out[key] == pytest.approx(0.0, abs=1e-12) and out[key] >= 0
+
+
+def test_time_stamp_mismatch_rejected():
+    """test_twolevel.py::test_time_stamp_mismatch_rejected"""
+    mat = material()
+    prob, lm = problem_of(mat, mat)
+    state = P.initial_state(prob, lm, P.uniform_field(prob.global_mesh, T0))
+    with pytest.raises(P.CouplingError):
+        two_level_iterate(prob, state, 1e-4, local_from=state.local_field, local_dt=5e-5)
+
+
+# ---- test_fem.py ------------------------------------------------------------------------
+
+def _bottom(grid, bc=BC0, value=T0, radiation=False, tags=(P.TOP,)):
+    return P.BoundarySpec(bc=bc, robin_tags=tags, radiation=radiation, dirichlet_nodes=grid.nodes_on(P.BOTTOM),
+                          dirichlet_values=value)
+
+
+@pytest.mark.parametrize("tdep", [False, True])
+def test_constant_state_preserved_adiabatic(tdep):
+    """test_fem.py::test_constant_state_preserved_adiabatic (fused linear solve and Picard path)"""
+    gm, _ = plates()
+    mat = material(10.0, 25.0, 400.0, 700.0) if tdep else material()
+    out = P.step_backward_euler(P.uniform_field(gm, 450.0), 1e-4, mat, None, _bottom(gm, value=450.0), CG)
+    assert np.allclose(out.values, 450.0, atol=1e-10)
+
+
+def test_fixed_dirichlet_everywhere_returns_boundary_value():
+    """test_fem.py::test_fixed_dirichlet_everywhere_returns_boundary_value"""
+    gm, _ = plates()
+    rng = np.random.default_rng(2)
+    g = rng.uniform(300.0, 900.0, gm.n_nodes)
+    bounds = P.BoundarySpec(bc=BC0, robin_tags=(), radiation=False, dirichlet_nodes=np.arange(gm.n_nodes),
+                            dirichlet_values=g)
+    out = P.step_backward_euler(P.uniform_field(gm, 500.0), 1e-4, material(10.0, 25.0), None, bounds, CG)
+    np.testing.assert_array_equal(out.values, g)
+
+
+def test_linear_problem_converges_in_one_picard_iteration():
+    """test_fem.py::test_linear_problem_converges_in_one_picard_iteration"""
+    gm, _ = plates()
+    rng = np.random.default_rng(3)
+    stats = P.RunStats()
+    st = P.FieldState(gm, rng.uniform(300.0, 900.0, gm.n_nodes), 0.0)
+    P.step_backward_euler(st, 1e-4, material(), None, _bottom(gm), CG, stats=stats)
+    assert stats.counters["picard_iterations"] == 1
+    stats2 = P.RunStats()
+    P.step_backward_euler(st, 1e-4, material(10.0, 25.0, 400.0, 700.0), None, _bottom(gm), CG, stats=stats2)
+    assert stats2.counters["picard_iterations"] > 1
+
+
+@pytest.mark.parametrize("tdep", [False, True])
+def test_discrete_maximum_principle_dirichlet_band(tdep):
+    """test_fem.py::test_discrete_maximum_principle_dirichlet_band: without sources the new
+    field stays within the range of the old field and the boundary data (M-matrix: lumped
+    mass, non-obtuse Kuhn tets)."""
+    gm, _ = plates()
+    rng = np.random.default_rng(4)
+    st = P.FieldState(gm, rng.uniform(350.0, 800.0, gm.n_nodes), 0.0)
+    mat = material(10.0, 25.0, 400.0, 700.0) if tdep else material()
+    out = P.step_backward_euler(st, 2e-4, mat, None, _bottom(gm, value=320.0), CG)
+    assert out.values.min() >= 320.0 - 1e-9 and out.values.max() <= 800.0 + 1e-9
+
+
+def test_energy_balance_with_source():
+    """test_fem.py::test_energy_balance_with_source: adiabatic walls and no Dirichlet set --
+    the lumped heat content rises by the discrete load times dt (and the discrete load is the
+    absorbed power up to quadrature error)."""
+    from oracle import kuhn
+    gm, _ = plates()
+    beam = P.LaserBeam(150.0, 0.4, 1e-4, 1e-4, 0.8)
+    src = P.GaussianSource(beam, (1e-3, 5e-4, 3e-4))
+    dt = 1e-4
+    out = P.step_backward_euler(P.uniform_field(gm, T0), dt, material(), src,
+                                P.BoundarySpec(bc=BC0, robin_tags=(), radiation=False), CG)
+    G = kuhn.KuhnGrid(gm.box.lo, gm.box.hi, gm.ncells)
+    lumped = float(np.prod(G.h)) * G.node_incidence().ravel() / 24.0
+    gained = 8000.0 * 400.0 * float(np.dot(lumped, out.values - T0))
+    load = float(np.sum(kuhn.gaussian_load(G, beam, src.center)))
+    assert gained == pytest.approx(load * dt, rel=1e-9)
+    assert out.values.max() > T0 + 10.0
+
+
+def test_monolithic_constant_trajectory():
+    """test_fem.py::test_monolithic_constant_trajectory"""
+    gm, _ = plates()
+    traj = P.solve_monolithic(gm, material(), lambda t: None, lambda t: _bottom(gm), 1e-4, 3,
+                              P.uniform_field(gm, T0), settings=CG, latent=False)
+    assert len(traj) == 4 and traj.times == [0.0] + [0.0 + k * 1e-4 for k in range(1, 4)]
+    for v in traj.values:
+        assert np.allclose(v, T0, atol=1e-10)
