@@ -414,3 +414,92 @@ def test_monolithic_constant_trajectory():
     assert len(traj) == 4 and traj.times == [0.0] + [0.0 + k * 1e-4 for k in range(1, 4)]
     for v in traj.values:
         assert np.allclose(v, T0, atol=1e-10)
+
+
+def test_radiation_fixed_point_matches_nonlinear_flux():
+    """test_fem.py::test_radiation_fixed_point_matches_nonlinear_flux: with the T^4 term
+    lagged in the Picard loop, the converged steady state balances the conductive flux through
+    the slab against convection + the exact radiation law at the top face."""
+    m = P.build_structured_grid(P.Box((0.0, 0.0, 0.0), (1.0, 1.0, 1.0)), 0.25)
+    mat = P.Material(np.array([[200.0, 100.0], [5000.0, 100.0]]), np.array([[200.0, 1.0], [5000.0, 1.0]]),
+                     1.0, 0.0, 1563.15, 1653.15, 0.05)
+    bc = P.ThermalBC(5.0, 0.7, 300.0, 300.0)
+    bounds = P.BoundarySpec(bc=bc, robin_tags=(P.TOP,), radiation=True, dirichlet_nodes=m.nodes_on(P.BOTTOM),
+                            dirichlet_values=1000.0)
+    settings = P.SolverSettings(picard_tol=1e-10, picard_max_iter=100, linear_tol=1e-12, linear_solver="cg")
+    state = P.uniform_field(m, 1000.0)
+    for _ in range(10):
+        state = P.step_backward_euler(state, 1e3, mat, None, bounds, settings)
+    Ttop = state.values[m.nodes_on(P.TOP)].mean()
+    q_out = bc.h_conv * (Ttop - 300.0) + bc.sigma_sb * 0.7 * (Ttop**4 - 300.0**4)
+    q_cond = 100.0 * (1000.0 - Ttop) / 1.0
+    assert 300.0 < Ttop < 1000.0
+    assert q_out == pytest.approx(q_cond, rel=1e-3)
+
+
+def _lumped_volume(grid):
+    from oracle import kuhn
+    G = kuhn.KuhnGrid(grid.box.lo, grid.box.hi, grid.ncells)
+    return float(np.prod(G.h)) * G.node_incidence().ravel() / 24.0
+
+
+def _mms_material():
+    return P.Material(np.array([[0.0, 2.0], [1e4, 2.0]]), np.array([[0.0, 3.0], [1e4, 3.0]]), 5.0, 0.0,
+                      1563.15, 1653.15, 0.05)
+
+
+def _spatial_mms_error(h):
+    """Exact solution (1 + t) sin(pi x) sin(pi y) sin(pi z): linear in t, so backward Euler
+    adds no temporal error.  The source enters as a nodal load (lumped volume times the
+    source at the node), the device's seam for arbitrary sources."""
+    k, c, rho = 2.0, 3.0, 5.0
+    m = P.build_structured_grid(P.Box((0.0, 0.0, 0.0), (1.0, 1.0, 1.0)), h)
+    X = m.coords
+    S = np.sin(np.pi * X[:, 0]) * np.sin(np.pi * X[:, 1]) * np.sin(np.pi * X[:, 2])
+    vol = _lumped_volume(m)
+    nodes = m.nodes_on(P.BOTTOM, P.TOP, P.LATERAL)
+    bounds = P.BoundarySpec(bc=P.ThermalBC(0.0, 0.0, 0.0, 0.0), robin_tags=(), dirichlet_nodes=nodes,
+                            dirichlet_values=0.0)
+    state = P.FieldState(m, S, 0.0)
+    dt, n = 0.05, 4
+    for kstep in range(1, n + 1):
+        t = kstep * dt
+        load = vol * (rho * c * S + 3.0 * np.pi**2 * k * (1.0 + t) * S)
+        state = P.step_backward_euler(state, dt, _mms_material(), None, bounds, CG, extra_load=load)
+    exact = (1.0 + n * dt) * S
+    return P.l2_norm(m, state.values - exact) / P.l2_norm(m, exact)
+
+
+def test_spatial_order_two():
+    """test_fem.py::test_spatial_order_two"""
+    hs = np.array([1 / 4, 1 / 8, 1 / 16])
+    errs = np.array([_spatial_mms_error(h) for h in hs])
+    slope = np.polyfit(np.log(hs), np.log(errs), 1)[0]
+    assert abs(slope - 2.0) < 0.15, (errs, slope)
+
+
+def _temporal_mms_error(dt):
+    """Exact solution x exp(t): spatially linear, so P1 carries no space error."""
+    c, rho = 3.0, 5.0
+    m = P.build_structured_grid(P.Box((0.0, 0.0, 0.0), (1.0, 1.0, 1.0)), 0.25)
+    x = m.coords[:, 0]
+    vol = _lumped_volume(m)
+    nodes = m.nodes_on(P.BOTTOM, P.TOP, P.LATERAL)
+    state = P.FieldState(m, x * 1.0, 0.0)
+    n = int(round(1.0 / dt))
+    for kstep in range(1, n + 1):
+        t = kstep * dt
+        bounds = P.BoundarySpec(bc=P.ThermalBC(0.0, 0.0, 0.0, 0.0), robin_tags=(), dirichlet_nodes=nodes,
+                                dirichlet_values=x[nodes] * np.exp(t))
+        state = P.step_backward_euler(state, dt, _mms_material(), None, bounds, CG,
+                                      extra_load=vol * rho * c * x * np.exp(t))
+    exact = x * np.exp(1.0)
+    return P.l2_norm(m, state.values - exact) / P.l2_norm(m, exact)
+
+
+def test_temporal_order_one():
+    """test_fem.py::test_temporal_order_one"""
+    dts = np.array([0.2, 0.1, 0.05])
+    errs = np.array([_temporal_mms_error(dt) for dt in dts])
+    slope = np.polyfit(np.log(dts), np.log(errs), 1)[0]
+    assert abs(slope - 1.0) < 0.15, (errs, slope)
