@@ -503,3 +503,140 @@ def test_temporal_order_one():
     errs = np.array([_temporal_mms_error(dt) for dt in dts])
     slope = np.polyfit(np.log(dts), np.log(errs), 1)[0]
     assert abs(slope - 1.0) < 0.15, (errs, slope)
+
+
+# ---- test_scanpath.py: relocation (scanpath.py:208-248) -----------------------------------
+
+def _relocation_case(origin=(0.1, 0.35, 0.5)):
+    gm = P.build_structured_grid(P.Box((0.0, 0.0, 0.0), (2.4, 1.2, 0.6)), 0.2)
+    mat = material()
+    prob = P.TwoLevelProblem(global_mesh=gm, mat_global=mat, mat_local=mat, bc=BC0, solver=CG)
+    lsize = (1.2, 0.5, 0.1)
+    lm = P.build_structured_grid(P.Box(origin, tuple(np.asarray(origin) + np.asarray(lsize))), 0.05)
+    gfield = P.FieldState(gm, 300.0 + 10.0 * gm.coords[:, 0], 0.0)
+    return prob, P.initial_state(prob, lm, gfield), P.LocalDomainPolicy(box_size=lsize)
+
+
+def test_relocate_noop_translate_snap_clamp():
+    """test_relocate_noop_when_snapped_target_matches, ..._translates_and_reinterpolates,
+    ..._snap_keeps_lattice, ..._clamps_at_global_wall: the box follows the laser in whole
+    local cells, the global field is untouched, the new local field and trace are the
+    (device) interpolant of the global field."""
+    from paper_2110_12932_b200.twolevel import relocate_local
+    prob, state, policy = _relocation_case()
+    ex = np.array([1.0, 0.0, 0.0])
+    x0 = 0.1 + (2 / 3) * 1.2
+    assert relocate_local(state, policy, np.array([x0, 0.6, 0.6]), ex, prob) is state
+    out = relocate_local(state, policy, np.array([x0 + 0.2, 0.6, 0.6]), ex, prob)
+    assert out is not state and out.global_field is state.global_field
+    shift = np.asarray(out.local_field.mesh.box.lo) - np.asarray(state.local_field.mesh.box.lo)
+    assert shift[0] == pytest.approx(0.2) and shift[1] == 0.0 and shift[2] == 0.0
+    expect = 300.0 + 10.0 * out.local_field.mesh.coords[:, 0]
+    assert np.allclose(out.local_field.values, expect, atol=1e-10)
+    np.testing.assert_array_equal(out.trace, out.local_field.values[out.gamma.trace_nodes])
+    snapped = relocate_local(state, policy, np.array([x0 + 0.137, 0.6, 0.6]), ex, prob)
+    s = snapped.local_field.mesh.box.lo[0] - state.local_field.mesh.box.lo[0]
+    assert s / 0.05 == pytest.approx(round(s / 0.05))
+    wall = relocate_local(state, policy, np.array([2.35, 0.6, 0.6]), ex, prob)
+    hi, ghi = np.asarray(wall.local_field.mesh.box.hi), np.asarray(prob.global_mesh.box.hi)
+    assert hi[0] < ghi[0] and hi[2] == pytest.approx(ghi[2])
+
+
+def test_relocate_constant_field_stays_constant():
+    """test_scanpath.py::test_relocate_constant_field_stays_constant"""
+    from paper_2110_12932_b200.twolevel import relocate_local
+    prob, state, policy = _relocation_case()
+    const = P.initial_state(prob, state.local_field.mesh, P.uniform_field(prob.global_mesh, 777.0))
+    out = relocate_local(const, policy, np.array([1.6, 0.6, 0.6]), np.array([1.0, 0.0, 0.0]), prob)
+    assert out is not const and np.allclose(out.local_field.values, 777.0)
+
+
+def test_direction_flip_places_box_behind_laser():
+    """test_scanpath.py::test_direction_flip_places_box_behind_laser"""
+    policy = P.LocalDomainPolicy(box_size=(1.2, 0.5, 0.1))
+    laser = np.array([1.0, 0.6, 0.6])
+    assert policy.target_origin(laser, np.array([1.0, 0.0, 0.0]))[0] == pytest.approx(1.0 - 0.8)
+    assert policy.target_origin(laser, np.array([-1.0, 0.0, 0.0]))[0] == pytest.approx(1.0 - 0.4)
+
+
+# ---- test_mesh.py: interpolation and the interface (mesh.py:308-361, 477-523) -------------
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_interpolation_reproduces_affine_fields(dim):
+    """test_mesh.py::test_interpolation_reproduces_affine_fields (seeded points instead of
+    hypothesis draws), on the device, 2D triangles and 3D Kuhn tets."""
+    rng = np.random.default_rng(7)
+    m = P.build_structured_grid(P.Box((0.0,) * dim, (1.0,) * dim), 0.25)
+    for _ in range(5):
+        c0, c = rng.uniform(-1.0, 1.0), rng.uniform(-2.0, 2.0, dim)
+        vals = c0 + m.coords @ c
+        pts = rng.uniform(0.05, 0.95, (25, dim))
+        assert np.abs(m.interpolate(vals, pts) - (c0 + pts @ c)).max() <= 1e-12
+
+
+def test_interpolation_midedge_of_quadratic():
+    """test_mesh.py::test_interpolation_midedge_of_quadratic: the interpolant of x^2 at an
+    edge midpoint is the endpoint average."""
+    m = P.build_structured_grid(P.Box((0.0, 0.0), (1.0, 1.0)), 0.25)
+    got = m.interpolate(m.coords[:, 0] ** 2, np.array([[0.375, 0.5]]))[0]
+    assert got == pytest.approx(0.5 * (0.25**2 + 0.5**2))
+    m3 = P.build_structured_grid(P.Box((0.0, 0.0, 0.0), (1.0, 1.0, 1.0)), 0.25)
+    got3 = m3.interpolate(m3.coords[:, 0] ** 2, np.array([[0.375, 0.5, 0.25]]))[0]
+    assert got3 == pytest.approx(0.5 * (0.25**2 + 0.5**2))
+
+
+def test_interface_measure_and_immersion():
+    """test_interface_measure_2d, test_interface_measure_3d, test_interface_requires_immersion"""
+    lm = P.build_structured_grid(P.Box((1.0, 0.625), (2.0, 1.0)), 0.125)
+    gm = P.build_structured_grid(P.Box((0.0, 0.0), (5.0, 1.0)), 0.125)
+    assert P.extract_interface(lm, gm).measure == pytest.approx(2 * 0.375 + 1.0, rel=1e-10)
+    lm3 = P.build_structured_grid(P.Box((0.0, 0.0, 0.0), (1.2, 0.5, 0.1)), 0.05)
+    gm3 = P.build_structured_grid(P.Box((-1.0, -1.0, -0.9), (3.0, 2.0, 0.1)), 0.2)
+    assert P.extract_interface(lm3, gm3).measure == pytest.approx(1.2 * 0.5 + 2 * (1.2 * 0.1 + 0.5 * 0.1), rel=1e-10)
+    flush = P.build_structured_grid(P.Box((0.0, 0.625), (2.0, 1.0)), 0.125)
+    with pytest.raises(P.MeshError):
+        P.extract_interface(flush, gm)
+    sunk = P.build_structured_grid(P.Box((1.0, 0.5), (2.0, 0.875)), 0.125)      # top must ride on the global top
+    with pytest.raises(P.MeshError):
+        P.extract_interface(sunk, gm)
+
+
+def test_interface_constant_functional_equals_measure():
+    """test_mesh.py::test_interface_constant_functional_equals_measure, through the device
+    functional: for T_local = z the normal derivative is -1 on the bottom facets and 0 on
+    the lateral ones, so the load of a unit conductivity jump sums to minus the bottom area
+    (the test functions sum to one)."""
+    gm, lm = plates()
+    gamma = P.extract_interface(lm, gm)
+    field = P.FieldState(lm, lm.coords[:, 2].copy(), 0.0)
+    load = transmission_load(field, gamma, gm, material(11.0, 11.0), material(10.0, 10.0))
+    assert float(np.sum(load)) == pytest.approx(-(8e-4 * 6e-4), rel=1e-10)
+
+
+# ---- test_metrics.py (metrics.py:123-165) -----------------------------------------------
+
+def _log_and_reference(scale=1.0):
+    gm, lm = plates()
+    base_g = 300.0 + 2e5 * gm.coords[:, 0] + 1e5 * gm.coords[:, 2]
+    base_l = 300.0 + 2e5 * lm.coords[:, 0] + 1e5 * lm.coords[:, 2]
+    log, ref = P.RunLog(), P.Trajectory(gm)
+    for k in range(4):
+        t = 0.1 * k
+        vals = base_g * (1 + 0.1 * k)
+        ref.append(P.FieldState(gm, vals, t))
+        log.record("initial" if k == 0 else "macro", t, P.FieldState(lm, scale * base_l * (1 + 0.1 * k), t),
+                   P.FieldState(gm, vals, t), 0)
+    return log, ref
+
+
+def test_error_metrics_identical_and_scaled_trajectories():
+    """test_error_metrics_identical_trajectories and test_error_metrics_relative_scaling: the
+    relative L2(local domain) error, interpolation and mass norms on the device."""
+    log, ref = _log_and_reference()
+    rep = P.error_metrics(log, ref)
+    assert np.allclose(rep.rel_l2, 0.0, atol=1e-12) and rep.mean_rel_l2 == pytest.approx(0.0, abs=1e-12)
+    eps = 0.03
+    log, ref = _log_and_reference(scale=1 + eps)
+    rep = P.error_metrics(log, ref)
+    assert np.allclose(rep.rel_l2[1:], eps, rtol=1e-10)
+    assert rep.mean_rel_l2 == pytest.approx(eps, rel=1e-10)
