@@ -352,7 +352,8 @@ def slab_bench(args):
     alg = sum(own * (64 * k + 32) for k in gits)
     ach = alg / (sum(gms) / 1e3) / 1e9 if gms else None
     roofline = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                "frac": ach / peak if ach else None, "traffic": None,
+                "frac": ach / peak if ach else None, "frac_of_8tbs_datasheet": ach / 8000.0 if ach else None,
+                "traffic": None,
                 "kernel": "z-slab global solve (rank 0): k_slab_rhs -> {k_sd_dir (bulk-copy sweep A), all-gather, "
                           "k_sd_upd_flat (boundary planes), halo || k_sd_upd (bulk-copy sweep B), all-gather} -> "
                           "k_sd_resid -> k_sd_finish; scalars on the device",
@@ -610,7 +611,8 @@ def scenario_bench(args):
     kloc, kglo = kernel_stats(loc_rows, Nl, share_ms), kernel_stats(glo_rows, Ng, share_ms)
     peak, peak_src = measured_peak()
     roofline = {"bound": "hbm", "achieved": kloc["achieved_gbs"], "peak": peak, "unit": "GB/s",
-                "frac": kloc["achieved_gbs"] / peak, "traffic": None,
+                "frac": kloc["achieved_gbs"] / peak, "frac_of_8tbs_datasheet": kloc["achieved_gbs"] / 8000.0,
+                "traffic": None,
                 "kernel": ("batched local-grid PCG solves: the i-th micro solve of every scenario of the group in "
                            "one launch sequence k_sb_rhs -> k_tb_cg (bulk-copy z-march CG loop over all systems, in "
                            "lockstep) -> k_sb_resid -> k_sb_final") if batched else
@@ -924,7 +926,8 @@ def device_arm(args):
             if kk and d_ and a_:
                 kk["ncu_dram_over_algorithmic"] = d_ / a_
     roofline = {"bound": "hbm", "achieved": kdom["achieved_gbs"], "peak": peak, "unit": "GB/s",
-                "frac": kdom["achieved_gbs"] / peak, "traffic": traffic, "traffic_note": tnote,
+                "frac": kdom["achieved_gbs"] / peak, "frac_of_8tbs_datasheet": kdom["achieved_gbs"] / 8000.0,
+                "traffic": traffic, "traffic_note": tnote,
                 "kernel": kname, "level": lev, "nodes": ndom, "peak_source": peak_src,
                 "note": "algorithmic bytes N(64k+32) per solve (SURVEY §8d) / the solve launches' CUDA-event "
                         "time on the run's stream"}
