@@ -196,6 +196,7 @@ __global__ void k_interp_nodes2(Grid G, Grid L, const double* __restrict__ vg, c
                                 double* __restrict__ out) {
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
         const int p = idx[e];
+        if (p < 0 || p >= L.n) { out[e] = nan(""); continue; }
         out[e] = p1_eval2(G, vg, node_coord(L, 0, p % L.NX), node_coord(L, 1, p / L.NX));
     }
 }

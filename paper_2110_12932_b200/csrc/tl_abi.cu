@@ -1169,7 +1169,7 @@ static int vc_impl(const tl_grid_desc* grid, const tl_vc_material* mat, const tl
         TL_CUDA(copy_in(dm, dirichlet_mask, n));
     } else {
         // sparse Dirichlet data: node list + values, scattered on the device
-        int* dnd = reinterpret_cast<int*>(tsrc + ntet);
+        int* dnd = reinterpret_cast<int*>(tsrc + 4 * ntet);
         double* dvl = reinterpret_cast<double*>(dnd + ((size_t)nd + 2) / 2 * 2);
         TL_CUDA(cudaMemset(dg, 0, sizeof(double) * n));
         TL_CUDA(cudaMemset(dm, 0, n));

@@ -1067,7 +1067,9 @@ __global__ void k_interp_nodes(Grid G, const double* __restrict__ v, Grid L, con
                                double* __restrict__ out) {
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
         int i, j, k;
-        decode(L, idx[e], i, j, k);
+        const int p = idx[e];
+        if (p < 0 || p >= L.n) { out[e] = nan(""); continue; }     // not a node of the target lattice
+        decode(L, p, i, j, k);
         out[e] = p1_eval(G, v, node_coord(L, 0, i), node_coord(L, 1, j), node_coord(L, 2, k));
     }
 }
