@@ -566,15 +566,16 @@ def experiments_case():
     print("experiments:", {k: v["summary"] for k, v in out.items() if k != "versions"})
 
 
-def experiments2d_case():
+def experiments2d_case(names=("oracle2d", "study2d", "matrix2d")):
     """runner.run_experiment on the reference's shipped 2D configs (configs/oracle2d.cfg,
-    configs/study2d.cfg restate them) with its own IN625 file: summaries, study matrix,
+    configs/study2d.cfg, configs/matrix2d.cfg restate them) with its own IN625 file: summaries, study matrix,
     errors.csv incl. the control-line temperature T_star; the tables go into the json."""
     import csv as _csv
     import shutil
     import tempfile
-    out = {}
-    for name in ("oracle2d", "study2d"):
+    dst = OUT / "experiments2d.json"
+    out = json.loads(dst.read_text()) if dst.exists() else {}      # cases not named keep their golden
+    for name in names:
         tmp = Path(tempfile.mkdtemp())
         shutil.copy(CFG / f"{name}.cfg", tmp / f"{name}.cfg")
         shutil.copy(REF / "lpbfsim" / "data" / "in625.mat", tmp / "in625.mat")
@@ -704,6 +705,8 @@ def main():
         return
     if "--2d-experiments" in sys.argv:
         return experiments2d_case()
+    if "--2d-matrix" in sys.argv:                 # only the matrix2d case; the others keep their golden
+        return experiments2d_case(("matrix2d",))
     if "--compare3d" in sys.argv:
         return compare3d_case()
     if "--vtk" in sys.argv:

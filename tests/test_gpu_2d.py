@@ -119,11 +119,12 @@ def test_2d_two_level_run_vs_reference(name, tmp_path):
             assert rel(Tg, z[f"g{k}"]) <= REL and rel(Tl_, z[f"l{k}"]) <= REL
 
 
-@pytest.mark.parametrize("name", ["oracle2d", "study2d"])
+@pytest.mark.parametrize("name", ["oracle2d", "study2d", "matrix2d"])
 def test_2d_shipped_experiments_vs_reference(name, tmp_path):
     """runner.run_experiment on the reference's shipped 2D configs (oracle_2d.cfg: the
     coupled pair reproduces the monolithic solve; study_2d.cfg: coarse-step sweep against
-    the monolithic reference): the same output files, solve counts, study pairs and
+    the monolithic reference; matrix_2d.cfg, unchanged: the 3 x 3 coarse-step x fine-step
+    error matrix against an 800-step reference): the same output files, solve counts, study pairs and
     errors.csv / study_matrix rows (relative L2 errors and the control-line temperature
     T_star) as the reference.  Relative L2 errors are differences of two solutions: they are
     compared to 1e-7 relative plus 2e-9 absolute (oracle2d's are ~3e-10, the solver noise)."""
