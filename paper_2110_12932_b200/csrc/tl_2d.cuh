@@ -242,4 +242,123 @@ __global__ void k_mass_norms2(Grid L, const double* __restrict__ a, const double
     }
 }
 
+// Masked mass norms in 2D (twolevel.masked_mass, twolevel.py:361-373): (a-b)^T M (a-b) over
+// the triangles whose centroid lies in the closed box -> part[2 blk], the others ->
+// part[2 blk + 1]; per triangle area/12 (sum d_i^2 + (sum d_i)^2) as k_mass_norms2.
+__global__ void k_mass_norms_split2(Grid L, const double* __restrict__ a, const double* __restrict__ b,
+                                    double blo0, double blo1, double bhi0, double bhi1, double* part) {
+    __shared__ double red[64];
+    const int ncell = L.nc[0] * L.nc[1];
+    const double blo[2] = {blo0, blo1}, bhi[2] = {bhi0, bhi1};
+    double acc[2] = {0.0, 0.0};
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncell; c += gridDim.x * blockDim.x) {
+        const int cell[2] = {c % L.nc[0], c / L.nc[0]};
+        for (int t = 0; t < 2; ++t) {
+            double d[3];
+            bool in = true;
+            for (int v = 0; v < 3; ++v) {
+                const int id = (cell[0] + c_tri[t][v][0]) + L.NX * (cell[1] + c_tri[t][v][1]);
+                d[v] = a[id] - b[id];
+            }
+            for (int ax = 0; ax < 2; ++ax) {
+                double sx = 0.0;
+                for (int v = 0; v < 3; ++v) sx += node_coord(L, ax, cell[ax] + c_tri[t][v][ax]);
+                const double cen = sx / 3.0;
+                in = in && cen >= blo[ax] && cen <= bhi[ax];
+            }
+            const double s1 = d[0] + d[1] + d[2];
+            acc[in ? 0 : 1] += d[0] * d[0] + d[1] * d[1] + d[2] * d[2] + s1 * s1;
+        }
+    }
+    block_sum<2>(acc, red);
+    if (threadIdx.x == 0) {
+        const double w = 0.5 * L.h[0] * L.h[1] / 12.0;
+        part[2 * blockIdx.x] = acc[0] * w;
+        part[2 * blockIdx.x + 1] = acc[1] * w;
+    }
+}
+
+// Full-mode overlap feedback in 2D (twolevel._overlap_feedback, twolevel.py:186-239; the 3D
+// kernel is k_overlap_feedback in tl_vc.cuh): per global node, over the (up to six) global
+// triangles touching it and their three edge-midpoint quadrature points that lie in the
+// closed local box, the local fields are located in the local lattice (cell by floor,
+// triangle 0 where xi >= eta, as p1_eval2) and the density
+//   -(c_eff,l rho_l k_g/k_l - c_g rho_g) dT/dt + ((k_g/k_l) k_l' - k_g') |grad T|^2 + (k_g/k_l - 1) Q
+// is gathered as w_q area density phi_i(x_q) (no atomics).
+__global__ void k_overlap_feedback2(Grid G, Grid L, const double* __restrict__ Tn, const double* __restrict__ To,
+                                    double dt, VcMat Mg, VcMat Ml, Gauss src, double* __restrict__ load) {
+    const double area = 0.5 * G.h[0] * G.h[1];
+    double llo[2], lhi[2];
+    for (int a = 0; a < 2; ++a) {
+        llo[a] = node_coord(L, a, 0);
+        lhi[a] = node_coord(L, a, L.nc[a]);
+    }
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < G.n; p += gridDim.x * blockDim.x) {
+        const int idx[2] = {p % G.NX, p / G.NX};
+        double acc = 0.0;
+        for (int o = 0; o < 4; ++o) {
+            const int oo[2] = {o & 1, (o >> 1) & 1};
+            const int cell[2] = {idx[0] - oo[0], idx[1] - oo[1]};
+            if (cell[0] < 0 || cell[0] >= G.nc[0] || cell[1] < 0 || cell[1] >= G.nc[1]) continue;
+            for (int t = 0; t < 2; ++t) {
+                int r = -1;
+                for (int v = 0; v < 3; ++v)
+                    if (c_tri[t][v][0] == oo[0] && c_tri[t][v][1] == oo[1]) r = v;
+                if (r < 0) continue;
+                for (int q = 0; q < 3; ++q) {
+                    if (c_qphi2[q][r] == 0.0) continue;          // the point on the opposite edge
+                    double x[2];
+                    bool in = true;
+                    for (int a = 0; a < 2; ++a) {
+                        double sx = 0.0;
+                        for (int v = 0; v < 3; ++v) sx += c_qphi2[q][v] * node_coord(G, a, cell[a] + c_tri[t][v][a]);
+                        x[a] = sx;
+                        in = in && x[a] >= llo[a] && x[a] <= lhi[a];
+                    }
+                    if (!in) continue;
+                    int c[2];
+                    double xi[2];
+                    for (int a = 0; a < 2; ++a) {
+                        int ci = (int)floor((x[a] - (L.lo0[a] + L.off[a])) / L.h[a]);
+                        ci = ci < 0 ? 0 : (ci > L.nc[a] - 1 ? L.nc[a] - 1 : ci);
+                        c[a] = ci;
+                        xi[a] = (x[a] - node_coord(L, a, ci)) / L.h[a];
+                    }
+                    const int n0 = c[0] + L.NX * c[1], n3 = n0 + L.NX + 1;
+                    double Tq, Tqo, gx, gy;
+                    if (xi[0] >= xi[1]) {                           // triangle (0,0) (1,0) (1,1)
+                        const int n1 = n0 + 1;
+                        const double w0 = 1.0 - xi[0], w1 = xi[0] - xi[1], w2 = xi[1];
+                        Tq = w0 * Tn[n0] + w1 * Tn[n1] + w2 * Tn[n3];
+                        Tqo = w0 * To[n0] + w1 * To[n1] + w2 * To[n3];
+                        gx = (Tn[n1] - Tn[n0]) / L.h[0];
+                        gy = (Tn[n3] - Tn[n1]) / L.h[1];
+                    } else {                                        // triangle (0,0) (1,1) (0,1)
+                        const int n2 = n0 + L.NX;
+                        const double w0 = 1.0 - xi[1], w1 = xi[0], w2 = xi[1] - xi[0];
+                        Tq = w0 * Tn[n0] + w1 * Tn[n3] + w2 * Tn[n2];
+                        Tqo = w0 * To[n0] + w1 * To[n3] + w2 * To[n2];
+                        gx = (Tn[n3] - Tn[n2]) / L.h[0];
+                        gy = (Tn[n2] - Tn[n0]) / L.h[1];
+                    }
+                    const double gsq = gx * gx + gy * gy;
+                    const double kg = tab_interp(Tq, Mg.kT, Mg.kv, Mg.nk);
+                    const double kl = tab_interp(Tq, Ml.kT, Ml.kv, Ml.nk);
+                    const double ratio = kg / kl;
+                    const double ceff = tab_interp(Tq, Ml.cT, Ml.cv, Ml.nc) + Ml.chi * vc_phase_deriv(Ml, Tq);
+                    const double cg = tab_interp(Tq, Mg.cT, Mg.cv, Mg.nc);
+                    double dens = -(ceff * Ml.rho * ratio - cg * Mg.rho) * ((Tq - Tqo) / dt);
+                    dens += (ratio * vc_dkdT(Tq, Ml.kT, Ml.kv, Ml.nk) - vc_dkdT(Tq, Mg.kT, Mg.kv, Mg.nk)) * gsq;
+                    if (src.on) {
+                        const double ux = (x[0] - src.center[0]) / src.radius, uy = (x[1] - src.center[1]) / src.depth;
+                        dens += (ratio - 1.0) * (src.peak * exp(-(ux * ux + uy * uy)));
+                    }
+                    acc += (1.0 / 3.0) * area * dens * c_qphi2[q][r];
+                }
+            }
+        }
+        load[p] = acc;
+    }
+}
+
 }  // namespace tl

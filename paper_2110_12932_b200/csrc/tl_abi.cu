@@ -1312,8 +1312,9 @@ int32_t tl_overlap_feedback_host(const tl_grid_desc* global_grid, const tl_grid_
         return fail(TL_E_INVALID, "null argument");
     if (!(dt > 0.0)) return fail(TL_E_INVALID, "time step must be positive");
     tl::Grid G{}, L{};
-    if (int rc = make_grid(*global_grid, tl::kBottom, G)) return rc;
-    if (int rc = make_grid(*local_grid, tl::kGamma, L)) return rc;
+    if (int rc = make_grid(*global_grid, tl::kBottom, G, true)) return rc;
+    if (int rc = make_grid(*local_grid, tl::kGamma, L, true)) return rc;
+    if (tl::grid_is_2d(G) != tl::grid_is_2d(L)) return fail(TL_E_INVALID, "grids of different dimension");
     const int ng = 2 * (mat_global->nk + mat_global->nc), nl = 2 * (mat_local->nk + mat_local->nc);
     std::lock_guard<std::mutex> lock(g_scratch_mu);
     const size_t pl = ((size_t)L.n + 31) / 32 * 32, pg = ((size_t)G.n + 31) / 32 * 32;
@@ -1343,7 +1344,8 @@ int32_t tl_overlap_feedback_host(const tl_grid_desc* global_grid, const tl_grid_
         for (int a = 0; a < 3; ++a) S.center[a] = src->center[a];
         S.on = 1;
     }
-    tl::k_overlap_feedback<<<296, 256>>>(G, L, dn, dold, dt, Mg, Ml, S, dload);
+    if (tl::grid_is_2d(G)) tl::k_overlap_feedback2<<<296, 256>>>(G, L, dn, dold, dt, Mg, Ml, S, dload);
+    else tl::k_overlap_feedback<<<296, 256>>>(G, L, dn, dold, dt, Mg, Ml, S, dload);
     TL_CUDA(cudaGetLastError());
     TL_CUDA(copy_out(load_out, dload, sizeof(double) * G.n));
     return TL_OK;
@@ -1441,7 +1443,7 @@ int32_t tl_mass_norms_split_host(const tl_grid_desc* grid, const double* a, cons
                                  const double* box_hi, double* out) {
     if (!grid || !a || !b || !box_lo || !box_hi || !out) return fail(TL_E_INVALID, "null argument");
     tl::Grid L{};
-    if (int rc = make_grid(*grid, tl::kBottom, L)) return rc;
+    if (int rc = make_grid(*grid, tl::kBottom, L, true)) return rc;
     constexpr int kNB = 296;
     double *da, *db, *dpart;
     std::lock_guard<std::mutex> lock(g_scratch_mu);
@@ -1450,6 +1452,8 @@ int32_t tl_mass_norms_split_host(const tl_grid_desc* grid, const double* a, cons
         return rc;
     TL_CUDA(copy_in(da, a, sizeof(double) * L.n));
     TL_CUDA(copy_in(db, b, sizeof(double) * L.n));
+    if (tl::grid_is_2d(L)) tl::k_mass_norms_split2<<<kNB, 256>>>(L, da, db, box_lo[0], box_lo[1], box_hi[0], box_hi[1], dpart);
+    else
     tl::k_mass_norms_split<<<kNB, 256>>>(L, da, db, box_lo[0], box_lo[1], box_lo[2], box_hi[0], box_hi[1],
                                          box_hi[2], dpart);
     TL_CUDA(cudaGetLastError());

@@ -190,9 +190,12 @@ class TwoLevelProblem:
             if resident:
                 raise UnsupportedOnDevice("the device-resident run is 3D; 2D runs go through the "
                                           "step-level drivers")
-            if not self.one_way:
-                raise UnsupportedOnDevice("2D two-way coupling (distinct conductivities or full mode) "
-                                          "is not on the device path")
+            a, b = self.mat_global, self.mat_local
+            if not (a is b or np.array_equal(a.conductivity_table, b.conductivity_table)):
+                # full mode with equal conductivities runs (k_overlap_feedback2); the
+                # interface functional of a conductivity jump has a 3D kernel only
+                raise UnsupportedOnDevice("2D two-way coupling with distinct conductivities is not on "
+                                          "the device path (the interface functional is 3D only)")
 
     @property
     def device_resident(self) -> bool:
@@ -419,8 +422,9 @@ def consistency_diagnostic(state: TwoLevelState, reference: FieldState, global_m
     local = float(np.sqrt(abs(out[0])))
     ref_g = np.ascontiguousarray(interpolate_to_grid(reference.mesh, rv, global_mesh), dtype=np.float64)
     gv = np.ascontiguousarray(state.global_field.values, dtype=np.float64)
-    lo = np.ascontiguousarray(lm.box.lo, dtype=np.float64)
-    hi = np.ascontiguousarray(lm.box.hi, dtype=np.float64)
+    lo = np.zeros(3)
+    hi = np.zeros(3)
+    lo[:lm.dim], hi[:lm.dim] = lm.box.lo, lm.box.hi          # 2D: the z entries are unused
     N.check(N.lib().tl_mass_norms_split_host(N.C.byref(gd), N.dptr(ref_g), N.dptr(gv), N.dptr(lo), N.dptr(hi),
                                              N.dptr(out)), "masked mass")
     return {"local": local, "overlap": float(np.sqrt(abs(out[0]))), "exterior": float(np.sqrt(abs(out[1])))}

@@ -603,6 +603,48 @@ def experiments2d_case(names=("oracle2d", "study2d", "matrix2d")):
     (OUT / "experiments2d.json").write_text(json.dumps(out, indent=1))
 
 
+def consistency2d_case():
+    """The reference's shipped consistency_2d.cfg (configs/consistency2d.cfg restates it
+    unchanged) driven as its acceptance criterion 9 does (tests/test_acceptance.py:342-367):
+    run_reference once (latent term masked to the local region), then run_spacetime and
+    consistency_diagnostic for the alternate and the full coarse formulation.  Norms, solve
+    counters, final fields; the IN625 tables go into the npz."""
+    import dataclasses
+    import shutil
+    import tempfile
+    from lpbfsim.multirate import MacroSchedule, run_spacetime
+    from lpbfsim.twolevel import consistency_diagnostic
+    from lpbfsim.stats import RunStats
+    tmp = Path(tempfile.mkdtemp())
+    shutil.copy(CFG / "consistency2d.cfg", tmp / "consistency2d.cfg")
+    shutil.copy(REF / "lpbfsim" / "data" / "in625.mat", tmp / "in625.mat")
+    cfg = load_config(tmp / "consistency2d.cfg")
+    t0 = time.perf_counter()
+    rstats = RunStats()
+    reference = runner.run_reference(cfg, stats=rstats)
+    ref_final = reference.state(len(reference) - 1)
+    out = {"ref_final": ref_final.values, "ref_time": ref_final.time, "ref_counters": json.dumps(rstats.counters)}
+    for mode in ("alternate", "full"):
+        c = dataclasses.replace(cfg, coupling_mode=mode)
+        problem, lmesh = runner.build_problem(c)
+        T0 = fem.uniform_field(problem.global_mesh, c.T_initial, time=0.0)
+        stats = RunStats()
+        state = run_spacetime(problem, MacroSchedule(c.dt_macro, c.micro_steps, 0.0, c.t_end), lmesh, T0, stats=stats)
+        norms = consistency_diagnostic(state, ref_final, problem.global_mesh)
+        out[f"{mode}_norms"] = np.array([norms["local"], norms["overlap"], norms["exterior"]])
+        out[f"{mode}_counters"] = json.dumps(stats.counters)
+        out[f"{mode}_global"] = state.global_field.values
+        out[f"{mode}_local"] = state.local_field.values
+        print(f"consistency2d {mode}: {norms} {stats.counters}")
+    mat = cfg.material
+    out.update(k_table=mat.conductivity_table, c_table=mat.heat_capacity_table,
+               mat_scalars=np.array([mat.rho, mat.chi, mat.T_solidus, mat.T_liquidus, mat.S]),
+               wall=time.perf_counter() - t0, versions=json.dumps(VERS))
+    np.savez_compressed(OUT / "consistency2d.npz", **out)
+    shutil.rmtree(tmp)
+    print(f"consistency2d: {out['wall']:.1f}s, melted={ref_final.values.max() > mat.T_liquidus}")
+
+
 def compare3d_case():
     """runner.run_experiment on the reference's shipped compare_3d.cfg (configs/compare3d.cfg
     restates it) with its own IN625 file: the compare summary (solve counts of both schemes)
@@ -709,6 +751,8 @@ def main():
         return experiments2d_case(("matrix2d",))
     if "--compare3d" in sys.argv:
         return compare3d_case()
+    if "--2d-consistency" in sys.argv:
+        return consistency2d_case()
     if "--vtk" in sys.argv:
         return vtk_case()
     if "--piecewise" in sys.argv:

@@ -159,3 +159,41 @@ def test_2d_shipped_experiments_vs_reference(name, tmp_path):
                     continue
                 slack = 2e-9 if "rel_l2" in got[0][col] or "mean" in got[0][col] else 1e-12
                 assert abs(fx - fy) <= 1e-7 * abs(fy) + slack, (f, got[0][col], a, b)
+
+
+def test_2d_consistency_shipped_config_vs_reference(tmp_path):
+    """The reference's shipped consistency_2d.cfg (configs/consistency2d.cfg, unchanged),
+    driven as its acceptance criterion 9 (tests/test_acceptance.py:342-367): the monolithic
+    reference with the latent term masked to the local region on the h/2 mesh, then
+    run_spacetime + consistency_diagnostic for the alternate and the FULL coarse formulation
+    (2D overlap feedback, k_overlap_feedback2; masked 2D mass norms, k_mass_norms_split2).
+    Counters (171 global solves / 121 coupling iterations / 2799 Picard passes in full
+    mode), final fields and norms against the reference's run, and the criterion itself."""
+    import dataclasses
+    from paper_2110_12932_b200.twolevel import consistency_diagnostic
+    z = np.load(GOLDEN / "consistency2d.npz")
+    _write_material(z, tmp_path / "in625.mat")
+    (tmp_path / "consistency2d.cfg").write_text((CONFIGS / "consistency2d.cfg").read_text())
+    cfg = P.load_config(tmp_path / "consistency2d.cfg")
+    rstats = P.RunStats()
+    reference = P.run_reference(cfg, stats=rstats)
+    ref_final = reference.state(len(reference) - 1)
+    assert rstats.counters == json.loads(str(z["ref_counters"]))
+    assert ref_final.time == float(z["ref_time"]) and rel(ref_final.values, z["ref_final"]) <= REL
+    norms = {}
+    for mode in ("alternate", "full"):
+        c = dataclasses.replace(cfg, coupling_mode=mode)
+        problem, lmesh = P.build_problem(c)
+        assert problem.one_way == (mode == "alternate")
+        stats = P.RunStats()
+        state = P.run_spacetime(problem, P.MacroSchedule(c.dt_macro, c.micro_steps, 0.0, c.t_end), lmesh,
+                                P.uniform_field(problem.global_mesh, c.T_initial, time=0.0), stats=stats)
+        assert stats.counters == json.loads(str(z[f"{mode}_counters"])), mode
+        assert rel(state.global_field.values, z[f"{mode}_global"]) <= REL, mode
+        assert rel(state.local_field.values, z[f"{mode}_local"]) <= REL, mode
+        norms[mode] = consistency_diagnostic(state, ref_final, problem.global_mesh)
+        got = np.array([norms[mode][k] for k in ("local", "overlap", "exterior")])
+        np.testing.assert_allclose(got, z[f"{mode}_norms"], rtol=1e-7)
+    assert ref_final.values.max() > cfg.material.T_liquidus
+    assert norms["full"]["overlap"] <= norms["alternate"]["overlap"]
+    assert 0.5 <= norms["full"]["exterior"] / norms["alternate"]["exterior"] <= 2.0
