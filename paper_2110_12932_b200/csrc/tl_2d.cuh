@@ -361,4 +361,71 @@ __global__ void k_overlap_feedback2(Grid G, Grid L, const double* __restrict__ T
     }
 }
 
+// Interface functional in 2D (twolevel.transmission_load, twolevel.py:159-183; the 3D kernel
+// is k_trans_entries): the interface edges of the local lattice are the bottom row
+// (nc[0] edges, owner triangle 0 of the cell above, normal -e_y) and the two lateral columns
+// (nc[1] edges each; left: owner triangle 1, normal -e_x; right: owner triangle 0, normal
+// +e_x) (mesh.py:477-523).  Each edge carries two Gauss points of weight length / 2
+// (mesh.py:129-131); dT/dn is the owner triangle's one-sided P1 gradient; jump as in 3D.
+// Entry e = 2 f + q writes 3 (global node, density * barycentric) pairs at 3 e + r.
+__global__ void k_trans_entries2(Grid G, Grid L, const double* __restrict__ T, double jump, KTab kg, KTab kl,
+                                 int nedge, int* __restrict__ keys, int* __restrict__ idx,
+                                 double* __restrict__ vals) {
+    const double gq = 0.5 / sqrt(3.0);
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < 2 * nedge; e += gridDim.x * blockDim.x) {
+        int f = e >> 1;
+        const int q = e & 1;
+        int na, nb;                      // the edge's end nodes (local ids)
+        double dTdn, len;
+        if (f < L.nc[0]) {               // bottom edge of cell (f, 0)
+            na = f;
+            nb = f + 1;
+            dTdn = -(T[nb + L.NX] - T[nb]) / L.h[1];            // triangle 0: gy = (T11 - T10) / hy
+            len = L.h[0];
+        } else if ((f -= L.nc[0]) < L.nc[1]) {                   // left edge of cell (0, f)
+            na = L.NX * f;
+            nb = na + L.NX;
+            dTdn = -(T[nb + 1] - T[nb]) / L.h[0];               // triangle 1: gx = (T11 - T01) / hx
+            len = L.h[1];
+        } else {                                                 // right edge of cell (nc0 - 1, f)
+            f -= L.nc[1];
+            na = L.NX * f + L.nc[0];
+            nb = na + L.NX;
+            dTdn = (T[na] - T[na - 1]) / L.h[0];                // triangle 0: gx = (T10 - T00) / hx
+            len = L.h[1];
+        }
+        const double wa = q == 0 ? 0.5 + gq : 0.5 - gq, wb = 1.0 - wa;
+        const double x = wa * node_coord(L, 0, na % L.NX) + wb * node_coord(L, 0, nb % L.NX);
+        const double y = wa * node_coord(L, 1, na / L.NX) + wb * node_coord(L, 1, nb / L.NX);
+        double jq = jump;
+        if (kg.n > 0) {
+            const double tq = wa * T[na] + wb * T[nb];
+            jq = tab_interp(tq, kg.T, kg.v, kg.n) - tab_interp(tq, kl.T, kl.v, kl.n);
+        }
+        const double dens = 0.5 * len * jq * dTdn;
+        // locate in the global lattice as p1_eval2 does
+        const double pt[2] = {x, y};
+        int c[2];
+        double xi[2];
+        for (int a = 0; a < 2; ++a) {
+            int ci = (int)floor((pt[a] - (G.lo0[a] + G.off[a])) / G.h[a]);
+            ci = ci < 0 ? 0 : (ci > G.nc[a] - 1 ? G.nc[a] - 1 : ci);
+            c[a] = ci;
+            xi[a] = (pt[a] - node_coord(G, a, ci)) / G.h[a];
+        }
+        const int p0 = c[0] + G.NX * c[1];
+        int nd[3];
+        double w[3];
+        nd[0] = p0;
+        nd[1] = p0 + G.NX + 1;
+        if (xi[0] >= xi[1]) { nd[2] = p0 + 1; w[0] = 1.0 - xi[0]; w[1] = xi[1]; w[2] = xi[0] - xi[1]; }
+        else { nd[2] = p0 + G.NX; w[0] = 1.0 - xi[1]; w[1] = xi[0]; w[2] = xi[1] - xi[0]; }
+        for (int r = 0; r < 3; ++r) {
+            keys[3 * e + r] = nd[r];
+            idx[3 * e + r] = 3 * e + r;
+            vals[3 * e + r] = dens * w[r];
+        }
+    }
+}
+
 }  // namespace tl

@@ -1369,11 +1369,15 @@ static int transmission_impl(const tl_grid_desc* global_grid, const tl_grid_desc
                              int32_t nkg, const double* kl_T, const double* kl_v, int32_t nkl, double* load_out) {
     if (!global_grid || !local_grid || !local_values || !load_out) return fail(TL_E_INVALID, "null argument");
     tl::Grid G{}, L{};
-    if (int rc = make_grid(*global_grid, tl::kBottom, G)) return rc;
-    if (int rc = make_grid(*local_grid, tl::kGamma, L)) return rc;
-    const long long nf = 2ll * ((long long)L.nc[1] * L.nc[2] * 2 + (long long)L.nc[0] * L.nc[2] * 2 +
-                                (long long)L.nc[0] * L.nc[1]);
-    const long long ne = 12 * nf;
+    if (int rc = make_grid(*global_grid, tl::kBottom, G, true)) return rc;
+    if (int rc = make_grid(*local_grid, tl::kGamma, L, true)) return rc;
+    const bool two_d = tl::grid_is_2d(G);
+    if (two_d != tl::grid_is_2d(L)) return fail(TL_E_INVALID, "grids of different dimension");
+    // 3D: facets (triangles), 3 points x 4 pairs each; 2D: edges, 2 points x 3 pairs each
+    const long long nf = two_d ? (long long)L.nc[0] + 2ll * L.nc[1]
+                               : 2ll * ((long long)L.nc[1] * L.nc[2] * 2 + (long long)L.nc[0] * L.nc[2] * 2 +
+                                        (long long)L.nc[0] * L.nc[1]);
+    const long long ne = two_d ? 6 * nf : 12 * nf;
     if (ne >= (1ll << 31)) return fail(TL_E_INVALID, "interface too large");
     std::lock_guard<std::mutex> lock(g_scratch_mu);
     const size_t pl = ((size_t)L.n + 31) / 32 * 32, pe = ((size_t)ne + 31) / 32 * 32, pg = ((size_t)G.n + 31) / 32 * 32;
@@ -1401,7 +1405,8 @@ static int transmission_impl(const tl_grid_desc* global_grid, const tl_grid_desc
         kg = tl::KTab{dtab, dtab + nkg, nkg};
         kl = tl::KTab{dtab + 2 * nkg, dtab + 2 * nkg + nkl, nkl};
     }
-    tl::k_trans_entries<<<296, 256>>>(G, L, dT, jump, kg, kl, (int)nf, keys, idx, dvals);
+    if (two_d) tl::k_trans_entries2<<<296, 256>>>(G, L, dT, jump, kg, kl, (int)nf, keys, idx, dvals);
+    else tl::k_trans_entries<<<296, 256>>>(G, L, dT, jump, kg, kl, (int)nf, keys, idx, dvals);
     TL_CUDA(cudaGetLastError());
     int bits = 1;
     while ((1ll << bits) < G.n) ++bits;

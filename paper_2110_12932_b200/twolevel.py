@@ -185,17 +185,12 @@ class TwoLevelProblem:
             raise UnsupportedOnDevice("the device-resident run uses the distributed (swept-track) "
                                       "global source; 'gaussian' runs through the step-level drivers")
         if self.global_mesh.dim != 3:
-            # 2D (P1 triangles, csrc/tl_2d.cuh): the step-level drivers with the Picard-path
-            # solves; the interface functional and the overlap feedback have no 2D kernels
+            # 2D (P1 triangles, csrc/tl_2d.cuh): the step-level drivers with the Picard-path solves
             if resident:
                 raise UnsupportedOnDevice("the device-resident run is 3D; 2D runs go through the "
                                           "step-level drivers")
-            a, b = self.mat_global, self.mat_local
-            if not (a is b or np.array_equal(a.conductivity_table, b.conductivity_table)):
-                # full mode with equal conductivities runs (k_overlap_feedback2); the
-                # interface functional of a conductivity jump has a 3D kernel only
-                raise UnsupportedOnDevice("2D two-way coupling with distinct conductivities is not on "
-                                          "the device path (the interface functional is 3D only)")
+            # two-way coupling in 2D runs too: k_trans_entries2 (interface functional) and
+            # k_overlap_feedback2 (full mode)
 
     @property
     def device_resident(self) -> bool:
@@ -237,9 +232,6 @@ def transmission_load(local_field, gamma, global_mesh, mat_global, mat_local, on
     if np.array_equal(mat_global.conductivity_table, mat_local.conductivity_table):
         return np.zeros(global_mesh.n_nodes)
     lmesh = local_field.mesh
-    if lmesh.dim != 3:
-        raise UnsupportedOnDevice("the interface functional has no 2D kernel (equal conductivities "
-                                  "make it exactly zero)")
     from .fem import field_arg
     T = field_arg(local_field)
     if T.shape != (lmesh.n_nodes,):

@@ -533,7 +533,8 @@ def run2d_case(name, full_at, stride):
         run_case(name, None, full_at, stride)
     finally:
         CFG = saved
-    mat = load_config(tmp / f"{name}.cfg").material
+    c = load_config(tmp / f"{name}.cfg")
+    mat = c.material_local if getattr(c, "material_local", None) is not None else c.material   # the file's own tables
     z = dict(np.load(OUT / f"run_{name}.npz"))
     z.update(k_table=mat.conductivity_table, c_table=mat.heat_capacity_table,
              mat_scalars=np.array([mat.rho, mat.chi, mat.T_solidus, mat.T_liquidus, mat.S]))
@@ -601,6 +602,42 @@ def experiments2d_case(names=("oracle2d", "study2d", "matrix2d")):
         print(f"experiment {name}: {wall:.1f}s {summ}")
     out["versions"] = VERS
     (OUT / "experiments2d.json").write_text(json.dumps(out, indent=1))
+
+
+def transmission2d_case():
+    """twolevel.transmission_load in 2D (interface edges, two Gauss points each) on random local
+    fields of the run2d geometry: a constant conductivity jump and the IN625 table jump
+    (global table scaled by 1.5), on the configured box and on a translated one."""
+    import shutil
+    import tempfile
+    tmp = Path(tempfile.mkdtemp())
+    shutil.copy(CFG / "run2d_twoway.cfg", tmp / "run2d_twoway.cfg")
+    shutil.copy(REF / "lpbfsim" / "data" / "in625.mat", tmp / "in625.mat")
+    cfg = load_config(tmp / "run2d_twoway.cfg")
+    problem, lm = runner.build_problem(cfg)
+    rng = np.random.default_rng(12)
+    const_g = lpbfsim.materials.MaterialModel(np.array([[200.0, 14.7], [5000.0, 14.7]]), np.array([[200.0, 410.0], [5000.0, 410.0]]),
+                                              8440.0, 0.0, 1563.15, 1653.15, 0.05)
+    const_l = lpbfsim.materials.MaterialModel(np.array([[200.0, 9.8], [5000.0, 9.8]]), np.array([[200.0, 410.0], [5000.0, 410.0]]),
+                                              8440.0, 0.0, 1563.15, 1653.15, 0.05)
+    out = {}
+    hl = lm.spacing
+    for k, off in enumerate([(0.0, 0.0), (-2 * hl[0], 0.0)]):
+        mesh = lm if k == 0 else lm.translated(off)
+        gamma = lmesh.extract_interface(mesh, problem.global_mesh)
+        v = rng.uniform(300.0, 2300.0, mesh.n_nodes)
+        st = fem.FieldState(mesh, v, 0.0)
+        out[f"off{k}"] = np.array(off)
+        out[f"v{k}"] = v
+        out[f"const{k}"] = twolevel.transmission_load(st, gamma, problem.global_mesh, const_g, const_l)
+        out[f"tables{k}"] = twolevel.transmission_load(st, gamma, problem.global_mesh, problem.mat_global, problem.mat_local)
+        print(f"transmission2d {k}: const sum {out[f'const{k}'].sum():.6e} tables sum {out[f'tables{k}'].sum():.6e}")
+    mat = problem.mat_local                       # the file's own (unscaled) tables
+    np.savez_compressed(OUT / "transmission2d.npz", box_lo=np.array(lm.box.lo), box_hi=np.array(lm.box.hi),
+                        ncells=np.array(lm.ncells), k_table=mat.conductivity_table, c_table=mat.heat_capacity_table,
+                        mat_scalars=np.array([mat.rho, mat.chi, mat.T_solidus, mat.T_liquidus, mat.S]),
+                        kg_table=problem.mat_global.conductivity_table, **out, versions=json.dumps(VERS))
+    shutil.rmtree(tmp)
 
 
 def consistency2d_case():
@@ -753,6 +790,9 @@ def main():
         return compare3d_case()
     if "--2d-consistency" in sys.argv:
         return consistency2d_case()
+    if "--2d-twoway" in sys.argv:
+        transmission2d_case()
+        return run2d_case("run2d_twoway", {1, 2, 3}, 3)
     if "--vtk" in sys.argv:
         return vtk_case()
     if "--piecewise" in sys.argv:

@@ -88,10 +88,40 @@ def _write_material(z, path):
     path.write_text("\n".join(lines) + "\n")
 
 
-@pytest.mark.parametrize("name", ["run2d", "run2d_uniform"])
+def test_2d_transmission_load_vs_reference():
+    """twolevel.transmission_load in 2D (k_trans_entries2: interface edges of the local
+    lattice, two Gauss points each, the owner triangle's one-sided normal derivative, scattered
+    to the global triangle's nodes by a stable sort + ordered sums): a constant conductivity
+    jump and the table jump kappa_g(T_qp) - kappa_l(T_qp), on the configured and on a
+    translated local box; bitwise run to run."""
+    from paper_2110_12932_b200.twolevel import transmission_load
+    z = np.load(GOLDEN / "transmission2d.npz")
+    gm = P.build_structured_grid(P.Box((0.0, 0.0), (5e-3, 1e-3)), 6.25e-5)
+    lm0 = P.StructuredGrid(P.LocalPlacement(P.Box(tuple(z["box_lo"]), tuple(z["box_hi"])), np.asarray(z["ncells"])))
+    rho, chi, Ts, Tl, S = (float(v) for v in z["mat_scalars"])
+    tab_l = P.Material(z["k_table"], z["c_table"], rho, chi, Ts, Tl, S)
+    tab_g = P.Material(z["kg_table"], z["c_table"], rho, chi, Ts, Tl, S)
+    flat = np.array([[200.0, 410.0], [5000.0, 410.0]])
+    const_g = P.Material(np.array([[200.0, 14.7], [5000.0, 14.7]]), flat, 8440.0, 0.0, 1563.15, 1653.15, 0.05)
+    const_l = P.Material(np.array([[200.0, 9.8], [5000.0, 9.8]]), flat, 8440.0, 0.0, 1563.15, 1653.15, 0.05)
+    for k in range(2):
+        mesh = lm0 if k == 0 else lm0.translated(tuple(z[f"off{k}"]))
+        gamma = P.extract_interface(mesh, gm)
+        st = P.FieldState(mesh, z[f"v{k}"], 0.0)
+        for key, mg, ml in (("const", const_g, const_l), ("tables", tab_g, tab_l)):
+            got = np.asarray(transmission_load(st, gamma, gm, mg, ml))
+            want = z[f"{key}{k}"]
+            assert np.abs(got - want).max() <= 1e-12 * np.abs(want).max(), (key, k)
+            assert np.abs(want).max() > 0.0
+            np.testing.assert_array_equal(np.asarray(transmission_load(st, gamma, gm, mg, ml)), got)
+
+
+@pytest.mark.parametrize("name", ["run2d", "run2d_uniform", "run2d_twoway"])
 def test_2d_two_level_run_vs_reference(name, tmp_path):
     """The shipped 2D study geometry and physics as two-level runs (multirate m = 10 with the
-    coupled corrector; uniform steps as oracle_2d.cfg): every RunStats counter (Picard
+    coupled corrector; uniform steps as oracle_2d.cfg; run2d_twoway: the coarse conductivity
+    table scaled by 1.5, so every corrector is the relaxed two-way fixed point fed by the 2D
+    interface functional -- 116 coupling iterations in three macro steps): every RunStats counter (Picard
     passes, solves, coupling iterations), record times, fields to 1e-9 and melt masks against
     the reference's run.  The IN625 tables come from the golden file."""
     z = np.load(GOLDEN / f"run_{name}.npz")
