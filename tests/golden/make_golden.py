@@ -36,6 +36,12 @@ comes from calling the reference's own functions:
                  convection + radiation, direct solver), 3 macro steps, + its tables
 - run_cfg1_gsrc(_uniform).npz  source_global gaussian (runner.py:64-71): the coarse
                  level sees the beam itself, the corrector is a coupled re-solve
+- experiments2d.json the shipped 2D configs oracle_2d / study_2d (shortened) / matrix_2d
+                 (unchanged) through runner.run_experiment  (--2d-experiments, --2d-matrix)
+- consistency2d.npz the shipped consistency_2d.cfg driven as acceptance criterion 9: reference,
+                 alternate and full runs, consistency_diagnostic norms  (--2d-consistency)
+- transmission2d.npz, run_run2d_twoway.npz  2D interface functional and a two-way 2D run
+                 (--2d-twoway)
 - experiments.json runner.run_experiment in compare and convergence-study modes:
                  output files, summaries, study matrix, errors.csv rows
 - transmission_tdep.npz / run_cfg1_tdep_twoway.npz  two-way coupling with temperature-

@@ -640,3 +640,67 @@ def test_error_metrics_identical_and_scaled_trajectories():
     rep = P.error_metrics(log, ref)
     assert np.allclose(rep.rel_l2[1:], eps, rtol=1e-10)
     assert rep.mean_rel_l2 == pytest.approx(eps, rel=1e-10)
+
+
+# ---- the reference's 2D toy setups themselves (test_twolevel.py:34-41,160-196) ------------
+
+def _toy2d():
+    gm = P.build_structured_grid(P.Box((0.0, 0.0), (5.0, 1.0)), 0.125)
+    lm = P.build_structured_grid(P.Box((1.0, 0.625), (2.0, 1.0)), 0.125)
+    return gm, lm
+
+
+def _toy_material(k_lo, k_hi):
+    """test_twolevel.py::melt_material: rho c = 1000 so a kW-class beam drives hundreds of
+    kelvin per second on the unit-scale box."""
+    return P.Material(np.array([[300.0, k_lo], [1300.0, k_hi]]), np.array([[300.0, 10.0], [1300.0, 10.0]]),
+                      100.0, 0.0, 400.0, 500.0, 0.05)
+
+
+def test_transmission_2d_hand_computed_linear_field():
+    """test_twolevel.py::test_transmission_hand_computed_linear_field, on its own 2D boxes:
+    T_local = x with a conductivity jump delta tested against w = 1 (the lateral edges
+    cancel) and w = x (delta (b - a)(H - c) for the local box [a, b] x [c, H]); and
+    test_transmission_linear_in_local_field."""
+    gm, lm = _toy2d()
+    gamma = P.extract_interface(lm, gm)
+    delta = 7.0
+    flat = np.array([[300.0, 400.0], [1300.0, 700.0]])
+    mk = lambda k: P.Material(np.array([[300.0, k], [1300.0, k]]), flat, 8000.0, 0.0, 1563.15, 1653.15, 0.05)  # noqa: E731
+    load = np.asarray(transmission_load(P.FieldState(lm, lm.coords[:, 0].copy(), 0.0), gamma, gm, mk(10.0 + delta), mk(10.0)))
+    assert load.sum() == pytest.approx(0.0, abs=1e-12)
+    assert load @ gm.coords[:, 0] == pytest.approx(delta * (2.0 - 1.0) * (1.0 - 0.625), rel=1e-12)
+    f1 = P.FieldState(lm, lm.coords[:, 0].copy(), 0.0)
+    f2 = P.FieldState(lm, lm.coords[:, 1].copy(), 0.0)
+    both = P.FieldState(lm, 2.0 * lm.coords[:, 0] + 3.0 * lm.coords[:, 1], 0.0)
+    l1, l2, lb = (np.asarray(transmission_load(f, gamma, gm, mk(12.0), mk(9.0))) for f in (f1, f2, both))
+    assert np.allclose(lb, 2.0 * l1 + 3.0 * l2, atol=1e-12)
+
+
+def test_two_way_2d_omega_independent_and_idempotent():
+    """test_two_way_coupling_converges_and_is_omega_independent and
+    test_iterate_idempotent_at_fixed_point with the reference's own 2D setup (unit-scale
+    boxes, a parked 3 kW line source at (1.5, 1.0), coarse / fine conductivities 2..3 / 5..8)."""
+    bc = P.ThermalBC(10.0, 0.0, T0, T0)
+    beam = P.LaserBeam(3000.0, 1.0, 0.25, 0.1, 1e-6)
+    path = P.path_from_segments([((1.5, 1.0), (1.5 + 1e-6, 1.0), beam.speed)])
+    gm, lm = _toy2d()
+
+    def problem(omega):
+        return P.TwoLevelProblem(global_mesh=gm, mat_global=_toy_material(2.0, 3.0), mat_local=_toy_material(5.0, 8.0),
+                                 bc=bc, solver=CG, coupling=P.CouplingSettings(omega=omega), beam=beam, path=path,
+                                 source_global="gaussian")
+
+    p1, p2 = problem(1.0), problem(0.5)
+    assert not p1.one_way
+    s1 = P.initial_state(p1, lm, P.uniform_field(gm, T0))
+    s2 = P.initial_state(p2, lm, P.uniform_field(gm, T0))
+    o1, it1 = two_level_iterate(p1, s1, 0.05)
+    o2, it2 = two_level_iterate(p2, s2, 0.05)
+    assert it1 >= 2 and it2 >= it1
+    assert o1.local_field.values.max() > T0 + 2.0           # 1.2e5 W/m^3 over rho c = 1000 for 0.05 s
+    diff = np.linalg.norm(o1.local_field.values - o2.local_field.values) / np.linalg.norm(o1.local_field.values)
+    assert diff < 10 * p1.coupling.tolerance
+    again, _ = two_level_iterate(p1, o1, 1e-12)
+    scale = max(np.linalg.norm(o1.trace), 1e-12)
+    assert np.linalg.norm(again.trace - o1.trace) / scale < p1.coupling.tolerance
