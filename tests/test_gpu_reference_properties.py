@@ -704,3 +704,35 @@ def test_two_way_2d_omega_independent_and_idempotent():
     again, _ = two_level_iterate(p1, o1, 1e-12)
     scale = max(np.linalg.norm(o1.trace), 1e-12)
     assert np.linalg.norm(again.trace - o1.trace) / scale < p1.coupling.tolerance
+
+
+def test_criterion_8_structural_invariants_on_the_2d_toy_boxes():
+    """tests/test_acceptance.py::test_criterion_8_structural_invariants, the device-side checks
+    on its own 2D boxes: the interface functional exactly zero for matching conductivities,
+    trace interpolation exact at the end points, a constant state preserved by the coupled
+    step, and m = 1 degenerating to the uniform-step scheme under two-way coupling (10 x the
+    coupling tolerance).  (omega independence: the previous test.)"""
+    from paper_2110_12932_b200.multirate import interpolate_trace
+    gm, lm = _toy2d()
+    gamma = P.extract_interface(lm, gm)
+    mat = P.Material(np.array([[0.0, 12.0], [5000.0, 12.0]]), np.array([[0.0, 500.0], [5000.0, 500.0]]), 8000.0, 0.0,
+                     1000.0, 1100.0, 0.05)
+    fld = P.FieldState(lm, 300.0 + 40 * lm.coords[:, 0] * lm.coords[:, 1], 0.0)
+    assert np.all(np.asarray(transmission_load(fld, gamma, gm, mat, mat)) == 0.0)
+    a, b = np.array([300.0, 310.0, 320.0]), np.array([400.0, 390.0, 380.0])
+    np.testing.assert_array_equal(interpolate_trace(0, 4, a, b), a)
+    np.testing.assert_array_equal(interpolate_trace(4, 4, a, b), b)
+    quiet = P.TwoLevelProblem(global_mesh=gm, mat_global=mat, mat_local=mat, bc=P.ThermalBC(0.0, 0.0, 321.0, 321.0),
+                              solver=CG)
+    st = P.initial_state(quiet, lm, P.uniform_field(gm, 321.0))
+    st, _ = two_level_iterate(quiet, st, 0.5)
+    assert np.allclose(st.global_field.values, 321.0, atol=1e-9) and np.allclose(st.local_field.values, 321.0, atol=1e-9)
+    beam = P.LaserBeam(3000.0, 1.0, 0.25, 0.1, 1e-6)
+    path = P.path_from_segments([((1.5, 1.0), (1.5 + 1e-6, 1.0), beam.speed)])
+    p = P.TwoLevelProblem(global_mesh=gm, mat_global=_toy_material(2.0, 3.0), mat_local=_toy_material(5.0, 8.0),
+                          bc=P.ThermalBC(10.0, 0.0, T0, T0), solver=CG, beam=beam, path=path, source_global="gaussian")
+    U = P.uniform_field(gm, T0)
+    st1 = P.run_spacetime(p, P.MacroSchedule(0.05, 1, 0.0, 0.25), lm, U)
+    st2 = P.run_space(p, 0.05, 5, lm, U)
+    rel = np.linalg.norm(st1.local_field.values - st2.local_field.values) / np.linalg.norm(st2.local_field.values)
+    assert rel < 10 * 1e-6
