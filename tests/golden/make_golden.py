@@ -36,8 +36,8 @@ comes from calling the reference's own functions:
                  convection + radiation, direct solver), 3 macro steps, + its tables
 - run_cfg1_gsrc(_uniform).npz  source_global gaussian (runner.py:64-71): the coarse
                  level sees the beam itself, the corrector is a coupled re-solve
-- experiments2d.json the shipped 2D configs oracle_2d / study_2d (shortened) / matrix_2d
-                 (unchanged) through runner.run_experiment  (--2d-experiments, --2d-matrix)
+- experiments2d.json the shipped 2D configs oracle_2d / study_2d / matrix_2d, unchanged,
+                 through runner.run_experiment  (--2d-experiments, --2d-matrix, --2d-study)
 - consistency2d.npz the shipped consistency_2d.cfg driven as acceptance criterion 9: reference,
                  alternate and full runs, consistency_diagnostic norms  (--2d-consistency)
 - transmission2d.npz, run_run2d_twoway.npz  2D interface functional and a two-way 2D run
@@ -792,6 +792,8 @@ def main():
         return experiments2d_case()
     if "--2d-matrix" in sys.argv:                 # only the matrix2d case; the others keep their golden
         return experiments2d_case(("matrix2d",))
+    if "--2d-study" in sys.argv:
+        return experiments2d_case(("study2d",))
     if "--compare3d" in sys.argv:
         return compare3d_case()
     if "--2d-consistency" in sys.argv:
