@@ -666,8 +666,8 @@ __global__ void __launch_bounds__(256) k_gauss_load(Grid g, Gauss src, double mb
 }
 
 // ---------------------------------------------------------------------------------
-// Kuhn-P1 location in the global grid (mesh.py:308-339): cell by floor((x-lo)/h)
-// clipped; tet by the descending order of the in-cell fractions.
+// Kuhn-P1 location in a grid (mesh.py:308-339; the grid may be a translated local one): cell
+// by floor((x-lo)/h) clipped; tet by the descending order of the in-cell fractions.
 // ---------------------------------------------------------------------------------
 __device__ __forceinline__ double p1_eval(const Grid& G, const double* v, double x, double y, double z) {
     const double pt[3] = {x, y, z};
@@ -675,7 +675,7 @@ __device__ __forceinline__ double p1_eval(const Grid& G, const double* v, double
     double xi[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-        int ci = (int)floor((pt[a] - G.lo0[a]) / G.h[a]);
+        int ci = (int)floor((pt[a] - (G.lo0[a] + G.off[a])) / G.h[a]);      // the grid may be translated
         ci = ci < 0 ? 0 : (ci > G.nc[a] - 1 ? G.nc[a] - 1 : ci);
         c[a] = ci;
         xi[a] = (pt[a] - node_coord(G, a, ci)) / G.h[a];
@@ -703,7 +703,7 @@ __device__ __forceinline__ void p1_locate(const Grid& G, double x, double y, dou
     double xi[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-        int ci = (int)floor((pt[a] - G.lo0[a]) / G.h[a]);
+        int ci = (int)floor((pt[a] - (G.lo0[a] + G.off[a])) / G.h[a]);      // the grid may be translated
         ci = ci < 0 ? 0 : (ci > G.nc[a] - 1 ? G.nc[a] - 1 : ci);
         c[a] = ci;
         xi[a] = (pt[a] - node_coord(G, a, ci)) / G.h[a];
@@ -878,7 +878,7 @@ __global__ void __launch_bounds__(1024) k_deposit(Grid G, const double* __restri
         int c[3];
         double xi[3];
         for (int a = 0; a < 3; ++a) {
-            int ci = (int)floor((pt[a] - G.lo0[a]) / G.h[a]);
+            int ci = (int)floor((pt[a] - (G.lo0[a] + G.off[a])) / G.h[a]);      // the grid may be translated
             ci = ci < 0 ? 0 : (ci > G.nc[a] - 1 ? G.nc[a] - 1 : ci);
             c[a] = ci;
             xi[a] = (pt[a] - node_coord(G, a, ci)) / G.h[a];

@@ -474,6 +474,35 @@ def track3d_case():
     shutil.rmtree(tmp)
 
 
+def track3d_centerline_case():
+    """The shipped track_3d.cfg through runner.run_experiment in its own mode and in mode
+    "reference" (acceptance criterion 6, tests/test_acceptance.py:74-84,222-238): the
+    centerline.csv rows of both runs."""
+    import csv as _csv
+    import dataclasses
+    import shutil
+    import tempfile
+    tmp = Path(tempfile.mkdtemp())
+    shutil.copy(CFG / "track3d.cfg", tmp / "track3d.cfg")
+    shutil.copy(REF / "lpbfsim" / "data" / "in625.mat", tmp / "in625.mat")
+    cfg = load_config(tmp / "track3d.cfg")
+    out = {}
+    t0 = time.perf_counter()
+    for tag, c in (("reference", dataclasses.replace(cfg, mode="reference")), ("two_level", cfg)):
+        res = tmp / tag
+        art = runner.run_experiment(c, res)
+        with (res / "centerline.csv").open() as fh:
+            rows = list(_csv.reader(fh))
+        out[tag] = {"header": rows[0], "rows": [[float(v) for v in r] for r in rows[1:]],
+                    "files": sorted(str(p.relative_to(res)) for p in res.rglob("*") if p.is_file()),
+                    "counters": art.stats.counters}
+    out["wall"] = time.perf_counter() - t0
+    out["versions"] = VERS
+    (OUT / "track3d_centerline.json").write_text(json.dumps(out))
+    shutil.rmtree(tmp)
+    print(f"track3d centerline: {out['wall']:.1f}s", {k: out[k]["counters"] for k in ("reference", "two_level")})
+
+
 def picard2d_case(name, latent, radiation, h_conv, seed=9):
     """One nonlinear implicit step on the shipped 2D plate (5 x 1 mm, h = 62.5 um, P1
     triangles) from a heated T_old, bottom-edge Dirichlet, 2D Gaussian beam, IN625 tables."""
@@ -792,6 +821,8 @@ def main():
         return experiments2d_case()
     if "--2d-matrix" in sys.argv:                 # only the matrix2d case; the others keep their golden
         return experiments2d_case(("matrix2d",))
+    if "--track3d-centerline" in sys.argv:
+        return track3d_centerline_case()
     if "--2d-study" in sys.argv:
         return experiments2d_case(("study2d",))
     if "--compare3d" in sys.argv:

@@ -873,6 +873,55 @@ def test_track3d_shipped_config_vs_reference(tmp_path):
             assert rel(Tg, z[f"g{k}"]) <= REL and rel(Tl_, z[f"l{k}"]) <= REL
 
 
+def test_track3d_centerline_acceptance_criterion_6(tmp_path):
+    """The shipped track_3d.cfg (configs/track3d.cfg, unchanged) through run_experiment in its
+    own mode and in mode "reference", as the reference's acceptance criterion 6 does
+    (tests/test_acceptance.py:74-84,222-238): the same output files, solve counters and
+    centerline.csv rows as the reference (15.5 min there), and the criterion's quantities
+    (peak error, pointwise error where T_ref >= T_s / 2, melting reached) as the reference's
+    own files give them.  The centre line crosses the relocated local box: the fine field is
+    sampled on a translated lattice (Mesh.interpolate, mesh.py:358-361)."""
+    import csv
+    import dataclasses
+    from paper_2110_12932_b200.experiment import run_experiment
+    gold = json.loads((GOLDEN / "track3d_centerline.json").read_text())
+    z = np.load(GOLDEN / "run_track3d.npz")
+    rho, chi, Ts, Tl, S = (float(v) for v in z["mat_scalars"])
+    lines = ["units K", f"rho {rho!r}", f"chi {chi!r}", f"T_solidus {Ts!r}", f"T_liquidus {Tl!r}", f"S {S!r}",
+             "[conductivity]"] + [f"{float(a)!r} {float(b)!r}" for a, b in z["k_table"]] + ["[heat_capacity]"] + \
+            [f"{float(a)!r} {float(b)!r}" for a, b in z["c_table"]]
+    (tmp_path / "in625.mat").write_text("\n".join(lines) + "\n")
+    (tmp_path / "track3d.cfg").write_text((CONFIGS / "track3d.cfg").read_text())
+    cfg = P.load_config(tmp_path / "track3d.cfg")
+    prof = {}
+    for tag, c in (("reference", dataclasses.replace(cfg, mode="reference")), ("two_level", cfg)):
+        out = tmp_path / tag
+        art = run_experiment(c, out)
+        assert sorted(str(p.relative_to(out)) for p in out.rglob("*") if p.is_file()) == gold[tag]["files"]
+        assert art.stats.counters == gold[tag]["counters"]
+        with (out / "centerline.csv").open() as fh:
+            rows = list(csv.reader(fh))
+        assert rows[0] == gold[tag]["header"]
+        got = np.array([[float(v) for v in r] for r in rows[1:]])
+        want = np.array(gold[tag]["rows"])
+        np.testing.assert_allclose(got[:, 0], want[:, 0], rtol=1e-12, atol=1e-15)
+        np.testing.assert_allclose(got[:, 1], want[:, 1], rtol=1e-7)
+        prof[tag] = got
+    def criterion(ref, st):
+        xr, Tr = ref[:, 0], ref[:, 1]
+        Ts_ = np.interp(xr, st[:, 0], st[:, 1])
+        hot = Tr >= 0.5 * cfg.material.T_solidus
+        return (abs(Ts_.max() - Tr.max()) / Tr.max(), np.max(np.abs(Ts_[hot] - Tr[hot]) / Tr[hot]),
+                bool(Tr.max() > cfg.material.T_liquidus))
+
+    # the criterion's quantities from the device's files equal those from the reference's own
+    # (its thresholds, 5 % / 10 %, are not met by the reference's numbers either: 7.2 % / 47 %)
+    got = criterion(prof["reference"], prof["two_level"])
+    want = criterion(np.array(gold["reference"]["rows"]), np.array(gold["two_level"]["rows"]))
+    assert got[2] and want[2]
+    assert got[0] == pytest.approx(want[0], rel=1e-5) and got[1] == pytest.approx(want[1], rel=1e-5)
+
+
 @pytest.mark.parametrize("name", ["cfg1_compare", "cfg1_study"])
 def test_experiment_modes_vs_reference(name, tmp_path):
     """runner.run_experiment (runner.py:270-440) in compare and convergence-study modes on the
