@@ -1230,7 +1230,15 @@ static int vc_impl(const tl_grid_desc* grid, const tl_vc_material* mat, const tl
     int dev = 0, sms = 0;
     TL_CUDA(cudaGetDevice(&dev));
     TL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const int NBc = std::max(1, std::min(per_sm * sms, (n + kT - 1) / kT));
+    // blocks per SM of the cooperative PCG: fewer blocks make the two grid barriers and the
+    // per-block fixed-order sums of the NB partials cheaper (TLGPU_VC_BPS overrides)
+    static int bps = -1;
+    if (bps < 0) {
+        const char* e = getenv("TLGPU_VC_BPS");
+        bps = e ? std::max(1, atoi(e)) : 4;          // measured on 520k nodes: 1: 10.7, 2: 8.3, 4: 7.9, 8: 8.1 ms per step
+    }
+    const int use_bps = std::min(bps, per_sm);
+    const int NBc = std::max(1, std::min(use_bps * sms, (n + kT - 1) / kT));
     if (NBc > 4096) return fail(TL_E_INVALID, "too many CTAs for the reduction workspace");
     tl::VcCg C{diag, wx, wy, wz, b, dm, dg, x, r, z, pv, q, cpart, rtol, maxiter, dinfo};
     void* args[] = {&G, &C};
