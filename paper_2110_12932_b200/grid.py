@@ -169,9 +169,16 @@ class StructuredGrid:
         return StructuredGrid(self._placement.translated(offset, within))
 
     def interpolate(self, values: np.ndarray, points: np.ndarray) -> np.ndarray:
-        """P1 interpolant at points, evaluated on the device (``mesh.py:358-361``)."""
+        """P1 interpolant at points, evaluated on the device (``mesh.py:358-361``).  A point
+        outside the box (inflated by 1e-12 h, ``mesh.py:316-320``) raises PointOutsideMesh,
+        as ``Mesh.locate`` does; the device would clip it into a boundary cell."""
+        from .errors import PointOutsideMesh
         from .ops import interpolate_points
-        return interpolate_points(self, values, points)
+        pts = np.atleast_2d(np.asarray(points, dtype=float))
+        inside = self.box.contains(pts, tol=1e-12 * self.h)
+        if not np.all(inside):
+            raise PointOutsideMesh(pts[np.nonzero(~inside)[0][0]])
+        return interpolate_points(self, values, pts)
 
     def desc(self):
         from ._native import GridDesc

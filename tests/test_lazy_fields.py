@@ -131,3 +131,13 @@ def test_arbitrary_dirichlet_sets_are_not_a_fused_kernel_kind():
     assert _dirichlet_kind(g, g.gamma_nodes()) == N.TL_DIRICHLET_GAMMA
     assert _dirichlet_kind(g, np.arange(g.n_nodes)) == -1
     assert _dirichlet_kind(g, np.empty(0, dtype=np.int64)) == -1
+
+
+def test_interpolate_outside_raises_with_coordinates():
+    """test_mesh.py::test_locate_outside_raises_with_coordinates: the host-side containment
+    check of StructuredGrid.interpolate (no device call is made for a point outside)."""
+    import pytest
+    m = P.build_structured_grid(P.Box((0.0, 0.0), (1.0, 1.0)), 0.5)
+    with pytest.raises(P.PointOutsideMesh) as err:
+        m.interpolate(np.zeros(m.n_nodes), np.array([[1.5, 0.5]]))
+    assert err.value.point[0] == pytest.approx(1.5)
