@@ -1218,7 +1218,7 @@ static int vc_impl(const tl_grid_desc* grid, const tl_vc_material* mat, const tl
         tl::k_vc_tris<<<4 * kNB, kT>>>(G, M, Mo, RG, dTo, dTl, dt, S, tk, tml, tsrc);
         tl::k_vc_assemble2<<<kNB, kT>>>(G, tk, tml, tsrc, dTo, dTl, dex, RB, diag, wx, wy, wz, b);
     } else {
-    tl::k_vc_tets<<<4 * kNB, kT>>>(G, M, Mo, RG, dTo, dTl, dt, S, tk, tml, tsrc);
+    tl::k_vc_tets<<<4 * kNB, kT, sizeof(double) * nt>>>(G, M, Mo, RG, dTo, dTl, dt, S, tk, tml, tsrc);
     tl::k_vc_assemble<<<kNB, kT>>>(G, tk, tml, tsrc, dTo, dTl, dex, RB, diag, wx, wy, wz, b);
     }
     tl::k_vc_constrain_b<<<kNB, kT>>>(G, dm, dg, wx, wy, wz, diag, b);

@@ -66,9 +66,23 @@ __device__ __forceinline__ double vc_latent(const VcMat& M, double T, double T_o
 // Phase 1, one thread per (cell, tet): kbar, the lumped mass of each vertex (times vol)
 // and the Gaussian load of each vertex (times vol), stored per tet so every tet's
 // quadrature-point material evaluations run once (not once per touching node).
-__global__ void k_vc_tets(Grid g, VcMat Mi, VcMat Mo, VcRegion R, const double* __restrict__ T_old,
+// The (T, value) tables of a material staged in shared memory (the np.interp searches are
+// chains of dependent loads: 8 per quadrature point); `at` holds 2 (nk + nc) doubles.
+__device__ __forceinline__ VcMat vc_stage_tables(const VcMat& M, double* at) {
+    for (int e = threadIdx.x; e < M.nk; e += blockDim.x) { at[e] = M.kT[e]; at[M.nk + e] = M.kv[e]; }
+    for (int e = threadIdx.x; e < M.nc; e += blockDim.x) { at[2 * M.nk + e] = M.cT[e]; at[2 * M.nk + M.nc + e] = M.cv[e]; }
+    VcMat S = M;
+    S.kT = at; S.kv = at + M.nk; S.cT = at + 2 * M.nk; S.cv = at + 2 * M.nk + M.nc;
+    return S;
+}
+
+__global__ void k_vc_tets(Grid g, VcMat Mi_g, VcMat Mo_g, VcRegion R, const double* __restrict__ T_old,
                           const double* __restrict__ T_lag, double dt, Gauss src, double* __restrict__ tk,
                           double* __restrict__ tml, double* __restrict__ tsrc) {
+    extern __shared__ double vc_tab[];           // 2 (nk + nc) of Mi, then of Mo (piecewise only)
+    const VcMat Mi = vc_stage_tables(Mi_g, vc_tab);
+    const VcMat Mo = R.piecewise ? vc_stage_tables(Mo_g, vc_tab + 2 * (Mi_g.nk + Mi_g.nc)) : Mi;
+    __syncthreads();
     const double A = TL_QA, B = TL_QB;
     const double vol = g.h[0] * g.h[1] * g.h[2] / 6.0;
     const int perms[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
