@@ -45,8 +45,14 @@ __device__ __forceinline__ double vc_interp(double x, const double* xp, const do
     return tab_interp(x, xp, fp, n);
 }
 
+// tanh saturates to +-1 exactly in fp64 beyond |a| ~ 19.1 (1 - tanh(22) = 1.6e-19 < ulp / 2):
+// the shortcut returns the same bits and spares the cold bulk of the plate two tanh calls
+// per quadrature point.
 __device__ __forceinline__ double vc_phase(const VcMat& M, double T) {
-    return 0.5 * (1.0 + tanh(M.S * (T - M.Tm)));
+    const double a = M.S * (T - M.Tm);
+    if (a > 22.0) return 1.0;
+    if (a < -22.0) return 0.0;
+    return 0.5 * (1.0 + tanh(a));
 }
 
 __device__ __forceinline__ double vc_phase_deriv(const VcMat& M, double T) {
@@ -139,7 +145,9 @@ __global__ void k_vc_tets(Grid g, VcMat Mi_g, VcMat Mo_g, VcRegion R, const doub
                 const double ex = 3.0 * ((x[0] - src.center[0]) / src.radius) * ((x[0] - src.center[0]) / src.radius);
                 const double ey = 3.0 * ((x[1] - src.center[1]) / src.radius) * ((x[1] - src.center[1]) / src.radius);
                 const double ez = 3.0 * ((x[2] - src.center[2]) / src.depth) * ((x[2] - src.center[2]) / src.depth);
-                Qq = 0.25 * (src.peak * exp(-(ex + ey + ez)));
+                // exp(-a) is exactly 0 for a > 745.14: the same bits without the call far from the beam
+                const double ea = ex + ey + ez;
+                Qq = ea > 745.2 ? 0.0 : 0.25 * (src.peak * exp(-ea));
             }
             for (int r = 0; r < 4; ++r) {
                 const double phr = (r == q) ? A : B;
