@@ -246,3 +246,90 @@ def test_2d_consistency_shipped_config_vs_reference(tmp_path):
     assert ref_final.values.max() > cfg.material.T_liquidus
     assert norms["full"]["overlap"] <= norms["alternate"]["overlap"]
     assert 0.5 <= norms["full"]["exterior"] / norms["alternate"]["exterior"] <= 2.0
+
+
+# ---- the reference's command-line tests on its own tiny 2D config (test_io_cli.py:13-137) ----
+
+_TINY_2D = """
+[domain]
+dimension 2
+global_min 0 0 mm
+global_max 2 1 mm
+local_min 0.5 0.5 mm
+local_max 1.5 1 mm
+[mesh]
+h_global 0.25 mm
+[material]
+file in625.mat
+chi_override 0
+[laser]
+power 500
+radius 0.2 mm
+depth 0.1 mm
+[bc]
+h_conv 10
+emissivity 0
+T_ambient 25 C
+T_buildplate 25 C
+[path]
+type segments
+speed 2 mm/s
+segment 0.6 1 1.4 1 mm
+[schedule]
+t_end 0.2 s
+dt_macro 0.1 s
+micro_steps 2
+dt_reference 0.05 s
+[experiment]
+mode two-level-spacetime
+control_line_y 0.9 mm
+snapshots macro
+"""
+
+
+def _tiny(tmp_path, text=_TINY_2D):
+    _write_material(np.load(GOLDEN / "run_run2d.npz"), tmp_path / "in625.mat")
+    cfg = tmp_path / "tiny.cfg"
+    cfg.write_text(text)
+    return cfg
+
+
+def test_cli_run_study_and_determinism_on_the_tiny_2d_config(tmp_path):
+    """test_io_cli.py::test_cli_run_writes_outputs, ::test_cli_determinism, ::test_cli_study_tiny
+    and ::test_cli_config_error_exit_code through this package's command line."""
+    import csv
+    from paper_2110_12932_b200.cli import main
+    cfg = _tiny(tmp_path)
+    out = tmp_path / "out"
+    assert main(["run", str(cfg), "--out", str(out)]) == 0
+    assert (out / "errors.csv").exists() and (out / "timing.csv").exists()
+    summary = json.loads((out / "summary.json").read_text())
+    assert summary["mode"] == "two-level-spacetime" and summary["macro_steps"] == 2
+    vtks = sorted((out / "vtk").glob("*.vtk"))
+    assert vtks, "macro snapshots expected"
+    text = vtks[0].read_text()
+    assert "DATASET UNSTRUCTURED_GRID" in text and "SCALARS temperature double" in text
+    o1, o2 = tmp_path / "o1", tmp_path / "o2"
+    assert main(["run", str(cfg), "--out", str(o1), "--snapshots", "none"]) == 0
+    assert main(["run", str(cfg), "--out", str(o2), "--snapshots", "none"]) == 0
+    assert (o1 / "errors.csv").read_text() == (o2 / "errors.csv").read_text()
+    study = tmp_path / "study"
+    assert main(["study", str(cfg), "--out", str(study)]) == 0
+    with (study / "study_matrix.csv").open() as fh:
+        rows = list(csv.reader(fh))
+    assert rows[0] == ["dt_global", "dt_local", "mean_rel_l2"] and len(rows) == 2
+    assert (study / "dt_0.1" / "micro_0.05" / "errors.csv").exists()
+    broken = tmp_path / "broken.cfg"
+    broken.write_text("[domain]\ndimension 7\n")
+    assert main(["run", str(broken), "--out", str(tmp_path / "o")]) == 2
+
+
+def test_cli_entry_point_subprocess_2d(tmp_path):
+    """test_io_cli.py::test_cli_entry_point_subprocess"""
+    import subprocess
+    import sys
+    cfg = _tiny(tmp_path)
+    proc = subprocess.run([sys.executable, "-m", "paper_2110_12932_b200", "run", str(cfg), "--out", str(tmp_path / "o"),
+                           "--snapshots", "none"], capture_output=True, text=True, cwd=str(ROOT), timeout=600)
+    assert proc.returncode == 0, proc.stderr[-2000:]
+    assert "outputs in" in proc.stdout
