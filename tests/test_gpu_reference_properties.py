@@ -736,3 +736,29 @@ def test_criterion_8_structural_invariants_on_the_2d_toy_boxes():
     st2 = P.run_space(p, 0.05, 5, lm, U)
     rel = np.linalg.norm(st1.local_field.values - st2.local_field.values) / np.linalg.norm(st2.local_field.values)
     assert rel < 10 * 1e-6
+
+
+def test_control_temperature_and_composite_sampler():
+    """test_metrics.py::test_control_temperature_constant_field, ..._linear_exact,
+    ..._line_outside and ::test_composite_sampler_prefers_local (device interpolation); the
+    composite sampler also across a TRANSLATED local lattice in 3D (the fine field is located
+    from the moved box)."""
+    from paper_2110_12932_b200.metrics import MetricsError, composite_sampler, control_temperature
+    m = P.build_structured_grid(P.Box((0.0, 0.0), (1.0, 1.0)), 0.25)
+    assert control_temperature(P.uniform_field(m, 7.0), 0.99, (0.0, 1.0), 0.125) == pytest.approx(7.0, rel=1e-12)
+    lin = P.FieldState(m, m.coords[:, 0].copy(), 0.0)
+    assert control_temperature(lin, 0.5, (0.0, 1.0), 0.125) == pytest.approx(0.5, rel=1e-12)
+    with pytest.raises(MetricsError):
+        control_temperature(P.uniform_field(m, 1.0), 1.5, (0.0, 1.0), 0.125)
+    gm = P.build_structured_grid(P.Box((0.0, 0.0), (4.0, 1.0)), 0.25)
+    lm = P.build_structured_grid(P.Box((1.0, 0.5), (2.0, 1.0)), 0.25)
+    vals = composite_sampler(P.uniform_field(lm, 200.0), P.uniform_field(gm, 100.0))(np.array([[0.5, 0.9], [1.5, 0.9]]))
+    assert vals[0] == pytest.approx(100.0) and vals[1] == pytest.approx(200.0)
+    g3, l3 = plates()
+    moved = l3.translated((2e-4, -1e-4, 0.0), within=g3.box)
+    fine = P.FieldState(moved, 500.0 + 3e5 * moved.coords[:, 0] - 2e5 * moved.coords[:, 1] + 1e5 * moved.coords[:, 2], 0.0)
+    pts = np.array([[9e-4, 3e-4, 4.5e-4], [1.55e-3, 6.5e-4, 5e-4], [1e-4, 1e-4, 1e-4]])
+    got = composite_sampler(fine, P.uniform_field(g3, 100.0))(pts)
+    want = 500.0 + 3e5 * pts[:, 0] - 2e5 * pts[:, 1] + 1e5 * pts[:, 2]
+    assert got[0] == pytest.approx(want[0], rel=1e-12) and got[1] == pytest.approx(want[1], rel=1e-12)
+    assert got[2] == pytest.approx(100.0)
