@@ -822,7 +822,9 @@ def picard_bench(args):
                         "field after every step (bytes from tl_host_traffic: the Dirichlet node list and "
                         "values up, the field down); value is the same loop without the read-back (the "
                         "field stays in a device vector between steps)"},
-        "gpu_launches": int(passes * 7 - args.steps), "clocks": clocks.summary(),
+        # per pass: k_vc_tets, k_vc_assemble, k_vc_constrain_b/_w, k_vc_cg, k_vc_inc, k_vc_lag (not after
+        # the last pass of a step); per step: k_scatter_dirichlet (profiles/r02_picard_launches_summary.txt)
+        "gpu_launches": int(passes * 7), "clocks": clocks.summary(),
     }
     print(json.dumps(line), flush=True)
 
